@@ -1,0 +1,190 @@
+/*
+ * sv.h -- C ABI of libsv, the B200 (sm_100a) hot path of Speculative Verification
+ *         (SV, arxiv 2509.24328).
+ *
+ * Citations: "P Lnnn" = PAPER.md line nnn (section / equation named), "S Lnnn" =
+ * SPEC.md line nnn, "R n" = reading n in DESIGN.md §3 (where the paper is silent or
+ * ambiguous).
+ *
+ * Conventions shared by every entry point
+ *  - All array pointers are DEVICE pointers owned by the caller, unless a parameter
+ *    says "host".  The library never allocates, frees or synchronises; every call only
+ *    enqueues kernels on `stream` (a cudaStream_t; NULL = legacy default stream) and is
+ *    therefore CUDA-graph capturable.  No global state; calls are thread-safe.
+ *  - Host-detectable argument errors (NULL pointer, k outside [1, SV_MAX_K], V < 2,
+ *    unsupported dtype, workspace too small, n_lat too short, V too large for the
+ *    on-chip design) return a status != SV_OK and launch nothing.
+ *  - Data errors found on the device (NaN / +inf logit, all -inf row, token outside
+ *    [0, V), p_d(t) = 0, non-finite p_hat, L[n] <= 0, gamma outside [0, k]) never trap:
+ *    they set per-row SV_ROW_* bits in `row_status` (when non-NULL) and write the
+ *    deterministic sentinels documented per call.
+ *  - Logit tensors are row-major with the vocabulary dimension contiguous; element
+ *    strides between sequences (stride_b) and positions (stride_i) are free (0 is a legal
+ *    broadcast).  Rows whose start is 16-byte aligned take the bulk-copy (TMA engine)
+ *    path; others take a slower element-wise path with identical results.
+ *  - Results are bitwise reproducible for identical inputs and independent of B and of
+ *    how a batch is split across GPUs: every reduction tree depends only on (V, dtype),
+ *    and the global sequence id (seq_base + b) enters the Philox counter.
+ */
+#ifndef SV_H_
+#define SV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SV_MAX_K 16 /* draft length limit (paper uses 3..13: P L305, L318, L559) */
+
+typedef enum {
+    SV_OK = 0,
+    SV_ERR_INVALID_ARG = 1,
+    SV_ERR_UNSUPPORTED = 2,
+    SV_ERR_CUDA = 3,
+    SV_ERR_WORKSPACE = 4
+} sv_status;
+
+typedef enum { SV_F32 = 0, SV_BF16 = 1 } sv_dtype;
+
+/* per-row data-error bits (row_status) */
+#define SV_ROW_NAN         1   /* NaN or +inf logit in a row that was read          */
+#define SV_ROW_ALL_NEG_INF 2   /* every logit of a row is -inf (or < -1e30)         */
+#define SV_ROW_BAD_TOKEN   4   /* draft token outside [0, V)                         */
+#define SV_ROW_DRAFT_ZERO  8   /* p_d(t) = 0 (draft logit of t is -inf)              */
+#define SV_ROW_PHAT_BAD    16  /* non-finite p_hat fed to the scheduler (used as 0)  */
+#define SV_ROW_RESID_ZERO  32  /* rejected but residual mass Z = 0: sampled p_t (R10) */
+#define SV_ROW_BAD_GAMMA   64  /* gamma outside [0, k]                               */
+#define SV_ROW_BAD_LATENCY 128 /* a latency entry used by the schedule is <= 0 / NaN */
+
+/* A [B, rows, V] logit tensor: element (b, i, v) is at ptr + b*stride_b + i*stride_i + v
+ * (strides in ELEMENTS).  dtype: sv_dtype. */
+typedef struct {
+    const void *ptr;
+    int32_t dtype;
+    int32_t reserved;
+    int64_t stride_b;
+    int64_t stride_i;
+} sv_logits;
+
+/* Adaptive-binned acceptance profile P(T_i | S, A) (P L176, Table 1 P L200; S L263-268).
+ * n_s bins over S with n_s + 1 ascending edges, n_a bins over A with n_a + 1 edges;
+ * cells[s_bin * n_a + a_bin].  Bins are right-closed (e_j, e_{j+1}] with the first bin
+ * [e_0, e_1]; a value's bin = number of interior edges strictly below it, so values
+ * outside [e_0, e_last] clamp to the boundary bins (R9).  Empty-cell fallbacks
+ * (S L296) must already be filled in.  Device pointers; 1 <= n_s, n_a <= 64. */
+typedef struct {
+    const float *s_edges;
+    int32_t n_s;
+    int32_t n_a;
+    const float *a_edges;
+    const float *cells;
+} sv_profile;
+
+/* Bytes of device workspace needed by sv_score / sv_schedule / sd_verify for this shape
+ * (one buffer may be shared by consecutive calls on one stream). */
+size_t sv_workspace_bytes(int32_t B, int32_t k, int32_t V, int32_t dtype);
+
+/* Human-readable text of a status code (static storage). */
+const char *sv_status_string(int32_t status);
+
+/* CTA-cluster size sv_score / sd_verify use for this (V, dtype); 0 if unsupported. */
+int32_t sv_cluster_size(int32_t V, int32_t dtype);
+
+/*
+ * sv_score -- steps a1-a3: softmax normalisers of the draft and companion rows,
+ * the alignment indicators and the profiled acceptance estimate, per (b, i).
+ *
+ *   p_d = softmax(draft[b,i,:] / tau_d), p_c = softmax(comp[b,i,:] / tau_c)
+ *        (P L159 "token distributions"; temperature P L739-740 Table 5, applied per
+ *         tensor before everything else, R7)
+ *   S  = sum_v min(p_d(v), p_c(v))                 (P L159, §4.2)
+ *   A  = min(1, p_c(t) / p_d(t)),  t = draft_tok[b,i]   (P L159, §4.2; R5)
+ *   KL = sum_v p_d(v) ln(p_d(v) / p_c(v))          (north_star; R6.  TV = 1 - S, P L164)
+ *   p_hat = prof->cells[bin_S(S) * n_a + bin_A(A)]  (P L176; S L293-301; R9)
+ *
+ * draft, comp : [B, k, V] logits (host structs describing device tensors).
+ * draft_tok   : [B, k] int32, contiguous.
+ * prof        : host struct of device pointers.
+ * Outputs [B, k] fp32, contiguous: S, A, KL, p_hat; draft_m = max_v draft[b,i,v] (raw
+ * logit, before temperature), draft_l = sum_v exp((draft[b,i,v] - draft_m) / tau_d),
+ * draft_ptok = p_d(t).  draft_m / draft_l / draft_ptok feed sd_verify.
+ * row_status [B, k] int32 or NULL.  Bad rows: S = A = KL = NaN, p_hat = 0.
+ * S, A, KL, p_hat may be NULL individually (not computed-out); draft_* may not.
+ * Limits: 1 <= k <= 16, 2 <= V, B * k < 2^31, sv_cluster_size(V, dtype) > 0.
+ */
+int32_t sv_score(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok,
+                 int32_t B, int32_t k, int32_t V, float tau_d, float tau_c, const sv_profile *prof,
+                 float *S, float *A, float *KL, float *p_hat, float *draft_m, float *draft_l,
+                 float *draft_ptok, int32_t *row_status, void *workspace, size_t workspace_bytes,
+                 void *stream);
+
+/* sv_schedule modes */
+#define SV_SCHED_PER_ROW 0      /* each sequence maximises its own goodput (P L236-239)  */
+#define SV_SCHED_BATCH_GREEDY 1 /* the paper's batch greedy (P L247-252; S L402-417)     */
+
+/*
+ * sv_schedule -- step a4: verification length per sequence (P L207-239, §5).
+ *
+ *   P_0 = 1, P_j = P_{j-1} * p_hat[b, j-1], E_j = E_{j-1} + P_j   (E(N|gamma), P L231-234;
+ *        identity S L378)
+ *   PER_ROW: g_j = (E_j + plus_one) / L[j + plus_one], j = 0..k, gamma_b = the smallest j
+ *        maximising g_j (exhaustive argmax == the paper's first-decline search whenever the
+ *        latency table is convex, P L239, R4).  fp64, left to right, no FMA contraction, so
+ *        the result is bit-identical to the oracle given the same p_hat.
+ *   BATCH_GREEDY: start from gamma = 0 for all sequences, repeatedly add the candidate
+ *        token with the largest marginal gain P_{gamma_q+1} (ties: lower sequence id) while
+ *        batch goodput (sum_q (E_q + 1)) / L[sum_q (gamma_q + 1)] strictly improves
+ *        (S L405, L421; R16, R17).  plus_one must be 1.
+ *
+ * p_hat [B, k] fp32; latency L[0 .. n_lat-1] fp64 device array indexed by the number of
+ * target positions; PER_ROW needs n_lat >= k + 2, BATCH_GREEDY n_lat >= B*(k+1) + 1.
+ * Outputs: gamma [B] int32 in [0, k]; exp_accept [B] fp32 = E_gamma; goodput [B] fp32 =
+ * g_gamma (BATCH_GREEDY: the batch goodput, same value in every entry).  row_status [B]
+ * (PHAT_BAD, BAD_LATENCY; sentinel gamma = 0) or NULL.  exp_accept / goodput may be NULL.
+ * BATCH_GREEDY requires B <= 4096.
+ */
+int32_t sv_schedule(const float *p_hat, int32_t B, int32_t k, const double *latency, int32_t n_lat,
+                    int32_t mode, int32_t plus_one, int32_t *gamma, float *exp_accept, float *goodput,
+                    int32_t *row_status, void *workspace, size_t workspace_bytes, void *stream);
+
+/*
+ * sd_verify -- steps a5-a6: standard speculative-decoding verification of the first
+ * gamma[b] draft tokens and the correction / bonus sample (P L29 citing Leviathan et al.;
+ * S L148-165; residual S L157-165; inverse CDF S L82-90; R1, R10-R13).
+ *
+ *   p_t = softmax(target[b,i,:] / tau_t) for rows i = 0..gamma_b (rows > gamma_b are
+ *         never read), p_d from draft_m / draft_l (sv_score's outputs)
+ *   for i < gamma_b: accept t_i iff u_{b,i} < p_t(t_i) / p_d(t_i)        (R13)
+ *   N_b = index of the first rejection, else gamma_b
+ *   N_b < gamma_b: sample r = max(0, p_t - p_d) at row N_b; N_b = gamma_b: sample
+ *        r = p_t at row gamma_b (bonus; gamma_b = 0 is plain target sampling)
+ *   token = smallest j with sum_{v<=j} r_v > u_s * Z, Z = sum_v r_v (fp64 sums)     (R11)
+ *   Philox4x32-10, key = (lo(seed), hi(seed)), counter = (i, seq_base + b, lo(offset),
+ *   hi(offset)); word 0 -> u of position i, word 1 -> u_s when N_b = i;
+ *   U24(w) = (w >> 8) * 2^-24 (R12).  Callers advance `offset` every step.
+ *
+ * draft [B, k, V], target [B, k+1, V] logits (host structs of device tensors).
+ * draft_tok [B, k]; gamma [B] int32; draft_m / draft_l / draft_ptok [B, k] fp32 from
+ * sv_score (same draft tensor and tau_d).
+ * Outputs: n_accept [B] int32; out_tok [B] int32 (correction or bonus token);
+ * accept_ratio [B, k] fp32 = min(1, p_t/p_d) for every verified position i < gamma_b
+ * (all those target rows are read anyway), NaN for i >= gamma_b (the paper's X, P L150;
+ * R13); resid_mass [B] fp32 = Z; row_status [B] or NULL.
+ * Bad sequences (NaN/+inf in a row read, bad token, bad gamma, p_d(t) = 0 at a verified
+ * position): n_accept = 0, out_tok = -1, resid_mass = NaN.  accept_ratio / resid_mass may
+ * be NULL.  Same limits as sv_score.
+ */
+int32_t sd_verify(const sv_logits *draft, const sv_logits *target, const int32_t *draft_tok,
+                  const int32_t *gamma, const float *draft_m, const float *draft_l,
+                  const float *draft_ptok, int32_t B, int32_t k, int32_t V, float tau_d, float tau_t,
+                  uint64_t seed, uint64_t offset, int64_t seq_base, int32_t *n_accept, int32_t *out_tok,
+                  float *accept_ratio, float *resid_mass, int32_t *row_status, void *workspace,
+                  size_t workspace_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SV_H_ */

@@ -366,7 +366,9 @@ double oracle_batch_greedy(const double *p_hat, int32_t B, int32_t k, const doub
 /*   all accepted (N = gamma)  -> sample P_t at row gamma (bonus, DESIGN R1)  */
 /*   token = smallest j with sum_{v<=j} r_v > u_s * Z; fallback: last r_j>0. */
 /* D: [B, k, V]; T: [B, k+1, V].  Per-sequence outputs; accept_ratio[b, i] =  */
-/* min(1, P_t/P_d) for i < gamma (the paper's X, P L150), NaN otherwise.      */
+/* min(1, P_t/P_d) for every i < gamma (the paper's X, P L150), NaN otherwise. */
+/* Any data error in a verified row (or the resampled row): status, N = 0,    */
+/* token = -1, Z = NaN.                                                       */
 /* margins (optional, [B, 2]): min |u_i - ratio_i| over the tests performed,  */
 /* and min(|cum_{j*} - theta|, |cum_{j*-1} - theta|) for the sampled token.   */
 /* ------------------------------------------------------------------------ */
@@ -389,6 +391,8 @@ void oracle_verify(const double *D, const double *T, const int32_t *tok, const i
             if (exp_accept_true) exp_accept_true[(int64_t)b * k + i] = NAN;
         }
         if (gamma < 0 || gamma > k) st |= O_ROW_BAD_GAMMA;
+        /* Every verified row i < gamma is scored (its X = min(1, ratio) is reported,
+         * DESIGN R13); the accept chain stops at the first rejection. */
         int32_t N = gamma;
         for (int i = 0; !st && i < gamma; ++i) {
             const double *drow = D + ((int64_t)b * k + i) * V;
@@ -400,13 +404,15 @@ void oracle_verify(const double *D, const double *T, const int32_t *tok, const i
             if (t < 0 || t >= V) { st |= O_ROW_BAD_TOKEN; break; }
             if (pd[t] == 0.0) { st |= O_ROW_DRAFT_ZERO; break; }
             double ratio = pt[t] / pd[t];
-            double u;
-            oracle_uniforms(seed, offset, seq_base + b, i, &u, NULL);
             accept_ratio[(int64_t)b * k + i] = ratio < 1.0 ? ratio : 1.0;
             if (exp_accept_true) exp_accept_true[(int64_t)b * k + i] = oracle_overlap(pd, pt, V);
-            double mg = fabs(u - ratio);
-            if (mg < m_acc) m_acc = mg;
-            if (!(u < ratio)) { N = i; break; }
+            if (N == gamma) {
+                double u;
+                oracle_uniforms(seed, offset, seq_base + b, i, &u, NULL);
+                double mg = fabs(u - ratio);
+                if (mg < m_acc) m_acc = mg;
+                if (!(u < ratio)) N = i;
+            }
         }
         if (st) {
             n_accept[b] = 0;
