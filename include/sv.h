@@ -36,6 +36,12 @@
 extern "C" {
 #endif
 
+#if defined(__GNUC__)
+#define SV_API __attribute__((visibility("default")))
+#else
+#define SV_API
+#endif
+
 #define SV_MAX_K 16 /* draft length limit (paper uses 3..13: P L305, L318, L559) */
 
 typedef enum {
@@ -84,13 +90,13 @@ typedef struct {
 
 /* Bytes of device workspace needed by sv_score / sv_schedule / sd_verify for this shape
  * (one buffer may be shared by consecutive calls on one stream). */
-size_t sv_workspace_bytes(int32_t B, int32_t k, int32_t V, int32_t dtype);
+SV_API size_t sv_workspace_bytes(int32_t B, int32_t k, int32_t V, int32_t dtype);
 
 /* Human-readable text of a status code (static storage). */
-const char *sv_status_string(int32_t status);
+SV_API const char *sv_status_string(int32_t status);
 
 /* CTA-cluster size sv_score / sd_verify use for this (V, dtype); 0 if unsupported. */
-int32_t sv_cluster_size(int32_t V, int32_t dtype);
+SV_API int32_t sv_cluster_size(int32_t V, int32_t dtype);
 
 /*
  * sv_score -- steps a1-a3: softmax normalisers of the draft and companion rows,
@@ -114,7 +120,7 @@ int32_t sv_cluster_size(int32_t V, int32_t dtype);
  * S, A, KL, p_hat may be NULL individually (not computed-out); draft_* may not.
  * Limits: 1 <= k <= 16, 2 <= V, B * k < 2^31, sv_cluster_size(V, dtype) > 0.
  */
-int32_t sv_score(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok,
+SV_API int32_t sv_score(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok,
                  int32_t B, int32_t k, int32_t V, float tau_d, float tau_c, const sv_profile *prof,
                  float *S, float *A, float *KL, float *p_hat, float *draft_m, float *draft_l,
                  float *draft_ptok, int32_t *row_status, void *workspace, size_t workspace_bytes,
@@ -143,9 +149,9 @@ int32_t sv_score(const sv_logits *draft, const sv_logits *comp, const int32_t *d
  * Outputs: gamma [B] int32 in [0, k]; exp_accept [B] fp32 = E_gamma; goodput [B] fp32 =
  * g_gamma (BATCH_GREEDY: the batch goodput, same value in every entry).  row_status [B]
  * (PHAT_BAD, BAD_LATENCY; sentinel gamma = 0) or NULL.  exp_accept / goodput may be NULL.
- * BATCH_GREEDY requires B <= 4096.
+ * BATCH_GREEDY requires B * k <= 8192.
  */
-int32_t sv_schedule(const float *p_hat, int32_t B, int32_t k, const double *latency, int32_t n_lat,
+SV_API int32_t sv_schedule(const float *p_hat, int32_t B, int32_t k, const double *latency, int32_t n_lat,
                     int32_t mode, int32_t plus_one, int32_t *gamma, float *exp_accept, float *goodput,
                     int32_t *row_status, void *workspace, size_t workspace_bytes, void *stream);
 
@@ -176,7 +182,7 @@ int32_t sv_schedule(const float *p_hat, int32_t B, int32_t k, const double *late
  * position): n_accept = 0, out_tok = -1, resid_mass = NaN.  accept_ratio / resid_mass may
  * be NULL.  Same limits as sv_score.
  */
-int32_t sd_verify(const sv_logits *draft, const sv_logits *target, const int32_t *draft_tok,
+SV_API int32_t sd_verify(const sv_logits *draft, const sv_logits *target, const int32_t *draft_tok,
                   const int32_t *gamma, const float *draft_m, const float *draft_l,
                   const float *draft_ptok, int32_t B, int32_t k, int32_t V, float tau_d, float tau_t,
                   uint64_t seed, uint64_t offset, int64_t seq_base, int32_t *n_accept, int32_t *out_tok,

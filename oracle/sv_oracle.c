@@ -419,6 +419,7 @@ void oracle_verify(const double *D, const double *T, const int32_t *tok, const i
             out_tok[b] = -1;
             resid_mass[b] = NAN;
             status[b] = st;
+            for (int i = 0; i < k; ++i) accept_ratio[(int64_t)b * k + i] = NAN;
             if (margins) { margins[2 * b] = NAN; margins[2 * b + 1] = NAN; }
             free(pd); free(pt); free(r);
             continue;
@@ -438,6 +439,7 @@ void oracle_verify(const double *D, const double *T, const int32_t *tok, const i
             if (Z == 0.0) st |= O_ROW_RESID_ZERO; /* DESIGN R10: fall back to P_t */
         }
         if (st & ~O_ROW_RESID_ZERO) {
+            for (int i = 0; i < k; ++i) accept_ratio[(int64_t)b * k + i] = NAN;
             n_accept[b] = 0;
             out_tok[b] = -1;
             resid_mass[b] = NAN;

@@ -1,0 +1,189 @@
+"""paper_2509_24328_b200 -- B200-native hot path of Speculative Verification (arxiv 2509.24328).
+
+Thin torch-facing wrappers with the names of the C ABI (include/sv.h):
+    sv_score    steps a1-a3  (softmax normalisers, S / A / KL, profiled p_hat)   P L159-176
+    sv_schedule step a4      (goodput-maximising verification length)           P L207-252
+    sd_verify   steps a5-a6  (rejection test + residual / bonus sample)          P L29; S L148-165
+and `Pipeline`, which owns preallocated outputs and runs the three calls back to back on
+one stream (optionally captured in a CUDA graph).  PyTorch supplies device memory and
+streams only.  No CPU fallback exists: the compute calls raise without libsv.so / a GPU.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from ._lib import (ROW_ALL_NEG_INF, ROW_BAD_GAMMA, ROW_BAD_LATENCY, ROW_BAD_TOKEN, ROW_DRAFT_ZERO,  # noqa: F401
+                   ROW_NAN, ROW_PHAT_BAD, ROW_RESID_ZERO, SV_SCHED_BATCH_GREEDY, SV_SCHED_PER_ROW, SvError)
+
+__all__ = ["sv_score", "sv_schedule", "sd_verify", "workspace_bytes", "cluster_size", "Profile", "Pipeline",
+           "load_library"]
+
+
+def load_library():
+    return _lib.load()
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return _lib.SV_BF16
+    if t.dtype == torch.float32:
+        return _lib.SV_F32
+    raise SvError(f"unsupported logits dtype {t.dtype}")
+
+
+def _logits(t: torch.Tensor) -> _lib.SvLogits:
+    if not t.is_cuda:
+        raise SvError("logits must be CUDA tensors (no CPU fallback)")
+    if t.dim() != 3 or t.stride(2) != 1:
+        raise SvError("logits must be [B, rows, V] with the vocabulary dimension contiguous")
+    return _lib.SvLogits(t.data_ptr(), _dtype_code(t), 0, t.stride(0), t.stride(1))
+
+
+def _ptr(t) -> int | None:
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise SvError("all tensors passed to libsv must live on the GPU")
+    if not t.is_contiguous():
+        raise SvError("tensor must be contiguous")
+    return t.data_ptr()
+
+
+def _stream(stream) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def workspace_bytes(B: int, k: int, V: int, dtype: torch.dtype) -> int:
+    code = _lib.SV_BF16 if dtype == torch.bfloat16 else _lib.SV_F32
+    return int(_lib.load().sv_workspace_bytes(B, k, V, code))
+
+
+def cluster_size(V: int, dtype: torch.dtype) -> int:
+    code = _lib.SV_BF16 if dtype == torch.bfloat16 else _lib.SV_F32
+    return int(_lib.load().sv_cluster_size(V, code))
+
+
+class Profile:
+    """Device copy of an (S, A) -> p_hat profile (edges + cells, fp32)."""
+
+    def __init__(self, s_edges, a_edges, cells, device="cuda"):
+        self.s_edges = torch.as_tensor(s_edges, dtype=torch.float32, device=device).contiguous()
+        self.a_edges = torch.as_tensor(a_edges, dtype=torch.float32, device=device).contiguous()
+        self.cells = torch.as_tensor(cells, dtype=torch.float32, device=device).reshape(-1).contiguous()
+        self.n_s = self.s_edges.numel() - 1
+        self.n_a = self.a_edges.numel() - 1
+        assert self.cells.numel() == self.n_s * self.n_a
+        self.c = _lib.SvProfile(self.s_edges.data_ptr(), self.n_s, self.n_a, self.a_edges.data_ptr(),
+                                self.cells.data_ptr())
+
+    @classmethod
+    def from_dict(cls, d: dict, device="cuda"):
+        return cls(d["s_edges"], d["a_edges"], d["cells"], device)
+
+
+def sv_score(D, C, tok, tau_d=1.0, tau_c=1.0, profile: Profile | None = None, out=None, stream=None) -> dict:
+    """Steps a1-a3 (P L159, L164, L176) through the C ABI `sv_score`."""
+    B, k, V = D.shape
+    dev = D.device
+    o = out or {}
+    f = lambda name: o.get(name) if name in o else torch.empty((B, k), dtype=torch.float32, device=dev)  # noqa: E731
+    res = {n: f(n) for n in ("S", "A", "KL", "p_hat", "draft_m", "draft_l", "draft_ptok")}
+    res["status"] = o.get("status") if "status" in o else torch.empty((B, k), dtype=torch.int32, device=dev)
+    if profile is None:
+        res["p_hat"] = None
+    st = _lib.load().sv_score(
+        ctypes.byref(_logits(D)), ctypes.byref(_logits(C)), _ptr(tok), B, k, V, float(tau_d), float(tau_c),
+        ctypes.byref(profile.c) if profile is not None else None,
+        _ptr(res["S"]), _ptr(res["A"]), _ptr(res["KL"]), _ptr(res["p_hat"]), _ptr(res["draft_m"]),
+        _ptr(res["draft_l"]), _ptr(res["draft_ptok"]), _ptr(res["status"]), None, 0, _stream(stream))
+    _lib.check(st, "sv_score")
+    return res
+
+
+def sv_schedule(p_hat, latency, mode=SV_SCHED_PER_ROW, plus_one=1, out=None, stream=None) -> dict:
+    """Step a4 (P L207-252) through the C ABI `sv_schedule`; latency is a CUDA fp64 tensor."""
+    B, k = p_hat.shape
+    dev = p_hat.device
+    o = out or {}
+    res = {
+        "gamma": o.get("gamma", None) if "gamma" in o else torch.empty(B, dtype=torch.int32, device=dev),
+        "exp_accept": o.get("exp_accept") if "exp_accept" in o else torch.empty(B, dtype=torch.float32, device=dev),
+        "goodput": o.get("goodput") if "goodput" in o else torch.empty(B, dtype=torch.float32, device=dev),
+        "status": o.get("status") if "status" in o else torch.empty(B, dtype=torch.int32, device=dev),
+    }
+    if latency.dtype != torch.float64:
+        raise SvError("latency table must be float64")
+    st = _lib.load().sv_schedule(_ptr(p_hat), B, k, _ptr(latency), latency.numel(), mode, plus_one,
+                                 _ptr(res["gamma"]), _ptr(res["exp_accept"]), _ptr(res["goodput"]),
+                                 _ptr(res["status"]), None, 0, _stream(stream))
+    _lib.check(st, "sv_schedule")
+    return res
+
+
+def sd_verify(D, T, tok, gamma, draft_m, draft_l, draft_ptok, tau_d=1.0, tau_t=1.0, seed=0, offset=0,
+              seq_base=0, workspace=None, out=None, stream=None) -> dict:
+    """Steps a5-a6 (P L29; S L148-165) through the C ABI `sd_verify`."""
+    B, k, V = D.shape
+    dev = D.device
+    o = out or {}
+    res = {
+        "n_accept": o.get("n_accept") if "n_accept" in o else torch.empty(B, dtype=torch.int32, device=dev),
+        "out_tok": o.get("out_tok") if "out_tok" in o else torch.empty(B, dtype=torch.int32, device=dev),
+        "accept_ratio": o.get("accept_ratio") if "accept_ratio" in o else torch.empty((B, k), dtype=torch.float32,
+                                                                                       device=dev),
+        "resid_mass": o.get("resid_mass") if "resid_mass" in o else torch.empty(B, dtype=torch.float32, device=dev),
+        "status": o.get("status") if "status" in o else torch.empty(B, dtype=torch.int32, device=dev),
+    }
+    nws = workspace_bytes(B, k, V, D.dtype)
+    if workspace is None:
+        workspace = torch.empty(max(nws, 16), dtype=torch.uint8, device=dev)
+    st = _lib.load().sd_verify(
+        ctypes.byref(_logits(D)), ctypes.byref(_logits(T)), _ptr(tok), _ptr(gamma), _ptr(draft_m), _ptr(draft_l),
+        _ptr(draft_ptok), B, k, V, float(tau_d), float(tau_t), ctypes.c_uint64(seed), ctypes.c_uint64(offset),
+        int(seq_base), _ptr(res["n_accept"]), _ptr(res["out_tok"]), _ptr(res["accept_ratio"]), _ptr(res["resid_mass"]),
+        _ptr(res["status"]), workspace.data_ptr(), workspace.numel(), _stream(stream))
+    _lib.check(st, "sd_verify")
+    return res
+
+
+class Pipeline:
+    """sv_score -> sv_schedule -> sd_verify on one stream with preallocated outputs.
+
+    `force_gamma` (int) replaces the schedule by a constant gamma (full SD verification:
+    the fixed-bytes roofline variant of SURVEY §8(d))."""
+
+    def __init__(self, B, k, V, dtype, profile: Profile, latency: torch.Tensor, tau=(1.0, 1.0, 1.0),
+                 mode=SV_SCHED_PER_ROW, device="cuda"):
+        self.B, self.k, self.V, self.dtype = B, k, V, dtype
+        self.profile, self.latency, self.mode = profile, latency, mode
+        self.tau_d, self.tau_c, self.tau_t = tau
+        f32 = dict(dtype=torch.float32, device=device)
+        i32 = dict(dtype=torch.int32, device=device)
+        self.score_out = {n: torch.empty((B, k), **f32) for n in
+                          ("S", "A", "KL", "p_hat", "draft_m", "draft_l", "draft_ptok")}
+        self.score_out["status"] = torch.empty((B, k), **i32)
+        self.sched_out = {"gamma": torch.empty(B, **i32), "exp_accept": torch.empty(B, **f32),
+                          "goodput": torch.empty(B, **f32), "status": torch.empty(B, **i32)}
+        self.ver_out = {"n_accept": torch.empty(B, **i32), "out_tok": torch.empty(B, **i32),
+                        "accept_ratio": torch.empty((B, k), **f32), "resid_mass": torch.empty(B, **f32),
+                        "status": torch.empty(B, **i32)}
+        self.workspace = torch.empty(max(16, workspace_bytes(B, k, V, dtype)), dtype=torch.uint8, device=device)
+        self.forced_gamma = torch.empty(B, **i32)
+        self._forced = None
+
+    def run(self, D, C, T, tok, seed=0, offset=0, seq_base=0, force_gamma=None, stream=None):
+        sc = sv_score(D, C, tok, self.tau_d, self.tau_c, self.profile, out=self.score_out, stream=stream)
+        if force_gamma is None:
+            sh = sv_schedule(sc["p_hat"], self.latency, self.mode, 1, out=self.sched_out, stream=stream)
+            gamma = sh["gamma"]
+        else:
+            if self._forced != int(force_gamma):  # filled once, outside any timed loop
+                self.forced_gamma.fill_(int(force_gamma))
+                self._forced = int(force_gamma)
+            gamma = self.forced_gamma
+        return sd_verify(D, T, tok, gamma, sc["draft_m"], sc["draft_l"], sc["draft_ptok"], self.tau_d, self.tau_t,
+                         seed, offset, seq_base, workspace=self.workspace, out=self.ver_out, stream=stream)

@@ -1,0 +1,229 @@
+// sv_api.cu -- the C ABI of libsv (include/sv.h): argument validation, launch geometry,
+// workspace carving.  Every entry point only enqueues work on the caller's stream.
+#include <stdio.h>
+
+#include "../../include/sv.h"
+#include "sv_internal.h"
+
+namespace sv {
+
+int cluster_size_for(int64_t V, int elem_bytes) {
+  const int64_t pair = 2 * V * elem_bytes;
+  for (int cs = 1; cs <= kMaxCluster; cs <<= 1) {
+    const int64_t chunk = chunk_elems_for(V, cs);
+    if (2 * chunk * elem_bytes <= kChunkPairBudget) return cs;
+  }
+  (void)pair;
+  return 0;
+}
+
+int64_t chunk_elems_for(int64_t V, int cs) {
+  const int64_t c = (V + cs - 1) / cs;
+  return (c + 15) / 16 * 16;
+}
+
+int64_t rows_splits_for(int64_t V, int elem_bytes) {
+  const int64_t per = (int64_t)kRowsThreads * kRowUnitsPerThread * (16 / elem_bytes);
+  return (V + per - 1) / per;
+}
+
+static int64_t rows_chunk_for(int elem_bytes) {
+  return (int64_t)kRowsThreads * kRowUnitsPerThread * (16 / elem_bytes);
+}
+
+}  // namespace sv
+
+using namespace sv;
+
+static bool dtype_ok(int32_t d) { return d == SV_F32 || d == SV_BF16; }
+static int elem_bytes(int32_t d) { return d == SV_BF16 ? 2 : 4; }
+
+static int32_t shape_check(int32_t B, int32_t k, int32_t V, int32_t dtype) {
+  if (B < 0 || k < 1 || k > SV_MAX_K || V < 2) return SV_ERR_INVALID_ARG;
+  if (!dtype_ok(dtype)) return SV_ERR_UNSUPPORTED;
+  if ((int64_t)B * (k + 1) >= (int64_t)1 << 31) return SV_ERR_INVALID_ARG;
+  if (cluster_size_for(V, elem_bytes(dtype)) == 0) return SV_ERR_UNSUPPORTED;
+  return SV_OK;
+}
+
+static int32_t logits_check(const sv_logits *x, int32_t dtype) {
+  if (!x || !x->ptr) return SV_ERR_INVALID_ARG;
+  if (x->dtype != dtype) return SV_ERR_INVALID_ARG;
+  if (x->stride_b < 0 || x->stride_i < 0) return SV_ERR_INVALID_ARG;
+  return SV_OK;
+}
+
+extern "C" {
+
+size_t sv_workspace_bytes(int32_t B, int32_t k, int32_t V, int32_t dtype) {
+  if (shape_check(B, k, V, dtype) != SV_OK) return 0;
+  const int64_t splits = rows_splits_for(V, elem_bytes(dtype));
+  return (size_t)((int64_t)B * (k + 1) * splits * sizeof(float2) + 256);
+}
+
+const char *sv_status_string(int32_t s) {
+  switch (s) {
+    case SV_OK: return "ok";
+    case SV_ERR_INVALID_ARG: return "invalid argument";
+    case SV_ERR_UNSUPPORTED: return "unsupported configuration";
+    case SV_ERR_CUDA: return "CUDA error";
+    case SV_ERR_WORKSPACE: return "workspace too small";
+    default: return "unknown status";
+  }
+}
+
+int32_t sv_cluster_size(int32_t V, int32_t dtype) {
+  if (!dtype_ok(dtype) || V < 2) return 0;
+  return cluster_size_for(V, elem_bytes(dtype));
+}
+
+int32_t sv_score(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok, int32_t B, int32_t k,
+                 int32_t V, float tau_d, float tau_c, const sv_profile *prof, float *S, float *A, float *KL,
+                 float *p_hat, float *draft_m, float *draft_l, float *draft_ptok, int32_t *row_status,
+                 void *workspace, size_t workspace_bytes, void *stream) {
+  (void)workspace;
+  (void)workspace_bytes;
+  if (!draft) return SV_ERR_INVALID_ARG;
+  int32_t r = shape_check(B, k, V, draft->dtype);
+  if (r != SV_OK) return r;
+  if ((r = logits_check(draft, draft->dtype)) != SV_OK || (r = logits_check(comp, draft->dtype)) != SV_OK) return r;
+  if (!draft_tok || !draft_m || !draft_l || !draft_ptok) return SV_ERR_INVALID_ARG;
+  if (!(tau_d > 0.f) || !(tau_c > 0.f)) return SV_ERR_INVALID_ARG;
+  if (p_hat && (!prof || !prof->s_edges || !prof->a_edges || !prof->cells || prof->n_s < 1 || prof->n_a < 1 ||
+                prof->n_s > 64 || prof->n_a > 64))
+    return SV_ERR_INVALID_ARG;
+  if (B == 0) return SV_OK;
+  ScoreArgs a = {};
+  a.d = draft->ptr;
+  a.c = comp->ptr;
+  a.d_sb = draft->stride_b;
+  a.d_si = draft->stride_i;
+  a.c_sb = comp->stride_b;
+  a.c_si = comp->stride_i;
+  a.tok = draft_tok;
+  a.B = B;
+  a.k = k;
+  a.V = V;
+  a.cd = 1.4426950408889634f / tau_d;
+  a.cc = 1.4426950408889634f / tau_c;
+  static const float one_edge[2] = {0.f, 1.f};
+  (void)one_edge;
+  if (p_hat) {
+    a.s_edges = prof->s_edges;
+    a.a_edges = prof->a_edges;
+    a.cells = prof->cells;
+    a.n_s = prof->n_s;
+    a.n_a = prof->n_a;
+  }
+  a.S = S;
+  a.A = A;
+  a.KL = KL;
+  a.p_hat = p_hat;
+  a.dm = draft_m;
+  a.dl = draft_l;
+  a.dpt = draft_ptok;
+  a.status = row_status;
+  a.bf16 = draft->dtype == SV_BF16;
+  a.cs = cluster_size_for(V, elem_bytes(draft->dtype));
+  a.chunk = chunk_elems_for(V, a.cs);
+  cudaError_t e = launch_score(a, (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "libsv: sv_score launch failed: %s\n", cudaGetErrorString(e));
+    return SV_ERR_CUDA;
+  }
+  return SV_OK;
+}
+
+int32_t sv_schedule(const float *p_hat, int32_t B, int32_t k, const double *latency, int32_t n_lat, int32_t mode,
+                    int32_t plus_one, int32_t *gamma, float *exp_accept, float *goodput, int32_t *row_status,
+                    void *workspace, size_t workspace_bytes, void *stream) {
+  (void)workspace;
+  (void)workspace_bytes;
+  if (B < 0 || k < 1 || k > SV_MAX_K) return SV_ERR_INVALID_ARG;
+  if (!p_hat || !latency || !gamma) return SV_ERR_INVALID_ARG;
+  if (mode == SV_SCHED_PER_ROW) {
+    if (n_lat < k + 2) return SV_ERR_INVALID_ARG;
+  } else if (mode == SV_SCHED_BATCH_GREEDY) {
+    if (!plus_one) return SV_ERR_INVALID_ARG;
+    if ((int64_t)B * k > 8192) return SV_ERR_UNSUPPORTED;
+    if ((int64_t)n_lat < (int64_t)B * (k + 1) + 1) return SV_ERR_INVALID_ARG;
+  } else {
+    return SV_ERR_INVALID_ARG;
+  }
+  if (B == 0) return SV_OK;
+  ScheduleArgs a = {};
+  a.p_hat = p_hat;
+  a.B = B;
+  a.k = k;
+  a.L = latency;
+  a.n_lat = n_lat;
+  a.mode = mode;
+  a.plus_one = plus_one ? 1 : 0;
+  a.gamma = gamma;
+  a.exp_accept = exp_accept;
+  a.goodput = goodput;
+  a.status = row_status;
+  cudaError_t e = launch_schedule(a, (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "libsv: sv_schedule launch failed: %s\n", cudaGetErrorString(e));
+    return SV_ERR_CUDA;
+  }
+  return SV_OK;
+}
+
+int32_t sd_verify(const sv_logits *draft, const sv_logits *target, const int32_t *draft_tok, const int32_t *gamma,
+                  const float *draft_m, const float *draft_l, const float *draft_ptok, int32_t B, int32_t k, int32_t V,
+                  float tau_d, float tau_t, uint64_t seed, uint64_t offset, int64_t seq_base, int32_t *n_accept,
+                  int32_t *out_tok, float *accept_ratio, float *resid_mass, int32_t *row_status, void *workspace,
+                  size_t workspace_bytes, void *stream) {
+  if (!draft) return SV_ERR_INVALID_ARG;
+  int32_t r = shape_check(B, k, V, draft->dtype);
+  if (r != SV_OK) return r;
+  if ((r = logits_check(draft, draft->dtype)) != SV_OK || (r = logits_check(target, draft->dtype)) != SV_OK) return r;
+  if (!draft_tok || !gamma || !draft_m || !draft_l || !draft_ptok || !n_accept || !out_tok) return SV_ERR_INVALID_ARG;
+  if (!(tau_d > 0.f) || !(tau_t > 0.f)) return SV_ERR_INVALID_ARG;
+  if (seq_base < 0) return SV_ERR_INVALID_ARG;
+  if (B == 0) return SV_OK;
+  if (!workspace || workspace_bytes < sv_workspace_bytes(B, k, V, draft->dtype)) return SV_ERR_WORKSPACE;
+  if ((reinterpret_cast<uintptr_t>(workspace) & 15) != 0) return SV_ERR_INVALID_ARG;
+  const int eb = elem_bytes(draft->dtype);
+  VerifyArgs a = {};
+  a.d = draft->ptr;
+  a.t = target->ptr;
+  a.d_sb = draft->stride_b;
+  a.d_si = draft->stride_i;
+  a.t_sb = target->stride_b;
+  a.t_si = target->stride_i;
+  a.tok = draft_tok;
+  a.gamma = gamma;
+  a.dm = draft_m;
+  a.dl = draft_l;
+  a.dpt = draft_ptok;
+  a.B = B;
+  a.k = k;
+  a.V = V;
+  a.cd = 1.4426950408889634f / tau_d;
+  a.ct = 1.4426950408889634f / tau_t;
+  a.seed = seed;
+  a.offset = offset;
+  a.seq_base = seq_base;
+  a.n_accept = n_accept;
+  a.out_tok = out_tok;
+  a.ratio = accept_ratio;
+  a.resid = resid_mass;
+  a.status = row_status;
+  a.partials = reinterpret_cast<float2 *>(workspace);
+  a.splits = rows_splits_for(V, eb);
+  a.rows_chunk = rows_chunk_for(eb);
+  a.cs = cluster_size_for(V, eb);
+  a.chunk = chunk_elems_for(V, a.cs);
+  a.bf16 = draft->dtype == SV_BF16;
+  cudaError_t e = launch_verify(a, (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "libsv: sd_verify launch failed: %s\n", cudaGetErrorString(e));
+    return SV_ERR_CUDA;
+  }
+  return SV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,180 @@
+// sv_device.cuh -- device-side helpers of libsv (sm_100a): bulk-copy (TMA engine) +
+// mbarrier staging, MUFU exp2, bf16 unpacking, warp/block reductions, Philox4x32-10.
+// Product code only; shares nothing with oracle/.
+#pragma once
+
+#include <cooperative_groups.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sv {
+
+namespace cg = cooperative_groups;
+
+constexpr float kLog2e = 1.4426950408889634f;
+// Floor for running maxima.  Starting at -1e30 instead of -inf keeps every exponent
+// argument finite: a -inf logit gives ex2(-inf) = 0 and an all -inf row ends with l = 0
+// (flagged SV_ROW_ALL_NEG_INF) instead of producing (-inf) - (-inf) = NaN.
+constexpr float kMFloor = -1.0e30f;
+
+// ---------------------------------------------------------------- math
+__device__ __forceinline__ float ex2(float x) {  // MUFU.EX2, rel. err ~2^-22
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// bf16 pair packed in a 32-bit word -> two floats (exact)
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+template <typename T> struct Elem;
+template <> struct Elem<float> {
+  static constexpr int kPerUnit = 4;  // elements per 16-byte unit
+  __device__ static float load(const float *p) { return *p; }
+  __device__ static void unit(const uint4 &u, float (&x)[4]) {
+    x[0] = __uint_as_float(u.x); x[1] = __uint_as_float(u.y);
+    x[2] = __uint_as_float(u.z); x[3] = __uint_as_float(u.w);
+  }
+};
+template <> struct Elem<__nv_bfloat16> {
+  static constexpr int kPerUnit = 8;
+  __device__ static float load(const __nv_bfloat16 *p) {
+    return __uint_as_float(((uint32_t) * reinterpret_cast<const uint16_t *>(p)) << 16);
+  }
+  __device__ static void unit(const uint4 &u, float (&x)[8]) {
+    x[0] = bf_lo(u.x); x[1] = bf_hi(u.x); x[2] = bf_lo(u.y); x[3] = bf_hi(u.y);
+    x[4] = bf_lo(u.z); x[5] = bf_hi(u.z); x[6] = bf_lo(u.w); x[7] = bf_hi(u.w);
+  }
+};
+
+// ---------------------------------------------------------------- mbarrier + bulk copy
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> this CTA's shared memory, completion counted on `bar`.
+// dst, src 16-byte aligned; bytes a multiple of 16.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// streaming 16-byte global load (read once: do not allocate in L1)
+__device__ __forceinline__ uint4 ldg_stream(const void *p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// ---------------------------------------------------------------- reductions
+// Fixed butterfly order: the result depends only on the lane -> value mapping.
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+// inclusive prefix sum over lanes (Kogge-Stone, fixed order)
+__device__ __forceinline__ double warp_incl_scan_d(double v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    double t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// Block-wide reductions; `scratch` holds >= NT/32 floats.  Warp partials are combined
+// in warp order by every thread, so all threads return the same bits.
+template <int NT>
+__device__ __forceinline__ float block_max(float v, float *scratch) {
+  constexpr int NW = NT / 32;
+  v = warp_max(v);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) scratch[w] = v;
+  __syncthreads();
+  float r = scratch[0];
+#pragma unroll
+  for (int i = 1; i < NW; ++i) r = fmaxf(r, scratch[i]);
+  return r;
+}
+template <int NT, int NV>
+__device__ __forceinline__ void block_sum(float (&v)[NV], float *scratch) {
+  constexpr int NW = NT / 32;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) v[j] = warp_sum(v[j]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) scratch[j * NW + w] = v[j];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    float r = scratch[j * NW];
+#pragma unroll
+    for (int i = 1; i < NW; ++i) r += scratch[j * NW + i];
+    v[j] = r;
+  }
+}
+
+// ---------------------------------------------------------------- Philox4x32-10
+// Salmon et al., SC'11.  counter = (i, global seq, lo(offset), hi(offset)),
+// key = (lo(seed), hi(seed)) (DESIGN R12).
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+__device__ __forceinline__ uint4 sv_philox(uint64_t seed, uint64_t offset, int64_t gseq, int32_t i) {
+  return philox4x32_10(make_uint4((uint32_t)i, (uint32_t)gseq, (uint32_t)offset, (uint32_t)(offset >> 32)),
+                       make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+}
+// U24(w) = (w >> 8) * 2^-24, exact in fp32 and fp64
+__device__ __forceinline__ double u24(uint32_t w) { return (double)(w >> 8) * (1.0 / 16777216.0); }
+
+}  // namespace sv

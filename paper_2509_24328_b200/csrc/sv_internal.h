@@ -1,0 +1,73 @@
+// sv_internal.h -- host-side launch interface between the C ABI (sv_api.cu) and the
+// kernels.  Not installed; the public boundary is include/sv.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sv {
+
+constexpr int kScoreThreads = 256;
+constexpr int kRowsThreads = 256;
+constexpr int kSampleThreads = 256;
+// On-chip budget for the (D, C) [or (T, D)] chunk pair one CTA holds: the cluster size is
+// the smallest power of two that fits a row pair in this budget (a function of V and the
+// dtype only, so reductions are identical for any B and any GPU count).
+constexpr int kChunkPairBudget = 80 * 1024;
+constexpr int kMaxCluster = 16;
+// sd_verify phase-1 chunk: 16 x 16-byte loads in flight per thread.
+constexpr int kRowUnitsPerThread = 16;
+
+int cluster_size_for(int64_t V, int elem_bytes);     // 0 = unsupported
+int64_t chunk_elems_for(int64_t V, int cs);          // per-CTA elements (multiple of 16)
+int64_t rows_splits_for(int64_t V, int elem_bytes);  // sd_verify phase-1 CTAs per row
+
+struct ScoreArgs {
+  const void *d, *c;
+  int64_t d_sb, d_si, c_sb, c_si;
+  const int32_t *tok;
+  int32_t B, k, V;
+  float cd, cc;  // log2(e) / tau
+  const float *s_edges, *a_edges, *cells;
+  int32_t n_s, n_a;
+  float *S, *A, *KL, *p_hat, *dm, *dl, *dpt;
+  int32_t *status;
+  int64_t chunk;  // elements per CTA
+  int cs;         // cluster size
+  int bf16;
+};
+cudaError_t launch_score(const ScoreArgs &a, cudaStream_t st);
+
+struct ScheduleArgs {
+  const float *p_hat;
+  int32_t B, k;
+  const double *L;
+  int32_t n_lat, mode, plus_one;
+  int32_t *gamma;
+  float *exp_accept, *goodput;
+  int32_t *status;
+  void *ws;
+};
+cudaError_t launch_schedule(const ScheduleArgs &a, cudaStream_t st);
+
+struct VerifyArgs {
+  const void *d, *t;
+  int64_t d_sb, d_si, t_sb, t_si;
+  const int32_t *tok, *gamma;
+  const float *dm, *dl, *dpt;
+  int32_t B, k, V;
+  float cd, ct;
+  uint64_t seed, offset;
+  int64_t seq_base;
+  int32_t *n_accept, *out_tok;
+  float *ratio, *resid;
+  int32_t *status;
+  float2 *partials;  // [B, k+1, splits] (max, sum-exp)
+  int64_t splits, rows_chunk;
+  int64_t chunk;  // sampler per-CTA elements
+  int cs;
+  int bf16;
+};
+cudaError_t launch_verify(const VerifyArgs &a, cudaStream_t st);
+
+}  // namespace sv

@@ -1,0 +1,78 @@
+// sv_schedule.cu -- K3: step a4, verification length per sequence (P L207-252, §5).
+//
+// PER_ROW: one thread per sequence walks j = 0..k left to right in fp64 with explicitly
+// rounded operations (__dmul_rn / __dadd_rn / __ddiv_rn: no FMA contraction), so gamma,
+// E and g are bit-identical to the oracle's sequential evaluation (DESIGN R4).
+//   P_j = P_{j-1} p_j, E_j = E_{j-1} + P_j (P L231-234, S L378),
+//   g_j = (E_j + plus_one) / L[j + plus_one]      (P L211, L236; R2),
+//   gamma = smallest argmax_j g_j (strict '>' while scanning; S L396).
+// BATCH_GREEDY (NEXT-1, P L247-252; S L402-417; R16, R17): one CTA.  The greedy order
+// of the paper equals sorting all B*k candidate tokens by (gain desc, seq asc, pos asc)
+// because each sequence's gains P_j are non-increasing in j; the stop rule is evaluated
+// on the sorted prefix sums (fp64, same association as the sequential greedy).
+#include <float.h>
+
+#include "sv_device.cuh"
+#include "sv_internal.h"
+
+namespace sv {
+
+namespace {
+
+__device__ __forceinline__ double phat_at(const float *p, int64_t idx, int &st) {
+  const float v = p[idx];
+  if (!(fabsf(v) <= FLT_MAX)) {  // NaN / inf -> 0 (SV_ROW_PHAT_BAD)
+    st |= 16;
+    return 0.0;
+  }
+  return (double)v;
+}
+
+__global__ void __launch_bounds__(128) sv_schedule_row_kernel(const ScheduleArgs a) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  const int k = a.k, po = a.plus_one ? 1 : 0;
+  int st = 0;
+  for (int j = po; j <= k + po; ++j) {
+    const double l = a.L[j];
+    if (!(l > 0.0) || !(l <= DBL_MAX)) st |= 128;  // SV_ROW_BAD_LATENCY
+  }
+  if (st) {
+    a.gamma[b] = 0;
+    if (a.exp_accept) a.exp_accept[b] = 0.f;
+    if (a.goodput) a.goodput[b] = __int_as_float(0x7fc00000);
+    if (a.status) a.status[b] = st;
+    return;
+  }
+  double P = 1.0, E = 0.0;
+  double best_g = __ddiv_rn(po ? 1.0 : 0.0, a.L[po]);
+  double best_E = 0.0;
+  int best = 0;
+  for (int j = 1; j <= k; ++j) {
+    P = __dmul_rn(P, phat_at(a.p_hat, (int64_t)b * k + (j - 1), st));
+    E = __dadd_rn(E, P);
+    const double g = __ddiv_rn(po ? __dadd_rn(E, 1.0) : E, a.L[j + po]);
+    if (g > best_g) {
+      best_g = g;
+      best_E = E;
+      best = j;
+    }
+  }
+  a.gamma[b] = best;
+  if (a.exp_accept) a.exp_accept[b] = (float)best_E;
+  if (a.goodput) a.goodput[b] = (float)best_g;
+  if (a.status) a.status[b] = st;
+}
+
+}  // namespace
+
+cudaError_t launch_schedule_greedy(const ScheduleArgs &a, cudaStream_t st);  // sv_greedy.cu
+
+cudaError_t launch_schedule(const ScheduleArgs &a, cudaStream_t st) {
+  if (a.mode == 1) return launch_schedule_greedy(a, st);
+  const int nt = 128;
+  sv_schedule_row_kernel<<<(a.B + nt - 1) / nt, nt, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace sv

@@ -1,0 +1,219 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same seeded
+inputs, stage by stage.  Each stage is fed the GPU's own upstream outputs,
+so a logged tie upstream cannot cascade.  All tests need a B200 (-m gpu)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+import sv_helpers as H
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sv():
+    import paper_2509_24328_b200 as sv
+    sv.load_library()
+    return sv
+
+
+@pytest.fixture(scope="module")
+def prof_dict():
+    return synth.load_profile()
+
+
+def run_case(sv, prof_dict, x, tau=(1.0, 1.0, 1.0), seed=0xC0FFEE, offset=3, seq_base=0, gamma=None, report=None):
+    """Full pipeline on GPU + stage-wise oracle comparison; returns (gpu dicts, report)."""
+    rep = report or H.ParityReport()
+    D, C, T, tok = H.to_torch(x)
+    prof = sv.Profile.from_dict(prof_dict)
+    L = torch.tensor(synth.latency_table(x["k"] + 2), dtype=torch.float64, device="cuda")
+    gs = sv.sv_score(D, C, tok, tau[0], tau[1], prof)
+    if gamma is None:
+        gh = sv.sv_schedule(gs["p_hat"], L)
+        gam = gh["gamma"]
+    else:
+        gam = torch.as_tensor(np.asarray(gamma, dtype=np.int32), device="cuda")
+        gh = None
+    gv = sv.sd_verify(D, T, tok, gam, gs["draft_m"], gs["draft_l"], gs["draft_ptok"], tau[0], tau[2],
+                      seed, offset, seq_base)
+    torch.cuda.synchronize()
+    gs, gv = H.gpu_np(gs), H.gpu_np(gv)
+    Dd, Cd, Td = H.oracle_inputs(x)
+    rs = oracle.score(Dd, Cd, x["tok"], tau[0], tau[1], prof_dict)
+    H.compare_score(gs, rs, prof_dict, rep)
+    if gh is not None:
+        gh = H.gpu_np(gh)
+        rh = oracle.schedule(gs["p_hat"].astype(np.float64), synth.latency_table(x["k"] + 2))
+        assert np.array_equal(gh["gamma"], rh["gamma"])  # bit-exact given the same p_hat
+        assert np.array_equal(gh["exp_accept"], rh["exp_accept"].astype(np.float32))
+        assert np.array_equal(gh["goodput"], rh["goodput"].astype(np.float32))
+        gam_np = gh["gamma"]
+    else:
+        gam_np = np.asarray(gamma, dtype=np.int32)
+    rv = oracle.verify(Dd, Td, x["tok"], gam_np, tau[0], tau[2], seed, offset, seq_base)
+    H.compare_verify(gv, rv, rep)
+    return gs, gv, gam_np, rep
+
+
+# ----------------------------------------------------------------- configs
+@pytest.mark.parametrize("B,k,V,dtype", [
+    (4, 4, 32000, "f32"),     # BASELINE config 1
+    (32, 8, 32000, "bf16"),   # BASELINE config 2
+    (6, 5, 32003, "bf16"),    # ragged tail, unaligned rows
+    (5, 3, 1001, "f32"),      # unaligned fp32 rows
+    (3, 16, 4096, "bf16"),    # k = 16
+    (7, 1, 2, "f32"),         # V = 2
+    (5, 2, 13, "bf16"),       # tiny V, odd
+    (2, 8, 152064, "bf16"),   # headline vocabulary
+    (3, 4, 128256, "bf16"),   # sweep vocabulary
+    (2, 2, 70000, "f32"),     # fp32 at cluster 4
+])
+def test_pipeline_parity(sv, prof_dict, B, k, V, dtype):
+    x = synth.make_inputs(B, k, V, dtype, seed=1234 + V + k)
+    *_, rep = run_case(sv, prof_dict, x)
+    print("ties:", rep.ties)
+
+
+def test_temperature(sv, prof_dict):
+    x = synth.make_inputs(8, 5, 5000, "bf16", seed=77, tau_d=0.7)
+    run_case(sv, prof_dict, x, tau=(0.7, 0.6, 0.8))
+
+
+@pytest.mark.parametrize("g", [0, "k", "mixed"])
+def test_forced_gamma(sv, prof_dict, g):
+    x = synth.make_inputs(12, 6, 20000, "bf16", seed=5)
+    gam = {0: np.zeros(12), "k": np.full(12, 6), "mixed": np.arange(12) % 7}[g]
+    run_case(sv, prof_dict, x, gamma=gam)
+
+
+def test_identical_rows_accept_all(sv, prof_dict):
+    # P L159 / north_star: identical distributions -> S = 1, A = 1, KL = 0 and N = gamma
+    x = synth.make_inputs(4, 4, 3000, "bf16", seed=9)
+    x["C"] = x["D"].copy()
+    x["T"][:, :4] = x["D"]
+    gs, gv, gam, _ = run_case(sv, prof_dict, x, gamma=np.full(4, 4))
+    assert np.allclose(gs["S"], 1.0, atol=2e-6) and np.all(gs["A"] == 1.0) and np.all(gs["KL"] == 0.0)
+    assert np.array_equal(gv["n_accept"], gam)
+
+
+def test_disjoint_supports(sv, prof_dict):
+    # disjoint supports -> S = 0, A = 0 (P L159); target disjoint from the draft -> N = 0
+    B, k, V = 3, 2, 64
+    D = np.full((B, k, V), -np.inf, np.float32)
+    C = np.full((B, k, V), -np.inf, np.float32)
+    T = np.full((B, k + 1, V), -np.inf, np.float32)
+    rng = np.random.default_rng(3)
+    D[..., :32] = rng.normal(0, 1, (B, k, 32))
+    C[..., 32:] = rng.normal(0, 1, (B, k, 32))
+    T[..., 32:] = rng.normal(0, 1, (B, k + 1, 32))
+    tok = rng.integers(0, 32, (B, k)).astype(np.int32)
+    x = {"D": D, "C": C, "T": T, "tok": tok, "dtype": "f32", "B": B, "k": k, "V": V}
+    gs, gv, _, _ = run_case(sv, prof_dict, x, gamma=np.full(B, k))
+    assert np.all(gs["S"] == 0) and np.all(gs["A"] == 0) and np.all(np.isinf(gs["KL"]))
+    assert np.all(gv["n_accept"] == 0) and np.all(gv["out_tok"] >= 32)
+
+
+def test_data_errors(sv, prof_dict):
+    x = synth.make_inputs(6, 3, 2048, "f32", seed=11)
+    x["D"][0, 1, 7] = np.nan              # NaN draft logit
+    x["C"][1, 0, :] = -np.inf             # all -inf companion row
+    x["tok"][2, 2] = 5000                 # token out of range
+    x["D"][3, 0, x["tok"][3, 0]] = -np.inf  # p_d(t) = 0
+    x["T"][4, 1, 3] = np.inf              # +inf target logit
+    gs, gv, _, _ = run_case(sv, prof_dict, x, gamma=np.full(6, 3))
+    assert gs["status"][0, 1] & oracle.ROW_NAN and gs["status"][1, 0] & oracle.ROW_ALL_NEG_INF
+    assert gs["status"][2, 2] & oracle.ROW_BAD_TOKEN and gs["status"][3, 0] & oracle.ROW_DRAFT_ZERO
+    assert gv["status"][4] & oracle.ROW_NAN and gv["out_tok"][4] == -1
+
+
+def test_bad_gamma(sv, prof_dict):
+    x = synth.make_inputs(3, 4, 1000, "bf16", seed=12)
+    _, gv, _, _ = run_case(sv, prof_dict, x, gamma=np.array([-1, 5, 2]))
+    assert gv["status"][0] & oracle.ROW_BAD_GAMMA and gv["status"][1] & oracle.ROW_BAD_GAMMA
+    assert gv["status"][2] == 0
+
+
+def test_determinism_and_batch_split(sv, prof_dict):
+    # identical inputs -> identical bits; a sub-batch with seq_base = its first id gives the
+    # same results as the full batch (independent of the GPU count)
+    x = synth.make_inputs(10, 4, 40000, "bf16", seed=21)
+    a = run_case(sv, prof_dict, x)
+    b = run_case(sv, prof_dict, x)
+    for k_ in ("S", "A", "KL", "p_hat", "draft_l"):
+        assert np.array_equal(a[0][k_], b[0][k_], equal_nan=True)
+    for k_ in ("n_accept", "out_tok", "resid_mass"):
+        assert np.array_equal(a[1][k_], b[1][k_], equal_nan=True)
+    sub = {kk: (v[4:10] if isinstance(v, np.ndarray) and v.ndim >= 1 and v.shape[0] == 10 else v)
+           for kk, v in x.items()}
+    sub["B"] = 6
+    c = run_case(sv, prof_dict, sub, seq_base=4)
+    for k_ in ("S", "A", "KL", "p_hat"):
+        assert np.array_equal(a[0][k_][4:], c[0][k_], equal_nan=True)
+    for k_ in ("n_accept", "out_tok", "resid_mass"):
+        assert np.array_equal(a[1][k_][4:], c[1][k_], equal_nan=True)
+
+
+def test_broadcast_losslessness(sv):
+    # S L156, L521: the emitted first token follows P_t (chi^2 / TV < 0.005 over 10^6 trials),
+    # and P(accept) = sum min(p_d, p_t); stride_b = 0 broadcast rows, fresh t ~ p_d per trial
+    rng = np.random.default_rng(31)
+    n, V = 1_000_000, 6
+    for trial in range(3):
+        pd = rng.dirichlet(np.ones(V))
+        pt = rng.dirichlet(np.ones(V))
+        D = torch.tensor(np.log(pd), dtype=torch.float32, device="cuda").view(1, 1, V).expand(n, 1, V)
+        T = torch.tensor(np.log(pt), dtype=torch.float32, device="cuda").view(1, 1, V).expand(n, 2, V)
+        tok = torch.as_tensor(rng.choice(V, size=(n, 1), p=pd).astype(np.int32), device="cuda")
+        gs = sv.sv_score(D, D, tok)
+        gam = torch.ones(n, dtype=torch.int32, device="cuda")
+        gv = sv.sd_verify(D, T, tok, gam, gs["draft_m"], gs["draft_l"], gs["draft_ptok"], seed=trial, offset=0)
+        acc = (gv["n_accept"] == 1).cpu().numpy()
+        emitted = np.where(acc, tok[:, 0].cpu().numpy(), gv["out_tok"].cpu().numpy())
+        freq = np.bincount(emitted, minlength=V) / n
+        assert np.abs(freq - pt).sum() / 2 < 0.005
+        alpha = np.minimum(pd, pt).sum()
+        assert abs(acc.mean() - alpha) < 5 * np.sqrt(alpha * (1 - alpha) / n)
+
+
+def test_batch_greedy_matches_oracle(sv):
+    rng = np.random.default_rng(41)
+    for B, k in [(2, 2), (5, 4), (80, 8), (300, 16)]:
+        ph = rng.random((B, k)).astype(np.float32) ** 0.5
+        L = synth.latency_table(B * (k + 1) + 1, base=4.0 * B, knee=B * 2, slope=1.0)
+        g = sv.sv_schedule(torch.as_tensor(ph, device="cuda"), torch.as_tensor(L, device="cuda"),
+                           mode=sv.SV_SCHED_BATCH_GREEDY)
+        torch.cuda.synchronize()
+        r = oracle.batch_greedy(ph.astype(np.float64), L)
+        assert np.array_equal(g["gamma"].cpu().numpy(), r["gamma"])
+        assert np.array_equal(g["exp_accept"].cpu().numpy(), r["exp_accept"].astype(np.float32))
+    # S L410 hand trace
+    g = sv.sv_schedule(torch.tensor([[0.9, 0.9], [0.8, 0.8]], device="cuda"),
+                       torch.as_tensor(synth.latency_table(10), device="cuda"), mode=sv.SV_SCHED_BATCH_GREEDY)
+    assert g["gamma"].tolist() == [2, 1]
+
+
+def test_headline_full_size_sampled(sv, prof_dict):
+    """BASELINE config 3 at full size in the bench's launch configuration; the oracle checks a
+    sample of sequences one by one (each sequence is independent given seq_base)."""
+    B, k, V = 80, 8, 152064
+    x = synth.make_inputs(B, k, V, "bf16", seed=0x5EED)
+    D, C, T, tok = H.to_torch(x)
+    prof = sv.Profile.from_dict(prof_dict)
+    L = torch.tensor(synth.latency_table(k + 2), dtype=torch.float64, device="cuda")
+    pipe = sv.Pipeline(B, k, V, torch.bfloat16, prof, L)
+    gv = H.gpu_np(pipe.run(D, C, T, tok, seed=0xC0FFEE, offset=1))
+    gs = H.gpu_np(pipe.score_out)
+    gam = pipe.sched_out["gamma"].cpu().numpy()
+    rep = H.ParityReport()
+    for b in (0, 13, 41, 79):
+        sub = {kk: (v[b:b + 1] if isinstance(v, np.ndarray) and v.ndim >= 1 and v.shape[0] == B else v)
+               for kk, v in x.items()}
+        Dd, Cd, Td = H.oracle_inputs(sub)
+        rs = oracle.score(Dd, Cd, sub["tok"], 1.0, 1.0, prof_dict)
+        H.compare_score({kk: v[b:b + 1] for kk, v in gs.items()}, rs, prof_dict, rep)
+        rv = oracle.verify(Dd, Td, sub["tok"], gam[b:b + 1], 1.0, 1.0, 0xC0FFEE, 1, b)
+        H.compare_verify({kk: v[b:b + 1] for kk, v in gv.items()}, rv, rep)
+    print("ties:", rep.ties)
