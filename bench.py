@@ -159,7 +159,7 @@ def cpu_baseline_sample(config):
     Dd, Cd, Td = synth.to_f64(x["D"], dt), synth.to_f64(x["C"], dt), synth.to_f64(x["T"], dt)
     cores = oracle.default_threads()
     reps, t_total = 0, 0.0
-    while t_total < 8.0 and reps < 50:
+    while t_total < 10.0:
         t0 = time.perf_counter()
         rs = oracle.score(Dd, Cd, x["tok"], 1.0, 1.0, prof, nthreads=cores)
         rh = oracle.schedule(rs["p_hat"], L)

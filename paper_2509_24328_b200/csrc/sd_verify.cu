@@ -305,30 +305,41 @@ __global__ void __launch_bounds__(kSampleThreads) sv_sample_kernel(const VerifyA
       tl->zslot[pass] = z;
     }
     cluster.sync();  // chunk masses of this pass visible cluster-wide
-    double Z = 0.0, Pc = 0.0, Zc = 0.0;
-    int owner = -1, last_pos = -1;
-    {
-      // every thread walks the ranks in order (identical bits everywhere)
-      double zr[kMaxCluster];
-      for (int r = 0; r < cs; ++r) zr[r] = cluster.map_shared_rank(tl->zslot, r)[pass];
-      for (int r = 0; r < cs; ++r) Z += zr[r];
-      const double theta = tl->us * Z;
-      double P = 0.0;
+    // warp 0 fetches the chunk masses (lane r <- rank r) and walks them in rank order
+    __shared__ double s_Z, s_Pc, s_Zc;
+    __shared__ int s_owner;
+    if (wid == 0) {
+      const double zr = lane < cs ? cluster.map_shared_rank(tl->zslot, lane)[pass] : 0.0;
+      double Zs = 0.0;
+      for (int r = 0; r < cs; ++r) Zs += __shfl_sync(0xffffffffu, zr, r);
+      const double th = tl->us * Zs;
+      double P = 0.0, Pc_ = 0.0, Zc_ = -1.0;
+      int own = -1, last_pos = -1;
       for (int r = 0; r < cs; ++r) {
-        if (zr[r] > 0.0) last_pos = r;
-        if (owner < 0 && P + zr[r] > theta) {
-          owner = r;
-          Pc = P;
-          Zc = zr[r];
+        const double z = __shfl_sync(0xffffffffu, zr, r);
+        if (z > 0.0) last_pos = r;
+        if (own < 0 && P + z > th) {
+          own = r;
+          Pc_ = P;
+          Zc_ = z;
         }
-        P += zr[r];
+        P += z;
       }
-      if (owner < 0) {  // rounding: no crossing -> last CTA with mass
-        owner = last_pos;
-        Pc = 0.0;
-        Zc = -1.0;
+      if (own < 0) {  // rounding: no crossing -> last CTA with mass
+        own = last_pos;
+        Pc_ = 0.0;
+        Zc_ = -1.0;
+      }
+      if (lane == 0) {
+        s_Z = Zs;
+        s_Pc = Pc_;
+        s_Zc = Zc_;
+        s_owner = own;
       }
     }
+    __syncthreads();
+    const double Z = s_Z, Pc = s_Pc, Zc = s_Zc;
+    const int owner = s_owner;
     if (cx.resid && !(Z > 0.0)) {  // DESIGN R10: residual mass 0 -> sample p_t instead
       st |= 32;
       cluster.sync();  // keep zslot[0] alive until every CTA has read it

@@ -7,7 +7,7 @@
 
 namespace sv {
 
-constexpr int kScoreThreads = 256;
+constexpr int kScoreThreads = 512;
 constexpr int kRowsThreads = 256;
 constexpr int kSampleThreads = 256;
 // On-chip budget for the (D, C) [or (T, D)] chunk pair one CTA holds: the cluster size is
@@ -21,6 +21,8 @@ constexpr int kRowUnitsPerThread = 16;
 int cluster_size_for(int64_t V, int elem_bytes);     // 0 = unsupported
 int64_t chunk_elems_for(int64_t V, int cs);          // per-CTA elements (multiple of 16)
 int64_t rows_splits_for(int64_t V, int elem_bytes);  // sd_verify phase-1 CTAs per row
+// co-resident clusters for a cluster kernel (cached per function / smem / cluster size / device)
+int max_active_clusters(const void *fn, cudaLaunchConfig_t cfg, int smem, int cs);
 
 struct ScoreArgs {
   const void *d, *c;

@@ -49,8 +49,13 @@ def latency_table(n_max: int, base: float = 4.0, knee: int = 2, slope: float = 1
 
 
 def load_profile(path: str = PROFILE_PATH) -> dict:
+    """The (S, A) profile as the fp32 table the C ABI consumes (sv_profile is fp32): edges and
+    cells are rounded to float32 once here, so the oracle and the GPU see identical values."""
     with open(path) as f:
-        return json.load(f)
+        prof = json.load(f)
+    for key in ("s_edges", "a_edges", "cells"):
+        prof[key] = np.asarray(prof[key], dtype=np.float32).astype(np.float64).tolist()
+    return prof
 
 
 def amplitudes(B: int, seed: int, alignment="mix") -> np.ndarray:
