@@ -230,7 +230,8 @@ def run_ours(args, rank, world, local_rank):
             D, C, T, tok = sets[j & 1]
             if ev:
                 ev[j][0].record(stream)
-                sc = sv.sv_score(D, C, tok, pipe.tau_d, pipe.tau_c, prof, out=pipe.score_out, stream=stream)
+                sc = sv.sv_score(D, C, tok, pipe.tau_d, pipe.tau_c, prof, workspace=pipe.workspace,
+                                 out=pipe.score_out, stream=stream)
                 ev[j][1].record(stream)
                 if force is None:
                     gam = sv.sv_schedule(sc["p_hat"], L, out=pipe.sched_out, stream=stream)["gamma"]

@@ -85,9 +85,18 @@ class Profile:
         return cls(d["s_edges"], d["a_edges"], d["cells"], device)
 
 
-def sv_score(D, C, tok, tau_d=1.0, tau_c=1.0, profile: Profile | None = None, out=None, stream=None) -> dict:
+def new_workspace(B: int, k: int, V: int, dtype: torch.dtype, device="cuda") -> torch.Tensor:
+    """Workspace for sv_score / sd_verify: zero-filled once (the library keeps its counters
+    zeroed at the end of every call), reusable across calls on one stream."""
+    return torch.zeros(max(16, workspace_bytes(B, k, V, dtype)), dtype=torch.uint8, device=device)
+
+
+def sv_score(D, C, tok, tau_d=1.0, tau_c=1.0, profile: Profile | None = None, workspace=None, out=None,
+             stream=None) -> dict:
     """Steps a1-a3 (P L159, L164, L176) through the C ABI `sv_score`."""
     B, k, V = D.shape
+    if workspace is None:
+        workspace = new_workspace(B, k, V, D.dtype, D.device)
     dev = D.device
     o = out or {}
     f = lambda name: o.get(name) if name in o else torch.empty((B, k), dtype=torch.float32, device=dev)  # noqa: E731
@@ -99,7 +108,8 @@ def sv_score(D, C, tok, tau_d=1.0, tau_c=1.0, profile: Profile | None = None, ou
         ctypes.byref(_logits(D)), ctypes.byref(_logits(C)), _ptr(tok), B, k, V, float(tau_d), float(tau_c),
         ctypes.byref(profile.c) if profile is not None else None,
         _ptr(res["S"]), _ptr(res["A"]), _ptr(res["KL"]), _ptr(res["p_hat"]), _ptr(res["draft_m"]),
-        _ptr(res["draft_l"]), _ptr(res["draft_ptok"]), _ptr(res["status"]), None, 0, _stream(stream))
+        _ptr(res["draft_l"]), _ptr(res["draft_ptok"]), _ptr(res["status"]), workspace.data_ptr(), workspace.numel(),
+        _stream(stream))
     _lib.check(st, "sv_score")
     return res
 
@@ -138,9 +148,8 @@ def sd_verify(D, T, tok, gamma, draft_m, draft_l, draft_ptok, tau_d=1.0, tau_t=1
         "resid_mass": o.get("resid_mass") if "resid_mass" in o else torch.empty(B, dtype=torch.float32, device=dev),
         "status": o.get("status") if "status" in o else torch.empty(B, dtype=torch.int32, device=dev),
     }
-    nws = workspace_bytes(B, k, V, D.dtype)
     if workspace is None:
-        workspace = torch.empty(max(nws, 16), dtype=torch.uint8, device=dev)
+        workspace = new_workspace(B, k, V, D.dtype, dev)
     st = _lib.load().sd_verify(
         ctypes.byref(_logits(D)), ctypes.byref(_logits(T)), _ptr(tok), _ptr(gamma), _ptr(draft_m), _ptr(draft_l),
         _ptr(draft_ptok), B, k, V, float(tau_d), float(tau_t), ctypes.c_uint64(seed), ctypes.c_uint64(offset),
@@ -171,12 +180,13 @@ class Pipeline:
         self.ver_out = {"n_accept": torch.empty(B, **i32), "out_tok": torch.empty(B, **i32),
                         "accept_ratio": torch.empty((B, k), **f32), "resid_mass": torch.empty(B, **f32),
                         "status": torch.empty(B, **i32)}
-        self.workspace = torch.empty(max(16, workspace_bytes(B, k, V, dtype)), dtype=torch.uint8, device=device)
+        self.workspace = new_workspace(B, k, V, dtype, device)
         self.forced_gamma = torch.empty(B, **i32)
         self._forced = None
 
     def run(self, D, C, T, tok, seed=0, offset=0, seq_base=0, force_gamma=None, stream=None):
-        sc = sv_score(D, C, tok, self.tau_d, self.tau_c, self.profile, out=self.score_out, stream=stream)
+        sc = sv_score(D, C, tok, self.tau_d, self.tau_c, self.profile, workspace=self.workspace, out=self.score_out,
+                      stream=stream)
         if force_gamma is None:
             sh = sv_schedule(sc["p_hat"], self.latency, self.mode, 1, out=self.sched_out, stream=stream)
             gamma = sh["gamma"]

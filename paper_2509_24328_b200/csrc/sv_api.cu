@@ -53,6 +53,32 @@ int max_active_clusters(const void *fn, cudaLaunchConfig_t cfg, int smem, int cs
   return ncl;
 }
 
+int resident_grid(const void *fn, int threads, int smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void *, int, int, int>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(fn, threads, smem, dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int per_sm = 0, sms = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess || per_sm <= 0) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int g = per_sm * (sms > 0 ? sms : 1);
+  cache[key] = g;
+  return g;
+}
+
+static int64_t score_chunk_for(int elem_bytes) { return (int64_t)kScoreThreads * kScoreUnits * (16 / elem_bytes); }
+static int64_t score_nch_for(int64_t V, int elem_bytes) {
+  const int64_t c = score_chunk_for(elem_bytes);
+  return (V + c - 1) / c;
+}
+
 static int64_t rows_chunk_for(int elem_bytes) {
   return (int64_t)kRowsThreads * kRowUnitsPerThread * (16 / elem_bytes);
 }
@@ -63,6 +89,11 @@ using namespace sv;
 
 static bool dtype_ok(int32_t d) { return d == SV_F32 || d == SV_BF16; }
 static int elem_bytes(int32_t d) { return d == SV_BF16 ? 2 : 4; }
+
+// sd_verify's partials follow sv_score's region, so one workspace serves both calls
+static int64_t verify_ws_offset(int32_t B, int32_t k, int32_t V, int eb) {
+  return score_ws_bytes((int64_t)B * k, score_nch_for(V, eb));
+}
 
 static int32_t shape_check(int32_t B, int32_t k, int32_t V, int32_t dtype) {
   if (B < 0 || k < 1 || k > SV_MAX_K || V < 2) return SV_ERR_INVALID_ARG;
@@ -83,8 +114,8 @@ extern "C" {
 
 size_t sv_workspace_bytes(int32_t B, int32_t k, int32_t V, int32_t dtype) {
   if (shape_check(B, k, V, dtype) != SV_OK) return 0;
-  const int64_t splits = rows_splits_for(V, elem_bytes(dtype));
-  return (size_t)((int64_t)B * (k + 1) * splits * sizeof(float2) + 256);
+  const int eb = elem_bytes(dtype);
+  return (size_t)(verify_ws_offset(B, k, V, eb) + ws_round((int64_t)B * (k + 1) * rows_splits_for(V, eb) * 8));
 }
 
 const char *sv_status_string(int32_t s) {
@@ -107,8 +138,6 @@ int32_t sv_score(const sv_logits *draft, const sv_logits *comp, const int32_t *d
                  int32_t V, float tau_d, float tau_c, const sv_profile *prof, float *S, float *A, float *KL,
                  float *p_hat, float *draft_m, float *draft_l, float *draft_ptok, int32_t *row_status,
                  void *workspace, size_t workspace_bytes, void *stream) {
-  (void)workspace;
-  (void)workspace_bytes;
   if (!draft) return SV_ERR_INVALID_ARG;
   int32_t r = shape_check(B, k, V, draft->dtype);
   if (r != SV_OK) return r;
@@ -119,6 +148,8 @@ int32_t sv_score(const sv_logits *draft, const sv_logits *comp, const int32_t *d
                 prof->n_s > 64 || prof->n_a > 64))
     return SV_ERR_INVALID_ARG;
   if (B == 0) return SV_OK;
+  if (!workspace || workspace_bytes < sv_workspace_bytes(B, k, V, draft->dtype)) return SV_ERR_WORKSPACE;
+  if ((reinterpret_cast<uintptr_t>(workspace) & 15) != 0) return SV_ERR_INVALID_ARG;
   ScoreArgs a = {};
   a.d = draft->ptr;
   a.c = comp->ptr;
@@ -132,8 +163,6 @@ int32_t sv_score(const sv_logits *draft, const sv_logits *comp, const int32_t *d
   a.V = V;
   a.cd = 1.4426950408889634f / tau_d;
   a.cc = 1.4426950408889634f / tau_c;
-  static const float one_edge[2] = {0.f, 1.f};
-  (void)one_edge;
   if (p_hat) {
     a.s_edges = prof->s_edges;
     a.a_edges = prof->a_edges;
@@ -150,8 +179,9 @@ int32_t sv_score(const sv_logits *draft, const sv_logits *comp, const int32_t *d
   a.dpt = draft_ptok;
   a.status = row_status;
   a.bf16 = draft->dtype == SV_BF16;
-  a.cs = cluster_size_for(V, elem_bytes(draft->dtype));
-  a.chunk = chunk_elems_for(V, a.cs);
+  a.chunk = score_chunk_for(elem_bytes(draft->dtype));
+  a.nch = (int32_t)score_nch_for(V, elem_bytes(draft->dtype));
+  a.ws = workspace;
   cudaError_t e = launch_score(a, (cudaStream_t)stream);
   if (e != cudaSuccess) {
     fprintf(stderr, "libsv: sv_score launch failed: %s\n", cudaGetErrorString(e));
@@ -238,7 +268,7 @@ int32_t sd_verify(const sv_logits *draft, const sv_logits *target, const int32_t
   a.ratio = accept_ratio;
   a.resid = resid_mass;
   a.status = row_status;
-  a.partials = reinterpret_cast<float2 *>(workspace);
+  a.partials = reinterpret_cast<float2 *>(reinterpret_cast<uint8_t *>(workspace) + verify_ws_offset(B, k, V, eb));
   a.splits = rows_splits_for(V, eb);
   a.rows_chunk = rows_chunk_for(eb);
   a.cs = cluster_size_for(V, eb);

@@ -7,7 +7,12 @@
 
 namespace sv {
 
-constexpr int kScoreThreads = 512;
+constexpr int kScoreThreads = 256;
+// sv_score work item: kScoreUnits 16-byte loads per thread per tensor (16384 bf16 / 8192
+// fp32 logits of the draft row + the same of the companion row)
+constexpr int kScoreUnits = 6;
+// phase 2 of an item runs kScoreLag iterations after its phase 1 (L2 reuse window)
+constexpr int kScoreLag = 2;
 constexpr int kRowsThreads = 256;
 constexpr int kSampleThreads = 256;
 // On-chip budget for the (D, C) [or (T, D)] chunk pair one CTA holds: the cluster size is
@@ -23,6 +28,25 @@ int64_t chunk_elems_for(int64_t V, int cs);          // per-CTA elements (multip
 int64_t rows_splits_for(int64_t V, int elem_bytes);  // sd_verify phase-1 CTAs per row
 // co-resident clusters for a cluster kernel (cached per function / smem / cluster size / device)
 int max_active_clusters(const void *fn, cudaLaunchConfig_t cfg, int smem, int cs);
+// co-resident CTAs of a persistent kernel on this device (cached)
+int resident_grid(const void *fn, int threads, int smem);
+
+// phase-1 partials of one sv_score work item (row, chunk)
+struct ItemPart {
+  double md, ld, mc, lc, w;
+};
+
+// ---- workspace layout (shared by sv_score and sd_verify; byte offsets, 256-aligned)
+//   [score counters: 2 x rows int32, zero at rest] [score item partials] [score S partials]
+//   [verify row partials]
+__host__ __device__ inline int64_t ws_round(int64_t x) { return (x + 255) / 256 * 256; }
+__host__ __device__ inline int64_t score_ws_part_offset(int64_t rows) { return ws_round(2 * rows * 4); }
+__host__ __device__ inline int64_t score_ws_spart_offset(int64_t rows, int64_t nch) {
+  return score_ws_part_offset(rows) + ws_round(rows * nch * (int64_t)sizeof(ItemPart));
+}
+__host__ __device__ inline int64_t score_ws_bytes(int64_t rows, int64_t nch) {
+  return score_ws_spart_offset(rows, nch) + ws_round(rows * nch * 4);
+}
 
 struct ScoreArgs {
   const void *d, *c;
@@ -34,8 +58,9 @@ struct ScoreArgs {
   int32_t n_s, n_a;
   float *S, *A, *KL, *p_hat, *dm, *dl, *dpt;
   int32_t *status;
-  int64_t chunk;  // elements per CTA
-  int cs;         // cluster size
+  int64_t chunk;  // elements per work item (per tensor)
+  int32_t nch;    // chunks per row
+  void *ws;       // workspace (counters zero at rest)
   int bf16;
 };
 cudaError_t launch_score(const ScoreArgs &a, cudaStream_t st);
