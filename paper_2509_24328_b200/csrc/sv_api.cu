@@ -73,7 +73,7 @@ int resident_grid(const void *fn, int threads, int smem) {
   return g;
 }
 
-static int64_t score_chunk_for(int elem_bytes) { return (int64_t)kScoreThreads * kScoreUnits * (16 / elem_bytes); }
+static int64_t score_chunk_for(int elem_bytes) { return (int64_t)kScoreBytes / elem_bytes; }
 static int64_t score_nch_for(int64_t V, int elem_bytes) {
   const int64_t c = score_chunk_for(elem_bytes);
   return (V + c - 1) / c;

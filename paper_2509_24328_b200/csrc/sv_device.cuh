@@ -25,6 +25,37 @@ __device__ __forceinline__ float ex2(float x) {  // MUFU.EX2, rel. err ~2^-22
   return y;
 }
 
+// ---- packed fp32x2 arithmetic (sm_100a FFMA2 / FADD2 / FMUL2: two lanes per instruction)
+struct f2 {
+  float x, y;
+};
+__device__ __forceinline__ uint64_t f2_bits(f2 a) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+  return r;
+}
+__device__ __forceinline__ f2 f2_from(uint64_t b) {
+  f2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)), "l"(f2_bits(c)));
+  return f2_from(r);
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return f2_from(r);
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return f2_from(r);
+}
+__device__ __forceinline__ f2 ex2x2(f2 a) { return f2{ex2(a.x), ex2(a.y)}; }
+
 // bf16 pair packed in a 32-bit word -> two floats (exact)
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
