@@ -1,6 +1,7 @@
 // sv_api.cu -- the C ABI of libsv (include/sv.h): argument validation, launch geometry,
 // workspace carving.  Every entry point only enqueues work on the caller's stream.
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <map>
 #include <mutex>
@@ -11,13 +12,20 @@
 
 namespace sv {
 
+// Tuning knobs, read once from the environment (benchmark experiments only; the defaults are
+// the shipped configuration).  Both are functions of nothing but the process environment, so
+// results stay independent of B and of the GPU count.
+int tune_knob(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
+
 int cluster_size_for(int64_t V, int elem_bytes) {
-  const int64_t pair = 2 * V * elem_bytes;
+  static const int budget = tune_knob("SV_CHUNK_PAIR_KB", kChunkPairBudget / 1024) * 1024;
   for (int cs = 1; cs <= kMaxCluster; cs <<= 1) {
     const int64_t chunk = chunk_elems_for(V, cs);
-    if (2 * chunk * elem_bytes <= kChunkPairBudget) return cs;
+    if (2 * chunk * elem_bytes <= budget) return cs;
   }
-  (void)pair;
   return 0;
 }
 
@@ -73,11 +81,6 @@ int resident_grid(const void *fn, int threads, int smem) {
   return g;
 }
 
-static int64_t score_chunk_for(int elem_bytes) { return (int64_t)kScoreBytes / elem_bytes; }
-static int64_t score_nch_for(int64_t V, int elem_bytes) {
-  const int64_t c = score_chunk_for(elem_bytes);
-  return (V + c - 1) / c;
-}
 
 static int64_t rows_chunk_for(int elem_bytes) {
   return (int64_t)kRowsThreads * kRowUnitsPerThread * (16 / elem_bytes);
@@ -91,9 +94,7 @@ static bool dtype_ok(int32_t d) { return d == SV_F32 || d == SV_BF16; }
 static int elem_bytes(int32_t d) { return d == SV_BF16 ? 2 : 4; }
 
 // sd_verify's partials follow sv_score's region, so one workspace serves both calls
-static int64_t verify_ws_offset(int32_t B, int32_t k, int32_t V, int eb) {
-  return score_ws_bytes((int64_t)B * k, score_nch_for(V, eb));
-}
+static int64_t verify_ws_offset(int32_t, int32_t, int32_t, int) { return 0; }
 
 static int32_t shape_check(int32_t B, int32_t k, int32_t V, int32_t dtype) {
   if (B < 0 || k < 1 || k > SV_MAX_K || V < 2) return SV_ERR_INVALID_ARG;
@@ -147,9 +148,9 @@ int32_t sv_score(const sv_logits *draft, const sv_logits *comp, const int32_t *d
   if (p_hat && (!prof || !prof->s_edges || !prof->a_edges || !prof->cells || prof->n_s < 1 || prof->n_a < 1 ||
                 prof->n_s > 64 || prof->n_a > 64))
     return SV_ERR_INVALID_ARG;
+  (void)workspace;  // sv_score needs no workspace (kept in the ABI for future variants)
+  (void)workspace_bytes;
   if (B == 0) return SV_OK;
-  if (!workspace || workspace_bytes < sv_workspace_bytes(B, k, V, draft->dtype)) return SV_ERR_WORKSPACE;
-  if ((reinterpret_cast<uintptr_t>(workspace) & 15) != 0) return SV_ERR_INVALID_ARG;
   ScoreArgs a = {};
   a.d = draft->ptr;
   a.c = comp->ptr;
@@ -179,9 +180,8 @@ int32_t sv_score(const sv_logits *draft, const sv_logits *comp, const int32_t *d
   a.dpt = draft_ptok;
   a.status = row_status;
   a.bf16 = draft->dtype == SV_BF16;
-  a.chunk = score_chunk_for(elem_bytes(draft->dtype));
-  a.nch = (int32_t)score_nch_for(V, elem_bytes(draft->dtype));
-  a.ws = workspace;
+  a.cs = cluster_size_for(V, elem_bytes(draft->dtype));
+  a.chunk = chunk_elems_for(V, a.cs);
   cudaError_t e = launch_score(a, (cudaStream_t)stream);
   if (e != cudaSuccess) {
     fprintf(stderr, "libsv: sv_score launch failed: %s\n", cudaGetErrorString(e));

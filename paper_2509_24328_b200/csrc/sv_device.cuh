@@ -25,6 +25,20 @@ __device__ __forceinline__ float ex2(float x) {  // MUFU.EX2, rel. err ~2^-22
   return y;
 }
 
+// Short-latency fp64 log2 / exp2 for the per-row epilogues: exact range reduction in fp64, the
+// transcendental of the reduced argument in fp32 (|error| ~1.5e-7 absolute for log2, ~1.2e-7
+// relative for exp2 -- far below the 1e-6 decision tie band), instead of the long dependent
+// DFMA chains of the fp64 library routines.
+__device__ __forceinline__ double log2_acc(double L) {  // L > 0, finite
+  int e;
+  const double m = frexp(L, &e);  // m in [0.5, 1)
+  return (double)e + (double)log2f((float)m);
+}
+__device__ __forceinline__ double exp2_acc(double a) {  // a finite
+  const double n = floor(a);
+  return ldexp((double)exp2f((float)(a - n)), (int)n);
+}
+
 // ---- packed fp32x2 arithmetic (sm_100a FFMA2 / FADD2 / FMUL2: two lanes per instruction)
 struct f2 {
   float x, y;

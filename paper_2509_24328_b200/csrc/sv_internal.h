@@ -23,6 +23,7 @@ constexpr int kMaxCluster = 16;
 constexpr int kRowUnitsPerThread = 16;
 
 int cluster_size_for(int64_t V, int elem_bytes);     // 0 = unsupported
+int tune_knob(const char *name, int dflt);           // integer from the environment (tuning)
 int64_t chunk_elems_for(int64_t V, int cs);          // per-CTA elements (multiple of 16)
 int64_t rows_splits_for(int64_t V, int elem_bytes);  // sd_verify phase-1 CTAs per row
 // co-resident clusters for a cluster kernel (cached per function / smem / cluster size / device)
@@ -65,9 +66,8 @@ struct ScoreArgs {
   int32_t n_s, n_a;
   float *S, *A, *KL, *p_hat, *dm, *dl, *dpt;
   int32_t *status;
-  int64_t chunk;  // elements per work item (per tensor)
-  int32_t nch;    // chunks per row
-  void *ws;       // workspace (counters zero at rest)
+  int64_t chunk;  // elements per CTA (per tensor)
+  int cs;         // cluster size
   int bf16;
 };
 cudaError_t launch_score(const ScoreArgs &a, cudaStream_t st);
