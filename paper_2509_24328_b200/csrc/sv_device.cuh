@@ -34,7 +34,8 @@ __device__ __forceinline__ double log2_acc(double L) {  // L > 0, finite
   const double m = frexp(L, &e);  // m in [0.5, 1)
   return (double)e + (double)log2f((float)m);
 }
-__device__ __forceinline__ double exp2_acc(double a) {  // a finite
+__device__ __forceinline__ double exp2_acc(double a) {  // 2^a; -inf -> 0, +inf / NaN pass through
+  if (!(a > -1100.0) || !(a < 1100.0)) return (a > 0.0 || a != a) ? a + 2048.0 : 0.0;
   const double n = floor(a);
   return ldexp((double)exp2f((float)(a - n)), (int)n);
 }

@@ -7,11 +7,10 @@
 
 namespace sv {
 
-constexpr int kScoreThreads = 256;
-// sv_score work item: kScoreBytes of the draft row + the same of the companion row
-// (8192 bf16 / 4096 fp32 logits each); a CTA keeps kScoreSlots items in a shared-memory ring
-constexpr int kScoreBytes = 16384;
-constexpr int kScoreSlots = 3;
+// sv_score: 15 compute warps + 1 control warp per CTA; kScoreGroup 16-byte loads per tensor
+// per compute thread in flight together (46 KB per CTA)
+constexpr int kScoreThreads = 512;
+constexpr int kScoreGroup = 2;
 constexpr int kRowsThreads = 256;
 constexpr int kSampleThreads = 256;
 // On-chip budget for the (D, C) [or (T, D)] chunk pair one CTA holds: the cluster size is
@@ -31,30 +30,7 @@ int max_active_clusters(const void *fn, cudaLaunchConfig_t cfg, int smem, int cs
 // co-resident CTAs of a persistent kernel on this device (cached)
 int resident_grid(const void *fn, int threads, int smem);
 
-// phase-1 partials of one sv_score work item (row, chunk)
-struct ItemPart {
-  double md, ld, mc, lc, w;
-};
-// merged row state published by the CTA that completes a row's phase 1
-struct RowState {
-  double g[5];  // M_d, L_d, M_c, L_c, W
-  float lam[2]; // Lambda_d, Lambda_c (log2 normalisers)
-};
-
-// ---- workspace layout (shared by sv_score and sd_verify; byte offsets, 256-aligned)
-//   [score counters: 2 x rows int32, zero at rest] [row states] [item partials] [S partials]
-//   [verify row partials]
 __host__ __device__ inline int64_t ws_round(int64_t x) { return (x + 255) / 256 * 256; }
-__host__ __device__ inline int64_t score_ws_row_offset(int64_t rows) { return ws_round(2 * rows * 4); }
-__host__ __device__ inline int64_t score_ws_part_offset(int64_t rows) {
-  return score_ws_row_offset(rows) + ws_round(rows * (int64_t)sizeof(RowState));
-}
-__host__ __device__ inline int64_t score_ws_spart_offset(int64_t rows, int64_t nch) {
-  return score_ws_part_offset(rows) + ws_round(rows * nch * (int64_t)sizeof(ItemPart));
-}
-__host__ __device__ inline int64_t score_ws_bytes(int64_t rows, int64_t nch) {
-  return score_ws_spart_offset(rows, nch) + ws_round(rows * nch * 4);
-}
 
 struct ScoreArgs {
   const void *d, *c;

@@ -1,22 +1,28 @@
 // sv_score.cu -- K1: steps a1-a3 of the SV hot path (P L159 S/A, P L164 divergence,
 // north_star KL, P L176 profile lookup).
 //
-// Design (DESIGN.md §5 K1).  One thread-block CLUSTER of cs CTAs per (b, i): CTA r owns the
-// vocabulary chunk [r*chunk, (r+1)*chunk) of BOTH the draft and the companion row and keeps it in
-// shared memory for the whole kernel, so every logit crosses HBM exactly once.
-//   load    : the chunk pair arrives through the bulk-copy (TMA) engine (one mbarrier)
-//   pass A  : thread maxima on packed bf16x2 (HMNMX2)
-//   pass B  : l = sum 2^{(x - m) log2e / tau} and the KL partial w = sum e_d (a_d - a_c)
-//             (log2 units) with packed fp32x2 FFMA2 / FADD2 -- two logits per instruction
-//   merge   : block merge in fixed warp order, then a cluster barrier and a DSMEM gather of the
-//             cs partials in rank order (identical bits in every CTA) -> Lambda = m c + log2 l
-//   phase 2 : S_r = sum 2^{min(x_d c_d - Lambda_d, x_c c_c - Lambda_c)} over the chunk still
-//             resident in smem (one MUFU per pair), pushed into rank 0's smem
-//   epilogue: rank 0 (one warp, fp64): S, A = min(1, p_c(t)/p_d(t)), KL, profile lookup,
-//             draft normalisers for sd_verify.
-// The cluster size is the smallest power of two that fits the (draft, companion) row pair in
-// the on-chip budget, a function of (V, dtype) only, so every reduction order -- and therefore
-// every output bit -- is independent of B and of how a batch is split across GPUs.
+// Design (DESIGN.md §5 K1): a PERSISTENT, warp-specialised, cluster-pipelined kernel.
+//  * A cluster of cs CTAs owns rows (b, i) = cid, cid + ncl, ...; CTA r of the cluster owns the
+//    vocabulary chunk [r*chunk, (r+1)*chunk) of the draft AND the companion row.
+//  * 15 compute warps per CTA; the 16th (highest id, favoured by the warp arbiter) is a control
+//    warp that runs every latency-bound step: DSMEM pushes, mbarrier waits, merges, epilogue.
+//  * Iteration j overlaps three rows of the cluster:
+//      pass 1 (row j, compute warps): stream the chunk pair from HBM (16-byte loads, L2
+//        evict_last), thread maxima, l = sum 2^{(x - m) log2e / tau}, KL partial
+//        w = sum e_d (a_d - a_c) with packed FFMA2 / FADD2; block merge -> 5 partials, which the
+//        control warp pushes into every CTA of the cluster (DSMEM + remote mbarrier arrive);
+//      pass 2 (row j - 1, compute warps): the control warp has merged row j - 1's partials in
+//        rank order (identical bits in every CTA) into Lambda = m c + log2 l while pass 1 ran;
+//        re-read the chunk pair -- an L2 hit, it was streamed one iteration ago -- and sum
+//        S_r = sum 2^{min(x_d c_d - Lambda_d, x_c c_c - Lambda_c)}; push S_r to the row's
+//        epilogue CTA;
+//      epilogue (row j - 2, control warp of CTA (j - 2) % cs): S, A, KL, profile lookup, draft
+//        normalisers for sd_verify.
+//    Slots are double-buffered with full / empty mbarriers, so no cluster-wide barrier is
+//    needed in steady state and every exchange latency hides under the other warps' streaming.
+//  * HBM traffic is one read of D and C; the second read is served by L2 (~15 TB/s measured).
+// The cluster size and chunking depend on (V, dtype) only, so every reduction order -- and
+// therefore every output bit -- is independent of B, of the grid size and of the GPU count.
 #include <float.h>
 
 #include "sv_device.cuh"
@@ -26,138 +32,303 @@ namespace sv {
 
 namespace {
 
-template <int NT>
-struct ScoreTail {
-  uint64_t bar;
-  double part[kMaxCluster][5];  // (M_d, L_d, M_c, L_c, W) of every rank, pushed by the ranks
-  double glob[5];           // merged values
-  float lam[2];             // Lambda_d, Lambda_c
-  float sarr[kMaxCluster];  // S partials (valid in rank 0)
-  float fscr[2 * (NT / 32)];
-  double dscr[3 * (NT / 32)];
+constexpr int NT = kScoreThreads, NW = NT / 32, NCW = NW - 1;  // NCW compute warps
+constexpr int NC = NCW * 32;                                    // compute threads
+constexpr int G = kScoreGroup;                                  // units per thread per group
+
+// named barriers (id 0 is __syncthreads)
+// P1Done alternates between two ids: the compute warps may run one pass 1 ahead of the
+// control warp's matching sync, never two (the LamReady / P2Done chain bounds them).
+enum : int { kBarCompute = 1, kBarP1Done = 2, kBarLamReady = 3, kBarP2Done = 4, kBarP1DoneOdd = 5 };
+__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+struct Smem {
+  uint64_t full_p[2], empty_p[2], full_s[2], empty_s[2];
+  double part[2][kMaxCluster][5];  // (M_d, L_d, M_c, L_c, W) pushed by every rank, per slot
+  float sarr[2][kMaxCluster];      // S partials pushed to the epilogue CTA, per slot
+  double glob[2][5];               // merged (M_d, L_d, M_c, L_c, W), per slot
+  float lam[2][2];                 // Lambda_d, Lambda_c, per slot
+  double mine[2][6];               // this CTA's pass-1 partial, per row parity ([4] unused)
+  float s_mine;                    // this CTA's pass-2 partial
+  float fscr[2 * NCW];
+  float fscr2[NCW];
+  double dscr[3 * NCW];
 };
 
-__device__ __forceinline__ void cluster_arrive() {
-  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+__device__ __forceinline__ uint32_t remote(const void *p, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
 }
-__device__ __forceinline__ void cluster_wait() {
-  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+__device__ __forceinline__ void remote_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void st_remote_f64(uint32_t addr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_remote_f32(uint32_t addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void wait_cluster(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "W_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra W_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// ---------------------------------------------------------------- pass B arithmetic
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint4 ldg_hint(const void *p, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+
+// ---------------------------------------------------------------- element arithmetic
 struct P1 {
   f2 ld, lc;  // l_d, l_c partials, two lanes each
   f2 w;       // KL partial, two lanes
 };
 
+template <bool kGuard>
 __device__ __forceinline__ void p1_pair(f2 xd, f2 xc, f2 cdd, f2 ccc, f2 nmdd, f2 nmcc, P1 &acc) {
   const f2 ad = fma2(xd, cdd, nmdd), ac = fma2(xc, ccc, nmcc);
   const f2 ed = ex2x2(ad), ec = ex2x2(ac);
   acc.ld = add2(acc.ld, ed);
   acc.lc = add2(acc.lc, ec);
-  acc.w = fma2(ed, sub2(ad, ac), acc.w);
-}
-
-template <typename T>
-__device__ __forceinline__ void p1_unit(const uint4 &ud, const uint4 &uc, f2 cdd, f2 ccc, f2 nmdd, f2 nmcc,
-                                        P1 &acc) {
-  if constexpr (sizeof(T) == 2) {  // 8 bf16: lane pairs (x_2j, x_2j+1) share an FFMA2
-    const uint32_t wd[4] = {ud.x, ud.y, ud.z, ud.w}, wc[4] = {uc.x, uc.y, uc.z, uc.w};
-#pragma unroll
-    for (int p = 0; p < 4; ++p)
-      p1_pair(f2{bf_lo(wd[p]), bf_hi(wd[p])}, f2{bf_lo(wc[p]), bf_hi(wc[p])}, cdd, ccc, nmdd, nmcc, acc);
+  if (kGuard) {  // p_d = 0 terms contribute 0 even against a_c = -inf
+    acc.w.x += ed.x > 0.f ? ed.x * (ad.x - ac.x) : 0.f;
+    acc.w.y += ed.y > 0.f ? ed.y * (ad.y - ac.y) : 0.f;
   } else {
-    p1_pair(f2{__uint_as_float(ud.x), __uint_as_float(ud.y)}, f2{__uint_as_float(uc.x), __uint_as_float(uc.y)}, cdd,
-            ccc, nmdd, nmcc, acc);
-    p1_pair(f2{__uint_as_float(ud.z), __uint_as_float(ud.w)}, f2{__uint_as_float(uc.z), __uint_as_float(uc.w)}, cdd,
-            ccc, nmdd, nmcc, acc);
+    acc.w = fma2(ed, sub2(ad, ac), acc.w);
   }
 }
 
-// element-wise (ragged tail / unaligned rows / guarded redo): p_d = 0 terms add 0 to w
-__device__ __forceinline__ void p1_one(float xd, float xc, float cd, float cc, float nmd, float nmc, P1 &acc) {
-  const float ad = fmaf(xd, cd, nmd), ac = fmaf(xc, cc, nmc);
-  const float ed = ex2(ad);
-  acc.ld.x += ed;
-  acc.lc.x += ex2(ac);
-  acc.w.x += ed > 0.f ? ed * (ad - ac) : 0.f;
-}
-
-__device__ __forceinline__ void umax(__nv_bfloat162 &m, const uint4 &v) {
-  const __nv_bfloat162 *p = reinterpret_cast<const __nv_bfloat162 *>(&v);
-  m = __hmax2(__hmax2(m, p[0]), __hmax2(p[1], __hmax2(p[2], p[3])));
-}
-
-// phase-2 arithmetic on one 16-byte unit of each tensor
 template <typename T>
-__device__ __forceinline__ void p2_unit(const uint4 &ud, const uint4 &uc, f2 cdd, f2 ccc, f2 lamdd, f2 lamcc,
-                                        f2 &acc) {
-  auto pair = [&](f2 xd, f2 xc) {
-    const f2 ad = fma2(xd, cdd, lamdd), ac = fma2(xc, ccc, lamcc);
-    acc = add2(acc, f2{ex2(fminf(ad.x, ac.x)), ex2(fminf(ad.y, ac.y))});
-  };
+__device__ __forceinline__ void unit_pairs(const uint4 &u, f2 (&x)[Elem<T>::kPerUnit / 2]) {
   if constexpr (sizeof(T) == 2) {
-    const uint32_t wd[4] = {ud.x, ud.y, ud.z, ud.w}, wc[4] = {uc.x, uc.y, uc.z, uc.w};
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-    for (int p = 0; p < 4; ++p) pair(f2{bf_lo(wd[p]), bf_hi(wd[p])}, f2{bf_lo(wc[p]), bf_hi(wc[p])});
+    for (int p = 0; p < 4; ++p) x[p] = f2{bf_lo(w[p]), bf_hi(w[p])};
   } else {
-    pair(f2{__uint_as_float(ud.x), __uint_as_float(ud.y)}, f2{__uint_as_float(uc.x), __uint_as_float(uc.y)});
-    pair(f2{__uint_as_float(ud.z), __uint_as_float(ud.w)}, f2{__uint_as_float(uc.z), __uint_as_float(uc.w)});
+    x[0] = f2{__uint_as_float(u.x), __uint_as_float(u.y)};
+    x[1] = f2{__uint_as_float(u.z), __uint_as_float(u.w)};
   }
 }
 
-// Values the epilogue needs from global memory, loaded by rank 0's warp 0 at kernel start so
-// their latency hides under the streaming phases.
-struct EpiPre {
-  int32_t t;
-  float xdt, xct;       // draft / companion logit of the draft token (lanes 0 / 1)
-  float se[2], ae[2];   // interior profile edges j = lane + 1 and lane + 33 (+inf past the end)
-};
-
+__device__ __forceinline__ float unit_max_bf16(const uint4 &v) {
+  const __nv_bfloat162 *p = reinterpret_cast<const __nv_bfloat162 *>(&v);
+  const __nv_bfloat162 m = __hmax2(__hmax2(p[0], p[1]), __hmax2(p[2], p[3]));
+  return fmaxf(__low2float(m), __high2float(m));
+}
 template <typename T>
-__device__ __forceinline__ EpiPre epi_prefetch(const ScoreArgs &a, int64_t row) {
-  const int lane = threadIdx.x & 31;
-  const int64_t b = row / a.k, i = row % a.k;
-  EpiPre p;
-  p.t = a.tok[row];
-  p.xdt = p.xct = 0.f;
-  const bool tok_ok = p.t >= 0 && p.t < a.V;
-  if (lane == 0 && tok_ok) p.xdt = Elem<T>::load(reinterpret_cast<const T *>(a.d) + b * a.d_sb + i * a.d_si + p.t);
-  if (lane == 1 && tok_ok) p.xct = Elem<T>::load(reinterpret_cast<const T *>(a.c) + b * a.c_sb + i * a.c_si + p.t);
-  const float inf = __int_as_float(0x7f800000);
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int j = lane + 1 + 32 * h;
-    p.se[h] = (a.p_hat && j < a.n_s) ? a.s_edges[j] : inf;
-    p.ae[h] = (a.p_hat && j < a.n_a) ? a.a_edges[j] : inf;
+__device__ __forceinline__ float unit_max(const uint4 &v) {
+  if constexpr (sizeof(T) == 2) {
+    return unit_max_bf16(v);
+  } else {
+    return fmaxf(fmaxf(__uint_as_float(v.x), __uint_as_float(v.y)), fmaxf(__uint_as_float(v.z), __uint_as_float(v.w)));
   }
-  return p;
 }
 
-// Epilogue of one row (warp 0 of rank 0; independent pieces on separate lanes, fp64 range
-// reduction + fp32 transcendentals).  The draft-side outputs depend on the draft row alone: a bad
-// companion row does not poison them.
-template <int NT>
-__device__ __noinline__ void epilogue(const ScoreArgs &a, int64_t row, const ScoreTail<NT> *tl, int cs,
-                                      const EpiPre &pre) {
+// Where this CTA's chunk of a row lives.
+template <typename T>
+struct Chunk {
+  const T *d, *c;
+  int n;      // elements
+  int units;  // 16-byte units (0 when the chunk pair is not 16-byte aligned)
+};
+template <typename T>
+__device__ __forceinline__ Chunk<T> chunk_of(const ScoreArgs &a, int64_t row, int rank) {
+  const int64_t b = row / a.k, i = row % a.k, v0 = (int64_t)rank * a.chunk;
+  Chunk<T> ch;
+  ch.d = reinterpret_cast<const T *>(a.d) + b * a.d_sb + i * a.d_si + v0;
+  ch.c = reinterpret_cast<const T *>(a.c) + b * a.c_sb + i * a.c_si + v0;
+  ch.n = (int)max((int64_t)0, min(a.chunk, (int64_t)a.V - v0));
+  const bool al = ((reinterpret_cast<uintptr_t>(ch.d) | reinterpret_cast<uintptr_t>(ch.c)) & 15) == 0;
+  ch.units = al ? ch.n / Elem<T>::kPerUnit : 0;
+  return ch;
+}
+
+// Pass 1 of one chunk by the compute warps: thread maxima and sums, processed in groups of G
+// units per thread (all loads of a group in flight together) with an exact online merge
+// between groups.  Returns the thread's (m_d, m_c, l_d, l_c, w).
+template <typename T, bool kGuard>
+__device__ __forceinline__ void pass1_thread(const Chunk<T> &ch, float cd, float cc, uint64_t pol, float &md,
+                                             float &mc, float &lf_d, float &lf_c, float &wf) {
+  constexpr int EPU = Elem<T>::kPerUnit;
+  const int tid = threadIdx.x;
+  md = kMFloor;
+  mc = kMFloor;
+  lf_d = lf_c = wf = 0.f;
+  for (int u0 = 0; u0 < ch.units; u0 += G * NC) {
+    uint4 rd[G], rc[G];
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      const int u = u0 + tid + q * NC;
+      if (u < ch.units) {
+        rd[q] = ldg_hint(ch.d + (size_t)u * EPU, pol);
+        rc[q] = ldg_hint(ch.c + (size_t)u * EPU, pol);
+      }
+    }
+    float gmd = md, gmc = mc;
+#pragma unroll
+    for (int q = 0; q < G; ++q)
+      if (u0 + tid + q * NC < ch.units) {
+        gmd = fmaxf(gmd, unit_max<T>(rd[q]));
+        gmc = fmaxf(gmc, unit_max<T>(rc[q]));
+      }
+    if (gmd > md || gmc > mc) {  // exact online rescale of the running sums
+      const float sdf = ex2((md - gmd) * cd), scf = ex2((mc - gmc) * cc);
+      const float delta = (gmc - mc) * cc - (gmd - md) * cd;
+      if (lf_d > 0.f) wf = fmaf(lf_d, delta, wf);
+      wf *= sdf;
+      lf_d *= sdf;
+      lf_c *= scf;
+      md = gmd;
+      mc = gmc;
+    }
+    const float nmd = -md * cd, nmc = -mc * cc;
+    const f2 cdd{cd, cd}, ccc{cc, cc}, nmdd{nmd, nmd}, nmcc{nmc, nmc};
+    P1 acc{{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+#pragma unroll
+    for (int q = 0; q < G; ++q)
+      if (u0 + tid + q * NC < ch.units) {
+        f2 xd[EPU / 2], xc[EPU / 2];
+        unit_pairs<T>(rd[q], xd);
+        unit_pairs<T>(rc[q], xc);
+#pragma unroll
+        for (int p = 0; p < EPU / 2; ++p) p1_pair<kGuard>(xd[p], xc[p], cdd, ccc, nmdd, nmcc, acc);
+      }
+    lf_d += acc.ld.x + acc.ld.y;
+    lf_c += acc.lc.x + acc.lc.y;
+    wf += acc.w.x + acc.w.y;
+  }
+  // element-wise remainder (ragged tail, or the whole chunk when unaligned)
+  const int e0 = ch.units * EPU;
+  float tmd = md, tmc = mc;
+  for (int e = e0 + tid; e < ch.n; e += NC) {
+    tmd = fmaxf(tmd, Elem<T>::load(ch.d + e));
+    tmc = fmaxf(tmc, Elem<T>::load(ch.c + e));
+  }
+  if (tmd > md || tmc > mc) {
+    const float sdf = ex2((md - tmd) * cd), scf = ex2((mc - tmc) * cc);
+    const float delta = (tmc - mc) * cc - (tmd - md) * cd;
+    if (lf_d > 0.f) wf = fmaf(lf_d, delta, wf);
+    wf *= sdf;
+    lf_d *= sdf;
+    lf_c *= scf;
+    md = tmd;
+    mc = tmc;
+  }
+  const float nmd = -md * cd, nmc = -mc * cc;
+  for (int e = e0 + tid; e < ch.n; e += NC) {
+    const float xd = Elem<T>::load(ch.d + e), xc = Elem<T>::load(ch.c + e);
+    const float ad = fmaf(xd, cd, nmd), ac = fmaf(xc, cc, nmc);
+    const float ed = ex2(ad);
+    lf_d += ed;
+    lf_c += ex2(ac);
+    wf += ed > 0.f ? ed * (ad - ac) : 0.f;
+  }
+}
+
+// Pass 2 of one chunk by the compute warps (L2 re-read): the thread's S partial.
+template <typename T>
+__device__ __forceinline__ float pass2_thread(const Chunk<T> &ch, float cd, float cc, float lamd, float lamc,
+                                              uint64_t pol) {
+  constexpr int EPU = Elem<T>::kPerUnit;
+  const int tid = threadIdx.x;
+  const f2 cdd{cd, cd}, ccc{cc, cc}, ld2{-lamd, -lamd}, lc2{-lamc, -lamc};
+  f2 acc{0.f, 0.f};
+  for (int u0 = 0; u0 < ch.units; u0 += G * NC) {
+    uint4 rd[G], rc[G];
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      const int u = u0 + tid + q * NC;
+      if (u < ch.units) {
+        rd[q] = ldg_hint(ch.d + (size_t)u * EPU, pol);
+        rc[q] = ldg_hint(ch.c + (size_t)u * EPU, pol);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < G; ++q)
+      if (u0 + tid + q * NC < ch.units) {
+        f2 xd[EPU / 2], xc[EPU / 2];
+        unit_pairs<T>(rd[q], xd);
+        unit_pairs<T>(rc[q], xc);
+#pragma unroll
+        for (int p = 0; p < EPU / 2; ++p) {
+          const f2 ad = fma2(xd[p], cdd, ld2), ac = fma2(xc[p], ccc, lc2);
+          acc = add2(acc, f2{ex2(fminf(ad.x, ac.x)), ex2(fminf(ad.y, ac.y))});
+        }
+      }
+  }
+  for (int e = ch.units * EPU + tid; e < ch.n; e += NC)
+    acc.x += ex2(fminf(fmaf(Elem<T>::load(ch.d + e), cd, -lamd), fmaf(Elem<T>::load(ch.c + e), cc, -lamc)));
+  return acc.x + acc.y;
+}
+
+// Epilogue of one row (control warp of its epilogue CTA; independent pieces on separate lanes,
+// fp64 range reduction + fp32 transcendentals).  The draft-side outputs depend on the draft row
+// alone: a bad companion row does not poison them.
+template <typename T>
+__device__ __noinline__ void epilogue(const ScoreArgs &a, int64_t row, const double *glob, const float *sarr,
+                                      int cs) {
   const int lane = threadIdx.x & 31;
   const float cd = a.cd, cc = a.cc;
-  const float GMd = (float)tl->glob[0], GMc = (float)tl->glob[2];
-  const double L_d = tl->glob[1], L_c = tl->glob[3], W = tl->glob[4];
+  const float GMd = (float)glob[0], GMc = (float)glob[2];
+  const double L_d = glob[1], L_c = glob[3], W = glob[4];
   auto row_bits = [](double L, float M) {
     if (!(L == L) || !(L < 1e300) || !(M < FLT_MAX)) return 1; /*SV_ROW_NAN*/
     return (L > 0.0) ? 0 : 2;                                  /*SV_ROW_ALL_NEG_INF*/
   };
   const int d_st = row_bits(L_d, GMd), c_st = row_bits(L_c, GMc);
-  const bool tok_ok = pre.t >= 0 && pre.t < a.V;
+  const int64_t b = row / a.k, i = row % a.k;
+  const int32_t t = a.tok[row];
+  const bool tok_ok = t >= 0 && t < a.V;
   int st = d_st | c_st | (tok_ok ? 0 : 4 /*SV_ROW_BAD_TOKEN*/);
+  // profile edges j = lane + 1, lane + 33 (+inf past the end) -- loads issued early
+  const float inf = __int_as_float(0x7f800000);
+  float se[2], ae[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int j = lane + 1 + 32 * h;
+    se[h] = (a.p_hat && j < a.n_s) ? a.s_edges[j] : inf;
+    ae[h] = (a.p_hat && j < a.n_a) ? a.a_edges[j] : inf;
+  }
   // lane 0: log2 p_d(t); lane 1: log2 p_c(t); lane 2: log2 L_d - log2 L_c; lane 3: S (rank order)
   double piece = 0.0;
-  if (lane == 0 && !d_st && tok_ok) piece = (double)pre.xdt * cd - (double)(GMd * cd) - log2_acc(L_d);
-  if (lane == 1 && !st) piece = (double)pre.xct * cc - (double)(GMc * cc) - log2_acc(L_c);
+  if (lane == 0 && !d_st && tok_ok) {
+    const float x = Elem<T>::load(reinterpret_cast<const T *>(a.d) + b * a.d_sb + i * a.d_si + t);
+    piece = (double)x * cd - (double)(GMd * cd) - log2_acc(L_d);
+  }
+  if (lane == 1 && !st) {
+    const float x = Elem<T>::load(reinterpret_cast<const T *>(a.c) + b * a.c_sb + i * a.c_si + t);
+    piece = (double)x * cc - (double)(GMc * cc) - log2_acc(L_c);
+  }
   if (lane == 2 && !st) piece = log2_acc(L_d) - log2_acc(L_c);
   if (lane == 3)
-    for (int r = 0; r < cs; ++r) piece += (double)tl->sarr[r];
+    for (int r = 0; r < cs; ++r) piece += (double)sarr[r];
   const double argd = __shfl_sync(0xffffffffu, piece, 0);
   double piece2 = 0.0;  // lane 0: p_d(t); lane 1: p_c(t) / p_d(t)
   if (lane == 0 && !d_st && tok_ok) piece2 = exp2_acc(argd);
@@ -176,7 +347,7 @@ __device__ __noinline__ void epilogue(const ScoreArgs &a, int64_t row, const Sco
   float phat = 0.f;
   if (!st && a.p_hat) {  // bin = number of interior edges strictly below the value (R9)
     const float Sf = (float)S, Af = (float)A;
-    int si = (pre.se[0] < Sf) + (pre.se[1] < Sf), ai = (pre.ae[0] < Af) + (pre.ae[1] < Af);
+    int si = (se[0] < Sf) + (se[1] < Sf), ai = (ae[0] < Af) + (ae[1] < Af);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       si += __shfl_xor_sync(0xffffffffu, si, o);
@@ -197,270 +368,192 @@ __device__ __noinline__ void epilogue(const ScoreArgs &a, int64_t row, const Sco
   }
 }
 
-#ifdef SV_TRACE
-__device__ unsigned long long *g_trace = nullptr;  // debug builds only: [cta][8] timestamps
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#define TR(k) \
-  if (trp && threadIdx.x == blockDim.x - 32) trp[(size_t)blockIdx.x * 12 + (k)] = gtime();
-#else
-#define TR(k)
-#endif
-
-template <typename T, int NT>
-__global__ void __launch_bounds__(NT, 1024 / NT) sv_score_kernel(const ScoreArgs a) {
-#ifdef SV_TRACE
-  unsigned long long *const trp = g_trace;  // loaded once
-#endif
-  TR(0);
-  cluster_arrive();  // (0) this CTA has started: peers may write its shared memory after wait (0)
-  EpiPre pre{};
-  constexpr int NW = NT / 32, EPU = Elem<T>::kPerUnit;
+template <typename T>
+__global__ void __launch_bounds__(kScoreThreads, 2) sv_score_kernel(const ScoreArgs a) {
+  __shared__ Smem sm;
   cg::cluster_group cluster = cg::this_cluster();
   const int cs = a.cs;
   const int rank = (int)cluster.block_rank();
-  const int64_t row = blockIdx.x / cs;
-  const int64_t b = row / a.k, i = row % a.k;
-  const int64_t v0 = (int64_t)rank * a.chunk;
-  const int n = (int)max((int64_t)0, min(a.chunk, (int64_t)a.V - v0));
+  const int64_t cid = blockIdx.x / cs, ncl = gridDim.x / cs;
+  const int64_t rows = (int64_t)a.B * a.k;
+  const int64_t nrows = rows > cid ? (rows - cid + ncl - 1) / ncl : 0;  // rows of this cluster
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  // Serial per-CTA work (bulk-copy issue, merges, epilogue) runs on the LAST warp: the warp
-  // arbiter favours high warp ids, so the critical path is not starved by co-resident compute.
-  const bool ctl = wid == NW - 1;
+  const bool ctl = wid == NCW;
   const float cd = a.cd, cc = a.cc;
+  auto row_of = [&](int64_t j) { return cid + j * ncl; };
 
-  extern __shared__ __align__(128) uint8_t smem[];
-  const size_t cbytes = (size_t)a.chunk * sizeof(T);
-  T *sd = reinterpret_cast<T *>(smem);
-  T *sc = reinterpret_cast<T *>(smem + cbytes);
-  ScoreTail<NT> *tl = reinterpret_cast<ScoreTail<NT> *>(smem + 2 * cbytes);
-
-  const T *gd = reinterpret_cast<const T *>(a.d) + b * a.d_sb + i * a.d_si + v0;
-  const T *gc = reinterpret_cast<const T *>(a.c) + b * a.c_sb + i * a.c_si + v0;
-  const bool al = ((reinterpret_cast<uintptr_t>(gd) | reinterpret_cast<uintptr_t>(gc)) & 15) == 0;
-  if (rank == 0 && ctl) pre = epi_prefetch<T>(a, row);
-  const int units = al ? n / EPU : 0;  // 16-byte units moved by the bulk-copy engine
-  const int e0 = units * EPU;          // elements [e0, n) are handled element-wise
-
-  if (ctl && lane == 0) {
-    mbar_init(&tl->bar, 1);
+  if (tid == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&sm.full_p[s], cs);
+      mbar_init(&sm.empty_p[s], cs);
+      mbar_init(&sm.full_s[s], cs);
+      mbar_init(&sm.empty_s[s], 1);
+    }
     fence_mbar_init();
-    if (units > 0) {
-      const uint32_t bytes = (uint32_t)units * 16u;
-      mbar_arrive_expect_tx(&tl->bar, 2u * bytes);
-      const uint32_t half = (bytes / 2) / 16 * 16;  // two pieces per tensor
-      bulk_g2s(sd, gd, half, &tl->bar);
-      bulk_g2s(sc, gc, half, &tl->bar);
-      if (bytes > half) {
-        bulk_g2s(reinterpret_cast<uint8_t *>(sd) + half, reinterpret_cast<const uint8_t *>(gd) + half, bytes - half,
-                 &tl->bar);
-        bulk_g2s(reinterpret_cast<uint8_t *>(sc) + half, reinterpret_cast<const uint8_t *>(gc) + half, bytes - half,
-                 &tl->bar);
+  }
+  cluster_sync_all();  // every barrier of the cluster is initialised before any remote arrive
+
+  if (!ctl) {
+    // ================================================================ compute warps
+    const uint64_t pol_keep = l2_policy_evict_last(), pol_last = l2_policy_evict_first();
+    for (int64_t j = 0; j <= nrows; ++j) {
+      if (j < nrows) {  // ---- pass 1 of row j
+        const Chunk<T> ch = chunk_of<T>(a, row_of(j), rank);
+        float md, mc, lf_d, lf_c, wf;
+        pass1_thread<T, false>(ch, cd, cc, pol_keep, md, mc, lf_d, lf_c, wf);
+        if (wf != wf && lf_d == lf_d && lf_c == lf_c)  // 0 * (-inf) from masked logits: guarded redo
+          pass1_thread<T, true>(ch, cd, cc, pol_keep, md, mc, lf_d, lf_c, wf);
+        // block merge over the compute warps (fixed warp / lane order)
+        float Md = warp_max(md), Mc = warp_max(mc);
+        if (lane == 0) {
+          sm.fscr[wid] = Md;
+          sm.fscr[NCW + wid] = Mc;
+        }
+        bar_sync(kBarCompute, NC);
+        Md = sm.fscr[0];
+        Mc = sm.fscr[NCW];
+#pragma unroll
+        for (int q = 1; q < NCW; ++q) {
+          Md = fmaxf(Md, sm.fscr[q]);
+          Mc = fmaxf(Mc, sm.fscr[NCW + q]);
+        }
+        const float sdf = ex2((md - Md) * cd), scf = ex2((mc - Mc) * cc);
+        const float delta = (Mc - mc) * cc - (Md - md) * cd;
+        double ww = wf;
+        if (lf_d > 0.f) ww += (double)lf_d * (double)delta;
+        double v[3] = {(double)lf_d * sdf, (double)lf_c * scf, ww * sdf};
+#pragma unroll
+        for (int k = 0; k < 3; ++k) v[k] = warp_sum_d(v[k]);
+        if (lane == 0)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) sm.dscr[k * NCW + wid] = v[k];
+        bar_sync(kBarCompute, NC);
+        double *mine = sm.mine[j & 1];
+        if (tid < 3) {
+          double r = 0.0;
+          for (int q = 0; q < NCW; ++q) r += sm.dscr[tid * NCW + q];
+          mine[1 + 2 * tid] = r;  // tid 0 -> L_d [1], 1 -> L_c [3], 2 -> W [5]
+        }
+        if (tid == 0) {
+          mine[0] = Md;
+          mine[2] = Mc;
+        }
+        bar_arrive((j & 1) ? kBarP1DoneOdd : kBarP1Done, NT);  // control warp may push the partial
+      }
+      if (j >= 1) {  // ---- pass 2 of row j - 1
+        const int s = (int)((j - 1) & 1);
+        bar_sync(kBarLamReady, NT);  // control warp merged row j - 1
+        const float lamd = sm.lam[s][0], lamc = sm.lam[s][1];
+        float sl = 0.f;
+        if (lamd == lamd && lamc == lamc) {  // bad rows skip the S sweep
+          const Chunk<T> ch = chunk_of<T>(a, row_of(j - 1), rank);
+          sl = pass2_thread<T>(ch, cd, cc, lamd, lamc, pol_last);
+        }
+        sl = warp_sum(sl);
+        if (lane == 0) sm.fscr2[wid] = sl;
+        bar_sync(kBarCompute, NC);
+        if (tid == 0) {
+          float r = sm.fscr2[0];
+          for (int q = 1; q < NCW; ++q) r += sm.fscr2[q];
+          sm.s_mine = r;
+        }
+        bar_arrive(kBarP2Done, NT);
       }
     }
-  }
-  for (int e = e0 + tid; e < n; e += NT) {  // ragged tail / unaligned rows
-    sd[e] = gd[e];
-    sc[e] = gc[e];
-  }
-  __syncthreads();
-  if (units > 0) mbar_wait(&tl->bar, 0);
-  TR(1);
-
-  // ---- pass A: thread maxima
-  float md = kMFloor, mc = kMFloor;
-  if constexpr (sizeof(T) == 2) {
-    __nv_bfloat162 pd = __halves2bfloat162(__ushort_as_bfloat16(0xFF80), __ushort_as_bfloat16(0xFF80));
-    __nv_bfloat162 pc = pd;
-#pragma unroll 4
-    for (int u = tid; u < units; u += NT) {
-      umax(pd, reinterpret_cast<const uint4 *>(sd)[u]);
-      umax(pc, reinterpret_cast<const uint4 *>(sc)[u]);
-    }
-    md = fmaxf(md, fmaxf(__low2float(pd), __high2float(pd)));
-    mc = fmaxf(mc, fmaxf(__low2float(pc), __high2float(pc)));
   } else {
-#pragma unroll 4
-    for (int u = tid; u < units; u += NT) {
-      const float4 xd = reinterpret_cast<const float4 *>(sd)[u], xc = reinterpret_cast<const float4 *>(sc)[u];
-      md = fmaxf(md, fmaxf(fmaxf(xd.x, xd.y), fmaxf(xd.z, xd.w)));
-      mc = fmaxf(mc, fmaxf(fmaxf(xc.x, xc.y), fmaxf(xc.z, xc.w)));
-    }
-  }
-  for (int e = e0 + tid; e < n; e += NT) {
-    md = fmaxf(md, Elem<T>::load(sd + e));
-    mc = fmaxf(mc, Elem<T>::load(sc + e));
-  }
-  // ---- pass B: sums against the thread maxima
-  const float nmd = -md * cd, nmc = -mc * cc;
-  P1 acc{{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
-  {
-    const f2 cdd{cd, cd}, ccc{cc, cc}, nmdd{nmd, nmd}, nmcc{nmc, nmc};
-#pragma unroll 2
-    for (int u = tid; u < units; u += NT)
-      p1_unit<T>(reinterpret_cast<const uint4 *>(sd)[u], reinterpret_cast<const uint4 *>(sc)[u], cdd, ccc, nmdd, nmcc,
-                 acc);
-  }
-  for (int e = e0 + tid; e < n; e += NT) p1_one(Elem<T>::load(sd + e), Elem<T>::load(sc + e), cd, cc, nmd, nmc, acc);
-  float lf_d = acc.ld.x + acc.ld.y, lf_c = acc.lc.x + acc.lc.y, wf = acc.w.x + acc.w.y;
-  if (wf != wf && lf_d == lf_d && lf_c == lf_c) {  // 0 * (-inf) from masked logits: guarded redo
-    P1 g{{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};      // (same elements per thread as the fast path)
-    for (int u = tid; u < units; u += NT)
-      for (int j = 0; j < EPU; ++j)
-        p1_one(Elem<T>::load(sd + u * EPU + j), Elem<T>::load(sc + u * EPU + j), cd, cc, nmd, nmc, g);
-    for (int e = e0 + tid; e < n; e += NT) p1_one(Elem<T>::load(sd + e), Elem<T>::load(sc + e), cd, cc, nmd, nmc, g);
-    lf_d = g.ld.x;
-    lf_c = g.lc.x;
-    wf = g.w.x;
-  }
-
-  TR(2);
-  cluster_wait();  // (0) every peer CTA has started (completes at once by now): DSMEM pushes are safe
-  // ---- block merge (fixed warp / lane order)
-  {
-    float Md = warp_max(md), Mc = warp_max(mc);
-    if (lane == 0) {
-      tl->fscr[wid] = Md;
-      tl->fscr[NW + wid] = Mc;
-    }
-    __syncthreads();
-    Md = tl->fscr[0];
-    Mc = tl->fscr[NW];
+    // ================================================================ control warp
+    for (int64_t j = 0; j <= nrows + 1; ++j) {
+      // (1) merge row j - 1's partials (pushed during the peers' iteration j - 1) while the
+      //     compute warps run pass 1 of row j
+      if (j >= 1 && j - 1 < nrows) {
+        const int s = (int)((j - 1) & 1);
+        wait_cluster(&sm.full_p[s], (uint32_t)(((j - 1) >> 1) & 1));
+        double pr[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        pr[0] = pr[2] = kMFloor;
+        if (lane < cs)
 #pragma unroll
-    for (int q = 1; q < NW; ++q) {
-      Md = fmaxf(Md, tl->fscr[q]);
-      Mc = fmaxf(Mc, tl->fscr[NW + q]);
-    }
-    const float sdf = ex2((md - Md) * cd), scf = ex2((mc - Mc) * cc);
-    const float delta = (Mc - mc) * cc - (Md - md) * cd;
-    double ww = wf;
-    if (lf_d > 0.f) ww += (double)lf_d * (double)delta;
-    double v[3] = {(double)lf_d * sdf, (double)lf_c * scf, ww * sdf};
+          for (int k = 0; k < 5; ++k) pr[k] = sm.part[s][lane][k];
+        __syncwarp();
+        if (lane < cs) remote_arrive(remote(&sm.empty_p[s], lane));  // slot s of every peer is free
+        const float rmd = (float)pr[0], rmc = (float)pr[2];
+        const float GMd = warp_max(rmd), GMc = warp_max(rmc);
+        const float sdf = ex2((rmd - GMd) * cd), scf = ex2((rmc - GMc) * cc);
+        const float delta = (GMc - rmc) * cc - (GMd - rmd) * cd;
+        double ww = pr[4];
+        if (pr[1] > 0.0) ww += pr[1] * (double)delta;
+        const double cl_d = pr[1] * sdf, cl_c = pr[3] * scf, cw = ww * sdf;
+        double L_d = 0.0, L_c = 0.0, W = 0.0;
+        for (int r = 0; r < cs; ++r) {  // rank order
+          L_d += __shfl_sync(0xffffffffu, cl_d, r);
+          L_c += __shfl_sync(0xffffffffu, cl_c, r);
+          W += __shfl_sync(0xffffffffu, cw, r);
+        }
+        if (lane == 0) {
+          sm.glob[s][0] = GMd;
+          sm.glob[s][1] = L_d;
+          sm.glob[s][2] = GMc;
+          sm.glob[s][3] = L_c;
+          sm.glob[s][4] = W;
+          const bool ok = L_d > 0.0 && L_c > 0.0 && L_d < 1e300 && L_c < 1e300 && GMd < FLT_MAX && GMc < FLT_MAX;
+          sm.lam[s][0] = ok ? (float)((double)GMd * cd + log2_acc(L_d)) : __int_as_float(0x7fc00000);
+          sm.lam[s][1] = ok ? (float)((double)GMc * cc + log2_acc(L_c)) : __int_as_float(0x7fc00000);
+        }
+        __syncwarp();
+        bar_arrive(kBarLamReady, NT);
+      }
+      // (2) push this CTA's pass-1 partial of row j into slot j % 2 of every peer
+      if (j < nrows) {
+        const int s = (int)(j & 1);
+        bar_sync((j & 1) ? kBarP1DoneOdd : kBarP1Done, NT);
+        if (j >= 2) wait_cluster(&sm.empty_p[s], (uint32_t)(((j >> 1) - 1) & 1));
+        if (lane < cs) {
+          const double *mine = sm.mine[j & 1];
+          const double v[5] = {mine[0], mine[1], mine[2], mine[3], mine[5]};
 #pragma unroll
-    for (int j = 0; j < 3; ++j) v[j] = warp_sum_d(v[j]);
-    if (lane == 0)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) tl->dscr[j * NW + wid] = v[j];
-    __syncthreads();
-    if (ctl) {  // control warp: lanes 0..2 sum the 3 quantities over warps (in warp order)
-      double r = 0.0;
-      if (lane < 3)
-        for (int q = 0; q < NW; ++q) r += tl->dscr[lane * NW + q];
-      const double r1 = __shfl_sync(0xffffffffu, r, 1), r2 = __shfl_sync(0xffffffffu, r, 2);
-      const double r0 = __shfl_sync(0xffffffffu, r, 0);
-      if (lane < cs) {  // push this CTA's partial into slot [rank] of every CTA of the cluster
-        double *dst = cluster.map_shared_rank(&tl->part[rank][0], lane);
-        dst[0] = Md;
-        dst[1] = r0;
-        dst[2] = Mc;
-        dst[3] = r1;
-        dst[4] = r2;
+          for (int k = 0; k < 5; ++k) st_remote_f64(remote(&sm.part[s][rank][k], lane), v[k]);
+          remote_arrive(remote(&sm.full_p[s], lane));
+        }
+      }
+      // (3) push this CTA's S partial of row j - 1 to the row's epilogue CTA
+      if (j >= 1 && j - 1 < nrows) {
+        const int s = (int)((j - 1) & 1);
+        const int epi = (int)((j - 1) % cs);
+        bar_sync(kBarP2Done, NT);
+        if (j - 1 >= 2) wait_cluster(&sm.empty_s[s], (uint32_t)((((j - 1) >> 1) - 1) & 1));
+        if (lane == 0) {
+          st_remote_f32(remote(&sm.sarr[s][rank], epi), sm.s_mine);
+          remote_arrive(remote(&sm.full_s[s], epi));
+        }
+        __syncwarp();
+      }
+      // (4) epilogue of row j - 2 (its S partials were pushed during iteration j - 1)
+      if (j >= 2 && j - 2 < nrows && (int)((j - 2) % cs) == rank) {
+        const int s = (int)((j - 2) & 1);
+        // this CTA's full_s[s] completes once per row r with r % 2 == s and r % cs == rank: the
+        // completion index of row r is r / lcm(2, cs)
+        const int64_t lcm2 = cs == 1 ? 2 : cs;
+        wait_cluster(&sm.full_s[s], (uint32_t)(((j - 2) / lcm2) & 1));
+        epilogue<T>(a, row_of(j - 2), sm.glob[s], sm.sarr[s], cs);
+        __syncwarp();
+        if (lane < cs) remote_arrive(remote(&sm.empty_s[s], lane));  // slot s free for row j
       }
     }
   }
-  TR(3);
-  cluster_arrive();  // (A) partials of this CTA published
-  cluster_wait();
-  TR(4);
-
-  // ---- cluster merge in rank order (identical in every CTA): lane r of warp 0 fetches rank r's
-  // partial through DSMEM in one round trip; shuffles combine them in rank order
-  if (ctl) {
-    double pr[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    pr[0] = pr[2] = kMFloor;
-    if (lane < cs) {
-#pragma unroll
-      for (int j = 0; j < 5; ++j) pr[j] = tl->part[lane][j];  // local: pushed before barrier (A)
-    }
-    const float rmd = (float)pr[0], rmc = (float)pr[2];
-    const float GMd = warp_max(rmd), GMc = warp_max(rmc);
-    TR(8);
-    const float sdf = ex2((rmd - GMd) * cd), scf = ex2((rmc - GMc) * cc);
-    const float delta = (GMc - rmc) * cc - (GMd - rmd) * cd;
-    double ww = pr[4];
-    if (pr[1] > 0.0) ww += pr[1] * (double)delta;
-    const double cl_d = pr[1] * sdf, cl_c = pr[3] * scf, cw = ww * sdf;
-    double L_d = 0.0, L_c = 0.0, W = 0.0;
-    for (int r = 0; r < cs; ++r) {  // rank order
-      L_d += __shfl_sync(0xffffffffu, cl_d, r);
-      L_c += __shfl_sync(0xffffffffu, cl_c, r);
-      W += __shfl_sync(0xffffffffu, cw, r);
-    }
-    TR(9);
-    if (lane == 0) {
-      tl->glob[0] = GMd;
-      tl->glob[1] = L_d;
-      tl->glob[2] = GMc;
-      tl->glob[3] = L_c;
-      tl->glob[4] = W;
-      const bool ok = L_d > 0.0 && L_c > 0.0 && L_d < 1e300 && L_c < 1e300 && GMd < FLT_MAX && GMc < FLT_MAX;
-      tl->lam[0] = ok ? (float)((double)GMd * cd + log2_acc(L_d)) : __int_as_float(0x7fc00000);
-      tl->lam[1] = ok ? (float)((double)GMc * cc + log2_acc(L_c)) : __int_as_float(0x7fc00000);
-    }
-    TR(10);
-  }
-  __syncthreads();
-
-  TR(5);
-  // ---- phase 2: S partial over the chunk still resident in smem (bad rows skip it)
-  const float lamd = tl->lam[0], lamc = tl->lam[1];
-  float s_loc = 0.f;
-  if (lamd == lamd && lamc == lamc) {
-    const f2 cdd{cd, cd}, ccc{cc, cc}, ld2{-lamd, -lamd}, lc2{-lamc, -lamc};
-    f2 acc2{0.f, 0.f};
-#pragma unroll 2
-    for (int u = tid; u < units; u += NT)
-      p2_unit<T>(reinterpret_cast<const uint4 *>(sd)[u], reinterpret_cast<const uint4 *>(sc)[u], cdd, ccc, ld2, lc2,
-                 acc2);
-    for (int e = e0 + tid; e < n; e += NT)
-      acc2.x += ex2(fminf(fmaf(Elem<T>::load(sd + e), cd, -lamd), fmaf(Elem<T>::load(sc + e), cc, -lamc)));
-    s_loc = acc2.x + acc2.y;
-  }
-  {
-    const float v = warp_sum(s_loc);
-    if (lane == 0) tl->fscr[wid] = v;
-    __syncthreads();
-    if (ctl && lane == 0) {
-      float r = tl->fscr[0];
-      for (int q = 1; q < NW; ++q) r += tl->fscr[q];
-      cluster.map_shared_rank(tl->sarr, 0)[rank] = r;
-    }
-  }
-  TR(6);
-  cluster_arrive();  // (B) S partials landed in rank 0; no DSMEM access after this point
-  cluster_wait();
-  TR(7);
-  if (rank == 0 && ctl) epilogue<NT>(a, row, tl, cs, pre);
+  cluster_sync_all();  // no CTA exits while a peer may still write its shared memory
 }
 
 }  // namespace
 
-#ifdef SV_TRACE
-extern "C" __attribute__((visibility("default"))) int sv_debug_set_trace(void *buf) {
-  return (int)cudaMemcpyToSymbol(g_trace, &buf, sizeof(buf));
-}
-#endif
-
-namespace {
-
-template <typename T, int NT>
-cudaError_t launch_score_t(const ScoreArgs &a, cudaStream_t st) {
-  const int elem = (int)sizeof(T);
-  const size_t smem = 2 * (size_t)a.chunk * elem + sizeof(ScoreTail<NT>);
-  const void *fn = (const void *)sv_score_kernel<T, NT>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+cudaError_t launch_score(const ScoreArgs &a, cudaStream_t st) {
+  const void *fn = a.bf16 ? (const void *)sv_score_kernel<__nv_bfloat16> : (const void *)sv_score_kernel<float>;
+  cudaError_t e = cudaSuccess;
   if (a.cs > 8) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)((int64_t)a.B * a.k * a.cs));
-  cfg.blockDim = dim3(NT);
-  cfg.dynamicSmemBytes = smem;
+  cfg.blockDim = dim3(kScoreThreads);
+  cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -469,17 +562,17 @@ cudaError_t launch_score_t(const ScoreArgs &a, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, sv_score_kernel<T, NT>, a);
-}
-
-}  // namespace
-
-cudaError_t launch_score(const ScoreArgs &a, cudaStream_t st) {
-  // 16 warps per CTA when a CTA holds a large chunk (2 CTAs / SM), 8 warps for small chunks
-  static const int nt = tune_knob("SV_SCORE_THREADS", 0);
-  const bool big = nt ? nt == 512 : (int64_t)a.chunk * (a.bf16 ? 2 : 4) * 2 > 48 * 1024;
-  if (a.bf16) return big ? launch_score_t<__nv_bfloat16, 512>(a, st) : launch_score_t<__nv_bfloat16, 256>(a, st);
-  return big ? launch_score_t<float, 512>(a, st) : launch_score_t<float, 256>(a, st);
+  // persistent: as many clusters as can be co-resident, never more than rows (clusters are
+  // independent, so residency is a performance choice, not a correctness requirement)
+  const int64_t rows = (int64_t)a.B * a.k;
+  int64_t ncl = max_active_clusters(fn, cfg, 0, a.cs);
+  static const int mult = tune_knob("SV_SCORE_CLUSTER_MULT", 1);
+  ncl *= mult;
+  if (ncl > rows) ncl = rows;
+  if (ncl < 1) ncl = 1;
+  cfg.gridDim = dim3((unsigned)(ncl * a.cs));
+  if (a.bf16) return cudaLaunchKernelEx(&cfg, sv_score_kernel<__nv_bfloat16>, a);
+  return cudaLaunchKernelEx(&cfg, sv_score_kernel<float>, a);
 }
 
 }  // namespace sv
