@@ -9,7 +9,7 @@ namespace sv {
 
 // sv_score: 15 compute warps + 1 control warp per CTA; kScoreGroup 16-byte loads per tensor
 // per compute thread in flight together (46 KB per CTA)
-constexpr int kScoreThreads = 512;
+constexpr int kScoreThreads = 384;
 constexpr int kScoreGroup = 2;
 constexpr int kRowsThreads = 256;
 constexpr int kSampleThreads = 256;

@@ -36,10 +36,13 @@ constexpr int NT = kScoreThreads, NW = NT / 32, NCW = NW - 1;  // NCW compute wa
 constexpr int NC = NCW * 32;                                    // compute threads
 constexpr int G = kScoreGroup;                                  // units per thread per group
 
-// named barriers (id 0 is __syncthreads)
-// P1Done alternates between two ids: the compute warps may run one pass 1 ahead of the
-// control warp's matching sync, never two (the LamReady / P2Done chain bounds them).
-enum : int { kBarCompute = 1, kBarP1Done = 2, kBarLamReady = 3, kBarP2Done = 4, kBarP1DoneOdd = 5 };
+// named barriers (id 0 is __syncthreads).  The compute warps may run ahead of the control warp
+// by up to two pass-1s and one pass-2 (the LamReady chain bounds them), so the per-row barriers
+// rotate over 3 (P1Done) and 2 (LamReady, P2Done) ids and never mix two rows.
+enum : int { kBarCompute = 1, kBarP1Done0 = 2, kBarLam0 = 5, kBarP2Done0 = 7 };
+__device__ __forceinline__ int bar_p1done(int64_t row) { return kBarP1Done0 + (int)(row % 3); }
+__device__ __forceinline__ int bar_lam(int64_t row) { return kBarLam0 + (int)(row & 1); }
+__device__ __forceinline__ int bar_p2done(int64_t row) { return kBarP2Done0 + (int)(row & 1); }
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -49,10 +52,10 @@ struct Smem {
   uint64_t full_p[2], empty_p[2], full_s[2], empty_s[2];
   double part[2][kMaxCluster][5];  // (M_d, L_d, M_c, L_c, W) pushed by every rank, per slot
   float sarr[2][kMaxCluster];      // S partials pushed to the epilogue CTA, per slot
-  double glob[2][5];               // merged (M_d, L_d, M_c, L_c, W), per slot
-  float lam[2][2];                 // Lambda_d, Lambda_c, per slot
-  double mine[2][6];               // this CTA's pass-1 partial, per row parity ([4] unused)
-  float s_mine;                    // this CTA's pass-2 partial
+  double glob[3][5];               // merged (M_d, L_d, M_c, L_c, W), per row % 3
+  float lam[2][2];                 // Lambda_d, Lambda_c, per row parity
+  double mine[3][6];               // this CTA's pass-1 partial, per row % 3 ([4] unused)
+  float s_mine[2];                 // this CTA's pass-2 partial, per row parity
   float fscr[2 * NCW];
   float fscr2[NCW];
   double dscr[3 * NCW];
@@ -181,14 +184,26 @@ __device__ __forceinline__ void pass1_thread(const Chunk<T> &ch, float cd, float
   md = kMFloor;
   mc = kMFloor;
   lf_d = lf_c = wf = 0.f;
+  // software pipeline: the next group's loads are in flight while this group is reduced
+  uint4 nd[G], nc[G];
+#pragma unroll
+  for (int q = 0; q < G; ++q) {
+    const int u = tid + q * NC;
+    if (u < ch.units) {
+      nd[q] = ldg_hint(ch.d + (size_t)u * EPU, pol);
+      nc[q] = ldg_hint(ch.c + (size_t)u * EPU, pol);
+    }
+  }
   for (int u0 = 0; u0 < ch.units; u0 += G * NC) {
     uint4 rd[G], rc[G];
 #pragma unroll
     for (int q = 0; q < G; ++q) {
-      const int u = u0 + tid + q * NC;
+      rd[q] = nd[q];
+      rc[q] = nc[q];
+      const int u = u0 + G * NC + tid + q * NC;
       if (u < ch.units) {
-        rd[q] = ldg_hint(ch.d + (size_t)u * EPU, pol);
-        rc[q] = ldg_hint(ch.c + (size_t)u * EPU, pol);
+        nd[q] = ldg_hint(ch.d + (size_t)u * EPU, pol);
+        nc[q] = ldg_hint(ch.c + (size_t)u * EPU, pol);
       }
     }
     float gmd = md, gmc = mc;
@@ -260,14 +275,26 @@ __device__ __forceinline__ float pass2_thread(const Chunk<T> &ch, float cd, floa
   const int tid = threadIdx.x;
   const f2 cdd{cd, cd}, ccc{cc, cc}, ld2{-lamd, -lamd}, lc2{-lamc, -lamc};
   f2 acc{0.f, 0.f};
+  // software pipeline: the next group's loads are in flight while this group is reduced
+  uint4 nd[G], nc[G];
+#pragma unroll
+  for (int q = 0; q < G; ++q) {
+    const int u = tid + q * NC;
+    if (u < ch.units) {
+      nd[q] = ldg_hint(ch.d + (size_t)u * EPU, pol);
+      nc[q] = ldg_hint(ch.c + (size_t)u * EPU, pol);
+    }
+  }
   for (int u0 = 0; u0 < ch.units; u0 += G * NC) {
     uint4 rd[G], rc[G];
 #pragma unroll
     for (int q = 0; q < G; ++q) {
-      const int u = u0 + tid + q * NC;
+      rd[q] = nd[q];
+      rc[q] = nc[q];
+      const int u = u0 + G * NC + tid + q * NC;
       if (u < ch.units) {
-        rd[q] = ldg_hint(ch.d + (size_t)u * EPU, pol);
-        rc[q] = ldg_hint(ch.c + (size_t)u * EPU, pol);
+        nd[q] = ldg_hint(ch.d + (size_t)u * EPU, pol);
+        nc[q] = ldg_hint(ch.c + (size_t)u * EPU, pol);
       }
     }
 #pragma unroll
@@ -395,8 +422,9 @@ __global__ void __launch_bounds__(kScoreThreads, 2) sv_score_kernel(const ScoreA
 
   if (!ctl) {
     // ================================================================ compute warps
+    // iteration j: pass 1 of row j, then pass 2 of row j - 2 (two rows of slack for the merge)
     const uint64_t pol_keep = l2_policy_evict_last(), pol_last = l2_policy_evict_first();
-    for (int64_t j = 0; j <= nrows; ++j) {
+    for (int64_t j = 0; j <= nrows + 1; ++j) {
       if (j < nrows) {  // ---- pass 1 of row j
         const Chunk<T> ch = chunk_of<T>(a, row_of(j), rank);
         float md, mc, lf_d, lf_c, wf;
@@ -428,7 +456,7 @@ __global__ void __launch_bounds__(kScoreThreads, 2) sv_score_kernel(const ScoreA
 #pragma unroll
           for (int k = 0; k < 3; ++k) sm.dscr[k * NCW + wid] = v[k];
         bar_sync(kBarCompute, NC);
-        double *mine = sm.mine[j & 1];
+        double *mine = sm.mine[j % 3];
         if (tid < 3) {
           double r = 0.0;
           for (int q = 0; q < NCW; ++q) r += sm.dscr[tid * NCW + q];
@@ -438,15 +466,15 @@ __global__ void __launch_bounds__(kScoreThreads, 2) sv_score_kernel(const ScoreA
           mine[0] = Md;
           mine[2] = Mc;
         }
-        bar_arrive((j & 1) ? kBarP1DoneOdd : kBarP1Done, NT);  // control warp may push the partial
+        bar_arrive(bar_p1done(j), NT);  // the control warp may push the partial
       }
-      if (j >= 1) {  // ---- pass 2 of row j - 1
-        const int s = (int)((j - 1) & 1);
-        bar_sync(kBarLamReady, NT);  // control warp merged row j - 1
-        const float lamd = sm.lam[s][0], lamc = sm.lam[s][1];
+      if (j >= 2 && j - 2 < nrows) {  // ---- pass 2 of row j - 2
+        const int64_t r2 = j - 2;
+        bar_sync(bar_lam(r2), NT);  // the control warp merged row j - 2
+        const float lamd = sm.lam[r2 & 1][0], lamc = sm.lam[r2 & 1][1];
         float sl = 0.f;
         if (lamd == lamd && lamc == lamc) {  // bad rows skip the S sweep
-          const Chunk<T> ch = chunk_of<T>(a, row_of(j - 1), rank);
+          const Chunk<T> ch = chunk_of<T>(a, row_of(r2), rank);
           sl = pass2_thread<T>(ch, cd, cc, lamd, lamc, pol_last);
         }
         sl = warp_sum(sl);
@@ -455,19 +483,20 @@ __global__ void __launch_bounds__(kScoreThreads, 2) sv_score_kernel(const ScoreA
         if (tid == 0) {
           float r = sm.fscr2[0];
           for (int q = 1; q < NCW; ++q) r += sm.fscr2[q];
-          sm.s_mine = r;
+          sm.s_mine[r2 & 1] = r;
         }
-        bar_arrive(kBarP2Done, NT);
+        bar_arrive(bar_p2done(r2), NT);
       }
     }
   } else {
     // ================================================================ control warp
-    for (int64_t j = 0; j <= nrows + 1; ++j) {
+    for (int64_t j = 0; j <= nrows + 2; ++j) {
       // (1) merge row j - 1's partials (pushed during the peers' iteration j - 1) while the
-      //     compute warps run pass 1 of row j
+      //     compute warps stream; needed by their pass 2 one iteration later
       if (j >= 1 && j - 1 < nrows) {
-        const int s = (int)((j - 1) & 1);
-        wait_cluster(&sm.full_p[s], (uint32_t)(((j - 1) >> 1) & 1));
+        const int64_t r1 = j - 1;
+        const int s = (int)(r1 & 1);
+        wait_cluster(&sm.full_p[s], (uint32_t)((r1 >> 1) & 1));
         double pr[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         pr[0] = pr[2] = kMFloor;
         if (lane < cs)
@@ -489,53 +518,56 @@ __global__ void __launch_bounds__(kScoreThreads, 2) sv_score_kernel(const ScoreA
           W += __shfl_sync(0xffffffffu, cw, r);
         }
         if (lane == 0) {
-          sm.glob[s][0] = GMd;
-          sm.glob[s][1] = L_d;
-          sm.glob[s][2] = GMc;
-          sm.glob[s][3] = L_c;
-          sm.glob[s][4] = W;
+          double *g = sm.glob[r1 % 3];
+          g[0] = GMd;
+          g[1] = L_d;
+          g[2] = GMc;
+          g[3] = L_c;
+          g[4] = W;
           const bool ok = L_d > 0.0 && L_c > 0.0 && L_d < 1e300 && L_c < 1e300 && GMd < FLT_MAX && GMc < FLT_MAX;
           sm.lam[s][0] = ok ? (float)((double)GMd * cd + log2_acc(L_d)) : __int_as_float(0x7fc00000);
           sm.lam[s][1] = ok ? (float)((double)GMc * cc + log2_acc(L_c)) : __int_as_float(0x7fc00000);
         }
         __syncwarp();
-        bar_arrive(kBarLamReady, NT);
+        bar_arrive(bar_lam(r1), NT);
       }
       // (2) push this CTA's pass-1 partial of row j into slot j % 2 of every peer
       if (j < nrows) {
         const int s = (int)(j & 1);
-        bar_sync((j & 1) ? kBarP1DoneOdd : kBarP1Done, NT);
+        bar_sync(bar_p1done(j), NT);
         if (j >= 2) wait_cluster(&sm.empty_p[s], (uint32_t)(((j >> 1) - 1) & 1));
         if (lane < cs) {
-          const double *mine = sm.mine[j & 1];
+          const double *mine = sm.mine[j % 3];
           const double v[5] = {mine[0], mine[1], mine[2], mine[3], mine[5]};
 #pragma unroll
           for (int k = 0; k < 5; ++k) st_remote_f64(remote(&sm.part[s][rank][k], lane), v[k]);
           remote_arrive(remote(&sm.full_p[s], lane));
         }
       }
-      // (3) push this CTA's S partial of row j - 1 to the row's epilogue CTA
-      if (j >= 1 && j - 1 < nrows) {
-        const int s = (int)((j - 1) & 1);
-        const int epi = (int)((j - 1) % cs);
-        bar_sync(kBarP2Done, NT);
-        if (j - 1 >= 2) wait_cluster(&sm.empty_s[s], (uint32_t)((((j - 1) >> 1) - 1) & 1));
+      // (3) push this CTA's S partial of row j - 2 to the row's epilogue CTA
+      if (j >= 2 && j - 2 < nrows) {
+        const int64_t r2 = j - 2;
+        const int s = (int)(r2 & 1);
+        const int epi = (int)(r2 % cs);
+        bar_sync(bar_p2done(r2), NT);
+        if (r2 >= 2) wait_cluster(&sm.empty_s[s], (uint32_t)(((r2 >> 1) - 1) & 1));
         if (lane == 0) {
-          st_remote_f32(remote(&sm.sarr[s][rank], epi), sm.s_mine);
+          st_remote_f32(remote(&sm.sarr[s][rank], epi), sm.s_mine[s]);
           remote_arrive(remote(&sm.full_s[s], epi));
         }
         __syncwarp();
       }
-      // (4) epilogue of row j - 2 (its S partials were pushed during iteration j - 1)
-      if (j >= 2 && j - 2 < nrows && (int)((j - 2) % cs) == rank) {
-        const int s = (int)((j - 2) & 1);
+      // (4) epilogue of row j - 3 (its S partials were pushed during iteration j - 1)
+      if (j >= 3 && j - 3 < nrows && (int)((j - 3) % cs) == rank) {
+        const int64_t r3 = j - 3;
+        const int s = (int)(r3 & 1);
         // this CTA's full_s[s] completes once per row r with r % 2 == s and r % cs == rank: the
         // completion index of row r is r / lcm(2, cs)
         const int64_t lcm2 = cs == 1 ? 2 : cs;
-        wait_cluster(&sm.full_s[s], (uint32_t)(((j - 2) / lcm2) & 1));
-        epilogue<T>(a, row_of(j - 2), sm.glob[s], sm.sarr[s], cs);
+        wait_cluster(&sm.full_s[s], (uint32_t)((r3 / lcm2) & 1));
+        epilogue<T>(a, row_of(r3), sm.glob[r3 % 3], sm.sarr[s], cs);
         __syncwarp();
-        if (lane < cs) remote_arrive(remote(&sm.empty_s[s], lane));  // slot s free for row j
+        if (lane < cs) remote_arrive(remote(&sm.empty_s[s], lane));  // slot s free for row r3 + 2
       }
     }
   }
