@@ -32,9 +32,14 @@ namespace sv {
 
 namespace {
 
-constexpr int NT = kScoreThreads, NW = NT / 32, NCW = NW - 1;  // NCW compute warps
-constexpr int NC = NCW * 32;                                    // compute threads
-constexpr int G = kScoreGroup;                                  // units per thread per group
+constexpr int NT = kScoreThreads, NW = NT / 32;
+constexpr int NCW = NW - 2;   // compute warps
+constexpr int NC = NCW * 32;  // compute threads
+constexpr int PW = NW - 2;    // producer warp (bulk copies into the ring)
+constexpr int XW = NW - 1;    // exchange warp (highest id: merges, pushes, epilogue)
+constexpr int kSlots = kScoreSlots;
+constexpr int kStageBytes = kScoreStageBytes;
+constexpr int NX = NC + 32;   // participants of the compute <-> exchange barriers
 
 // named barriers (id 0 is __syncthreads).  The compute warps may run ahead of the control warp
 // by up to two pass-1s and one pass-2 (the LamReady chain bounds them), so the per-row barriers
@@ -49,6 +54,7 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
 }
 
 struct Smem {
+  uint64_t ring_full[kSlots], ring_empty[kSlots];
   uint64_t full_p[2], empty_p[2], full_s[2], empty_s[2];
   double part[2][kMaxCluster][5];  // (M_d, L_d, M_c, L_c, W) pushed by every rank, per slot
   float sarr[2][kMaxCluster];      // S partials pushed to the epilogue CTA, per slot
@@ -86,6 +92,7 @@ __device__ __forceinline__ void wait_cluster(uint64_t *bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void wait_cta(uint64_t *bar, uint32_t parity) { mbar_wait(bar, parity); }
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -154,164 +161,140 @@ __device__ __forceinline__ float unit_max(const uint4 &v) {
   }
 }
 
-// Where this CTA's chunk of a row lives.
+// ---------------------------------------------------------------- stages
+// A row's chunk is consumed in stages of kStageBytes per tensor.  The producer warp moves each
+// stage (draft part + companion part) into a ring slot with the bulk-copy engine; the compute
+// warps read it from shared memory.  Both sides walk the same (row, pass, stage) sequence.
 template <typename T>
-struct Chunk {
-  const T *d, *c;
-  int n;      // elements
-  int units;  // 16-byte units (0 when the chunk pair is not 16-byte aligned)
+struct Stage {
+  const T *d, *c;  // global source of this stage
+  int n;           // elements in the stage
+  int units;       // 16-byte units moved by the bulk-copy engine (0: unaligned rows)
 };
 template <typename T>
-__device__ __forceinline__ Chunk<T> chunk_of(const ScoreArgs &a, int64_t row, int rank) {
-  const int64_t b = row / a.k, i = row % a.k, v0 = (int64_t)rank * a.chunk;
-  Chunk<T> ch;
-  ch.d = reinterpret_cast<const T *>(a.d) + b * a.d_sb + i * a.d_si + v0;
-  ch.c = reinterpret_cast<const T *>(a.c) + b * a.c_sb + i * a.c_si + v0;
-  ch.n = (int)max((int64_t)0, min(a.chunk, (int64_t)a.V - v0));
-  const bool al = ((reinterpret_cast<uintptr_t>(ch.d) | reinterpret_cast<uintptr_t>(ch.c)) & 15) == 0;
-  ch.units = al ? ch.n / Elem<T>::kPerUnit : 0;
-  return ch;
+__device__ __forceinline__ int stages_per_row(const ScoreArgs &a, int rank) {
+  const int64_t n = max((int64_t)0, min(a.chunk, (int64_t)a.V - (int64_t)rank * a.chunk));
+  constexpr int SE = kStageBytes / sizeof(T);
+  return (int)((n + SE - 1) / SE);
 }
-
-// Pass 1 of one chunk by the compute warps: thread maxima and sums, processed in groups of G
-// units per thread (all loads of a group in flight together) with an exact online merge
-// between groups.  Returns the thread's (m_d, m_c, l_d, l_c, w).
-template <typename T, bool kGuard>
-__device__ __forceinline__ void pass1_thread(const Chunk<T> &ch, float cd, float cc, uint64_t pol, float &md,
-                                             float &mc, float &lf_d, float &lf_c, float &wf) {
-  constexpr int EPU = Elem<T>::kPerUnit;
-  const int tid = threadIdx.x;
-  md = kMFloor;
-  mc = kMFloor;
-  lf_d = lf_c = wf = 0.f;
-  // software pipeline: the next group's loads are in flight while this group is reduced
-  uint4 nd[G], nc[G];
-#pragma unroll
-  for (int q = 0; q < G; ++q) {
-    const int u = tid + q * NC;
-    if (u < ch.units) {
-      nd[q] = ldg_hint(ch.d + (size_t)u * EPU, pol);
-      nc[q] = ldg_hint(ch.c + (size_t)u * EPU, pol);
-    }
-  }
-  for (int u0 = 0; u0 < ch.units; u0 += G * NC) {
-    uint4 rd[G], rc[G];
-#pragma unroll
-    for (int q = 0; q < G; ++q) {
-      rd[q] = nd[q];
-      rc[q] = nc[q];
-      const int u = u0 + G * NC + tid + q * NC;
-      if (u < ch.units) {
-        nd[q] = ldg_hint(ch.d + (size_t)u * EPU, pol);
-        nc[q] = ldg_hint(ch.c + (size_t)u * EPU, pol);
-      }
-    }
-    float gmd = md, gmc = mc;
-#pragma unroll
-    for (int q = 0; q < G; ++q)
-      if (u0 + tid + q * NC < ch.units) {
-        gmd = fmaxf(gmd, unit_max<T>(rd[q]));
-        gmc = fmaxf(gmc, unit_max<T>(rc[q]));
-      }
-    if (gmd > md || gmc > mc) {  // exact online rescale of the running sums
-      const float sdf = ex2((md - gmd) * cd), scf = ex2((mc - gmc) * cc);
-      const float delta = (gmc - mc) * cc - (gmd - md) * cd;
-      if (lf_d > 0.f) wf = fmaf(lf_d, delta, wf);
-      wf *= sdf;
-      lf_d *= sdf;
-      lf_c *= scf;
-      md = gmd;
-      mc = gmc;
-    }
-    const float nmd = -md * cd, nmc = -mc * cc;
-    const f2 cdd{cd, cd}, ccc{cc, cc}, nmdd{nmd, nmd}, nmcc{nmc, nmc};
-    P1 acc{{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
-#pragma unroll
-    for (int q = 0; q < G; ++q)
-      if (u0 + tid + q * NC < ch.units) {
-        f2 xd[EPU / 2], xc[EPU / 2];
-        unit_pairs<T>(rd[q], xd);
-        unit_pairs<T>(rc[q], xc);
-#pragma unroll
-        for (int p = 0; p < EPU / 2; ++p) p1_pair<kGuard>(xd[p], xc[p], cdd, ccc, nmdd, nmcc, acc);
-      }
-    lf_d += acc.ld.x + acc.ld.y;
-    lf_c += acc.lc.x + acc.lc.y;
-    wf += acc.w.x + acc.w.y;
-  }
-  // element-wise remainder (ragged tail, or the whole chunk when unaligned)
-  const int e0 = ch.units * EPU;
-  float tmd = md, tmc = mc;
-  for (int e = e0 + tid; e < ch.n; e += NC) {
-    tmd = fmaxf(tmd, Elem<T>::load(ch.d + e));
-    tmc = fmaxf(tmc, Elem<T>::load(ch.c + e));
-  }
-  if (tmd > md || tmc > mc) {
-    const float sdf = ex2((md - tmd) * cd), scf = ex2((mc - tmc) * cc);
-    const float delta = (tmc - mc) * cc - (tmd - md) * cd;
-    if (lf_d > 0.f) wf = fmaf(lf_d, delta, wf);
-    wf *= sdf;
-    lf_d *= sdf;
-    lf_c *= scf;
-    md = tmd;
-    mc = tmc;
-  }
-  const float nmd = -md * cd, nmc = -mc * cc;
-  for (int e = e0 + tid; e < ch.n; e += NC) {
-    const float xd = Elem<T>::load(ch.d + e), xc = Elem<T>::load(ch.c + e);
-    const float ad = fmaf(xd, cd, nmd), ac = fmaf(xc, cc, nmc);
-    const float ed = ex2(ad);
-    lf_d += ed;
-    lf_c += ex2(ac);
-    wf += ed > 0.f ? ed * (ad - ac) : 0.f;
-  }
-}
-
-// Pass 2 of one chunk by the compute warps (L2 re-read): the thread's S partial.
 template <typename T>
-__device__ __forceinline__ float pass2_thread(const Chunk<T> &ch, float cd, float cc, float lamd, float lamc,
-                                              uint64_t pol) {
-  constexpr int EPU = Elem<T>::kPerUnit;
+__device__ __forceinline__ Stage<T> stage_of(const ScoreArgs &a, int64_t row, int rank, int st) {
+  constexpr int SE = kStageBytes / sizeof(T), EPU = Elem<T>::kPerUnit;
+  const int64_t b = row / a.k, i = row % a.k;
+  const int64_t n_rank = max((int64_t)0, min(a.chunk, (int64_t)a.V - (int64_t)rank * a.chunk));
+  const int64_t v0 = (int64_t)rank * a.chunk + (int64_t)st * SE;
+  Stage<T> s;
+  s.d = reinterpret_cast<const T *>(a.d) + b * a.d_sb + i * a.d_si + v0;
+  s.c = reinterpret_cast<const T *>(a.c) + b * a.c_sb + i * a.c_si + v0;
+  s.n = (int)min((int64_t)SE, n_rank - (int64_t)st * SE);
+  const bool al = ((reinterpret_cast<uintptr_t>(s.d) | reinterpret_cast<uintptr_t>(s.c)) & 15) == 0;
+  s.units = al ? s.n / EPU : 0;
+  return s;
+}
+
+// Walk of the (row, pass, stage) sequence shared by the producer and the compute warps:
+// iteration j = pass 1 of row j (if j < nrows), then pass 2 of row j - 2 (if valid).
+template <typename F>
+__device__ __forceinline__ void walk_stages(int64_t nrows, int nst, F &&f) {
+  int64_t g = 0;  // global stage counter -> ring slot g % kSlots, use g / kSlots
+  for (int64_t j = 0; j <= nrows + 1; ++j) {
+    if (j < nrows)
+      for (int st = 0; st < nst; ++st, ++g) f(g, j, 1, st);
+    if (j >= 2 && j - 2 < nrows)
+      for (int st = 0; st < nst; ++st, ++g) f(g, j - 2, 2, st);
+  }
+}
+
+// pass-1 state of one compute thread across the stages of a row
+struct P1State {
+  float md, mc, ld, lc, w;
+};
+
+__device__ __forceinline__ void p1_rescale(P1State &t, float gmd, float gmc, float cd, float cc) {
+  if (gmd > t.md || gmc > t.mc) {  // exact online rescale of the running sums
+    const float sdf = ex2((t.md - gmd) * cd), scf = ex2((t.mc - gmc) * cc);
+    const float delta = (gmc - t.mc) * cc - (gmd - t.md) * cd;
+    if (t.ld > 0.f) t.w = fmaf(t.ld, delta, t.w);
+    t.w *= sdf;
+    t.ld *= sdf;
+    t.lc *= scf;
+    t.md = gmd;
+    t.mc = gmc;
+  }
+}
+
+// Pass 1 on one stage (smem copy sd / sc, or global when unaligned).
+template <typename T, bool kGuard>
+__device__ __forceinline__ void p1_stage(const Stage<T> &sg, const T *sd, const T *sc, float cd, float cc,
+                                         P1State &t) {
+  constexpr int EPU = Elem<T>::kPerUnit, UPT = kStageBytes / 16 / NC;
+  const int tid = threadIdx.x;
+  uint4 rd[UPT], rc[UPT];
+  float gmd = t.md, gmc = t.mc;
+#pragma unroll
+  for (int q = 0; q < UPT; ++q) {
+    const int u = tid + q * NC;
+    if (u < sg.units) {
+      rd[q] = reinterpret_cast<const uint4 *>(sd)[u];
+      rc[q] = reinterpret_cast<const uint4 *>(sc)[u];
+      gmd = fmaxf(gmd, unit_max<T>(rd[q]));
+      gmc = fmaxf(gmc, unit_max<T>(rc[q]));
+    }
+  }
+  const int e0 = sg.units * EPU;  // element-wise remainder, read from global
+  for (int e = e0 + tid; e < sg.n; e += NC) {
+    gmd = fmaxf(gmd, Elem<T>::load(sg.d + e));
+    gmc = fmaxf(gmc, Elem<T>::load(sg.c + e));
+  }
+  p1_rescale(t, gmd, gmc, cd, cc);
+  const float nmd = -t.md * cd, nmc = -t.mc * cc;
+  const f2 cdd{cd, cd}, ccc{cc, cc}, nmdd{nmd, nmd}, nmcc{nmc, nmc};
+  P1 acc{{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+#pragma unroll
+  for (int q = 0; q < UPT; ++q)
+    if (tid + q * NC < sg.units) {
+      f2 xd[EPU / 2], xc[EPU / 2];
+      unit_pairs<T>(rd[q], xd);
+      unit_pairs<T>(rc[q], xc);
+#pragma unroll
+      for (int p = 0; p < EPU / 2; ++p) p1_pair<kGuard>(xd[p], xc[p], cdd, ccc, nmdd, nmcc, acc);
+    }
+  t.ld += acc.ld.x + acc.ld.y;
+  t.lc += acc.lc.x + acc.lc.y;
+  t.w += acc.w.x + acc.w.y;
+  for (int e = e0 + tid; e < sg.n; e += NC) {
+    const float ad = fmaf(Elem<T>::load(sg.d + e), cd, nmd), ac = fmaf(Elem<T>::load(sg.c + e), cc, nmc);
+    const float ed = ex2(ad);
+    t.ld += ed;
+    t.lc += ex2(ac);
+    t.w += ed > 0.f ? ed * (ad - ac) : 0.f;
+  }
+}
+
+// Pass 2 on one stage: the thread's S partial.
+template <typename T>
+__device__ __forceinline__ float p2_stage(const Stage<T> &sg, const T *sd, const T *sc, float cd, float cc,
+                                          float lamd, float lamc) {
+  constexpr int EPU = Elem<T>::kPerUnit, UPT = kStageBytes / 16 / NC;
   const int tid = threadIdx.x;
   const f2 cdd{cd, cd}, ccc{cc, cc}, ld2{-lamd, -lamd}, lc2{-lamc, -lamc};
   f2 acc{0.f, 0.f};
-  // software pipeline: the next group's loads are in flight while this group is reduced
-  uint4 nd[G], nc[G];
 #pragma unroll
-  for (int q = 0; q < G; ++q) {
+  for (int q = 0; q < UPT; ++q) {
     const int u = tid + q * NC;
-    if (u < ch.units) {
-      nd[q] = ldg_hint(ch.d + (size_t)u * EPU, pol);
-      nc[q] = ldg_hint(ch.c + (size_t)u * EPU, pol);
-    }
-  }
-  for (int u0 = 0; u0 < ch.units; u0 += G * NC) {
-    uint4 rd[G], rc[G];
+    if (u < sg.units) {
+      f2 xd[EPU / 2], xc[EPU / 2];
+      unit_pairs<T>(reinterpret_cast<const uint4 *>(sd)[u], xd);
+      unit_pairs<T>(reinterpret_cast<const uint4 *>(sc)[u], xc);
 #pragma unroll
-    for (int q = 0; q < G; ++q) {
-      rd[q] = nd[q];
-      rc[q] = nc[q];
-      const int u = u0 + G * NC + tid + q * NC;
-      if (u < ch.units) {
-        nd[q] = ldg_hint(ch.d + (size_t)u * EPU, pol);
-        nc[q] = ldg_hint(ch.c + (size_t)u * EPU, pol);
+      for (int p = 0; p < EPU / 2; ++p) {
+        const f2 ad = fma2(xd[p], cdd, ld2), ac = fma2(xc[p], ccc, lc2);
+        acc = add2(acc, f2{ex2(fminf(ad.x, ac.x)), ex2(fminf(ad.y, ac.y))});
       }
     }
-#pragma unroll
-    for (int q = 0; q < G; ++q)
-      if (u0 + tid + q * NC < ch.units) {
-        f2 xd[EPU / 2], xc[EPU / 2];
-        unit_pairs<T>(rd[q], xd);
-        unit_pairs<T>(rc[q], xc);
-#pragma unroll
-        for (int p = 0; p < EPU / 2; ++p) {
-          const f2 ad = fma2(xd[p], cdd, ld2), ac = fma2(xc[p], ccc, lc2);
-          acc = add2(acc, f2{ex2(fminf(ad.x, ac.x)), ex2(fminf(ad.y, ac.y))});
-        }
-      }
   }
-  for (int e = ch.units * EPU + tid; e < ch.n; e += NC)
-    acc.x += ex2(fminf(fmaf(Elem<T>::load(ch.d + e), cd, -lamd), fmaf(Elem<T>::load(ch.c + e), cc, -lamc)));
+  for (int e = sg.units * EPU + tid; e < sg.n; e += NC)
+    acc.x += ex2(fminf(fmaf(Elem<T>::load(sg.d + e), cd, -lamd), fmaf(Elem<T>::load(sg.c + e), cc, -lamc)));
   return acc.x + acc.y;
 }
 
@@ -395,9 +378,21 @@ __device__ __noinline__ void epilogue(const ScoreArgs &a, int64_t row, const dou
   }
 }
 
+__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kScoreThreads, 2) sv_score_kernel(const ScoreArgs a) {
+  constexpr int SE = kStageBytes / sizeof(T);
   __shared__ Smem sm;
+  extern __shared__ __align__(128) uint8_t ring_raw[];
+  T *const ring = reinterpret_cast<T *>(ring_raw);  // kSlots x [draft stage | companion stage]
   cg::cluster_group cluster = cg::this_cluster();
   const int cs = a.cs;
   const int rank = (int)cluster.block_rank();
@@ -405,11 +400,15 @@ __global__ void __launch_bounds__(kScoreThreads, 2) sv_score_kernel(const ScoreA
   const int64_t rows = (int64_t)a.B * a.k;
   const int64_t nrows = rows > cid ? (rows - cid + ncl - 1) / ncl : 0;  // rows of this cluster
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const bool ctl = wid == NCW;
   const float cd = a.cd, cc = a.cc;
+  const int nst = stages_per_row<T>(a, rank);
   auto row_of = [&](int64_t j) { return cid + j * ncl; };
 
   if (tid == 0) {
+    for (int k = 0; k < kSlots; ++k) {
+      mbar_init(&sm.ring_full[k], 1);
+      mbar_init(&sm.ring_empty[k], NCW);
+    }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sm.full_p[s], cs);
       mbar_init(&sm.empty_p[s], cs);
@@ -420,79 +419,113 @@ __global__ void __launch_bounds__(kScoreThreads, 2) sv_score_kernel(const ScoreA
   }
   cluster_sync_all();  // every barrier of the cluster is initialised before any remote arrive
 
-  if (!ctl) {
+  if (wid < NCW) {
     // ================================================================ compute warps
-    // iteration j: pass 1 of row j, then pass 2 of row j - 2 (two rows of slack for the merge)
-    const uint64_t pol_keep = l2_policy_evict_last(), pol_last = l2_policy_evict_first();
-    for (int64_t j = 0; j <= nrows + 1; ++j) {
-      if (j < nrows) {  // ---- pass 1 of row j
-        const Chunk<T> ch = chunk_of<T>(a, row_of(j), rank);
-        float md, mc, lf_d, lf_c, wf;
-        pass1_thread<T, false>(ch, cd, cc, pol_keep, md, mc, lf_d, lf_c, wf);
-        if (wf != wf && lf_d == lf_d && lf_c == lf_c)  // 0 * (-inf) from masked logits: guarded redo
-          pass1_thread<T, true>(ch, cd, cc, pol_keep, md, mc, lf_d, lf_c, wf);
-        // block merge over the compute warps (fixed warp / lane order)
-        float Md = warp_max(md), Mc = warp_max(mc);
-        if (lane == 0) {
-          sm.fscr[wid] = Md;
-          sm.fscr[NCW + wid] = Mc;
+    P1State t{kMFloor, kMFloor, 0.f, 0.f, 0.f};
+    float lamd = 0.f, lamc = 0.f, s_acc = 0.f;
+    walk_stages(nrows, nst, [&](int64_t g, int64_t row, int pass, int st) {
+      const int slot = (int)(g % kSlots);
+      const Stage<T> sg = stage_of<T>(a, row_of(row), rank, st);  // row = local index
+      const T *sd = ring + (size_t)slot * 2 * SE, *sc = sd + SE;
+      if (pass == 1) {
+        if (st == 0) t = P1State{kMFloor, kMFloor, 0.f, 0.f, 0.f};
+        mbar_wait(&sm.ring_full[slot], (uint32_t)((g / kSlots) & 1));
+        const P1State t0 = t;
+        p1_stage<T, false>(sg, sd, sc, cd, cc, t);
+        if (t.w != t.w && t.ld == t.ld && t.lc == t.lc) {  // 0 * (-inf) from masked logits: redo guarded
+          t = t0;
+          p1_stage<T, true>(sg, sd, sc, cd, cc, t);
         }
-        bar_sync(kBarCompute, NC);
-        Md = sm.fscr[0];
-        Mc = sm.fscr[NCW];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.ring_empty[slot]);
+        if (st == nst - 1) {  // ---- block merge of the row's pass 1 (fixed warp / lane order)
+          float Md = warp_max(t.md), Mc = warp_max(t.mc);
+          if (lane == 0) {
+            sm.fscr[wid] = Md;
+            sm.fscr[NCW + wid] = Mc;
+          }
+          bar_sync(kBarCompute, NC);
+          Md = sm.fscr[0];
+          Mc = sm.fscr[NCW];
 #pragma unroll
-        for (int q = 1; q < NCW; ++q) {
-          Md = fmaxf(Md, sm.fscr[q]);
-          Mc = fmaxf(Mc, sm.fscr[NCW + q]);
-        }
-        const float sdf = ex2((md - Md) * cd), scf = ex2((mc - Mc) * cc);
-        const float delta = (Mc - mc) * cc - (Md - md) * cd;
-        double ww = wf;
-        if (lf_d > 0.f) ww += (double)lf_d * (double)delta;
-        double v[3] = {(double)lf_d * sdf, (double)lf_c * scf, ww * sdf};
+          for (int q = 1; q < NCW; ++q) {
+            Md = fmaxf(Md, sm.fscr[q]);
+            Mc = fmaxf(Mc, sm.fscr[NCW + q]);
+          }
+          const float sdf = ex2((t.md - Md) * cd), scf = ex2((t.mc - Mc) * cc);
+          const float delta = (Mc - t.mc) * cc - (Md - t.md) * cd;
+          double ww = t.w;
+          if (t.ld > 0.f) ww += (double)t.ld * (double)delta;
+          double v[3] = {(double)t.ld * sdf, (double)t.lc * scf, ww * sdf};
 #pragma unroll
-        for (int k = 0; k < 3; ++k) v[k] = warp_sum_d(v[k]);
-        if (lane == 0)
+          for (int k = 0; k < 3; ++k) v[k] = warp_sum_d(v[k]);
+          if (lane == 0)
 #pragma unroll
-          for (int k = 0; k < 3; ++k) sm.dscr[k * NCW + wid] = v[k];
-        bar_sync(kBarCompute, NC);
-        double *mine = sm.mine[j % 3];
-        if (tid < 3) {
-          double r = 0.0;
-          for (int q = 0; q < NCW; ++q) r += sm.dscr[tid * NCW + q];
-          mine[1 + 2 * tid] = r;  // tid 0 -> L_d [1], 1 -> L_c [3], 2 -> W [5]
+            for (int k = 0; k < 3; ++k) sm.dscr[k * NCW + wid] = v[k];
+          bar_sync(kBarCompute, NC);
+          double *mine = sm.mine[row % 3];
+          if (tid < 3) {
+            double r = 0.0;
+            for (int q = 0; q < NCW; ++q) r += sm.dscr[tid * NCW + q];
+            mine[1 + 2 * tid] = r;  // tid 0 -> L_d [1], 1 -> L_c [3], 2 -> W [5]
+          }
+          if (tid == 0) {
+            mine[0] = Md;
+            mine[2] = Mc;
+          }
+          bar_arrive(bar_p1done(row), NX);  // the exchange warp may push the partial
         }
-        if (tid == 0) {
-          mine[0] = Md;
-          mine[2] = Mc;
+      } else {
+        if (st == 0) {
+          bar_sync(bar_lam(row), NX);  // the exchange warp merged this row
+          lamd = sm.lam[row & 1][0];
+          lamc = sm.lam[row & 1][1];
+          s_acc = 0.f;
         }
-        bar_arrive(bar_p1done(j), NT);  // the control warp may push the partial
+        mbar_wait(&sm.ring_full[slot], (uint32_t)((g / kSlots) & 1));
+        if (lamd == lamd && lamc == lamc) s_acc += p2_stage<T>(sg, sd, sc, cd, cc, lamd, lamc);  // bad rows skip
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.ring_empty[slot]);
+        if (st == nst - 1) {
+          const float sl = warp_sum(s_acc);
+          if (lane == 0) sm.fscr2[wid] = sl;
+          bar_sync(kBarCompute, NC);
+          if (tid == 0) {
+            float r = sm.fscr2[0];
+            for (int q = 1; q < NCW; ++q) r += sm.fscr2[q];
+            sm.s_mine[row & 1] = r;
+          }
+          bar_arrive(bar_p2done(row), NX);
+        }
       }
-      if (j >= 2 && j - 2 < nrows) {  // ---- pass 2 of row j - 2
-        const int64_t r2 = j - 2;
-        bar_sync(bar_lam(r2), NT);  // the control warp merged row j - 2
-        const float lamd = sm.lam[r2 & 1][0], lamc = sm.lam[r2 & 1][1];
-        float sl = 0.f;
-        if (lamd == lamd && lamc == lamc) {  // bad rows skip the S sweep
-          const Chunk<T> ch = chunk_of<T>(a, row_of(r2), rank);
-          sl = pass2_thread<T>(ch, cd, cc, lamd, lamc, pol_last);
+    });
+  } else if (wid == PW) {
+    // ================================================================ producer warp
+    if (lane == 0) {
+      const uint64_t pol_keep = l2_policy_evict_last(), pol_last = l2_policy_evict_first();
+      walk_stages(nrows, nst, [&](int64_t g, int64_t row, int pass, int st) {
+        const int slot = (int)(g % kSlots);
+        if (g >= kSlots) wait_cta(&sm.ring_empty[slot], (uint32_t)(((g / kSlots) - 1) & 1));
+        const Stage<T> sg = stage_of<T>(a, row_of(row), rank, st);  // row = local index
+        T *sd = ring + (size_t)slot * 2 * SE, *sc = sd + SE;
+        if (sg.units > 0) {
+          const uint32_t bytes = (uint32_t)sg.units * 16u;
+          const uint64_t pol = pass == 1 ? pol_keep : pol_last;  // pass 2 is the last use
+          fence_proxy_async();
+          mbar_arrive_expect_tx(&sm.ring_full[slot], 2u * bytes);
+          bulk_g2s_hint(sd, sg.d, bytes, &sm.ring_full[slot], pol);
+          bulk_g2s_hint(sc, sg.c, bytes, &sm.ring_full[slot], pol);
+        } else {
+          mbar_arrive(&sm.ring_full[slot]);  // unaligned / empty stage: read from global
         }
-        sl = warp_sum(sl);
-        if (lane == 0) sm.fscr2[wid] = sl;
-        bar_sync(kBarCompute, NC);
-        if (tid == 0) {
-          float r = sm.fscr2[0];
-          for (int q = 1; q < NCW; ++q) r += sm.fscr2[q];
-          sm.s_mine[r2 & 1] = r;
-        }
-        bar_arrive(bar_p2done(r2), NT);
-      }
+      });
     }
+    __syncwarp();
   } else {
-    // ================================================================ control warp
+    // ================================================================ exchange warp
     for (int64_t j = 0; j <= nrows + 2; ++j) {
       // (1) merge row j - 1's partials (pushed during the peers' iteration j - 1) while the
-      //     compute warps stream; needed by their pass 2 one iteration later
+      //     compute warps stream; their pass 2 of that row starts one iteration later
       if (j >= 1 && j - 1 < nrows) {
         const int64_t r1 = j - 1;
         const int s = (int)(r1 & 1);
@@ -518,23 +551,23 @@ __global__ void __launch_bounds__(kScoreThreads, 2) sv_score_kernel(const ScoreA
           W += __shfl_sync(0xffffffffu, cw, r);
         }
         if (lane == 0) {
-          double *g = sm.glob[r1 % 3];
-          g[0] = GMd;
-          g[1] = L_d;
-          g[2] = GMc;
-          g[3] = L_c;
-          g[4] = W;
+          double *gl = sm.glob[r1 % 3];
+          gl[0] = GMd;
+          gl[1] = L_d;
+          gl[2] = GMc;
+          gl[3] = L_c;
+          gl[4] = W;
           const bool ok = L_d > 0.0 && L_c > 0.0 && L_d < 1e300 && L_c < 1e300 && GMd < FLT_MAX && GMc < FLT_MAX;
           sm.lam[s][0] = ok ? (float)((double)GMd * cd + log2_acc(L_d)) : __int_as_float(0x7fc00000);
           sm.lam[s][1] = ok ? (float)((double)GMc * cc + log2_acc(L_c)) : __int_as_float(0x7fc00000);
         }
         __syncwarp();
-        bar_arrive(bar_lam(r1), NT);
+        bar_arrive(bar_lam(r1), NX);
       }
       // (2) push this CTA's pass-1 partial of row j into slot j % 2 of every peer
       if (j < nrows) {
         const int s = (int)(j & 1);
-        bar_sync(bar_p1done(j), NT);
+        bar_sync(bar_p1done(j), NX);
         if (j >= 2) wait_cluster(&sm.empty_p[s], (uint32_t)(((j >> 1) - 1) & 1));
         if (lane < cs) {
           const double *mine = sm.mine[j % 3];
@@ -549,7 +582,7 @@ __global__ void __launch_bounds__(kScoreThreads, 2) sv_score_kernel(const ScoreA
         const int64_t r2 = j - 2;
         const int s = (int)(r2 & 1);
         const int epi = (int)(r2 % cs);
-        bar_sync(bar_p2done(r2), NT);
+        bar_sync(bar_p2done(r2), NX);
         if (r2 >= 2) wait_cluster(&sm.empty_s[s], (uint32_t)(((r2 >> 1) - 1) & 1));
         if (lane == 0) {
           st_remote_f32(remote(&sm.sarr[s][rank], epi), sm.s_mine[s]);
@@ -578,14 +611,16 @@ __global__ void __launch_bounds__(kScoreThreads, 2) sv_score_kernel(const ScoreA
 
 cudaError_t launch_score(const ScoreArgs &a, cudaStream_t st) {
   const void *fn = a.bf16 ? (const void *)sv_score_kernel<__nv_bfloat16> : (const void *)sv_score_kernel<float>;
-  cudaError_t e = cudaSuccess;
+  const size_t smem = (size_t)kSlots * 2 * kStageBytes;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
   if (a.cs > 8) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(kScoreThreads);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -597,7 +632,7 @@ cudaError_t launch_score(const ScoreArgs &a, cudaStream_t st) {
   // persistent: as many clusters as can be co-resident, never more than rows (clusters are
   // independent, so residency is a performance choice, not a correctness requirement)
   const int64_t rows = (int64_t)a.B * a.k;
-  int64_t ncl = max_active_clusters(fn, cfg, 0, a.cs);
+  int64_t ncl = max_active_clusters(fn, cfg, (int)smem, a.cs);
   static const int mult = tune_knob("SV_SCORE_CLUSTER_MULT", 1);
   ncl *= mult;
   if (ncl > rows) ncl = rows;
