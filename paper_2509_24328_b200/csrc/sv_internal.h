@@ -7,11 +7,11 @@
 
 namespace sv {
 
-// sv_score: 8 compute warps + a producer warp (bulk copies into a kScoreSlots-deep ring of
-// kScoreStageBytes-per-tensor stages) + an exchange warp per CTA
-constexpr int kScoreThreads = 320;
-constexpr int kScoreSlots = 3;
-constexpr int kScoreStageBytes = 16384;
+// sv_score: 8-warp CTAs, kScoreMinBlocks per SM (<= 64 registers), kScoreGroup 16-byte loads
+// per tensor per thread in flight together
+constexpr int kScoreThreads = 256;
+constexpr int kScoreMinBlocks = 5;
+constexpr int kScoreGroup = 2;
 constexpr int kRowsThreads = 256;
 constexpr int kSampleThreads = 256;
 // On-chip budget for the (D, C) [or (T, D)] chunk pair one CTA holds: the cluster size is
