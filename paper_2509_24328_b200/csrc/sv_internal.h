@@ -12,6 +12,10 @@ namespace sv {
 constexpr int kScoreThreads = 256;
 constexpr int kScoreMinBlocks = 5;
 constexpr int kScoreGroup = 2;
+// sd_verify: one cluster per sequence, 8-warp CTAs, kVerifyGroup loads per thread in flight
+constexpr int kVerifyThreads = 256;
+constexpr int kVerifyMinBlocks = 4;
+constexpr int kVerifyGroup = 2;
 constexpr int kRowsThreads = 256;
 constexpr int kSampleThreads = 256;
 // On-chip budget for the (D, C) [or (T, D)] chunk pair one CTA holds: the cluster size is
