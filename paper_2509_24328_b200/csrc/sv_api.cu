@@ -240,8 +240,8 @@ int32_t sd_verify(const sv_logits *draft, const sv_logits *target, const int32_t
   if (!(tau_d > 0.f) || !(tau_t > 0.f)) return SV_ERR_INVALID_ARG;
   if (seq_base < 0) return SV_ERR_INVALID_ARG;
   if (B == 0) return SV_OK;
-  (void)workspace;  // the fused verify kernel needs no workspace (kept in the ABI)
-  (void)workspace_bytes;
+  if (!workspace || workspace_bytes < sv_workspace_bytes(B, k, V, draft->dtype)) return SV_ERR_WORKSPACE;
+  if ((reinterpret_cast<uintptr_t>(workspace) & 15) != 0) return SV_ERR_INVALID_ARG;
   const int eb = elem_bytes(draft->dtype);
   VerifyArgs a = {};
   a.d = draft->ptr;
@@ -268,6 +268,7 @@ int32_t sd_verify(const sv_logits *draft, const sv_logits *target, const int32_t
   a.ratio = accept_ratio;
   a.resid = resid_mass;
   a.status = row_status;
+  a.partials = reinterpret_cast<float2 *>(workspace);
   a.splits = rows_splits_for(V, eb);
   a.rows_chunk = rows_chunk_for(eb);
   a.cs = cluster_size_for(V, eb);

@@ -24,7 +24,7 @@ constexpr int kSampleThreads = 256;
 constexpr int kChunkPairBudget = 80 * 1024;
 constexpr int kMaxCluster = 16;
 // sd_verify phase-1 chunk: 16 x 16-byte loads in flight per thread.
-constexpr int kRowUnitsPerThread = 16;
+constexpr int kRowUnitsPerThread = 8;
 
 int cluster_size_for(int64_t V, int elem_bytes);     // 0 = unsupported
 int tune_knob(const char *name, int dflt);           // integer from the environment (tuning)
