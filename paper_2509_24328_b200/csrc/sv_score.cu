@@ -351,7 +351,7 @@ __device__ __noinline__ void epilogue(const ScoreArgs &a, int64_t row, const dou
 }
 
 template <typename T, int MINB, int G>
-__global__ void __launch_bounds__(kScoreThreads, MINB) sv_score_kernel(const ScoreArgs a) {
+__global__ void __launch_bounds__(kScoreThreads, MINB) sv_score_kernel(const __grid_constant__ ScoreArgs a) {
   __shared__ Smem sm;
   cg::cluster_group cluster = cg::this_cluster();
   const int cs = a.cs;
