@@ -118,7 +118,8 @@ SV_API int32_t sv_cluster_size(int32_t V, int32_t dtype);
  * draft_ptok = p_d(t).  draft_m / draft_l / draft_ptok feed sd_verify.
  * row_status [B, k] int32 or NULL.  Bad rows: S = A = KL = NaN, p_hat = 0.
  * S, A, KL, p_hat may be NULL individually (not computed-out); draft_* may not.
- * Limits: 1 <= k <= 16, 2 <= V, B * k < 2^31, sv_cluster_size(V, dtype) > 0.
+ * Limits: 1 <= k <= 16, 2 <= V, B * sv_cluster_size(V, dtype) < 2^31 (else SV_ERR_UNSUPPORTED),
+ * sv_cluster_size(V, dtype) > 0.
  */
 SV_API int32_t sv_score(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok,
                  int32_t B, int32_t k, int32_t V, float tau_d, float tau_c, const sv_profile *prof,

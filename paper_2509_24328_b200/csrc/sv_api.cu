@@ -1,6 +1,7 @@
 // sv_api.cu -- the C ABI of libsv (include/sv.h): argument validation, launch geometry,
 // workspace carving.  Every entry point only enqueues work on the caller's stream.
 #include <stdio.h>
+#include <stdint.h>
 #include <stdlib.h>
 
 #include <map>
@@ -182,6 +183,7 @@ int32_t sv_score(const sv_logits *draft, const sv_logits *comp, const int32_t *d
   a.bf16 = draft->dtype == SV_BF16;
   a.cs = cluster_size_for(V, elem_bytes(draft->dtype));
   a.chunk = chunk_elems_for(V, a.cs);
+  if ((int64_t)B * a.cs > INT32_MAX) return SV_ERR_UNSUPPORTED;  // grid x = B * cluster size
   cudaError_t e = launch_score(a, (cudaStream_t)stream);
   if (e != cudaSuccess) {
     fprintf(stderr, "libsv: sv_score launch failed: %s\n", cudaGetErrorString(e));

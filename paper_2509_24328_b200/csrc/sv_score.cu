@@ -26,8 +26,7 @@ namespace sv {
 
 namespace {
 
-constexpr int NT = kScoreThreads, NW = NT / 32;
-
+template <int NW>
 struct Smem {
   uint64_t bar_part;            // all cs partials have landed in this CTA (count cs)
   uint64_t bar_s;               // all cs S partials have landed (rank 0; count cs)
@@ -146,8 +145,8 @@ struct Chunk {
   int units;  // 16-byte units (0 when the chunk pair is not 16-byte aligned)
 };
 template <typename T>
-__device__ __forceinline__ Chunk<T> chunk_of(const ScoreArgs &a, int64_t row, int rank) {
-  const int64_t b = row / a.k, i = row % a.k, v0 = (int64_t)rank * a.chunk;
+__device__ __forceinline__ Chunk<T> chunk_of(const ScoreArgs &a, int64_t b, int64_t i, int rank) {
+  const int64_t v0 = (int64_t)rank * a.chunk;
   Chunk<T> ch;
   ch.d = reinterpret_cast<const T *>(a.d) + b * a.d_sb + i * a.d_si + v0;
   ch.c = reinterpret_cast<const T *>(a.c) + b * a.c_sb + i * a.c_si + v0;
@@ -157,31 +156,35 @@ __device__ __forceinline__ Chunk<T> chunk_of(const ScoreArgs &a, int64_t row, in
   return ch;
 }
 
-// pass-1 state of one thread
+// pass-1 state of one thread: true running maxima (md, mc) and the reference maxima (rd, rc)
+// the partial sums are taken against.  The reference moves only when the maximum has grown by
+// more than kLazy (log2 units) -- 2^{a - ref} <= 2^kLazy stays far from fp32 overflow -- so the
+// rescale branch is rare instead of taken on almost every group (lazy rescaling).
 struct P1State {
-  float md, mc, ld, lc, w;
+  float md, mc, rd, rc, ld, lc, w;
 };
+constexpr float kLazy = 8.f;
 
-__device__ __forceinline__ void p1_rescale(P1State &t, float gmd, float gmc, float cd, float cc) {
-  if (gmd > t.md || gmc > t.mc) {  // exact online rescale of the running sums
-    const float sdf = ex2((t.md - gmd) * cd), scf = ex2((t.mc - gmc) * cc);
-    const float delta = (gmc - t.mc) * cc - (gmd - t.md) * cd;
+__device__ __forceinline__ void p1_rescale(P1State &t, float cd, float cc) {
+  if ((t.md - t.rd) * cd > kLazy || (t.mc - t.rc) * cc > kLazy) {  // exact rescale to (md, mc)
+    const float sdf = ex2((t.rd - t.md) * cd), scf = ex2((t.rc - t.mc) * cc);
+    const float delta = (t.mc - t.rc) * cc - (t.md - t.rd) * cd;
     if (t.ld > 0.f) t.w = fmaf(t.ld, delta, t.w);
     t.w *= sdf;
     t.ld *= sdf;
     t.lc *= scf;
-    t.md = gmd;
-    t.mc = gmc;
+    t.rd = t.md;
+    t.rc = t.mc;
   }
 }
 
 // Pass 1 of the thread's share of a chunk: groups of G units per tensor, all loads of a group in
 // flight together, exact online merge between groups; element-wise remainder from global.
-template <typename T, bool kGuard, int G>
+template <typename T, bool kGuard, int NT, int G>
 __device__ __forceinline__ P1State pass1_thread(const Chunk<T> &ch, float cd, float cc, uint64_t pol) {
   constexpr int EPU = Elem<T>::kPerUnit;
   const int tid = threadIdx.x;
-  P1State t{kMFloor, kMFloor, 0.f, 0.f, 0.f};
+  P1State t{kMFloor, kMFloor, kMFloor, kMFloor, 0.f, 0.f, 0.f};
   for (int u0 = tid; u0 < ch.units; u0 += G * NT) {
     uint4 rd[G], rc[G];
 #pragma unroll
@@ -192,15 +195,14 @@ __device__ __forceinline__ P1State pass1_thread(const Chunk<T> &ch, float cd, fl
         rc[q] = ldg_hint(ch.c + (size_t)u * EPU, pol);
       }
     }
-    float gmd = t.md, gmc = t.mc;
 #pragma unroll
     for (int q = 0; q < G; ++q)
       if (u0 + q * NT < ch.units) {
-        gmd = fmaxf(gmd, unit_max<T>(rd[q]));
-        gmc = fmaxf(gmc, unit_max<T>(rc[q]));
+        t.md = fmaxf(t.md, unit_max<T>(rd[q]));
+        t.mc = fmaxf(t.mc, unit_max<T>(rc[q]));
       }
-    p1_rescale(t, gmd, gmc, cd, cc);
-    const float nmd = -t.md * cd, nmc = -t.mc * cc;
+    p1_rescale(t, cd, cc);
+    const float nmd = -t.rd * cd, nmc = -t.rc * cc;
     const f2 cdd{cd, cd}, ccc{cc, cc}, nmdd{nmd, nmd}, nmcc{nmc, nmc};
     P1 acc{{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
 #pragma unroll
@@ -217,13 +219,12 @@ __device__ __forceinline__ P1State pass1_thread(const Chunk<T> &ch, float cd, fl
     t.w += acc.w.x + acc.w.y;
   }
   const int e0 = ch.units * EPU;
-  float gmd = t.md, gmc = t.mc;
   for (int e = e0 + tid; e < ch.n; e += NT) {
-    gmd = fmaxf(gmd, Elem<T>::load(ch.d + e));
-    gmc = fmaxf(gmc, Elem<T>::load(ch.c + e));
+    t.md = fmaxf(t.md, Elem<T>::load(ch.d + e));
+    t.mc = fmaxf(t.mc, Elem<T>::load(ch.c + e));
   }
-  p1_rescale(t, gmd, gmc, cd, cc);
-  const float nmd = -t.md * cd, nmc = -t.mc * cc;
+  p1_rescale(t, cd, cc);
+  const float nmd = -t.rd * cd, nmc = -t.rc * cc;
   for (int e = e0 + tid; e < ch.n; e += NT) {
     const float ad = fmaf(Elem<T>::load(ch.d + e), cd, nmd), ac = fmaf(Elem<T>::load(ch.c + e), cc, nmc);
     const float ed = ex2(ad);
@@ -235,7 +236,7 @@ __device__ __forceinline__ P1State pass1_thread(const Chunk<T> &ch, float cd, fl
 }
 
 // Pass 2 of the thread's share of a chunk (L2 re-read): its S partial.
-template <typename T, int G>
+template <typename T, int NT, int G>
 __device__ __forceinline__ float pass2_thread(const Chunk<T> &ch, float cd, float cc, float lamd, float lamc,
                                               uint64_t pol) {
   constexpr int EPU = Elem<T>::kPerUnit;
@@ -274,8 +275,9 @@ __device__ __forceinline__ float pass2_thread(const Chunk<T> &ch, float cd, floa
 // fp64 range reduction + fp32 transcendentals).  The draft-side outputs depend on the draft row
 // alone: a bad companion row does not poison them.
 template <typename T>
-__device__ __noinline__ void epilogue(const ScoreArgs &a, int64_t row, const double *glob, const float *sarr,
-                                      int cs) {
+__device__ __noinline__ void epilogue(const ScoreArgs &a, int64_t b, int64_t i, const double *glob,
+                                      const float *sarr, int cs) {
+  const int64_t row = b * a.k + i;
   const int lane = threadIdx.x & 31;
   const float cd = a.cd, cc = a.cc;
   const float GMd = (float)glob[0], GMc = (float)glob[2];
@@ -285,7 +287,6 @@ __device__ __noinline__ void epilogue(const ScoreArgs &a, int64_t row, const dou
     return (L > 0.0) ? 0 : 2;                                  /*SV_ROW_ALL_NEG_INF*/
   };
   const int d_st = row_bits(L_d, GMd), c_st = row_bits(L_c, GMc);
-  const int64_t b = row / a.k, i = row % a.k;
   const int32_t t = a.tok[row];
   const bool tok_ok = t >= 0 && t < a.V;
   int st = d_st | c_st | (tok_ok ? 0 : 4 /*SV_ROW_BAD_TOKEN*/);
@@ -350,10 +351,22 @@ __device__ __noinline__ void epilogue(const ScoreArgs &a, int64_t row, const dou
   }
 }
 
-template <typename T, int MINB, int G>
-__global__ void __launch_bounds__(kScoreThreads, MINB) sv_score_kernel(const __grid_constant__ ScoreArgs a) {
-  __shared__ Smem sm;
-  cg::cluster_group cluster = cg::this_cluster();
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+// grid (B * cs, k), cluster (cs, 1, 1): cluster x-index = b, blockIdx.y = i -- no divisions.
+template <typename T, int NT, int MINB, int G>
+__global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constant__ ScoreArgs a) {
+  constexpr int NW = NT / 32;
+  __shared__ Smem<NW> sm;
   const int cs = a.cs;
   if (threadIdx.x == 0) {
     mbar_init(&sm.bar_part, cs);
@@ -362,18 +375,18 @@ __global__ void __launch_bounds__(kScoreThreads, MINB) sv_score_kernel(const __g
   }
   __syncthreads();
   cluster_arrive_relaxed();  // (0) started, barriers initialised: peers may push after wait (0)
-  const int rank = (int)cluster.block_rank();
-  const int64_t row = blockIdx.x / cs;
+  const int rank = (int)cluster_ctarank();
+  const int64_t bb = cluster_id_x(), ii = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const bool ctl = wid == NW - 1;  // serial work on the highest warp id
   const float cd = a.cd, cc = a.cc;
-  const Chunk<T> ch = chunk_of<T>(a, row, rank);
+  const Chunk<T> ch = chunk_of<T>(a, bb, ii, rank);
 
   // ---- pass 1 (HBM)
   const uint64_t pol_keep = l2_policy_evict_last();
-  P1State t = pass1_thread<T, false, G>(ch, cd, cc, pol_keep);
+  P1State t = pass1_thread<T, false, NT, G>(ch, cd, cc, pol_keep);
   if (t.w != t.w && t.ld == t.ld && t.lc == t.lc)  // 0 * (-inf) from masked logits: guarded redo
-    t = pass1_thread<T, true, G>(ch, cd, cc, pol_keep);
+    t = pass1_thread<T, true, NT, G>(ch, cd, cc, pol_keep);
 
   // ---- block merge (fixed warp / lane order)
   float Md = warp_max(t.md), Mc = warp_max(t.mc);
@@ -390,8 +403,8 @@ __global__ void __launch_bounds__(kScoreThreads, MINB) sv_score_kernel(const __g
     Mc = fmaxf(Mc, sm.fscr[NW + q]);
   }
   {
-    const float sdf = ex2((t.md - Md) * cd), scf = ex2((t.mc - Mc) * cc);
-    const float delta = (Mc - t.mc) * cc - (Md - t.md) * cd;
+    const float sdf = ex2((t.rd - Md) * cd), scf = ex2((t.rc - Mc) * cc);
+    const float delta = (Mc - t.rc) * cc - (Md - t.rd) * cd;
     double ww = t.w;
     if (t.ld > 0.f) ww += (double)t.ld * (double)delta;
     double v[3] = {(double)t.ld * sdf, (double)t.lc * scf, ww * sdf};
@@ -454,7 +467,7 @@ __global__ void __launch_bounds__(kScoreThreads, MINB) sv_score_kernel(const __g
   // ---- pass 2 (L2 re-read; bad rows skip it)
   const float lamd = sm.lam[0], lamc = sm.lam[1];
   float s_loc = 0.f;
-  if (lamd == lamd && lamc == lamc) s_loc = pass2_thread<T, G>(ch, cd, cc, lamd, lamc, l2_policy_evict_first());
+  if (lamd == lamd && lamc == lamc) s_loc = pass2_thread<T, NT, G>(ch, cd, cc, lamd, lamc, l2_policy_evict_first());
   s_loc = warp_sum(s_loc);
   if (lane == 0) sm.fscr[wid] = s_loc;
   __syncthreads();
@@ -467,21 +480,21 @@ __global__ void __launch_bounds__(kScoreThreads, MINB) sv_score_kernel(const __g
   // Ranks != 0 may exit now: every push INTO them completed before their bar_part wait.
   if (rank == 0 && ctl) {
     wait_cluster(&sm.bar_s, 0);
-    epilogue<T>(a, row, sm.glob, sm.sarr, cs);
+    epilogue<T>(a, bb, ii, sm.glob, sm.sarr, cs);
   }
 }
 
-template <typename T, int MINB, int G>
+template <typename T, int NT, int MINB, int G>
 cudaError_t launch_score_t(const ScoreArgs &a, cudaStream_t st) {
-  const void *fn = (const void *)sv_score_kernel<T, MINB, G>;
+  const void *fn = (const void *)sv_score_kernel<T, NT, MINB, G>;
   cudaError_t e = cudaSuccess;
   if (a.cs > 8) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)((int64_t)a.B * a.k * a.cs));
-  cfg.blockDim = dim3(kScoreThreads);
+  cfg.gridDim = dim3((unsigned)((int64_t)a.B * a.cs), (unsigned)a.k);
+  cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -491,7 +504,7 @@ cudaError_t launch_score_t(const ScoreArgs &a, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, sv_score_kernel<T, MINB, G>, a);
+  return cudaLaunchKernelEx(&cfg, sv_score_kernel<T, NT, MINB, G>, a);
 }
 
 template <typename T>
@@ -499,11 +512,11 @@ cudaError_t launch_score_cfg(const ScoreArgs &a, cudaStream_t st) {
   // CTAs per SM (register budget) x loads in flight per thread; SV_SCORE_CFG overrides (tuning)
   static const int cfg = tune_knob("SV_SCORE_CFG", 0);
   switch (cfg) {
-    case 1: return launch_score_t<T, 5, 2>(a, st);
-    case 2: return launch_score_t<T, 6, 1>(a, st);
-    case 3: return launch_score_t<T, 4, 2>(a, st);
-    case 4: return launch_score_t<T, 3, 4>(a, st);
-    default: return launch_score_t<T, kScoreMinBlocks, kScoreGroup>(a, st);
+    case 1: return launch_score_t<T, 256, 5, 2>(a, st);
+    case 2: return launch_score_t<T, 128, 10, 2>(a, st);
+    case 3: return launch_score_t<T, 128, 12, 1>(a, st);
+    case 4: return launch_score_t<T, 256, 4, 2>(a, st);
+    default: return launch_score_t<T, kScoreThreads, kScoreMinBlocks, kScoreGroup>(a, st);
   }
 }
 
