@@ -89,7 +89,10 @@ typedef struct {
 } sv_profile;
 
 /* Bytes of device workspace needed by sv_score / sv_schedule / sd_verify for this shape
- * (one buffer may be shared by consecutive calls on one stream). */
+ * (one buffer may be shared by consecutive calls on one stream, 16-byte aligned).
+ * The buffer must be ZERO-FILLED before its first use (sv_score keeps per-row completion
+ * counters in it and leaves them zero when it finishes); it must not be used by two calls
+ * that run concurrently.  After a failed / aborted kernel, zero it again. */
 SV_API size_t sv_workspace_bytes(int32_t B, int32_t k, int32_t V, int32_t dtype);
 
 /* Human-readable text of a status code (static storage). */

@@ -30,6 +30,12 @@ int cluster_size_for(int64_t V, int elem_bytes) {
   return 0;
 }
 
+int score_splits_for(int64_t V) {
+  static const int target = tune_knob("SV_SCORE_CHUNK", kScoreChunk);
+  const int64_t s = (V + target - 1) / target;
+  return (int)(s < 1 ? 1 : (s > kScoreMaxSplits ? kScoreMaxSplits : s));
+}
+
 int64_t chunk_elems_for(int64_t V, int cs) {
   const int64_t c = (V + cs - 1) / cs;
   return (c + 15) / 16 * 16;
@@ -87,6 +93,10 @@ static int64_t rows_chunk_for(int elem_bytes) {
   return (int64_t)kRowsThreads * kRowUnitsPerThread * (16 / elem_bytes);
 }
 
+int64_t score_ws_bytes(int64_t rows, int cs) {
+  return ws_round(rows * cs * 5 * 8) + ws_round(rows * cs * 4) + ws_round(rows * 2 * 4);
+}
+
 }  // namespace sv
 
 using namespace sv;
@@ -95,7 +105,10 @@ static bool dtype_ok(int32_t d) { return d == SV_F32 || d == SV_BF16; }
 static int elem_bytes(int32_t d) { return d == SV_BF16 ? 2 : 4; }
 
 // sd_verify's partials follow sv_score's region, so one workspace serves both calls
-static int64_t verify_ws_offset(int32_t, int32_t, int32_t, int) { return 0; }
+static int64_t verify_ws_offset(int32_t B, int32_t k, int32_t V, int eb) {
+  (void)eb;
+  return score_ws_bytes((int64_t)B * k, score_splits_for(V));
+}
 
 static int32_t shape_check(int32_t B, int32_t k, int32_t V, int32_t dtype) {
   if (B < 0 || k < 1 || k > SV_MAX_K || V < 2) return SV_ERR_INVALID_ARG;
@@ -149,9 +162,9 @@ int32_t sv_score(const sv_logits *draft, const sv_logits *comp, const int32_t *d
   if (p_hat && (!prof || !prof->s_edges || !prof->a_edges || !prof->cells || prof->n_s < 1 || prof->n_a < 1 ||
                 prof->n_s > 64 || prof->n_a > 64))
     return SV_ERR_INVALID_ARG;
-  (void)workspace;  // sv_score needs no workspace (kept in the ABI for future variants)
-  (void)workspace_bytes;
   if (B == 0) return SV_OK;
+  if (!workspace || workspace_bytes < sv_workspace_bytes(B, k, V, draft->dtype)) return SV_ERR_WORKSPACE;
+  if ((reinterpret_cast<uintptr_t>(workspace) & 15) != 0) return SV_ERR_INVALID_ARG;
   ScoreArgs a = {};
   a.d = draft->ptr;
   a.c = comp->ptr;
@@ -181,9 +194,16 @@ int32_t sv_score(const sv_logits *draft, const sv_logits *comp, const int32_t *d
   a.dpt = draft_ptok;
   a.status = row_status;
   a.bf16 = draft->dtype == SV_BF16;
-  a.cs = cluster_size_for(V, elem_bytes(draft->dtype));
+  a.cs = score_splits_for(V);
   a.chunk = chunk_elems_for(V, a.cs);
-  if ((int64_t)B * a.cs > INT32_MAX) return SV_ERR_UNSUPPORTED;  // grid x = B * cluster size
+  const int64_t rows = (int64_t)B * k;
+  if (2 * rows * a.cs > INT32_MAX) return SV_ERR_UNSUPPORTED;  // one CTA per chunk task
+  static const int lag = tune_knob("SV_SCORE_LAG", kScoreLag);
+  a.lead = (rows < lag ? rows : (int64_t)lag) * a.cs;
+  uint8_t *ws = reinterpret_cast<uint8_t *>(workspace);
+  a.part = reinterpret_cast<double *>(ws);
+  a.spart = reinterpret_cast<float *>(ws + ws_round(rows * a.cs * 5 * 8));
+  a.cnt = reinterpret_cast<uint32_t *>(ws + ws_round(rows * a.cs * 5 * 8) + ws_round(rows * a.cs * 4));
   cudaError_t e = launch_score(a, (cudaStream_t)stream);
   if (e != cudaSuccess) {
     fprintf(stderr, "libsv: sv_score launch failed: %s\n", cudaGetErrorString(e));
@@ -270,7 +290,7 @@ int32_t sd_verify(const sv_logits *draft, const sv_logits *target, const int32_t
   a.ratio = accept_ratio;
   a.resid = resid_mass;
   a.status = row_status;
-  a.partials = reinterpret_cast<float2 *>(workspace);
+  a.partials = reinterpret_cast<float2 *>(reinterpret_cast<uint8_t *>(workspace) + verify_ws_offset(B, k, V, eb));
   a.splits = rows_splits_for(V, eb);
   a.rows_chunk = rows_chunk_for(eb);
   a.cs = cluster_size_for(V, eb);

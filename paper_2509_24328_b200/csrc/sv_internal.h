@@ -7,11 +7,14 @@
 
 namespace sv {
 
-// sv_score: 8-warp CTAs, kScoreMinBlocks per SM (<= 64 registers), kScoreGroup 16-byte loads
-// per tensor per thread in flight together
+// sv_score: 8-warp CTAs, kScoreMinBlocks per SM (<= 48 registers), kScoreGroup 16-byte loads
+// per tensor per thread in flight together; kScoreLag rows between a chunk's two reads
 constexpr int kScoreThreads = 256;
 constexpr int kScoreMinBlocks = 5;
 constexpr int kScoreGroup = 2;
+constexpr int kScoreLag = 64;
+constexpr int kScoreChunk = 32768;  // target elements per chunk task (per tensor)
+constexpr int kScoreMaxSplits = 32;
 // sd_verify: one cluster per sequence, 8-warp CTAs, kVerifyGroup loads per thread in flight
 constexpr int kVerifyThreads = 256;
 constexpr int kVerifyMinBlocks = 4;
@@ -27,6 +30,7 @@ constexpr int kMaxCluster = 16;
 constexpr int kRowUnitsPerThread = 8;
 
 int cluster_size_for(int64_t V, int elem_bytes);     // 0 = unsupported
+int score_splits_for(int64_t V);                     // sv_score chunks per row
 int tune_knob(const char *name, int dflt);           // integer from the environment (tuning)
 int64_t chunk_elems_for(int64_t V, int cs);          // per-CTA elements (multiple of 16)
 int64_t rows_splits_for(int64_t V, int elem_bytes);  // sd_verify phase-1 CTAs per row
@@ -47,10 +51,16 @@ struct ScoreArgs {
   int32_t n_s, n_a;
   float *S, *A, *KL, *p_hat, *dm, *dl, *dpt;
   int32_t *status;
-  int64_t chunk;  // elements per CTA (per tensor)
-  int cs;         // cluster size
+  int64_t chunk;  // elements per chunk task (per tensor)
+  int cs;         // chunks per row
   int bf16;
+  int64_t lead;     // leading P1 tasks before P1 / P2 alternate (= min(lag, B k) * cs)
+  double *part;     // workspace: [B k cs][5] P1 partials (M_d, L_d, M_c, L_c, W)
+  float *spart;     // workspace: [B k cs] S partials
+  uint32_t *cnt;    // workspace: [B k][2] counters, zero between calls (self-cleaning)
 };
+// sv_score's share of the workspace (offset 0); sd_verify's follows it
+int64_t score_ws_bytes(int64_t rows, int cs);
 cudaError_t launch_score(const ScoreArgs &a, cudaStream_t st);
 
 struct ScheduleArgs {

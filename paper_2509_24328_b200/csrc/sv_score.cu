@@ -1,22 +1,25 @@
 // sv_score.cu -- K1: steps a1-a3 of the SV hot path (P L159 S/A, P L164 divergence,
 // north_star KL, P L176 profile lookup).
 //
-// Design (DESIGN.md §5 K1).  One thread-block CLUSTER of cs CTAs per (b, i); CTA r owns the
-// vocabulary chunk [r*chunk, (r+1)*chunk) of the draft AND the companion row.  CTAs are small
-// (8 warps, no shared-memory staging of the data, <= 64 registers) so that 4 of them -- 32
-// warps -- share an SM: the exp-heavy reductions are latency bound and need the warps.
-//   pass 1  : stream the chunk pair from HBM (16-byte loads, L2 evict_last, kScoreGroup units
-//             per tensor in flight per thread), thread maxima (packed bf16x2 max),
-//             l = sum 2^{(x - m) log2e / tau} and the KL partial w = sum e_d (a_d - a_c) with
-//             packed FFMA2 / FADD2 and an exact online merge between groups
-//   merge   : block merge in fixed warp order; the last warp (highest id: favoured by the warp
-//             arbiter) pushes the 5 partials into every CTA of the cluster over DSMEM, one
-//             cluster barrier, then merges them in rank order (identical bits everywhere)
-//   pass 2  : re-read the same chunk pair -- an L2 hit (evict_first: last use) -- and sum
-//             S_r = sum 2^{min(x_d c_d - Lambda_d, x_c c_c - Lambda_c)}; push S_r to rank 0
-//   epilogue: rank 0's last warp: S, A, KL, profile lookup, draft normalisers for sd_verify.
-// HBM traffic is one read of D and C.  The cluster size and chunking depend on (V, dtype) only,
-// so every reduction order -- and every output bit -- is independent of B and of the GPU count.
+// Design (DESIGN.md §5 K1): a DECOUPLED two-phase kernel, no clusters.  Row (b, i) is split into
+// cs vocabulary chunks; each chunk is two CTA tasks:
+//   P1(row, r): stream the chunk pair from HBM (16-byte loads, L2 evict_last) -- thread maxima
+//             (packed bf16x2 max), l = sum 2^{(x - m) log2e / tau} and the KL partial
+//             w = sum e_d (a_d - a_c) with packed FFMA2 / FADD2, lazy online rescaling -- block
+//             merge in fixed warp order, publish (M_d, L_d, M_c, L_c, W) to the workspace and
+//             bump the row's counter (release).
+//   P2(row, r): wait for the row's cs P1 partials (acquire; they were issued ~lag rows earlier,
+//             so the wait is normally already satisfied), merge them in chunk order, re-read
+//             the chunk pair -- an L2 hit (evict_first: last use) -- and sum
+//             S_r = sum 2^{min(x_d c_d - Lambda_d, x_c c_c - Lambda_c)}; publish S_r.  The
+//             row's last P2 task (r = cs - 1) waits for the other cs - 1 S partials and runs
+//             the epilogue (S, A, KL, profile lookup, draft normalisers for sd_verify), then
+//             zeroes the row's counters for the next call (self-cleaning workspace).
+// Task order interleaves P1 of row j + lag with P2 of row j, so the L2 holds ~lag rows between
+// a chunk's two reads, no CTA ever idles at a cluster barrier, and a P2 task only waits on tasks
+// with LOWER linear block indices (which the hardware dispatches first: forward progress).
+// HBM traffic is one read of D and C.  cs and the chunking depend on (V, dtype) only, so every
+// reduction order -- and every output bit -- is independent of B and of the GPU count.
 #include <float.h>
 
 #include "sv_device.cuh"
@@ -28,50 +31,11 @@ namespace {
 
 template <int NW>
 struct Smem {
-  uint64_t bar_part;            // all cs partials have landed in this CTA (count cs)
-  uint64_t bar_s;               // all cs S partials have landed (rank 0; count cs)
-  double part[kMaxCluster][5];  // (M_d, L_d, M_c, L_c, W) pushed by every rank of the cluster
-  float sarr[kMaxCluster];      // S partials (valid in rank 0)
-  double glob[5];               // merged (M_d, L_d, M_c, L_c, W)
-  float lam[2];                 // Lambda_d, Lambda_c
+  double glob[5];  // merged (M_d, L_d, M_c, L_c, W)
+  float lam[2];    // Lambda_d, Lambda_c
   float fscr[2 * NW];
   double dscr[3 * NW];
 };
-
-// relaxed arrive: no MEMBAR.GPU (the only thing published through this barrier is "started,
-// mbarriers initialised", which fence.mbarrier_init orders)
-__device__ __forceinline__ void cluster_arrive_relaxed() {
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void cluster_wait() {
-  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
-__device__ __forceinline__ uint32_t remote(const void *p, int rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void remote_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void st_remote_f64(uint32_t addr, double v) {
-  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
-}
-__device__ __forceinline__ void st_remote_f32(uint32_t addr, float v) {
-  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
-}
-__device__ __forceinline__ void wait_cluster(uint64_t *bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "W_%=:\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra W_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
 
 __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   uint64_t p;
@@ -89,6 +53,17 @@ __device__ __forceinline__ uint4 ldg_hint(const void *p, uint64_t pol) {
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p), "l"(pol));
   return r;
+}
+__device__ __forceinline__ void red_release_add(uint32_t *p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void wait_count(const uint32_t *p, uint32_t target) {
+  while (ld_acquire(p) < target) __nanosleep(100);
 }
 
 // ---------------------------------------------------------------- element arithmetic
@@ -178,45 +153,52 @@ __device__ __forceinline__ void p1_rescale(P1State &t, float cd, float cc) {
   }
 }
 
-// Pass 1 of the thread's share of a chunk: groups of G units per tensor, all loads of a group in
-// flight together, exact online merge between groups; element-wise remainder from global.
+// One group of g units per tensor (loads already in registers): maxima, lazy rescale, sums.
+template <typename T, bool kGuard, int g>
+__device__ __forceinline__ void p1_group(P1State &t, const uint4 (&rd)[g], const uint4 (&rc)[g], float cd, float cc) {
+  constexpr int EPU = Elem<T>::kPerUnit;
+#pragma unroll
+  for (int q = 0; q < g; ++q) {
+    t.md = fmaxf(t.md, unit_max<T>(rd[q]));
+    t.mc = fmaxf(t.mc, unit_max<T>(rc[q]));
+  }
+  p1_rescale(t, cd, cc);
+  const float nmd = -t.rd * cd, nmc = -t.rc * cc;
+  const f2 cdd{cd, cd}, ccc{cc, cc}, nmdd{nmd, nmd}, nmcc{nmc, nmc};
+  P1 acc{{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+#pragma unroll
+  for (int q = 0; q < g; ++q) {
+    f2 xd[EPU / 2], xc[EPU / 2];
+    unit_pairs<T>(rd[q], xd);
+    unit_pairs<T>(rc[q], xc);
+#pragma unroll
+    for (int p = 0; p < EPU / 2; ++p) p1_pair<kGuard>(xd[p], xc[p], cdd, ccc, nmdd, nmcc, acc);
+  }
+  t.ld += acc.ld.x + acc.ld.y;
+  t.lc += acc.lc.x + acc.lc.y;
+  t.w += acc.w.x + acc.w.y;
+}
+
+// Pass 1 of the thread's share of a chunk: full groups of G units per tensor (all loads of a
+// group in flight together, no per-unit guards), then single units, then the element tail.
 template <typename T, bool kGuard, int NT, int G>
 __device__ __forceinline__ P1State pass1_thread(const Chunk<T> &ch, float cd, float cc, uint64_t pol) {
   constexpr int EPU = Elem<T>::kPerUnit;
   const int tid = threadIdx.x;
   P1State t{kMFloor, kMFloor, kMFloor, kMFloor, 0.f, 0.f, 0.f};
-  for (int u0 = tid; u0 < ch.units; u0 += G * NT) {
+  int u0 = tid;
+  for (; u0 + (G - 1) * NT < ch.units; u0 += G * NT) {
     uint4 rd[G], rc[G];
 #pragma unroll
     for (int q = 0; q < G; ++q) {
-      const int u = u0 + q * NT;
-      if (u < ch.units) {
-        rd[q] = ldg_hint(ch.d + (size_t)u * EPU, pol);
-        rc[q] = ldg_hint(ch.c + (size_t)u * EPU, pol);
-      }
+      rd[q] = ldg_hint(ch.d + (size_t)(u0 + q * NT) * EPU, pol);
+      rc[q] = ldg_hint(ch.c + (size_t)(u0 + q * NT) * EPU, pol);
     }
-#pragma unroll
-    for (int q = 0; q < G; ++q)
-      if (u0 + q * NT < ch.units) {
-        t.md = fmaxf(t.md, unit_max<T>(rd[q]));
-        t.mc = fmaxf(t.mc, unit_max<T>(rc[q]));
-      }
-    p1_rescale(t, cd, cc);
-    const float nmd = -t.rd * cd, nmc = -t.rc * cc;
-    const f2 cdd{cd, cd}, ccc{cc, cc}, nmdd{nmd, nmd}, nmcc{nmc, nmc};
-    P1 acc{{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
-#pragma unroll
-    for (int q = 0; q < G; ++q)
-      if (u0 + q * NT < ch.units) {
-        f2 xd[EPU / 2], xc[EPU / 2];
-        unit_pairs<T>(rd[q], xd);
-        unit_pairs<T>(rc[q], xc);
-#pragma unroll
-        for (int p = 0; p < EPU / 2; ++p) p1_pair<kGuard>(xd[p], xc[p], cdd, ccc, nmdd, nmcc, acc);
-      }
-    t.ld += acc.ld.x + acc.ld.y;
-    t.lc += acc.lc.x + acc.lc.y;
-    t.w += acc.w.x + acc.w.y;
+    p1_group<T, kGuard, G>(t, rd, rc, cd, cc);
+  }
+  for (; u0 < ch.units; u0 += NT) {
+    uint4 rd[1] = {ldg_hint(ch.d + (size_t)u0 * EPU, pol)}, rc[1] = {ldg_hint(ch.c + (size_t)u0 * EPU, pol)};
+    p1_group<T, kGuard, 1>(t, rd, rc, cd, cc);
   }
   const int e0 = ch.units * EPU;
   for (int e = e0 + tid; e < ch.n; e += NT) {
@@ -235,6 +217,23 @@ __device__ __forceinline__ P1State pass1_thread(const Chunk<T> &ch, float cd, fl
   return t;
 }
 
+template <typename T, int g>
+__device__ __forceinline__ void p2_group(f2 &acc, const uint4 (&rd)[g], const uint4 (&rc)[g], f2 cdd, f2 ccc, f2 ld2,
+                                         f2 lc2) {
+  constexpr int EPU = Elem<T>::kPerUnit;
+#pragma unroll
+  for (int q = 0; q < g; ++q) {
+    f2 xd[EPU / 2], xc[EPU / 2];
+    unit_pairs<T>(rd[q], xd);
+    unit_pairs<T>(rc[q], xc);
+#pragma unroll
+    for (int p = 0; p < EPU / 2; ++p) {
+      const f2 ad = fma2(xd[p], cdd, ld2), ac = fma2(xc[p], ccc, lc2);
+      acc = add2(acc, f2{ex2(fminf(ad.x, ac.x)), ex2(fminf(ad.y, ac.y))});
+    }
+  }
+}
+
 // Pass 2 of the thread's share of a chunk (L2 re-read): its S partial.
 template <typename T, int NT, int G>
 __device__ __forceinline__ float pass2_thread(const Chunk<T> &ch, float cd, float cc, float lamd, float lamc,
@@ -243,28 +242,19 @@ __device__ __forceinline__ float pass2_thread(const Chunk<T> &ch, float cd, floa
   const int tid = threadIdx.x;
   const f2 cdd{cd, cd}, ccc{cc, cc}, ld2{-lamd, -lamd}, lc2{-lamc, -lamc};
   f2 acc{0.f, 0.f};
-  for (int u0 = tid; u0 < ch.units; u0 += G * NT) {
+  int u0 = tid;
+  for (; u0 + (G - 1) * NT < ch.units; u0 += G * NT) {
     uint4 rd[G], rc[G];
 #pragma unroll
     for (int q = 0; q < G; ++q) {
-      const int u = u0 + q * NT;
-      if (u < ch.units) {
-        rd[q] = ldg_hint(ch.d + (size_t)u * EPU, pol);
-        rc[q] = ldg_hint(ch.c + (size_t)u * EPU, pol);
-      }
+      rd[q] = ldg_hint(ch.d + (size_t)(u0 + q * NT) * EPU, pol);
+      rc[q] = ldg_hint(ch.c + (size_t)(u0 + q * NT) * EPU, pol);
     }
-#pragma unroll
-    for (int q = 0; q < G; ++q)
-      if (u0 + q * NT < ch.units) {
-        f2 xd[EPU / 2], xc[EPU / 2];
-        unit_pairs<T>(rd[q], xd);
-        unit_pairs<T>(rc[q], xc);
-#pragma unroll
-        for (int p = 0; p < EPU / 2; ++p) {
-          const f2 ad = fma2(xd[p], cdd, ld2), ac = fma2(xc[p], ccc, lc2);
-          acc = add2(acc, f2{ex2(fminf(ad.x, ac.x)), ex2(fminf(ad.y, ac.y))});
-        }
-      }
+    p2_group<T, G>(acc, rd, rc, cdd, ccc, ld2, lc2);
+  }
+  for (; u0 < ch.units; u0 += NT) {
+    uint4 rd[1] = {ldg_hint(ch.d + (size_t)u0 * EPU, pol)}, rc[1] = {ldg_hint(ch.c + (size_t)u0 * EPU, pol)};
+    p2_group<T, 1>(acc, rd, rc, cdd, ccc, ld2, lc2);
   }
   for (int e = ch.units * EPU + tid; e < ch.n; e += NT)
     acc.x += ex2(fminf(fmaf(Elem<T>::load(ch.d + e), cd, -lamd), fmaf(Elem<T>::load(ch.c + e), cc, -lamc)));
@@ -276,7 +266,7 @@ __device__ __forceinline__ float pass2_thread(const Chunk<T> &ch, float cd, floa
 // alone: a bad companion row does not poison them.
 template <typename T>
 __device__ __noinline__ void epilogue(const ScoreArgs &a, int64_t b, int64_t i, const double *glob,
-                                      const float *sarr, int cs) {
+                                      const float *sarr, int cs) {  // sarr: global, this row's S partials
   const int64_t row = b * a.k + i;
   const int lane = threadIdx.x & 31;
   const float cd = a.cd, cc = a.cc;
@@ -311,7 +301,7 @@ __device__ __noinline__ void epilogue(const ScoreArgs &a, int64_t b, int64_t i, 
   }
   if (lane == 2 && !st) piece = log2_acc(L_d) - log2_acc(L_c);
   if (lane == 3)
-    for (int r = 0; r < cs; ++r) piece += (double)sarr[r];
+    for (int r = 0; r < cs; ++r) piece += (double)__ldcg(sarr + r);
   const double argd = __shfl_sync(0xffffffffu, piece, 0);
   double piece2 = 0.0;  // lane 0: p_d(t); lane 1: p_c(t) / p_d(t)
   if (lane == 0 && !d_st && tok_ok) piece2 = exp2_acc(argd);
@@ -351,93 +341,104 @@ __device__ __noinline__ void epilogue(const ScoreArgs &a, int64_t b, int64_t i, 
   }
 }
 
-__device__ __forceinline__ uint32_t cluster_id_x() {
-  uint32_t r;
-  asm("mov.u32 %0, %%clusterid.x;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
+// Task t of the 2 * R * cs tasks (R = B * k rows; < 2^31): E = min(lag, R) * cs leading P1 tasks,
+// then P1 and P2 tasks alternate, then the remaining P2 tasks.  Returns the chunk-task index q
+// (row = q / cs) and whether it is a P2 task.
+__device__ __forceinline__ void decode_task(uint32_t t, uint32_t RC, uint32_t E, uint32_t &q, bool &p2) {
+  if (t < E) {
+    q = t;
+    p2 = false;
+    return;
+  }
+  const uint32_t j = t - E, mid = 2 * (RC - E);
+  if (j < mid) {
+    p2 = (j & 1) != 0;
+    q = p2 ? (j >> 1) : E + (j >> 1);
+  } else {
+    p2 = true;
+    q = RC - E + (j - mid);
+  }
 }
 
-// grid (B * cs, k), cluster (cs, 1, 1): cluster x-index = b, blockIdx.y = i -- no divisions.
 template <typename T, int NT, int MINB, int G>
 __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constant__ ScoreArgs a) {
   constexpr int NW = NT / 32;
   __shared__ Smem<NW> sm;
   const int cs = a.cs;
-  if (threadIdx.x == 0) {
-    mbar_init(&sm.bar_part, cs);
-    mbar_init(&sm.bar_s, cs);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  cluster_arrive_relaxed();  // (0) started, barriers initialised: peers may push after wait (0)
-  const int rank = (int)cluster_ctarank();
-  const int64_t bb = cluster_id_x(), ii = blockIdx.y;
+  const uint32_t RC = (uint32_t)a.B * (uint32_t)a.k * (uint32_t)cs;
+  uint32_t q;
+  bool p2;
+  decode_task(blockIdx.x, RC, (uint32_t)a.lead, q, p2);
+  const uint32_t row = q / (uint32_t)cs;
+  const int rank = (int)(q - row * cs);
+  const uint32_t bb = row / (uint32_t)a.k, ii = row - bb * a.k;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const bool ctl = wid == NW - 1;  // serial work on the highest warp id
+  const bool ctl = wid == NW - 1;  // serial work on the highest warp id (favoured by the arbiter)
   const float cd = a.cd, cc = a.cc;
   const Chunk<T> ch = chunk_of<T>(a, bb, ii, rank);
+  uint32_t *cnt = a.cnt + 2 * (size_t)row;  // [0] P1 partials published, [1] S partials published
 
-  // ---- pass 1 (HBM)
-  const uint64_t pol_keep = l2_policy_evict_last();
-  P1State t = pass1_thread<T, false, NT, G>(ch, cd, cc, pol_keep);
-  if (t.w != t.w && t.ld == t.ld && t.lc == t.lc)  // 0 * (-inf) from masked logits: guarded redo
-    t = pass1_thread<T, true, NT, G>(ch, cd, cc, pol_keep);
-
-  // ---- block merge (fixed warp / lane order)
-  float Md = warp_max(t.md), Mc = warp_max(t.mc);
-  if (lane == 0) {
-    sm.fscr[wid] = Md;
-    sm.fscr[NW + wid] = Mc;
-  }
-  __syncthreads();
-  Md = sm.fscr[0];
-  Mc = sm.fscr[NW];
-#pragma unroll
-  for (int q = 1; q < NW; ++q) {
-    Md = fmaxf(Md, sm.fscr[q]);
-    Mc = fmaxf(Mc, sm.fscr[NW + q]);
-  }
-  {
-    const float sdf = ex2((t.rd - Md) * cd), scf = ex2((t.rc - Mc) * cc);
-    const float delta = (Mc - t.rc) * cc - (Md - t.rd) * cd;
-    double ww = t.w;
-    if (t.ld > 0.f) ww += (double)t.ld * (double)delta;
-    double v[3] = {(double)t.ld * sdf, (double)t.lc * scf, ww * sdf};
-#pragma unroll
-    for (int k = 0; k < 3; ++k) v[k] = warp_sum_d(v[k]);
-    if (lane == 0)
-#pragma unroll
-      for (int k = 0; k < 3; ++k) sm.dscr[k * NW + wid] = v[k];
-  }
-  __syncthreads();
-  cluster_wait();  // (0) every peer has started: DSMEM pushes are safe
-  if (ctl) {       // lanes 0..2 sum the 3 quantities over warps (warp order); push to every rank
-    double r = 0.0;
-    if (lane < 3)
-      for (int q = 0; q < NW; ++q) r += sm.dscr[lane * NW + q];
-    const double r0 = __shfl_sync(0xffffffffu, r, 0), r1 = __shfl_sync(0xffffffffu, r, 1),
-                 r2 = __shfl_sync(0xffffffffu, r, 2);
-    if (lane < cs) {
-      const double v[5] = {(double)Md, r0, (double)Mc, r1, r2};
-#pragma unroll
-      for (int k = 0; k < 5; ++k) st_remote_f64(remote(&sm.part[rank][k], lane), v[k]);
-      remote_arrive(remote(&sm.bar_part, lane));  // release at cluster scope, no MEMBAR.GPU
+  if (!p2) {
+    // ---- P1: pass 1 (HBM) + block merge (fixed warp / lane order) -> workspace
+    const uint64_t pol_keep = l2_policy_evict_last();
+    P1State t = pass1_thread<T, false, NT, G>(ch, cd, cc, pol_keep);
+    if (t.w != t.w && t.ld == t.ld && t.lc == t.lc)  // 0 * (-inf) from masked logits: guarded redo
+      t = pass1_thread<T, true, NT, G>(ch, cd, cc, pol_keep);
+    float Md = warp_max(t.md), Mc = warp_max(t.mc);
+    if (lane == 0) {
+      sm.fscr[wid] = Md;
+      sm.fscr[NW + wid] = Mc;
     }
+    __syncthreads();
+    Md = sm.fscr[0];
+    Mc = sm.fscr[NW];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) {
+      Md = fmaxf(Md, sm.fscr[w]);
+      Mc = fmaxf(Mc, sm.fscr[NW + w]);
+    }
+    {
+      const float sdf = ex2((t.rd - Md) * cd), scf = ex2((t.rc - Mc) * cc);
+      const float delta = (Mc - t.rc) * cc - (Md - t.rd) * cd;
+      double ww = t.w;
+      if (t.ld > 0.f) ww += (double)t.ld * (double)delta;
+      double v[3] = {(double)t.ld * sdf, (double)t.lc * scf, ww * sdf};
+#pragma unroll
+      for (int k = 0; k < 3; ++k) v[k] = warp_sum_d(v[k]);
+      if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) sm.dscr[k * NW + wid] = v[k];
+    }
+    __syncthreads();
+    if (ctl) {  // lanes 0..2 sum the 3 quantities over warps (warp order); lane 0 publishes
+      double r = 0.0;
+      if (lane < 3)
+        for (int w = 0; w < NW; ++w) r += sm.dscr[lane * NW + w];
+      const double r0 = __shfl_sync(0xffffffffu, r, 0), r1 = __shfl_sync(0xffffffffu, r, 1),
+                   r2 = __shfl_sync(0xffffffffu, r, 2);
+      if (lane == 0) {
+        double *part = a.part + (size_t)q * 5;
+        part[0] = (double)Md;
+        part[1] = r0;
+        part[2] = (double)Mc;
+        part[3] = r1;
+        part[4] = r2;
+        red_release_add(cnt, 1u);
+      }
+    }
+    return;
   }
 
-  // ---- cluster merge in rank order (local shared memory; identical in every CTA)
+  // ---- P2: merge the row's P1 partials in chunk order (identical bits in every P2 task)
   if (ctl) {
-    wait_cluster(&sm.bar_part, 0);  // every rank's partial is here
+    wait_count(cnt, (uint32_t)cs);  // every lane acquires
     double pr[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     pr[0] = pr[2] = kMFloor;
-    if (lane < cs)
+    if (lane < cs) {
+      const double *part = a.part + ((size_t)row * cs + lane) * 5;
 #pragma unroll
-      for (int k = 0; k < 5; ++k) pr[k] = sm.part[lane][k];
+      for (int k = 0; k < 5; ++k) pr[k] = __ldcg(part + k);
+    }
     const float rmd = (float)pr[0], rmc = (float)pr[2];
     const float GMd = warp_max(rmd), GMc = warp_max(rmc);
     const float sdf = ex2((rmd - GMd) * cd), scf = ex2((rmc - GMc) * cc);
@@ -446,7 +447,7 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constan
     if (pr[1] > 0.0) ww += pr[1] * (double)delta;
     const double cl_d = pr[1] * sdf, cl_c = pr[3] * scf, cw = ww * sdf;
     double L_d = 0.0, L_c = 0.0, W = 0.0;
-    for (int r = 0; r < cs; ++r) {  // rank order
+    for (int r = 0; r < cs; ++r) {  // chunk order
       L_d += __shfl_sync(0xffffffffu, cl_d, r);
       L_c += __shfl_sync(0xffffffffu, cl_c, r);
       W += __shfl_sync(0xffffffffu, cw, r);
@@ -471,50 +472,40 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constan
   s_loc = warp_sum(s_loc);
   if (lane == 0) sm.fscr[wid] = s_loc;
   __syncthreads();
-  if (ctl && lane == 0) {
+  if (!ctl) return;
+  float *srow = a.spart + (size_t)row * cs;
+  if (lane == 0) {
     float r = sm.fscr[0];
-    for (int q = 1; q < NW; ++q) r += sm.fscr[q];
-    st_remote_f32(remote(&sm.sarr[rank], 0), r);
-    remote_arrive(remote(&sm.bar_s, 0));
+    for (int w = 1; w < NW; ++w) r += sm.fscr[w];
+    srow[rank] = r;
+    if (rank != cs - 1) red_release_add(cnt + 1, 1u);
   }
-  // Ranks != 0 may exit now: every push INTO them completed before their bar_part wait.
-  if (rank == 0 && ctl) {
-    wait_cluster(&sm.bar_s, 0);
-    epilogue<T>(a, bb, ii, sm.glob, sm.sarr, cs);
+  if (rank != cs - 1) return;
+  // the row's last P2 task: wait for the other S partials, epilogue, reset the counters
+  wait_count(cnt + 1, (uint32_t)(cs - 1));  // every lane acquires
+  epilogue<T>(a, bb, ii, sm.glob, srow, cs);
+  if (lane == 0) {
+    cnt[0] = 0u;  // every P1 / P2 task of this row is past its use of the counters
+    cnt[1] = 0u;
   }
 }
 
 template <typename T, int NT, int MINB, int G>
 cudaError_t launch_score_t(const ScoreArgs &a, cudaStream_t st) {
-  const void *fn = (const void *)sv_score_kernel<T, NT, MINB, G>;
-  cudaError_t e = cudaSuccess;
-  if (a.cs > 8) {
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)((int64_t)a.B * a.cs), (unsigned)a.k);
-  cfg.blockDim = dim3(NT);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = a.cs;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, sv_score_kernel<T, NT, MINB, G>, a);
+  const int64_t tasks = 2 * (int64_t)a.B * a.k * a.cs;
+  if (tasks == 0) return cudaSuccess;
+  sv_score_kernel<T, NT, MINB, G><<<(unsigned)tasks, NT, 0, st>>>(a);
+  return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t launch_score_cfg(const ScoreArgs &a, cudaStream_t st) {
-  // CTAs per SM (register budget) x loads in flight per thread; SV_SCORE_CFG overrides (tuning)
+  // threads x CTAs per SM (register budget) x loads in flight per thread; SV_SCORE_CFG overrides
   static const int cfg = tune_knob("SV_SCORE_CFG", 0);
   switch (cfg) {
     case 1: return launch_score_t<T, 256, 5, 2>(a, st);
     case 2: return launch_score_t<T, 128, 10, 2>(a, st);
-    case 3: return launch_score_t<T, 128, 12, 1>(a, st);
+    case 3: return launch_score_t<T, 256, 6, 1>(a, st);
     case 4: return launch_score_t<T, 256, 4, 2>(a, st);
     default: return launch_score_t<T, kScoreThreads, kScoreMinBlocks, kScoreGroup>(a, st);
   }
