@@ -12,7 +12,7 @@ namespace sv {
 constexpr int kScoreThreads = 256;
 constexpr int kScoreMinBlocks = 5;
 constexpr int kScoreGroup = 2;
-constexpr int kScoreLag = 64;
+constexpr int kScoreLag = 128;
 constexpr int kScoreChunk = 32768;  // target elements per chunk task (per tensor)
 constexpr int kScoreMaxSplits = 32;
 // sd_verify: one cluster per sequence, 8-warp CTAs, kVerifyGroup loads per thread in flight

@@ -181,20 +181,51 @@ __device__ __forceinline__ void p1_group(P1State &t, const uint4 (&rd)[g], const
 
 // Pass 1 of the thread's share of a chunk: full groups of G units per tensor (all loads of a
 // group in flight together, no per-unit guards), then single units, then the element tail.
-template <typename T, bool kGuard, int NT, int G>
+template <typename T, bool kGuard, int NT, int G, bool PF>
 __device__ __forceinline__ P1State pass1_thread(const Chunk<T> &ch, float cd, float cc, uint64_t pol) {
   constexpr int EPU = Elem<T>::kPerUnit;
   const int tid = threadIdx.x;
   P1State t{kMFloor, kMFloor, kMFloor, kMFloor, 0.f, 0.f, 0.f};
   int u0 = tid;
-  for (; u0 + (G - 1) * NT < ch.units; u0 += G * NT) {
+  if constexpr (PF) {  // software pipelined: the next group's loads are in flight during this one
     uint4 rd[G], rc[G];
+    if (u0 + (G - 1) * NT < ch.units) {
 #pragma unroll
-    for (int q = 0; q < G; ++q) {
-      rd[q] = ldg_hint(ch.d + (size_t)(u0 + q * NT) * EPU, pol);
-      rc[q] = ldg_hint(ch.c + (size_t)(u0 + q * NT) * EPU, pol);
+      for (int q = 0; q < G; ++q) {
+        rd[q] = ldg_hint(ch.d + (size_t)(u0 + q * NT) * EPU, pol);
+        rc[q] = ldg_hint(ch.c + (size_t)(u0 + q * NT) * EPU, pol);
+      }
+      while (true) {
+        const int un = u0 + G * NT;
+        const bool more = un + (G - 1) * NT < ch.units;
+        uint4 nd[G], nc[G];
+        if (more) {
+#pragma unroll
+          for (int q = 0; q < G; ++q) {
+            nd[q] = ldg_hint(ch.d + (size_t)(un + q * NT) * EPU, pol);
+            nc[q] = ldg_hint(ch.c + (size_t)(un + q * NT) * EPU, pol);
+          }
+        }
+        p1_group<T, kGuard, G>(t, rd, rc, cd, cc);
+        u0 = un;
+        if (!more) break;
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+          rd[q] = nd[q];
+          rc[q] = nc[q];
+        }
+      }
     }
-    p1_group<T, kGuard, G>(t, rd, rc, cd, cc);
+  } else {
+    for (; u0 + (G - 1) * NT < ch.units; u0 += G * NT) {
+      uint4 rd[G], rc[G];
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        rd[q] = ldg_hint(ch.d + (size_t)(u0 + q * NT) * EPU, pol);
+        rc[q] = ldg_hint(ch.c + (size_t)(u0 + q * NT) * EPU, pol);
+      }
+      p1_group<T, kGuard, G>(t, rd, rc, cd, cc);
+    }
   }
   for (; u0 < ch.units; u0 += NT) {
     uint4 rd[1] = {ldg_hint(ch.d + (size_t)u0 * EPU, pol)}, rc[1] = {ldg_hint(ch.c + (size_t)u0 * EPU, pol)};
@@ -360,7 +391,7 @@ __device__ __forceinline__ void decode_task(uint32_t t, uint32_t RC, uint32_t E,
   }
 }
 
-template <typename T, int NT, int MINB, int G>
+template <typename T, int NT, int MINB, int G, bool PF>
 __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constant__ ScoreArgs a) {
   constexpr int NW = NT / 32;
   __shared__ Smem<NW> sm;
@@ -381,9 +412,9 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constan
   if (!p2) {
     // ---- P1: pass 1 (HBM) + block merge (fixed warp / lane order) -> workspace
     const uint64_t pol_keep = l2_policy_evict_last();
-    P1State t = pass1_thread<T, false, NT, G>(ch, cd, cc, pol_keep);
+    P1State t = pass1_thread<T, false, NT, G, PF>(ch, cd, cc, pol_keep);
     if (t.w != t.w && t.ld == t.ld && t.lc == t.lc)  // 0 * (-inf) from masked logits: guarded redo
-      t = pass1_thread<T, true, NT, G>(ch, cd, cc, pol_keep);
+      t = pass1_thread<T, true, NT, G, false>(ch, cd, cc, pol_keep);
     float Md = warp_max(t.md), Mc = warp_max(t.mc);
     if (lane == 0) {
       sm.fscr[wid] = Md;
@@ -490,11 +521,11 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constan
   }
 }
 
-template <typename T, int NT, int MINB, int G>
+template <typename T, int NT, int MINB, int G, bool PF = false>
 cudaError_t launch_score_t(const ScoreArgs &a, cudaStream_t st) {
   const int64_t tasks = 2 * (int64_t)a.B * a.k * a.cs;
   if (tasks == 0) return cudaSuccess;
-  sv_score_kernel<T, NT, MINB, G><<<(unsigned)tasks, NT, 0, st>>>(a);
+  sv_score_kernel<T, NT, MINB, G, PF><<<(unsigned)tasks, NT, 0, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -503,10 +534,10 @@ cudaError_t launch_score_cfg(const ScoreArgs &a, cudaStream_t st) {
   // threads x CTAs per SM (register budget) x loads in flight per thread; SV_SCORE_CFG overrides
   static const int cfg = tune_knob("SV_SCORE_CFG", 0);
   switch (cfg) {
-    case 1: return launch_score_t<T, 256, 5, 2>(a, st);
-    case 2: return launch_score_t<T, 128, 10, 2>(a, st);
-    case 3: return launch_score_t<T, 256, 6, 1>(a, st);
-    case 4: return launch_score_t<T, 256, 4, 2>(a, st);
+    case 1: return launch_score_t<T, 256, 4, 2, true>(a, st);
+    case 2: return launch_score_t<T, 256, 5, 1, true>(a, st);
+    case 3: return launch_score_t<T, 256, 4, 3>(a, st);
+    case 4: return launch_score_t<T, 256, 3, 2, true>(a, st);
     default: return launch_score_t<T, kScoreThreads, kScoreMinBlocks, kScoreGroup>(a, st);
   }
 }
