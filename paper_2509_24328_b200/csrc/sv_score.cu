@@ -391,134 +391,306 @@ __device__ __forceinline__ void decode_task(uint32_t t, uint32_t RC, uint32_t E,
   }
 }
 
-template <typename T, int NT, int MINB, int G, bool PF>
-__global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constant__ ScoreArgs a) {
-  constexpr int NW = NT / 32;
-  __shared__ Smem<NW> sm;
-  const int cs = a.cs;
-  const uint32_t RC = (uint32_t)a.B * (uint32_t)a.k * (uint32_t)cs;
-  uint32_t q;
+// Where a task sits: row, chunk rank, (b, i) and the row's counters.
+struct Task {
+  uint32_t q, row, bb, ii;
+  int rank;
   bool p2;
-  decode_task(blockIdx.x, RC, (uint32_t)a.lead, q, p2);
-  const uint32_t row = q / (uint32_t)cs;
-  const int rank = (int)(q - row * cs);
-  const uint32_t bb = row / (uint32_t)a.k, ii = row - bb * a.k;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const bool ctl = wid == NW - 1;  // serial work on the highest warp id (favoured by the arbiter)
+};
+__device__ __forceinline__ Task task_of(const ScoreArgs &a) {
+  Task k;
+  const uint32_t cs = (uint32_t)a.cs, RC = (uint32_t)a.B * (uint32_t)a.k * cs;
+  decode_task(blockIdx.x, RC, (uint32_t)a.lead, k.q, k.p2);
+  k.row = k.q / cs;
+  k.rank = (int)(k.q - k.row * cs);
+  k.bb = k.row / (uint32_t)a.k;
+  k.ii = k.row - k.bb * a.k;
+  return k;
+}
+
+// P1 tail: block merge of the threads' pass-1 states (fixed warp / lane order), the last warp
+// publishes (M_d, L_d, M_c, L_c, W) and bumps the row counter (release).  All NW warps call it.
+template <int NW>
+__device__ __forceinline__ void p1_publish(const ScoreArgs &a, const Task &k, const P1State &t, Smem<NW> &sm) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const float cd = a.cd, cc = a.cc;
-  const Chunk<T> ch = chunk_of<T>(a, bb, ii, rank);
-  uint32_t *cnt = a.cnt + 2 * (size_t)row;  // [0] P1 partials published, [1] S partials published
-
-  if (!p2) {
-    // ---- P1: pass 1 (HBM) + block merge (fixed warp / lane order) -> workspace
-    const uint64_t pol_keep = l2_policy_evict_last();
-    P1State t = pass1_thread<T, false, NT, G, PF>(ch, cd, cc, pol_keep);
-    if (t.w != t.w && t.ld == t.ld && t.lc == t.lc)  // 0 * (-inf) from masked logits: guarded redo
-      t = pass1_thread<T, true, NT, G, false>(ch, cd, cc, pol_keep);
-    float Md = warp_max(t.md), Mc = warp_max(t.mc);
-    if (lane == 0) {
-      sm.fscr[wid] = Md;
-      sm.fscr[NW + wid] = Mc;
-    }
-    __syncthreads();
-    Md = sm.fscr[0];
-    Mc = sm.fscr[NW];
-#pragma unroll
-    for (int w = 1; w < NW; ++w) {
-      Md = fmaxf(Md, sm.fscr[w]);
-      Mc = fmaxf(Mc, sm.fscr[NW + w]);
-    }
-    {
-      const float sdf = ex2((t.rd - Md) * cd), scf = ex2((t.rc - Mc) * cc);
-      const float delta = (Mc - t.rc) * cc - (Md - t.rd) * cd;
-      double ww = t.w;
-      if (t.ld > 0.f) ww += (double)t.ld * (double)delta;
-      double v[3] = {(double)t.ld * sdf, (double)t.lc * scf, ww * sdf};
-#pragma unroll
-      for (int k = 0; k < 3; ++k) v[k] = warp_sum_d(v[k]);
-      if (lane == 0)
-#pragma unroll
-        for (int k = 0; k < 3; ++k) sm.dscr[k * NW + wid] = v[k];
-    }
-    __syncthreads();
-    if (ctl) {  // lanes 0..2 sum the 3 quantities over warps (warp order); lane 0 publishes
-      double r = 0.0;
-      if (lane < 3)
-        for (int w = 0; w < NW; ++w) r += sm.dscr[lane * NW + w];
-      const double r0 = __shfl_sync(0xffffffffu, r, 0), r1 = __shfl_sync(0xffffffffu, r, 1),
-                   r2 = __shfl_sync(0xffffffffu, r, 2);
-      if (lane == 0) {
-        double *part = a.part + (size_t)q * 5;
-        part[0] = (double)Md;
-        part[1] = r0;
-        part[2] = (double)Mc;
-        part[3] = r1;
-        part[4] = r2;
-        red_release_add(cnt, 1u);
-      }
-    }
-    return;
-  }
-
-  // ---- P2: merge the row's P1 partials in chunk order (identical bits in every P2 task)
-  if (ctl) {
-    wait_count(cnt, (uint32_t)cs);  // every lane acquires
-    double pr[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    pr[0] = pr[2] = kMFloor;
-    if (lane < cs) {
-      const double *part = a.part + ((size_t)row * cs + lane) * 5;
-#pragma unroll
-      for (int k = 0; k < 5; ++k) pr[k] = __ldcg(part + k);
-    }
-    const float rmd = (float)pr[0], rmc = (float)pr[2];
-    const float GMd = warp_max(rmd), GMc = warp_max(rmc);
-    const float sdf = ex2((rmd - GMd) * cd), scf = ex2((rmc - GMc) * cc);
-    const float delta = (GMc - rmc) * cc - (GMd - rmd) * cd;
-    double ww = pr[4];
-    if (pr[1] > 0.0) ww += pr[1] * (double)delta;
-    const double cl_d = pr[1] * sdf, cl_c = pr[3] * scf, cw = ww * sdf;
-    double L_d = 0.0, L_c = 0.0, W = 0.0;
-    for (int r = 0; r < cs; ++r) {  // chunk order
-      L_d += __shfl_sync(0xffffffffu, cl_d, r);
-      L_c += __shfl_sync(0xffffffffu, cl_c, r);
-      W += __shfl_sync(0xffffffffu, cw, r);
-    }
-    if (lane == 0) {
-      sm.glob[0] = GMd;
-      sm.glob[1] = L_d;
-      sm.glob[2] = GMc;
-      sm.glob[3] = L_c;
-      sm.glob[4] = W;
-      const bool ok = L_d > 0.0 && L_c > 0.0 && L_d < 1e300 && L_c < 1e300 && GMd < FLT_MAX && GMc < FLT_MAX;
-      sm.lam[0] = ok ? (float)((double)GMd * cd + log2_acc(L_d)) : __int_as_float(0x7fc00000);
-      sm.lam[1] = ok ? (float)((double)GMc * cc + log2_acc(L_c)) : __int_as_float(0x7fc00000);
-    }
+  float Md = warp_max(t.md), Mc = warp_max(t.mc);
+  if (lane == 0) {
+    sm.fscr[wid] = Md;
+    sm.fscr[NW + wid] = Mc;
   }
   __syncthreads();
+  Md = sm.fscr[0];
+  Mc = sm.fscr[NW];
+#pragma unroll
+  for (int w = 1; w < NW; ++w) {
+    Md = fmaxf(Md, sm.fscr[w]);
+    Mc = fmaxf(Mc, sm.fscr[NW + w]);
+  }
+  {
+    const float sdf = ex2((t.rd - Md) * cd), scf = ex2((t.rc - Mc) * cc);
+    const float delta = (Mc - t.rc) * cc - (Md - t.rd) * cd;
+    double ww = t.w;
+    if (t.ld > 0.f) ww += (double)t.ld * (double)delta;
+    double v[3] = {(double)t.ld * sdf, (double)t.lc * scf, ww * sdf};
+#pragma unroll
+    for (int j = 0; j < 3; ++j) v[j] = warp_sum_d(v[j]);
+    if (lane == 0)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) sm.dscr[j * NW + wid] = v[j];
+  }
+  __syncthreads();
+  if (wid == NW - 1) {  // lanes 0..2 sum the 3 quantities over warps (warp order); lane 0 publishes
+    double r = 0.0;
+    if (lane < 3)
+      for (int w = 0; w < NW; ++w) r += sm.dscr[lane * NW + w];
+    const double r0 = __shfl_sync(0xffffffffu, r, 0), r1 = __shfl_sync(0xffffffffu, r, 1),
+                 r2 = __shfl_sync(0xffffffffu, r, 2);
+    if (lane == 0) {
+      double *part = a.part + (size_t)k.q * 5;
+      part[0] = (double)Md;
+      part[1] = r0;
+      part[2] = (double)Mc;
+      part[3] = r1;
+      part[4] = r2;
+      red_release_add(a.cnt + 2 * (size_t)k.row, 1u);
+    }
+  }
+}
 
-  // ---- pass 2 (L2 re-read; bad rows skip it)
-  const float lamd = sm.lam[0], lamc = sm.lam[1];
-  float s_loc = 0.f;
-  if (lamd == lamd && lamc == lamc) s_loc = pass2_thread<T, NT, G>(ch, cd, cc, lamd, lamc, l2_policy_evict_first());
+// P2 head (one warp): wait for the row's cs P1 partials, merge them in chunk order (identical
+// bits in every P2 task of the row) -> sm.glob, sm.lam.
+template <int NW>
+__device__ __forceinline__ void p2_merge(const ScoreArgs &a, const Task &k, Smem<NW> &sm) {
+  const int lane = threadIdx.x & 31, cs = a.cs;
+  const float cd = a.cd, cc = a.cc;
+  wait_count(a.cnt + 2 * (size_t)k.row, (uint32_t)cs);  // every lane acquires
+  double pr[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  pr[0] = pr[2] = kMFloor;
+  if (lane < cs) {
+    const double *part = a.part + ((size_t)k.row * cs + lane) * 5;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) pr[j] = __ldcg(part + j);
+  }
+  const float rmd = (float)pr[0], rmc = (float)pr[2];
+  const float GMd = warp_max(rmd), GMc = warp_max(rmc);
+  const float sdf = ex2((rmd - GMd) * cd), scf = ex2((rmc - GMc) * cc);
+  const float delta = (GMc - rmc) * cc - (GMd - rmd) * cd;
+  double ww = pr[4];
+  if (pr[1] > 0.0) ww += pr[1] * (double)delta;
+  const double cl_d = pr[1] * sdf, cl_c = pr[3] * scf, cw = ww * sdf;
+  double L_d = 0.0, L_c = 0.0, W = 0.0;
+  for (int r = 0; r < cs; ++r) {  // chunk order
+    L_d += __shfl_sync(0xffffffffu, cl_d, r);
+    L_c += __shfl_sync(0xffffffffu, cl_c, r);
+    W += __shfl_sync(0xffffffffu, cw, r);
+  }
+  if (lane == 0) {
+    sm.glob[0] = GMd;
+    sm.glob[1] = L_d;
+    sm.glob[2] = GMc;
+    sm.glob[3] = L_c;
+    sm.glob[4] = W;
+    const bool ok = L_d > 0.0 && L_c > 0.0 && L_d < 1e300 && L_c < 1e300 && GMd < FLT_MAX && GMc < FLT_MAX;
+    sm.lam[0] = ok ? (float)((double)GMd * cd + log2_acc(L_d)) : __int_as_float(0x7fc00000);
+    sm.lam[1] = ok ? (float)((double)GMc * cc + log2_acc(L_c)) : __int_as_float(0x7fc00000);
+  }
+}
+
+// P2 tail: block sum of the S partials, publish; the row's last P2 task runs the epilogue and
+// resets the row's counters.  All NW warps call it.
+template <typename T, int NW>
+__device__ __forceinline__ void p2_finish(const ScoreArgs &a, const Task &k, float s_loc, Smem<NW> &sm) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, cs = a.cs;
   s_loc = warp_sum(s_loc);
   if (lane == 0) sm.fscr[wid] = s_loc;
   __syncthreads();
-  if (!ctl) return;
-  float *srow = a.spart + (size_t)row * cs;
+  if (wid != NW - 1) return;
+  uint32_t *cnt = a.cnt + 2 * (size_t)k.row;
+  float *srow = a.spart + (size_t)k.row * cs;
   if (lane == 0) {
     float r = sm.fscr[0];
     for (int w = 1; w < NW; ++w) r += sm.fscr[w];
-    srow[rank] = r;
-    if (rank != cs - 1) red_release_add(cnt + 1, 1u);
+    srow[k.rank] = r;
+    if (k.rank != cs - 1) red_release_add(cnt + 1, 1u);
   }
-  if (rank != cs - 1) return;
+  if (k.rank != cs - 1) return;
   // the row's last P2 task: wait for the other S partials, epilogue, reset the counters
   wait_count(cnt + 1, (uint32_t)(cs - 1));  // every lane acquires
-  epilogue<T>(a, bb, ii, sm.glob, srow, cs);
+  epilogue<T>(a, k.bb, k.ii, sm.glob, srow, cs);
   if (lane == 0) {
     cnt[0] = 0u;  // every P1 / P2 task of this row is past its use of the counters
     cnt[1] = 0u;
   }
+}
+
+// LDG variant: every thread loads its own units (kScoreGroup 16-byte loads per tensor in flight).
+template <typename T, int NT, int MINB, int G, bool PF>
+__global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constant__ ScoreArgs a) {
+  constexpr int NW = NT / 32;
+  __shared__ Smem<NW> sm;
+  const Task k = task_of(a);
+  const float cd = a.cd, cc = a.cc;
+  const Chunk<T> ch = chunk_of<T>(a, k.bb, k.ii, k.rank);
+  if (!k.p2) {
+    const uint64_t pol_keep = l2_policy_evict_last();
+    P1State t = pass1_thread<T, false, NT, G, PF>(ch, cd, cc, pol_keep);
+    if (t.w != t.w && t.ld == t.ld && t.lc == t.lc)  // 0 * (-inf) from masked logits: guarded redo
+      t = pass1_thread<T, true, NT, G, false>(ch, cd, cc, pol_keep);
+    p1_publish<NW>(a, k, t, sm);
+    return;
+  }
+  if ((threadIdx.x >> 5) == NW - 1) p2_merge<NW>(a, k, sm);
+  __syncthreads();
+  const float lamd = sm.lam[0], lamc = sm.lam[1];
+  float s_loc = 0.f;
+  if (lamd == lamd && lamc == lamc) s_loc = pass2_thread<T, NT, G>(ch, cd, cc, lamd, lamc, l2_policy_evict_first());
+  p2_finish<T, NW>(a, k, s_loc, sm);
+}
+
+__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+      "%4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+// Bulk-copy (TMA engine) variant: NC consumer threads + one producer warp.  The producer's lane 0
+// streams the chunk pair through a ring of NS shared-memory stages (SU units per consumer thread
+// per tensor per stage) with cp.async.bulk + mbarrier complete_tx, so the bytes in flight do not
+// depend on registers; consumers take unit tid + q NC of each stage -- the same units, per
+// thread, as the LDG variant's stride-NC walk.
+template <typename T, int SU, int NS, int MINB>
+__global__ void __launch_bounds__(kScoreThreads + 32, MINB) sv_score_tma_kernel(const __grid_constant__ ScoreArgs a) {
+  constexpr int NC = kScoreThreads, NW = NC / 32 + 1, EPU = Elem<T>::kPerUnit, SUN = SU * NC;
+  __shared__ Smem<NW> sm;
+  __shared__ uint64_t full[NS], empty[NS];
+  extern __shared__ __align__(128) uint4 stage_buf[];  // [NS][2][SUN]
+  const Task k = task_of(a);
+  const float cd = a.cd, cc = a.cc;
+  const Chunk<T> ch = chunk_of<T>(a, k.bb, k.ii, k.rank);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const bool producer = wid == NW - 1;
+  const int nst = (ch.units + SUN - 1) / SUN;
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NC / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t pol = k.p2 ? l2_policy_evict_first() : l2_policy_evict_last();
+  auto issue = [&](int st) {  // producer lane 0 only
+    const int slot = st % NS;
+    if (st >= NS) mbar_wait(&empty[slot], ((st / NS) - 1) & 1);
+    const int u0 = st * SUN, nu = min(SUN, ch.units - u0);
+    uint4 *dst = stage_buf + (size_t)slot * 2 * SUN;
+    mbar_arrive_expect_tx(&full[slot], (uint32_t)(2 * nu * 16));
+    bulk_g2s_hint(dst, ch.d + (size_t)u0 * EPU, (uint32_t)(nu * 16), &full[slot], pol);
+    bulk_g2s_hint(dst + SUN, ch.c + (size_t)u0 * EPU, (uint32_t)(nu * 16), &full[slot], pol);
+  };
+
+  if (!k.p2) {
+    P1State t{kMFloor, kMFloor, kMFloor, kMFloor, 0.f, 0.f, 0.f};
+    if (producer) {
+      if (lane == 0)
+        for (int st = 0; st < nst; ++st) issue(st);
+    } else {
+      for (int st = 0; st < nst; ++st) {
+        const int slot = st % NS;
+        mbar_wait(&full[slot], (st / NS) & 1);
+        const uint4 *sd = stage_buf + (size_t)slot * 2 * SUN, *sc = sd + SUN;
+        const int nu = min(SUN, ch.units - st * SUN);
+        if (nu == SUN) {
+          uint4 rd[SU], rc[SU];
+#pragma unroll
+          for (int q = 0; q < SU; ++q) {
+            rd[q] = sd[tid + q * NC];
+            rc[q] = sc[tid + q * NC];
+          }
+          p1_group<T, false, SU>(t, rd, rc, cd, cc);
+        } else {
+          for (int u = tid; u < nu; u += NC) {
+            const uint4 rd[1] = {sd[u]}, rc[1] = {sc[u]};
+            p1_group<T, false, 1>(t, rd, rc, cd, cc);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+      }
+      // element tail (and the unaligned-chunk case, units == 0) from global
+      const int e0 = ch.units * EPU;
+      for (int e = e0 + tid; e < ch.n; e += NC) {
+        t.md = fmaxf(t.md, Elem<T>::load(ch.d + e));
+        t.mc = fmaxf(t.mc, Elem<T>::load(ch.c + e));
+      }
+      p1_rescale(t, cd, cc);
+      const float nmd = -t.rd * cd, nmc = -t.rc * cc;
+      for (int e = e0 + tid; e < ch.n; e += NC) {
+        const float ad = fmaf(Elem<T>::load(ch.d + e), cd, nmd), ac = fmaf(Elem<T>::load(ch.c + e), cc, nmc);
+        const float ed = ex2(ad);
+        t.ld += ed;
+        t.lc += ex2(ac);
+        t.w += ed > 0.f ? ed * (ad - ac) : 0.f;
+      }
+      if (t.w != t.w && t.ld == t.ld && t.lc == t.lc)  // 0 * (-inf) from masked logits: guarded redo
+        t = pass1_thread<T, true, NC, 1, false>(ch, cd, cc, pol);
+    }
+    p1_publish<NW>(a, k, t, sm);
+    return;
+  }
+
+  // P2: the first NS stages are requested before the partials are even merged
+  if (producer) {
+    if (lane == 0)
+      for (int st = 0; st < min(NS, nst); ++st) issue(st);
+    __syncwarp();
+    p2_merge<NW>(a, k, sm);
+  }
+  __syncthreads();
+  const float lamd = sm.lam[0], lamc = sm.lam[1];
+  const bool good = lamd == lamd && lamc == lamc;
+  float s_loc = 0.f;
+  if (producer) {
+    if (lane == 0)
+      for (int st = NS; st < nst; ++st) issue(st);
+  } else {
+    const f2 cdd{cd, cd}, ccc{cc, cc}, ld2{-lamd, -lamd}, lc2{-lamc, -lamc};
+    f2 acc{0.f, 0.f};
+    for (int st = 0; st < nst; ++st) {
+      const int slot = st % NS;
+      mbar_wait(&full[slot], (st / NS) & 1);
+      const uint4 *sd = stage_buf + (size_t)slot * 2 * SUN, *sc = sd + SUN;
+      const int nu = min(SUN, ch.units - st * SUN);
+      if (good) {
+        if (nu == SUN) {
+          uint4 rd[SU], rc[SU];
+#pragma unroll
+          for (int q = 0; q < SU; ++q) {
+            rd[q] = sd[tid + q * NC];
+            rc[q] = sc[tid + q * NC];
+          }
+          p2_group<T, SU>(acc, rd, rc, cdd, ccc, ld2, lc2);
+        } else {
+          for (int u = tid; u < nu; u += NC) {
+            const uint4 rd[1] = {sd[u]}, rc[1] = {sc[u]};
+            p2_group<T, 1>(acc, rd, rc, cdd, ccc, ld2, lc2);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+    if (good)
+      for (int e = ch.units * EPU + tid; e < ch.n; e += NC)
+        acc.x += ex2(fminf(fmaf(Elem<T>::load(ch.d + e), cd, -lamd), fmaf(Elem<T>::load(ch.c + e), cc, -lamc)));
+    s_loc = acc.x + acc.y;
+  }
+  p2_finish<T, NW>(a, k, s_loc, sm);
 }
 
 template <typename T, int NT, int MINB, int G, bool PF = false>
@@ -529,15 +701,33 @@ cudaError_t launch_score_t(const ScoreArgs &a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+template <typename T, int SU, int NS, int MINB>
+cudaError_t launch_score_tma(const ScoreArgs &a, cudaStream_t st) {
+  const int64_t tasks = 2 * (int64_t)a.B * a.k * a.cs;
+  if (tasks == 0) return cudaSuccess;
+  const int smem = NS * 2 * SU * kScoreThreads * 16;
+  auto fn = sv_score_tma_kernel<T, SU, NS, MINB>;
+  static bool attr_done = false;  // per instantiation
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  fn<<<(unsigned)tasks, kScoreThreads + 32, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t launch_score_cfg(const ScoreArgs &a, cudaStream_t st) {
   // threads x CTAs per SM (register budget) x loads in flight per thread; SV_SCORE_CFG overrides
   static const int cfg = tune_knob("SV_SCORE_CFG", 0);
   switch (cfg) {
     case 1: return launch_score_t<T, 256, 4, 2, true>(a, st);
-    case 2: return launch_score_t<T, 256, 5, 1, true>(a, st);
     case 3: return launch_score_t<T, 256, 4, 3>(a, st);
-    case 4: return launch_score_t<T, 256, 3, 2, true>(a, st);
+    case 5: return launch_score_tma<T, 2, 3, 4>(a, st);
+    case 6: return launch_score_tma<T, 1, 4, 5>(a, st);
+    case 7: return launch_score_tma<T, 2, 2, 5>(a, st);
+    case 8: return launch_score_tma<T, 1, 6, 4>(a, st);
     default: return launch_score_t<T, kScoreThreads, kScoreMinBlocks, kScoreGroup>(a, st);
   }
 }
