@@ -26,6 +26,9 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+# kernels one pipeline step launches: sv_score (K1), sv_schedule (K3), sd_verify (K4 rows, K4b decide,
+# K5 residual slices, K5b token search)
+KERNELS_PER_STEP = 6
 sys.path.insert(0, ROOT)
 
 METRIC = "scored (b,i) positions/sec at B=80,k=8,V=152064; HBM GB/s vs B200 peak"
@@ -333,7 +336,7 @@ def run_ours(args, rank, world, local_rank):
             "e2e": {"value": world * B * k / (e2e_ms / e2e_steps * 1e-3), "unit": "positions/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                     "path": "pinned host -> cudaMemcpyAsync -> sv_score/sv_schedule/sd_verify (C ABI) -> host"},
-            "gpu_launches": 4 * args.steps,
+            "gpu_launches": KERNELS_PER_STEP * args.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }

@@ -1,20 +1,23 @@
 // sd_verify.cu -- K4 + K5: steps a5-a6 (standard SD verification and the correction /
 // bonus sample; P L29 citing Leviathan et al.; S L148-165, L82-90; DESIGN R1, R10-R13).
 //
-// K4 sv_rows_kernel: one CTA per (target row, vocabulary split).  Rows i > gamma_b exit at
-//   once, so only the verified target rows are streamed from HBM.  16 independent 16-byte
-//   streaming loads per thread are issued before any use (64 KB in flight per CTA), then
-//   the split's raw max m and l = sum 2^{(x - m) log2e / tau_t} are reduced (per-unit
-//   fp32 sums, fp64 per thread and per block) and written as one (m, l) partial.
-// K5 sv_sample_kernel: one CTA cluster per sequence.
-//   prologue (every CTA, identically): merge the (m, l) partials of rows 0..gamma_b in
-//   split order, p_t(t_i), ratio_i = p_t(t_i) / p_d(t_i), Philox u_i, N_b = first
-//   rejection; u_s = word 1 of position N_b.
-//   body: CTA r bulk-copies its vocabulary chunk of the target row N_b (and of the draft
-//   row N_b when rejected) into smem, computes r_v = max(0, p_t - p_d) (or p_t for the
-//   bonus), and sums it in fp64 in a fixed (lane, round, warp, rank) order.  The chunk
-//   sums are exchanged through DSMEM; the CTA whose range contains u_s * Z locates the
-//   token by warp scan + in-lane sequential scan (smallest j with cum_j > u_s Z).
+// K4 sv_rows_kernel: a persistent grid over the COMPACTED list of (sequence b, target row
+//   i <= gamma_b, vocabulary split) items -- rows past gamma_b are never read and cost no CTA.
+//   Items are WARP-granular (no block barrier on the path): a warp streams 32 lanes x 8
+//   16-byte units of one target row (8 independent loads per lane in flight), reduces the raw
+//   max m and l = sum 2^{(x - m) log2e / tau_t} (fp32 per unit, fp64 per lane and butterfly)
+//   and writes one (m, l) partial.  acq_rel completion counters elect the warp that finishes a
+//   row (it merges the row's partials in a fixed order) and then the warp that finishes a
+//   sequence: it computes p_t(t_i), ratio_i = p_t(t_i) / p_d(t_i), the Philox u_i, N_b = first
+//   rejection and u_s (word 1 of position N_b), and writes the sequence's Decision
+//   (+ n_accept, accept_ratio).
+// K5 sv_resid_kernel: persistent, one warp per (sequence, slice of 32 lanes x 4 contiguous
+//   16-byte units).  r_v = max(0, p_t - p_d) on row N_b (or p_t for the bonus), every lane
+//   summing its contiguous elements in vocabulary order in fp64, a fixed-order warp scan gives
+//   the slice mass.  The warp that completes a sequence walks the slice masses in vocabulary
+//   order (Z, theta = u_s Z, owning slice), recomputes the owning slice -- identical bits, an
+//   L2 hit -- and locates the smallest j with cum_j > theta (R11) by warp scan + in-lane
+//   sequential scan.  Every reduction order is a function of V and the dtype only.
 #include <float.h>
 
 #include "sv_device.cuh"
@@ -24,21 +27,20 @@ namespace sv {
 
 namespace {
 
+#define kNaNf __int_as_float(0x7fc00000)
+#define SV_MAX_K_DEV 16
+constexpr int kFindChunks = 8;  // K5b: slice-mass chunks of 32 loaded together
+
 // ------------------------------------------------------------------ K4
+// One warp item (row, split): the (M, sum-exp) partial of 32 lanes x U 16-byte units of the
+// target row (unit u = lane + 32 j: every load instruction reads 512 contiguous bytes).
 template <typename T>
-__global__ void __launch_bounds__(kRowsThreads, 4) sv_rows_kernel(const VerifyArgs a) {
-  constexpr int NT = kRowsThreads, EPU = Elem<T>::kPerUnit, U = kRowUnitsPerThread;
-  __shared__ float fscr[NT / 32];
-  __shared__ double dscr[NT / 32];
-  const int64_t cta = blockIdx.x;
-  const int64_t row = cta / a.splits, split = cta % a.splits;
-  const int64_t b = row / (a.k + 1), i = row % (a.k + 1);
-  const int g = a.gamma[b];
-  if (g < 0 || g > a.k || i > g) return;
+__device__ __forceinline__ float2 rows_warp_item(const VerifyArgs &a, int64_t b, int64_t i, int64_t split) {
+  constexpr int EPU = Elem<T>::kPerUnit, U = kRowUnitsPerThread;
+  const int lane = threadIdx.x & 31;
   const int64_t v0 = split * a.rows_chunk;
   const int n = (int)min(a.rows_chunk, (int64_t)a.V - v0);
   const T *src = reinterpret_cast<const T *>(a.t) + b * a.t_sb + i * a.t_si + v0;
-  const int tid = threadIdx.x;
   const float c = a.ct;
   float m = kMFloor;
   double l = 0.0;
@@ -47,15 +49,15 @@ __global__ void __launch_bounds__(kRowsThreads, 4) sv_rows_kernel(const VerifyAr
     uint4 r[U];
 #pragma unroll
     for (int j = 0; j < U; ++j) {
-      const int u = tid + j * NT;
+      const int u = lane + 32 * j;
       if (u < units) r[j] = ldg_stream(src + (size_t)u * EPU);
     }
-    const int tail = n - units * EPU;
+    const int tail = n - units * EPU;  // < EPU <= 32
     float xt = kMFloor;
-    if (tid < tail) xt = Elem<T>::load(src + units * EPU + tid);
+    if (lane < tail) xt = Elem<T>::load(src + units * EPU + lane);
 #pragma unroll
     for (int j = 0; j < U; ++j) {
-      if (tid + j * NT < units) {
+      if (lane + 32 * j < units) {
         float x[EPU];
         Elem<T>::unit(r[j], x);
 #pragma unroll
@@ -66,7 +68,7 @@ __global__ void __launch_bounds__(kRowsThreads, 4) sv_rows_kernel(const VerifyAr
     const float nm = -m * c;
 #pragma unroll
     for (int j = 0; j < U; ++j) {
-      if (tid + j * NT < units) {
+      if (lane + 32 * j < units) {
         float x[EPU], ex[EPU];
         Elem<T>::unit(r[j], x);
 #pragma unroll
@@ -78,9 +80,9 @@ __global__ void __launch_bounds__(kRowsThreads, 4) sv_rows_kernel(const VerifyAr
         l += ex[0];
       }
     }
-    if (tid < tail) l += ex2(fmaf(xt, c, nm));
+    if (lane < tail) l += ex2(fmaf(xt, c, nm));
   } else {  // unaligned row start (edge cases): element-wise online loop
-    for (int e = tid; e < n; e += NT) {
+    for (int e = lane; e < n; e += 32) {
       const float x = Elem<T>::load(src + e);
       if (x > m) {
         l *= ex2((m - x) * c);
@@ -89,377 +91,445 @@ __global__ void __launch_bounds__(kRowsThreads, 4) sv_rows_kernel(const VerifyAr
       l += ex2(fmaf(x, c, -m * c));
     }
   }
-  const float M = block_max<NT>(m, fscr);
-  double v = l * ex2((m - M) * c);
-  v = warp_sum_d(v);
-  if ((tid & 31) == 0) dscr[tid >> 5] = v;
+  const float M = warp_max(m);
+  const double v = warp_sum_d(l * ex2((m - M) * c));
+  return make_float2(M, (float)v);
+}
+
+// K4b sv_decide_kernel: one CTA of k+1 warps per sequence.  Warp i <= gamma_b merges row i's
+// split partials in a fixed order (lane-strided sequential, then butterfly) into (M_i, L_i);
+// warp 0 then runs the accept tests: p_t(t_i), ratio_i = p_t(t_i) / p_d(t_i), u_i, N_b =
+// first rejection, and writes the Decision for K5 (+ n_accept, accept_ratio).
+template <typename T>
+__global__ void __launch_bounds__(32 * (SV_MAX_K_DEV + 1)) sv_decide_kernel(const __grid_constant__ VerifyArgs a) {
+  __shared__ float s_M[SV_MAX_K_DEV + 1];
+  __shared__ double s_L[SV_MAX_K_DEV + 1];
+  pdl_wait();
+  pdl_trigger();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, k = a.k;
+  const int64_t b = blockIdx.x;
+  const int g = a.gamma[b];
+  const bool gok = g >= 0 && g <= k;
+  // warp 0 issues everything the accept tests need that does not depend on the merged rows
+  int t = -1;
+  float dl = 0.f, dpt = 0.f, dmv = 0.f, xt = 0.f;
+  uint4 w = make_uint4(0u, 0u, 0u, 0u);
+  if (wid == 0 && gok && lane <= g) {
+    if (lane < g) {
+      const int64_t ri = b * k + lane;
+      t = a.tok[ri];
+      dl = a.dl[ri];
+      dpt = a.dpt[ri];
+      dmv = a.dm[ri];
+      if (t >= 0 && t < a.V) xt = Elem<T>::load(reinterpret_cast<const T *>(a.t) + b * a.t_sb + lane * a.t_si + t);
+    }
+    w = sv_philox(a.seed, a.offset, a.seq_base + b, lane);
+  }
+  if (gok && wid <= g) {  // merge row wid: lane-strided sequential, then butterfly
+    const float2 *pp = a.partials + (b * (k + 1) + wid) * a.splits;
+    const int64_t ns = a.splits;
+    float M;
+    double l = 0.0;
+    if (ns <= 128) {  // all partials in flight at once
+      float2 p[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) p[j] = (lane + 32 * j < ns) ? pp[lane + 32 * j] : make_float2(kMFloor, 0.f);
+      float m = kMFloor;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) m = fmaxf(m, p[j].x);
+      M = warp_max(m);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (lane + 32 * j < ns) l += (double)p[j].y * ex2((p[j].x - M) * a.ct);
+    } else {
+      float m = kMFloor;
+      for (int64_t s = lane; s < ns; s += 32) m = fmaxf(m, pp[s].x);
+      M = warp_max(m);
+      for (int64_t s = lane; s < ns; s += 32) {
+        const float2 p = pp[s];
+        l += (double)p.y * ex2((p.x - M) * a.ct);
+      }
+    }
+    const double L = warp_sum_d(l);
+    if (lane == 0) {
+      s_M[wid] = M;
+      s_L[wid] = L;
+    }
+  }
   __syncthreads();
-  if (tid == 0) {
-    double s = dscr[0];
-    for (int w = 1; w < NT / 32; ++w) s += dscr[w];
-    a.partials[row * a.splits + split] = make_float2(M, (float)s);
+  if (wid != 0) return;
+
+  int st = gok ? 0 : 64 /*BAD_GAMMA*/;
+  const int gg = st ? -1 : g;
+  float Mi = kMFloor;
+  double Li = 0.0;
+  int lst = 0;
+  bool acc = true;
+  double ratio = 0.0;
+  if (lane <= gg) {
+    Mi = s_M[lane];
+    Li = s_L[lane];
+    if (!(Li == Li) || !(Mi < FLT_MAX) || !(Li < 1e300)) lst |= 1;
+    else if (!(Li > 0.0)) lst |= 2;
+    if (lane < gg) {
+      if (!(dl == dl)) lst |= 1;
+      else if (!(dl > 0.f)) lst |= 2;
+      if (t < 0 || t >= a.V) lst |= 4;
+      else if (!lst) {
+        if (!(dpt > 0.f)) {
+          lst |= (dpt == 0.f) ? 8 : 1;
+        } else {
+          const double pt = exp2((double)xt * a.ct - (double)(Mi * a.ct)) / Li;
+          ratio = pt / (double)dpt;
+          acc = u24(w.x) < ratio;
+        }
+      }
+    }
+  }
+  // statuses of rows 0..g-1 always count; row g (target) only if it is sampled
+  const unsigned rej = __ballot_sync(0xffffffffu, lane < gg && !acc);
+  const int N = st ? 0 : (rej ? (__ffs(rej) - 1) : gg);
+  int all = lst;
+  if (lane == gg && N != gg) all = 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) all |= __shfl_xor_sync(0xffffffffu, all, o);
+  st |= all;
+  const float MN = __shfl_sync(0xffffffffu, Mi, st ? 0 : N);
+  const double LN = __shfl_sync(0xffffffffu, Li, st ? 0 : N);
+  const float dmN = __shfl_sync(0xffffffffu, dmv, N), dlN = __shfl_sync(0xffffffffu, dl, N);
+  const uint32_t w1N = __shfl_sync(0xffffffffu, w.y, N);
+  if (a.ratio && lane < k) a.ratio[b * k + lane] = (!st && lane < gg) ? (float)fmin(1.0, ratio) : kNaNf;
+  if (lane == 0) {
+    Decision dc;
+    dc.N = N;
+    dc.st = st;
+    dc.Mt = MN;
+    dc.Lt = LN;
+    const bool resid = !st && N < gg;
+    dc.dm = resid ? dmN : 0.f;
+    dc.dl = resid ? (double)dlN : 1.0;
+    dc.us = st ? 0.0 : u24(w1N);
+    dc.mode = resid ? 1 : 0;  // 1 = residual, 0 = target (bonus)
+    dc.pad = 0;
+    a.dec[b] = dc;
+    a.n_accept[b] = st ? 0 : N;
+    if (st) {
+      a.out_tok[b] = -1;
+      if (a.resid) a.resid[b] = kNaNf;
+      if (a.status) a.status[b] = st;
+    }
+  }
+}
+
+// Persistent warp-granular K4 over the items (b, i <= gamma_b, split), in sequence order.
+template <typename T>
+__global__ void __launch_bounds__(kRowsThreads, 3) sv_rows_kernel(const __grid_constant__ VerifyArgs a) {
+  constexpr int NT = kRowsThreads, NW = NT / 32;
+  __shared__ int s_pref[NT + 1];
+  __shared__ int s_wtot[NW];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  pdl_wait();
+  pdl_trigger();
+  const int splits = (int)a.splits;
+  const int64_t nwarps = (int64_t)gridDim.x * NW;
+  int64_t base = 0, my = (int64_t)blockIdx.x * NW + wid;
+  for (int b0 = 0; b0 < a.B; b0 += NT) {
+    const int nb = min(NT, a.B - b0);
+    int cnt = 0;
+    if (tid < nb) {
+      const int g = a.gamma[b0 + tid];
+      cnt = (g >= 0 && g <= a.k) ? (g + 1) * splits : 0;
+    }
+    int v = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += t;
+    }
+    __syncthreads();  // previous chunk's readers are done
+    if (lane == 31) s_wtot[wid] = v;
+    __syncthreads();
+    int off = 0;
+    for (int w = 0; w < wid; ++w) off += s_wtot[w];
+    s_pref[tid + 1] = v + off;
+    if (tid == 0) s_pref[0] = 0;
+    __syncthreads();
+    const int total = s_pref[nb];
+    for (; my < base + total; my += nwarps) {
+      const int local = (int)(my - base);
+      int lo = 0, hi = nb - 1;  // largest j with s_pref[j] <= local (empty sequences skipped)
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_pref[mid] <= local) lo = mid;
+        else hi = mid - 1;
+      }
+      const int64_t b = b0 + lo;
+      const int rem = local - s_pref[lo];
+      const int i = rem / splits, split = rem - i * splits;
+      const float2 p = rows_warp_item<T>(a, b, i, split);
+      if (lane == 0) a.partials[(b * (a.k + 1) + i) * a.splits + split] = p;
+    }
+    base += total;
   }
 }
 
 // ------------------------------------------------------------------ K5
-struct SampleSmemTail {
-  uint64_t bar;
-  int N, st, gamma, mode;
-  float Mt, dm;
-  double Lt, dl, us;
-  double wsum[kSampleThreads / 32];
-  double zslot[2];  // this CTA's chunk mass, per pass
-  int found_tok;
+template <typename T>
+struct SampleRow {
+  const T *t, *d;  // target / draft row N_b
+  float ct, nmt, ilt, cd, nmd, ild;
 };
 
 template <typename T>
-struct SampleCtx {
-  const T *st_, *sd_;
-  int n, units, NW;
-  bool resid;
-  float ct, cd, nmt, nmd, ilt, ild;
-  __device__ __forceinline__ float r_at(int e) const {
-    const float pt = ex2(fmaf(Elem<T>::load(st_ + e), ct, nmt)) * ilt;
-    if (!resid) return pt;
-    const float pd = ex2(fmaf(Elem<T>::load(sd_ + e), cd, nmd)) * ild;
-    return fmaxf(0.f, pt - pd);
-  }
-  // fp64 mass of one 16-byte unit (elements in order)
-  __device__ __forceinline__ double unit_mass(int u) const {
-    constexpr int EPU = Elem<T>::kPerUnit;
-    double v = 0.0;
-    const int e0 = u * EPU;
-    if (e0 + EPU <= n) {
+__device__ __forceinline__ SampleRow<T> sample_row(const VerifyArgs &a, const Decision &dc, int64_t b) {
+  SampleRow<T> r;
+  r.t = reinterpret_cast<const T *>(a.t) + b * a.t_sb + (int64_t)dc.N * a.t_si;
+  r.d = reinterpret_cast<const T *>(a.d) + b * a.d_sb + (int64_t)dc.N * a.d_si;
+  r.ct = a.ct;
+  r.nmt = -(dc.Mt * a.ct);
+  r.ilt = (float)(1.0 / dc.Lt);
+  r.cd = a.cd;
+  r.nmd = -(dc.dm * a.cd);
+  r.ild = (float)(1.0 / dc.dl);
+  return r;
+}
+
+// This lane's EPT contiguous elements of warp slice s: r_v (residual when kMode = 1, else p_t)
+// and, in vocabulary order, their fp64 sum (and the fp64 sum of p_t, the R10 fallback mass).
+template <typename T, int kMode, bool kKeep>
+__device__ __forceinline__ void slice_lane(const VerifyArgs &a, const SampleRow<T> &sr, int64_t s, float *r,
+                                           double &sum, double &sum_t) {
+  constexpr int EPU = Elem<T>::kPerUnit, UPT = kSampleUnitsPerThread, EPT = UPT * EPU;
+  const int lane = threadIdx.x & 31;
+  const int64_t v0 = s * a.slice + (int64_t)lane * EPT;
+  const int n = (int)max((int64_t)0, min((int64_t)EPT, (int64_t)a.V - v0));
+  const T *tp = sr.t + v0, *dp = sr.d + v0;
+  const bool vec = n == EPT && ((reinterpret_cast<uintptr_t>(tp) & 15) == 0) &&
+                   (!kMode || (reinterpret_cast<uintptr_t>(dp) & 15) == 0);
+  sum = 0.0;
+  sum_t = 0.0;
+  if (vec) {
+    uint4 ut[UPT], ud[kMode ? UPT : 1];
+#pragma unroll
+    for (int q = 0; q < UPT; ++q) ut[q] = *reinterpret_cast<const uint4 *>(tp + q * EPU);
+    if (kMode) {
+#pragma unroll
+      for (int q = 0; q < UPT; ++q) ud[q] = *reinterpret_cast<const uint4 *>(dp + q * EPU);
+    }
+#pragma unroll
+    for (int q = 0; q < UPT; ++q) {
       float xt[EPU], xd[EPU];
-      Elem<T>::unit(*reinterpret_cast<const uint4 *>(st_ + e0), xt);
-      if (resid) Elem<T>::unit(*reinterpret_cast<const uint4 *>(sd_ + e0), xd);
+      Elem<T>::unit(ut[q], xt);
+      if (kMode) Elem<T>::unit(ud[q], xd);
 #pragma unroll
-      for (int j = 0; j < EPU; ++j) {
-        const float pt = ex2(fmaf(xt[j], ct, nmt)) * ilt;
-        float r = pt;
-        if (resid) r = fmaxf(0.f, pt - ex2(fmaf(xd[j], cd, nmd)) * ild);
-        v += (double)r;
+      for (int e = 0; e < EPU; ++e) {
+        const float pt = ex2(fmaf(xt[e], sr.ct, sr.nmt)) * sr.ilt;
+        const float v = kMode ? fmaxf(0.f, pt - ex2(fmaf(xd[e], sr.cd, sr.nmd)) * sr.ild) : pt;
+        if (kKeep) r[q * EPU + e] = v;
+        sum += (double)v;
+        if (kMode) sum_t += (double)pt;
       }
-    } else {
-      for (int e = e0; e < n; ++e) v += (double)r_at(e);
     }
-    return v;
+  } else {
+    for (int e = 0; e < EPT; ++e) {
+      float v = 0.f, pt = 0.f;
+      if (e < n) {
+        pt = ex2(fmaf(Elem<T>::load(tp + e), sr.ct, sr.nmt)) * sr.ilt;
+        v = kMode ? fmaxf(0.f, pt - ex2(fmaf(Elem<T>::load(dp + e), sr.cd, sr.nmd)) * sr.ild) : pt;
+      }
+      if (kKeep) r[e] = v;
+      sum += (double)v;
+      if (kMode) sum_t += (double)pt;
+    }
   }
-};
+  if (!kMode) sum_t = sum;
+}
 
+// Exclusive / inclusive warp prefix (fixed Kogge-Stone order).
+__device__ __forceinline__ void warp_scan_d(double v, double &incl, double &excl) {
+  const int lane = threadIdx.x & 31;
+  incl = warp_incl_scan_d(v, lane);
+  excl = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) excl = 0.0;
+}
+
+// The sequence's last warp: Z, theta = u_s Z, the owning slice, then the token inside it.
+// Prefixes over slices: chunks of 32 slices, warp scan per chunk, running total across chunks
+// (all in fp64, fixed order); the owning slice is the first q with P_q + m_q > theta, and
+// inside it the same test is repeated on the lanes' scan -- bit-identical at the slice end,
+// so a crossing lane always exists.
 template <typename T>
-__global__ void __launch_bounds__(kSampleThreads) sv_sample_kernel(const VerifyArgs a) {
-  constexpr int NT = kSampleThreads, NW = NT / 32, EPU = Elem<T>::kPerUnit;
-  cg::cluster_group cluster = cg::this_cluster();
-  const int cs = a.cs;
-  const int rank = (int)cluster.block_rank();
-  const int64_t b = blockIdx.x / cs;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int k = a.k;
-  extern __shared__ __align__(128) uint8_t smem[];
-  const size_t cbytes = (size_t)a.chunk * sizeof(T);
-  T *s_t = reinterpret_cast<T *>(smem);
-  T *s_d = reinterpret_cast<T *>(smem + cbytes);
-  SampleSmemTail *tl = reinterpret_cast<SampleSmemTail *>(smem + 2 * cbytes);
-  const float nanf_ = __int_as_float(0x7fc00000);
-
-  // ---------------- prologue (warp 0): merge row partials, accept tests, N_b
-  if (wid == 0) {
-    const int g = a.gamma[b];
-    int st = (g < 0 || g > k) ? 64 /*BAD_GAMMA*/ : 0;
-    const int gg = st ? -1 : g;
-    float Mi = kMFloor;
-    double Li = 0.0;
-    int lst = 0;
-    bool acc = true;
-    double ratio = 0.0;
-    if (lane <= gg) {
-      const float2 *pp = a.partials + ((int64_t)b * (k + 1) + lane) * a.splits;
-      for (int s = 0; s < a.splits; ++s) Mi = fmaxf(Mi, pp[s].x);
-      for (int s = 0; s < a.splits; ++s) Li += (double)pp[s].y * ex2((pp[s].x - Mi) * a.ct);
-      if (!(Li == Li) || !(Mi < FLT_MAX) || !(Li < 1e300)) lst |= 1;
-      else if (!(Li > 0.0)) lst |= 2;
-      if (lane < gg) {
-        const int64_t ri = b * k + lane;
-        const int t = a.tok[ri];
-        const float dl = a.dl[ri], dpt = a.dpt[ri];
-        if (!(dl == dl)) lst |= 1;
-        else if (!(dl > 0.f)) lst |= 2;
-        if (t < 0 || t >= a.V) lst |= 4;
-        else if (!lst) {
-          if (!(dpt > 0.f)) {
-            lst |= (dpt == 0.f) ? 8 : 1;
-          } else {
-            const T *trow = reinterpret_cast<const T *>(a.t) + b * a.t_sb + lane * a.t_si;
-            const float xt = Elem<T>::load(trow + t);
-            const double pt = exp2((double)xt * a.ct - (double)(Mi * a.ct)) / Li;
-            ratio = pt / (double)dpt;
-            const uint4 w = sv_philox(a.seed, a.offset, a.seq_base + b, lane);
-            acc = u24(w.x) < ratio;
-          }
-        }
-      }
-    }
-    // statuses of rows 0..g-1 always count; row g (target) only if it is sampled
-    const unsigned rej = __ballot_sync(0xffffffffu, lane < gg && !acc);
-    const int N = st ? 0 : (rej ? (__ffs(rej) - 1) : gg);
-    int all = lst;
-    if (lane == gg && N != gg) all = 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) all |= __shfl_xor_sync(0xffffffffu, all, o);
-    st |= all;
-    const float MN = __shfl_sync(0xffffffffu, Mi, st ? 0 : N);
-    const double LN = __shfl_sync(0xffffffffu, Li, st ? 0 : N);
-    if (rank == 0 && lane < k) {
-      float out = nanf_;
-      if (!st && lane < gg) out = (float)fmin(1.0, ratio);
-      if (a.ratio) a.ratio[b * k + lane] = out;
-    }
-    if (lane == 0) {
-      tl->N = N;
-      tl->st = st;
-      tl->gamma = gg;
-      tl->Mt = MN;
-      tl->Lt = LN;
-      if (!st && N < gg) {
-        tl->dm = a.dm[b * k + N];
-        tl->dl = (double)a.dl[b * k + N];
-      } else {
-        tl->dm = 0.f;
-        tl->dl = 1.0;
-      }
-      tl->us = st ? 0.0 : u24(sv_philox(a.seed, a.offset, a.seq_base + b, N).y);
-      tl->mode = (!st && N < gg) ? 1 : 0;  // 1 = residual, 0 = target (bonus)
-      tl->found_tok = -1;
-      mbar_init(&tl->bar, 1);
-      fence_mbar_init();
-    }
-  }
-  __syncthreads();
-  const int N = tl->N;
-  int st = tl->st;
-  if (st) {
-    if (rank == 0 && tid == 0) {
-      a.n_accept[b] = 0;
-      a.out_tok[b] = -1;
-      if (a.resid) a.resid[b] = nanf_;
-      if (a.status) a.status[b] = st;
-    }
-    return;  // uniform over the whole cluster: no cluster barrier was entered
-  }
-  const bool resid0 = tl->mode == 1;
-
-  // ---------------- load this CTA's chunk of target row N (+ draft row N)
-  const int64_t v0 = (int64_t)rank * a.chunk;
-  const int n = (int)max((int64_t)0, min(a.chunk, (int64_t)a.V - v0));
-  const T *gt = reinterpret_cast<const T *>(a.t) + b * a.t_sb + (int64_t)N * a.t_si + v0;
-  const T *gd = reinterpret_cast<const T *>(a.d) + b * a.d_sb + (int64_t)N * a.d_si + v0;
-  const int units_full = n / EPU;
-  const bool bulk = units_full > 0 && (reinterpret_cast<uintptr_t>(gt) & 15) == 0 &&
-                    (!resid0 || (reinterpret_cast<uintptr_t>(gd) & 15) == 0);
-  const int bulk_units = bulk ? units_full : 0;
-  if (tid == 0 && bulk) {
-    const uint32_t bytes = (uint32_t)bulk_units * 16u;
-    mbar_arrive_expect_tx(&tl->bar, resid0 ? 2u * bytes : bytes);
-    bulk_g2s(s_t, gt, bytes, &tl->bar);
-    if (resid0) bulk_g2s(s_d, gd, bytes, &tl->bar);
-  }
-  for (int e = bulk_units * EPU + tid; e < n; e += NT) {
-    s_t[e] = gt[e];
-    if (resid0) s_d[e] = gd[e];
-  }
-  __syncthreads();
-  if (bulk) mbar_wait(&tl->bar, 0);
-
-  SampleCtx<T> cx;
-  cx.st_ = s_t;
-  cx.sd_ = s_d;
-  cx.n = n;
-  cx.units = (n + EPU - 1) / EPU;
-  cx.NW = NW;
-  cx.ct = a.ct;
-  cx.cd = a.cd;
-  cx.nmt = -(tl->Mt * a.ct);
-  cx.ilt = (float)(1.0 / tl->Lt);
-  cx.nmd = -(tl->dm * a.cd);
-  cx.ild = (float)(1.0 / tl->dl);
-  const int Uw = (cx.units + NW - 1) / NW;
-  const int wbeg = min(cx.units, wid * Uw), wend = min(cx.units, (wid + 1) * Uw);
-
+__global__ void __launch_bounds__(256) sv_find_kernel(const __grid_constant__ VerifyArgs a) {
+  constexpr int EPT = kSampleUnitsPerThread * Elem<T>::kPerUnit;
+  const int lane = threadIdx.x & 31;
+  pdl_wait();
+  pdl_trigger();
+  const int64_t b = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (b >= a.B) return;
+  const Decision dc = a.dec[b];
+  if (dc.st) return;  // K4b wrote the sentinels
+  const SampleRow<T> sr = sample_row<T>(a, dc, b);
+  const int nsl = a.nsl;
+  int mode = dc.mode, st = 0;
+  const double *sm = a.smass + b * 2 * (int64_t)nsl;
+  // Z: first the residual masses; R10 (Z = 0) falls back to the target masses (same row).
+  // Slices go in chunks of 32 (one warp scan each, running total across chunks); the loads of
+  // kFindChunks chunks are issued together.
+  double Z = 0.0;
   for (int pass = 0; pass < 2; ++pass) {
-    cx.resid = resid0 && pass == 0;
-    // per-warp mass: rounds of 32 units, lane value = in-unit sequential fp64 sum,
-    // round total = lane 31 of the inclusive warp scan, summed round by round
-    double R = 0.0;
-    for (int base = wbeg; base < wend; base += 32) {
-      const int u = base + lane;
-      const double v = (u < wend) ? cx.unit_mass(u) : 0.0;
-      const double incl = warp_incl_scan_d(v, lane);
-      R += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    if (lane == 0) tl->wsum[wid] = R;
-    __syncthreads();
-    if (tid == 0) {
-      double z = 0.0;
-      for (int w = 0; w < NW; ++w) z += tl->wsum[w];
-      tl->zslot[pass] = z;
-    }
-    cluster.sync();  // chunk masses of this pass visible cluster-wide
-    // warp 0 fetches the chunk masses (lane r <- rank r) and walks them in rank order
-    __shared__ double s_Z, s_Pc, s_Zc;
-    __shared__ int s_owner;
-    if (wid == 0) {
-      const double zr = lane < cs ? cluster.map_shared_rank(tl->zslot, lane)[pass] : 0.0;
-      double Zs = 0.0;
-      for (int r = 0; r < cs; ++r) Zs += __shfl_sync(0xffffffffu, zr, r);
-      const double th = tl->us * Zs;
-      double P = 0.0, Pc_ = 0.0, Zc_ = -1.0;
-      int own = -1, last_pos = -1;
-      for (int r = 0; r < cs; ++r) {
-        const double z = __shfl_sync(0xffffffffu, zr, r);
-        if (z > 0.0) last_pos = r;
-        if (own < 0 && P + z > th) {
-          own = r;
-          Pc_ = P;
-          Zc_ = z;
-        }
-        P += z;
+    const double *mq = sm + (mode ? 0 : nsl);
+    double run = 0.0;
+    for (int c0 = 0; c0 < nsl; c0 += 32 * kFindChunks) {
+      double m[kFindChunks];
+#pragma unroll
+      for (int j = 0; j < kFindChunks; ++j) {
+        const int q = c0 + 32 * j + lane;
+        m[j] = q < nsl ? __ldcg(mq + q) : 0.0;
       }
-      if (own < 0) {  // rounding: no crossing -> last CTA with mass
-        own = last_pos;
-        Pc_ = 0.0;
-        Zc_ = -1.0;
-      }
-      if (lane == 0) {
-        s_Z = Zs;
-        s_Pc = Pc_;
-        s_Zc = Zc_;
-        s_owner = own;
+#pragma unroll
+      for (int j = 0; j < kFindChunks; ++j) {
+        if (c0 + 32 * j >= nsl) break;
+        double incl, excl;
+        warp_scan_d(m[j], incl, excl);
+        run += __shfl_sync(0xffffffffu, incl, 31);
       }
     }
-    __syncthreads();
-    const double Z = s_Z, Pc = s_Pc, Zc = s_Zc;
-    const int owner = s_owner;
-    if (cx.resid && !(Z > 0.0)) {  // DESIGN R10: residual mass 0 -> sample p_t instead
-      st |= 32;
-      cluster.sync();  // keep zslot[0] alive until every CTA has read it
+    Z = run;
+    if (mode == 1 && !(Z > 0.0)) {
+      mode = 0;
+      st = 32;  // SV_ROW_RESID_ZERO
       continue;
     }
-    const double theta = tl->us * Z;
-    if (rank == owner) {
-      // level 2: the warp whose range crosses theta (thread 0, fixed order)
-      __shared__ int s_w;
-      __shared__ double s_Q;
-      if (tid == 0) {
-        int w_star = -1, w_last = -1;
-        double Q = Pc, Qs = 0.0;
-        const bool exact = Zc >= 0.0;
-        for (int w = 0; w < NW; ++w) {
-          if (tl->wsum[w] > 0.0) w_last = w;
-          if (w_star < 0 && exact && Q + tl->wsum[w] > theta) {
-            w_star = w;
-            Qs = Q;
-          }
-          Q += tl->wsum[w];
-        }
-        if (w_star < 0) {
-          w_star = w_last;
-          Qs = -1.0;  // fallback marker: take the last positive element of that warp
-        }
-        s_w = w_star;
-        s_Q = Qs;
-      }
-      __syncthreads();
-      if (wid == s_w) {
-        // level 3: rounds of the warp; level 4: in-lane sequential scan
-        const bool exact = s_Q >= 0.0;
-        double Rq = s_Q;
-        int tok = -1, last_u = -1;
-        for (int base = wbeg; base < wend && tok < 0; base += 32) {
-          const int u = base + lane;
-          const double v = (u < wend) ? cx.unit_mass(u) : 0.0;
-          const double incl = warp_incl_scan_d(v, lane);
-          const unsigned pos = __ballot_sync(0xffffffffu, v > 0.0);
-          if (pos) last_u = base + 31 - __clz(pos);
-          const unsigned cross = exact ? __ballot_sync(0xffffffffu, Rq + incl > theta) : 0u;
-          if (cross) {
-            const int ls = __ffs(cross) - 1;
-            const double excl = __shfl_sync(0xffffffffu, incl, ls > 0 ? ls - 1 : 0);
-            if (lane == ls) {
-              double cum = Rq + (ls > 0 ? excl : 0.0);
-              const int e0 = u * EPU, e1 = min(n, e0 + EPU);
-              int lastp = -1;
-              for (int e = e0; e < e1; ++e) {
-                const float r = cx.r_at(e);
-                if (r > 0.f) lastp = e;
-                cum += (double)r;
-                if (cum > theta) {
-                  tok = e;
-                  break;
-                }
-              }
-              if (tok < 0) tok = lastp;
-            }
-            tok = __shfl_sync(0xffffffffu, tok, ls);
-            break;
-          }
-          Rq += __shfl_sync(0xffffffffu, incl, 31);
-        }
-        if (tok < 0 && last_u >= 0 && lane == 0) {  // fallback: last positive element
-          const int e0 = last_u * EPU, e1 = min(n, e0 + EPU);
-          for (int e = e0; e < e1; ++e)
-            if (cx.r_at(e) > 0.f) tok = e;
-        }
-        if (lane == 0) a.out_tok[b] = (int)(v0 + tok);
-      }
-    }
-    if (rank == 0 && tid == 0) {
-      a.n_accept[b] = N;
-      if (a.resid) a.resid[b] = (float)Z;
-      if (a.status) a.status[b] = st;
-    }
-    cluster.sync();  // no CTA exits while others may still read its zslot
     break;
+  }
+  const double theta = dc.us * Z;
+  const double *mq = sm + (mode ? 0 : nsl);
+  double run = 0.0, Pc = 0.0;
+  int own = -1, last_pos = -1;
+  for (int c0 = 0; c0 < nsl; c0 += 32 * kFindChunks) {
+    double mm[kFindChunks];
+#pragma unroll
+    for (int j = 0; j < kFindChunks; ++j) {
+      const int q = c0 + 32 * j + lane;
+      mm[j] = q < nsl ? __ldcg(mq + q) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < kFindChunks; ++j) {
+      const int cj = c0 + 32 * j;
+      if (cj >= nsl) break;
+      const bool valid = cj + lane < nsl;
+      const double m = mm[j];
+      double incl, excl;
+      warp_scan_d(m, incl, excl);
+      const double P = run + excl;
+      const unsigned pos = __ballot_sync(0xffffffffu, valid && m > 0.0);
+      if (pos) last_pos = cj + 31 - __clz(pos);
+      if (own < 0) {
+        const unsigned cross = __ballot_sync(0xffffffffu, valid && P + m > theta);
+        if (cross) {
+          const int l = __ffs(cross) - 1;
+          own = cj + l;
+          Pc = __shfl_sync(0xffffffffu, P, l);
+        }
+      }
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+  const bool exact = own >= 0;
+  if (!exact) own = last_pos;
+  int tok = -1;
+  if (own >= 0) {
+    float r[EPT];
+    double mine, mine_t;
+    if (mode) slice_lane<T, 1, true>(a, sr, own, r, mine, mine_t);
+    else slice_lane<T, 0, true>(a, sr, own, r, mine, mine_t);
+    double incl, excl;
+    warp_scan_d(mine, incl, excl);
+    // crossing lane (exact), else the last lane with mass (fallback)
+    const unsigned sel = exact ? __ballot_sync(0xffffffffu, Pc + incl > theta) : __ballot_sync(0xffffffffu, mine > 0.0);
+    if (sel) {
+      const int ls = exact ? __ffs(sel) - 1 : 31 - __clz(sel);
+      if (lane == ls) {
+        double cum = Pc + excl;
+        int lastp = -1;
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+          if (r[e] > 0.f) lastp = e;
+          cum += (double)r[e];
+          if (exact && tok < 0 && cum > theta) tok = e;
+        }
+        if (tok < 0) tok = lastp;  // rounding left no crossing: the last positive element
+        if (tok >= 0) tok = (int)((int64_t)own * a.slice + (int64_t)ls * EPT + tok);
+      }
+      tok = __shfl_sync(0xffffffffu, tok, ls);
+    }
+  }
+  if (lane == 0) {
+    a.out_tok[b] = tok;
+    if (a.resid) a.resid[b] = (float)Z;
+    if (a.status) a.status[b] = st;
+  }
+}
+
+// Persistent warp-granular K5 over the B x nsl warp slices: per slice the residual mass and
+// the target mass (the R10 fallback), each the lane-31 value of a fixed-order warp scan.
+template <typename T>
+__global__ void __launch_bounds__(kSampleThreads, 3) sv_resid_kernel(const __grid_constant__ VerifyArgs a) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  pdl_wait();
+  pdl_trigger();
+  const int64_t nwarps = (int64_t)gridDim.x * (kSampleThreads / 32);
+  const int64_t items = (int64_t)a.B * a.nsl;
+  for (int64_t it = (int64_t)blockIdx.x * (kSampleThreads / 32) + wid; it < items; it += nwarps) {
+    const int64_t b = it / a.nsl, s = it - b * a.nsl;
+    const Decision dc = a.dec[b];
+    if (dc.st) continue;  // K4b wrote the sentinels
+    const SampleRow<T> sr = sample_row<T>(a, dc, b);
+    double mine, mine_t;
+    if (dc.mode) slice_lane<T, 1, false>(a, sr, s, nullptr, mine, mine_t);
+    else slice_lane<T, 0, false>(a, sr, s, nullptr, mine, mine_t);
+    double incl, excl, incl_t, excl_t;
+    warp_scan_d(mine, incl, excl);
+    warp_scan_d(mine_t, incl_t, excl_t);
+    if (lane == 31) {
+      double *sm = a.smass + b * 2 * (int64_t)a.nsl;
+      sm[s] = incl;
+      sm[a.nsl + s] = incl_t;
+    }
   }
 }
 
 }  // namespace
 
+int64_t verify_ws_bytes(int64_t B, int k, int64_t splits, int nsl) {
+  return ws_round(B * (k + 1) * splits * 8) + ws_round(B * (int64_t)sizeof(Decision)) + ws_round(B * nsl * 16);
+}
+
 cudaError_t launch_verify(const VerifyArgs &a, cudaStream_t st) {
-  // K4
+  // K4: persistent over the compacted (sequence, row <= gamma, split) items
   {
-    const int64_t grid = (int64_t)a.B * (a.k + 1) * a.splits;
-    if (a.bf16)
-      sv_rows_kernel<__nv_bfloat16><<<(unsigned)grid, kRowsThreads, 0, st>>>(a);
-    else
-      sv_rows_kernel<float><<<(unsigned)grid, kRowsThreads, 0, st>>>(a);
-    cudaError_t e = cudaGetLastError();
+    const void *fn = a.bf16 ? (const void *)sv_rows_kernel<__nv_bfloat16> : (const void *)sv_rows_kernel<float>;
+    const int64_t need = ((int64_t)a.B * (a.k + 1) * a.splits + kRowsThreads / 32 - 1) / (kRowsThreads / 32);
+    const int64_t grid = need < resident_grid(fn, kRowsThreads, 0) ? need : resident_grid(fn, kRowsThreads, 0);
+    cudaError_t e = a.bf16 ? launch_k(sv_rows_kernel<__nv_bfloat16>, dim3((unsigned)grid), dim3(kRowsThreads), 0, st, a)
+                           : launch_k(sv_rows_kernel<float>, dim3((unsigned)grid), dim3(kRowsThreads), 0, st, a);
     if (e != cudaSuccess) return e;
   }
-  // K5
-  const int elem = a.bf16 ? 2 : 4;
-  const size_t smem = 2 * (size_t)a.chunk * elem + sizeof(SampleSmemTail);
-  const void *fn = a.bf16 ? (const void *)sv_sample_kernel<__nv_bfloat16> : (const void *)sv_sample_kernel<float>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // K4b
+  cudaError_t e = a.bf16 ? launch_k(sv_decide_kernel<__nv_bfloat16>, dim3((unsigned)a.B), dim3(32 * (a.k + 1)), 0, st, a)
+                         : launch_k(sv_decide_kernel<float>, dim3((unsigned)a.B), dim3(32 * (a.k + 1)), 0, st, a);
   if (e != cudaSuccess) return e;
-  if (a.cs > 8) {
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)((int64_t)a.B * a.cs));
-  cfg.blockDim = dim3(kSampleThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = a.cs;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (a.bf16) return cudaLaunchKernelEx(&cfg, sv_sample_kernel<__nv_bfloat16>, a);
-  return cudaLaunchKernelEx(&cfg, sv_sample_kernel<float>, a);
+  // K5
+  const void *fn = a.bf16 ? (const void *)sv_resid_kernel<__nv_bfloat16> : (const void *)sv_resid_kernel<float>;
+  const int64_t need = ((int64_t)a.B * a.nsl + kSampleThreads / 32 - 1) / (kSampleThreads / 32);
+  const int64_t grid = need < resident_grid(fn, kSampleThreads, 0) ? need : resident_grid(fn, kSampleThreads, 0);
+  e = a.bf16 ? launch_k(sv_resid_kernel<__nv_bfloat16>, dim3((unsigned)grid), dim3(kSampleThreads), 0, st, a)
+             : launch_k(sv_resid_kernel<float>, dim3((unsigned)grid), dim3(kSampleThreads), 0, st, a);
+  if (e != cudaSuccess) return e;
+  // K5b
+  const unsigned fgrid = (unsigned)((a.B + 7) / 8);
+  return a.bf16 ? launch_k(sv_find_kernel<__nv_bfloat16>, dim3(fgrid), dim3(256), 0, st, a)
+                : launch_k(sv_find_kernel<float>, dim3(fgrid), dim3(256), 0, st, a);
 }
 
 }  // namespace sv

@@ -21,6 +21,11 @@ int tune_knob(const char *name, int dflt) {
   return (v && *v) ? atoi(v) : dflt;
 }
 
+bool pdl_enabled() {
+  static const bool on = tune_knob("SV_PDL", 1) != 0;
+  return on;
+}
+
 int cluster_size_for(int64_t V, int elem_bytes) {
   static const int budget = tune_knob("SV_CHUNK_PAIR_KB", kChunkPairBudget / 1024) * 1024;
   for (int cs = 1; cs <= kMaxCluster; cs <<= 1) {
@@ -42,7 +47,7 @@ int64_t chunk_elems_for(int64_t V, int cs) {
 }
 
 int64_t rows_splits_for(int64_t V, int elem_bytes) {
-  const int64_t per = (int64_t)kRowsThreads * kRowUnitsPerThread * (16 / elem_bytes);
+  const int64_t per = (int64_t)32 * kRowUnitsPerThread * (16 / elem_bytes);
   return (V + per - 1) / per;
 }
 
@@ -89,8 +94,17 @@ int resident_grid(const void *fn, int threads, int smem) {
 }
 
 
+static int64_t sample_slice_for(int elem_bytes) {
+  return (int64_t)32 * kSampleUnitsPerThread * (16 / elem_bytes);
+}
+
+static int sample_slices_for(int64_t V, int elem_bytes) {
+  const int64_t s = sample_slice_for(elem_bytes);
+  return (int)((V + s - 1) / s);
+}
+
 static int64_t rows_chunk_for(int elem_bytes) {
-  return (int64_t)kRowsThreads * kRowUnitsPerThread * (16 / elem_bytes);
+  return (int64_t)32 * kRowUnitsPerThread * (16 / elem_bytes);
 }
 
 int64_t score_ws_bytes(int64_t rows, int cs) {
@@ -130,7 +144,7 @@ extern "C" {
 size_t sv_workspace_bytes(int32_t B, int32_t k, int32_t V, int32_t dtype) {
   if (shape_check(B, k, V, dtype) != SV_OK) return 0;
   const int eb = elem_bytes(dtype);
-  return (size_t)(verify_ws_offset(B, k, V, eb) + ws_round((int64_t)B * (k + 1) * rows_splits_for(V, eb) * 8));
+  return (size_t)(verify_ws_offset(B, k, V, eb) + verify_ws_bytes(B, k, rows_splits_for(V, eb), sample_slices_for(V, eb)));
 }
 
 const char *sv_status_string(int32_t s) {
@@ -290,11 +304,18 @@ int32_t sd_verify(const sv_logits *draft, const sv_logits *target, const int32_t
   a.ratio = accept_ratio;
   a.resid = resid_mass;
   a.status = row_status;
-  a.partials = reinterpret_cast<float2 *>(reinterpret_cast<uint8_t *>(workspace) + verify_ws_offset(B, k, V, eb));
   a.splits = rows_splits_for(V, eb);
   a.rows_chunk = rows_chunk_for(eb);
-  a.cs = cluster_size_for(V, eb);
-  a.chunk = chunk_elems_for(V, a.cs);
+  a.slice = sample_slice_for(eb);
+  a.nsl = sample_slices_for(V, eb);
+  {
+    uint8_t *w = reinterpret_cast<uint8_t *>(workspace) + verify_ws_offset(B, k, V, eb);
+    a.partials = reinterpret_cast<float2 *>(w);
+    w += ws_round((int64_t)B * (k + 1) * a.splits * 8);
+    a.dec = reinterpret_cast<Decision *>(w);
+    w += ws_round((int64_t)B * (int64_t)sizeof(Decision));
+    a.smass = reinterpret_cast<double *>(w);
+  }
   a.bf16 = draft->dtype == SV_BF16;
   cudaError_t e = launch_verify(a, (cudaStream_t)stream);
   if (e != cudaSuccess) {

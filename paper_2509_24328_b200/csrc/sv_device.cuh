@@ -147,6 +147,14 @@ __device__ __forceinline__ uint4 ldg_stream(const void *p) {
   return r;
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every libsv kernel is launched with programmatic stream serialization (PDL): it may start
+// while the previous kernel on the stream drains, so it first waits for that grid's completion
+// and memory flush (a no-op when launched without the attribute), then lets its own dependent
+// launch as early as possible.  Nothing is read from global memory before pdl_wait().
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- reductions
 // Fixed butterfly order: the result depends only on the lane -> value mapping.
 __device__ __forceinline__ float warp_max(float v) {

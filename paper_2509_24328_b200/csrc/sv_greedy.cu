@@ -26,6 +26,8 @@ __device__ __forceinline__ bool before(double ga, int ia, double gb, int ib) {
 }
 
 __global__ void __launch_bounds__(kGreedyThreads) sv_greedy_kernel(const ScheduleArgs a, int npow2) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) uint8_t smem[];
   double *g = reinterpret_cast<double *>(smem);
   int *id = reinterpret_cast<int *>(g + npow2);
@@ -123,8 +125,7 @@ cudaError_t launch_schedule_greedy(const ScheduleArgs &a, cudaStream_t st) {
   const size_t smem = (size_t)npow2 * (sizeof(double) + sizeof(int));
   cudaError_t e = cudaFuncSetAttribute(sv_greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  sv_greedy_kernel<<<1, kGreedyThreads, smem, st>>>(a, npow2);
-  return cudaGetLastError();
+  return launch_k(sv_greedy_kernel, dim3(1), dim3(kGreedyThreads), smem, st, a, npow2);
 }
 
 }  // namespace sv

@@ -26,8 +26,10 @@ constexpr int kSampleThreads = 256;
 // dtype only, so reductions are identical for any B and any GPU count).
 constexpr int kChunkPairBudget = 80 * 1024;
 constexpr int kMaxCluster = 16;
-// sd_verify phase-1 chunk: 16 x 16-byte loads in flight per thread.
+// sd_verify K4: 8 x 16-byte loads in flight per thread per (row, split) item.
 constexpr int kRowUnitsPerThread = 8;
+// sd_verify K5: every lane owns 4 contiguous 16-byte units of a warp slice.
+constexpr int kSampleUnitsPerThread = 4;
 
 int cluster_size_for(int64_t V, int elem_bytes);     // 0 = unsupported
 int score_splits_for(int64_t V);                     // sv_score chunks per row
@@ -38,6 +40,23 @@ int64_t rows_splits_for(int64_t V, int elem_bytes);  // sd_verify phase-1 CTAs p
 int max_active_clusters(const void *fn, cudaLaunchConfig_t cfg, int smem, int cs);
 // co-resident CTAs of a persistent kernel on this device (cached)
 int resident_grid(const void *fn, int threads, int smem);
+
+// Launch with programmatic stream serialization (PDL, see sv_device.cuh); SV_PDL=0 disables it.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
 
 __host__ __device__ inline int64_t ws_round(int64_t x) { return (x + 255) / 256 * 256; }
 
@@ -75,6 +94,13 @@ struct ScheduleArgs {
 };
 cudaError_t launch_schedule(const ScheduleArgs &a, cudaStream_t st);
 
+// Per-sequence verification decision (K4's last CTA of the sequence -> K5).
+struct Decision {
+  double Lt, dl, us;  // target normaliser of row N, draft normaliser of row N, sampling uniform
+  float Mt, dm;       // raw maxima of the target / draft row N
+  int32_t N, st, mode, pad;  // first rejection, status bits, 1 = residual / 0 = target sample
+};
+
 struct VerifyArgs {
   const void *d, *t;
   int64_t d_sb, d_si, t_sb, t_si;
@@ -87,12 +113,16 @@ struct VerifyArgs {
   int32_t *n_accept, *out_tok;
   float *ratio, *resid;
   int32_t *status;
-  float2 *partials;  // [B, k+1, splits] (max, sum-exp)
+  float2 *partials;  // workspace: [B, k+1, splits] (max, sum-exp)
   int64_t splits, rows_chunk;
-  int64_t chunk;  // sampler per-CTA elements
-  int cs;
+  Decision *dec;       // workspace: [B]
+  double *smass;       // workspace: [B][2][nsl] residual and target mass per vocabulary slice
+  int64_t slice;       // K5 elements per slice
+  int nsl;             // K5 slices per row
   int bf16;
 };
+// sd_verify's share of the workspace
+int64_t verify_ws_bytes(int64_t B, int k, int64_t splits, int nsl);
 cudaError_t launch_verify(const VerifyArgs &a, cudaStream_t st);
 
 }  // namespace sv

@@ -19,8 +19,9 @@ namespace sv {
 
 namespace {
 
-__device__ __forceinline__ double phat_at(const float *p, int64_t idx, int &st) {
-  const float v = p[idx];
+constexpr int kMaxK = 16;  // SV_MAX_K
+
+__device__ __forceinline__ double phat_val(float v, int &st) {
   if (!(fabsf(v) <= FLT_MAX)) {  // NaN / inf -> 0 (SV_ROW_PHAT_BAD)
     st |= 16;
     return 0.0;
@@ -28,14 +29,23 @@ __device__ __forceinline__ double phat_at(const float *p, int64_t idx, int &st) 
   return (double)v;
 }
 
-__global__ void __launch_bounds__(128) sv_schedule_row_kernel(const ScheduleArgs a) {
+__global__ void __launch_bounds__(128) sv_schedule_row_kernel(const __grid_constant__ ScheduleArgs a) {
+  pdl_wait();
+  pdl_trigger();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= a.B) return;
   const int k = a.k, po = a.plus_one ? 1 : 0;
+  // all loads up front (k <= SV_MAX_K): the fp64 chain below then never waits on memory
+  float ph[kMaxK];
+  double Lj[kMaxK + 1];
+#pragma unroll
+  for (int j = 0; j < kMaxK; ++j) ph[j] = j < k ? a.p_hat[(int64_t)b * k + j] : 0.f;
+#pragma unroll
+  for (int j = 0; j <= kMaxK; ++j) Lj[j] = j <= k ? a.L[j + po] : 1.0;
   int st = 0;
-  for (int j = po; j <= k + po; ++j) {
-    const double l = a.L[j];
-    if (!(l > 0.0) || !(l <= DBL_MAX)) st |= 128;  // SV_ROW_BAD_LATENCY
+#pragma unroll
+  for (int j = 0; j <= kMaxK; ++j) {
+    if (j <= k && (!(Lj[j] > 0.0) || !(Lj[j] <= DBL_MAX))) st |= 128;  // SV_ROW_BAD_LATENCY
   }
   if (st) {
     a.gamma[b] = 0;
@@ -45,13 +55,15 @@ __global__ void __launch_bounds__(128) sv_schedule_row_kernel(const ScheduleArgs
     return;
   }
   double P = 1.0, E = 0.0;
-  double best_g = __ddiv_rn(po ? 1.0 : 0.0, a.L[po]);
+  double best_g = __ddiv_rn(po ? 1.0 : 0.0, Lj[0]);
   double best_E = 0.0;
   int best = 0;
-  for (int j = 1; j <= k; ++j) {
-    P = __dmul_rn(P, phat_at(a.p_hat, (int64_t)b * k + (j - 1), st));
+#pragma unroll
+  for (int j = 1; j <= kMaxK; ++j) {
+    if (j > k) break;
+    P = __dmul_rn(P, phat_val(ph[j - 1], st));
     E = __dadd_rn(E, P);
-    const double g = __ddiv_rn(po ? __dadd_rn(E, 1.0) : E, a.L[j + po]);
+    const double g = __ddiv_rn(po ? __dadd_rn(E, 1.0) : E, Lj[j]);
     if (g > best_g) {
       best_g = g;
       best_E = E;
@@ -71,8 +83,7 @@ cudaError_t launch_schedule_greedy(const ScheduleArgs &a, cudaStream_t st);  // 
 cudaError_t launch_schedule(const ScheduleArgs &a, cudaStream_t st) {
   if (a.mode == 1) return launch_schedule_greedy(a, st);
   const int nt = 128;
-  sv_schedule_row_kernel<<<(a.B + nt - 1) / nt, nt, 0, st>>>(a);
-  return cudaGetLastError();
+  return launch_k(sv_schedule_row_kernel, dim3((a.B + nt - 1) / nt), dim3(nt), 0, st, a);
 }
 
 }  // namespace sv

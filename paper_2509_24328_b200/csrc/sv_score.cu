@@ -529,6 +529,8 @@ template <typename T, int NT, int MINB, int G, bool PF>
 __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constant__ ScoreArgs a) {
   constexpr int NW = NT / 32;
   __shared__ Smem<NW> sm;
+  pdl_wait();
+  pdl_trigger();
   const Task k = task_of(a);
   const float cd = a.cd, cc = a.cc;
   const Chunk<T> ch = chunk_of<T>(a, k.bb, k.ii, k.rank);
@@ -568,6 +570,8 @@ __global__ void __launch_bounds__(kScoreThreads + 32, MINB) sv_score_tma_kernel(
   __shared__ Smem<NW> sm;
   __shared__ uint64_t full[NS], empty[NS];
   extern __shared__ __align__(128) uint4 stage_buf[];  // [NS][2][SUN]
+  pdl_wait();
+  pdl_trigger();
   const Task k = task_of(a);
   const float cd = a.cd, cc = a.cc;
   const Chunk<T> ch = chunk_of<T>(a, k.bb, k.ii, k.rank);
@@ -697,8 +701,7 @@ template <typename T, int NT, int MINB, int G, bool PF = false>
 cudaError_t launch_score_t(const ScoreArgs &a, cudaStream_t st) {
   const int64_t tasks = 2 * (int64_t)a.B * a.k * a.cs;
   if (tasks == 0) return cudaSuccess;
-  sv_score_kernel<T, NT, MINB, G, PF><<<(unsigned)tasks, NT, 0, st>>>(a);
-  return cudaGetLastError();
+  return launch_k(sv_score_kernel<T, NT, MINB, G, PF>, dim3((unsigned)tasks), dim3(NT), 0, st, a);
 }
 
 template <typename T, int SU, int NS, int MINB>
@@ -713,8 +716,7 @@ cudaError_t launch_score_tma(const ScoreArgs &a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  fn<<<(unsigned)tasks, kScoreThreads + 32, smem, st>>>(a);
-  return cudaGetLastError();
+  return launch_k(fn, dim3((unsigned)tasks), dim3(kScoreThreads + 32), smem, st, a);
 }
 
 template <typename T>
