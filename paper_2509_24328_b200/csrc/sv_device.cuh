@@ -95,6 +95,21 @@ template <> struct Elem<__nv_bfloat16> {
   }
 };
 
+// max of one 16-byte unit straight from the packed bits (bf16x2 HMNMX2 is exact)
+__device__ __forceinline__ float unit_max_bf16(const uint4 &v) {
+  const __nv_bfloat162 *p = reinterpret_cast<const __nv_bfloat162 *>(&v);
+  const __nv_bfloat162 m = __hmax2(__hmax2(p[0], p[1]), __hmax2(p[2], p[3]));
+  return fmaxf(__low2float(m), __high2float(m));
+}
+template <typename T>
+__device__ __forceinline__ float unit_max(const uint4 &v) {
+  if constexpr (sizeof(T) == 2) {
+    return unit_max_bf16(v);
+  } else {
+    return fmaxf(fmaxf(__uint_as_float(v.x), __uint_as_float(v.y)), fmaxf(__uint_as_float(v.z), __uint_as_float(v.w)));
+  }
+}
+
 // ---------------------------------------------------------------- mbarrier + bulk copy
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
