@@ -193,6 +193,59 @@ SV_API int32_t sd_verify(const sv_logits *draft, const sv_logits *target, const 
                   float *accept_ratio, float *resid_mass, int32_t *row_status, void *workspace,
                   size_t workspace_bytes, void *stream);
 
+/* ------------------------------------------------------------------------------------
+ * Vocab-sharded staging (BASELINE config 4): the vocabulary of every row is
+ * split over G ranks, rank r holding columns [v_begin, v_begin + V_local) of D, C and T
+ * (a vocab-parallel lm_head layout; all ranks use the same V_local, V = G * V_local).  Each
+ * stage writes one fixed-layout exchange block (sv_shard_xch_bytes(stage, ...) bytes); the
+ * CALLER all-gathers the G blocks (rank order, back to back: e.g. NCCL all_gather_into_tensor
+ * over NVLink) between the calls.  Every merge runs over the gathered (rank, chunk) partials
+ * in vocabulary order, so all ranks compute identical S / A / KL / p_hat / gamma / N_b /
+ * Z; the token is located by the rank that owns the crossing slice (two-level inverse CDF,
+ * R11), the others write -1, and the caller all-reduces MAX over out_tok.  Results equal the
+ * unsharded calls up to the reduction order (within the R20 tolerance / tie band).
+ * Stages:  0 = score P1, 1 = score P2, 2 = verify P1, 3 = verify P2.
+ *   sv_shard_score_p1      rank-local chunk partials (M_d, L_d, M_c, L_c, W) + token logits
+ *   sv_shard_score_p2      (after gathering stage 0) rank-local S partials
+ *   sv_shard_score_finish  (after gathering stage 1) every sv_score output, identical on all ranks
+ *   sv_schedule            unchanged (replicated)
+ *   sv_shard_verify_p1     rank-local (m, l) partials of target rows 0..gamma_b + token logits
+ *   sv_shard_verify_p2     (after gathering stage 2) accept tests -> n_accept, accept_ratio
+ *                          (identical on all ranks), rank-local residual / target slice masses
+ *   sv_shard_verify_finish (after gathering stage 3) Z, theta, owning rank + slice; out_tok =
+ *                          global token id on the owner rank, -1 elsewhere; resid_mass, status
+ * Same argument conventions as the unsharded calls; `draft`, `comp`, `target` describe the
+ * RANK-LOCAL column slices (V_local wide).  Workspace: sv_workspace_bytes(B, k, V_local, .),
+ * zero-filled before first use; the verify stages keep the per-sequence decision in it.
+ * Limits: G * (sv_score chunks of V_local) <= 32 (SV_ERR_UNSUPPORTED otherwise).
+ * ---------------------------------------------------------------------------------- */
+SV_API size_t sv_shard_xch_bytes(int32_t stage, int32_t B, int32_t k, int32_t V_local, int32_t dtype);
+SV_API int32_t sv_shard_score_p1(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok,
+                                 int32_t B, int32_t k, int32_t V_local, int64_t v_begin, float tau_d,
+                                 float tau_c, void *xch, void *stream);
+SV_API int32_t sv_shard_score_p2(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok,
+                                 int32_t B, int32_t k, int32_t V_local, float tau_d, float tau_c,
+                                 const void *xch_all, int32_t G, void *xch_s, void *stream);
+SV_API int32_t sv_shard_score_finish(const int32_t *draft_tok, int32_t B, int32_t k, int32_t V, int32_t V_local,
+                                     int32_t dtype, float tau_d, float tau_c, const sv_profile *prof,
+                                     const void *xch_all, const void *xch_s_all, int32_t G, float *S, float *A,
+                                     float *KL, float *p_hat, float *draft_m, float *draft_l, float *draft_ptok,
+                                     int32_t *row_status, void *stream);
+SV_API int32_t sv_shard_verify_p1(const sv_logits *target, const int32_t *draft_tok, const int32_t *gamma,
+                                  int32_t B, int32_t k, int32_t V_local, int64_t v_begin, float tau_t, void *xch,
+                                  void *stream);
+SV_API int32_t sv_shard_verify_p2(const sv_logits *draft, const sv_logits *target, const int32_t *draft_tok,
+                                  const int32_t *gamma, const float *draft_m, const float *draft_l,
+                                  const float *draft_ptok, int32_t B, int32_t k, int32_t V, int32_t V_local,
+                                  float tau_d, float tau_t, uint64_t seed, uint64_t offset, int64_t seq_base,
+                                  const void *xch_all, int32_t G, int32_t *n_accept, float *accept_ratio,
+                                  void *xch_m, void *workspace, size_t workspace_bytes, void *stream);
+SV_API int32_t sv_shard_verify_finish(const sv_logits *draft, const sv_logits *target, int32_t B, int32_t k,
+                                      int32_t V_local, int64_t v_begin, float tau_d, float tau_t,
+                                      const void *xch_m_all, int32_t G, int32_t rank, int32_t *out_tok,
+                                      float *resid_mass, int32_t *row_status, void *workspace,
+                                      size_t workspace_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

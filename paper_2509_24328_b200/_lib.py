@@ -15,7 +15,9 @@ SV_SCHED_PER_ROW, SV_SCHED_BATCH_GREEDY = 0, 1
 ROW_NAN, ROW_ALL_NEG_INF, ROW_BAD_TOKEN, ROW_DRAFT_ZERO = 1, 2, 4, 8
 ROW_PHAT_BAD, ROW_RESID_ZERO, ROW_BAD_GAMMA, ROW_BAD_LATENCY = 16, 32, 64, 128
 
-EXPORTS = ("sv_workspace_bytes", "sv_status_string", "sv_cluster_size", "sv_score", "sv_schedule", "sd_verify")
+EXPORTS = ("sv_workspace_bytes", "sv_status_string", "sv_cluster_size", "sv_score", "sv_schedule", "sd_verify",
+           "sv_shard_xch_bytes", "sv_shard_score_p1", "sv_shard_score_p2", "sv_shard_score_finish",
+           "sv_shard_verify_p1", "sv_shard_verify_p2", "sv_shard_verify_finish")
 
 
 class SvLogits(ctypes.Structure):
@@ -60,6 +62,19 @@ def load(path: str = LIB_PATH):
     lib.sd_verify.argtypes = [LP, LP, P, P, P, P, P, i32, i32, i32, f32, f32, u64, u64, i64,
                               P, P, P, P, P, P, sz, P]
     lib.sd_verify.restype = i32
+    lib.sv_shard_xch_bytes.argtypes = [i32, i32, i32, i32, i32]
+    lib.sv_shard_xch_bytes.restype = sz
+    lib.sv_shard_score_p1.argtypes = [LP, LP, P, i32, i32, i32, i64, f32, f32, P, P]
+    lib.sv_shard_score_p2.argtypes = [LP, LP, P, i32, i32, i32, f32, f32, P, i32, P, P]
+    lib.sv_shard_score_finish.argtypes = [P, i32, i32, i32, i32, i32, f32, f32, ctypes.POINTER(SvProfile), P, P, i32,
+                                          P, P, P, P, P, P, P, P, P]
+    lib.sv_shard_verify_p1.argtypes = [LP, P, P, i32, i32, i32, i64, f32, P, P]
+    lib.sv_shard_verify_p2.argtypes = [LP, LP, P, P, P, P, P, i32, i32, i32, i32, f32, f32, u64, u64, i64, P, i32,
+                                       P, P, P, P, sz, P]
+    lib.sv_shard_verify_finish.argtypes = [LP, LP, i32, i32, i32, i64, f32, f32, P, i32, i32, P, P, P, P, sz, P]
+    for name in ("sv_shard_score_p1", "sv_shard_score_p2", "sv_shard_score_finish", "sv_shard_verify_p1",
+                 "sv_shard_verify_p2", "sv_shard_verify_finish"):
+        getattr(lib, name).restype = i32
     _lib = lib
     return lib
 

@@ -121,19 +121,31 @@ __global__ void __launch_bounds__(32 * (SV_MAX_K_DEV + 1)) sv_decide_kernel(cons
       dl = a.dl[ri];
       dpt = a.dpt[ri];
       dmv = a.dm[ri];
-      if (t >= 0 && t < a.V) xt = Elem<T>::load(reinterpret_cast<const T *>(a.t) + b * a.t_sb + lane * a.t_si + t);
+      if (t >= 0 && t < a.Vg) {
+        if (a.xtok_all) {  // vocab-sharded: the owner rank's logit (NaN elsewhere)
+          xt = __int_as_float(0x7fc00000);
+          for (int q = 0; q < a.G; ++q) {
+            const float v = a.xtok_all[(int64_t)q * a.gs_tok + b * k + lane];
+            if (xt != xt) xt = v;
+          }
+        } else {
+          xt = Elem<T>::load(reinterpret_cast<const T *>(a.t) + b * a.t_sb + lane * a.t_si + t);
+        }
+      }
     }
     w = sv_philox(a.seed, a.offset, a.seq_base + b, lane);
   }
   if (gok && wid <= g) {  // merge row wid: lane-strided sequential, then butterfly
-    const float2 *pp = a.partials + (b * (k + 1) + wid) * a.splits;
-    const int64_t ns = a.splits;
+    // partial j of G x splits (rank, split) = vocabulary order; G = 1 unless vocab-sharded
+    const int64_t sp = a.splits, ns = (int64_t)a.G * sp;
+    auto pidx = [&](int64_t j) { return (j / sp) * a.gs_part + (b * (k + 1) + wid) * sp + j % sp; };
+    const float2 *pp = a.partials;
     float M;
     double l = 0.0;
     if (ns <= 128) {  // all partials in flight at once
       float2 p[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) p[j] = (lane + 32 * j < ns) ? pp[lane + 32 * j] : make_float2(kMFloor, 0.f);
+      for (int j = 0; j < 4; ++j) p[j] = (lane + 32 * j < ns) ? pp[pidx(lane + 32 * j)] : make_float2(kMFloor, 0.f);
       float m = kMFloor;
 #pragma unroll
       for (int j = 0; j < 4; ++j) m = fmaxf(m, p[j].x);
@@ -143,10 +155,10 @@ __global__ void __launch_bounds__(32 * (SV_MAX_K_DEV + 1)) sv_decide_kernel(cons
         if (lane + 32 * j < ns) l += (double)p[j].y * ex2((p[j].x - M) * a.ct);
     } else {
       float m = kMFloor;
-      for (int64_t s = lane; s < ns; s += 32) m = fmaxf(m, pp[s].x);
+      for (int64_t s = lane; s < ns; s += 32) m = fmaxf(m, pp[pidx(s)].x);
       M = warp_max(m);
       for (int64_t s = lane; s < ns; s += 32) {
-        const float2 p = pp[s];
+        const float2 p = pp[pidx(s)];
         l += (double)p.y * ex2((p.x - M) * a.ct);
       }
     }
@@ -174,7 +186,7 @@ __global__ void __launch_bounds__(32 * (SV_MAX_K_DEV + 1)) sv_decide_kernel(cons
     if (lane < gg) {
       if (!(dl == dl)) lst |= 1;
       else if (!(dl > 0.f)) lst |= 2;
-      if (t < 0 || t >= a.V) lst |= 4;
+      if (t < 0 || t >= a.Vg) lst |= 4;
       else if (!lst) {
         if (!(dpt > 0.f)) {
           lst |= (dpt == 0.f) ? 8 : 1;
@@ -214,7 +226,7 @@ __global__ void __launch_bounds__(32 * (SV_MAX_K_DEV + 1)) sv_decide_kernel(cons
     a.dec[b] = dc;
     a.n_accept[b] = st ? 0 : N;
     if (st) {
-      a.out_tok[b] = -1;
+      if (a.out_tok) a.out_tok[b] = -1;
       if (a.resid) a.resid[b] = kNaNf;
       if (a.status) a.status[b] = st;
     }
@@ -267,7 +279,15 @@ __global__ void __launch_bounds__(kRowsThreads, 3) sv_rows_kernel(const __grid_c
       const int rem = local - s_pref[lo];
       const int i = rem / splits, split = rem - i * splits;
       const float2 p = rows_warp_item<T>(a, b, i, split);
-      if (lane == 0) a.partials[(b * (a.k + 1) + i) * a.splits + split] = p;
+      if (lane == 0) {
+        a.partials[(b * (a.k + 1) + i) * a.splits + split] = p;
+        if (a.xtok_out && split == 0 && i < a.k) {  // vocab-sharded: token logit if owned, else NaN
+          const int64_t loc = (int64_t)a.tok[b * a.k + i] - a.v_begin;
+          a.xtok_out[b * a.k + i] = (loc >= 0 && loc < a.V)
+                                        ? Elem<T>::load(reinterpret_cast<const T *>(a.t) + b * a.t_sb + i * a.t_si + loc)
+                                        : __int_as_float(0x7fc00000);
+        }
+      }
     }
     base += total;
   }
@@ -367,28 +387,38 @@ __global__ void __launch_bounds__(256) sv_find_kernel(const __grid_constant__ Ve
   const int64_t b = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (b >= a.B) return;
   const Decision dc = a.dec[b];
-  if (dc.st) return;  // K4b wrote the sentinels
+  if (dc.st) {  // sentinels (K4b wrote them too, except in the vocab-sharded staging)
+    if (lane == 0) {
+      a.out_tok[b] = -1;
+      if (a.resid) a.resid[b] = kNaNf;
+      if (a.status) a.status[b] = dc.st;
+    }
+    return;
+  }
   const SampleRow<T> sr = sample_row<T>(a, dc, b);
   const int nsl = a.nsl;
   int mode = dc.mode, st = 0;
-  const double *sm = a.smass + b * 2 * (int64_t)nsl;
+  // mass entry q of G x nsl (rank, slice) = vocabulary order; G = 1 unless vocab-sharded
+  const int nq = a.G * nsl;
+  auto midx = [&](int half, int q) { return (int64_t)(q / nsl) * a.gs_mass + (b * 2 + half) * nsl + q % nsl; };
+  const double *sm = a.smass;
   // Z: first the residual masses; R10 (Z = 0) falls back to the target masses (same row).
   // Slices go in chunks of 32 (one warp scan each, running total across chunks); the loads of
   // kFindChunks chunks are issued together.
   double Z = 0.0;
   for (int pass = 0; pass < 2; ++pass) {
-    const double *mq = sm + (mode ? 0 : nsl);
+    const int half = mode ? 0 : 1;
     double run = 0.0;
-    for (int c0 = 0; c0 < nsl; c0 += 32 * kFindChunks) {
+    for (int c0 = 0; c0 < nq; c0 += 32 * kFindChunks) {
       double m[kFindChunks];
 #pragma unroll
       for (int j = 0; j < kFindChunks; ++j) {
         const int q = c0 + 32 * j + lane;
-        m[j] = q < nsl ? __ldcg(mq + q) : 0.0;
+        m[j] = q < nq ? __ldcg(sm + midx(half, q)) : 0.0;
       }
 #pragma unroll
       for (int j = 0; j < kFindChunks; ++j) {
-        if (c0 + 32 * j >= nsl) break;
+        if (c0 + 32 * j >= nq) break;
         double incl, excl;
         warp_scan_d(m[j], incl, excl);
         run += __shfl_sync(0xffffffffu, incl, 31);
@@ -403,21 +433,21 @@ __global__ void __launch_bounds__(256) sv_find_kernel(const __grid_constant__ Ve
     break;
   }
   const double theta = dc.us * Z;
-  const double *mq = sm + (mode ? 0 : nsl);
+  const int half = mode ? 0 : 1;
   double run = 0.0, Pc = 0.0;
   int own = -1, last_pos = -1;
-  for (int c0 = 0; c0 < nsl; c0 += 32 * kFindChunks) {
+  for (int c0 = 0; c0 < nq; c0 += 32 * kFindChunks) {
     double mm[kFindChunks];
 #pragma unroll
     for (int j = 0; j < kFindChunks; ++j) {
       const int q = c0 + 32 * j + lane;
-      mm[j] = q < nsl ? __ldcg(mq + q) : 0.0;
+      mm[j] = q < nq ? __ldcg(sm + midx(half, q)) : 0.0;
     }
 #pragma unroll
     for (int j = 0; j < kFindChunks; ++j) {
       const int cj = c0 + 32 * j;
-      if (cj >= nsl) break;
-      const bool valid = cj + lane < nsl;
+      if (cj >= nq) break;
+      const bool valid = cj + lane < nq;
       const double m = mm[j];
       double incl, excl;
       warp_scan_d(m, incl, excl);
@@ -438,7 +468,10 @@ __global__ void __launch_bounds__(256) sv_find_kernel(const __grid_constant__ Ve
   const bool exact = own >= 0;
   if (!exact) own = last_pos;
   int tok = -1;
-  if (own >= 0) {
+  // the owning slice lives on rank own / nsl: only that rank locates the token (others: -1)
+  const int own_rank = own >= 0 ? own / nsl : -1;
+  own = own >= 0 ? own % nsl : -1;
+  if (own >= 0 && own_rank == a.rank) {
     float r[EPT];
     double mine, mine_t;
     if (mode) slice_lane<T, 1, true>(a, sr, own, r, mine, mine_t);
@@ -459,7 +492,7 @@ __global__ void __launch_bounds__(256) sv_find_kernel(const __grid_constant__ Ve
           if (exact && tok < 0 && cum > theta) tok = e;
         }
         if (tok < 0) tok = lastp;  // rounding left no crossing: the last positive element
-        if (tok >= 0) tok = (int)((int64_t)own * a.slice + (int64_t)ls * EPT + tok);
+        if (tok >= 0) tok = (int)(a.v_begin + (int64_t)own * a.slice + (int64_t)ls * EPT + tok);
       }
       tok = __shfl_sync(0xffffffffu, tok, ls);
     }
@@ -505,31 +538,40 @@ int64_t verify_ws_bytes(int64_t B, int k, int64_t splits, int nsl) {
   return ws_round(B * (k + 1) * splits * 8) + ws_round(B * (int64_t)sizeof(Decision)) + ws_round(B * nsl * 16);
 }
 
+// stage 0: K4 rows, 1: K4b decide, 2: K5 residual slices, 3: K5b token search
+cudaError_t launch_verify_stage(int stage, const VerifyArgs &a, cudaStream_t st) {
+  switch (stage) {
+    case 0: {  // K4: persistent over the compacted (sequence, row <= gamma, split) items
+      const void *fn = a.bf16 ? (const void *)sv_rows_kernel<__nv_bfloat16> : (const void *)sv_rows_kernel<float>;
+      const int64_t need = ((int64_t)a.B * (a.k + 1) * a.splits + kRowsThreads / 32 - 1) / (kRowsThreads / 32);
+      const int64_t grid = need < resident_grid(fn, kRowsThreads, 0) ? need : resident_grid(fn, kRowsThreads, 0);
+      return a.bf16 ? launch_k(sv_rows_kernel<__nv_bfloat16>, dim3((unsigned)grid), dim3(kRowsThreads), 0, st, a)
+                    : launch_k(sv_rows_kernel<float>, dim3((unsigned)grid), dim3(kRowsThreads), 0, st, a);
+    }
+    case 1:
+      return a.bf16 ? launch_k(sv_decide_kernel<__nv_bfloat16>, dim3((unsigned)a.B), dim3(32 * (a.k + 1)), 0, st, a)
+                    : launch_k(sv_decide_kernel<float>, dim3((unsigned)a.B), dim3(32 * (a.k + 1)), 0, st, a);
+    case 2: {
+      const void *fn = a.bf16 ? (const void *)sv_resid_kernel<__nv_bfloat16> : (const void *)sv_resid_kernel<float>;
+      const int64_t need = ((int64_t)a.B * a.nsl + kSampleThreads / 32 - 1) / (kSampleThreads / 32);
+      const int64_t grid = need < resident_grid(fn, kSampleThreads, 0) ? need : resident_grid(fn, kSampleThreads, 0);
+      return a.bf16 ? launch_k(sv_resid_kernel<__nv_bfloat16>, dim3((unsigned)grid), dim3(kSampleThreads), 0, st, a)
+                    : launch_k(sv_resid_kernel<float>, dim3((unsigned)grid), dim3(kSampleThreads), 0, st, a);
+    }
+    default: {
+      const unsigned fgrid = (unsigned)((a.B + 7) / 8);
+      return a.bf16 ? launch_k(sv_find_kernel<__nv_bfloat16>, dim3(fgrid), dim3(256), 0, st, a)
+                    : launch_k(sv_find_kernel<float>, dim3(fgrid), dim3(256), 0, st, a);
+    }
+  }
+}
+
 cudaError_t launch_verify(const VerifyArgs &a, cudaStream_t st) {
-  // K4: persistent over the compacted (sequence, row <= gamma, split) items
-  {
-    const void *fn = a.bf16 ? (const void *)sv_rows_kernel<__nv_bfloat16> : (const void *)sv_rows_kernel<float>;
-    const int64_t need = ((int64_t)a.B * (a.k + 1) * a.splits + kRowsThreads / 32 - 1) / (kRowsThreads / 32);
-    const int64_t grid = need < resident_grid(fn, kRowsThreads, 0) ? need : resident_grid(fn, kRowsThreads, 0);
-    cudaError_t e = a.bf16 ? launch_k(sv_rows_kernel<__nv_bfloat16>, dim3((unsigned)grid), dim3(kRowsThreads), 0, st, a)
-                           : launch_k(sv_rows_kernel<float>, dim3((unsigned)grid), dim3(kRowsThreads), 0, st, a);
+  for (int stage = 0; stage < 4; ++stage) {
+    const cudaError_t e = launch_verify_stage(stage, a, st);
     if (e != cudaSuccess) return e;
   }
-  // K4b
-  cudaError_t e = a.bf16 ? launch_k(sv_decide_kernel<__nv_bfloat16>, dim3((unsigned)a.B), dim3(32 * (a.k + 1)), 0, st, a)
-                         : launch_k(sv_decide_kernel<float>, dim3((unsigned)a.B), dim3(32 * (a.k + 1)), 0, st, a);
-  if (e != cudaSuccess) return e;
-  // K5
-  const void *fn = a.bf16 ? (const void *)sv_resid_kernel<__nv_bfloat16> : (const void *)sv_resid_kernel<float>;
-  const int64_t need = ((int64_t)a.B * a.nsl + kSampleThreads / 32 - 1) / (kSampleThreads / 32);
-  const int64_t grid = need < resident_grid(fn, kSampleThreads, 0) ? need : resident_grid(fn, kSampleThreads, 0);
-  e = a.bf16 ? launch_k(sv_resid_kernel<__nv_bfloat16>, dim3((unsigned)grid), dim3(kSampleThreads), 0, st, a)
-             : launch_k(sv_resid_kernel<float>, dim3((unsigned)grid), dim3(kSampleThreads), 0, st, a);
-  if (e != cudaSuccess) return e;
-  // K5b
-  const unsigned fgrid = (unsigned)((a.B + 7) / 8);
-  return a.bf16 ? launch_k(sv_find_kernel<__nv_bfloat16>, dim3(fgrid), dim3(256), 0, st, a)
-                : launch_k(sv_find_kernel<float>, dim3(fgrid), dim3(256), 0, st, a);
+  return cudaSuccess;
 }
 
 }  // namespace sv

@@ -139,6 +139,98 @@ static int32_t logits_check(const sv_logits *x, int32_t dtype) {
   return SV_OK;
 }
 
+static ScoreArgs make_score_args(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok, int32_t B,
+                                 int32_t k, int32_t V, float tau_d, float tau_c, const sv_profile *prof, float *S,
+                                 float *A, float *KL, float *p_hat, float *draft_m, float *draft_l, float *draft_ptok,
+                                 int32_t *row_status, int32_t dtype, int32_t V_chunks) {
+  ScoreArgs a = {};
+  if (draft && comp) {
+    a.d = draft->ptr;
+    a.c = comp->ptr;
+    a.d_sb = draft->stride_b;
+    a.d_si = draft->stride_i;
+    a.c_sb = comp->stride_b;
+    a.c_si = comp->stride_i;
+  }
+  a.tok = draft_tok;
+  a.B = B;
+  a.k = k;
+  a.V = V;
+  a.cd = 1.4426950408889634f / tau_d;
+  a.cc = 1.4426950408889634f / tau_c;
+  if (p_hat) {
+    a.s_edges = prof->s_edges;
+    a.a_edges = prof->a_edges;
+    a.cells = prof->cells;
+    a.n_s = prof->n_s;
+    a.n_a = prof->n_a;
+  }
+  a.S = S;
+  a.A = A;
+  a.KL = KL;
+  a.p_hat = p_hat;
+  a.dm = draft_m;
+  a.dl = draft_l;
+  a.dpt = draft_ptok;
+  a.status = row_status;
+  a.bf16 = dtype == SV_BF16;
+  a.cs = score_splits_for(V_chunks);  // chunking of the (rank-local) columns
+  a.chunk = chunk_elems_for(V_chunks, a.cs);
+  return a;
+}
+
+static VerifyArgs make_verify_args(const sv_logits *draft, const sv_logits *target, const int32_t *draft_tok,
+                                   const int32_t *gamma, const float *draft_m, const float *draft_l,
+                                   const float *draft_ptok, int32_t B, int32_t k, int32_t V, float tau_d, float tau_t,
+                                   uint64_t seed, uint64_t offset, int64_t seq_base, int32_t *n_accept,
+                                   int32_t *out_tok, float *accept_ratio, float *resid_mass, int32_t *row_status,
+                                   void *workspace, int32_t V_ws) {
+  const int eb = elem_bytes(draft->dtype);
+  VerifyArgs a = {};
+  a.d = draft->ptr;
+  a.t = target->ptr;
+  a.d_sb = draft->stride_b;
+  a.d_si = draft->stride_i;
+  a.t_sb = target->stride_b;
+  a.t_si = target->stride_i;
+  a.tok = draft_tok;
+  a.gamma = gamma;
+  a.dm = draft_m;
+  a.dl = draft_l;
+  a.dpt = draft_ptok;
+  a.B = B;
+  a.k = k;
+  a.V = V;
+  a.cd = 1.4426950408889634f / tau_d;
+  a.ct = 1.4426950408889634f / tau_t;
+  a.seed = seed;
+  a.offset = offset;
+  a.seq_base = seq_base;
+  a.n_accept = n_accept;
+  a.out_tok = out_tok;
+  a.ratio = accept_ratio;
+  a.resid = resid_mass;
+  a.status = row_status;
+  a.splits = rows_splits_for(V, eb);
+  a.rows_chunk = rows_chunk_for(eb);
+  a.slice = sample_slice_for(eb);
+  a.nsl = sample_slices_for(V, eb);
+  {
+    uint8_t *w = reinterpret_cast<uint8_t *>(workspace) + verify_ws_offset(B, k, V_ws, eb);
+    a.partials = reinterpret_cast<float2 *>(w);
+    w += ws_round((int64_t)B * (k + 1) * a.splits * 8);
+    a.dec = reinterpret_cast<Decision *>(w);
+    w += ws_round((int64_t)B * (int64_t)sizeof(Decision));
+    a.smass = reinterpret_cast<double *>(w);
+  }
+  a.bf16 = draft->dtype == SV_BF16;
+  a.G = 1;
+  a.rank = 0;
+  a.v_begin = 0;
+  a.Vg = V;
+  return a;
+}
+
 extern "C" {
 
 size_t sv_workspace_bytes(int32_t B, int32_t k, int32_t V, int32_t dtype) {
@@ -179,37 +271,8 @@ int32_t sv_score(const sv_logits *draft, const sv_logits *comp, const int32_t *d
   if (B == 0) return SV_OK;
   if (!workspace || workspace_bytes < sv_workspace_bytes(B, k, V, draft->dtype)) return SV_ERR_WORKSPACE;
   if ((reinterpret_cast<uintptr_t>(workspace) & 15) != 0) return SV_ERR_INVALID_ARG;
-  ScoreArgs a = {};
-  a.d = draft->ptr;
-  a.c = comp->ptr;
-  a.d_sb = draft->stride_b;
-  a.d_si = draft->stride_i;
-  a.c_sb = comp->stride_b;
-  a.c_si = comp->stride_i;
-  a.tok = draft_tok;
-  a.B = B;
-  a.k = k;
-  a.V = V;
-  a.cd = 1.4426950408889634f / tau_d;
-  a.cc = 1.4426950408889634f / tau_c;
-  if (p_hat) {
-    a.s_edges = prof->s_edges;
-    a.a_edges = prof->a_edges;
-    a.cells = prof->cells;
-    a.n_s = prof->n_s;
-    a.n_a = prof->n_a;
-  }
-  a.S = S;
-  a.A = A;
-  a.KL = KL;
-  a.p_hat = p_hat;
-  a.dm = draft_m;
-  a.dl = draft_l;
-  a.dpt = draft_ptok;
-  a.status = row_status;
-  a.bf16 = draft->dtype == SV_BF16;
-  a.cs = score_splits_for(V);
-  a.chunk = chunk_elems_for(V, a.cs);
+  ScoreArgs a = make_score_args(draft, comp, draft_tok, B, k, V, tau_d, tau_c, prof, S, A, KL, p_hat, draft_m, draft_l,
+                                draft_ptok, row_status, draft->dtype, V);
   const int64_t rows = (int64_t)B * k;
   if (2 * rows * a.cs > INT32_MAX) return SV_ERR_UNSUPPORTED;  // one CTA per chunk task
   static const int lag = tune_knob("SV_SCORE_LAG", kScoreLag);
@@ -278,50 +341,202 @@ int32_t sd_verify(const sv_logits *draft, const sv_logits *target, const int32_t
   if (B == 0) return SV_OK;
   if (!workspace || workspace_bytes < sv_workspace_bytes(B, k, V, draft->dtype)) return SV_ERR_WORKSPACE;
   if ((reinterpret_cast<uintptr_t>(workspace) & 15) != 0) return SV_ERR_INVALID_ARG;
-  const int eb = elem_bytes(draft->dtype);
-  VerifyArgs a = {};
-  a.d = draft->ptr;
-  a.t = target->ptr;
-  a.d_sb = draft->stride_b;
-  a.d_si = draft->stride_i;
-  a.t_sb = target->stride_b;
-  a.t_si = target->stride_i;
-  a.tok = draft_tok;
-  a.gamma = gamma;
-  a.dm = draft_m;
-  a.dl = draft_l;
-  a.dpt = draft_ptok;
-  a.B = B;
-  a.k = k;
-  a.V = V;
-  a.cd = 1.4426950408889634f / tau_d;
-  a.ct = 1.4426950408889634f / tau_t;
-  a.seed = seed;
-  a.offset = offset;
-  a.seq_base = seq_base;
-  a.n_accept = n_accept;
-  a.out_tok = out_tok;
-  a.ratio = accept_ratio;
-  a.resid = resid_mass;
-  a.status = row_status;
-  a.splits = rows_splits_for(V, eb);
-  a.rows_chunk = rows_chunk_for(eb);
-  a.slice = sample_slice_for(eb);
-  a.nsl = sample_slices_for(V, eb);
-  {
-    uint8_t *w = reinterpret_cast<uint8_t *>(workspace) + verify_ws_offset(B, k, V, eb);
-    a.partials = reinterpret_cast<float2 *>(w);
-    w += ws_round((int64_t)B * (k + 1) * a.splits * 8);
-    a.dec = reinterpret_cast<Decision *>(w);
-    w += ws_round((int64_t)B * (int64_t)sizeof(Decision));
-    a.smass = reinterpret_cast<double *>(w);
-  }
-  a.bf16 = draft->dtype == SV_BF16;
+  VerifyArgs a = make_verify_args(draft, target, draft_tok, gamma, draft_m, draft_l, draft_ptok, B, k, V, tau_d, tau_t,
+                                  seed, offset, seq_base, n_accept, out_tok, accept_ratio, resid_mass, row_status,
+                                  workspace, V);
   cudaError_t e = launch_verify(a, (cudaStream_t)stream);
   if (e != cudaSuccess) {
     fprintf(stderr, "libsv: sd_verify launch failed: %s\n", cudaGetErrorString(e));
     return SV_ERR_CUDA;
   }
+  return SV_OK;
+}
+
+// ------------------------------------------------------------------ vocab-sharded staging
+// Exchange blocks (sv_shard_xch_bytes): 0 = score P1, 1 = score P2, 2 = verify P1, 3 = verify P2.
+static int64_t xch_part_bytes(int stage, int64_t B, int k, int64_t V_local, int eb) {
+  const int64_t rows = B * k;
+  switch (stage) {
+    case 0: return ws_round(rows * score_splits_for(V_local) * 40);  // [rows][cs][5] f64
+    case 1: return ws_round(rows * score_splits_for(V_local) * 4);   // [rows][cs] f32
+    case 2: return ws_round(B * (k + 1) * rows_splits_for(V_local, eb) * 8);  // [B][k+1][splits] (m, l)
+    default: return ws_round(B * 2 * sample_slices_for(V_local, eb) * 8);     // [B][2][nsl] f64
+  }
+}
+static int64_t xch_block_bytes(int stage, int64_t B, int k, int64_t V_local, int eb) {
+  const int64_t p = xch_part_bytes(stage, B, k, V_local, eb);
+  if (stage == 0) return p + ws_round(B * k * 8);  // + [rows][2] token logits
+  if (stage == 2) return p + ws_round(B * k * 4);  // + [B][k] token logits
+  return p;
+}
+
+static void report(const char *what, cudaError_t e) {
+  fprintf(stderr, "libsv: %s launch failed: %s\n", what, cudaGetErrorString(e));
+}
+
+size_t sv_shard_xch_bytes(int32_t stage, int32_t B, int32_t k, int32_t V_local, int32_t dtype) {
+  if (stage < 0 || stage > 3 || shape_check(B, k, V_local, dtype) != SV_OK) return 0;
+  return (size_t)xch_block_bytes(stage, B, k, V_local, elem_bytes(dtype));
+}
+
+int32_t sv_shard_score_p1(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok, int32_t B, int32_t k,
+                          int32_t V_local, int64_t v_begin, float tau_d, float tau_c, void *xch, void *stream) {
+  if (!draft) return SV_ERR_INVALID_ARG;
+  int32_t r = shape_check(B, k, V_local, draft->dtype);
+  if (r != SV_OK) return r;
+  if ((r = logits_check(draft, draft->dtype)) != SV_OK || (r = logits_check(comp, draft->dtype)) != SV_OK) return r;
+  if (!draft_tok || !xch || v_begin < 0 || !(tau_d > 0.f) || !(tau_c > 0.f)) return SV_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(xch) & 15) != 0) return SV_ERR_INVALID_ARG;
+  if (B == 0) return SV_OK;
+  ScoreArgs a = make_score_args(draft, comp, draft_tok, B, k, V_local, tau_d, tau_c, nullptr, nullptr, nullptr, nullptr,
+                                nullptr, nullptr, nullptr, nullptr, nullptr, draft->dtype, V_local);
+  if ((int64_t)B * k * a.cs > INT32_MAX) return SV_ERR_UNSUPPORTED;
+  a.part = reinterpret_cast<double *>(xch);
+  a.cnt = nullptr;
+  ShardScoreArgs h = {};
+  h.stage = 0;
+  h.v_begin = v_begin;
+  h.xtok_out = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(xch) +
+                                         xch_part_bytes(0, B, k, V_local, elem_bytes(draft->dtype)));
+  const cudaError_t e = launch_shard_score(h, a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return report("sv_shard_score_p1", e), SV_ERR_CUDA;
+  return SV_OK;
+}
+
+int32_t sv_shard_score_p2(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok, int32_t B, int32_t k,
+                          int32_t V_local, float tau_d, float tau_c, const void *xch_all, int32_t G, void *xch_s,
+                          void *stream) {
+  if (!draft) return SV_ERR_INVALID_ARG;
+  int32_t r = shape_check(B, k, V_local, draft->dtype);
+  if (r != SV_OK) return r;
+  if ((r = logits_check(draft, draft->dtype)) != SV_OK || (r = logits_check(comp, draft->dtype)) != SV_OK) return r;
+  if (!draft_tok || !xch_all || !xch_s || G < 1 || !(tau_d > 0.f) || !(tau_c > 0.f)) return SV_ERR_INVALID_ARG;
+  if (B == 0) return SV_OK;
+  const int eb = elem_bytes(draft->dtype);
+  ScoreArgs a = make_score_args(draft, comp, draft_tok, B, k, V_local, tau_d, tau_c, nullptr, nullptr, nullptr, nullptr,
+                                nullptr, nullptr, nullptr, nullptr, nullptr, draft->dtype, V_local);
+  if (G * a.cs > 32) return SV_ERR_UNSUPPORTED;  // one merge lane per (rank, chunk) partial
+  ShardScoreArgs h = {};
+  h.stage = 1;
+  h.G = G;
+  h.xall = reinterpret_cast<const double *>(xch_all);
+  h.gs_part = xch_block_bytes(0, B, k, V_local, eb) / 8;
+  h.s_out = reinterpret_cast<float *>(xch_s);
+  const cudaError_t e = launch_shard_score(h, a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return report("sv_shard_score_p2", e), SV_ERR_CUDA;
+  return SV_OK;
+}
+
+int32_t sv_shard_score_finish(const int32_t *draft_tok, int32_t B, int32_t k, int32_t V, int32_t V_local, int32_t dtype,
+                              float tau_d, float tau_c, const sv_profile *prof, const void *xch_all,
+                              const void *xch_s_all, int32_t G, float *S, float *A, float *KL, float *p_hat,
+                              float *draft_m, float *draft_l, float *draft_ptok, int32_t *row_status, void *stream) {
+  int32_t r = shape_check(B, k, V_local, dtype);
+  if (r != SV_OK) return r;
+  if (V < V_local || !draft_tok || !xch_all || !xch_s_all || G < 1 || !draft_m || !draft_l || !draft_ptok)
+    return SV_ERR_INVALID_ARG;
+  if (!(tau_d > 0.f) || !(tau_c > 0.f)) return SV_ERR_INVALID_ARG;
+  if (p_hat && (!prof || !prof->s_edges || !prof->a_edges || !prof->cells || prof->n_s < 1 || prof->n_a < 1 ||
+                prof->n_s > 64 || prof->n_a > 64))
+    return SV_ERR_INVALID_ARG;
+  if (B == 0) return SV_OK;
+  const int eb = elem_bytes(dtype);
+  ScoreArgs a = make_score_args(nullptr, nullptr, draft_tok, B, k, V, tau_d, tau_c, prof, S, A, KL, p_hat, draft_m,
+                                draft_l, draft_ptok, row_status, dtype, V_local);
+  if (G * a.cs > 32) return SV_ERR_UNSUPPORTED;
+  ShardScoreArgs h = {};
+  h.stage = 2;
+  h.G = G;
+  h.xall = reinterpret_cast<const double *>(xch_all);
+  const int64_t blk0 = xch_block_bytes(0, B, k, V_local, eb);
+  h.gs_part = blk0 / 8;
+  h.xtok_all = reinterpret_cast<const float *>(reinterpret_cast<const uint8_t *>(xch_all) +
+                                               xch_part_bytes(0, B, k, V_local, eb));
+  h.gs_tok = blk0 / 4;
+  h.sall = reinterpret_cast<const float *>(xch_s_all);
+  h.gs_s = xch_block_bytes(1, B, k, V_local, eb) / 4;
+  const cudaError_t e = launch_shard_score(h, a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return report("sv_shard_score_finish", e), SV_ERR_CUDA;
+  return SV_OK;
+}
+
+int32_t sv_shard_verify_p1(const sv_logits *target, const int32_t *draft_tok, const int32_t *gamma, int32_t B, int32_t k,
+                           int32_t V_local, int64_t v_begin, float tau_t, void *xch, void *stream) {
+  if (!target) return SV_ERR_INVALID_ARG;
+  int32_t r = shape_check(B, k, V_local, target->dtype);
+  if (r != SV_OK) return r;
+  if ((r = logits_check(target, target->dtype)) != SV_OK) return r;
+  if (!draft_tok || !gamma || !xch || v_begin < 0 || !(tau_t > 0.f)) return SV_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(xch) & 15) != 0) return SV_ERR_INVALID_ARG;
+  if (B == 0) return SV_OK;
+  const int eb = elem_bytes(target->dtype);
+  VerifyArgs a = make_verify_args(target, target, draft_tok, gamma, nullptr, nullptr, nullptr, B, k, V_local, 1.f, tau_t,
+                                  0, 0, 0, nullptr, nullptr, nullptr, nullptr, nullptr, xch, V_local);
+  a.partials = reinterpret_cast<float2 *>(xch);
+  a.xtok_out = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(xch) + xch_part_bytes(2, B, k, V_local, eb));
+  a.v_begin = v_begin;
+  const cudaError_t e = launch_verify_stage(0, a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return report("sv_shard_verify_p1", e), SV_ERR_CUDA;
+  return SV_OK;
+}
+
+int32_t sv_shard_verify_p2(const sv_logits *draft, const sv_logits *target, const int32_t *draft_tok, const int32_t *gamma,
+                           const float *draft_m, const float *draft_l, const float *draft_ptok, int32_t B, int32_t k,
+                           int32_t V, int32_t V_local, float tau_d, float tau_t, uint64_t seed, uint64_t offset,
+                           int64_t seq_base, const void *xch_all, int32_t G, int32_t *n_accept, float *accept_ratio,
+                           void *xch_m, void *workspace, size_t workspace_bytes, void *stream) {
+  if (!draft) return SV_ERR_INVALID_ARG;
+  int32_t r = shape_check(B, k, V_local, draft->dtype);
+  if (r != SV_OK) return r;
+  if ((r = logits_check(draft, draft->dtype)) != SV_OK || (r = logits_check(target, draft->dtype)) != SV_OK) return r;
+  if (!draft_tok || !gamma || !draft_m || !draft_l || !draft_ptok || !n_accept || !xch_all || !xch_m || G < 1 ||
+      V < V_local || seq_base < 0 || !(tau_d > 0.f) || !(tau_t > 0.f))
+    return SV_ERR_INVALID_ARG;
+  if (B == 0) return SV_OK;
+  if (!workspace || workspace_bytes < sv_workspace_bytes(B, k, V_local, draft->dtype)) return SV_ERR_WORKSPACE;
+  if ((reinterpret_cast<uintptr_t>(workspace) & 15) != 0) return SV_ERR_INVALID_ARG;
+  const int eb = elem_bytes(draft->dtype);
+  VerifyArgs a = make_verify_args(draft, target, draft_tok, gamma, draft_m, draft_l, draft_ptok, B, k, V_local, tau_d,
+                                  tau_t, seed, offset, seq_base, n_accept, nullptr, accept_ratio, nullptr, nullptr,
+                                  workspace, V_local);
+  a.Vg = V;
+  a.G = G;
+  const int64_t blk2 = xch_block_bytes(2, B, k, V_local, eb);
+  a.partials = const_cast<float2 *>(reinterpret_cast<const float2 *>(xch_all));
+  a.gs_part = blk2 / 8;
+  a.xtok_all = reinterpret_cast<const float *>(reinterpret_cast<const uint8_t *>(xch_all) + xch_part_bytes(2, B, k, V_local, eb));
+  a.gs_tok = blk2 / 4;
+  a.smass = reinterpret_cast<double *>(xch_m);
+  // a bad sequence's out_tok / resid_mass / row_status sentinels are written by _finish (from
+  // the same Decision): _p2 writes n_accept and accept_ratio only
+  cudaError_t e = launch_verify_stage(1, a, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = launch_verify_stage(2, a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return report("sv_shard_verify_p2", e), SV_ERR_CUDA;
+  return SV_OK;
+}
+
+int32_t sv_shard_verify_finish(const sv_logits *draft, const sv_logits *target, int32_t B, int32_t k, int32_t V_local,
+                               int64_t v_begin, float tau_d, float tau_t, const void *xch_m_all, int32_t G, int32_t rank,
+                               int32_t *out_tok, float *resid_mass, int32_t *row_status, void *workspace,
+                               size_t workspace_bytes, void *stream) {
+  if (!draft) return SV_ERR_INVALID_ARG;
+  int32_t r = shape_check(B, k, V_local, draft->dtype);
+  if (r != SV_OK) return r;
+  if ((r = logits_check(draft, draft->dtype)) != SV_OK || (r = logits_check(target, draft->dtype)) != SV_OK) return r;
+  if (!out_tok || !xch_m_all || G < 1 || rank < 0 || rank >= G || v_begin < 0 || !(tau_d > 0.f) || !(tau_t > 0.f))
+    return SV_ERR_INVALID_ARG;
+  if (B == 0) return SV_OK;
+  if (!workspace || workspace_bytes < sv_workspace_bytes(B, k, V_local, draft->dtype)) return SV_ERR_WORKSPACE;
+  const int eb = elem_bytes(draft->dtype);
+  VerifyArgs a = make_verify_args(draft, target, nullptr, nullptr, nullptr, nullptr, nullptr, B, k, V_local, tau_d, tau_t,
+                                  0, 0, 0, nullptr, out_tok, nullptr, resid_mass, row_status, workspace, V_local);
+  a.G = G;
+  a.rank = rank;
+  a.v_begin = v_begin;
+  a.smass = const_cast<double *>(reinterpret_cast<const double *>(xch_m_all));
+  a.gs_mass = xch_block_bytes(3, B, k, V_local, eb) / 8;
+  const cudaError_t e = launch_verify_stage(3, a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return report("sv_shard_verify_finish", e), SV_ERR_CUDA;
   return SV_OK;
 }
 

@@ -81,6 +81,21 @@ struct ScoreArgs {
 // sv_score's share of the workspace (offset 0); sd_verify's follows it
 int64_t score_ws_bytes(int64_t rows, int cs);
 cudaError_t launch_score(const ScoreArgs &a, cudaStream_t st);
+// vocab-sharded staging of sv_score: stage 0 = P1 (a.part <- chunk partials, xtok_out <- token
+// logits), 1 = P2 (gathered partials -> s_out S partials), 2 = finish (epilogue outputs of a).
+// Gathered arrays hold G rank blocks; gs_* = elements between consecutive ranks' blocks.
+struct ShardScoreArgs {
+  int stage, G;
+  int64_t v_begin;
+  const double *xall;  // [G] x [rows][cs][5]
+  int64_t gs_part;
+  const float *xtok_all;  // [G] x [rows][2]
+  int64_t gs_tok;
+  const float *sall;  // [G] x [rows][cs]
+  int64_t gs_s;
+  float *xtok_out, *s_out;
+};
+cudaError_t launch_shard_score(const ShardScoreArgs &h, const ScoreArgs &a, cudaStream_t st);
 
 struct ScheduleArgs {
   const float *p_hat;
@@ -119,10 +134,19 @@ struct VerifyArgs {
   double *smass;       // workspace: [B][2][nsl] residual and target mass per vocabulary slice
   int64_t slice;       // K5 elements per slice
   int nsl;             // K5 slices per row
+  // vocab-sharded staging (G = 1, rank = 0, v_begin = 0, xtok_* = NULL when unsharded):
+  // partials / smass then point at the all-gathered [G][...] blocks
+  int G, rank;
+  int64_t v_begin;
+  int32_t Vg;  // global vocabulary (token range checks); = V unless vocab-sharded
+  int64_t gs_part, gs_tok, gs_mass;  // elements between consecutive ranks' gathered blocks
+  const float *xtok_all;  // [G][B][k] target token logits (NaN where not owned)
+  float *xtok_out;        // [B][k] this rank's (K4 writes them when non-NULL)
   int bf16;
 };
 // sd_verify's share of the workspace
 int64_t verify_ws_bytes(int64_t B, int k, int64_t splits, int nsl);
 cudaError_t launch_verify(const VerifyArgs &a, cudaStream_t st);
+cudaError_t launch_verify_stage(int stage, const VerifyArgs &a, cudaStream_t st);
 
 }  // namespace sv

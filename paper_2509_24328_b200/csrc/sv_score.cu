@@ -281,9 +281,13 @@ __device__ __forceinline__ float pass2_thread(const Chunk<T> &ch, float cd, floa
 // Epilogue of one row (control warp of its epilogue CTA; independent pieces on separate lanes,
 // fp64 range reduction + fp32 transcendentals).  The draft-side outputs depend on the draft row
 // alone: a bad companion row does not poison them.
+// S partials: entry j < G cs of this row is sarr[(j / cs) gstride + j % cs] (vocabulary order);
+// xtok: NULL = load the token logits from the rows, else the owner's of xtok[g gstride2 + 0/1]
+// over g (NaN = not owned; vocab-sharded staging).
 template <typename T>
 __device__ __noinline__ void epilogue(const ScoreArgs &a, int64_t b, int64_t i, const double *glob,
-                                      const float *sarr, int cs) {  // sarr: global, this row's S partials
+                                      const float *sarr, int cs, int G, int64_t gstride, const float *xtok,
+                                      int64_t gstride2) {
   const int64_t row = b * a.k + i;
   const int lane = threadIdx.x & 31;
   const float cd = a.cd, cc = a.cc;
@@ -308,17 +312,29 @@ __device__ __noinline__ void epilogue(const ScoreArgs &a, int64_t b, int64_t i, 
   }
   // lane 0: log2 p_d(t); lane 1: log2 p_c(t); lane 2: log2 L_d - log2 L_c; lane 3: S (rank order)
   double piece = 0.0;
+  auto tok_logit = [&](int which) {  // 0 = draft, 1 = companion
+    if (!xtok) {
+      return which == 0 ? Elem<T>::load(reinterpret_cast<const T *>(a.d) + b * a.d_sb + i * a.d_si + t)
+                        : Elem<T>::load(reinterpret_cast<const T *>(a.c) + b * a.c_sb + i * a.c_si + t);
+    }
+    float x = __int_as_float(0x7fc00000);
+    for (int g = 0; g < G; ++g) {
+      const float v = __ldcg(xtok + g * gstride2 + which);
+      if (x != x) x = v;
+    }
+    return x;
+  };
   if (lane == 0 && !d_st && tok_ok) {
-    const float x = Elem<T>::load(reinterpret_cast<const T *>(a.d) + b * a.d_sb + i * a.d_si + t);
+    const float x = tok_logit(0);
     piece = (double)x * cd - (double)(GMd * cd) - log2_acc(L_d);
   }
   if (lane == 1 && !st) {
-    const float x = Elem<T>::load(reinterpret_cast<const T *>(a.c) + b * a.c_sb + i * a.c_si + t);
+    const float x = tok_logit(1);
     piece = (double)x * cc - (double)(GMc * cc) - log2_acc(L_c);
   }
   if (lane == 2 && !st) piece = log2_acc(L_d) - log2_acc(L_c);
   if (lane == 3)
-    for (int r = 0; r < cs; ++r) piece += (double)__ldcg(sarr + r);
+    for (int j = 0; j < G * cs; ++j) piece += (double)__ldcg(sarr + (j / cs) * gstride + j % cs);
   const double argd = __shfl_sync(0xffffffffu, piece, 0);
   double piece2 = 0.0;  // lane 0: p_d(t); lane 1: p_c(t) / p_d(t)
   if (lane == 0 && !d_st && tok_ok) piece2 = exp2_acc(argd);
@@ -439,22 +455,24 @@ __device__ __forceinline__ void p1_publish(const ScoreArgs &a, const Task &k, co
       part[2] = (double)Mc;
       part[3] = r1;
       part[4] = r2;
-      red_release_add(a.cnt + 2 * (size_t)k.row, 1u);
+      if (a.cnt) red_release_add(a.cnt + 2 * (size_t)k.row, 1u);
     }
   }
 }
 
 // P2 head (one warp): wait for the row's cs P1 partials, merge them in chunk order (identical
 // bits in every P2 task of the row) -> sm.glob, sm.lam.
-template <int NW>
-__device__ __forceinline__ void p2_merge(const ScoreArgs &a, const Task &k, Smem<NW> &sm) {
-  const int lane = threadIdx.x & 31, cs = a.cs;
+// Merge of a row's np <= 32 P1 partials (one per lane, vocabulary order) into sm.glob / sm.lam:
+// part(j) = partial j.  Shared by K1 and the vocab-sharded staging (identical arithmetic).
+template <int NW, typename PartFn>
+__device__ __forceinline__ void merge_partials(const ScoreArgs &a, int np, PartFn part_of, Smem<NW> &sm) {
+  const int lane = threadIdx.x & 31;
+  const int cs = np;
   const float cd = a.cd, cc = a.cc;
-  wait_count(a.cnt + 2 * (size_t)k.row, (uint32_t)cs);  // every lane acquires
   double pr[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
   pr[0] = pr[2] = kMFloor;
   if (lane < cs) {
-    const double *part = a.part + ((size_t)k.row * cs + lane) * 5;
+    const double *part = part_of(lane);
 #pragma unroll
     for (int j = 0; j < 5; ++j) pr[j] = __ldcg(part + j);
   }
@@ -483,6 +501,12 @@ __device__ __forceinline__ void p2_merge(const ScoreArgs &a, const Task &k, Smem
   }
 }
 
+template <int NW>
+__device__ __forceinline__ void p2_merge(const ScoreArgs &a, const Task &k, Smem<NW> &sm) {
+  wait_count(a.cnt + 2 * (size_t)k.row, (uint32_t)a.cs);  // every lane acquires
+  merge_partials<NW>(a, a.cs, [&](int j) { return a.part + ((size_t)k.row * a.cs + j) * 5; }, sm);
+}
+
 // P2 tail: block sum of the S partials, publish; the row's last P2 task runs the epilogue and
 // resets the row's counters.  All NW warps call it.
 template <typename T, int NW>
@@ -503,7 +527,7 @@ __device__ __forceinline__ void p2_finish(const ScoreArgs &a, const Task &k, flo
   if (k.rank != cs - 1) return;
   // the row's last P2 task: wait for the other S partials, epilogue, reset the counters
   wait_count(cnt + 1, (uint32_t)(cs - 1));  // every lane acquires
-  epilogue<T>(a, k.bb, k.ii, sm.glob, srow, cs);
+  epilogue<T>(a, k.bb, k.ii, sm.glob, srow, cs, 1, 0, nullptr, 0);
   if (lane == 0) {
     cnt[0] = 0u;  // every P1 / P2 task of this row is past its use of the counters
     cnt[1] = 0u;
@@ -720,10 +744,121 @@ cudaError_t launch_score_cfg(const ScoreArgs &a, cudaStream_t st) {
   }
 }
 
+// ---------------------------------------------------------------- vocab-sharded staging
+// (BASELINE config 4).  Each rank holds columns [v_begin, v_begin + V_local) of
+// every row (a.V = V_local, a.cs / a.chunk from V_local); the caller all-gathers the stage
+// outputs between the calls.  Merges run over the G x cs chunk partials in (rank, chunk) =
+// vocabulary order with the same arithmetic as K1, so every rank computes identical bits.
+__device__ __forceinline__ Task shard_task(const ScoreArgs &a) {
+  Task k;
+  k.q = blockIdx.x;
+  k.row = k.q / (uint32_t)a.cs;
+  k.rank = (int)(k.q - k.row * (uint32_t)a.cs);
+  k.bb = k.row / (uint32_t)a.k;
+  k.ii = k.row - k.bb * a.k;
+  k.p2 = false;
+  return k;
+}
+
+// P1 of the rank's chunks: (M_d, L_d, M_c, L_c, W) per (row, chunk) -> part (a.part, no counter);
+// chunk 0 also records the token logits x_d(t), x_c(t) when this rank owns t (NaN otherwise).
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT) sv_shard_p1_kernel(const __grid_constant__ ScoreArgs a, int64_t v_begin,
+                                                         float *xtok) {
+  constexpr int NW = NT / 32;
+  __shared__ Smem<NW> sm;
+  pdl_wait();
+  pdl_trigger();
+  const Task k = shard_task(a);
+  const Chunk<T> ch = chunk_of<T>(a, k.bb, k.ii, k.rank);
+  const uint64_t pol = l2_policy_evict_last();
+  P1State t = pass1_thread<T, false, NT, kScoreGroup, false>(ch, a.cd, a.cc, pol);
+  if (t.w != t.w && t.ld == t.ld && t.lc == t.lc) t = pass1_thread<T, true, NT, 1, false>(ch, a.cd, a.cc, pol);
+  p1_publish<NW>(a, k, t, sm);
+  if (k.rank == 0 && threadIdx.x == 0) {
+    const int64_t loc = (int64_t)a.tok[k.row] - v_begin;
+    float xd = __int_as_float(0x7fc00000), xc = xd;
+    if (loc >= 0 && loc < a.V) {
+      xd = Elem<T>::load(reinterpret_cast<const T *>(a.d) + (int64_t)k.bb * a.d_sb + (int64_t)k.ii * a.d_si + loc);
+      xc = Elem<T>::load(reinterpret_cast<const T *>(a.c) + (int64_t)k.bb * a.c_sb + (int64_t)k.ii * a.c_si + loc);
+    }
+    xtok[(size_t)k.row * 2] = xd;
+    xtok[(size_t)k.row * 2 + 1] = xc;
+  }
+}
+
+// P2 of the rank's chunks: merge all G x cs partials (xall = [G][rows][cs][5]), then the S
+// partial of this chunk -> sout[row][chunk].
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT) sv_shard_p2_kernel(const __grid_constant__ ScoreArgs a, const double *xall,
+                                                         int64_t gs_part, int G, float *sout) {
+  constexpr int NW = NT / 32;
+  __shared__ Smem<NW> sm;
+  pdl_wait();
+  pdl_trigger();
+  const Task k = shard_task(a);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (wid == NW - 1)
+    merge_partials<NW>(a, G * a.cs,
+                       [&](int j) { return xall + (size_t)(j / a.cs) * gs_part + ((size_t)k.row * a.cs + j % a.cs) * 5; },
+                       sm);
+  __syncthreads();
+  const float lamd = sm.lam[0], lamc = sm.lam[1];
+  const Chunk<T> ch = chunk_of<T>(a, k.bb, k.ii, k.rank);
+  float s_loc = 0.f;
+  if (lamd == lamd && lamc == lamc) s_loc = pass2_thread<T, NT, kScoreGroup>(ch, a.cd, a.cc, lamd, lamc, l2_policy_evict_first());
+  s_loc = warp_sum(s_loc);
+  if (lane == 0) sm.fscr[wid] = s_loc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float r = sm.fscr[0];
+    for (int w = 1; w < NW; ++w) r += sm.fscr[w];
+    sout[(size_t)k.row * a.cs + k.rank] = r;
+  }
+}
+
+// Epilogue per row (one warp): the same merge, S over the G x cs partials (sall = [G][rows][cs]),
+// token logits from their owner (xtok_all = [G][rows][2]); a.V is the GLOBAL vocabulary here.
+template <typename T>
+__global__ void __launch_bounds__(32) sv_shard_finish_kernel(const __grid_constant__ ScoreArgs a, const double *xall,
+                                                             int64_t gs_part, const float *xtok_all, int64_t gs_tok,
+                                                             const float *sall, int64_t gs_s, int G) {
+  __shared__ Smem<1> sm;
+  pdl_wait();
+  pdl_trigger();
+  const size_t row = blockIdx.x;
+  merge_partials<1>(a, G * a.cs, [&](int j) { return xall + (size_t)(j / a.cs) * gs_part + (row * a.cs + j % a.cs) * 5; },
+                    sm);
+  __syncwarp();
+  epilogue<T>(a, (int64_t)(row / a.k), (int64_t)(row % a.k), sm.glob, sall + row * a.cs, a.cs, G, gs_s,
+              xtok_all + row * 2, gs_tok);
+}
+
+template <typename T>
+cudaError_t shard_score_stage_t(const ShardScoreArgs &h, const ScoreArgs &a, cudaStream_t st) {
+  const unsigned rows = (unsigned)((int64_t)a.B * a.k);
+  if (rows == 0) return cudaSuccess;
+  switch (h.stage) {
+    case 0:
+      return launch_k(sv_shard_p1_kernel<T, kScoreThreads>, dim3(rows * (unsigned)a.cs), dim3(kScoreThreads), 0, st, a,
+                      h.v_begin, h.xtok_out);
+    case 1:
+      return launch_k(sv_shard_p2_kernel<T, kScoreThreads>, dim3(rows * (unsigned)a.cs), dim3(kScoreThreads), 0, st, a,
+                      h.xall, h.gs_part, h.G, h.s_out);
+    default:
+      return launch_k(sv_shard_finish_kernel<T>, dim3(rows), dim3(32), 0, st, a, h.xall, h.gs_part, h.xtok_all, h.gs_tok,
+                      h.sall, h.gs_s, h.G);
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_score(const ScoreArgs &a, cudaStream_t st) {
   return a.bf16 ? launch_score_cfg<__nv_bfloat16>(a, st) : launch_score_cfg<float>(a, st);
+}
+
+cudaError_t launch_shard_score(const ShardScoreArgs &h, const ScoreArgs &a, cudaStream_t st) {
+  return a.bf16 ? shard_score_stage_t<__nv_bfloat16>(h, a, st) : shard_score_stage_t<float>(h, a, st);
 }
 
 }  // namespace sv
