@@ -12,16 +12,16 @@
  *    enqueues kernels on `stream` (a cudaStream_t; NULL = legacy default stream) and is
  *    therefore CUDA-graph capturable.  No global state; calls are thread-safe.
  *  - Host-detectable argument errors (NULL pointer, k outside [1, SV_MAX_K], V < 2,
- *    unsupported dtype, workspace too small, n_lat too short, V too large for the
- *    on-chip design) return a status != SV_OK and launch nothing.
+ *    unsupported dtype, workspace too small, n_lat too short, grid limits exceeded)
+ *    return a status != SV_OK and launch nothing.
  *  - Data errors found on the device (NaN / +inf logit, all -inf row, token outside
  *    [0, V), p_d(t) = 0, non-finite p_hat, L[n] <= 0, gamma outside [0, k]) never trap:
  *    they set per-row SV_ROW_* bits in `row_status` (when non-NULL) and write the
  *    deterministic sentinels documented per call.
  *  - Logit tensors are row-major with the vocabulary dimension contiguous; element
  *    strides between sequences (stride_b) and positions (stride_i) are free (0 is a legal
- *    broadcast).  Rows whose start is 16-byte aligned take the bulk-copy (TMA engine)
- *    path; others take a slower element-wise path with identical results.
+ *    broadcast).  Rows whose start is 16-byte aligned take the 16-byte vector-load path;
+ *    others take a slower element-wise path with identical results.
  *  - Results are bitwise reproducible for identical inputs and independent of B and of
  *    how a batch is split across GPUs: every reduction tree depends only on (V, dtype),
  *    and the global sequence id (seq_base + b) enters the Philox counter.
@@ -98,7 +98,8 @@ SV_API size_t sv_workspace_bytes(int32_t B, int32_t k, int32_t V, int32_t dtype)
 /* Human-readable text of a status code (static storage). */
 SV_API const char *sv_status_string(int32_t status);
 
-/* CTA-cluster size sv_score / sd_verify use for this (V, dtype); 0 if unsupported. */
+/* Vestigial (earlier on-chip designs): the CTA-cluster size that would hold a (D, C) row pair
+ * of this (V, dtype) in <= 80 KB per CTA; 0 if none <= 16.  No current kernel uses clusters. */
 SV_API int32_t sv_cluster_size(int32_t V, int32_t dtype);
 
 /*
@@ -121,8 +122,8 @@ SV_API int32_t sv_cluster_size(int32_t V, int32_t dtype);
  * draft_ptok = p_d(t).  draft_m / draft_l / draft_ptok feed sd_verify.
  * row_status [B, k] int32 or NULL.  Bad rows: S = A = KL = NaN, p_hat = 0.
  * S, A, KL, p_hat may be NULL individually (not computed-out); draft_* may not.
- * Limits: 1 <= k <= 16, 2 <= V, B * sv_cluster_size(V, dtype) < 2^31 (else SV_ERR_UNSUPPORTED),
- * sv_cluster_size(V, dtype) > 0.
+ * Limits: 1 <= k <= 16, 2 <= V < 2^31, 2 * B * k * ceil(V / 32768) < 2^31 (one CTA per
+ * chunk task; else SV_ERR_UNSUPPORTED).
  */
 SV_API int32_t sv_score(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok,
                  int32_t B, int32_t k, int32_t V, float tau_d, float tau_c, const sv_profile *prof,

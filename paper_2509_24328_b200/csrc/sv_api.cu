@@ -128,7 +128,6 @@ static int32_t shape_check(int32_t B, int32_t k, int32_t V, int32_t dtype) {
   if (B < 0 || k < 1 || k > SV_MAX_K || V < 2) return SV_ERR_INVALID_ARG;
   if (!dtype_ok(dtype)) return SV_ERR_UNSUPPORTED;
   if ((int64_t)B * (k + 1) >= (int64_t)1 << 31) return SV_ERR_INVALID_ARG;
-  if (cluster_size_for(V, elem_bytes(dtype)) == 0) return SV_ERR_UNSUPPORTED;
   return SV_OK;
 }
 
