@@ -10,6 +10,21 @@ __device__ __forceinline__ uint4 ldg(const void *p) {
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
+// exp2 on the FMA pipe: Cody-Waite split at the nearest integer (magic-number rounding), a
+// degree-6 minimax-style Taylor polynomial of 2^f on [-0.5, 0.5], exponent by integer add.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;
+  const float f = x - (t - 12582912.f);
+  float p = 1.5403530e-4f;
+  p = fmaf(p, f, 1.3333558e-3f);
+  p = fmaf(p, f, 9.6181291e-3f);
+  p = fmaf(p, f, 5.5504109e-2f);
+  p = fmaf(p, f, 2.4022651e-1f);
+  p = fmaf(p, f, 6.9314718e-1f);
+  p = fmaf(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+}
 template <int MODE, int U, int NT>
 __global__ void __launch_bounds__(256) k(const uint4 *__restrict__ d, const uint4 *__restrict__ c, size_t n, float *out) {
   float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f;
@@ -37,11 +52,25 @@ __global__ void __launch_bounds__(256) k(const uint4 *__restrict__ d, const uint
           acc0 += e0 + e1; acc1 += f0 + f1; acc2 = fmaf(e0, x0 - y0, fmaf(e1, x1 - y1, acc2));
         }
         if (MODE == 3) acc2 += ex2(fminf(fmaf(x0, 1.44f, -5.f), fmaf(y0, 1.44f, -5.f))) + ex2(fminf(fmaf(x1, 1.44f, -5.f), fmaf(y1, 1.44f, -5.f)));
+        if (MODE == 4) acc2 += ex2_poly(fminf(fmaf(x0, 1.44f, -5.f), fmaf(y0, 1.44f, -5.f))) + ex2_poly(fminf(fmaf(x1, 1.44f, -5.f), fmaf(y1, 1.44f, -5.f)));
+        if (MODE == 5) acc2 += ex2_poly(fminf(fmaf(x0, 1.44f, -5.f), fmaf(y0, 1.44f, -5.f))) + ex2(fminf(fmaf(x1, 1.44f, -5.f), fmaf(y1, 1.44f, -5.f)));
       }
     }
   }
   if (acc0 + acc1 + acc2 == 1234.5f) out[0] = acc0;
 }
+__global__ void acc_kernel(float *acc) {
+  float e1 = 0.f, e2 = 0.f;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 4000000; i += gridDim.x * blockDim.x) {
+    const float x = -40.f * (float)i / 4000000.f;
+    const double r = exp2((double)x);
+    e1 = fmaxf(e1, (float)fabs((ex2_poly(x) - r) / r));
+    e2 = fmaxf(e2, (float)fabs((ex2(x) - r) / r));
+  }
+  atomicMax((int *)&acc[0], __float_as_int(e1));
+  atomicMax((int *)&acc[1], __float_as_int(e2));
+}
+#include <cstdlib>
 int main() {
   const size_t big = (size_t)194584320;  // one of D / C at the headline (B=80, k=8, V=152064, bf16)
   uint4 *d, *c, *fl;
@@ -62,6 +91,19 @@ int main() {
     printf("%-26s %6.1f MB x%d blocks %5d: %7.1f us  %6.0f GB/s\n", name, bytes / 1e6, nt, blocks, ms * 1e3, nt * bytes / ms / 1e6);
   };
   const size_t t86 = (size_t)86 << 20;  // ~ K4's target rows at mean gamma 2.5
+  for (int bpsm : {4, 8}) {
+    run(k<3, 4, 2>, "3 ex2/pair 2T U4", sms * bpsm, big, 2);
+    run(k<4, 4, 2>, "2 ex2 + 1 poly /pair U4", sms * bpsm, big, 2);
+    run(k<5, 4, 2>, "2.5 ex2 + .5 poly U4", sms * bpsm, big, 2);
+  }
+  // accuracy of ex2_poly vs exp2 over [-40, 0]
+  {
+    float *acc; cudaMallocManaged(&acc, 4 * sizeof(float));
+    acc_kernel<<<256, 256>>>(acc);
+    cudaDeviceSynchronize();
+    printf("ex2_poly max rel err %.3g (vs exp2f), ex2.approx max rel err %.3g\n", acc[0], acc[1]);
+  }
+  if (getenv("CEIL_ONLY_POLY")) return 0;
   for (int bpsm : {2, 4, 8}) {
     run(k<0, 4, 1>, "read U4", sms * bpsm, t86, 1);
     run(k<0, 8, 1>, "read U8", sms * bpsm, t86, 1);
