@@ -194,6 +194,25 @@ SV_API int32_t sd_verify(const sv_logits *draft, const sv_logits *target, const 
                   float *accept_ratio, float *resid_mass, int32_t *row_status, void *workspace,
                   size_t workspace_bytes, void *stream);
 
+/*
+ * sd_verify_ragged -- sd_verify over a COMPACTED target (NEXT-3; P L266: the target forward
+ * only produces the gamma_b + 1 verified positions of each sequence).  Row i <= gamma_b of
+ * sequence b lives at target + (target_rowptr[b] + i) * target_row_stride elements (dtype of
+ * `draft`, vocabulary contiguous); target_rowptr [B] int64 on the device, e.g. the exclusive
+ * prefix sum of gamma_b + 1.  Rows past gamma_b do not exist and are never read.
+ * offset_dev: when non-NULL the Philox offset is read from this device word at run time
+ * (so a captured CUDA graph can advance it between replays); `offset` is then ignored.
+ * Everything else -- outputs, sentinels, workspace, limits, determinism -- as sd_verify;
+ * the results are bit-identical to sd_verify on the equivalent dense target.
+ */
+SV_API int32_t sd_verify_ragged(const sv_logits *draft, const void *target, int64_t target_row_stride,
+                                const int64_t *target_rowptr, const int32_t *draft_tok, const int32_t *gamma,
+                                const float *draft_m, const float *draft_l, const float *draft_ptok, int32_t B,
+                                int32_t k, int32_t V, float tau_d, float tau_t, uint64_t seed, uint64_t offset,
+                                const uint64_t *offset_dev, int64_t seq_base, int32_t *n_accept, int32_t *out_tok,
+                                float *accept_ratio, float *resid_mass, int32_t *row_status, void *workspace,
+                                size_t workspace_bytes, void *stream);
+
 /* ------------------------------------------------------------------------------------
  * Vocab-sharded staging (BASELINE config 4): the vocabulary of every row is
  * split over G ranks, rank r holding columns [v_begin, v_begin + V_local) of D, C and T

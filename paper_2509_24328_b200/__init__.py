@@ -18,8 +18,8 @@ from . import _lib
 from ._lib import (ROW_ALL_NEG_INF, ROW_BAD_GAMMA, ROW_BAD_LATENCY, ROW_BAD_TOKEN, ROW_DRAFT_ZERO,  # noqa: F401
                    ROW_NAN, ROW_PHAT_BAD, ROW_RESID_ZERO, SV_SCHED_BATCH_GREEDY, SV_SCHED_PER_ROW, SvError)
 
-__all__ = ["sv_score", "sv_schedule", "sd_verify", "workspace_bytes", "cluster_size", "Profile", "Pipeline",
-           "load_library"]
+__all__ = ["sv_score", "sv_schedule", "sd_verify", "sd_verify_ragged", "workspace_bytes", "cluster_size", "Profile",
+           "Pipeline", "GraphPipeline", "load_library"]
 
 
 def load_library():
@@ -157,6 +157,85 @@ def sd_verify(D, T, tok, gamma, draft_m, draft_l, draft_ptok, tau_d=1.0, tau_t=1
         _ptr(res["status"]), workspace.data_ptr(), workspace.numel(), _stream(stream))
     _lib.check(st, "sd_verify")
     return res
+
+
+def sd_verify_ragged(D, T_rows, t_rowptr, tok, gamma, draft_m, draft_l, draft_ptok, tau_d=1.0, tau_t=1.0, seed=0,
+                     offset=0, offset_dev=None, seq_base=0, workspace=None, out=None, stream=None) -> dict:
+    """Steps a5-a6 over a compacted target `T_rows` [R, V] (NEXT-3, P L266) through the C ABI
+    `sd_verify_ragged`; `t_rowptr` [B] int64 = first row of each sequence.  `offset_dev` (a CUDA
+    uint64/int64 scalar tensor) makes the Philox offset a device value (CUDA-graph replays)."""
+    B, k, V = D.shape
+    dev = D.device
+    if T_rows.dim() != 2 or T_rows.stride(1) != 1 or T_rows.dtype != D.dtype:
+        raise SvError("ragged target must be [rows, V] with the vocabulary contiguous and the draft's dtype")
+    o = out or {}
+    res = {
+        "n_accept": o.get("n_accept") if "n_accept" in o else torch.empty(B, dtype=torch.int32, device=dev),
+        "out_tok": o.get("out_tok") if "out_tok" in o else torch.empty(B, dtype=torch.int32, device=dev),
+        "accept_ratio": o.get("accept_ratio") if "accept_ratio" in o else torch.empty((B, k), dtype=torch.float32,
+                                                                                       device=dev),
+        "resid_mass": o.get("resid_mass") if "resid_mass" in o else torch.empty(B, dtype=torch.float32, device=dev),
+        "status": o.get("status") if "status" in o else torch.empty(B, dtype=torch.int32, device=dev),
+    }
+    if workspace is None:
+        workspace = new_workspace(B, k, V, D.dtype, dev)
+    st = _lib.load().sd_verify_ragged(
+        ctypes.byref(_logits(D)), T_rows.data_ptr(), T_rows.stride(0), _ptr(t_rowptr), _ptr(tok), _ptr(gamma),
+        _ptr(draft_m), _ptr(draft_l), _ptr(draft_ptok), B, k, V, float(tau_d), float(tau_t), ctypes.c_uint64(seed),
+        ctypes.c_uint64(offset), _ptr(offset_dev), int(seq_base), _ptr(res["n_accept"]), _ptr(res["out_tok"]),
+        _ptr(res["accept_ratio"]), _ptr(res["resid_mass"]), _ptr(res["status"]), workspace.data_ptr(),
+        workspace.numel(), _stream(stream))
+    _lib.check(st, "sd_verify_ragged")
+    return res
+
+
+class GraphPipeline:
+    """The whole step (sv_score -> sv_schedule -> sd_verify) captured once in a CUDA graph
+    (NEXT-3): inputs are copied into fixed device buffers, the Philox offset lives on the device
+    and advances by one per replay inside the graph, so replay j draws the same uniforms as an
+    eager step with offset = offset0 + j."""
+
+    def __init__(self, B, k, V, dtype, profile: Profile, latency: torch.Tensor, tau=(1.0, 1.0, 1.0),
+                 mode=SV_SCHED_PER_ROW, device="cuda", seed=0, offset0=0, seq_base=0):
+        self.pipe = Pipeline(B, k, V, dtype, profile, latency, tau, mode, device)
+        self.B, self.k, self.V = B, k, V
+        self.D = torch.empty((B, k, V), dtype=dtype, device=device)
+        self.C = torch.empty((B, k, V), dtype=dtype, device=device)
+        self.T = torch.empty((B, k + 1, V), dtype=dtype, device=device)
+        self.tok = torch.empty((B, k), dtype=torch.int32, device=device)
+        self.offset = torch.full((1,), offset0, dtype=torch.int64, device=device)
+        self.rowptr = (torch.arange(B, dtype=torch.int64, device=device) * (k + 1)).contiguous()
+        self.seed, self.seq_base = seed, seq_base
+        self.graph = None
+
+    def _step(self, stream):
+        p = self.pipe
+        sc = sv_score(self.D, self.C, self.tok, p.tau_d, p.tau_c, p.profile, workspace=p.workspace, out=p.score_out,
+                      stream=stream)
+        sh = sv_schedule(sc["p_hat"], p.latency, p.mode, 1, out=p.sched_out, stream=stream)
+        r = sd_verify_ragged(self.D, self.T.view(-1, self.V), self.rowptr, self.tok, sh["gamma"], sc["draft_m"],
+                             sc["draft_l"], sc["draft_ptok"], p.tau_d, p.tau_t, self.seed, 0, self.offset,
+                             self.seq_base, workspace=p.workspace, out=p.ver_out, stream=stream)
+        self.offset.add_(1)
+        return r
+
+    def capture(self):
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):  # warm the launch paths once outside the graph, then restore
+            off = self.offset.clone()
+            self._step(s)
+            self.offset.copy_(off)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.out = self._step(torch.cuda.current_stream())
+        return self
+
+    def replay(self):
+        self.graph.replay()
+        return self.out
 
 
 class Pipeline:

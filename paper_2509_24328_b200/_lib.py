@@ -17,7 +17,7 @@ ROW_PHAT_BAD, ROW_RESID_ZERO, ROW_BAD_GAMMA, ROW_BAD_LATENCY = 16, 32, 64, 128
 
 EXPORTS = ("sv_workspace_bytes", "sv_status_string", "sv_cluster_size", "sv_score", "sv_schedule", "sd_verify",
            "sv_shard_xch_bytes", "sv_shard_score_p1", "sv_shard_score_p2", "sv_shard_score_finish",
-           "sv_shard_verify_p1", "sv_shard_verify_p2", "sv_shard_verify_finish")
+           "sv_shard_verify_p1", "sv_shard_verify_p2", "sv_shard_verify_finish", "sd_verify_ragged")
 
 
 class SvLogits(ctypes.Structure):
@@ -62,6 +62,9 @@ def load(path: str = LIB_PATH):
     lib.sd_verify.argtypes = [LP, LP, P, P, P, P, P, i32, i32, i32, f32, f32, u64, u64, i64,
                               P, P, P, P, P, P, sz, P]
     lib.sd_verify.restype = i32
+    lib.sd_verify_ragged.argtypes = [LP, P, i64, P, P, P, P, P, P, i32, i32, i32, f32, f32, u64, u64, P, i64,
+                                     P, P, P, P, P, P, sz, P]
+    lib.sd_verify_ragged.restype = i32
     lib.sv_shard_xch_bytes.argtypes = [i32, i32, i32, i32, i32]
     lib.sv_shard_xch_bytes.restype = sz
     lib.sv_shard_score_p1.argtypes = [LP, LP, P, i32, i32, i32, i64, f32, f32, P, P]

@@ -31,6 +31,14 @@ namespace {
 #define SV_MAX_K_DEV 16
 constexpr int kFindChunks = 8;  // K5b: slice-mass chunks of 32 loaded together
 
+// Target row i of sequence b: dense [B, k+1, V] (strides) or ragged / compacted (NEXT-3, P L266:
+// rows of sequence b at t_rowptr[b] + i, i <= gamma_b, row stride t_si)
+template <typename T>
+__device__ __forceinline__ const T *trow(const VerifyArgs &a, int64_t b, int64_t i) {
+  const T *base = reinterpret_cast<const T *>(a.t);
+  return a.t_rowptr ? base + (a.t_rowptr[b] + i) * a.t_si : base + b * a.t_sb + i * a.t_si;
+}
+
 // ------------------------------------------------------------------ K4
 // One warp item (row, split): the (M, sum-exp) partial of 32 lanes x U 16-byte units of the
 // target row (unit u = lane + 32 j: every load instruction reads 512 contiguous bytes).
@@ -40,7 +48,7 @@ __device__ __forceinline__ float2 rows_warp_item(const VerifyArgs &a, int64_t b,
   const int lane = threadIdx.x & 31;
   const int64_t v0 = split * a.rows_chunk;
   const int n = (int)min(a.rows_chunk, (int64_t)a.V - v0);
-  const T *src = reinterpret_cast<const T *>(a.t) + b * a.t_sb + i * a.t_si + v0;
+  const T *src = trow<T>(a, b, i) + v0;
   const float c = a.ct;
   float m = kMFloor;
   double l = 0.0;
@@ -115,6 +123,7 @@ __global__ void __launch_bounds__(32 * (SV_MAX_K_DEV + 1)) sv_decide_kernel(cons
   float dl = 0.f, dpt = 0.f, dmv = 0.f, xt = 0.f;
   uint4 w = make_uint4(0u, 0u, 0u, 0u);
   if (wid == 0 && gok && lane <= g) {
+    const uint64_t off = a.offset_dev ? *a.offset_dev : a.offset;  // device offset: graph replays
     if (lane < g) {
       const int64_t ri = b * k + lane;
       t = a.tok[ri];
@@ -129,11 +138,11 @@ __global__ void __launch_bounds__(32 * (SV_MAX_K_DEV + 1)) sv_decide_kernel(cons
             if (xt != xt) xt = v;
           }
         } else {
-          xt = Elem<T>::load(reinterpret_cast<const T *>(a.t) + b * a.t_sb + lane * a.t_si + t);
+          xt = Elem<T>::load(trow<T>(a, b, lane) + t);
         }
       }
     }
-    w = sv_philox(a.seed, a.offset, a.seq_base + b, lane);
+    w = sv_philox(a.seed, off, a.seq_base + b, lane);
   }
   if (gok && wid <= g) {  // merge row wid: lane-strided sequential, then butterfly
     // partial j of G x splits (rank, split) = vocabulary order; G = 1 unless vocab-sharded
@@ -284,7 +293,7 @@ __global__ void __launch_bounds__(kRowsThreads, 3) sv_rows_kernel(const __grid_c
         if (a.xtok_out && split == 0 && i < a.k) {  // vocab-sharded: token logit if owned, else NaN
           const int64_t loc = (int64_t)a.tok[b * a.k + i] - a.v_begin;
           a.xtok_out[b * a.k + i] = (loc >= 0 && loc < a.V)
-                                        ? Elem<T>::load(reinterpret_cast<const T *>(a.t) + b * a.t_sb + i * a.t_si + loc)
+                                        ? Elem<T>::load(trow<T>(a, b, i) + loc)
                                         : __int_as_float(0x7fc00000);
         }
       }
@@ -303,7 +312,7 @@ struct SampleRow {
 template <typename T>
 __device__ __forceinline__ SampleRow<T> sample_row(const VerifyArgs &a, const Decision &dc, int64_t b) {
   SampleRow<T> r;
-  r.t = reinterpret_cast<const T *>(a.t) + b * a.t_sb + (int64_t)dc.N * a.t_si;
+  r.t = trow<T>(a, b, dc.N);
   r.d = reinterpret_cast<const T *>(a.d) + b * a.d_sb + (int64_t)dc.N * a.d_si;
   r.ct = a.ct;
   r.nmt = -(dc.Mt * a.ct);

@@ -351,6 +351,36 @@ int32_t sd_verify(const sv_logits *draft, const sv_logits *target, const int32_t
   return SV_OK;
 }
 
+int32_t sd_verify_ragged(const sv_logits *draft, const void *target, int64_t target_row_stride,
+                         const int64_t *target_rowptr, const int32_t *draft_tok, const int32_t *gamma,
+                         const float *draft_m, const float *draft_l, const float *draft_ptok, int32_t B, int32_t k,
+                         int32_t V, float tau_d, float tau_t, uint64_t seed, uint64_t offset,
+                         const uint64_t *offset_dev, int64_t seq_base, int32_t *n_accept, int32_t *out_tok,
+                         float *accept_ratio, float *resid_mass, int32_t *row_status, void *workspace,
+                         size_t workspace_bytes, void *stream) {
+  if (!draft || !target || !target_rowptr || target_row_stride < V) return SV_ERR_INVALID_ARG;
+  int32_t r = shape_check(B, k, V, draft->dtype);
+  if (r != SV_OK) return r;
+  if ((r = logits_check(draft, draft->dtype)) != SV_OK) return r;
+  if (!draft_tok || !gamma || !draft_m || !draft_l || !draft_ptok || !n_accept || !out_tok) return SV_ERR_INVALID_ARG;
+  if (!(tau_d > 0.f) || !(tau_t > 0.f) || seq_base < 0) return SV_ERR_INVALID_ARG;
+  if (B == 0) return SV_OK;
+  if (!workspace || workspace_bytes < sv_workspace_bytes(B, k, V, draft->dtype)) return SV_ERR_WORKSPACE;
+  if ((reinterpret_cast<uintptr_t>(workspace) & 15) != 0) return SV_ERR_INVALID_ARG;
+  const sv_logits tl = {target, draft->dtype, 0, 0, target_row_stride};
+  VerifyArgs a = make_verify_args(draft, &tl, draft_tok, gamma, draft_m, draft_l, draft_ptok, B, k, V, tau_d, tau_t,
+                                  seed, offset, seq_base, n_accept, out_tok, accept_ratio, resid_mass, row_status,
+                                  workspace, V);
+  a.t_rowptr = target_rowptr;
+  a.offset_dev = offset_dev;
+  const cudaError_t e = launch_verify(a, (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "libsv: sd_verify_ragged launch failed: %s\n", cudaGetErrorString(e));
+    return SV_ERR_CUDA;
+  }
+  return SV_OK;
+}
+
 // ------------------------------------------------------------------ vocab-sharded staging
 // Exchange blocks (sv_shard_xch_bytes): 0 = score P1, 1 = score P2, 2 = verify P1, 3 = verify P2.
 static int64_t xch_part_bytes(int stage, int64_t B, int k, int64_t V_local, int eb) {

@@ -139,6 +139,8 @@ struct VerifyArgs {
   int G, rank;
   int64_t v_begin;
   int32_t Vg;  // global vocabulary (token range checks); = V unless vocab-sharded
+  const int64_t *t_rowptr;    // ragged target (NEXT-3): first row of sequence b, NULL = dense
+  const uint64_t *offset_dev;  // Philox offset read on the device (CUDA-graph replays), NULL = offset
   int64_t gs_part, gs_tok, gs_mass;  // elements between consecutive ranks' gathered blocks
   const float *xtok_all;  // [G][B][k] target token logits (NaN where not owned)
   float *xtok_out;        // [B][k] this rank's (K4 writes them when non-NULL)
