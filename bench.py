@@ -437,6 +437,24 @@ def run_ours(args, rank, world, local_rank):
     g_ms_step = g_ms / args.steps
     del gp
 
+    # ---------------- NEXT-4: GPU profile builder on a 65,536-record profiling run (P L176,
+    # S L331's run size): records = this step's (S, A, accept_ratio) with gamma = k, tiled
+    ver_full = pipe.ver_out
+    recs = [t.reshape(-1) for t in (pipe.score_out["S"], pipe.score_out["A"], ver_full["accept_ratio"])]
+    n_rec = 65536
+    rep = (n_rec + recs[0].numel() - 1) // recs[0].numel()
+    S_r, A_r, X_r = (torch.nan_to_num(t, nan=0.0).repeat(rep)[:n_rec].contiguous() for t in recs)
+    sv.sv_profile_build(S_r, A_r, X_r)
+    barrier()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    n_pb = 5
+    for _ in range(n_pb):
+        sv.sv_profile_build(S_r, A_r, X_r)
+    p1.record(stream)
+    barrier()
+    prof_ms = p0.elapsed_time(p1) / n_pb
+
     # ---------------- e2e: host buffers, H2D + pipeline + D2H every step
     e2e_steps = min(args.steps, 20)
     hout = torch.empty((2, B), dtype=torch.int32).pin_memory()
@@ -494,6 +512,9 @@ def run_ours(args, rank, world, local_rank):
                            "ms_per_step": g_ms_step,
                            "note": "whole step captured once (sv_score, sv_schedule, sd_verify_ragged, offset += 1) "
                                    "and replayed; inputs (608 MB) > L2"},
+            "profile_build": {"records": n_rec, "ms": prof_ms, "bins": "20 x 15, X in 10 bins",
+                              "note": "NEXT-4 offline builder (sv_profile_build), incl. its host sync for the "
+                                      "kept-bin counts"},
             "e2e": {"value": world * B * k / (e2e_ms / e2e_steps * 1e-3), "unit": "positions/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                     "path": "pinned host -> cudaMemcpyAsync -> sv_score/sv_schedule/sd_verify (C ABI) -> host"},

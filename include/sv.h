@@ -213,6 +213,29 @@ SV_API int32_t sd_verify_ragged(const sv_logits *draft, const void *target, int6
                                 float *accept_ratio, float *resid_mass, int32_t *row_status, void *workspace,
                                 size_t workspace_bytes, void *stream);
 
+/*
+ * sv_profile_build -- NEXT-4: the offline (S, A) -> acceptance profile of a profiling run and
+ * its information-gain report (P L176 "adaptive binning ... compute the average token
+ * acceptance probability for each bin combination"; S L275-310; Table 2 layout P L347-368).
+ * Records: S, A, X [N] fp32 on the device (S, A from sv_score; X = accept_ratio from sd_verify,
+ * the true acceptance probability min(1, p_t(t)/p_d(t)), P L150).
+ * Edges: equal-frequency, interior edge j = the ceil(j N / n_bins)-th order statistic, first =
+ * min, last = max, duplicates collapsed (S L278, L281) -> s_edges [n_s_bins + 1],
+ * a_edges [n_a_bins + 1] fp32; n_bins[0..1] (device int32) = bins kept per axis (n_s, n_a).
+ * cells [n_s][n_a] fp64 (layout with the KEPT bin counts) = mean X per right-closed cell (R9)
+ * with the S L296 fallbacks pre-filled (empty cell -> its S-row mean -> global mean): the
+ * `cells` sv_score looks up (cast to fp32).  counts [n_s][n_a] int32.
+ * info [5] fp64 or NULL: H(X), H(X|S), H(X|A), H(X|S,A), I(X;S,A) in bits, X in x_bins
+ * equal-width bins on [0, 1] (S L328).  Deterministic (integer / fixed-point accumulation).
+ * Limits: 1 <= n_s_bins, n_a_bins <= 64, 1 <= x_bins <= 1024.  Workspace:
+ * sv_profile_workspace_bytes(N, n_s_bins, n_a_bins, x_bins) bytes (no zero-fill needed).
+ */
+SV_API size_t sv_profile_workspace_bytes(int32_t N, int32_t n_s_bins, int32_t n_a_bins, int32_t x_bins);
+SV_API int32_t sv_profile_build(const float *S, const float *A, const float *X, int32_t N, int32_t n_s_bins,
+                                int32_t n_a_bins, int32_t x_bins, float *s_edges, float *a_edges, int32_t *n_bins,
+                                double *cells, int32_t *counts, double *info, void *workspace,
+                                size_t workspace_bytes, void *stream);
+
 /* ------------------------------------------------------------------------------------
  * Vocab-sharded staging (BASELINE config 4): the vocabulary of every row is
  * split over G ranks, rank r holding columns [v_begin, v_begin + V_local) of D, C and T

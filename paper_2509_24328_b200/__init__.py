@@ -19,7 +19,7 @@ from ._lib import (ROW_ALL_NEG_INF, ROW_BAD_GAMMA, ROW_BAD_LATENCY, ROW_BAD_TOKE
                    ROW_NAN, ROW_PHAT_BAD, ROW_RESID_ZERO, SV_SCHED_BATCH_GREEDY, SV_SCHED_PER_ROW, SvError)
 
 __all__ = ["sv_score", "sv_schedule", "sd_verify", "sd_verify_ragged", "workspace_bytes", "cluster_size", "Profile",
-           "Pipeline", "GraphPipeline", "load_library"]
+           "Pipeline", "GraphPipeline", "sv_profile_build", "load_library"]
 
 
 def load_library():
@@ -187,6 +187,30 @@ def sd_verify_ragged(D, T_rows, t_rowptr, tok, gamma, draft_m, draft_l, draft_pt
         workspace.numel(), _stream(stream))
     _lib.check(st, "sd_verify_ragged")
     return res
+
+
+def sv_profile_build(S, A, X, n_s_bins=20, n_a_bins=15, x_bins=10, stream=None) -> dict:
+    """NEXT-4 (P L176; S L275-310): the offline (S, A) -> acceptance profile of N records and the
+    Table-2 information-gain report, through the C ABI `sv_profile_build`."""
+    S, A, X = (t.reshape(-1).contiguous().float() for t in (S, A, X))
+    N = S.numel()
+    dev = S.device
+    ws = torch.empty(int(_lib.load().sv_profile_workspace_bytes(N, n_s_bins, n_a_bins, x_bins)) or 16,
+                     dtype=torch.uint8, device=dev)
+    se = torch.empty(n_s_bins + 1, dtype=torch.float32, device=dev)
+    ae = torch.empty(n_a_bins + 1, dtype=torch.float32, device=dev)
+    nb = torch.empty(2, dtype=torch.int32, device=dev)
+    cells = torch.empty(n_s_bins * n_a_bins, dtype=torch.float64, device=dev)
+    counts = torch.empty(n_s_bins * n_a_bins, dtype=torch.int32, device=dev)
+    info = torch.empty(5, dtype=torch.float64, device=dev)
+    st = _lib.load().sv_profile_build(_ptr(S), _ptr(A), _ptr(X), N, n_s_bins, n_a_bins, x_bins, _ptr(se), _ptr(ae),
+                                      _ptr(nb), _ptr(cells), _ptr(counts), _ptr(info), ws.data_ptr(), ws.numel(),
+                                      _stream(stream))
+    _lib.check(st, "sv_profile_build")
+    ns, na = (int(v) for v in nb.tolist())
+    return {"s_edges": se[: ns + 1], "a_edges": ae[: na + 1], "cells": cells[: ns * na].view(ns, na),
+            "counts": counts[: ns * na].view(ns, na), "n_s": ns, "n_a": na,
+            "info": dict(zip(("h_x", "h_x_s", "h_x_a", "h_x_sa", "i_x_sa"), info.tolist()))}
 
 
 class GraphPipeline:

@@ -17,7 +17,8 @@ ROW_PHAT_BAD, ROW_RESID_ZERO, ROW_BAD_GAMMA, ROW_BAD_LATENCY = 16, 32, 64, 128
 
 EXPORTS = ("sv_workspace_bytes", "sv_status_string", "sv_cluster_size", "sv_score", "sv_schedule", "sd_verify",
            "sv_shard_xch_bytes", "sv_shard_score_p1", "sv_shard_score_p2", "sv_shard_score_finish",
-           "sv_shard_verify_p1", "sv_shard_verify_p2", "sv_shard_verify_finish", "sd_verify_ragged")
+           "sv_shard_verify_p1", "sv_shard_verify_p2", "sv_shard_verify_finish", "sd_verify_ragged",
+           "sv_profile_workspace_bytes", "sv_profile_build")
 
 
 class SvLogits(ctypes.Structure):
@@ -65,6 +66,10 @@ def load(path: str = LIB_PATH):
     lib.sd_verify_ragged.argtypes = [LP, P, i64, P, P, P, P, P, P, i32, i32, i32, f32, f32, u64, u64, P, i64,
                                      P, P, P, P, P, P, sz, P]
     lib.sd_verify_ragged.restype = i32
+    lib.sv_profile_workspace_bytes.argtypes = [i32, i32, i32, i32]
+    lib.sv_profile_workspace_bytes.restype = sz
+    lib.sv_profile_build.argtypes = [P, P, P, i32, i32, i32, i32, P, P, P, P, P, P, P, sz, P]
+    lib.sv_profile_build.restype = i32
     lib.sv_shard_xch_bytes.argtypes = [i32, i32, i32, i32, i32]
     lib.sv_shard_xch_bytes.restype = sz
     lib.sv_shard_score_p1.argtypes = [LP, LP, P, i32, i32, i32, i64, f32, f32, P, P]

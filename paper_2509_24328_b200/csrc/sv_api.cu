@@ -381,6 +381,65 @@ int32_t sd_verify_ragged(const sv_logits *draft, const void *target, int64_t tar
   return SV_OK;
 }
 
+// ------------------------------------------------------------------ NEXT-4 profile builder
+static int64_t prof_ws_layout(int32_t N, int32_t ns, int32_t na, int32_t xb, int64_t off[5]) {
+  off[0] = 0;                                              // s_sorted
+  off[1] = off[0] + ws_round((int64_t)N * 4);              // a_sorted
+  off[2] = off[1] + ws_round((int64_t)N * 4);              // xsum
+  off[3] = off[2] + ws_round((int64_t)ns * na * 8);        // joint
+  off[4] = off[3] + ws_round((int64_t)ns * na * xb * 4);   // scratch
+  return off[4] + ws_round((int64_t)xb * 4);
+}
+
+size_t sv_profile_workspace_bytes(int32_t N, int32_t n_s_bins, int32_t n_a_bins, int32_t x_bins) {
+  if (N < 1 || n_s_bins < 1 || n_a_bins < 1 || x_bins < 1 || n_s_bins > kProfMaxBins || n_a_bins > kProfMaxBins ||
+      x_bins > 1024)
+    return 0;
+  int64_t off[5];
+  return (size_t)prof_ws_layout(N, n_s_bins, n_a_bins, x_bins, off);
+}
+
+int32_t sv_profile_build(const float *S, const float *A, const float *X, int32_t N, int32_t n_s_bins, int32_t n_a_bins,
+                         int32_t x_bins, float *s_edges, float *a_edges, int32_t *n_bins, double *cells,
+                         int32_t *counts, double *info, void *workspace, size_t workspace_bytes, void *stream) {
+  const size_t need = sv_profile_workspace_bytes(N, n_s_bins, n_a_bins, x_bins);
+  if (need == 0 || !S || !A || !X || !s_edges || !a_edges || !n_bins || !cells || !counts) return SV_ERR_INVALID_ARG;
+  if (!workspace || workspace_bytes < need) return SV_ERR_WORKSPACE;
+  if ((reinterpret_cast<uintptr_t>(workspace) & 15) != 0) return SV_ERR_INVALID_ARG;
+  int64_t off[5];
+  prof_ws_layout(N, n_s_bins, n_a_bins, x_bins, off);
+  uint8_t *w = reinterpret_cast<uint8_t *>(workspace);
+  ProfileArgs a = {};
+  a.S = S;
+  a.A = A;
+  a.X = X;
+  a.N = N;
+  a.n_s_bins = n_s_bins;
+  a.n_a_bins = n_a_bins;
+  a.x_bins = x_bins;
+  a.s_sorted = reinterpret_cast<float *>(w + off[0]);
+  a.a_sorted = reinterpret_cast<float *>(w + off[1]);
+  a.xsum = reinterpret_cast<unsigned long long *>(w + off[2]);
+  a.joint = reinterpret_cast<int32_t *>(w + off[3]);
+  a.scratch = reinterpret_cast<int32_t *>(w + off[4]);
+  a.s_edges = s_edges;
+  a.a_edges = a_edges;
+  a.n_s = n_bins;
+  a.n_a = n_bins + 1;
+  a.counts = counts;
+  a.cells = cells;
+  a.info = info;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(w + off[2], 0, (size_t)(off[4] - off[2]), st);  // xsum + joint
+  if (e == cudaSuccess) e = cudaMemsetAsync(counts, 0, (size_t)n_s_bins * n_a_bins * 4, st);
+  if (e == cudaSuccess) e = launch_profile(a, st);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "libsv: sv_profile_build launch failed: %s\n", cudaGetErrorString(e));
+    return SV_ERR_CUDA;
+  }
+  return SV_OK;
+}
+
 // ------------------------------------------------------------------ vocab-sharded staging
 // Exchange blocks (sv_shard_xch_bytes): 0 = score P1, 1 = score P2, 2 = verify P1, 3 = verify P2.
 static int64_t xch_part_bytes(int stage, int64_t B, int k, int64_t V_local, int eb) {

@@ -149,6 +149,23 @@ struct VerifyArgs {
 // sd_verify's share of the workspace
 int64_t verify_ws_bytes(int64_t B, int k, int64_t splits, int nsl);
 cudaError_t launch_verify(const VerifyArgs &a, cudaStream_t st);
+
+// NEXT-4: offline profile builder (sv_profile.cu)
+constexpr int kProfMaxBins = 64;
+struct ProfileArgs {
+  const float *S, *A, *X;
+  int32_t N, n_s_bins, n_a_bins, x_bins;
+  float *s_sorted, *a_sorted;  // workspace [N] each
+  float *s_edges, *a_edges;    // outputs [n_bins + 1]
+  int32_t *n_s, *n_a;          // outputs: bins after the duplicate collapse
+  int32_t *counts;             // output [n_s][n_a] (actual bins), zeroed by the launcher
+  unsigned long long *xsum;    // workspace [n_s_bins * n_a_bins] fixed-point X sums
+  int32_t *joint;              // workspace [n_s_bins * n_a_bins * x_bins]
+  int32_t *scratch;            // workspace [x_bins]
+  double *cells;               // output [n_s][n_a]
+  double *info;                // output [5] or NULL
+};
+cudaError_t launch_profile(const ProfileArgs &a, cudaStream_t st);
 cudaError_t launch_verify_stage(int stage, const VerifyArgs &a, cudaStream_t st);
 
 }  // namespace sv
