@@ -429,3 +429,97 @@ def test_verify_bad_inputs():
     assert r["status"][0] == 0 and r["status"][1] & oracle.ROW_NAN and r["out_tok"][1] == -1
     r = oracle.verify(D, T[:, :, :], [[0, 5], [0, 0]], [2, 3])
     assert r["status"][0] & oracle.ROW_BAD_TOKEN and r["status"][1] & oracle.ROW_BAD_GAMMA
+
+
+# ----------------------------------------------------------------- NEXT-2: sampling filters
+def test_filter_spec_examples():
+    """S L79-81: [.7,.2,.1] with top_k = 1 -> [1,0,0]; [.5,.3,.2] with top_p = .8 keeps the
+    first two -> [.625,.375,0].  The literal top_p = 0.8 sits exactly on the cumulative 0.5+0.3
+    (a rounding tie in fp64), so the pin uses 0.79 (keeps two) and 0.81 (keeps three)."""
+    from oracle.filtered import filter_dist
+    p, keep = filter_dist(np.log([0.7, 0.2, 0.1]), top_k=1)
+    assert np.array_equal(p, [1.0, 0.0, 0.0]) and list(keep) == [0]
+    p, _ = filter_dist(np.log([0.5, 0.3, 0.2]), top_p=0.79)
+    assert np.allclose(p, [0.625, 0.375, 0.0], rtol=0, atol=1e-15)
+    p, _ = filter_dist(np.log([0.5, 0.3, 0.2]), top_p=0.81)
+    assert np.allclose(p, [0.5, 0.3, 0.2], rtol=0, atol=1e-15)
+
+
+def test_filter_identity_idempotence_support():
+    """Identity config = plain softmax (S L78) and idempotent; every config shrinks the support
+    (S L196-197: "idempotent for identity config and monotone-support-shrinking otherwise");
+    top-k alone is idempotent; top_k ties go to the lower index (DESIGN R21)."""
+    import oracle
+    from oracle.filtered import filter_dist
+    rng = np.random.default_rng(5)
+    for _ in range(20):
+        x = rng.normal(0, 3, 50)
+        p, _ = filter_dist(x, 0.7)
+        ref, _ = oracle.softmax(x, 0.7)
+        assert np.allclose(p, ref, rtol=1e-13, atol=1e-16)
+        for k, tp in ((20, 0.8), (0, 0.9), (5, 1.0), (1, 0.5)):
+            q, keep = filter_dist(x, 0.7, k, tp)
+            assert abs(q.sum() - 1.0) < 1e-12 and np.all(q >= 0)
+            assert np.count_nonzero(q) <= (k if k else 50) and np.count_nonzero(q) == len(keep)
+            xf = np.where(q > 0, np.log(np.where(q > 0, q, 1.0)), -np.inf)
+            q2, _ = filter_dist(xf, 1.0, k, tp)
+            assert np.all((q2 > 0) <= (q > 0)) and np.all((q > 0) <= (p > 0))  # support shrinks
+            if tp == 1.0:
+                assert np.allclose(q, q2, rtol=1e-12, atol=1e-15)  # top-k alone: idempotent
+    # ties: equal logits -> the lower indices are kept
+    q, keep = filter_dist(np.array([1.0, 3.0, 3.0, 3.0, 0.0]), 1.0, 2)
+    assert list(keep) == [1, 2] and q[3] == 0.0
+
+
+def test_filter_score_identities():
+    """Filtered S / A / KL keep the unfiltered identities (S L233-235): identical rows -> S = 1,
+    A = 1, KL = 0; S = 1 - TV; A = 1 whenever p'_c(t) >= p'_d(t)."""
+    from oracle.filtered import filter_dist, score_filtered
+    rng = np.random.default_rng(9)
+    D = rng.normal(0, 2, (2, 3, 40))
+    C = D + rng.normal(0, 0.7, D.shape)
+    tok = np.zeros((2, 3), dtype=np.int32)
+    for b in range(2):
+        for i in range(3):
+            tok[b, i] = int(np.argmax(filter_dist(D[b, i], 1.0, 8, 0.9)[0]))
+    r = score_filtered(D, D, tok, 1.0, 1.0, 8, 0.9)
+    assert np.allclose(r["S"], 1.0) and np.allclose(r["A"], 1.0) and np.allclose(r["KL"], 0.0)
+    r = score_filtered(D, C, tok, 1.0, 1.0, 8, 0.9)
+    for b in range(2):
+        for i in range(3):
+            pd, _ = filter_dist(D[b, i], 1.0, 8, 0.9)
+            pc, _ = filter_dist(C[b, i], 1.0, 8, 0.9)
+            assert abs(r["S"][b, i] - (1 - 0.5 * np.abs(pd - pc).sum())) < 1e-12
+            if pc[tok[b, i]] >= pd[tok[b, i]]:
+                assert r["A"][b, i] == 1.0
+
+
+def test_filter_losslessness_monte_carlo():
+    """Under filters the emitted token still follows the FILTERED target (S L156, L183):
+    t ~ p'_d per trial, verify_filtered with gamma = 1, chi-square over 20,000 trials."""
+    from scipy import stats
+    from oracle.filtered import filter_dist, verify_filtered
+    import oracle
+    rng = np.random.default_rng(13)
+    V = 7
+    xd = rng.normal(0, 1.5, V)
+    xt = rng.normal(0, 1.5, V)
+    pd, _ = filter_dist(xd, 1.0, 5, 0.95)
+    pt, _ = filter_dist(xt, 1.0, 5, 0.95)
+    D = xd.reshape(1, 1, V)
+    T = np.stack([xt, xt]).reshape(1, 2, V)
+    n = 20000
+    counts = np.zeros(V)
+    cdf = np.cumsum(pd)
+    for j in range(n):
+        u = oracle.uniforms(77, j, 0, 1)[0]  # an independent stream for the draft token
+        t = int(np.searchsorted(cdf, u, side="right"))
+        t = min(t, V - 1)
+        while pd[t] == 0.0:
+            t -= 1
+        r = verify_filtered(D, T, np.array([[t]]), np.array([1]), 1.0, 1.0, 5, 0.95, 11, j)
+        counts[r["out_tok"][0] if r["n_accept"][0] == 0 else t] += 1
+    m = pt > 0
+    assert counts[~m].sum() == 0
+    chi = stats.chisquare(counts[m], pt[m] * n)
+    assert chi.pvalue > 1e-4, chi
