@@ -437,6 +437,29 @@ def run_ours(args, rank, world, local_rank):
     g_ms_step = g_ms / args.steps
     del gp
 
+    # ---------------- NEXT-2: the step under the paper's Qwen sampling filters (Table 5: top_k 20,
+    # top_p 0.8, tau 0.7) on the same inputs
+    fws = sv.new_filter_workspace(B, k, dev)
+    fgam = torch.empty(B, dtype=torch.int32, device=dev)
+
+    def fstep(j):
+        D, C, T, tok = sets[j & 1]
+        fs = sv.sv_score_filtered(D, C, tok, 20, 0.8, 0.7, 0.7, prof, fworkspace=fws, stream=stream)
+        g = sv.sv_schedule(fs["p_hat"], L, out={"gamma": fgam}, stream=stream)["gamma"]
+        return sv.sd_verify_filtered(T, tok, g, fws, 20, 0.8, 0.7, 0xC0FFEE, j, seq_base, stream=stream)
+
+    for j in range(args.warmup):
+        fstep(j)
+    barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f_steps = max(10, args.steps // 4)
+    f0.record(stream)
+    for j in range(f_steps):
+        fstep(args.warmup + j)
+    f1.record(stream)
+    barrier()
+    f_ms_step = f0.elapsed_time(f1) / f_steps
+
     # ---------------- NEXT-4: GPU profile builder on a 65,536-record profiling run (P L176,
     # S L331's run size): records = this step's (S, A, accept_ratio) with gamma = k, tiled
     ver_full = pipe.ver_out
@@ -512,6 +535,10 @@ def run_ours(args, rank, world, local_rank):
                            "ms_per_step": g_ms_step,
                            "note": "whole step captured once (sv_score, sv_schedule, sd_verify_ragged, offset += 1) "
                                    "and replayed; inputs (608 MB) > L2"},
+            "filtered": {"value": world * B * k / (f_ms_step * 1e-3), "unit": "positions/s", "ms_per_step": f_ms_step,
+                         "filters": "top_k 20, top_p 0.8, tau 0.7 on draft / companion / target (P L731-743)",
+                         "note": "NEXT-2: radix-select top-k per row + list arithmetic; output allocations per "
+                                 "call included"},
             "profile_build": {"records": n_rec, "ms": prof_ms, "bins": "20 x 15, X in 10 bins",
                               "note": "NEXT-4 offline builder (sv_profile_build), incl. its host sync for the "
                                       "kept-bin counts"},

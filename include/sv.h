@@ -214,6 +214,42 @@ SV_API int32_t sd_verify_ragged(const sv_logits *draft, const void *target, int6
                                 size_t workspace_bytes, void *stream);
 
 /*
+ * Sampling filters (NEXT-2): temperature -> top_k -> top_p -> renormalise, applied to the
+ * draft, companion AND target distributions before S / A and the accept test (S L73-81, L183,
+ * L238; P L731-743 Table 5: Qwen top_k 20, top_p 0.8, tau 0.7).  Readings (DESIGN R21): top_k
+ * keeps the top_k largest logits, ties to the lower vocabulary index; top_p keeps the shortest
+ * prefix of the top-k distribution (probability desc, index asc) whose sequential fp64
+ * cumulative mass is >= top_p.  Supported: 1 <= top_k <= 32 (each filtered distribution has at
+ * most 32 entries), 0 < top_p <= 1; top_p without top_k (full-vocabulary nucleus) returns
+ * SV_ERR_UNSUPPORTED.
+ *
+ * sv_score_filtered: S, A, KL, p_hat, draft_ptok (= p'_d(t)), row_status [B, k] as sv_score but
+ * over the filtered distributions (KL = +inf when the draft keeps a token the companion
+ * dropped); it also leaves the filtered draft lists in `fworkspace` for sd_verify_filtered.
+ * sd_verify_filtered: accept t_i iff u_i < p'_t(t_i)/p'_d(t_i); at the first rejection N the
+ * residual max(0, p'_t - p'_d), else the bonus p'_t of row gamma; inverse CDF in vocabulary
+ * order (R11), Philox as sd_verify (R12).  accept_ratio = min(1, ratio) for the positions
+ * tested (i <= N, i < gamma), NaN beyond.  fworkspace: sv_filter_workspace_bytes(B, k), the
+ * same buffer for both calls of a step (no zero-fill needed).
+ */
+typedef struct {
+    int32_t top_k;
+    float top_p;
+} sv_filter;
+
+SV_API size_t sv_filter_workspace_bytes(int32_t B, int32_t k);
+SV_API int32_t sv_score_filtered(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok,
+                                 int32_t B, int32_t k, int32_t V, float tau_d, float tau_c,
+                                 const sv_filter *filt, const sv_profile *prof, float *S, float *A, float *KL,
+                                 float *p_hat, float *draft_ptok, int32_t *row_status, void *fworkspace,
+                                 size_t fworkspace_bytes, void *stream);
+SV_API int32_t sd_verify_filtered(const sv_logits *target, const int32_t *draft_tok, const int32_t *gamma,
+                                  int32_t B, int32_t k, int32_t V, float tau_t, const sv_filter *filt,
+                                  uint64_t seed, uint64_t offset, int64_t seq_base, int32_t *n_accept,
+                                  int32_t *out_tok, float *accept_ratio, float *resid_mass, int32_t *row_status,
+                                  void *fworkspace, size_t fworkspace_bytes, void *stream);
+
+/*
  * sv_profile_build -- NEXT-4: the offline (S, A) -> acceptance profile of a profiling run and
  * its information-gain report (P L176 "adaptive binning ... compute the average token
  * acceptance probability for each bin combination"; S L275-310; Table 2 layout P L347-368).

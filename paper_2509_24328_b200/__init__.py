@@ -19,7 +19,7 @@ from ._lib import (ROW_ALL_NEG_INF, ROW_BAD_GAMMA, ROW_BAD_LATENCY, ROW_BAD_TOKE
                    ROW_NAN, ROW_PHAT_BAD, ROW_RESID_ZERO, SV_SCHED_BATCH_GREEDY, SV_SCHED_PER_ROW, SvError)
 
 __all__ = ["sv_score", "sv_schedule", "sd_verify", "sd_verify_ragged", "workspace_bytes", "cluster_size", "Profile",
-           "Pipeline", "GraphPipeline", "sv_profile_build", "load_library"]
+           "Pipeline", "GraphPipeline", "sv_profile_build", "sv_score_filtered", "sd_verify_filtered", "load_library"]
 
 
 def load_library():
@@ -186,6 +186,52 @@ def sd_verify_ragged(D, T_rows, t_rowptr, tok, gamma, draft_m, draft_l, draft_pt
         _ptr(res["accept_ratio"]), _ptr(res["resid_mass"]), _ptr(res["status"]), workspace.data_ptr(),
         workspace.numel(), _stream(stream))
     _lib.check(st, "sd_verify_ragged")
+    return res
+
+
+def new_filter_workspace(B: int, k: int, device="cuda") -> torch.Tensor:
+    return torch.empty(max(16, int(_lib.load().sv_filter_workspace_bytes(B, k))), dtype=torch.uint8, device=device)
+
+
+def sv_score_filtered(D, C, tok, top_k=20, top_p=0.8, tau_d=1.0, tau_c=1.0, profile: Profile | None = None,
+                      fworkspace=None, stream=None) -> dict:
+    """Steps a1-a3 over the filtered distributions (NEXT-2; S L73-81, L238) through the C ABI
+    `sv_score_filtered`.  Keep `fworkspace` for `sd_verify_filtered` (it holds the draft lists)."""
+    B, k, V = D.shape
+    dev = D.device
+    fworkspace = fworkspace if fworkspace is not None else new_filter_workspace(B, k, dev)
+    res = {n: torch.empty((B, k), dtype=torch.float32, device=dev) for n in ("S", "A", "KL", "p_hat", "draft_ptok")}
+    res["status"] = torch.empty((B, k), dtype=torch.int32, device=dev)
+    if profile is None:
+        res["p_hat"] = None
+    f = _lib.SvFilter(int(top_k), float(top_p))
+    st = _lib.load().sv_score_filtered(
+        ctypes.byref(_logits(D)), ctypes.byref(_logits(C)), _ptr(tok), B, k, V, float(tau_d), float(tau_c),
+        ctypes.byref(f), ctypes.byref(profile.c) if profile is not None else None, _ptr(res["S"]), _ptr(res["A"]),
+        _ptr(res["KL"]), _ptr(res["p_hat"]), _ptr(res["draft_ptok"]), _ptr(res["status"]), fworkspace.data_ptr(),
+        fworkspace.numel(), _stream(stream))
+    _lib.check(st, "sv_score_filtered")
+    res["fworkspace"] = fworkspace
+    return res
+
+
+def sd_verify_filtered(T, tok, gamma, fworkspace, top_k=20, top_p=0.8, tau_t=1.0, seed=0, offset=0, seq_base=0,
+                       stream=None) -> dict:
+    """Steps a5-a6 over the filtered distributions (NEXT-2; S L183) through `sd_verify_filtered`."""
+    B, k1, V = T.shape
+    k = k1 - 1
+    dev = T.device
+    res = {"n_accept": torch.empty(B, dtype=torch.int32, device=dev),
+           "out_tok": torch.empty(B, dtype=torch.int32, device=dev),
+           "accept_ratio": torch.empty((B, k), dtype=torch.float32, device=dev),
+           "resid_mass": torch.empty(B, dtype=torch.float32, device=dev),
+           "status": torch.empty(B, dtype=torch.int32, device=dev)}
+    f = _lib.SvFilter(int(top_k), float(top_p))
+    st = _lib.load().sd_verify_filtered(
+        ctypes.byref(_logits(T)), _ptr(tok), _ptr(gamma), B, k, V, float(tau_t), ctypes.byref(f), ctypes.c_uint64(seed),
+        ctypes.c_uint64(offset), int(seq_base), _ptr(res["n_accept"]), _ptr(res["out_tok"]), _ptr(res["accept_ratio"]),
+        _ptr(res["resid_mass"]), _ptr(res["status"]), fworkspace.data_ptr(), fworkspace.numel(), _stream(stream))
+    _lib.check(st, "sd_verify_filtered")
     return res
 
 

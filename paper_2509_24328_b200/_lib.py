@@ -18,7 +18,8 @@ ROW_PHAT_BAD, ROW_RESID_ZERO, ROW_BAD_GAMMA, ROW_BAD_LATENCY = 16, 32, 64, 128
 EXPORTS = ("sv_workspace_bytes", "sv_status_string", "sv_cluster_size", "sv_score", "sv_schedule", "sd_verify",
            "sv_shard_xch_bytes", "sv_shard_score_p1", "sv_shard_score_p2", "sv_shard_score_finish",
            "sv_shard_verify_p1", "sv_shard_verify_p2", "sv_shard_verify_finish", "sd_verify_ragged",
-           "sv_profile_workspace_bytes", "sv_profile_build")
+           "sv_profile_workspace_bytes", "sv_profile_build", "sv_filter_workspace_bytes", "sv_score_filtered",
+           "sd_verify_filtered")
 
 
 class SvLogits(ctypes.Structure):
@@ -29,6 +30,10 @@ class SvLogits(ctypes.Structure):
 class SvProfile(ctypes.Structure):
     _fields_ = [("s_edges", ctypes.c_void_p), ("n_s", ctypes.c_int32), ("n_a", ctypes.c_int32),
                 ("a_edges", ctypes.c_void_p), ("cells", ctypes.c_void_p)]
+
+
+class SvFilter(ctypes.Structure):
+    _fields_ = [("top_k", ctypes.c_int32), ("top_p", ctypes.c_float)]
 
 
 class SvError(RuntimeError):
@@ -66,6 +71,14 @@ def load(path: str = LIB_PATH):
     lib.sd_verify_ragged.argtypes = [LP, P, i64, P, P, P, P, P, P, i32, i32, i32, f32, f32, u64, u64, P, i64,
                                      P, P, P, P, P, P, sz, P]
     lib.sd_verify_ragged.restype = i32
+    FP = ctypes.POINTER(SvFilter)
+    lib.sv_filter_workspace_bytes.argtypes = [i32, i32]
+    lib.sv_filter_workspace_bytes.restype = sz
+    lib.sv_score_filtered.argtypes = [LP, LP, P, i32, i32, i32, f32, f32, FP, ctypes.POINTER(SvProfile), P, P, P, P,
+                                      P, P, P, sz, P]
+    lib.sv_score_filtered.restype = i32
+    lib.sd_verify_filtered.argtypes = [LP, P, P, i32, i32, i32, f32, FP, u64, u64, i64, P, P, P, P, P, P, sz, P]
+    lib.sd_verify_filtered.restype = i32
     lib.sv_profile_workspace_bytes.argtypes = [i32, i32, i32, i32]
     lib.sv_profile_workspace_bytes.restype = sz
     lib.sv_profile_build.argtypes = [P, P, P, i32, i32, i32, i32, P, P, P, P, P, P, P, sz, P]

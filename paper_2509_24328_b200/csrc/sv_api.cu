@@ -381,6 +381,122 @@ int32_t sd_verify_ragged(const sv_logits *draft, const void *target, int64_t tar
   return SV_OK;
 }
 
+// ------------------------------------------------------------------ NEXT-2 sampling filters
+size_t sv_filter_workspace_bytes(int32_t B, int32_t k) {
+  if (B < 0 || k < 1 || k > SV_MAX_K) return 0;
+  return (size_t)(ws_round((int64_t)B * k * (int64_t)sizeof(FList)) * 2 +
+                  ws_round((int64_t)B * (k + 1) * (int64_t)sizeof(FList)));
+}
+
+static int32_t filter_check(const sv_filter *f) {
+  if (!f) return SV_ERR_INVALID_ARG;
+  if (f->top_k < 1 || f->top_k > 32) return SV_ERR_UNSUPPORTED;  // full-vocabulary top-p: not built
+  if (!(f->top_p > 0.f) || f->top_p > 1.f) return SV_ERR_INVALID_ARG;
+  return SV_OK;
+}
+
+static void filter_ws(FilterArgs &a, void *ws, int32_t B, int32_t k) {
+  uint8_t *w = reinterpret_cast<uint8_t *>(ws);
+  a.dl = reinterpret_cast<FList *>(w);
+  a.cl = reinterpret_cast<FList *>(w + ws_round((int64_t)B * k * (int64_t)sizeof(FList)));
+  a.tl = reinterpret_cast<FList *>(w + 2 * ws_round((int64_t)B * k * (int64_t)sizeof(FList)));
+}
+
+int32_t sv_score_filtered(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok, int32_t B, int32_t k,
+                          int32_t V, float tau_d, float tau_c, const sv_filter *filt, const sv_profile *prof, float *S,
+                          float *A, float *KL, float *p_hat, float *draft_ptok, int32_t *row_status, void *fworkspace,
+                          size_t fworkspace_bytes, void *stream) {
+  if (!draft) return SV_ERR_INVALID_ARG;
+  int32_t r = shape_check(B, k, V, draft->dtype);
+  if (r != SV_OK) return r;
+  if ((r = logits_check(draft, draft->dtype)) != SV_OK || (r = logits_check(comp, draft->dtype)) != SV_OK) return r;
+  if ((r = filter_check(filt)) != SV_OK) return r;
+  if (!draft_tok || !(tau_d > 0.f) || !(tau_c > 0.f)) return SV_ERR_INVALID_ARG;
+  if (p_hat && (!prof || !prof->s_edges || !prof->a_edges || !prof->cells || prof->n_s < 1 || prof->n_a < 1))
+    return SV_ERR_INVALID_ARG;
+  if (B == 0) return SV_OK;
+  if (!fworkspace || fworkspace_bytes < sv_filter_workspace_bytes(B, k)) return SV_ERR_WORKSPACE;
+  FilterArgs a = {};
+  a.d = draft->ptr;
+  a.c = comp->ptr;
+  a.d_sb = draft->stride_b;
+  a.d_si = draft->stride_i;
+  a.c_sb = comp->stride_b;
+  a.c_si = comp->stride_i;
+  a.tok = draft_tok;
+  a.B = B;
+  a.k = k;
+  a.V = V;
+  a.tau_d = tau_d;
+  a.tau_c = tau_c;
+  a.top_k = filt->top_k;
+  a.top_p = filt->top_p;
+  if (p_hat) {
+    a.s_edges = prof->s_edges;
+    a.a_edges = prof->a_edges;
+    a.cells = prof->cells;
+    a.n_s = prof->n_s;
+    a.n_a = prof->n_a;
+  }
+  a.S = S;
+  a.A = A;
+  a.KL = KL;
+  a.p_hat = p_hat;
+  a.dpt = draft_ptok;
+  a.status = row_status;
+  a.bf16 = draft->dtype == SV_BF16;
+  filter_ws(a, fworkspace, B, k);
+  const cudaError_t e = launch_filter_score(a, (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "libsv: sv_score_filtered launch failed: %s\n", cudaGetErrorString(e));
+    return SV_ERR_CUDA;
+  }
+  return SV_OK;
+}
+
+int32_t sd_verify_filtered(const sv_logits *target, const int32_t *draft_tok, const int32_t *gamma, int32_t B, int32_t k,
+                           int32_t V, float tau_t, const sv_filter *filt, uint64_t seed, uint64_t offset,
+                           int64_t seq_base, int32_t *n_accept, int32_t *out_tok, float *accept_ratio,
+                           float *resid_mass, int32_t *row_status, void *fworkspace, size_t fworkspace_bytes,
+                           void *stream) {
+  if (!target) return SV_ERR_INVALID_ARG;
+  int32_t r = shape_check(B, k, V, target->dtype);
+  if (r != SV_OK) return r;
+  if ((r = logits_check(target, target->dtype)) != SV_OK) return r;
+  if ((r = filter_check(filt)) != SV_OK) return r;
+  if (!draft_tok || !gamma || !n_accept || !out_tok || !(tau_t > 0.f) || seq_base < 0) return SV_ERR_INVALID_ARG;
+  if (B == 0) return SV_OK;
+  if (!fworkspace || fworkspace_bytes < sv_filter_workspace_bytes(B, k)) return SV_ERR_WORKSPACE;
+  FilterArgs a = {};
+  a.t = target->ptr;
+  a.t_sb = target->stride_b;
+  a.t_si = target->stride_i;
+  a.tok = draft_tok;
+  a.gamma = gamma;
+  a.B = B;
+  a.k = k;
+  a.V = V;
+  a.tau_t = tau_t;
+  a.top_k = filt->top_k;
+  a.top_p = filt->top_p;
+  a.seed = seed;
+  a.offset = offset;
+  a.seq_base = seq_base;
+  a.n_accept = n_accept;
+  a.out_tok = out_tok;
+  a.ratio = accept_ratio;
+  a.resid = resid_mass;
+  a.status = row_status;
+  a.bf16 = target->dtype == SV_BF16;
+  filter_ws(a, fworkspace, B, k);
+  const cudaError_t e = launch_filter_verify(a, (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "libsv: sd_verify_filtered launch failed: %s\n", cudaGetErrorString(e));
+    return SV_ERR_CUDA;
+  }
+  return SV_OK;
+}
+
 // ------------------------------------------------------------------ NEXT-4 profile builder
 static int64_t prof_ws_layout(int32_t N, int32_t ns, int32_t na, int32_t xb, int64_t off[5]) {
   off[0] = 0;                                              // s_sorted

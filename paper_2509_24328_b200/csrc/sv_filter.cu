@@ -1,0 +1,414 @@
+// sv_filter.cu -- NEXT-2: the SV path under the paper's sampling filters (P L731-743 Table 5:
+// top_k 20 / top_p 0.8 / tau 0.7 for Qwen), applied to draft, companion and target alike before
+// S / A and the accept test (S L73-81, L183, L238; DESIGN R21).  With top_k <= 32 every filtered
+// distribution has at most 32 support entries, so after one selection pass per row the rest of
+// the path runs on tiny lists:
+//
+//   KF1 sv_topk_kernel  one CTA per row: radix select of the top_k-th largest logit on the
+//                       order-preserving key of the raw bits (bf16: 2 passes of 8 bits, fp32: 4),
+//                       256-bin shared-memory histograms over the row (the first pass streams
+//                       it from HBM, the rest hit L2), then one collection pass: keys above the
+//                       threshold in any order, keys equal to it in VOCABULARY order until
+//                       top_k entries are held (ties to the lower index, R21); the list is
+//                       sorted by (logit desc, index asc), softmaxed in fp64 over the kept
+//                       entries, cut by top_p (sequential fp64 cumulative >= top_p) and
+//                       renormalised -> FList {n, idx[32], p[32]}.
+//   KF2 sv_fscore_kernel one warp per (b, i): S = sum min(p'_d, p'_c) over the draft list,
+//                       A = min(1, p'_c(t)/p'_d(t)), KL(p'_d || p'_c), profile lookup.
+//   KF3 sv_fverify_kernel one warp per sequence: p'_t(t_i)/p'_d(t_i), Philox u_i, N_b, then
+//                       the residual max(0, p'_t - p'_d) (or the bonus p'_t) over the <= 32
+//                       entries sorted by vocabulary index, sequential fp64 Z and inverse CDF.
+#include <float.h>
+
+#include "sv_device.cuh"
+#include "sv_internal.h"
+
+namespace sv {
+
+namespace {
+
+constexpr int kTopKThreads = 512;
+constexpr int kTieCap = 2048;  // tie indices held for the ordered pick (power of two)
+
+template <typename T> struct KeyOf;
+template <> struct KeyOf<__nv_bfloat16> {
+  using K = uint32_t;
+  static constexpr int kBits = 16;
+  __device__ static K key(const __nv_bfloat16 *p, int64_t e) {
+    const uint32_t b = *reinterpret_cast<const uint16_t *>(p + e);
+    return (b & 0x8000u) ? (~b & 0xFFFFu) : (b | 0x8000u);
+  }
+  __device__ static bool bad(K k) { return k >= 0xFF80u; }  // +inf or NaN (R18)
+  __device__ static float value(K k) {
+    const uint32_t b = (k & 0x8000u) ? (k & 0x7FFFu) : (~k & 0xFFFFu);
+    return __uint_as_float(b << 16);
+  }
+};
+template <> struct KeyOf<float> {
+  using K = uint32_t;
+  static constexpr int kBits = 32;
+  __device__ static K key(const float *p, int64_t e) {
+    const uint32_t b = __float_as_uint(p[e]);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+  }
+  __device__ static bool bad(K k) { return k >= 0xFF800000u; }
+  __device__ static float value(K k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+  }
+};
+
+// Row r of the set the launch processes (draft / companion rows for the score, target rows
+// 0..gamma_b for the verify); returns false for rows that are skipped.
+__device__ __forceinline__ bool row_of(const FilterArgs &a, int64_t r, int which, const void *&base, int64_t &off,
+                                       FList *&out) {
+  if (which == 2) {  // target rows (b, i <= gamma_b)
+    const int64_t b = r / (a.k + 1), i = r % (a.k + 1);
+    const int g = a.gamma[b];
+    if (g < 0 || g > a.k || i > g) return false;
+    base = a.t;
+    off = b * a.t_sb + i * a.t_si;
+    out = a.tl + r;
+    return true;
+  }
+  const int64_t b = r / a.k, i = r % a.k;
+  base = which == 0 ? a.d : a.c;
+  off = which == 0 ? b * a.d_sb + i * a.d_si : b * a.c_sb + i * a.c_si;
+  out = (which == 0 ? a.dl : a.cl) + r;
+  return true;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_constant__ FilterArgs a, int which) {
+  using KO = KeyOf<T>;
+  using K = typename KO::K;
+  constexpr int NT = kTopKThreads;
+  __shared__ uint32_t hist[256];
+  __shared__ K s_prefix, s_mask;
+  __shared__ int s_remaining, s_bad, s_ngt, s_ntie;
+  __shared__ int s_tie[kTieCap];
+  __shared__ K c_key[32];
+  __shared__ int c_idx[32];
+  pdl_wait();
+  pdl_trigger();
+  const void *base;
+  int64_t off;
+  FList *out;
+  if (!row_of(a, blockIdx.x, which, base, off, out)) return;
+  const T *x = reinterpret_cast<const T *>(base) + off;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int V = a.V, KK = min(a.top_k, V);
+  if (tid == 0) {
+    s_prefix = 0;
+    s_mask = 0;
+    s_remaining = KK;
+    s_bad = 0;
+    s_ngt = 0;
+    s_ntie = 0;
+  }
+  // ---- radix select of the KK-th largest key, 8 bits per pass from the top
+  for (int shift = KO::kBits - 8; shift >= 0; shift -= 8) {
+    for (int j = tid; j < 256; j += NT) hist[j] = 0u;
+    __syncthreads();
+    const K prefix = s_prefix, mask = s_mask;
+    int bad = 0;
+    for (int e = tid; e < V; e += NT) {
+      const K kk = KO::key(x, e);
+      bad |= KO::bad(kk);
+      if ((kk & mask) == prefix) atomicAdd(&hist[(kk >> shift) & 255u], 1u);
+    }
+    if (shift == KO::kBits - 8 && __any_sync(0xffffffffu, bad) && lane == 0) s_bad = 1;
+    __syncthreads();
+    if (tid == 0) {
+      int rem = s_remaining, cum = 0, d = 255;
+      for (; d > 0; --d) {
+        if (cum + (int)hist[d] >= rem) break;
+        cum += (int)hist[d];
+      }
+      s_remaining = rem - cum;  // still to take inside digit d
+      s_prefix = prefix | ((K)d << shift);
+      s_mask = mask | ((K)255u << shift);
+    }
+    __syncthreads();
+  }
+  const K theta = s_prefix;
+  const int need = s_remaining;  // entries equal to theta to take, lowest indices first
+  // ---- collection: keys > theta (< top_k of them, any order) and the indices of keys ==
+  // theta (up to kTieCap, any order); the `need` lowest tie indices are then taken in order
+  for (int e = tid; e < V; e += NT) {
+    const K kk = KO::key(x, e);
+    if (kk > theta) {
+      const int slot = atomicAdd(&s_ngt, 1);
+      c_key[slot] = kk;
+      c_idx[slot] = e;
+    } else if (kk == theta) {
+      const int slot = atomicAdd(&s_ntie, 1);
+      if (slot < kTieCap) s_tie[slot] = e;
+    }
+  }
+  __syncthreads();
+  const int ntie = s_ntie;
+  if (ntie <= kTieCap) {  // bitonic sort of the tie indices (padded with INT32_MAX)
+    int np2 = 1;
+    while (np2 < ntie) np2 <<= 1;
+    for (int j = ntie + tid; j < np2; j += NT) s_tie[j] = INT32_MAX;
+    __syncthreads();
+    for (int size = 2; size <= np2; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int j = tid; j < np2; j += NT) {
+          const int o = j ^ stride;
+          if (o > j) {
+            const bool up = (j & size) == 0;
+            const int u = s_tie[j], v = s_tie[o];
+            if ((u > v) == up) {
+              s_tie[j] = v;
+              s_tie[o] = u;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    if (tid < need) {
+      c_key[KK - need + tid] = theta;
+      c_idx[KK - need + tid] = s_tie[tid];
+    }
+  } else {  // pathological tie counts: one ordered pass (warp 0, vocabulary order)
+    if (wid == 0) {
+      int taken = 0;
+      for (int e0 = 0; e0 < V && taken < need; e0 += 32) {
+        const int e = e0 + lane;
+        const bool eq = e < V && KO::key(x, e) == theta;
+        const unsigned m = __ballot_sync(0xffffffffu, eq);
+        const int rank = taken + __popc(m & ((1u << lane) - 1u));
+        if (eq && rank < need) {
+          c_key[KK - need + rank] = theta;
+          c_idx[KK - need + rank] = e;
+        }
+        taken += __popc(m);
+      }
+    }
+  }
+  __syncthreads();
+  if (wid != 0) return;
+  // ---- sort by (key desc, index asc), softmax (fp64), top_p, renormalise
+  const K mk = lane < KK ? c_key[lane] : (K)0;
+  const int mi = lane < KK ? c_idx[lane] : INT32_MAX;
+  int rank = 0;
+  for (int l = 0; l < KK; ++l) {
+    const K ok = __shfl_sync(0xffffffffu, mk, l);
+    const int oi = __shfl_sync(0xffffffffu, mi, l);
+    rank += (ok > mk) || (ok == mk && oi < mi);
+  }
+  __syncwarp();
+  if (lane < KK) {
+    c_key[rank] = mk;
+    c_idx[rank] = mi;
+  }
+  __syncwarp();
+  const double tau = (double)(which == 0 ? a.tau_d : which == 1 ? a.tau_c : a.tau_t);
+  const double y = lane < KK ? (double)KO::value(c_key[lane]) / tau : -INFINITY;
+  const double y0 = __shfl_sync(0xffffffffu, y, 0);
+  int st = s_bad ? 1 /*SV_ROW_NAN*/ : 0;
+  if (!st && !(y0 > -INFINITY)) st = 2; /*SV_ROW_ALL_NEG_INF*/
+  double p = (lane < KK && !st) ? exp(y - y0) : 0.0;
+  double tot = 0.0;  // sequential in sorted order (the oracle's order)
+  for (int l = 0; l < KK; ++l) tot += __shfl_sync(0xffffffffu, p, l);
+  p = p / tot;
+  int n = KK;
+  if (a.top_p < 1.f) {
+    double c = 0.0;
+    for (int l = 0; l < KK; ++l) {
+      c += __shfl_sync(0xffffffffu, p, l);
+      if (c >= (double)a.top_p) {
+        n = l + 1;
+        break;
+      }
+    }
+    double s = 0.0;
+    for (int l = 0; l < n; ++l) s += __shfl_sync(0xffffffffu, p, l);
+    p = p / s;
+  }
+  if (st) n = 0;
+  if (lane < n) {
+    out->idx[lane] = c_idx[lane];
+    out->p[lane] = p;
+  }
+  if (lane == 0) {
+    out->n = n;
+    out->st = st;
+  }
+}
+
+// p of vocabulary index v in a list (0 when absent); every lane returns the same value
+__device__ __forceinline__ double list_p(const FList *L, int n, int v) {
+  const int lane = threadIdx.x & 31;
+  const bool hit = lane < n && L->idx[lane] == v;
+  const unsigned m = __ballot_sync(0xffffffffu, hit);
+  const double mine = hit ? L->p[lane] : 0.0;
+  return m ? __shfl_sync(0xffffffffu, mine, __ffs(m) - 1) : 0.0;
+}
+
+__global__ void __launch_bounds__(256) sv_fscore_kernel(const __grid_constant__ FilterArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r >= (int64_t)a.B * a.k) return;
+  const FList *Ld = a.dl + r, *Lc = a.cl + r;
+  const int nd = Ld->n, nc = Lc->n;
+  int st = Ld->st | Lc->st;
+  const int t = a.tok[r];
+  if (t < 0 || t >= a.V) st |= 4; /*SV_ROW_BAD_TOKEN*/
+  // S over the draft list (sorted order, sequential fp64), KL, p(t)
+  const int vd = lane < nd ? Ld->idx[lane] : -1;
+  const double pd = lane < nd ? Ld->p[lane] : 0.0;
+  double pcv = 0.0;
+  for (int l = 0; l < nc; ++l) {  // companion p at this lane's draft index
+    const int ci = Lc->idx[l];
+    if (ci == vd) pcv = Lc->p[l];
+  }
+  const double mn = fmin(pd, pcv);
+  const double klt = pd > 0.0 ? (pcv > 0.0 ? pd * log(pd / pcv) : INFINITY) : 0.0;
+  double S = 0.0, KL = 0.0;
+  for (int l = 0; l < nd; ++l) {
+    S += __shfl_sync(0xffffffffu, mn, l);
+    KL += __shfl_sync(0xffffffffu, klt, l);
+  }
+  const double pdt = (st & 4) ? 0.0 : list_p(Ld, nd, t), pct = (st & 4) ? 0.0 : list_p(Lc, nc, t);
+  if (!st && pdt == 0.0) st |= 8; /*SV_ROW_DRAFT_ZERO*/
+  const double A = st ? 0.0 : fmin(1.0, pct / pdt);
+  float phat = 0.f;
+  if (!st && a.p_hat) {  // bin = number of interior edges strictly below the value (R9)
+    const float Sf = (float)S, Af = (float)A;
+    int si = 0, ai = 0;
+    for (int j = 1; j < a.n_s; ++j) si += a.s_edges[j] < Sf;
+    for (int j = 1; j < a.n_a; ++j) ai += a.a_edges[j] < Af;
+    phat = a.cells[si * a.n_a + ai];
+  }
+  if (lane == 0) {
+    const float nanf_ = __int_as_float(0x7fc00000);
+    if (a.S) a.S[r] = st ? nanf_ : (float)S;
+    if (a.A) a.A[r] = st ? nanf_ : (float)A;
+    if (a.KL) a.KL[r] = st ? nanf_ : (float)KL;
+    if (a.p_hat) a.p_hat[r] = phat;
+    if (a.dpt) a.dpt[r] = (st & ~8) ? nanf_ : (float)pdt;
+    if (a.status) a.status[r] = st;
+  }
+}
+
+__global__ void __launch_bounds__(256) sv_fverify_kernel(const __grid_constant__ FilterArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  const int lane = threadIdx.x & 31, k = a.k;
+  const int64_t b = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (b >= a.B) return;
+  const int g = a.gamma[b];
+  int st = (g < 0 || g > k) ? 64 /*BAD_GAMMA*/ : 0;
+  const int gg = st ? -1 : g;
+  const uint64_t off = a.offset;
+  // accept tests: one draft position per iteration (all lanes), ratios kept in lane i
+  double ratio_mine = 0.0;
+  int N = st ? 0 : gg;
+  for (int i = 0; i < gg; ++i) {
+    const int64_t rd = b * k + i, rt = b * (k + 1) + i;
+    const int t = a.tok[rd];
+    int rst = a.dl[rd].st | a.tl[rt].st;
+    if (t < 0 || t >= a.V) rst |= 4;
+    const double pdt = (rst & 4) ? 0.0 : list_p(a.dl + rd, a.dl[rd].n, t);
+    const double ptt = (rst & 4) ? 0.0 : list_p(a.tl + rt, a.tl[rt].n, t);
+    if (!rst && pdt == 0.0) rst |= 8;
+    if (rst) {
+      st |= rst;
+      break;
+    }
+    const double ratio = ptt / pdt;
+    if (lane == i) ratio_mine = ratio;
+    const uint4 w = sv_philox(a.seed, off, a.seq_base + b, i);
+    if (!(u24(w.x) < ratio)) {
+      N = i;
+      break;
+    }
+  }
+  if (a.ratio && lane < k) a.ratio[b * k + lane] = (!st && lane < N + (N < gg ? 1 : 0)) ? (float)fmin(1.0, ratio_mine)
+                                                                                          : __int_as_float(0x7fc00000);
+  if (st) {
+    if (lane == 0) {
+      a.n_accept[b] = 0;
+      a.out_tok[b] = -1;
+      if (a.resid) a.resid[b] = __int_as_float(0x7fc00000);
+      if (a.status) a.status[b] = st;
+    }
+    return;
+  }
+  // residual (N < gamma) or bonus (N == gamma) over the target list of row N
+  const int64_t rt = b * (k + 1) + N;
+  const FList *Lt = a.tl + rt;
+  const int nt = Lt->n;
+  if (Lt->st) st |= Lt->st;
+  const int vi = lane < nt ? Lt->idx[lane] : INT32_MAX;
+  double r = lane < nt ? Lt->p[lane] : 0.0;
+  if (N < gg) {
+    const FList *Ld = a.dl + b * k + N;
+    double pdv = 0.0;
+    for (int l = 0; l < Ld->n; ++l)
+      if (Ld->idx[l] == vi) pdv = Ld->p[l];
+    r = fmax(0.0, r - pdv);
+  }
+  // entries in vocabulary order (rank by index), then sequential Z and inverse CDF (R11)
+  int rank = 0;
+  for (int l = 0; l < nt; ++l) rank += __shfl_sync(0xffffffffu, vi, l) < vi;
+  __shared__ double s_r[8][32];
+  __shared__ int s_v[8][32];
+  const int w8 = threadIdx.x >> 5;
+  if (lane < nt) {
+    s_r[w8][rank] = r;
+    s_v[w8][rank] = vi;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    double Z = 0.0;
+    for (int l = 0; l < nt; ++l) Z += s_r[w8][l];
+    if (!(Z > 0.0)) st |= 32; /*SV_ROW_RESID_ZERO*/
+    const double us = u24(sv_philox(a.seed, off, a.seq_base + b, N).y);
+    const double th = us * Z;
+    double cum = 0.0;
+    int tok = -1, lastp = -1;
+    for (int l = 0; l < nt; ++l) {
+      if (!(s_r[w8][l] > 0.0)) continue;
+      lastp = s_v[w8][l];
+      cum += s_r[w8][l];
+      if (cum > th) {
+        tok = s_v[w8][l];
+        break;
+      }
+    }
+    if (tok < 0) tok = lastp;
+    a.n_accept[b] = N;
+    a.out_tok[b] = tok;
+    if (a.resid) a.resid[b] = (float)Z;
+    if (a.status) a.status[b] = st;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_filter_score(const FilterArgs &a, cudaStream_t st) {
+  const unsigned rows = (unsigned)((int64_t)a.B * a.k);
+  cudaError_t e;
+  for (int which = 0; which < 2; ++which) {
+    e = a.bf16 ? launch_k(sv_topk_kernel<__nv_bfloat16>, dim3(rows), dim3(kTopKThreads), 0, st, a, which)
+               : launch_k(sv_topk_kernel<float>, dim3(rows), dim3(kTopKThreads), 0, st, a, which);
+    if (e != cudaSuccess) return e;
+  }
+  return launch_k(sv_fscore_kernel, dim3((rows + 7) / 8), dim3(256), 0, st, a);
+}
+
+cudaError_t launch_filter_verify(const FilterArgs &a, cudaStream_t st) {
+  const unsigned rows = (unsigned)((int64_t)a.B * (a.k + 1));
+  cudaError_t e = a.bf16 ? launch_k(sv_topk_kernel<__nv_bfloat16>, dim3(rows), dim3(kTopKThreads), 0, st, a, 2)
+                         : launch_k(sv_topk_kernel<float>, dim3(rows), dim3(kTopKThreads), 0, st, a, 2);
+  if (e != cudaSuccess) return e;
+  return launch_k(sv_fverify_kernel, dim3((unsigned)((a.B + 7) / 8)), dim3(256), 0, st, a);
+}
+
+}  // namespace sv

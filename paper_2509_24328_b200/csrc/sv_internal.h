@@ -150,6 +150,34 @@ struct VerifyArgs {
 int64_t verify_ws_bytes(int64_t B, int k, int64_t splits, int nsl);
 cudaError_t launch_verify(const VerifyArgs &a, cudaStream_t st);
 
+// NEXT-2: sampling filters (sv_filter.cu).  A filtered distribution: at most 32 entries.
+struct FList {
+  int32_t n, st;     // kept entries, row status bits
+  int32_t idx[32];   // vocabulary indices, sorted by (probability desc, index asc)
+  double p[32];      // renormalised filtered probabilities
+};
+struct FilterArgs {
+  const void *d, *c, *t;
+  int64_t d_sb, d_si, c_sb, c_si, t_sb, t_si;
+  const int32_t *tok, *gamma;
+  int32_t B, k, V;
+  float tau_d, tau_c, tau_t;
+  int32_t top_k;
+  float top_p;
+  FList *dl, *cl, *tl;  // workspace lists: draft [B k], companion [B k], target [B (k+1)]
+  const float *s_edges, *a_edges, *cells;
+  int32_t n_s, n_a;
+  float *S, *A, *KL, *p_hat, *dpt;
+  int32_t *status;
+  uint64_t seed, offset;
+  int64_t seq_base;
+  int32_t *n_accept, *out_tok;
+  float *ratio, *resid;
+  int bf16;
+};
+cudaError_t launch_filter_score(const FilterArgs &a, cudaStream_t st);
+cudaError_t launch_filter_verify(const FilterArgs &a, cudaStream_t st);
+
 // NEXT-4: offline profile builder (sv_profile.cu)
 constexpr int kProfMaxBins = 64;
 struct ProfileArgs {
