@@ -28,7 +28,28 @@ namespace sv {
 namespace {
 
 constexpr int kTopKThreads = 512;
-constexpr int kTieCap = 2048;  // tie indices held for the ordered pick (power of two)
+constexpr int kTieCap = 2048;   // tie indices held for the ordered pick (power of two)
+constexpr int kCandCap = 4096;  // fast-path candidates (power of two, >= kTopKThreads)
+
+// in-place bitonic sort, descending, of n (a power of two <= kCandCap) 64-bit keys; all threads
+__device__ __forceinline__ void bitonic_desc(unsigned long long *v, int n) {
+  for (int size = 2; size <= n; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        const int o = j ^ stride;
+        if (o > j) {
+          const bool desc = (j & size) == 0;
+          const unsigned long long a = v[j], b = v[o];
+          if ((a < b) == desc) {
+            v[j] = b;
+            v[o] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
 
 template <typename T> struct KeyOf;
 template <> struct KeyOf<__nv_bfloat16> {
@@ -78,7 +99,8 @@ __device__ __forceinline__ bool row_of(const FilterArgs &a, int64_t r, int which
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_constant__ FilterArgs a, int which) {
+__global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_constant__ FilterArgs a, int which0) {
+  const int which = which0 + (int)blockIdx.y;  // score: y = 0 draft rows, y = 1 companion rows
   using KO = KeyOf<T>;
   using K = typename KO::K;
   constexpr int NT = kTopKThreads;
@@ -86,6 +108,8 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
   __shared__ K s_prefix, s_mask;
   __shared__ int s_remaining, s_bad, s_ngt, s_ntie;
   __shared__ int s_tie[kTieCap];
+  __shared__ unsigned long long s_cand[kCandCap];
+  __shared__ int s_ncand;
   __shared__ K c_key[32];
   __shared__ int c_idx[32];
   pdl_wait();
@@ -105,90 +129,163 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
     s_ngt = 0;
     s_ntie = 0;
   }
-  // ---- radix select of the KK-th largest key, 8 bits per pass from the top
-  for (int shift = KO::kBits - 8; shift >= 0; shift -= 8) {
-    for (int j = tid; j < 256; j += NT) hist[j] = 0u;
-    __syncthreads();
-    const K prefix = s_prefix, mask = s_mask;
+  bool fast = false;
+  // ---- fast path: the KK-th largest of the 512 thread maxima is a lower bound of the KK-th
+  // largest key, so every top-KK element has key >= that bound; gather those few candidates
+  // (second pass, an L2 hit) and sort them by (key desc, index asc).  Falls back to the radix
+  // select when the candidates overflow kCandCap.
+  {
+    constexpr int EPU = 16 / sizeof(T);
+    const bool vec = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    const int units = vec ? V / EPU : 0;
+    K tmax = 0;
     int bad = 0;
+    for (int u = tid; u < units; u += NT) {
+      const uint4 w = ldg_stream(x + (size_t)u * EPU);
+      const T *e = reinterpret_cast<const T *>(&w);
+#pragma unroll
+      for (int j = 0; j < EPU; ++j) {
+        const K kk = KO::key(e, j);
+        tmax = kk > tmax ? kk : tmax;
+        bad |= KO::bad(kk);
+      }
+    }
+    for (int e = units * EPU + tid; e < V; e += NT) {
+      const K kk = KO::key(x, e);
+      tmax = kk > tmax ? kk : tmax;
+      bad |= KO::bad(kk);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) s_bad = 1;
+    __syncthreads();
+    s_cand[tid] = (unsigned long long)tmax << 32;  // thread maxima, sorted descending
+    __syncthreads();
+    bitonic_desc(s_cand, NT);
+    const K lb = (K)(s_cand[KK - 1] >> 32);
+    __syncthreads();
+    if (tid == 0) s_ncand = 0;
+    __syncthreads();
+    for (int u = tid; u < units; u += NT) {
+      const uint4 w = ldg_stream(x + (size_t)u * EPU);
+      const T *e = reinterpret_cast<const T *>(&w);
+#pragma unroll
+      for (int j = 0; j < EPU; ++j) {
+        const K kk = KO::key(e, j);
+        if (kk >= lb) {
+          const int slot = atomicAdd(&s_ncand, 1);
+          if (slot < kCandCap)
+            s_cand[slot] = ((unsigned long long)kk << 32) | (0xFFFFFFFFu - (uint32_t)(u * EPU + j));
+        }
+      }
+    }
+    for (int e = units * EPU + tid; e < V; e += NT) {
+      const K kk = KO::key(x, e);
+      if (kk >= lb) {
+        const int slot = atomicAdd(&s_ncand, 1);
+        if (slot < kCandCap) s_cand[slot] = ((unsigned long long)kk << 32) | (0xFFFFFFFFu - (uint32_t)e);
+      }
+    }
+    __syncthreads();
+    const int nc = s_ncand;
+    if (nc <= kCandCap) {  // (key desc, index asc) == composite desc
+      int np2 = 1;
+      while (np2 < nc) np2 <<= 1;
+      for (int j = nc + tid; j < np2; j += NT) s_cand[j] = 0ull;
+      __syncthreads();
+      bitonic_desc(s_cand, np2);
+      if (tid < KK) {
+        c_key[tid] = (K)(s_cand[tid] >> 32);
+        c_idx[tid] = (int)(0xFFFFFFFFu - (uint32_t)s_cand[tid]);
+      }
+      fast = true;
+    }
+    __syncthreads();
+  }
+  if (!fast) {
+    // ---- radix select of the KK-th largest key, 8 bits per pass from the top
+    for (int shift = KO::kBits - 8; shift >= 0; shift -= 8) {
+      for (int j = tid; j < 256; j += NT) hist[j] = 0u;
+      __syncthreads();
+      const K prefix = s_prefix, mask = s_mask;
+      int bad = 0;
+      for (int e = tid; e < V; e += NT) {
+        const K kk = KO::key(x, e);
+        bad |= KO::bad(kk);
+        if ((kk & mask) == prefix) atomicAdd(&hist[(kk >> shift) & 255u], 1u);
+      }
+      if (shift == KO::kBits - 8 && __any_sync(0xffffffffu, bad) && lane == 0) s_bad = 1;
+      __syncthreads();
+      if (tid == 0) {
+        int rem = s_remaining, cum = 0, d = 255;
+        for (; d > 0; --d) {
+          if (cum + (int)hist[d] >= rem) break;
+          cum += (int)hist[d];
+        }
+        s_remaining = rem - cum;  // still to take inside digit d
+        s_prefix = prefix | ((K)d << shift);
+        s_mask = mask | ((K)255u << shift);
+      }
+      __syncthreads();
+    }
+    const K theta = s_prefix;
+    const int need = s_remaining;  // entries equal to theta to take, lowest indices first
+    // ---- collection: keys > theta (< top_k of them, any order) and the indices of keys ==
+    // theta (up to kTieCap, any order); the `need` lowest tie indices are then taken in order
     for (int e = tid; e < V; e += NT) {
       const K kk = KO::key(x, e);
-      bad |= KO::bad(kk);
-      if ((kk & mask) == prefix) atomicAdd(&hist[(kk >> shift) & 255u], 1u);
-    }
-    if (shift == KO::kBits - 8 && __any_sync(0xffffffffu, bad) && lane == 0) s_bad = 1;
-    __syncthreads();
-    if (tid == 0) {
-      int rem = s_remaining, cum = 0, d = 255;
-      for (; d > 0; --d) {
-        if (cum + (int)hist[d] >= rem) break;
-        cum += (int)hist[d];
+      if (kk > theta) {
+        const int slot = atomicAdd(&s_ngt, 1);
+        c_key[slot] = kk;
+        c_idx[slot] = e;
+      } else if (kk == theta) {
+        const int slot = atomicAdd(&s_ntie, 1);
+        if (slot < kTieCap) s_tie[slot] = e;
       }
-      s_remaining = rem - cum;  // still to take inside digit d
-      s_prefix = prefix | ((K)d << shift);
-      s_mask = mask | ((K)255u << shift);
     }
     __syncthreads();
-  }
-  const K theta = s_prefix;
-  const int need = s_remaining;  // entries equal to theta to take, lowest indices first
-  // ---- collection: keys > theta (< top_k of them, any order) and the indices of keys ==
-  // theta (up to kTieCap, any order); the `need` lowest tie indices are then taken in order
-  for (int e = tid; e < V; e += NT) {
-    const K kk = KO::key(x, e);
-    if (kk > theta) {
-      const int slot = atomicAdd(&s_ngt, 1);
-      c_key[slot] = kk;
-      c_idx[slot] = e;
-    } else if (kk == theta) {
-      const int slot = atomicAdd(&s_ntie, 1);
-      if (slot < kTieCap) s_tie[slot] = e;
-    }
-  }
-  __syncthreads();
-  const int ntie = s_ntie;
-  if (ntie <= kTieCap) {  // bitonic sort of the tie indices (padded with INT32_MAX)
-    int np2 = 1;
-    while (np2 < ntie) np2 <<= 1;
-    for (int j = ntie + tid; j < np2; j += NT) s_tie[j] = INT32_MAX;
-    __syncthreads();
-    for (int size = 2; size <= np2; size <<= 1) {
-      for (int stride = size >> 1; stride > 0; stride >>= 1) {
-        for (int j = tid; j < np2; j += NT) {
-          const int o = j ^ stride;
-          if (o > j) {
-            const bool up = (j & size) == 0;
-            const int u = s_tie[j], v = s_tie[o];
-            if ((u > v) == up) {
-              s_tie[j] = v;
-              s_tie[o] = u;
+    const int ntie = s_ntie;
+    if (ntie <= kTieCap) {  // bitonic sort of the tie indices (padded with INT32_MAX)
+      int np2 = 1;
+      while (np2 < ntie) np2 <<= 1;
+      for (int j = ntie + tid; j < np2; j += NT) s_tie[j] = INT32_MAX;
+      __syncthreads();
+      for (int size = 2; size <= np2; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+          for (int j = tid; j < np2; j += NT) {
+            const int o = j ^ stride;
+            if (o > j) {
+              const bool up = (j & size) == 0;
+              const int u = s_tie[j], v = s_tie[o];
+              if ((u > v) == up) {
+                s_tie[j] = v;
+                s_tie[o] = u;
+              }
             }
           }
+          __syncthreads();
         }
-        __syncthreads();
+      }
+      if (tid < need) {
+        c_key[KK - need + tid] = theta;
+        c_idx[KK - need + tid] = s_tie[tid];
+      }
+    } else {  // pathological tie counts: one ordered pass (warp 0, vocabulary order)
+      if (wid == 0) {
+        int taken = 0;
+        for (int e0 = 0; e0 < V && taken < need; e0 += 32) {
+          const int e = e0 + lane;
+          const bool eq = e < V && KO::key(x, e) == theta;
+          const unsigned m = __ballot_sync(0xffffffffu, eq);
+          const int rank = taken + __popc(m & ((1u << lane) - 1u));
+          if (eq && rank < need) {
+            c_key[KK - need + rank] = theta;
+            c_idx[KK - need + rank] = e;
+          }
+          taken += __popc(m);
+        }
       }
     }
-    if (tid < need) {
-      c_key[KK - need + tid] = theta;
-      c_idx[KK - need + tid] = s_tie[tid];
-    }
-  } else {  // pathological tie counts: one ordered pass (warp 0, vocabulary order)
-    if (wid == 0) {
-      int taken = 0;
-      for (int e0 = 0; e0 < V && taken < need; e0 += 32) {
-        const int e = e0 + lane;
-        const bool eq = e < V && KO::key(x, e) == theta;
-        const unsigned m = __ballot_sync(0xffffffffu, eq);
-        const int rank = taken + __popc(m & ((1u << lane) - 1u));
-        if (eq && rank < need) {
-          c_key[KK - need + rank] = theta;
-          c_idx[KK - need + rank] = e;
-        }
-        taken += __popc(m);
-      }
-    }
+    __syncthreads();
   }
-  __syncthreads();
   if (wid != 0) return;
   // ---- sort by (key desc, index asc), softmax (fp64), top_p, renormalise
   const K mk = lane < KK ? c_key[lane] : (K)0;
@@ -394,12 +491,9 @@ __global__ void __launch_bounds__(256) sv_fverify_kernel(const __grid_constant__
 
 cudaError_t launch_filter_score(const FilterArgs &a, cudaStream_t st) {
   const unsigned rows = (unsigned)((int64_t)a.B * a.k);
-  cudaError_t e;
-  for (int which = 0; which < 2; ++which) {
-    e = a.bf16 ? launch_k(sv_topk_kernel<__nv_bfloat16>, dim3(rows), dim3(kTopKThreads), 0, st, a, which)
-               : launch_k(sv_topk_kernel<float>, dim3(rows), dim3(kTopKThreads), 0, st, a, which);
-    if (e != cudaSuccess) return e;
-  }
+  const cudaError_t e = a.bf16 ? launch_k(sv_topk_kernel<__nv_bfloat16>, dim3(rows, 2), dim3(kTopKThreads), 0, st, a, 0)
+                               : launch_k(sv_topk_kernel<float>, dim3(rows, 2), dim3(kTopKThreads), 0, st, a, 0);
+  if (e != cudaSuccess) return e;
   return launch_k(sv_fscore_kernel, dim3((rows + 7) / 8), dim3(256), 0, st, a);
 }
 
