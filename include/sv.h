@@ -122,7 +122,7 @@ SV_API int32_t sv_cluster_size(int32_t V, int32_t dtype);
  * draft_ptok = p_d(t).  draft_m / draft_l / draft_ptok feed sd_verify.
  * row_status [B, k] int32 or NULL.  Bad rows: S = A = KL = NaN, p_hat = 0.
  * S, A, KL, p_hat may be NULL individually (not computed-out); draft_* may not.
- * Limits: 1 <= k <= 16, 2 <= V < 2^31, 2 * B * k * ceil(V / 32768) < 2^31 (one CTA per
+ * Limits: 1 <= k <= 16, 2 <= V < 2^31, 2 * B * k * ceil(V / 40960) < 2^31 (one CTA per
  * chunk task; else SV_ERR_UNSUPPORTED).
  */
 SV_API int32_t sv_score(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok,

@@ -13,7 +13,7 @@ constexpr int kScoreThreads = 256;
 constexpr int kScoreMinBlocks = 5;
 constexpr int kScoreGroup = 2;
 constexpr int kScoreLag = 128;
-constexpr int kScoreChunk = 32768;  // target elements per chunk task (per tensor)
+constexpr int kScoreChunk = 40960;  // target elements per chunk task (per tensor); cs = ceil(V / it)
 constexpr int kScoreMaxSplits = 32;
 // sd_verify: one cluster per sequence, 8-warp CTAs, kVerifyGroup loads per thread in flight
 constexpr int kVerifyThreads = 256;
