@@ -6,8 +6,8 @@
 //
 //   K_rank   stable ranks by all-pairs comparison through shared-memory tiles (rank_i =
 //            #{x_j < x_i} + #{j < i : x_j == x_i}, unique), then a scatter sorts S and A exactly.
-//            O(N^2 / lanes): ~0.2-0.5 ms at N = 65536 -- an offline step, chosen for exactness
-//            and determinism over a radix sort.
+//            O(N^2 / lanes): ~2 ms for both axes at N = 65536 -- an offline step, chosen for
+//            exactness and determinism over a radix sort.
 //   K_edges  equal-frequency edges (interior edge j = the ceil(j n / n_bins)-th order statistic,
 //            first = min, last = max, duplicates collapsed: S L278, L281), one thread per axis.
 //   K_bin    per record: right-closed bins (R9: index = #interior edges < value), integer counts
@@ -107,77 +107,100 @@ __global__ void __launch_bounds__(256) sv_bin_kernel(const ProfileArgs a) {
   }
 }
 
-__device__ double entropy_bits(const int *c, int n, int stride, int total) {
-  double h = 0.0;
-  for (int j = 0; j < n; ++j) {
-    const int v = c[j * stride];
-    if (v > 0) {
-      const double p = (double)v / (double)total;
-      h -= p * log2(p);
-    }
-  }
-  return h;
-}
-
-// one thread: cell means with fallbacks, then the entropies (small tables, fixed order)
-__global__ void sv_prof_final_kernel(const ProfileArgs a) {
+// one CTA: counts / joint histogram staged in shared memory, cell means with the fallbacks,
+// then the entropy terms in parallel (one thread per S bin, A bin or cell) and their sums in a
+// fixed order by thread 0 (deterministic)
+constexpr int kFinalThreads = 256;
+__global__ void __launch_bounds__(kFinalThreads) sv_prof_final_kernel(const ProfileArgs a, int joint_in_smem) {
+  extern __shared__ __align__(16) uint8_t dyn[];  // [nc] u64 X sums, [nc] counts, [nc xb] joint
+  __shared__ double term_s[kProfMaxBins], term_a[kProfMaxBins];
+  __shared__ double term_c[kProfMaxBins * kProfMaxBins];
+  __shared__ double hx, rmean[kProfMaxBins];
   pdl_wait();
   pdl_trigger();
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const int ns = *a.n_s, na = *a.n_a, xb = a.x_bins, N = a.N;
-  unsigned long long gsum = 0;
-  for (int c = 0; c < ns * na; ++c) gsum += a.xsum[c];
+  const int tid = threadIdx.x;
+  const int ns = *a.n_s, na = *a.n_a, xb = a.x_bins, N = a.N, nc = ns * na;
+  unsigned long long *sx = reinterpret_cast<unsigned long long *>(dyn);
+  int *scnt = reinterpret_cast<int *>(sx + kProfMaxBins * kProfMaxBins);
+  int *sj = joint_in_smem ? scnt + kProfMaxBins * kProfMaxBins : a.joint;
+  for (int c = tid; c < nc; c += kFinalThreads) {
+    sx[c] = a.xsum[c];
+    scnt[c] = a.counts[c];
+  }
+  if (joint_in_smem)
+    for (int j = tid; j < nc * xb; j += kFinalThreads) sj[j] = a.joint[j];
+  __syncthreads();
   const double scale = 1.0 / 4294967296.0;
+  // cell means with the S L296 fallbacks: integer sums (exact, any order), one thread per S row
+  unsigned long long gsum = 0;
+  for (int c = 0; c < nc; ++c) gsum += sx[c];
   const double gmean = (double)gsum * scale / (double)N;
-  for (int i = 0; i < ns; ++i) {
+  for (int i = tid; i < ns; i += kFinalThreads) {
     unsigned long long rs = 0;
     long long rn = 0;
     for (int j = 0; j < na; ++j) {
-      rs += a.xsum[i * na + j];
-      rn += a.counts[i * na + j];
+      rs += sx[i * na + j];
+      rn += scnt[i * na + j];
     }
-    const double rmean = rn > 0 ? (double)rs * scale / (double)rn : gmean;
-    for (int j = 0; j < na; ++j) {
-      const int c = a.counts[i * na + j];
-      a.cells[i * na + j] = c > 0 ? (double)a.xsum[i * na + j] * scale / (double)c : rmean;
-    }
+    rmean[i] = rn > 0 ? (double)rs * scale / (double)rn : gmean;
   }
+  __syncthreads();
+  for (int c = tid; c < nc; c += kFinalThreads)
+    a.cells[c] = scnt[c] > 0 ? (double)sx[c] * scale / (double)scnt[c] : rmean[c / na];
   if (!a.info) return;
-  // H(X): marginal over x bins; conditionals as sum over keys (in key order) of
-  // n_key / N * H(X | key)
-  int *tmp = a.scratch;  // [x_bins]
-  for (int x = 0; x < xb; ++x) tmp[x] = 0;
-  for (int c = 0; c < ns * na; ++c)
-    for (int x = 0; x < xb; ++x) tmp[x] += a.joint[c * xb + x];
-  const double hx = entropy_bits(tmp, xb, 1, N);
-  double hs = 0.0, ha = 0.0, hsa = 0.0;
-  for (int i = 0; i < ns; ++i) {  // H(X | S)
-    int tot = 0;
+  auto ent = [&](auto count_of, int tot) {  // H over the x bins of one group, bits
+    double h = 0.0;
     for (int x = 0; x < xb; ++x) {
-      tmp[x] = 0;
-      for (int j = 0; j < na; ++j) tmp[x] += a.joint[(i * na + j) * xb + x];
-      tot += tmp[x];
+      const int v = count_of(x);
+      if (v > 0) {
+        const double p = (double)v / (double)tot;
+        h -= p * log2(p);
+      }
     }
-    if (tot > 0) hs += (double)tot / N * entropy_bits(tmp, xb, 1, tot);
-  }
-  for (int j = 0; j < na; ++j) {  // H(X | A)
+    return h;
+  };
+  for (int i = tid; i < ns; i += kFinalThreads) {  // S bin i: n_i / N * H(X | S = i)
     int tot = 0;
-    for (int x = 0; x < xb; ++x) {
-      tmp[x] = 0;
-      for (int i = 0; i < ns; ++i) tmp[x] += a.joint[(i * na + j) * xb + x];
-      tot += tmp[x];
-    }
-    if (tot > 0) ha += (double)tot / N * entropy_bits(tmp, xb, 1, tot);
+    for (int j = 0; j < na * xb; ++j) tot += sj[i * na * xb + j];
+    term_s[i] = tot > 0 ? (double)tot / N * ent([&](int x) {
+      int v = 0;
+      for (int j = 0; j < na; ++j) v += sj[(i * na + j) * xb + x];
+      return v;
+    }, tot) : 0.0;
   }
-  for (int c = 0; c < ns * na; ++c) {  // H(X | S, A)
-    const int tot = a.counts[c];
-    if (tot > 0) hsa += (double)tot / N * entropy_bits(a.joint + c * xb, xb, 1, tot);
+  for (int j = tid; j < na; j += kFinalThreads) {  // A bin j
+    int tot = 0;
+    for (int i = 0; i < ns; ++i)
+      for (int x = 0; x < xb; ++x) tot += sj[(i * na + j) * xb + x];
+    term_a[j] = tot > 0 ? (double)tot / N * ent([&](int x) {
+      int v = 0;
+      for (int i = 0; i < ns; ++i) v += sj[(i * na + j) * xb + x];
+      return v;
+    }, tot) : 0.0;
   }
-  a.info[0] = hx;
-  a.info[1] = hs;
-  a.info[2] = ha;
-  a.info[3] = hsa;
-  a.info[4] = hx - hsa;
+  for (int c = tid; c < nc; c += kFinalThreads) {  // cell c
+    const int tot = scnt[c];
+    term_c[c] = tot > 0 ? (double)tot / N * ent([&](int x) { return sj[c * xb + x]; }, tot) : 0.0;
+  }
+  if (tid == 0) {
+    hx = ent([&](int x) {
+      int v = 0;
+      for (int c = 0; c < nc; ++c) v += sj[c * xb + x];
+      return v;
+    }, N);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double hs = 0.0, ha = 0.0, hsa = 0.0;
+    for (int i = 0; i < ns; ++i) hs += term_s[i];
+    for (int j = 0; j < na; ++j) ha += term_a[j];
+    for (int c = 0; c < nc; ++c) hsa += term_c[c];
+    a.info[0] = hx;
+    a.info[1] = hs;
+    a.info[2] = ha;
+    a.info[3] = hsa;
+    a.info[4] = hx - hsa;
+  }
 }
 
 }  // namespace
@@ -190,7 +213,14 @@ cudaError_t launch_profile(const ProfileArgs &a, cudaStream_t st) {
   if ((e = launch_k(sv_edges_kernel, dim3(1), dim3(64), 0, st, a)) != cudaSuccess) return e;
   const int grid = (int)((a.N + 255) / 256 < 1184 ? (a.N + 255) / 256 : 1184);
   if ((e = launch_k(sv_bin_kernel, dim3((unsigned)grid), dim3(256), 0, st, a)) != cudaSuccess) return e;
-  return launch_k(sv_prof_final_kernel, dim3(1), dim3(32), 0, st, a);
+  const size_t base = (size_t)kProfMaxBins * kProfMaxBins * 12;
+  const size_t joint = (size_t)a.n_s_bins * a.n_a_bins * a.x_bins * 4;
+  const int jsm = base + joint <= 160 * 1024;
+  const size_t smem = base + (jsm ? joint : 0);
+  if ((e = cudaFuncSetAttribute(sv_prof_final_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+      cudaSuccess)
+    return e;
+  return launch_k(sv_prof_final_kernel, dim3(1), dim3(kFinalThreads), smem, st, a, jsm);
 }
 
 }  // namespace sv
