@@ -217,3 +217,12 @@ def test_headline_full_size_sampled(sv, prof_dict):
         rv = oracle.verify(Dd, Td, sub["tok"], gam[b:b + 1], 1.0, 1.0, 0xC0FFEE, 1, b)
         H.compare_verify({kk: v[b:b + 1] for kk, v in gv.items()}, rv, rep)
     print("ties:", rep.ties)
+
+
+@pytest.mark.parametrize("B,k", [(4, 2), (12, 4), (6, 8)])
+def test_config5_sweep_points(sv, prof_dict, B, k):
+    """BASELINE config 5: V = 128256 bf16, k in {2, 4, 8}, alignment swept so the per-sequence
+    acceptance spans ~0.1..0.9 (synth 'sweep' amplitudes)."""
+    x = synth.make_inputs(B, k, 128256, "bf16", seed=5000 + B * k, alignment="sweep")
+    *_, rep = run_case(sv, prof_dict, x)
+    print("ties:", rep.ties)
