@@ -4,7 +4,10 @@
 // distribution has at most 32 support entries, so after one selection pass per row the rest of
 // the path runs on tiny lists:
 //
-//   KF1 sv_topk_kernel  one CTA per row: radix select of the top_k-th largest logit on the
+//   KF1 sv_topk_kernel  one CTA per row: the minimum of the 32 half-warp maxima bounds the
+//                       top_k-th largest key from below, so one more pass gathers the few keys
+//                       above it, ranked by counting; on overflow: radix select of the top_k-th
+//                       largest logit on the
 //                       order-preserving key of the raw bits (bf16: 2 passes of 8 bits, fp32: 4),
 //                       256-bin shared-memory histograms over the row (the first pass streams
 //                       it from HBM, the rest hit L2), then one collection pass: keys above the
@@ -29,27 +32,7 @@ namespace {
 
 constexpr int kTopKThreads = 512;
 constexpr int kTieCap = 2048;   // tie indices held for the ordered pick (power of two)
-constexpr int kCandCap = 4096;  // fast-path candidates (power of two, >= kTopKThreads)
-
-// in-place bitonic sort, descending, of n (a power of two <= kCandCap) 64-bit keys; all threads
-__device__ __forceinline__ void bitonic_desc(unsigned long long *v, int n) {
-  for (int size = 2; size <= n; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int j = threadIdx.x; j < n; j += blockDim.x) {
-        const int o = j ^ stride;
-        if (o > j) {
-          const bool desc = (j & size) == 0;
-          const unsigned long long a = v[j], b = v[o];
-          if ((a < b) == desc) {
-            v[j] = b;
-            v[o] = a;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
+constexpr int kCandCap = 2048;  // fast-path candidates (ranked by counting: O(n^2 / threads))
 
 template <typename T> struct KeyOf;
 template <> struct KeyOf<__nv_bfloat16> {
@@ -109,6 +92,7 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
   __shared__ int s_remaining, s_bad, s_ngt, s_ntie;
   __shared__ int s_tie[kTieCap];
   __shared__ unsigned long long s_cand[kCandCap];
+  __shared__ uint32_t s_gmax[kTopKThreads / 16];
   __shared__ int s_ncand;
   __shared__ K c_key[32];
   __shared__ int c_idx[32];
@@ -140,14 +124,24 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
     const int units = vec ? V / EPU : 0;
     K tmax = 0;
     int bad = 0;
-    for (int u = tid; u < units; u += NT) {
-      const uint4 w = ldg_stream(x + (size_t)u * EPU);
-      const T *e = reinterpret_cast<const T *>(&w);
+    constexpr int UF = 4;  // independent 16-byte loads in flight per thread
+    for (int u0 = tid; u0 < units; u0 += UF * NT) {
+      uint4 w[UF];
 #pragma unroll
-      for (int j = 0; j < EPU; ++j) {
-        const K kk = KO::key(e, j);
-        tmax = kk > tmax ? kk : tmax;
-        bad |= KO::bad(kk);
+      for (int q = 0; q < UF; ++q) {
+        const int u = u0 + q * NT;
+        w[q] = u < units ? ldg_stream(x + (size_t)u * EPU) : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int q = 0; q < UF; ++q) {
+        if (u0 + q * NT >= units) continue;
+        const T *e = reinterpret_cast<const T *>(&w[q]);
+#pragma unroll
+        for (int j = 0; j < EPU; ++j) {
+          const K kk = KO::key(e, j);
+          tmax = kk > tmax ? kk : tmax;
+          bad |= KO::bad(kk);
+        }
       }
     }
     for (int e = units * EPU + tid; e < V; e += NT) {
@@ -157,23 +151,41 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) s_bad = 1;
     __syncthreads();
-    s_cand[tid] = (unsigned long long)tmax << 32;  // thread maxima, sorted descending
+    // lower bound: the minimum of the 32 half-warp maxima -- 32 distinct elements are >= it, so
+    // the KK-th largest (KK <= 32) is too (no sort of the thread maxima needed)
+    K gmax = tmax;
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      const K v = __shfl_xor_sync(0xffffffffu, gmax, o);
+      gmax = v > gmax ? v : gmax;
+    }
+    if ((lane & 15) == 0) s_gmax[tid >> 4] = gmax;
     __syncthreads();
-    bitonic_desc(s_cand, NT);
-    const K lb = (K)(s_cand[KK - 1] >> 32);
-    __syncthreads();
+    K lb = s_gmax[0];
+#pragma unroll 8
+    for (int g = 1; g < NT / 16; ++g) lb = s_gmax[g] < lb ? s_gmax[g] : lb;
     if (tid == 0) s_ncand = 0;
     __syncthreads();
-    for (int u = tid; u < units; u += NT) {
-      const uint4 w = ldg_stream(x + (size_t)u * EPU);
-      const T *e = reinterpret_cast<const T *>(&w);
+    for (int u0 = tid; u0 < units; u0 += UF * NT) {
+      uint4 w[UF];
 #pragma unroll
-      for (int j = 0; j < EPU; ++j) {
-        const K kk = KO::key(e, j);
-        if (kk >= lb) {
-          const int slot = atomicAdd(&s_ncand, 1);
-          if (slot < kCandCap)
-            s_cand[slot] = ((unsigned long long)kk << 32) | (0xFFFFFFFFu - (uint32_t)(u * EPU + j));
+      for (int q = 0; q < UF; ++q) {
+        const int u = u0 + q * NT;
+        w[q] = u < units ? ldg_stream(x + (size_t)u * EPU) : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int q = 0; q < UF; ++q) {
+        const int u = u0 + q * NT;
+        if (u >= units) continue;
+        const T *e = reinterpret_cast<const T *>(&w[q]);
+#pragma unroll
+        for (int j = 0; j < EPU; ++j) {
+          const K kk = KO::key(e, j);
+          if (kk >= lb) {
+            const int slot = atomicAdd(&s_ncand, 1);
+            if (slot < kCandCap)
+              s_cand[slot] = ((unsigned long long)kk << 32) | (0xFFFFFFFFu - (uint32_t)(u * EPU + j));
+          }
         }
       }
     }
@@ -186,15 +198,15 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
     }
     __syncthreads();
     const int nc = s_ncand;
-    if (nc <= kCandCap) {  // (key desc, index asc) == composite desc
-      int np2 = 1;
-      while (np2 < nc) np2 <<= 1;
-      for (int j = nc + tid; j < np2; j += NT) s_cand[j] = 0ull;
-      __syncthreads();
-      bitonic_desc(s_cand, np2);
-      if (tid < KK) {
-        c_key[tid] = (K)(s_cand[tid] >> 32);
-        c_idx[tid] = (int)(0xFFFFFFFFu - (uint32_t)s_cand[tid]);
+    if (nc <= kCandCap) {  // rank by counting on the unique composite (key desc, index asc)
+      for (int j = tid; j < nc; j += NT) {
+        const unsigned long long cj = s_cand[j];
+        int rank = 0;
+        for (int i = 0; i < nc; ++i) rank += s_cand[i] > cj;
+        if (rank < KK) {
+          c_key[rank] = (K)(cj >> 32);
+          c_idx[rank] = (int)(0xFFFFFFFFu - (uint32_t)cj);
+        }
       }
       fast = true;
     }
