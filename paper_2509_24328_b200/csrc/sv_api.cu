@@ -51,28 +51,6 @@ int64_t rows_splits_for(int64_t V, int elem_bytes) {
   return (V + per - 1) / per;
 }
 
-int max_active_clusters(const void *fn, cudaLaunchConfig_t cfg, int smem, int cs) {
-  static std::mutex mu;
-  static std::map<std::tuple<const void *, int, int, int>, int> cache;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const auto key = std::make_tuple(fn, smem, cs, dev);
-  std::lock_guard<std::mutex> lock(mu);
-  auto it = cache.find(key);
-  if (it != cache.end()) return it->second;
-  cfg.gridDim = dim3((unsigned)cs);
-  cfg.stream = 0;
-  int ncl = 0;
-  if (cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg) != cudaSuccess || ncl <= 0) {
-    cudaGetLastError();
-    int sms = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    ncl = sms / cs > 0 ? sms / cs : 1;
-  }
-  cache[key] = ncl;
-  return ncl;
-}
-
 int resident_grid(const void *fn, int threads, int smem) {
   static std::mutex mu;
   static std::map<std::tuple<const void *, int, int, int>, int> cache;

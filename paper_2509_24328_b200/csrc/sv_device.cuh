@@ -132,11 +132,6 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// order this thread's earlier generic-proxy shared-memory accesses before later async-proxy
-// (bulk copy) writes to the same buffer
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -217,27 +212,6 @@ __device__ __forceinline__ float block_max(float v, float *scratch) {
   for (int i = 1; i < NW; ++i) r = fmaxf(r, scratch[i]);
   return r;
 }
-template <int NT, int NV>
-__device__ __forceinline__ void block_sum(float (&v)[NV], float *scratch) {
-  constexpr int NW = NT / 32;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-  for (int j = 0; j < NV; ++j) v[j] = warp_sum(v[j]);
-  __syncthreads();
-  if (lane == 0) {
-#pragma unroll
-    for (int j = 0; j < NV; ++j) scratch[j * NW + w] = v[j];
-  }
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < NV; ++j) {
-    float r = scratch[j * NW];
-#pragma unroll
-    for (int i = 1; i < NW; ++i) r += scratch[j * NW + i];
-    v[j] = r;
-  }
-}
-
 // ---------------------------------------------------------------- Philox4x32-10
 // Salmon et al., SC'11.  counter = (i, global seq, lo(offset), hi(offset)),
 // key = (lo(seed), hi(seed)) (DESIGN R12).

@@ -15,10 +15,6 @@ constexpr int kScoreGroup = 2;
 constexpr int kScoreLag = 128;
 constexpr int kScoreChunk = 40960;  // target elements per chunk task (per tensor); cs = ceil(V / it)
 constexpr int kScoreMaxSplits = 32;
-// sd_verify: one cluster per sequence, 8-warp CTAs, kVerifyGroup loads per thread in flight
-constexpr int kVerifyThreads = 256;
-constexpr int kVerifyMinBlocks = 4;
-constexpr int kVerifyGroup = 2;
 constexpr int kRowsThreads = 256;
 constexpr int kSampleThreads = 256;
 // On-chip budget for the (D, C) [or (T, D)] chunk pair one CTA holds: the cluster size is
@@ -36,8 +32,6 @@ int score_splits_for(int64_t V);                     // sv_score chunks per row
 int tune_knob(const char *name, int dflt);           // integer from the environment (tuning)
 int64_t chunk_elems_for(int64_t V, int cs);          // per-CTA elements (multiple of 16)
 int64_t rows_splits_for(int64_t V, int elem_bytes);  // sd_verify phase-1 CTAs per row
-// co-resident clusters for a cluster kernel (cached per function / smem / cluster size / device)
-int max_active_clusters(const void *fn, cudaLaunchConfig_t cfg, int smem, int cs);
 // co-resident CTAs of a persistent kernel on this device (cached)
 int resident_grid(const void *fn, int threads, int smem);
 
