@@ -77,3 +77,41 @@ def test_product_has_no_cpu_fallback():
             assert "oracle" not in open(os.path.join(pkg, fn)).read().replace("fp64 oracle", "")
     with pytest.raises(sv.SvError):
         sv.sv_score(torch.zeros(1, 1, 8), torch.zeros(1, 1, 8), torch.zeros(1, 1, dtype=torch.int32))
+
+
+def test_host_validation_of_the_widened_abi(lib):
+    """NEXT-2/3/4 and vocab-sharded entry points reject bad arguments on the host, before any
+    CUDA call (so this runs without a GPU)."""
+    from paper_2509_24328_b200 import _lib
+    P = ctypes.c_void_p(16)  # a non-NULL dummy: validation fails before any dereference
+    L = _lib.SvLogits(16, _lib.SV_BF16, 0, 0, 0)
+    # filters: top_k 0 (nucleus only) and 33 are unsupported, top_p outside (0, 1] invalid
+    for top_k, top_p, want in ((0, 0.9, _lib.SV_ERR_UNSUPPORTED), (33, 0.9, _lib.SV_ERR_UNSUPPORTED),
+                               (20, 0.0, _lib.SV_ERR_INVALID_ARG), (20, 1.5, _lib.SV_ERR_INVALID_ARG)):
+        f = _lib.SvFilter(top_k, top_p)
+        st = lib.sv_score_filtered(ctypes.byref(L), ctypes.byref(L), P, 2, 2, 100, 1.0, 1.0, ctypes.byref(f), None,
+                                   None, None, None, None, None, None, P, 1 << 20, None)
+        assert st == want, (top_k, top_p, st)
+    assert lib.sv_filter_workspace_bytes(80, 8) > 0 and lib.sv_filter_workspace_bytes(80, 17) == 0
+    # ragged verify: missing row pointers / short row stride
+    st = lib.sd_verify_ragged(ctypes.byref(L), P, 99, P, P, P, P, P, P, 2, 2, 100, 1.0, 1.0, 0, 0, None, 0,
+                              P, P, None, None, None, P, 1 << 30, None)
+    assert st == _lib.SV_ERR_INVALID_ARG
+    st = lib.sd_verify_ragged(ctypes.byref(L), P, 100, None, P, P, P, P, P, 2, 2, 100, 1.0, 1.0, 0, 0, None, 0,
+                              P, P, None, None, None, P, 1 << 30, None)
+    assert st == _lib.SV_ERR_INVALID_ARG
+    # profile builder: bins beyond 64, empty input, small workspace
+    assert lib.sv_profile_workspace_bytes(100, 65, 10, 10) == 0
+    assert lib.sv_profile_workspace_bytes(0, 20, 15, 10) == 0
+    st = lib.sv_profile_build(P, P, P, 100, 20, 15, 10, P, P, P, P, P, None, P, 16, None)
+    assert st == _lib.SV_ERR_WORKSPACE
+    # vocab-sharded: G < 1, rank out of range, G * chunks > 32
+    assert lib.sv_shard_xch_bytes(0, 80, 8, 19008, _lib.SV_BF16) > 0
+    assert lib.sv_shard_xch_bytes(4, 80, 8, 19008, _lib.SV_BF16) == 0
+    st = lib.sv_shard_score_p2(ctypes.byref(L), ctypes.byref(L), P, 2, 2, 100, 1.0, 1.0, P, 0, P, None)
+    assert st == _lib.SV_ERR_INVALID_ARG
+    st = lib.sv_shard_score_p2(ctypes.byref(L), ctypes.byref(L), P, 2, 2, 152064, 1.0, 1.0, P, 9, P, None)
+    assert st == _lib.SV_ERR_UNSUPPORTED  # 9 ranks x 4 chunks > 32 merge lanes
+    st = lib.sv_shard_verify_finish(ctypes.byref(L), ctypes.byref(L), 2, 2, 100, 0, 1.0, 1.0, P, 2, 2, P, None,
+                                    None, P, 1 << 30, None)
+    assert st == _lib.SV_ERR_INVALID_ARG
