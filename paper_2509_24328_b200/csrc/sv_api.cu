@@ -37,7 +37,9 @@ int cluster_size_for(int64_t V, int elem_bytes) {
 
 int score_splits_for(int64_t V) {
   static const int target = tune_knob("SV_SCORE_CHUNK", kScoreChunk);
-  const int64_t s = (V + target - 1) / target;
+  static const int min_cs = tune_knob("SV_SCORE_MIN_CS", kScoreMinSplits);
+  int64_t s = (V + target - 1) / target;
+  if (s < min_cs) s = min_cs;  // short rows: several chunk tasks per row (latency at small B)
   return (int)(s < 1 ? 1 : (s > kScoreMaxSplits ? kScoreMaxSplits : s));
 }
 

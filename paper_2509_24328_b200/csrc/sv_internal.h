@@ -15,6 +15,7 @@ constexpr int kScoreGroup = 2;
 constexpr int kScoreLag = 128;
 constexpr int kScoreChunk = 40960;  // target elements per chunk task (per tensor); cs = ceil(V / it)
 constexpr int kScoreMaxSplits = 32;
+constexpr int kScoreMinSplits = 4;  // chunk tasks per row at least (a function of V only)
 constexpr int kRowsThreads = 256;
 constexpr int kSampleThreads = 256;
 // On-chip budget for the (D, C) [or (T, D)] chunk pair one CTA holds: the cluster size is
