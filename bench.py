@@ -172,9 +172,25 @@ def cpu_baseline_sample(config):
         oracle.verify(Dd, Td, x["tok"], rh["gamma"], 1.0, 1.0, 0xC0FFEE, reps, 0, nthreads=cores)
         t_total += time.perf_counter() - t0
         reps += 1
+    # the same oracle on one host thread (single-thread and all-core figures)
+    reps1, t1 = 0, 0.0
+    while t1 < 4.0:
+        t0 = time.perf_counter()
+        rs = oracle.score(Dd[:1], Cd[:1], x["tok"][:1], 1.0, 1.0, prof, nthreads=1)
+        rh = oracle.schedule(rs["p_hat"], L)
+        oracle.verify(Dd[:1], Td[:1], x["tok"][:1], rh["gamma"], 1.0, 1.0, 0xC0FFEE, reps1, 0, nthreads=1)
+        t1 += time.perf_counter() - t0
+        reps1 += 1
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), "")
+    except OSError:
+        pass
     return {"value": reps * n_seq * k / t_total, "unit": "positions/s", "cores": cores, "kind": "oracle",
             "sample": f"{n_seq} sequences x {k} positions of the {config} workload, {reps} repetitions, "
-                      f"{t_total:.1f} s"}
+                      f"{t_total:.1f} s",
+            "single_thread_value": reps1 * k / t1, "cpu_model": model, "host_cpus": os.cpu_count()}
 
 
 # --------------------------------------------------------------------------- vocab-sharded arm
