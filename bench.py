@@ -499,24 +499,49 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     prof_ms = p0.elapsed_time(p1) / n_pb
 
-    # ---------------- e2e: host buffers, H2D + pipeline + D2H every step
+    # ---------------- e2e: host buffers, H2D + pipeline + D2H every step.  As in the paper's
+    # serving loop (P L266, NEXT-3) the target side only ships the gamma_b + 1 verified rows of
+    # each sequence: D, C and the draft tokens go up first, sv_score -> sv_schedule run, gamma
+    # comes back (the target forward would run here), then only the compacted target rows go
+    # up and sd_verify_ragged consumes them; n_accept / tokens come back.
     e2e_steps = min(args.steps, 20)
     hout = torch.empty((2, B), dtype=torch.int32).pin_memory()
     dsets = sets[0]
+    rows_dev = torch.empty((B * (k + 1), V), dtype=tdtype, device=dev)
+    rowptr_h = torch.zeros(B, dtype=torch.int64).pin_memory()
+    rowptr_d = torch.empty(B, dtype=torch.int64, device=dev)
+    gam_h = torch.empty(B, dtype=torch.int32).pin_memory()
+    h2d_acc = [0]
 
     def e2e_step(j):
-        D, C, T, tok = dsets
+        D, C, _, tok = dsets
         D.copy_(hD, non_blocking=True)
         C.copy_(hC, non_blocking=True)
-        T.copy_(hT, non_blocking=True)
         tok.copy_(htok, non_blocking=True)
-        r = pipe.run(D, C, T, tok, seed=0xC0FFEE, offset=j, seq_base=seq_base)
+        sc = sv.sv_score(D, C, tok, pipe.tau_d, pipe.tau_c, prof, workspace=pipe.workspace, out=pipe.score_out,
+                         stream=stream)
+        g = sv.sv_schedule(sc["p_hat"], L, out=pipe.sched_out, stream=stream)["gamma"]
+        gam_h.copy_(g, non_blocking=True)
+        stream.synchronize()
+        gg = gam_h.numpy()
+        off = 0
+        for b in range(B):
+            n = int(gg[b]) + 1
+            rowptr_h[b] = off
+            rows_dev[off:off + n].copy_(hT[b, :n], non_blocking=True)
+            off += n
+        rowptr_d.copy_(rowptr_h, non_blocking=True)
+        h2d_acc[0] += (hD.numel() + hC.numel() + off * V) * elem + htok.numel() * 4 + B * 8
+        r = sv.sd_verify_ragged(D, rows_dev[:off], rowptr_d, tok, g, sc["draft_m"], sc["draft_l"], sc["draft_ptok"],
+                                pipe.tau_d, pipe.tau_t, 0xC0FFEE, j, None, seq_base, workspace=pipe.workspace,
+                                out=pipe.ver_out, stream=stream)
         hout[0].copy_(r["n_accept"], non_blocking=True)
         hout[1].copy_(r["out_tok"], non_blocking=True)
 
     for j in range(2):
         e2e_step(j)
     barrier()
+    h2d_acc[0] = 0
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for j in range(e2e_steps):
@@ -528,8 +553,8 @@ def run_ours(args, rank, world, local_rank):
         tt = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt.item())
-    h2d = (hD.numel() + hC.numel() + hT.numel()) * elem + htok.numel() * 4
-    d2h = hout.numel() * 4
+    h2d = h2d_acc[0] // e2e_steps
+    d2h = hout.numel() * 4 + gam_h.numel() * 4
 
     cpu = cpu_baseline_sample(args.config) if (rank == 0 and world == 1 and not args.no_cpu_baseline) else None
     if rank == 0:
@@ -570,7 +595,9 @@ def run_ours(args, rank, world, local_rank):
                                       "kept-bin counts"},
             "e2e": {"value": world * B * k / (e2e_ms / e2e_steps * 1e-3), "unit": "positions/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e2e_steps,
-                    "path": "pinned host -> cudaMemcpyAsync -> sv_score/sv_schedule/sd_verify (C ABI) -> host"},
+                    "path": "pinned host -> D, C, tokens -> sv_score, sv_schedule -> gamma to host -> only the "
+                            "gamma_b + 1 verified target rows -> sd_verify_ragged -> n_accept, tokens to host "
+                            "(C ABI)"},
             "gpu_launches": KERNELS_PER_STEP * args.steps,  # per timed step: 6 libsv kernels (+ 1 torch add)
             "clocks": gclk.summary(),
             "cpu_baseline": cpu,
