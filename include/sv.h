@@ -253,7 +253,7 @@ SV_API int32_t sd_verify_filtered(const sv_logits *target, const int32_t *draft_
  * sv_profile_build -- NEXT-4: the offline (S, A) -> acceptance profile of a profiling run and
  * its information-gain report (P L176 "adaptive binning ... compute the average token
  * acceptance probability for each bin combination"; S L275-310; Table 2 layout P L347-368).
- * Records: S, A, X [N] fp32 on the device (S, A from sv_score; X = accept_ratio from sd_verify,
+ * Records: S, A, X [N] finite fp32 on the device (S, A from sv_score; X = accept_ratio from sd_verify,
  * the true acceptance probability min(1, p_t(t)/p_d(t)), P L150).
  * Edges: equal-frequency, interior edge j = the ceil(j N / n_bins)-th order statistic, first =
  * min, last = max, duplicates collapsed (S L278, L281) -> s_edges [n_s_bins + 1],

@@ -479,17 +479,19 @@ int32_t sd_verify_filtered(const sv_logits *target, const int32_t *draft_tok, co
 
 // ------------------------------------------------------------------ NEXT-4 profile builder
 static int64_t prof_ws_layout(int32_t N, int32_t ns, int32_t na, int32_t xb, int64_t off[5]) {
+  int64_t P = 1;  // sort buffers: the next power of two
+  while (P < N) P <<= 1;
   off[0] = 0;                                              // s_sorted
-  off[1] = off[0] + ws_round((int64_t)N * 4);              // a_sorted
-  off[2] = off[1] + ws_round((int64_t)N * 4);              // xsum
+  off[1] = off[0] + ws_round(P * 4);                       // a_sorted
+  off[2] = off[1] + ws_round(P * 4);                       // xsum
   off[3] = off[2] + ws_round((int64_t)ns * na * 8);        // joint
   off[4] = off[3] + ws_round((int64_t)ns * na * xb * 4);   // scratch
   return off[4] + ws_round((int64_t)xb * 4);
 }
 
 size_t sv_profile_workspace_bytes(int32_t N, int32_t n_s_bins, int32_t n_a_bins, int32_t x_bins) {
-  if (N < 1 || n_s_bins < 1 || n_a_bins < 1 || x_bins < 1 || n_s_bins > kProfMaxBins || n_a_bins > kProfMaxBins ||
-      x_bins > 1024)
+  if (N < 1 || N > (1 << 30) || n_s_bins < 1 || n_a_bins < 1 || x_bins < 1 || n_s_bins > kProfMaxBins ||
+      n_a_bins > kProfMaxBins || x_bins > 1024)
     return 0;
   int64_t off[5];
   return (size_t)prof_ws_layout(N, n_s_bins, n_a_bins, x_bins, off);

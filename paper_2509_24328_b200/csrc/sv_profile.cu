@@ -4,10 +4,8 @@
 // Table 2 layout P L347-368).  Input: N records (S, A, X) as produced by sv_score (S, A) and
 // sd_verify (X = accept_ratio = min(1, p_t(t)/p_d(t)), the true acceptance probability P L150).
 //
-//   K_rank   stable ranks by all-pairs comparison through shared-memory tiles (rank_i =
-//            #{x_j < x_i} + #{j < i : x_j == x_i}, unique), then a scatter sorts S and A exactly.
-//            O(N^2 / lanes): ~2 ms for both axes at N = 65536 -- an offline step, chosen for
-//            exactness and determinism over a radix sort.
+//   K_sort   bitonic sort of S and A (padded to a power of two with +inf): shared-memory tiles
+//            for the strides below 4096, one global pass per larger stride.
 //   K_edges  equal-frequency edges (interior edge j = the ceil(j n / n_bins)-th order statistic,
 //            first = min, last = max, duplicates collapsed: S L278, L281), one thread per axis.
 //   K_bin    per record: right-closed bins (R9: index = #interior edges < value), integer counts
@@ -25,34 +23,68 @@ namespace sv {
 
 namespace {
 
-constexpr int kRankThreads = 256;
-constexpr int kRankTile = 4096;
+// Sort: bitonic network over P = next power of two >= N (padding +inf), ascending, on both axes
+// at once (blockIdx.y = 0: S, 1: A).  Tiles of kSortTile elements run every stage with a stride
+// below the tile in shared memory; the larger strides are one global pass each.  Equal values are
+// interchangeable for the order statistics, so no stability is needed.
+constexpr int kSortThreads = 512;
+constexpr int kSortTile = 4096;
 
-// blockIdx.y selects the array (0 = S, 1 = A)
-__global__ void __launch_bounds__(kRankThreads) sv_rank_kernel(const ProfileArgs a) {
-  __shared__ float tile[kRankTile];
+__device__ __forceinline__ float *sort_buf(const ProfileArgs &a) { return blockIdx.y == 0 ? a.s_sorted : a.a_sorted; }
+
+__global__ void __launch_bounds__(kSortThreads) sv_sort_load_kernel(const ProfileArgs a, int P) {
   pdl_wait();
   pdl_trigger();
   const float *x = blockIdx.y == 0 ? a.S : a.A;
-  float *sorted = blockIdx.y == 0 ? a.s_sorted : a.a_sorted;
-  const int i = blockIdx.x * kRankThreads + threadIdx.x;
-  const float xi = i < a.N ? x[i] : 0.f;
-  int rank = 0;
-  for (int t0 = 0; t0 < a.N; t0 += kRankTile) {
-    const int n = min(kRankTile, a.N - t0);
-    __syncthreads();
-    for (int j = threadIdx.x; j < n; j += kRankThreads) tile[j] = x[t0 + j];
-    __syncthreads();
-    if (i < a.N) {
-      const int jlim = i - t0;  // tile entries with global index < i
-#pragma unroll 8
-      for (int j = 0; j < n; ++j) {
-        const float xj = tile[j];
-        rank += (xj < xi) | ((xj == xi) & (j < jlim));
+  float *buf = sort_buf(a);
+  for (int i = blockIdx.x * kSortThreads + threadIdx.x; i < P; i += gridDim.x * kSortThreads)
+    buf[i] = i < a.N ? x[i] : __int_as_float(0x7f800000);
+}
+
+// stages (size, stride) with stride < kSortTile inside one shared-memory tile: from size = 2 up
+// to size_hi when `full`, else only the strides below the tile of the single size `size_hi`
+__global__ void __launch_bounds__(kSortThreads) sv_sort_tile_kernel(const ProfileArgs a, int size_hi, int full, int P) {
+  __shared__ float t[kSortTile];
+  pdl_wait();
+  pdl_trigger();
+  float *buf = sort_buf(a);
+  const int n = min(kSortTile, P), base = blockIdx.x * n;
+  for (int j = threadIdx.x; j < n; j += kSortThreads) t[j] = buf[base + j];
+  __syncthreads();
+  for (int size = full ? 2 : size_hi; size <= size_hi; size <<= 1) {
+    for (int stride = min(size, n) >> 1; stride > 0; stride >>= 1) {
+      for (int j = threadIdx.x; j < n; j += kSortThreads) {
+        const int o = j ^ stride;
+        if (o > j) {
+          const bool up = ((base + j) & size) == 0;
+          const float u = t[j], v = t[o];
+          if ((u > v) == up) {
+            t[j] = v;
+            t[o] = u;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int j = threadIdx.x; j < n; j += kSortThreads) buf[base + j] = t[j];
+}
+
+__global__ void __launch_bounds__(kSortThreads) sv_sort_global_kernel(const ProfileArgs a, int size, int stride, int P) {
+  pdl_wait();
+  pdl_trigger();
+  float *buf = sort_buf(a);
+  for (int j = blockIdx.x * kSortThreads + threadIdx.x; j < P; j += gridDim.x * kSortThreads) {
+    const int o = j ^ stride;
+    if (o > j) {
+      const bool up = (j & size) == 0;
+      const float u = buf[j], v = buf[o];
+      if ((u > v) == up) {
+        buf[j] = v;
+        buf[o] = u;
       }
     }
   }
-  if (i < a.N) sorted[rank] = xi;
 }
 
 // equal-frequency edges of one sorted axis with the duplicate collapse (matches
@@ -207,9 +239,20 @@ __global__ void __launch_bounds__(kFinalThreads) sv_prof_final_kernel(const Prof
 
 cudaError_t launch_profile(const ProfileArgs &a, cudaStream_t st) {
   cudaError_t e;
-  if ((e = launch_k(sv_rank_kernel, dim3((unsigned)((a.N + kRankThreads - 1) / kRankThreads), 2), dim3(kRankThreads),
-                    0, st, a)) != cudaSuccess)
-    return e;
+  int P = 1;
+  while (P < a.N) P <<= 1;
+  const unsigned gblocks = (unsigned)((P + kSortThreads - 1) / kSortThreads < 512 ? (P + kSortThreads - 1) / kSortThreads : 512);
+  if ((e = launch_k(sv_sort_load_kernel, dim3(gblocks, 2), dim3(kSortThreads), 0, st, a, P)) != cudaSuccess) return e;
+  const int tile = P < kSortTile ? P : kSortTile;
+  const dim3 tgrid((unsigned)(P / tile), 2);
+  if ((e = launch_k(sv_sort_tile_kernel, tgrid, dim3(kSortThreads), 0, st, a, tile, 1, P)) != cudaSuccess) return e;
+  for (int size = 2 * tile; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride >= tile; stride >>= 1)
+      if ((e = launch_k(sv_sort_global_kernel, dim3(gblocks, 2), dim3(kSortThreads), 0, st, a, size, stride, P)) !=
+          cudaSuccess)
+        return e;
+    if ((e = launch_k(sv_sort_tile_kernel, tgrid, dim3(kSortThreads), 0, st, a, size, 0, P)) != cudaSuccess) return e;
+  }
   if ((e = launch_k(sv_edges_kernel, dim3(1), dim3(64), 0, st, a)) != cudaSuccess) return e;
   const int grid = (int)((a.N + 255) / 256 < 1184 ? (a.N + 255) / 256 : 1184);
   if ((e = launch_k(sv_bin_kernel, dim3((unsigned)grid), dim3(256), 0, st, a)) != cudaSuccess) return e;
