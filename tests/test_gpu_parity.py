@@ -226,3 +226,14 @@ def test_config5_sweep_points(sv, prof_dict, B, k):
     x = synth.make_inputs(B, k, 128256, "bf16", seed=5000 + B * k, alignment="sweep")
     *_, rep = run_case(sv, prof_dict, x)
     print("ties:", rep.ties)
+
+
+@pytest.mark.parametrize("B,k,V,dtype", [
+    (1, 1, 1_000_003, "bf16"),   # one very long row: 25 chunk tasks, 489 K4 splits, ragged tail
+    (512, 16, 256, "bf16"),      # many short rows at the k limit (8192 positions)
+    (1, 16, 33, "f32"),          # k = 16 with V barely above a unit
+])
+def test_extreme_shapes(sv, prof_dict, B, k, V, dtype):
+    x = synth.make_inputs(B, k, V, dtype, seed=31337 + V)
+    *_, rep = run_case(sv, prof_dict, x)
+    print("ties:", rep.ties)
