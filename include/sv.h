@@ -161,6 +161,22 @@ SV_API int32_t sv_schedule(const float *p_hat, int32_t B, int32_t k, const doubl
                     int32_t *row_status, void *workspace, size_t workspace_bytes, void *stream);
 
 /*
+ * sv_score_schedule -- sv_score followed by sv_schedule in PER_ROW mode in ONE launch: the
+ * row epilogue that completes a sequence's last row runs step a4 for that sequence (P L207-239;
+ * R2-R4), so no separate schedule kernel sits on the critical path.  Arguments: those of
+ * sv_score (p_hat must be non-NULL) plus those of sv_schedule (latency [n_lat] fp64 with
+ * n_lat >= k + 2, plus_one, gamma / exp_accept / goodput / sched_status [B]).  Outputs are
+ * bit-identical to sv_score + sv_schedule(PER_ROW).  Same workspace as sv_score.
+ */
+SV_API int32_t sv_score_schedule(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok,
+                                 int32_t B, int32_t k, int32_t V, float tau_d, float tau_c,
+                                 const sv_profile *prof, float *S, float *A, float *KL, float *p_hat,
+                                 float *draft_m, float *draft_l, float *draft_ptok, int32_t *row_status,
+                                 const double *latency, int32_t n_lat, int32_t plus_one, int32_t *gamma,
+                                 float *exp_accept, float *goodput, int32_t *sched_status, void *workspace,
+                                 size_t workspace_bytes, void *stream);
+
+/*
  * sd_verify -- steps a5-a6: standard speculative-decoding verification of the first
  * gamma[b] draft tokens and the correction / bonus sample (P L29 citing Leviathan et al.;
  * S L148-165; residual S L157-165; inverse CDF S L82-90; R1, R10-R13).

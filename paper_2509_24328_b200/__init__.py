@@ -11,6 +11,7 @@ streams only.  No CPU fallback exists: the compute calls raise without libsv.so 
 from __future__ import annotations
 
 import ctypes
+import os
 
 import torch
 
@@ -18,7 +19,7 @@ from . import _lib
 from ._lib import (ROW_ALL_NEG_INF, ROW_BAD_GAMMA, ROW_BAD_LATENCY, ROW_BAD_TOKEN, ROW_DRAFT_ZERO,  # noqa: F401
                    ROW_NAN, ROW_PHAT_BAD, ROW_RESID_ZERO, SV_SCHED_BATCH_GREEDY, SV_SCHED_PER_ROW, SvError)
 
-__all__ = ["sv_score", "sv_schedule", "sd_verify", "sd_verify_ragged", "workspace_bytes", "cluster_size", "Profile",
+__all__ = ["sv_score", "sv_score_schedule", "sv_schedule", "sd_verify", "sd_verify_ragged", "workspace_bytes", "cluster_size", "Profile",
            "Pipeline", "GraphPipeline", "sv_profile_build", "sv_score_filtered", "sd_verify_filtered", "load_library"]
 
 
@@ -112,6 +113,38 @@ def sv_score(D, C, tok, tau_d=1.0, tau_c=1.0, profile: Profile | None = None, wo
         _stream(stream))
     _lib.check(st, "sv_score")
     return res
+
+
+def sv_score_schedule(D, C, tok, latency, tau_d=1.0, tau_c=1.0, profile: Profile | None = None, plus_one=1,
+                      workspace=None, out=None, sched_out=None, stream=None) -> tuple[dict, dict]:
+    """Steps a1-a4 in one launch (C ABI `sv_score_schedule`): sv_score, and the last row epilogue
+    of each sequence runs the per-row schedule.  Bit-identical to sv_score + sv_schedule."""
+    B, k, V = D.shape
+    dev = D.device
+    if profile is None:
+        raise SvError("sv_score_schedule needs a profile (p_hat drives the schedule)")
+    if latency.dtype != torch.float64:
+        raise SvError("latency table must be float64")
+    if workspace is None:
+        workspace = new_workspace(B, k, V, D.dtype, dev)
+    o = out or {}
+    f = lambda name: o.get(name) if name in o else torch.empty((B, k), dtype=torch.float32, device=dev)  # noqa: E731
+    res = {n: f(n) for n in ("S", "A", "KL", "p_hat", "draft_m", "draft_l", "draft_ptok")}
+    res["status"] = o.get("status") if "status" in o else torch.empty((B, k), dtype=torch.int32, device=dev)
+    so = sched_out or {}
+    sch = {"gamma": so.get("gamma") if "gamma" in so else torch.empty(B, dtype=torch.int32, device=dev),
+           "exp_accept": so.get("exp_accept") if "exp_accept" in so else torch.empty(B, dtype=torch.float32,
+                                                                                      device=dev),
+           "goodput": so.get("goodput") if "goodput" in so else torch.empty(B, dtype=torch.float32, device=dev),
+           "status": so.get("status") if "status" in so else torch.empty(B, dtype=torch.int32, device=dev)}
+    st = _lib.load().sv_score_schedule(
+        ctypes.byref(_logits(D)), ctypes.byref(_logits(C)), _ptr(tok), B, k, V, float(tau_d), float(tau_c),
+        ctypes.byref(profile.c), _ptr(res["S"]), _ptr(res["A"]), _ptr(res["KL"]), _ptr(res["p_hat"]),
+        _ptr(res["draft_m"]), _ptr(res["draft_l"]), _ptr(res["draft_ptok"]), _ptr(res["status"]), _ptr(latency),
+        latency.numel(), int(plus_one), _ptr(sch["gamma"]), _ptr(sch["exp_accept"]), _ptr(sch["goodput"]),
+        _ptr(sch["status"]), workspace.data_ptr(), workspace.numel(), _stream(stream))
+    _lib.check(st, "sv_score_schedule")
+    return res, sch
 
 
 def sv_schedule(p_hat, latency, mode=SV_SCHED_PER_ROW, plus_one=1, out=None, stream=None) -> dict:
@@ -280,9 +313,13 @@ class GraphPipeline:
 
     def _step(self, stream):
         p = self.pipe
-        sc = sv_score(self.D, self.C, self.tok, p.tau_d, p.tau_c, p.profile, workspace=p.workspace, out=p.score_out,
-                      stream=stream)
-        sh = sv_schedule(sc["p_hat"], p.latency, p.mode, 1, out=p.sched_out, stream=stream)
+        if p.mode == SV_SCHED_PER_ROW and p.fused:
+            sc, sh = sv_score_schedule(self.D, self.C, self.tok, p.latency, p.tau_d, p.tau_c, p.profile,
+                                       workspace=p.workspace, out=p.score_out, sched_out=p.sched_out, stream=stream)
+        else:
+            sc = sv_score(self.D, self.C, self.tok, p.tau_d, p.tau_c, p.profile, workspace=p.workspace,
+                          out=p.score_out, stream=stream)
+            sh = sv_schedule(sc["p_hat"], p.latency, p.mode, 1, out=p.sched_out, stream=stream)
         r = sd_verify_ragged(self.D, self.T.view(-1, self.V), self.rowptr, self.tok, sh["gamma"], sc["draft_m"],
                              sc["draft_l"], sc["draft_ptok"], p.tau_d, p.tau_t, self.seed, 0, self.offset,
                              self.seq_base, workspace=p.workspace, out=p.ver_out, stream=stream)
@@ -332,8 +369,18 @@ class Pipeline:
         self.workspace = new_workspace(B, k, V, dtype, device)
         self.forced_gamma = torch.empty(B, **i32)
         self._forced = None
+        # sv_score_schedule (K3 folded into K1's last row epilogue) measured ~1.5 us SLOWER per step
+        # than sv_score + a PDL-overlapped sv_schedule at every config; SV_FUSED_SCHED=1 opts in
+        self.fused = os.environ.get("SV_FUSED_SCHED", "0") == "1"
 
     def run(self, D, C, T, tok, seed=0, offset=0, seq_base=0, force_gamma=None, stream=None):
+        if force_gamma is None and self.mode == SV_SCHED_PER_ROW and self.fused:
+            sc, sh = sv_score_schedule(D, C, tok, self.latency, self.tau_d, self.tau_c, self.profile,
+                                       workspace=self.workspace, out=self.score_out, sched_out=self.sched_out,
+                                       stream=stream)
+            return sd_verify(D, T, tok, sh["gamma"], sc["draft_m"], sc["draft_l"], sc["draft_ptok"], self.tau_d,
+                             self.tau_t, seed, offset, seq_base, workspace=self.workspace, out=self.ver_out,
+                             stream=stream)
         sc = sv_score(D, C, tok, self.tau_d, self.tau_c, self.profile, workspace=self.workspace, out=self.score_out,
                       stream=stream)
         if force_gamma is None:

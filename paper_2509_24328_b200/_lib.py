@@ -19,7 +19,7 @@ EXPORTS = ("sv_workspace_bytes", "sv_status_string", "sv_cluster_size", "sv_scor
            "sv_shard_xch_bytes", "sv_shard_score_p1", "sv_shard_score_p2", "sv_shard_score_finish",
            "sv_shard_verify_p1", "sv_shard_verify_p2", "sv_shard_verify_finish", "sd_verify_ragged",
            "sv_profile_workspace_bytes", "sv_profile_build", "sv_filter_workspace_bytes", "sv_score_filtered",
-           "sd_verify_filtered")
+           "sd_verify_filtered", "sv_score_schedule")
 
 
 class SvLogits(ctypes.Structure):
@@ -63,6 +63,9 @@ def load(path: str = LIB_PATH):
     lib.sv_score.argtypes = [LP, LP, P, i32, i32, i32, f32, f32, ctypes.POINTER(SvProfile),
                              P, P, P, P, P, P, P, P, P, sz, P]
     lib.sv_score.restype = i32
+    lib.sv_score_schedule.argtypes = [LP, LP, P, i32, i32, i32, f32, f32, ctypes.POINTER(SvProfile),
+                                      P, P, P, P, P, P, P, P, P, i32, i32, P, P, P, P, P, sz, P]
+    lib.sv_score_schedule.restype = i32
     lib.sv_schedule.argtypes = [P, i32, i32, P, i32, i32, i32, P, P, P, P, P, sz, P]
     lib.sv_schedule.restype = i32
     lib.sd_verify.argtypes = [LP, LP, P, P, P, P, P, i32, i32, i32, f32, f32, u64, u64, i64,

@@ -87,8 +87,8 @@ static int64_t rows_chunk_for(int elem_bytes) {
   return (int64_t)32 * kRowUnitsPerThread * (16 / elem_bytes);
 }
 
-int64_t score_ws_bytes(int64_t rows, int cs) {
-  return ws_round(rows * cs * 5 * 8) + ws_round(rows * cs * 4) + ws_round(rows * 2 * 4);
+int64_t score_ws_bytes(int64_t rows, int cs) {  // + per-sequence counters (<= rows sequences)
+  return ws_round(rows * cs * 5 * 8) + ws_round(rows * cs * 4) + ws_round(rows * 2 * 4) + ws_round(rows * 4);
 }
 
 }  // namespace sv
@@ -234,10 +234,11 @@ int32_t sv_cluster_size(int32_t V, int32_t dtype) {
   return cluster_size_for(V, elem_bytes(dtype));
 }
 
-int32_t sv_score(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok, int32_t B, int32_t k,
-                 int32_t V, float tau_d, float tau_c, const sv_profile *prof, float *S, float *A, float *KL,
-                 float *p_hat, float *draft_m, float *draft_l, float *draft_ptok, int32_t *row_status,
-                 void *workspace, size_t workspace_bytes, void *stream) {
+static int32_t score_impl(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok, int32_t B,
+                          int32_t k, int32_t V, float tau_d, float tau_c, const sv_profile *prof, float *S, float *A,
+                          float *KL, float *p_hat, float *draft_m, float *draft_l, float *draft_ptok,
+                          int32_t *row_status, void *workspace, size_t workspace_bytes, void *stream,
+                          const ScheduleArgs *sch) {
   if (!draft) return SV_ERR_INVALID_ARG;
   int32_t r = shape_check(B, k, V, draft->dtype);
   if (r != SV_OK) return r;
@@ -260,12 +261,49 @@ int32_t sv_score(const sv_logits *draft, const sv_logits *comp, const int32_t *d
   a.part = reinterpret_cast<double *>(ws);
   a.spart = reinterpret_cast<float *>(ws + ws_round(rows * a.cs * 5 * 8));
   a.cnt = reinterpret_cast<uint32_t *>(ws + ws_round(rows * a.cs * 5 * 8) + ws_round(rows * a.cs * 4));
+  a.seq_cnt = reinterpret_cast<uint32_t *>(ws + ws_round(rows * a.cs * 5 * 8) + ws_round(rows * a.cs * 4) +
+                                           ws_round(rows * 2 * 4));
+  if (sch) {
+    a.fuse_sched = 1;
+    a.sch = *sch;
+  }
   cudaError_t e = launch_score(a, (cudaStream_t)stream);
   if (e != cudaSuccess) {
-    fprintf(stderr, "libsv: sv_score launch failed: %s\n", cudaGetErrorString(e));
+    fprintf(stderr, "libsv: sv_score%s launch failed: %s\n", sch ? "_schedule" : "", cudaGetErrorString(e));
     return SV_ERR_CUDA;
   }
   return SV_OK;
+}
+
+int32_t sv_score(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok, int32_t B, int32_t k,
+                 int32_t V, float tau_d, float tau_c, const sv_profile *prof, float *S, float *A, float *KL,
+                 float *p_hat, float *draft_m, float *draft_l, float *draft_ptok, int32_t *row_status,
+                 void *workspace, size_t workspace_bytes, void *stream) {
+  return score_impl(draft, comp, draft_tok, B, k, V, tau_d, tau_c, prof, S, A, KL, p_hat, draft_m, draft_l, draft_ptok,
+                    row_status, workspace, workspace_bytes, stream, nullptr);
+}
+
+int32_t sv_score_schedule(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok, int32_t B, int32_t k,
+                          int32_t V, float tau_d, float tau_c, const sv_profile *prof, float *S, float *A, float *KL,
+                          float *p_hat, float *draft_m, float *draft_l, float *draft_ptok, int32_t *row_status,
+                          const double *latency, int32_t n_lat, int32_t plus_one, int32_t *gamma, float *exp_accept,
+                          float *goodput, int32_t *sched_status, void *workspace, size_t workspace_bytes,
+                          void *stream) {
+  if (!p_hat || !latency || !gamma || n_lat < k + 2 || k < 1 || k > SV_MAX_K) return SV_ERR_INVALID_ARG;
+  ScheduleArgs sa = {};
+  sa.p_hat = p_hat;
+  sa.B = B;
+  sa.k = k;
+  sa.L = latency;
+  sa.n_lat = n_lat;
+  sa.mode = SV_SCHED_PER_ROW;
+  sa.plus_one = plus_one ? 1 : 0;
+  sa.gamma = gamma;
+  sa.exp_accept = exp_accept;
+  sa.goodput = goodput;
+  sa.status = sched_status;
+  return score_impl(draft, comp, draft_tok, B, k, V, tau_d, tau_c, prof, S, A, KL, p_hat, draft_m, draft_l, draft_ptok,
+                    row_status, workspace, workspace_bytes, stream, &sa);
 }
 
 int32_t sv_schedule(const float *p_hat, int32_t B, int32_t k, const double *latency, int32_t n_lat, int32_t mode,

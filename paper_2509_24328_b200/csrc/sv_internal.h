@@ -55,6 +55,16 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
 
 __host__ __device__ inline int64_t ws_round(int64_t x) { return (x + 255) / 256 * 256; }
 
+struct ScheduleArgs {
+  const float *p_hat;
+  int32_t B, k;
+  const double *L;
+  int32_t n_lat, mode, plus_one;
+  int32_t *gamma;
+  float *exp_accept, *goodput;
+  int32_t *status;
+  void *ws;
+};
 struct ScoreArgs {
   const void *d, *c;
   int64_t d_sb, d_si, c_sb, c_si;
@@ -72,6 +82,10 @@ struct ScoreArgs {
   double *part;     // workspace: [B k cs][5] P1 partials (M_d, L_d, M_c, L_c, W)
   float *spart;     // workspace: [B k cs] S partials
   uint32_t *cnt;    // workspace: [B k][2] counters, zero between calls (self-cleaning)
+  // sv_score_schedule: the last row epilogue of each sequence runs step a4 (K3 folded in)
+  int fuse_sched;
+  uint32_t *seq_cnt;  // workspace: [B] per-sequence row counters, zero between calls
+  ScheduleArgs sch;
 };
 // sv_score's share of the workspace (offset 0); sd_verify's follows it
 int64_t score_ws_bytes(int64_t rows, int cs);
@@ -92,16 +106,6 @@ struct ShardScoreArgs {
 };
 cudaError_t launch_shard_score(const ShardScoreArgs &h, const ScoreArgs &a, cudaStream_t st);
 
-struct ScheduleArgs {
-  const float *p_hat;
-  int32_t B, k;
-  const double *L;
-  int32_t n_lat, mode, plus_one;
-  int32_t *gamma;
-  float *exp_accept, *goodput;
-  int32_t *status;
-  void *ws;
-};
 cudaError_t launch_schedule(const ScheduleArgs &a, cudaStream_t st);
 
 // Per-sequence verification decision (K4's last CTA of the sequence -> K5).

@@ -14,66 +14,18 @@
 
 #include "sv_device.cuh"
 #include "sv_internal.h"
+#include "sv_schedule.cuh"
 
 namespace sv {
 
 namespace {
-
-constexpr int kMaxK = 16;  // SV_MAX_K
-
-__device__ __forceinline__ double phat_val(float v, int &st) {
-  if (!(fabsf(v) <= FLT_MAX)) {  // NaN / inf -> 0 (SV_ROW_PHAT_BAD)
-    st |= 16;
-    return 0.0;
-  }
-  return (double)v;
-}
 
 __global__ void __launch_bounds__(128) sv_schedule_row_kernel(const __grid_constant__ ScheduleArgs a) {
   pdl_wait();
   pdl_trigger();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= a.B) return;
-  const int k = a.k, po = a.plus_one ? 1 : 0;
-  // all loads up front (k <= SV_MAX_K): the fp64 chain below then never waits on memory
-  float ph[kMaxK];
-  double Lj[kMaxK + 1];
-#pragma unroll
-  for (int j = 0; j < kMaxK; ++j) ph[j] = j < k ? a.p_hat[(int64_t)b * k + j] : 0.f;
-#pragma unroll
-  for (int j = 0; j <= kMaxK; ++j) Lj[j] = j <= k ? a.L[j + po] : 1.0;
-  int st = 0;
-#pragma unroll
-  for (int j = 0; j <= kMaxK; ++j) {
-    if (j <= k && (!(Lj[j] > 0.0) || !(Lj[j] <= DBL_MAX))) st |= 128;  // SV_ROW_BAD_LATENCY
-  }
-  if (st) {
-    a.gamma[b] = 0;
-    if (a.exp_accept) a.exp_accept[b] = 0.f;
-    if (a.goodput) a.goodput[b] = __int_as_float(0x7fc00000);
-    if (a.status) a.status[b] = st;
-    return;
-  }
-  double P = 1.0, E = 0.0;
-  double best_g = __ddiv_rn(po ? 1.0 : 0.0, Lj[0]);
-  double best_E = 0.0;
-  int best = 0;
-#pragma unroll
-  for (int j = 1; j <= kMaxK; ++j) {
-    if (j > k) break;
-    P = __dmul_rn(P, phat_val(ph[j - 1], st));
-    E = __dadd_rn(E, P);
-    const double g = __ddiv_rn(po ? __dadd_rn(E, 1.0) : E, Lj[j]);
-    if (g > best_g) {
-      best_g = g;
-      best_E = E;
-      best = j;
-    }
-  }
-  a.gamma[b] = best;
-  if (a.exp_accept) a.exp_accept[b] = (float)best_E;
-  if (a.goodput) a.goodput[b] = (float)best_g;
-  if (a.status) a.status[b] = st;
+  schedule_one(a, b);
 }
 
 }  // namespace

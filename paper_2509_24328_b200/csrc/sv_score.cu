@@ -24,6 +24,7 @@
 
 #include "sv_device.cuh"
 #include "sv_internal.h"
+#include "sv_schedule.cuh"
 
 namespace sv {
 
@@ -531,6 +532,15 @@ __device__ __forceinline__ void p2_finish(const ScoreArgs &a, const Task &k, flo
   if (lane == 0) {
     cnt[0] = 0u;  // every P1 / P2 task of this row is past its use of the counters
     cnt[1] = 0u;
+    if (a.fuse_sched) {  // the sequence's last row runs step a4 (sv_score_schedule)
+      __threadfence();   // this row's p_hat before the count
+      const uint32_t old = atomicAdd(a.seq_cnt + k.bb, 1u);
+      if (old == (uint32_t)a.k - 1u) {
+        __threadfence();  // the other rows' p_hat
+        a.seq_cnt[k.bb] = 0u;
+        schedule_one(a.sch, k.bb);
+      }
+    }
   }
 }
 

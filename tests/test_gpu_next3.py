@@ -65,3 +65,31 @@ def test_graph_replay_matches_eager(sv):
         for n in ref:
             assert _eq(out[n], ref[n]), (j, n)
     assert int(gp.offset.item()) == 13
+
+
+@pytest.mark.parametrize("B,k,V,dtype", [(80, 8, 32000, "bf16"), (1, 1, 4096, "f32"), (5, 16, 1001, "f32"),
+                                         (3, 8, 152064, "bf16")])
+def test_score_schedule_fused_matches_separate(sv, B, k, V, dtype):
+    """sv_score_schedule (K3 folded into K1's last row epilogue) == sv_score + sv_schedule, bitwise."""
+    x = synth.make_inputs(B, k, V, dtype, seed=808 + V + k)
+    D, C, T, tok = H.to_torch(x)
+    prof = sv.Profile.from_dict(synth.load_profile())
+    L = torch.tensor(synth.latency_table(k + 2), dtype=torch.float64, device="cuda")
+    ws = sv.new_workspace(B, k, V, D.dtype)
+    sc = sv.sv_score(D, C, tok, 1.0, 1.0, prof, workspace=ws)
+    sh = sv.sv_schedule(sc["p_hat"], L)
+    fc, fh = sv.sv_score_schedule(D, C, tok, L, 1.0, 1.0, prof, workspace=ws)
+    torch.cuda.synchronize()
+    for n in sc:
+        if sc[n] is not None:
+            assert _eq(sc[n], fc[n]), n
+    for n in sh:
+        assert _eq(sh[n], fh[n]), n
+    # a bad latency entry: every sequence flagged, as the separate kernel does
+    Lbad = L.clone()
+    Lbad[2] = -1.0
+    sh = sv.sv_schedule(sc["p_hat"], Lbad)
+    fc, fh = sv.sv_score_schedule(D, C, tok, Lbad, 1.0, 1.0, prof, workspace=ws)
+    torch.cuda.synchronize()
+    for n in sh:
+        assert _eq(sh[n], fh[n]), n
