@@ -63,8 +63,14 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// Bounded: the producers are CTAs with lower linear indices (dispatched first), so the count is
+// always reached unless the workspace invariant is broken (counters not zero at entry); then the
+// kernel traps (a CUDA error the caller sees) instead of spinning forever.
 __device__ __forceinline__ void wait_count(const uint32_t *p, uint32_t target) {
-  while (ld_acquire(p) < target) __nanosleep(100);
+  for (uint32_t n = 0; ld_acquire(p) < target; ++n) {
+    if (n > (1u << 26)) __trap();
+    __nanosleep(100);
+  }
 }
 
 // ---------------------------------------------------------------- element arithmetic
