@@ -481,6 +481,24 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     f_ms_step = f0.elapsed_time(f1) / f_steps
 
+    # ---------------- NEXT-1: the paper's batch greedy schedule (one CTA: gains, bitonic sort,
+    # greedy walk) on this step's p_hat, latency L[n] over the batch's total target positions
+    Lg = torch.tensor(synth.latency_table(B * (k + 1) + 1, base=4.0, knee=2 * B, slope=4.0 / B),
+                      dtype=torch.float64, device=dev)
+    gout = {"gamma": torch.empty(B, dtype=torch.int32, device=dev), "exp_accept": torch.empty(B, device=dev),
+            "goodput": torch.empty(B, device=dev), "status": torch.empty(B, dtype=torch.int32, device=dev)}
+    for _ in range(args.warmup):
+        sv.sv_schedule(pipe.score_out["p_hat"], Lg, sv.SV_SCHED_BATCH_GREEDY, 1, out=gout, stream=stream)
+    barrier()
+    q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    q0.record(stream)
+    for _ in range(50):
+        sv.sv_schedule(pipe.score_out["p_hat"], Lg, sv.SV_SCHED_BATCH_GREEDY, 1, out=gout, stream=stream)
+    q1.record(stream)
+    barrier()
+    greedy_us = q0.elapsed_time(q1) / 50 * 1e3
+    greedy_mean_gamma = float(gout["gamma"].float().mean().item())
+
     # ---------------- NEXT-4: GPU profile builder on a 65,536-record profiling run (P L176,
     # S L331's run size): records = this step's (S, A, accept_ratio) with gamma = k, tiled
     ver_full = pipe.ver_out
@@ -590,6 +608,9 @@ def run_ours(args, rank, world, local_rank):
                          "filters": "top_k 20, top_p 0.8, tau 0.7 on draft / companion / target (P L731-743)",
                          "note": "NEXT-2: radix-select top-k per row + list arithmetic; output allocations per "
                                  "call included"},
+            "batch_greedy": {"us_per_call": greedy_us, "mean_gamma": greedy_mean_gamma,
+                             "latency": f"L[n] = 4 + (4/B) max(0, n - 2B) over the batch's target positions",
+                             "note": "NEXT-1 sv_schedule mode BATCH_GREEDY on the step's p_hat (B*k candidates)"},
             "profile_build": {"records": n_rec, "ms": prof_ms, "bins": "20 x 15, X in 10 bins",
                               "note": "NEXT-4 offline builder (sv_profile_build), incl. its host sync for the "
                                       "kept-bin counts"},

@@ -30,17 +30,23 @@ __global__ void __launch_bounds__(kGreedyThreads) sv_greedy_kernel(const Schedul
   pdl_trigger();
   extern __shared__ __align__(16) uint8_t smem[];
   double *g = reinterpret_cast<double *>(smem);
-  int *id = reinterpret_cast<int *>(g + npow2);
+  double *Ls = g + npow2 + 2;                        // L[B .. B + N + 1]: the walk's latencies
+  float *ph = reinterpret_cast<float *>(Ls + npow2 + 2);  // p_hat staged once
+  int *id = reinterpret_cast<int *>(ph + npow2);
   __shared__ int s_stop;
   __shared__ double s_G;
   const int B = a.B, k = a.k, N = B * k, tid = threadIdx.x;
 
+  // (0) stage p_hat and the latencies the walk can reach (coalesced, all threads)
+  for (int x = tid; x < N; x += blockDim.x) ph[x] = a.p_hat[x];
+  for (int x = tid; x <= N + 1; x += blockDim.x) Ls[x] = (int64_t)B + x < a.n_lat ? a.L[B + x] : 1.0;
+  __syncthreads();
   // (1) gains: per-sequence prefix products (thread per sequence, sequential fp64)
   for (int q = tid; q < B; q += blockDim.x) {
     double P = 1.0;
     int st = 0;
     for (int j = 0; j < k; ++j) {
-      float v = a.p_hat[(int64_t)q * k + j];
+      float v = ph[q * k + j];
       if (!(fabsf(v) <= FLT_MAX)) {
         v = 0.f;
         st |= 16;
@@ -77,24 +83,35 @@ __global__ void __launch_bounds__(kGreedyThreads) sv_greedy_kernel(const Schedul
       __syncthreads();
     }
   }
-  // (3) walk the sorted prefix with the greedy's stop rule
+  // (3) the greedy's stop rule on the sorted prefix: the running numerators B + G_m in the
+  //     greedy's own association (one thread, sequential fp64, written over the sorted gains),
+  //     then every
+  //     goodput (B + G_m) / L[B + m] in parallel and the first m whose successor is not strictly
+  //     better (block min).  Identical operations to the sequential walk, so identical bits.
   if (tid == 0) {
     double num = 0.0;
     for (int q = 0; q < B; ++q) num = __dadd_rn(num, 1.0);
-    int64_t n = B;
-    double G = __ddiv_rn(num, a.L[n]);
-    int m = 0;
-    while (m < N && n + 1 < a.n_lat) {
-      const double num2 = __dadd_rn(num, g[m]);
-      const double G2 = __ddiv_rn(num2, a.L[n + 1]);
-      if (!(G2 > G)) break;
-      num = num2;
-      G = G2;
-      ++n;
-      ++m;
+    double prev = g[0];
+    g[0] = num;  // g[m] <- numerator before candidate m (g has npow2 + 2 slots)
+    for (int m = 0; m < N; ++m) {
+      const double gm = prev;
+      prev = g[m + 1];
+      num = __dadd_rn(num, gm);
+      g[m + 1] = num;
     }
-    s_stop = m;
-    s_G = G;
+    s_stop = N;  // default: every candidate taken (or the latency table ends first)
+  }
+  __syncthreads();
+  const int mmax = (int)min((int64_t)N, (int64_t)a.n_lat - 1 - B);  // n + 1 < n_lat
+  for (int m = tid; m < mmax; m += blockDim.x) {
+    const double G = __ddiv_rn(g[m], Ls[m]), G2 = __ddiv_rn(g[m + 1], Ls[m + 1]);
+    if (!(G2 > G)) atomicMin(&s_stop, m);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const int stop = min(s_stop, mmax < 0 ? 0 : mmax);
+    s_stop = stop;
+    s_G = __ddiv_rn(g[stop], Ls[stop]);
   }
   __syncthreads();
   // (4) per-sequence gamma and E (selected gains of a sequence are its first gamma_q
@@ -105,7 +122,7 @@ __global__ void __launch_bounds__(kGreedyThreads) sv_greedy_kernel(const Schedul
     for (int x = 0; x < stop; ++x) gam += (id[x] / k == q) ? 1 : 0;
     double E = 0.0, P = 1.0;
     for (int j = 0; j < gam; ++j) {
-      float v = a.p_hat[(int64_t)q * k + j];
+      float v = ph[q * k + j];
       if (!(fabsf(v) <= FLT_MAX)) v = 0.f;
       P = __dmul_rn(P, (double)v);
       E = __dadd_rn(E, P);
@@ -122,9 +139,16 @@ cudaError_t launch_schedule_greedy(const ScheduleArgs &a, cudaStream_t st) {
   int npow2 = 1;
   while (npow2 < a.B * a.k) npow2 <<= 1;
   if (npow2 > kGreedyMax) return cudaErrorInvalidValue;
-  const size_t smem = (size_t)npow2 * (sizeof(double) + sizeof(int));
-  cudaError_t e = cudaFuncSetAttribute(sv_greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  const size_t smem = (size_t)npow2 * (2 * sizeof(double) + sizeof(float) + sizeof(int)) + 4 * sizeof(double);
+  // raise the shared-memory opt-in once per device and size (a host API call, not per launch)
+  static size_t attr_smem[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || smem > attr_smem[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(sv_greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64) attr_smem[dev] = smem;
+  }
   return launch_k(sv_greedy_kernel, dim3(1), dim3(kGreedyThreads), smem, st, a, npow2);
 }
 

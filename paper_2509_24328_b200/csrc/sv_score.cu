@@ -736,11 +736,13 @@ cudaError_t launch_score_tma(const ScoreArgs &a, cudaStream_t st) {
   if (tasks == 0) return cudaSuccess;
   const int smem = NS * 2 * SU * kScoreThreads * 16;
   auto fn = sv_score_tma_kernel<T, SU, NS, MINB>;
-  static bool attr_done = false;  // per instantiation
-  if (!attr_done) {
+  static bool attr_done[64] = {};  // per instantiation and device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr_done[dev]) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    attr_done = true;
+    if (dev >= 0 && dev < 64) attr_done[dev] = true;
   }
   return launch_k(fn, dim3((unsigned)tasks), dim3(kScoreThreads + 32), smem, st, a);
 }
