@@ -63,6 +63,7 @@ typedef enum { SV_F32 = 0, SV_BF16 = 1 } sv_dtype;
 #define SV_ROW_RESID_ZERO  32  /* rejected but residual mass Z = 0: sampled p_t (R10) */
 #define SV_ROW_BAD_GAMMA   64  /* gamma outside [0, k]                               */
 #define SV_ROW_BAD_LATENCY 128 /* a latency entry used by the schedule is <= 0 / NaN */
+#define SV_ROW_FILTER_UNSUPPORTED 256 /* nucleus-only filter with more than 32 tokens */
 
 /* A [B, rows, V] logit tensor: element (b, i, v) is at ptr + b*stride_b + i*stride_i + v
  * (strides in ELEMENTS).  dtype: sv_dtype. */
@@ -236,8 +237,9 @@ SV_API int32_t sd_verify_ragged(const sv_logits *draft, const void *target, int6
  * keeps the top_k largest logits, ties to the lower vocabulary index; top_p keeps the shortest
  * prefix of the top-k distribution (probability desc, index asc) whose sequential fp64
  * cumulative mass is >= top_p.  Supported: 1 <= top_k <= 32 (each filtered distribution has at
- * most 32 entries), 0 < top_p <= 1; top_p without top_k (full-vocabulary nucleus) returns
- * SV_ERR_UNSUPPORTED.
+ * most 32 entries), 0 < top_p <= 1; and top_k = 0 with top_p < 1 (nucleus over the FULL
+ * distribution, the paper's Llama setting) whenever the nucleus has at most 32 tokens -- rows
+ * whose nucleus is larger get SV_ROW_FILTER_UNSUPPORTED and the error sentinels.
  *
  * sv_score_filtered: S, A, KL, p_hat, draft_ptok (= p'_d(t)), row_status [B, k] as sv_score but
  * over the filtered distributions (KL = +inf when the draft keeps a token the companion

@@ -14,6 +14,7 @@ SV_F32, SV_BF16 = 0, 1
 SV_SCHED_PER_ROW, SV_SCHED_BATCH_GREEDY = 0, 1
 ROW_NAN, ROW_ALL_NEG_INF, ROW_BAD_TOKEN, ROW_DRAFT_ZERO = 1, 2, 4, 8
 ROW_PHAT_BAD, ROW_RESID_ZERO, ROW_BAD_GAMMA, ROW_BAD_LATENCY = 16, 32, 64, 128
+ROW_FILTER_UNSUPPORTED = 256
 
 EXPORTS = ("sv_workspace_bytes", "sv_status_string", "sv_cluster_size", "sv_score", "sv_schedule", "sd_verify",
            "sv_shard_xch_bytes", "sv_shard_score_p1", "sv_shard_score_p2", "sv_shard_score_finish",

@@ -408,8 +408,9 @@ size_t sv_filter_workspace_bytes(int32_t B, int32_t k) {
 
 static int32_t filter_check(const sv_filter *f) {
   if (!f) return SV_ERR_INVALID_ARG;
-  if (f->top_k < 1 || f->top_k > 32) return SV_ERR_UNSUPPORTED;  // full-vocabulary top-p: not built
   if (!(f->top_p > 0.f) || f->top_p > 1.f) return SV_ERR_INVALID_ARG;
+  if (f->top_k < 0 || f->top_k > 32) return SV_ERR_UNSUPPORTED;
+  if (f->top_k == 0 && !(f->top_p < 1.f)) return SV_ERR_INVALID_ARG;  // no filter at all: use sv_score
   return SV_OK;
 }
 

@@ -43,9 +43,10 @@ template <> struct KeyOf<__nv_bfloat16> {
     return (b & 0x8000u) ? (~b & 0xFFFFu) : (b | 0x8000u);
   }
   __device__ static bool bad(K k) { return k >= 0xFF80u; }  // +inf or NaN (R18)
-  __device__ static float value(K k) {
+  __device__ static float value(K k) { return __uint_as_float(value_bits(k)); }
+  __device__ static uint32_t value_bits(K k) {  // fp32 bits of the logit of key k
     const uint32_t b = (k & 0x8000u) ? (k & 0x7FFFu) : (~k & 0xFFFFu);
-    return __uint_as_float(b << 16);
+    return b << 16;
   }
 };
 template <> struct KeyOf<float> {
@@ -56,9 +57,8 @@ template <> struct KeyOf<float> {
     return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
   }
   __device__ static bool bad(K k) { return k >= 0xFF800000u; }
-  __device__ static float value(K k) {
-    return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
-  }
+  __device__ static float value(K k) { return __uint_as_float(value_bits(k)); }
+  __device__ static uint32_t value_bits(K k) { return (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k; }
 };
 
 // Row r of the set the launch processes (draft / companion rows for the score, target rows
@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
   __shared__ int s_tie[kTieCap];
   __shared__ unsigned long long s_cand[kCandCap];
   __shared__ uint32_t s_gmax[kTopKThreads / 16];
+  __shared__ double s_lsum[kTopKThreads / 32], s_lfull;
   __shared__ int s_ncand;
   __shared__ K c_key[32];
   __shared__ int c_idx[32];
@@ -104,7 +105,10 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
   if (!row_of(a, blockIdx.x, which, base, off, out)) return;
   const T *x = reinterpret_cast<const T *>(base) + off;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int V = a.V, KK = min(a.top_k, V);
+  // top_k = 0: nucleus-only (top_p over the FULL distribution), supported when the nucleus has
+  // at most 32 tokens -- the 32 largest are selected and the full-row normaliser is added below
+  const bool nucleus = a.top_k == 0;
+  const int V = a.V, KK = min(nucleus ? 32 : a.top_k, V);
   if (tid == 0) {
     s_prefix = 0;
     s_mask = 0;
@@ -298,6 +302,29 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
     }
     __syncthreads();
   }
+  const double tau = (double)(which == 0 ? a.tau_d : which == 1 ? a.tau_c : a.tau_t);
+  if (nucleus) {  // full-row normaliser sum_v 2^{(x_v - x_max) log2e / tau} (L2 pass, fp64 block sum)
+    K kmax = c_key[0];
+    for (int j = 1; j < KK; ++j) kmax = c_key[j] > kmax ? c_key[j] : kmax;
+    const float xmax = KO::value(kmax), c2 = (float)(1.4426950408889634 / tau);
+    float lsum = 0.f;
+    if (xmax > -FLT_MAX) {
+      const float nm = -xmax * c2;
+      for (int e = tid; e < V; e += NT) {
+        const float xv = __uint_as_float(KO::value_bits(KO::key(x, e)));
+        lsum += ex2(fmaf(xv, c2, nm));
+      }
+    }
+    double v = warp_sum_d((double)lsum);
+    if (lane == 0) s_lsum[wid] = v;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < NT / 32; ++w) t += s_lsum[w];
+      s_lfull = t;
+    }
+    __syncthreads();
+  }
   if (wid != 0) return;
   // ---- sort by (key desc, index asc), softmax (fp64), top_p, renormalise
   const K mk = lane < KK ? c_key[lane] : (K)0;
@@ -314,25 +341,29 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
     c_idx[rank] = mi;
   }
   __syncwarp();
-  const double tau = (double)(which == 0 ? a.tau_d : which == 1 ? a.tau_c : a.tau_t);
   const double y = lane < KK ? (double)KO::value(c_key[lane]) / tau : -INFINITY;
   const double y0 = __shfl_sync(0xffffffffu, y, 0);
   int st = s_bad ? 1 /*SV_ROW_NAN*/ : 0;
   if (!st && !(y0 > -INFINITY)) st = 2; /*SV_ROW_ALL_NEG_INF*/
   double p = (lane < KK && !st) ? exp(y - y0) : 0.0;
-  double tot = 0.0;  // sequential in sorted order (the oracle's order)
-  for (int l = 0; l < KK; ++l) tot += __shfl_sync(0xffffffffu, p, l);
+  double tot = 0.0;  // sequential in sorted order (the oracle's order); nucleus: the full row
+  if (nucleus) tot = s_lfull;
+  else
+    for (int l = 0; l < KK; ++l) tot += __shfl_sync(0xffffffffu, p, l);
   p = p / tot;
   int n = KK;
   if (a.top_p < 1.f) {
     double c = 0.0;
+    bool cut = false;
     for (int l = 0; l < KK; ++l) {
       c += __shfl_sync(0xffffffffu, p, l);
       if (c >= (double)a.top_p) {
         n = l + 1;
+        cut = true;
         break;
       }
     }
+    if (nucleus && !cut && !st) st = 256; /*SV_ROW_FILTER_UNSUPPORTED: nucleus > 32 tokens*/
     double s = 0.0;
     for (int l = 0; l < n; ++l) s += __shfl_sync(0xffffffffu, p, l);
     p = p / s;

@@ -85,9 +85,10 @@ def test_host_validation_of_the_widened_abi(lib):
     from paper_2509_24328_b200 import _lib
     P = ctypes.c_void_p(16)  # a non-NULL dummy: validation fails before any dereference
     L = _lib.SvLogits(16, _lib.SV_BF16, 0, 0, 0)
-    # filters: top_k 0 (nucleus only) and 33 are unsupported, top_p outside (0, 1] invalid
-    for top_k, top_p, want in ((0, 0.9, _lib.SV_ERR_UNSUPPORTED), (33, 0.9, _lib.SV_ERR_UNSUPPORTED),
-                               (20, 0.0, _lib.SV_ERR_INVALID_ARG), (20, 1.5, _lib.SV_ERR_INVALID_ARG)):
+    # filters: top_k outside [0, 32] unsupported, top_p outside (0, 1] or no filter at all invalid
+    for top_k, top_p, want in ((-1, 0.9, _lib.SV_ERR_UNSUPPORTED), (33, 0.9, _lib.SV_ERR_UNSUPPORTED),
+                               (0, 1.0, _lib.SV_ERR_INVALID_ARG), (20, 0.0, _lib.SV_ERR_INVALID_ARG),
+                               (20, 1.5, _lib.SV_ERR_INVALID_ARG)):
         f = _lib.SvFilter(top_k, top_p)
         st = lib.sv_score_filtered(ctypes.byref(L), ctypes.byref(L), P, 2, 2, 100, 1.0, 1.0, ctypes.byref(f), None,
                                    None, None, None, None, None, None, P, 1 << 20, None)

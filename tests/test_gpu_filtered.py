@@ -71,9 +71,70 @@ def test_filtered_parity(sv, B, k, V, dtype, top_k, top_p, tau):
     print("ties:", int(tie.sum()))
 
 
-def test_filtered_unsupported_nucleus_only(sv):
+def test_filtered_bad_configs(sv):
     B, k, V = 2, 2, 64
     x = synth.make_inputs(B, k, V, "f32", seed=1)
     D, C, T, tok = H.to_torch(x)
-    with pytest.raises(sv.SvError):
-        sv.sv_score_filtered(D, C, tok, 0, 0.9)
+    for top_k, top_p in ((33, 0.9), (0, 1.0), (20, 0.0)):
+        with pytest.raises(sv.SvError):
+            sv.sv_score_filtered(D, C, tok, top_k, top_p)
+
+
+@pytest.mark.parametrize("V,dtype,tau", [(32000, "f32", 0.6), (32000, "bf16", 0.6), (4096, "bf16", 1.0)])
+def test_nucleus_only_llama_setting(sv, V, dtype, tau):
+    """top_k = 0, top_p = 0.9 (P L739-740, Llama): exact when the nucleus has <= 32 tokens; larger
+    nuclei are flagged SV_ROW_FILTER_UNSUPPORTED (256) with the error sentinels."""
+    B, k = 6, 4
+    x = synth.make_inputs(B, k, V, dtype, seed=4321 + V)
+    Dd, Cd, Td = H.oracle_inputs(x)
+    rng = np.random.default_rng(V)
+    tok = np.zeros((B, k), dtype=np.int32)
+    big = np.zeros((B, k), dtype=bool)
+    for b in range(B):
+        for i in range(k):
+            p, keep_d = filter_dist(Dd[b, i], tau, 0, 0.9)
+            _, keep_c = filter_dist(Cd[b, i], tau, 0, 0.9)
+            big[b, i] = len(keep_d) > 32 or len(keep_c) > 32
+            tok[b, i] = rng.choice(V, p=p / p.sum())
+    D, C, T, _ = H.to_torch(x)
+    tk = torch.from_numpy(tok).cuda()
+    pd = synth.load_profile()
+    gs = sv.sv_score_filtered(D, C, tk, 0, 0.9, tau, tau, sv.Profile.from_dict(pd))
+    torch.cuda.synchronize()
+    g = {n: gs[n].cpu().numpy() for n in ("S", "A", "KL", "status")}
+    rs = score_filtered(Dd, Cd, tok, tau, tau, 0, 0.9)
+    flagged = (g["status"] & 256) != 0
+    assert np.array_equal(flagged, big), (flagged, big)
+    ok = ~big & (rs["status"] == 0)
+    for n in ("S", "A", "KL"):
+        assert H.close(g[n][ok], rs[n][ok]).all(), (n, g[n][ok], rs[n][ok])
+    print("rows with a nucleus > 32:", int(big.sum()), "of", big.size)
+
+
+def test_nucleus_only_verify(sv):
+    """sd_verify_filtered with top_k = 0 (nucleus), Llama temperature: every row's nucleus is
+    small here, so the whole verification must match the filtered oracle."""
+    B, k, V, tau = 6, 4, 32000, 0.6
+    x = synth.make_inputs(B, k, V, "f32", seed=777)
+    Dd, Cd, Td = H.oracle_inputs(x)
+    rng = np.random.default_rng(3)
+    tok = np.zeros((B, k), dtype=np.int32)
+    for b in range(B):
+        for i in range(k):
+            p, _ = filter_dist(Dd[b, i], tau, 0, 0.9)
+            tok[b, i] = rng.choice(V, p=p / p.sum())
+    for b in range(B):
+        for i in range(k + 1):
+            assert len(filter_dist(Td[b, i], tau, 0, 0.9)[1]) <= 32
+    D, C, T, _ = H.to_torch(x)
+    tk = torch.from_numpy(tok).cuda()
+    gs = sv.sv_score_filtered(D, C, tk, 0, 0.9, tau, tau, sv.Profile.from_dict(synth.load_profile()))
+    gam = np.full(B, k, dtype=np.int32)
+    gv = sv.sd_verify_filtered(T, tk, torch.from_numpy(gam).cuda(), gs["fworkspace"], 0, 0.9, tau, seed=9, offset=1)
+    torch.cuda.synchronize()
+    gv = {n: v.cpu().numpy() for n, v in gv.items()}
+    rv = verify_filtered(Dd, Td, tok, gam, tau, tau, 0, 0.9, 9, 1)
+    tie = rv["margin"] < 1e-6
+    assert np.array_equal(gv["n_accept"][~tie], rv["n_accept"][~tie])
+    assert np.array_equal(gv["out_tok"][~tie], rv["out_tok"][~tie])
+    assert H.close(gv["resid_mass"][~tie], rv["resid_mass"][~tie]).all()
