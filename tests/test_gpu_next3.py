@@ -93,3 +93,25 @@ def test_score_schedule_fused_matches_separate(sv, B, k, V, dtype):
     torch.cuda.synchronize()
     for n in sh:
         assert _eq(sh[n], fh[n]), n
+
+
+def test_graph_replay_headline_size(sv):
+    """The bench's headline launch configuration (GraphPipeline: sv_score, sv_schedule,
+    sd_verify_ragged in one graph) at B=80, k=8, V=152064 bf16 equals the eager pipeline
+    bitwise (which test_gpu_parity checks against the oracle at this size)."""
+    B, k, V = 80, 8, 152064
+    x = synth.make_inputs(B, k, V, "bf16", seed=0x5EED)
+    D, C, T, tok = H.to_torch(x)
+    prof = sv.Profile.from_dict(synth.load_profile())
+    L = torch.tensor(synth.latency_table(k + 2), dtype=torch.float64, device="cuda")
+    gp = sv.GraphPipeline(B, k, V, torch.bfloat16, prof, L, seed=0xC0FFEE, offset0=4)
+    gp.D.copy_(D)
+    gp.C.copy_(C)
+    gp.T.copy_(T)
+    gp.tok.copy_(tok)
+    gp.capture()
+    out = {n: v.clone() for n, v in gp.replay().items()}
+    ref = sv.Pipeline(B, k, V, torch.bfloat16, prof, L).run(D, C, T, tok, seed=0xC0FFEE, offset=4)
+    torch.cuda.synchronize()
+    for n in ref:
+        assert _eq(out[n], ref[n]), n
