@@ -70,6 +70,20 @@ __global__ void acc_kernel(float *acc) {
   atomicMax((int *)&acc[0], __float_as_int(e1));
   atomicMax((int *)&acc[1], __float_as_int(e2));
 }
+// MUFU.EX2 throughput from registers (no memory): 8 independent chains per thread
+__global__ void __launch_bounds__(256) mufu_kernel(float *out, int iters) {
+  float v[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = -0.001f * (threadIdx.x + j);
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = ex2(v[j]) - 1.5f;
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += v[j];
+  if (s == 1234.5f) out[0] = s;
+}
 #include <cstdlib>
 int main() {
   const size_t big = (size_t)194584320;  // one of D / C at the headline (B=80, k=8, V=152064, bf16)
@@ -95,6 +109,21 @@ int main() {
     run(k<3, 4, 2>, "3 ex2/pair 2T U4", sms * bpsm, big, 2);
     run(k<4, 4, 2>, "2 ex2 + 1 poly /pair U4", sms * bpsm, big, 2);
     run(k<5, 4, 2>, "2.5 ex2 + .5 poly U4", sms * bpsm, big, 2);
+  }
+  {  // MUFU ex2 rate
+    int clk_khz = 0;
+    cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
+    const int iters = 4096, blocks = sms * 8;
+    mufu_kernel<<<blocks, 256>>>(out, iters);
+    cudaEventRecord(e0);
+    mufu_kernel<<<blocks, 256>>>(out, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double ops = (double)blocks * 256 * iters * 8;
+    printf("MUFU.EX2: %.3g ex2/s = %.2f per clk per SM at the %.0f MHz max clock (%.1f us)\n", ops / (ms * 1e-3),
+           ops / (ms * 1e-3) / sms / (clk_khz * 1e3), clk_khz / 1e3, ms * 1e3);
   }
   // accuracy of ex2_poly vs exp2 over [-40, 0]
   {
