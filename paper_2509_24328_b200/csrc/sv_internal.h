@@ -13,6 +13,8 @@ constexpr int kScoreThreads = 256;
 constexpr int kScoreMinBlocks = 5;
 constexpr int kScoreGroup = 2;
 constexpr int kScoreLag = 128;
+constexpr int kScoreSmallGrid = 592;   // <= this many chunk tasks: all-loads-up-front variant
+constexpr int kScoreSmallUnits = 8;    // its units per thread per tensor (chunks of <= 8 x 256 units)
 constexpr int kScoreChunk = 40960;  // target elements per chunk task (per tensor); cs = ceil(V / it)
 constexpr int kScoreMaxSplits = 32;
 constexpr int kScoreMinSplits = 4;  // chunk tasks per row at least (a function of V only)

@@ -241,6 +241,60 @@ __device__ __forceinline__ P1State pass1_thread(const Chunk<T> &ch, float cd, fl
   return t;
 }
 
+// Small-grid variant of pass1_thread: ALL of the thread's units (<= PFA per tensor) are loaded
+// up front -- one memory round trip instead of one per group -- then processed in exactly the
+// groups and order of pass1_thread (full groups of G, then single units, then the element tail),
+// so every output bit is identical.
+template <typename T, bool kGuard, int NT, int G, int PFA>
+__device__ __forceinline__ P1State pass1_thread_all(const Chunk<T> &ch, float cd, float cc, uint64_t pol) {
+  constexpr int EPU = Elem<T>::kPerUnit;
+  const int tid = threadIdx.x;
+  P1State t{kMFloor, kMFloor, kMFloor, kMFloor, 0.f, 0.f, 0.f};
+  uint4 rd[PFA], rc[PFA];
+#pragma unroll
+  for (int j = 0; j < PFA; ++j) {
+    const int u = tid + j * NT;
+    rd[j] = u < ch.units ? ldg_hint(ch.d + (size_t)u * EPU, pol) : make_uint4(0u, 0u, 0u, 0u);
+    rc[j] = u < ch.units ? ldg_hint(ch.c + (size_t)u * EPU, pol) : make_uint4(0u, 0u, 0u, 0u);
+  }
+  int j0 = 0;
+#pragma unroll
+  for (int g = 0; g < PFA / G; ++g) {
+    if (tid + (g * G + G - 1) * NT < ch.units) {  // full groups form a prefix
+      uint4 gd[G], gc[G];
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        gd[q] = rd[g * G + q];
+        gc[q] = rc[g * G + q];
+      }
+      p1_group<T, kGuard, G>(t, gd, gc, cd, cc);
+      j0 = g * G + G;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < PFA; ++j) {
+    if (j >= j0 && tid + j * NT < ch.units) {
+      const uint4 sd[1] = {rd[j]}, sc[1] = {rc[j]};
+      p1_group<T, kGuard, 1>(t, sd, sc, cd, cc);
+    }
+  }
+  const int e0 = ch.units * EPU;
+  for (int e = e0 + tid; e < ch.n; e += NT) {
+    t.md = fmaxf(t.md, Elem<T>::load(ch.d + e));
+    t.mc = fmaxf(t.mc, Elem<T>::load(ch.c + e));
+  }
+  p1_rescale(t, cd, cc);
+  const float nmd = -t.rd * cd, nmc = -t.rc * cc;
+  for (int e = e0 + tid; e < ch.n; e += NT) {
+    const float ad = fmaf(Elem<T>::load(ch.d + e), cd, nmd), ac = fmaf(Elem<T>::load(ch.c + e), cc, nmc);
+    const float ed = ex2(ad);
+    t.ld += ed;
+    t.lc += ex2(ac);
+    t.w += ed > 0.f ? ed * (ad - ac) : 0.f;
+  }
+  return t;
+}
+
 template <typename T, int g>
 __device__ __forceinline__ void p2_group(f2 &acc, const uint4 (&rd)[g], const uint4 (&rc)[g], f2 cdd, f2 ccc, f2 ld2,
                                          f2 lc2) {
@@ -279,6 +333,47 @@ __device__ __forceinline__ float pass2_thread(const Chunk<T> &ch, float cd, floa
   for (; u0 < ch.units; u0 += NT) {
     uint4 rd[1] = {ldg_hint(ch.d + (size_t)u0 * EPU, pol)}, rc[1] = {ldg_hint(ch.c + (size_t)u0 * EPU, pol)};
     p2_group<T, 1>(acc, rd, rc, cdd, ccc, ld2, lc2);
+  }
+  for (int e = ch.units * EPU + tid; e < ch.n; e += NT)
+    acc.x += ex2(fminf(fmaf(Elem<T>::load(ch.d + e), cd, -lamd), fmaf(Elem<T>::load(ch.c + e), cc, -lamc)));
+  return acc.x + acc.y;
+}
+
+// Small-grid variant of pass2_thread (all loads up front, identical arithmetic order).
+template <typename T, int NT, int G, int PFA>
+__device__ __forceinline__ float pass2_thread_all(const Chunk<T> &ch, float cd, float cc, float lamd, float lamc,
+                                                  uint64_t pol) {
+  constexpr int EPU = Elem<T>::kPerUnit;
+  const int tid = threadIdx.x;
+  const f2 cdd{cd, cd}, ccc{cc, cc}, ld2{-lamd, -lamd}, lc2{-lamc, -lamc};
+  f2 acc{0.f, 0.f};
+  uint4 rd[PFA], rc[PFA];
+#pragma unroll
+  for (int j = 0; j < PFA; ++j) {
+    const int u = tid + j * NT;
+    rd[j] = u < ch.units ? ldg_hint(ch.d + (size_t)u * EPU, pol) : make_uint4(0u, 0u, 0u, 0u);
+    rc[j] = u < ch.units ? ldg_hint(ch.c + (size_t)u * EPU, pol) : make_uint4(0u, 0u, 0u, 0u);
+  }
+  int j0 = 0;
+#pragma unroll
+  for (int g = 0; g < PFA / G; ++g) {
+    if (tid + (g * G + G - 1) * NT < ch.units) {
+      uint4 gd[G], gc[G];
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        gd[q] = rd[g * G + q];
+        gc[q] = rc[g * G + q];
+      }
+      p2_group<T, G>(acc, gd, gc, cdd, ccc, ld2, lc2);
+      j0 = g * G + G;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < PFA; ++j) {
+    if (j >= j0 && tid + j * NT < ch.units) {
+      const uint4 sd[1] = {rd[j]}, sc[1] = {rc[j]};
+      p2_group<T, 1>(acc, sd, sc, cdd, ccc, ld2, lc2);
+    }
   }
   for (int e = ch.units * EPU + tid; e < ch.n; e += NT)
     acc.x += ex2(fminf(fmaf(Elem<T>::load(ch.d + e), cd, -lamd), fmaf(Elem<T>::load(ch.c + e), cc, -lamc)));
@@ -514,6 +609,10 @@ __device__ __forceinline__ void p2_merge(const ScoreArgs &a, const Task &k, Smem
   merge_partials<NW>(a, a.cs, [&](int j) { return a.part + ((size_t)k.row * a.cs + j) * 5; }, sm);
 }
 
+// sv_score_schedule's step a4 for one sequence, out of line (its fp64 arrays stay out of the
+// streaming kernel's register allocation)
+__device__ __noinline__ void fused_schedule(const ScheduleArgs &s, int64_t b) { schedule_one(s, b); }
+
 // P2 tail: block sum of the S partials, publish; the row's last P2 task runs the epilogue and
 // resets the row's counters.  All NW warps call it.
 template <typename T, int NW>
@@ -544,14 +643,14 @@ __device__ __forceinline__ void p2_finish(const ScoreArgs &a, const Task &k, flo
       if (old == (uint32_t)a.k - 1u) {
         __threadfence();  // the other rows' p_hat
         a.seq_cnt[k.bb] = 0u;
-        schedule_one(a.sch, k.bb);
+        fused_schedule(a.sch, k.bb);
       }
     }
   }
 }
 
 // LDG variant: every thread loads its own units (kScoreGroup 16-byte loads per tensor in flight).
-template <typename T, int NT, int MINB, int G, bool PF>
+template <typename T, int NT, int MINB, int G, bool PF, int PFA = 0>
 __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constant__ ScoreArgs a) {
   constexpr int NW = NT / 32;
   __shared__ Smem<NW> sm;
@@ -562,7 +661,13 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constan
   const Chunk<T> ch = chunk_of<T>(a, k.bb, k.ii, k.rank);
   if (!k.p2) {
     const uint64_t pol_keep = l2_policy_evict_last();
-    P1State t = pass1_thread<T, false, NT, G, PF>(ch, cd, cc, pol_keep);
+    P1State t;
+    if constexpr (PFA > 0) {
+      t = ch.units <= PFA * NT ? pass1_thread_all<T, false, NT, G, PFA>(ch, cd, cc, pol_keep)
+                               : pass1_thread<T, false, NT, G, PF>(ch, cd, cc, pol_keep);
+    } else {
+      t = pass1_thread<T, false, NT, G, PF>(ch, cd, cc, pol_keep);
+    }
     if (t.w != t.w && t.ld == t.ld && t.lc == t.lc)  // 0 * (-inf) from masked logits: guarded redo
       t = pass1_thread<T, true, NT, G, false>(ch, cd, cc, pol_keep);
     p1_publish<NW>(a, k, t, sm);
@@ -572,7 +677,14 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constan
   __syncthreads();
   const float lamd = sm.lam[0], lamc = sm.lam[1];
   float s_loc = 0.f;
-  if (lamd == lamd && lamc == lamc) s_loc = pass2_thread<T, NT, G>(ch, cd, cc, lamd, lamc, l2_policy_evict_first());
+  if (lamd == lamd && lamc == lamc) {
+    if constexpr (PFA > 0) {
+      s_loc = ch.units <= PFA * NT ? pass2_thread_all<T, NT, G, PFA>(ch, cd, cc, lamd, lamc, l2_policy_evict_first())
+                                   : pass2_thread<T, NT, G>(ch, cd, cc, lamd, lamc, l2_policy_evict_first());
+    } else {
+      s_loc = pass2_thread<T, NT, G>(ch, cd, cc, lamd, lamc, l2_policy_evict_first());
+    }
+  }
   p2_finish<T, NW>(a, k, s_loc, sm);
 }
 
@@ -723,11 +835,11 @@ __global__ void __launch_bounds__(kScoreThreads + 32, MINB) sv_score_tma_kernel(
   p2_finish<T, NW>(a, k, s_loc, sm);
 }
 
-template <typename T, int NT, int MINB, int G, bool PF = false>
+template <typename T, int NT, int MINB, int G, bool PF = false, int PFA = 0>
 cudaError_t launch_score_t(const ScoreArgs &a, cudaStream_t st) {
   const int64_t tasks = 2 * (int64_t)a.B * a.k * a.cs;
   if (tasks == 0) return cudaSuccess;
-  return launch_k(sv_score_kernel<T, NT, MINB, G, PF>, dim3((unsigned)tasks), dim3(NT), 0, st, a);
+  return launch_k(sv_score_kernel<T, NT, MINB, G, PF, PFA>, dim3((unsigned)tasks), dim3(NT), 0, st, a);
 }
 
 template <typename T, int SU, int NS, int MINB>
@@ -758,7 +870,15 @@ cudaError_t launch_score_cfg(const ScoreArgs &a, cudaStream_t st) {
     case 6: return launch_score_tma<T, 1, 4, 5>(a, st);
     case 7: return launch_score_tma<T, 2, 2, 5>(a, st);
     case 8: return launch_score_tma<T, 1, 6, 4>(a, st);
-    default: return launch_score_t<T, kScoreThreads, kScoreMinBlocks, kScoreGroup>(a, st);
+    default: {
+      // small grids (every task resident at once): the all-loads-up-front variant -- one memory
+      // round trip per pass instead of one per group; identical arithmetic, so identical bits
+      static const int small = tune_knob("SV_SCORE_SMALL", 1);
+      const int64_t tasks = 2 * (int64_t)a.B * a.k * a.cs;
+      if (small && tasks <= kScoreSmallGrid)
+        return launch_score_t<T, kScoreThreads, 2, kScoreGroup, false, kScoreSmallUnits>(a, st);
+      return launch_score_t<T, kScoreThreads, kScoreMinBlocks, kScoreGroup>(a, st);
+    }
   }
 }
 
