@@ -596,7 +596,15 @@ def run_ours(args, rank, world, local_rank):
                          "unit": "GB/s", "frac": k1_gbs / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": k1_bytes, "avg_launch_ms": k1_ms,
                          "k1_share_of_step": k1_ms / ms_step, "share_of": "eager step",
-                         "peak_source": peak_src},
+                         "peak_source": peak_src, "frac_of_spec_8TBs": k1_gbs / 8000.0,
+                         # MUFU co-roofline: 1.5 ex2 per logit element; peak = the
+                         # measured 15.9 MUFU.EX2 / clk / SM (profiles/r01/microbench_ceil.txt) x 148
+                         # SMs x the sampled SM clock
+                         "mufu": {"ex2_per_launch": int(1.5 * B * k * V * 2),
+                                  "achieved_per_s": 1.5 * B * k * V * 2 / (k1_ms * 1e-3),
+                                  "peak_per_s": 15.9 * 148 * (clk.summary()["sm_mhz"] or 1965) * 1e6,
+                                  "frac": 1.5 * B * k * V * 2 / (k1_ms * 1e-3)
+                                          / (15.9 * 148 * (clk.summary()["sm_mhz"] or 1965) * 1e6)}},
             "sd_full_verify": {"value": world * B * k / (ms_full_step * 1e-3), "unit": "positions/s",
                                "ms_per_step": ms_full_step,
                                "hbm_gbs": full_bytes / (ms_full_step * 1e-3) / 1e9,
