@@ -63,7 +63,7 @@ typedef enum { SV_F32 = 0, SV_BF16 = 1 } sv_dtype;
 #define SV_ROW_RESID_ZERO  32  /* rejected but residual mass Z = 0: sampled p_t (R10) */
 #define SV_ROW_BAD_GAMMA   64  /* gamma outside [0, k]                               */
 #define SV_ROW_BAD_LATENCY 128 /* a latency entry used by the schedule is <= 0 / NaN */
-#define SV_ROW_FILTER_UNSUPPORTED 256 /* nucleus-only filter with more than 32 tokens */
+#define SV_ROW_FILTER_UNSUPPORTED 256 /* wide draft nucleus but no draft logits given to sd_verify_filtered */
 
 /* A [B, rows, V] logit tensor: element (b, i, v) is at ptr + b*stride_b + i*stride_i + v
  * (strides in ELEMENTS).  dtype: sv_dtype. */
@@ -238,8 +238,9 @@ SV_API int32_t sd_verify_ragged(const sv_logits *draft, const void *target, int6
  * prefix of the top-k distribution (probability desc, index asc) whose sequential fp64
  * cumulative mass is >= top_p.  Supported: 1 <= top_k <= 32 (each filtered distribution has at
  * most 32 entries), 0 < top_p <= 1; and top_k = 0 with top_p < 1 (nucleus over the FULL
- * distribution, the paper's Llama setting) whenever the nucleus has at most 32 tokens -- rows
- * whose nucleus is larger get SV_ROW_FILTER_UNSUPPORTED and the error sentinels.
+ * distribution, the paper's Llama setting) of any size: nuclei of at most 32 tokens are held as
+ * lists, larger ones in threshold form (the cut key and the last kept index among its ties,
+ * found by a mass-weighted radix select) and scored / sampled by full-row passes.
  *
  * sv_score_filtered: S, A, KL, p_hat, draft_ptok (= p'_d(t)), row_status [B, k] as sv_score but
  * over the filtered distributions (KL = +inf when the draft keeps a token the companion
@@ -248,7 +249,10 @@ SV_API int32_t sd_verify_ragged(const sv_logits *draft, const void *target, int6
  * residual max(0, p'_t - p'_d), else the bonus p'_t of row gamma; inverse CDF in vocabulary
  * order (R11), Philox as sd_verify (R12).  accept_ratio = min(1, ratio) for the positions
  * tested (i <= N, i < gamma), NaN beyond.  fworkspace: sv_filter_workspace_bytes(B, k), the
- * same buffer for both calls of a step (no zero-fill needed).
+ * same buffer for both calls of a step (no zero-fill needed).  `draft`: the draft logits of
+ * sv_score_filtered (same layout), read only for sequences whose tested draft row has a nucleus
+ * wider than 32 tokens; may be NULL, in which case such sequences get
+ * SV_ROW_FILTER_UNSUPPORTED and the error sentinels.
  */
 typedef struct {
     int32_t top_k;
@@ -261,7 +265,7 @@ SV_API int32_t sv_score_filtered(const sv_logits *draft, const sv_logits *comp, 
                                  const sv_filter *filt, const sv_profile *prof, float *S, float *A, float *KL,
                                  float *p_hat, float *draft_ptok, int32_t *row_status, void *fworkspace,
                                  size_t fworkspace_bytes, void *stream);
-SV_API int32_t sd_verify_filtered(const sv_logits *target, const int32_t *draft_tok, const int32_t *gamma,
+SV_API int32_t sd_verify_filtered(const sv_logits *target, const sv_logits *draft, const int32_t *draft_tok, const int32_t *gamma,
                                   int32_t B, int32_t k, int32_t V, float tau_t, const sv_filter *filt,
                                   uint64_t seed, uint64_t offset, int64_t seq_base, int32_t *n_accept,
                                   int32_t *out_tok, float *accept_ratio, float *resid_mass, int32_t *row_status,

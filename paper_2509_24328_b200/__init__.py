@@ -249,8 +249,10 @@ def sv_score_filtered(D, C, tok, top_k=20, top_p=0.8, tau_d=1.0, tau_c=1.0, prof
 
 
 def sd_verify_filtered(T, tok, gamma, fworkspace, top_k=20, top_p=0.8, tau_t=1.0, seed=0, offset=0, seq_base=0,
-                       stream=None) -> dict:
-    """Steps a5-a6 over the filtered distributions (NEXT-2; S L183) through `sd_verify_filtered`."""
+                       stream=None, D=None) -> dict:
+    """Steps a5-a6 over the filtered distributions (NEXT-2; S L183) through `sd_verify_filtered`.
+    `D` (the draft logits given to `sv_score_filtered`) is needed only when a draft nucleus may
+    exceed 32 tokens (top_k = 0)."""
     B, k1, V = T.shape
     k = k1 - 1
     dev = T.device
@@ -261,7 +263,8 @@ def sd_verify_filtered(T, tok, gamma, fworkspace, top_k=20, top_p=0.8, tau_t=1.0
            "status": torch.empty(B, dtype=torch.int32, device=dev)}
     f = _lib.SvFilter(int(top_k), float(top_p))
     st = _lib.load().sd_verify_filtered(
-        ctypes.byref(_logits(T)), _ptr(tok), _ptr(gamma), B, k, V, float(tau_t), ctypes.byref(f), ctypes.c_uint64(seed),
+        ctypes.byref(_logits(T)), ctypes.byref(_logits(D)) if D is not None else None, _ptr(tok), _ptr(gamma), B, k, V,
+        float(tau_t), ctypes.byref(f), ctypes.c_uint64(seed),
         ctypes.c_uint64(offset), int(seq_base), _ptr(res["n_accept"]), _ptr(res["out_tok"]), _ptr(res["accept_ratio"]),
         _ptr(res["resid_mass"]), _ptr(res["status"]), fworkspace.data_ptr(), fworkspace.numel(), _stream(stream))
     _lib.check(st, "sd_verify_filtered")

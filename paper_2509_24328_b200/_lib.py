@@ -81,7 +81,7 @@ def load(path: str = LIB_PATH):
     lib.sv_score_filtered.argtypes = [LP, LP, P, i32, i32, i32, f32, f32, FP, ctypes.POINTER(SvProfile), P, P, P, P,
                                       P, P, P, sz, P]
     lib.sv_score_filtered.restype = i32
-    lib.sd_verify_filtered.argtypes = [LP, P, P, i32, i32, i32, f32, FP, u64, u64, i64, P, P, P, P, P, P, sz, P]
+    lib.sd_verify_filtered.argtypes = [LP, LP, P, P, i32, i32, i32, f32, FP, u64, u64, i64, P, P, P, P, P, P, sz, P]
     lib.sd_verify_filtered.restype = i32
     lib.sv_profile_workspace_bytes.argtypes = [i32, i32, i32, i32]
     lib.sv_profile_workspace_bytes.restype = sz

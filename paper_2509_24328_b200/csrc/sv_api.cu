@@ -172,6 +172,11 @@ static VerifyArgs make_verify_args(const sv_logits *draft, const sv_logits *targ
   a.d_si = draft->stride_i;
   a.t_sb = target->stride_b;
   a.t_si = target->stride_i;
+  if (draft) {
+    a.d = draft->ptr;
+    a.d_sb = draft->stride_b;
+    a.d_si = draft->stride_i;
+  }
   a.tok = draft_tok;
   a.gamma = gamma;
   a.dm = draft_m;
@@ -473,7 +478,7 @@ int32_t sv_score_filtered(const sv_logits *draft, const sv_logits *comp, const i
   return SV_OK;
 }
 
-int32_t sd_verify_filtered(const sv_logits *target, const int32_t *draft_tok, const int32_t *gamma, int32_t B, int32_t k,
+int32_t sd_verify_filtered(const sv_logits *target, const sv_logits *draft, const int32_t *draft_tok, const int32_t *gamma, int32_t B, int32_t k,
                            int32_t V, float tau_t, const sv_filter *filt, uint64_t seed, uint64_t offset,
                            int64_t seq_base, int32_t *n_accept, int32_t *out_tok, float *accept_ratio,
                            float *resid_mass, int32_t *row_status, void *fworkspace, size_t fworkspace_bytes,
@@ -482,6 +487,7 @@ int32_t sd_verify_filtered(const sv_logits *target, const int32_t *draft_tok, co
   int32_t r = shape_check(B, k, V, target->dtype);
   if (r != SV_OK) return r;
   if ((r = logits_check(target, target->dtype)) != SV_OK) return r;
+  if (draft && (r = logits_check(draft, target->dtype)) != SV_OK) return r;
   if ((r = filter_check(filt)) != SV_OK) return r;
   if (!draft_tok || !gamma || !n_accept || !out_tok || !(tau_t > 0.f) || seq_base < 0) return SV_ERR_INVALID_ARG;
   if (B == 0) return SV_OK;
@@ -490,6 +496,11 @@ int32_t sd_verify_filtered(const sv_logits *target, const int32_t *draft_tok, co
   a.t = target->ptr;
   a.t_sb = target->stride_b;
   a.t_si = target->stride_i;
+  if (draft) {
+    a.d = draft->ptr;
+    a.d_sb = draft->stride_b;
+    a.d_si = draft->stride_i;
+  }
   a.tok = draft_tok;
   a.gamma = gamma;
   a.B = B;

@@ -325,58 +325,231 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
     }
     __syncthreads();
   }
-  if (wid != 0) return;
-  // ---- sort by (key desc, index asc), softmax (fp64), top_p, renormalise
-  const K mk = lane < KK ? c_key[lane] : (K)0;
-  const int mi = lane < KK ? c_idx[lane] : INT32_MAX;
-  int rank = 0;
-  for (int l = 0; l < KK; ++l) {
-    const K ok = __shfl_sync(0xffffffffu, mk, l);
-    const int oi = __shfl_sync(0xffffffffu, mi, l);
-    rank += (ok > mk) || (ok == mk && oi < mi);
-  }
-  __syncwarp();
-  if (lane < KK) {
-    c_key[rank] = mk;
-    c_idx[rank] = mi;
-  }
-  __syncwarp();
-  const double y = lane < KK ? (double)KO::value(c_key[lane]) / tau : -INFINITY;
-  const double y0 = __shfl_sync(0xffffffffu, y, 0);
-  int st = s_bad ? 1 /*SV_ROW_NAN*/ : 0;
-  if (!st && !(y0 > -INFINITY)) st = 2; /*SV_ROW_ALL_NEG_INF*/
-  double p = (lane < KK && !st) ? exp(y - y0) : 0.0;
-  double tot = 0.0;  // sequential in sorted order (the oracle's order); nucleus: the full row
-  if (nucleus) tot = s_lfull;
-  else
-    for (int l = 0; l < KK; ++l) tot += __shfl_sync(0xffffffffu, p, l);
-  p = p / tot;
-  int n = KK;
-  if (a.top_p < 1.f) {
-    double c = 0.0;
-    bool cut = false;
+  __shared__ int s_wide;
+  __shared__ double s_y0;
+  if (wid == 0) {
+    // ---- sort by (key desc, index asc), softmax (fp64), top_p, renormalise
+    const K mk = lane < KK ? c_key[lane] : (K)0;
+    const int mi = lane < KK ? c_idx[lane] : INT32_MAX;
+    int rank = 0;
     for (int l = 0; l < KK; ++l) {
-      c += __shfl_sync(0xffffffffu, p, l);
-      if (c >= (double)a.top_p) {
-        n = l + 1;
-        cut = true;
-        break;
+      const K ok = __shfl_sync(0xffffffffu, mk, l);
+      const int oi = __shfl_sync(0xffffffffu, mi, l);
+      rank += (ok > mk) || (ok == mk && oi < mi);
+    }
+    __syncwarp();
+    if (lane < KK) {
+      c_key[rank] = mk;
+      c_idx[rank] = mi;
+    }
+    __syncwarp();
+    const double y = lane < KK ? (double)KO::value(c_key[lane]) / tau : -INFINITY;
+    const double y0 = __shfl_sync(0xffffffffu, y, 0);
+    int st = s_bad ? 1 /*SV_ROW_NAN*/ : 0;
+    if (!st && !(y0 > -INFINITY)) st = 2; /*SV_ROW_ALL_NEG_INF*/
+    double p = (lane < KK && !st) ? exp(y - y0) : 0.0;
+    double tot = 0.0;  // sequential in sorted order (the oracle's order); nucleus: the full row
+    if (nucleus) tot = s_lfull;
+    else
+      for (int l = 0; l < KK; ++l) tot += __shfl_sync(0xffffffffu, p, l);
+    p = p / tot;
+    int n = KK;
+    bool wide = false;
+    double s = 1.0;
+    if (a.top_p < 1.f) {
+      double c = 0.0;
+      bool cut = false;
+      for (int l = 0; l < KK; ++l) {
+        c += __shfl_sync(0xffffffffu, p, l);
+        if (c >= (double)a.top_p) {
+          n = l + 1;
+          cut = true;
+          break;
+        }
+      }
+      wide = nucleus && !cut && !st;  // nucleus larger than 32 tokens: threshold form below
+      s = 0.0;
+      for (int l = 0; l < n; ++l) s += __shfl_sync(0xffffffffu, p, l);
+      p = p / s;
+    }
+    if (st || wide) n = 0;
+    if (lane < n) {
+      out->idx[lane] = c_idx[lane];
+      out->p[lane] = p;
+    }
+    if (lane == 0) {
+      out->n = n;
+      out->st = st;
+      out->wide = wide;
+      out->tau = tau;
+      out->y0 = y0;
+      out->tot = tot;
+      if (!wide) {
+        out->s = s;
+        out->th_key = n ? (uint32_t)c_key[n - 1] : 0xFFFFFFFFu;
+        out->th_idx = n ? c_idx[n - 1] : -1;
+      }
+      s_wide = wide;
+      s_y0 = y0;
+    }
+  }
+  __syncthreads();
+  if (!s_wide) return;
+  // ---- nucleus larger than 32 tokens: the threshold form directly.  Mass-weighted radix select
+  // of the cut key theta on the order-preserving key, 8 bits per pass from the top: per digit the
+  // mass sum exp(y_v - y0) / tot of the keys under the current prefix, in 2^-60 fixed point
+  // (integer shared atomics: order-independent, exact bin sums, deterministic), into 8
+  // privatised histograms in the (now free) candidate buffer.  The cut digit is the first, from
+  // the top, whose cumulative mass reaches top_p.
+  {
+    constexpr double kFix = 1152921504606846976.0;  // 2^60
+    unsigned long long *wm = s_cand;
+    __shared__ unsigned long long s_cab;
+    __shared__ int s_all, s_m;
+    __shared__ double s_s;
+    const double y0 = s_y0, tot = s_lfull;
+    const unsigned long long tp_fix = (unsigned long long)((double)a.top_p * kFix);
+    if (tid == 0) {
+      s_prefix = 0;
+      s_mask = 0;
+      s_cab = 0ull;
+      s_all = 0;
+      s_ntie = 0;
+    }
+    for (int shift = KO::kBits - 8; shift >= 0; shift -= 8) {
+      for (int j = tid; j < kCandCap; j += NT) wm[j] = 0ull;
+      __syncthreads();
+      const K prefix = s_prefix, mask = s_mask;
+      unsigned long long *mine = wm + (wid & 7) * 256;
+      for (int e = tid; e < V; e += NT) {
+        const K kk = KO::key(x, e);
+        if ((kk & mask) == prefix) {
+          const double m = exp((double)KO::value(kk) / tau - y0) / tot;
+          atomicAdd(mine + ((kk >> shift) & 255u), (unsigned long long)(m * kFix));
+        }
+      }
+      __syncthreads();
+      if (tid < 256) {
+        unsigned long long t = 0ull;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) t += wm[c * 256 + tid];
+        wm[tid] = t;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        unsigned long long c = s_cab;
+        int d = 255;
+        for (; d >= 0; --d) {
+          if (c + wm[d] >= tp_fix) break;
+          c += wm[d];
+        }
+        if (d < 0) s_all = 1;  // the whole distribution rounds below top_p: keep every token
+        s_cab = c;
+        s_prefix = prefix | ((K)(d < 0 ? 0 : d) << shift);
+        s_mask = mask | ((K)255u << shift);
+      }
+      __syncthreads();
+      if (s_all) break;
+    }
+    if (s_all) {
+      if (tid == 0) {
+        out->th_key = 0u;
+        out->th_idx = INT32_MAX;
+        out->s = (double)s_cab / kFix;
+      }
+      return;
+    }
+    const K theta = s_prefix;
+    for (int e = tid; e < V; e += NT)
+      if (KO::key(x, e) == theta) {
+        const int slot = atomicAdd(&s_ntie, 1);
+        if (slot < kTieCap) s_tie[slot] = e;
+      }
+    __syncthreads();
+    const int ntie = s_ntie;
+    if (tid == 0) {  // the oracle's sequential cumulative over the tie group (index order)
+      const double pth = exp((double)KO::value(theta) / tau - y0) / tot;
+      double c = (double)s_cab / kFix;
+      int m = 0;
+      while (m < ntie) {
+        c += pth;
+        ++m;
+        if (c >= (double)a.top_p) break;
+      }
+      s_m = m;
+      s_s = c;
+    }
+    __syncthreads();
+    const int m = s_m;
+    if (ntie <= kTieCap) {  // bitonic sort of the tie indices; the m-th smallest closes the nucleus
+      int np2 = 1;
+      while (np2 < ntie) np2 <<= 1;
+      for (int j = ntie + tid; j < np2; j += NT) s_tie[j] = INT32_MAX;
+      __syncthreads();
+      for (int size = 2; size <= np2; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+          for (int j = tid; j < np2; j += NT) {
+            const int o = j ^ stride;
+            if (o > j) {
+              const bool up = (j & size) == 0;
+              const int u = s_tie[j], v = s_tie[o];
+              if ((u > v) == up) {
+                s_tie[j] = v;
+                s_tie[o] = u;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      }
+      if (tid == 0) out->th_idx = s_tie[m - 1];
+    } else if (wid == 0) {  // pathological tie counts: one ordered pass (vocabulary order)
+      int taken = 0;
+      for (int e0 = 0; e0 < V && taken < m; e0 += 32) {
+        const int e = e0 + lane;
+        const bool eq = e < V && KO::key(x, e) == theta;
+        const unsigned msk = __ballot_sync(0xffffffffu, eq);
+        const int rank = taken + __popc(msk & ((1u << lane) - 1u));
+        if (eq && rank == m - 1) out->th_idx = e;
+        taken += __popc(msk);
       }
     }
-    if (nucleus && !cut && !st) st = 256; /*SV_ROW_FILTER_UNSUPPORTED: nucleus > 32 tokens*/
-    double s = 0.0;
-    for (int l = 0; l < n; ++l) s += __shfl_sync(0xffffffffu, p, l);
-    p = p / s;
+    if (tid == 0) {
+      out->th_key = (uint32_t)theta;
+      out->s = s_s;
+    }
   }
-  if (st) n = 0;
-  if (lane < n) {
-    out->idx[lane] = c_idx[lane];
-    out->p[lane] = p;
-  }
-  if (lane == 0) {
-    out->n = n;
-    out->st = st;
-  }
+}
+
+// threshold form of a row (every FList carries it, see sv_internal.h)
+struct Thr {
+  uint32_t key;
+  int32_t idx;
+  double tau, y0, tot, s;
+};
+__device__ __forceinline__ Thr load_thr(const FList *L) { return Thr{L->th_key, L->th_idx, L->tau, L->y0, L->tot, L->s}; }
+
+// p'(v) of a row in threshold form: the kept set and the same fp64 operations as the list entries
+// (exp(y - y0), / tot, / s), so list values are reproduced bit for bit
+template <typename T>
+__device__ __forceinline__ double thr_p(const T *x, int v, const Thr &L) {
+  using KO = KeyOf<T>;
+  const uint32_t kk = KO::key(x, v);
+  if (kk < L.key || (kk == L.key && v > L.idx)) return 0.0;
+  double p = exp((double)KO::value(kk) / L.tau - L.y0);
+  p = p / L.tot;
+  return p / L.s;
+}
+
+__device__ __forceinline__ double block_sum_d(double v, double *red) {  // fixed order: warps, then 0..nw-1
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum_d(v);
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < nw; ++w) t += red[w];
+  return t;
 }
 
 // p of vocabulary index v in a list (0 when absent); every lane returns the same value
@@ -388,6 +561,26 @@ __device__ __forceinline__ double list_p(const FList *L, int n, int v) {
   return m ? __shfl_sync(0xffffffffu, mine, __ffs(m) - 1) : 0.0;
 }
 
+// the score outputs of row r (lane / thread 0 of the row's owner)
+__device__ __forceinline__ void write_fscore(const FilterArgs &a, int64_t r, int st, double S, double A, double KL,
+                                             double pdt) {
+  const float nanf_ = __int_as_float(0x7fc00000);
+  float phat = 0.f;
+  if (!st && a.p_hat) {  // bin = number of interior edges strictly below the value (R9)
+    const float Sf = (float)S, Af = (float)A;
+    int si = 0, ai = 0;
+    for (int j = 1; j < a.n_s; ++j) si += a.s_edges[j] < Sf;
+    for (int j = 1; j < a.n_a; ++j) ai += a.a_edges[j] < Af;
+    phat = a.cells[si * a.n_a + ai];
+  }
+  if (a.S) a.S[r] = st ? nanf_ : (float)S;
+  if (a.A) a.A[r] = st ? nanf_ : (float)A;
+  if (a.KL) a.KL[r] = st ? nanf_ : (float)KL;
+  if (a.p_hat) a.p_hat[r] = phat;
+  if (a.dpt) a.dpt[r] = (st & ~8) ? nanf_ : (float)pdt;
+  if (a.status) a.status[r] = st;
+}
+
 __global__ void __launch_bounds__(256) sv_fscore_kernel(const __grid_constant__ FilterArgs a) {
   pdl_wait();
   pdl_trigger();
@@ -395,6 +588,7 @@ __global__ void __launch_bounds__(256) sv_fscore_kernel(const __grid_constant__ 
   const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (r >= (int64_t)a.B * a.k) return;
   const FList *Ld = a.dl + r, *Lc = a.cl + r;
+  if (Ld->wide || Lc->wide) return;  // sv_fwide_score_kernel
   const int nd = Ld->n, nc = Lc->n;
   int st = Ld->st | Lc->st;
   const int t = a.tok[r];
@@ -417,25 +611,48 @@ __global__ void __launch_bounds__(256) sv_fscore_kernel(const __grid_constant__ 
   const double pdt = (st & 4) ? 0.0 : list_p(Ld, nd, t), pct = (st & 4) ? 0.0 : list_p(Lc, nc, t);
   if (!st && pdt == 0.0) st |= 8; /*SV_ROW_DRAFT_ZERO*/
   const double A = st ? 0.0 : fmin(1.0, pct / pdt);
-  float phat = 0.f;
-  if (!st && a.p_hat) {  // bin = number of interior edges strictly below the value (R9)
-    const float Sf = (float)S, Af = (float)A;
-    int si = 0, ai = 0;
-    for (int j = 1; j < a.n_s; ++j) si += a.s_edges[j] < Sf;
-    for (int j = 1; j < a.n_a; ++j) ai += a.a_edges[j] < Af;
-    phat = a.cells[si * a.n_a + ai];
-  }
-  if (lane == 0) {
-    const float nanf_ = __int_as_float(0x7fc00000);
-    if (a.S) a.S[r] = st ? nanf_ : (float)S;
-    if (a.A) a.A[r] = st ? nanf_ : (float)A;
-    if (a.KL) a.KL[r] = st ? nanf_ : (float)KL;
-    if (a.p_hat) a.p_hat[r] = phat;
-    if (a.dpt) a.dpt[r] = (st & ~8) ? nanf_ : (float)pdt;
-    if (a.status) a.status[r] = st;
-  }
+  if (lane == 0) write_fscore(a, r, st, S, A, KL, pdt);
 }
 
+// KF2w: rows where the draft or the companion nucleus exceeds 32 tokens -- one CTA per (b, i),
+// full-row pass over both rows in threshold form (S = sum min(p'_d, p'_c), KL over p'_d > 0)
+template <typename T>
+__global__ void __launch_bounds__(512) sv_fwide_score_kernel(const __grid_constant__ FilterArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ double red[16];
+  const int64_t r = blockIdx.x;
+  const FList *Ld = a.dl + r, *Lc = a.cl + r;
+  if (!Ld->wide && !Lc->wide) return;
+  const int64_t b = r / a.k, i = r % a.k;
+  const T *xd = reinterpret_cast<const T *>(a.d) + b * a.d_sb + i * a.d_si;
+  const T *xc = reinterpret_cast<const T *>(a.c) + b * a.c_sb + i * a.c_si;
+  const Thr ld = load_thr(Ld), lc = load_thr(Lc);
+  int st = Ld->st | Lc->st;
+  const int t = a.tok[r];
+  if (t < 0 || t >= a.V) st |= 4;
+  double S = 0.0, KL = 0.0;
+  if (!st)
+    for (int v = threadIdx.x; v < a.V; v += blockDim.x) {
+      const double pd = thr_p(xd, v, ld);
+      if (pd > 0.0) {
+        const double pc = thr_p(xc, v, lc);
+        S += fmin(pd, pc);
+        KL += pc > 0.0 ? pd * log(pd / pc) : INFINITY;
+      }
+    }
+  S = block_sum_d(S, red);
+  KL = block_sum_d(KL, red);
+  if (threadIdx.x != 0) return;
+  const double pdt = (st & 4) ? 0.0 : thr_p(xd, t, ld), pct = (st & 4) ? 0.0 : thr_p(xc, t, lc);
+  if (!st && pdt == 0.0) st |= 8;
+  const double A = st ? 0.0 : fmin(1.0, pct / pdt);
+  write_fscore(a, r, st, S, A, KL, pdt);
+}
+
+constexpr int kPendingWide = -2;  // out_tok marker: the residual / bonus sample needs a full-row pass
+
+template <typename T>
 __global__ void __launch_bounds__(256) sv_fverify_kernel(const __grid_constant__ FilterArgs a) {
   pdl_wait();
   pdl_trigger();
@@ -451,11 +668,18 @@ __global__ void __launch_bounds__(256) sv_fverify_kernel(const __grid_constant__
   int N = st ? 0 : gg;
   for (int i = 0; i < gg; ++i) {
     const int64_t rd = b * k + i, rt = b * (k + 1) + i;
+    const FList *Ldr = a.dl + rd, *Ltr = a.tl + rt;
     const int t = a.tok[rd];
-    int rst = a.dl[rd].st | a.tl[rt].st;
+    int rst = Ldr->st | Ltr->st;
     if (t < 0 || t >= a.V) rst |= 4;
-    const double pdt = (rst & 4) ? 0.0 : list_p(a.dl + rd, a.dl[rd].n, t);
-    const double ptt = (rst & 4) ? 0.0 : list_p(a.tl + rt, a.tl[rt].n, t);
+    if (Ldr->wide && !a.d) rst |= 256; /*SV_ROW_FILTER_UNSUPPORTED: wide draft row, no draft logits*/
+    double pdt = 0.0, ptt = 0.0;
+    if (!(rst & (4 | 256))) {
+      pdt = Ldr->wide ? thr_p(reinterpret_cast<const T *>(a.d) + b * a.d_sb + i * a.d_si, t, load_thr(Ldr))
+                      : list_p(Ldr, Ldr->n, t);
+      ptt = Ltr->wide ? thr_p(reinterpret_cast<const T *>(a.t) + b * a.t_sb + i * a.t_si, t, load_thr(Ltr))
+                      : list_p(Ltr, Ltr->n, t);
+    }
     if (!rst && pdt == 0.0) rst |= 8;
     if (rst) {
       st |= rst;
@@ -471,6 +695,10 @@ __global__ void __launch_bounds__(256) sv_fverify_kernel(const __grid_constant__
   }
   if (a.ratio && lane < k) a.ratio[b * k + lane] = (!st && lane < N + (N < gg ? 1 : 0)) ? (float)fmin(1.0, ratio_mine)
                                                                                           : __int_as_float(0x7fc00000);
+  const int64_t rt = b * (k + 1) + (st ? 0 : N);
+  const FList *Lt = a.tl + rt;
+  const FList *LdN = (!st && N < gg) ? a.dl + b * k + N : nullptr;
+  if (!st && LdN && LdN->wide && !a.d) st |= 256;
   if (st) {
     if (lane == 0) {
       a.n_accept[b] = 0;
@@ -480,18 +708,23 @@ __global__ void __launch_bounds__(256) sv_fverify_kernel(const __grid_constant__
     }
     return;
   }
-  // residual (N < gamma) or bonus (N == gamma) over the target list of row N
-  const int64_t rt = b * (k + 1) + N;
-  const FList *Lt = a.tl + rt;
-  const int nt = Lt->n;
   if (Lt->st) st |= Lt->st;
+  if (Lt->wide || (LdN && LdN->wide)) {  // sv_fwide_sample_kernel draws the token
+    if (lane == 0) {
+      a.n_accept[b] = N;
+      a.out_tok[b] = kPendingWide;
+      if (a.status) a.status[b] = st;
+    }
+    return;
+  }
+  // residual (N < gamma) or bonus (N == gamma) over the target list of row N
+  const int nt = Lt->n;
   const int vi = lane < nt ? Lt->idx[lane] : INT32_MAX;
   double r = lane < nt ? Lt->p[lane] : 0.0;
-  if (N < gg) {
-    const FList *Ld = a.dl + b * k + N;
+  if (LdN) {
     double pdv = 0.0;
-    for (int l = 0; l < Ld->n; ++l)
-      if (Ld->idx[l] == vi) pdv = Ld->p[l];
+    for (int l = 0; l < LdN->n; ++l)
+      if (LdN->idx[l] == vi) pdv = LdN->p[l];
     r = fmax(0.0, r - pdv);
   }
   // entries in vocabulary order (rank by index), then sequential Z and inverse CDF (R11)
@@ -530,14 +763,122 @@ __global__ void __launch_bounds__(256) sv_fverify_kernel(const __grid_constant__
   }
 }
 
+// KF3w: the residual max(0, p'_t - p'_d) (or the bonus p'_t) of sequences whose row N has a
+// nucleus wider than 32 tokens -- one CTA per sequence, full-row pass in threshold form: every
+// thread sums a contiguous vocabulary chunk (fp64, sequential), a fixed-order prefix over the
+// chunks gives Z and the chunk holding the crossing of u_s Z, which is rescanned (R11)
+template <typename T>
+__global__ void __launch_bounds__(512) sv_fwide_sample_kernel(const __grid_constant__ FilterArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int NT = 512;
+  __shared__ double s_sum[NT], s_pre[NT];
+  __shared__ int s_last[NT];
+  __shared__ int s_j;
+  __shared__ double s_Z, s_th;
+  const int64_t b = blockIdx.x;
+  if (a.out_tok[b] != kPendingWide) return;
+  const int tid = threadIdx.x, k = a.k, V = a.V;
+  const int N = a.n_accept[b], g = a.gamma[b];
+  const Thr lt = load_thr(a.tl + b * (k + 1) + N);
+  const T *xt = reinterpret_cast<const T *>(a.t) + b * a.t_sb + (int64_t)N * a.t_si;
+  const bool resid = N < g;
+  const FList *LdN = a.dl + b * k + N;
+  const bool dwide = resid && LdN->wide;  // else the <= 32 draft entries, walked in index order
+  const Thr ld = dwide ? load_thr(LdN) : lt;
+  const T *xd = dwide ? reinterpret_cast<const T *>(a.d) + b * a.d_sb + (int64_t)N * a.d_si : xt;
+  __shared__ int s_di[32];
+  __shared__ double s_dp[32];
+  const int nd = (resid && !dwide) ? LdN->n : 0;
+  if (tid < nd) {
+    const int vi = LdN->idx[tid];
+    int rank = 0;
+    for (int l = 0; l < nd; ++l) rank += LdN->idx[l] < vi;
+    s_di[rank] = vi;
+    s_dp[rank] = LdN->p[tid];
+  }
+  __syncthreads();
+  const int chunk = (V + NT - 1) / NT, v0 = min(V, tid * chunk), v1 = min(V, v0 + chunk);
+  int q = 0;  // first draft entry with index >= v (list-mode draft rows; v ascends within a pass)
+  auto rv = [&](int v) {
+    const double pt = thr_p(xt, v, lt);
+    if (!resid || !(pt > 0.0)) return pt;
+    if (dwide) return fmax(0.0, pt - thr_p(xd, v, ld));
+    while (q < nd && s_di[q] < v) ++q;
+    return fmax(0.0, pt - ((q < nd && s_di[q] == v) ? s_dp[q] : 0.0));
+  };
+  double sum = 0.0;
+  int lastp = -1;
+  for (int v = v0; v < v1; ++v) {
+    const double r = rv(v);
+    if (r > 0.0) {
+      sum += r;
+      lastp = v;
+    }
+  }
+  s_sum[tid] = sum;
+  s_last[tid] = lastp;
+  __syncthreads();
+  if (tid == 0) {
+    double c = 0.0;
+    for (int j = 0; j < NT; ++j) {
+      s_pre[j] = c;
+      c += s_sum[j];
+    }
+    const double us = u24(sv_philox(a.seed, a.offset, a.seq_base + b, N).y);
+    const double th = us * c;
+    int jc = -1;
+    for (int j = 0; j < NT; ++j)
+      if (s_sum[j] > 0.0 && s_pre[j] + s_sum[j] > th) {
+        jc = j;
+        break;
+      }
+    s_j = jc;
+    s_Z = c;
+    s_th = th;
+  }
+  __syncthreads();
+  const int jc = s_j;
+  if (jc < 0) {  // rounding left no crossing (or Z = 0): the last positive entry (R11 fallback)
+    if (tid == 0) {
+      int tok = -1;
+      for (int j = NT - 1; j >= 0 && tok < 0; --j) tok = s_last[j];
+      const double Z = s_Z;
+      a.out_tok[b] = tok;
+      if (a.resid) a.resid[b] = (float)Z;
+      if (a.status && !(Z > 0.0)) a.status[b] |= 32;
+    }
+    return;
+  }
+  if (tid != jc) return;
+  const double th = s_th;
+  double cum = s_pre[jc];
+  int tok = s_last[jc];
+  q = 0;
+  for (int v = v0; v < v1; ++v) {
+    const double r = rv(v);
+    if (!(r > 0.0)) continue;
+    cum += r;
+    if (cum > th) {
+      tok = v;
+      break;
+    }
+  }
+  a.out_tok[b] = tok;
+  if (a.resid) a.resid[b] = (float)s_Z;
+}
+
 }  // namespace
 
 cudaError_t launch_filter_score(const FilterArgs &a, cudaStream_t st) {
   const unsigned rows = (unsigned)((int64_t)a.B * a.k);
-  const cudaError_t e = a.bf16 ? launch_k(sv_topk_kernel<__nv_bfloat16>, dim3(rows, 2), dim3(kTopKThreads), 0, st, a, 0)
-                               : launch_k(sv_topk_kernel<float>, dim3(rows, 2), dim3(kTopKThreads), 0, st, a, 0);
+  cudaError_t e = a.bf16 ? launch_k(sv_topk_kernel<__nv_bfloat16>, dim3(rows, 2), dim3(kTopKThreads), 0, st, a, 0)
+                         : launch_k(sv_topk_kernel<float>, dim3(rows, 2), dim3(kTopKThreads), 0, st, a, 0);
   if (e != cudaSuccess) return e;
-  return launch_k(sv_fscore_kernel, dim3((rows + 7) / 8), dim3(256), 0, st, a);
+  e = launch_k(sv_fscore_kernel, dim3((rows + 7) / 8), dim3(256), 0, st, a);
+  if (e != cudaSuccess || a.top_k != 0) return e;  // wide rows exist only without top_k
+  return a.bf16 ? launch_k(sv_fwide_score_kernel<__nv_bfloat16>, dim3(rows), dim3(512), 0, st, a)
+                : launch_k(sv_fwide_score_kernel<float>, dim3(rows), dim3(512), 0, st, a);
 }
 
 cudaError_t launch_filter_verify(const FilterArgs &a, cudaStream_t st) {
@@ -545,7 +886,12 @@ cudaError_t launch_filter_verify(const FilterArgs &a, cudaStream_t st) {
   cudaError_t e = a.bf16 ? launch_k(sv_topk_kernel<__nv_bfloat16>, dim3(rows), dim3(kTopKThreads), 0, st, a, 2)
                          : launch_k(sv_topk_kernel<float>, dim3(rows), dim3(kTopKThreads), 0, st, a, 2);
   if (e != cudaSuccess) return e;
-  return launch_k(sv_fverify_kernel, dim3((unsigned)((a.B + 7) / 8)), dim3(256), 0, st, a);
+  const dim3 gv((unsigned)((a.B + 7) / 8));
+  e = a.bf16 ? launch_k(sv_fverify_kernel<__nv_bfloat16>, gv, dim3(256), 0, st, a)
+             : launch_k(sv_fverify_kernel<float>, gv, dim3(256), 0, st, a);
+  if (e != cudaSuccess || a.top_k != 0) return e;
+  return a.bf16 ? launch_k(sv_fwide_sample_kernel<__nv_bfloat16>, dim3((unsigned)a.B), dim3(512), 0, st, a)
+                : launch_k(sv_fwide_sample_kernel<float>, dim3((unsigned)a.B), dim3(512), 0, st, a);
 }
 
 }  // namespace sv

@@ -153,9 +153,16 @@ cudaError_t launch_verify(const VerifyArgs &a, cudaStream_t st);
 
 // NEXT-2: sampling filters (sv_filter.cu).  A filtered distribution: at most 32 entries.
 struct FList {
-  int32_t n, st;     // kept entries, row status bits
+  int32_t n, st;     // kept entries (0 for a wide row), row status bits
   int32_t idx[32];   // vocabulary indices, sorted by (probability desc, index asc)
   double p[32];      // renormalised filtered probabilities
+  // threshold form of the kept set, filled for every row: v is kept iff key(v) > th_key, or
+  // key(v) == th_key and v <= th_idx (a prefix in (key desc, index asc) order); then
+  // p'(v) = exp(x_v / tau - y0) / tot / s.  wide = 1: nucleus larger than 32 tokens, only the
+  // threshold form is held
+  uint32_t th_key;
+  int32_t th_idx, wide, pad_;
+  double tau, y0, tot, s;
 };
 struct FilterArgs {
   const void *d, *c, *t;

@@ -13,7 +13,8 @@ for (B, k, V, dt) in [(3, 4, 3001, "bf16"), (2, 3, 1001, "f32")]:
     sv.sv_score_schedule(D, C, tok, L, 1.0, 1.0, prof, workspace=pipe.workspace)
     gs = sv.sv_score_filtered(D, C, tok, 20, 0.8, 0.7, 0.7, prof)
     sv.sd_verify_filtered(T, tok, pipe.sched_out["gamma"], gs["fworkspace"], 20, 0.8, 0.7, 1, 0)
-    gs = sv.sv_score_filtered(D, C, tok, 0, 0.9, 0.6, 0.6, prof)
+    gs = sv.sv_score_filtered(D, C, tok, 0, 0.9, 1.0, 1.0, prof)  # nucleus-only: wide rows at tau 1
+    sv.sd_verify_filtered(T, tok, pipe.sched_out["gamma"], gs["fworkspace"], 0, 0.9, 1.0, 1, 0, D=D)
     g = pipe.sched_out["gamma"]
     gn = g.cpu().numpy()
     rows = torch.cat([T[b, : gn[b] + 1] for b in range(B)])

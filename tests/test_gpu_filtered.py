@@ -57,7 +57,7 @@ def test_filtered_parity(sv, B, k, V, dtype, top_k, top_p, tau):
         assert np.float32(want) == g["p_hat"][idx]
     gam = rng.integers(0, k + 1, B).astype(np.int32)
     gv = sv.sd_verify_filtered(T, tk, torch.from_numpy(gam).cuda(), gs["fworkspace"], top_k, top_p, tau, seed=5,
-                               offset=2)
+                               offset=2, D=D)
     torch.cuda.synchronize()
     gv = {n: v.cpu().numpy() for n, v in gv.items()}
     rv = verify_filtered(Dd, Td, tok, gam, tau, tau, top_k, top_p, 5, 2)
@@ -80,35 +80,105 @@ def test_filtered_bad_configs(sv):
             sv.sv_score_filtered(D, C, tok, top_k, top_p)
 
 
-@pytest.mark.parametrize("V,dtype,tau", [(32000, "f32", 0.6), (32000, "bf16", 0.6), (4096, "bf16", 1.0)])
+def _cut_margin(x, tau, top_p):
+    """Distance of the oracle's sequential cumulative to top_p at the nucleus cut (the last two
+    prefix sums): inside ~1e-6 the GPU's normaliser rounding may move the cut by one token."""
+    _, keep = filter_dist(x, tau, 0, top_p)
+    y = np.asarray(x, dtype=np.float64) / tau
+    order = np.lexsort((np.arange(y.size), -y))
+    p = np.exp(y[order] - y[order[0]])
+    p = p / p.sum()
+    c = np.cumsum(p)
+    n = len(keep)
+    return min(abs(c[n - 1] - top_p), abs(c[n - 2] - top_p) if n > 1 else 1.0)
+
+
+@pytest.mark.parametrize("V,dtype,tau", [(32000, "f32", 0.6), (32000, "bf16", 0.6), (4096, "bf16", 1.0),
+                                         (32000, "f32", 1.0), (152064, "bf16", 1.0)])
 def test_nucleus_only_llama_setting(sv, V, dtype, tau):
-    """top_k = 0, top_p = 0.9 (P L739-740, Llama): exact when the nucleus has <= 32 tokens; larger
-    nuclei are flagged SV_ROW_FILTER_UNSUPPORTED (256) with the error sentinels."""
-    B, k = 6, 4
+    """top_k = 0, top_p = 0.9 (P L739-740, Llama) over the FULL distribution, any nucleus size:
+    <= 32 tokens as lists, larger nuclei in threshold form (mass-weighted radix select, full-row
+    scoring) -- every row against the filtered oracle."""
+    B, k = (6, 4) if V < 100000 else (2, 3)
     x = synth.make_inputs(B, k, V, dtype, seed=4321 + V)
     Dd, Cd, Td = H.oracle_inputs(x)
     rng = np.random.default_rng(V)
     tok = np.zeros((B, k), dtype=np.int32)
     big = np.zeros((B, k), dtype=bool)
+    tie = np.zeros((B, k), dtype=bool)
     for b in range(B):
         for i in range(k):
             p, keep_d = filter_dist(Dd[b, i], tau, 0, 0.9)
             _, keep_c = filter_dist(Cd[b, i], tau, 0, 0.9)
             big[b, i] = len(keep_d) > 32 or len(keep_c) > 32
+            tie[b, i] = min(_cut_margin(Dd[b, i], tau, 0.9), _cut_margin(Cd[b, i], tau, 0.9)) < 1e-6
             tok[b, i] = rng.choice(V, p=p / p.sum())
     D, C, T, _ = H.to_torch(x)
     tk = torch.from_numpy(tok).cuda()
     pd = synth.load_profile()
     gs = sv.sv_score_filtered(D, C, tk, 0, 0.9, tau, tau, sv.Profile.from_dict(pd))
     torch.cuda.synchronize()
-    g = {n: gs[n].cpu().numpy() for n in ("S", "A", "KL", "status")}
+    g = {n: gs[n].cpu().numpy() for n in ("S", "A", "KL", "status", "draft_ptok")}
     rs = score_filtered(Dd, Cd, tok, tau, tau, 0, 0.9)
-    flagged = (g["status"] & 256) != 0
-    assert np.array_equal(flagged, big), (flagged, big)
-    ok = ~big & (rs["status"] == 0)
+    assert np.array_equal(g["status"], rs["status"])
+    ok = (rs["status"] == 0) & ~tie
     for n in ("S", "A", "KL"):
         assert H.close(g[n][ok], rs[n][ok]).all(), (n, g[n][ok], rs[n][ok])
-    print("rows with a nucleus > 32:", int(big.sum()), "of", big.size)
+    assert H.close(g["draft_ptok"][ok], rs["pd_tok"][ok]).all()
+    print("rows with a nucleus > 32:", int(big.sum()), "of", big.size, "cut ties:", int(tie.sum()))
+
+
+@pytest.mark.parametrize("V,dtype,tau", [(4096, "bf16", 1.0), (32000, "f32", 1.0), (32000, "bf16", 0.8)])
+def test_nucleus_wide_verify(sv, V, dtype, tau):
+    """sd_verify_filtered, nucleus-only, with nuclei wider than 32 tokens on draft and target rows:
+    accept tests in threshold form and the full-row residual / bonus sample against the oracle;
+    without the draft logits the sequences that need a wide draft row are flagged 256."""
+    B, k = 8, 4
+    x = synth.make_inputs(B, k, V, dtype, seed=97 + V)
+    Dd, Cd, Td = H.oracle_inputs(x)
+    rng = np.random.default_rng(V + 1)
+    tok = np.zeros((B, k), dtype=np.int32)
+    wide_d = np.zeros((B, k), dtype=bool)
+    wide_t = np.zeros((B, k + 1), dtype=bool)
+    tie = np.zeros(B, dtype=bool)
+    for b in range(B):
+        for i in range(k):
+            p, keep = filter_dist(Dd[b, i], tau, 0, 0.9)
+            wide_d[b, i] = len(keep) > 32
+            tie[b] |= _cut_margin(Dd[b, i], tau, 0.9) < 1e-6
+            tok[b, i] = rng.choice(V, p=p / p.sum())
+        for i in range(k + 1):
+            wide_t[b, i] = len(filter_dist(Td[b, i], tau, 0, 0.9)[1]) > 32
+            tie[b] |= _cut_margin(Td[b, i], tau, 0.9) < 1e-6
+    assert wide_d.any() and wide_t.any()
+    D, C, T, _ = H.to_torch(x)
+    tk = torch.from_numpy(tok).cuda()
+    gs = sv.sv_score_filtered(D, C, tk, 0, 0.9, tau, tau, sv.Profile.from_dict(synth.load_profile()))
+    gam = rng.integers(0, k + 1, B).astype(np.int32)
+    gam[0], gam[1] = k, 0
+    gg = torch.from_numpy(gam).cuda()
+    gv = sv.sd_verify_filtered(T, tk, gg, gs["fworkspace"], 0, 0.9, tau, seed=9, offset=1, D=D)
+    torch.cuda.synchronize()
+    gv = {n: v.cpu().numpy() for n, v in gv.items()}
+    rv = verify_filtered(Dd, Td, tok, gam, tau, tau, 0, 0.9, 9, 1)
+    tie |= rv["margin"] < 1e-6
+    assert (gv["status"][~tie] == 0).all()
+    assert np.array_equal(gv["n_accept"][~tie], rv["n_accept"][~tie])
+    assert np.array_equal(gv["out_tok"][~tie], rv["out_tok"][~tie])
+    assert H.close(gv["resid_mass"][~tie], rv["resid_mass"][~tie]).all()
+    r_ok = ~np.isnan(rv["accept_ratio"]) & ~tie[:, None]
+    assert H.close(gv["accept_ratio"][r_ok], rv["accept_ratio"][r_ok]).all()
+    wide_seq = np.array([wide_t[b, rv["n_accept"][b]] or (rv["n_accept"][b] < gam[b] and wide_d[b, rv["n_accept"][b]])
+                         for b in range(B)])
+    print("sequences sampled in threshold form:", int(wide_seq.sum()), "of", B, "ties:", int(tie.sum()))
+    # without the draft logits: a sequence whose draft row 0 is wide and gamma >= 1 cannot be tested
+    nv = sv.sd_verify_filtered(T, tk, gg, gs["fworkspace"], 0, 0.9, tau, seed=9, offset=1)
+    torch.cuda.synchronize()
+    nst = nv["status"].cpu().numpy()
+    need = (gam >= 1) & wide_d[:, 0]
+    assert ((nst[need] & 256) != 0).all()
+    no_wide = np.array([not wide_d[b, :gam[b]].any() for b in range(B)])
+    assert ((nst[no_wide] & 256) == 0).all()
 
 
 def test_nucleus_only_verify(sv):
@@ -130,7 +200,7 @@ def test_nucleus_only_verify(sv):
     tk = torch.from_numpy(tok).cuda()
     gs = sv.sv_score_filtered(D, C, tk, 0, 0.9, tau, tau, sv.Profile.from_dict(synth.load_profile()))
     gam = np.full(B, k, dtype=np.int32)
-    gv = sv.sd_verify_filtered(T, tk, torch.from_numpy(gam).cuda(), gs["fworkspace"], 0, 0.9, tau, seed=9, offset=1)
+    gv = sv.sd_verify_filtered(T, tk, torch.from_numpy(gam).cuda(), gs["fworkspace"], 0, 0.9, tau, seed=9, offset=1, D=D)
     torch.cuda.synchronize()
     gv = {n: v.cpu().numpy() for n, v in gv.items()}
     rv = verify_filtered(Dd, Td, tok, gam, tau, tau, 0, 0.9, 9, 1)
