@@ -208,3 +208,37 @@ def test_nucleus_only_verify(sv):
     assert np.array_equal(gv["n_accept"][~tie], rv["n_accept"][~tie])
     assert np.array_equal(gv["out_tok"][~tie], rv["out_tok"][~tie])
     assert H.close(gv["resid_mass"][~tie], rv["resid_mass"][~tie]).all()
+
+
+def test_nucleus_wide_closed_form(sv):
+    """Geometric rows p_j ∝ r^j on a shuffled vocabulary (fp32 logits): nucleus size
+    ceil(log(1 - top_p (1 - r^V)) / log r) > 32, so the GPU holds them in threshold form; with
+    draft = companion, S = 1, A = 1, KL = 0 and p'_d(t) = r^j (1 - r) / (1 - r^n) for the token of
+    rank j; a token just outside the nucleus is DRAFT_ZERO."""
+    import math
+    r, V, tp = 0.995, 5000, 0.9
+    n = math.ceil(math.log(1 - tp * (1 - r ** V)) / math.log(r))
+    rng = np.random.default_rng(3)
+    B, k = 2, 3
+    perm = [rng.permutation(V) for _ in range(B * k)]
+    x = np.empty((B, k, V), dtype=np.float32)
+    for j in range(B * k):
+        x[j // k, j % k, perm[j]] = (np.arange(V) * math.log(r)).astype(np.float32)
+    ranks = np.array([[3, n - 1, 0], [n, 17, n - 2]])
+    tok = np.array([[perm[b * k + i][ranks[b, i]] for i in range(k)] for b in range(B)], dtype=np.int32)
+    D = torch.from_numpy(x).cuda()
+    gs = sv.sv_score_filtered(D, D, torch.from_numpy(tok).cuda(), 0, tp, 1.0, 1.0)
+    torch.cuda.synchronize()
+    g = {n_: gs[n_].cpu().numpy() for n_ in ("S", "A", "KL", "draft_ptok", "status")}
+    xs = x.astype(np.float64)
+    for b in range(B):
+        for i in range(k):
+            if ranks[b, i] >= n:
+                assert g["status"][b, i] == 8
+                continue
+            assert g["status"][b, i] == 0
+            assert abs(g["S"][b, i] - 1.0) < 1e-6 and g["A"][b, i] == 1.0 and abs(g["KL"][b, i]) < 1e-6
+            # the fp32-rounded logits make p_j slightly off the closed form: compare with it at 1e-5
+            j = ranks[b, i]
+            want = math.exp(xs[b, i, perm[b * k + i][j]]) * (1 - r) / (1 - r ** n)
+            assert abs(g["draft_ptok"][b, i] - want) <= 1e-5 * want

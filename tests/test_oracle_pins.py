@@ -471,6 +471,28 @@ def test_filter_identity_idempotence_support():
     assert list(keep) == [1, 2] and q[3] == 0.0
 
 
+def test_filter_wide_nucleus_closed_form():
+    """A nucleus of hundreds of tokens (the case the GPU holds in threshold form): geometric
+    probabilities p_j ∝ r^j on a shuffled vocabulary; the cumulative of the sorted prefix is
+    (1 - r^n) / (1 - r^V), so the nucleus size is the closed form ceil(log(1 - top_p (1 - r^V)) / log r)
+    and the kept mass renormalises to p_j (1 - r) / (1 - r^n)."""
+    from oracle.filtered import filter_dist
+    rng = np.random.default_rng(17)
+    for r, V, tp in ((0.995, 5000, 0.9), (0.98, 3000, 0.8), (0.9993, 20000, 0.95)):
+        n_exact = math.log(1 - tp * (1 - r ** V)) / math.log(r)
+        assert abs(n_exact - round(n_exact)) > 1e-6  # not a rounding tie
+        n = math.ceil(n_exact)
+        perm = rng.permutation(V)
+        x = np.empty(V)
+        x[perm] = np.arange(V) * math.log(r)  # rank j sits at vocabulary index perm[j]
+        q, keep = filter_dist(x, 1.0, 0, tp)
+        assert len(keep) == n > 32
+        assert list(keep) == list(perm[:n])
+        want = r ** np.arange(n) * (1 - r) / (1 - r ** n)
+        assert np.allclose(q[perm[:n]], want, rtol=1e-10, atol=0)
+        assert np.count_nonzero(q) == n
+
+
 def test_filter_score_identities():
     """Filtered S / A / KL keep the unfiltered identities (S L233-235): identical rows -> S = 1,
     A = 1, KL = 0; S = 1 - TV; A = 1 whenever p'_c(t) >= p'_d(t)."""
