@@ -481,6 +481,24 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     f_ms_step = f0.elapsed_time(f1) / f_steps
 
+    # the Llama setting (Table 5: nucleus only, top_p 0.9, tau 0.6; any nucleus size -- lists up to
+    # 32 tokens, threshold form beyond)
+    def nstep(j):
+        D, C, T, tok = sets[j & 1]
+        fs = sv.sv_score_filtered(D, C, tok, 0, 0.9, 0.6, 0.6, prof, fworkspace=fws, stream=stream)
+        g = sv.sv_schedule(fs["p_hat"], L, out={"gamma": fgam}, stream=stream)["gamma"]
+        return sv.sd_verify_filtered(T, tok, g, fws, 0, 0.9, 0.6, 0xC0FFEE, j, seq_base, stream=stream, D=D)
+
+    for j in range(args.warmup):
+        nstep(j)
+    barrier()
+    f0.record(stream)
+    for j in range(f_steps):
+        nstep(args.warmup + j)
+    f1.record(stream)
+    barrier()
+    n_ms_step = f0.elapsed_time(f1) / f_steps
+
     # ---------------- NEXT-1: the paper's batch greedy schedule (one CTA: gains, bitonic sort,
     # greedy walk) on this step's p_hat, latency L[n] over the batch's total target positions
     Lg = torch.tensor(synth.latency_table(B * (k + 1) + 1, base=4.0, knee=2 * B, slope=4.0 / B),
@@ -616,6 +634,11 @@ def run_ours(args, rank, world, local_rank):
                          "filters": "top_k 20, top_p 0.8, tau 0.7 on draft / companion / target (P L731-743)",
                          "note": "NEXT-2: radix-select top-k per row + list arithmetic; output allocations per "
                                  "call included"},
+            "filtered_nucleus": {"value": world * B * k / (n_ms_step * 1e-3), "unit": "positions/s",
+                                 "ms_per_step": n_ms_step,
+                                 "filters": "top_k 0, top_p 0.9, tau 0.6 (the Llama setting, P L739-740)",
+                                 "note": "NEXT-2 nucleus-only: lists up to 32 tokens, threshold form (mass-"
+                                         "weighted radix select, full-row passes) beyond"},
             "batch_greedy": {"us_per_call": greedy_us, "mean_gamma": greedy_mean_gamma,
                              "latency": f"L[n] = 4 + (4/B) max(0, n - 2B) over the batch's target positions",
                              "note": "NEXT-1 sv_schedule mode BATCH_GREEDY on the step's p_hat (B*k candidates)"},

@@ -61,6 +61,24 @@ template <> struct KeyOf<float> {
   __device__ static uint32_t value_bits(K k) { return (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k; }
 };
 
+// order-preserving keys of the 8 consecutive elements v0 .. v0+7 (L2-resident re-reads: plain
+// vector loads when the row is 16-byte aligned; entries at or beyond V are left 0 -- callers mask)
+template <typename T>
+__device__ __forceinline__ void load8(const T *x, int v0, int V, bool vec, uint32_t (&kk)[8]) {
+  using KO = KeyOf<T>;
+  if (vec && v0 + 8 <= V) {
+    uint4 w[sizeof(T) / 2];
+#pragma unroll
+    for (int q = 0; q < (int)(sizeof(T) / 2); ++q) w[q] = __ldg(reinterpret_cast<const uint4 *>(x + v0) + q);
+    const T *e = reinterpret_cast<const T *>(w);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) kk[j] = KO::key(e, j);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) kk[j] = v0 + j < V ? KO::key(x, v0 + j) : 0u;
+  }
+}
+
 // Row r of the set the launch processes (draft / companion rows for the score, target rows
 // 0..gamma_b for the verify); returns false for rows that are skipped.
 __device__ __forceinline__ bool row_of(const FilterArgs &a, int64_t r, int which, const void *&base, int64_t &off,
@@ -310,9 +328,13 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
     float lsum = 0.f;
     if (xmax > -FLT_MAX) {
       const float nm = -xmax * c2;
-      for (int e = tid; e < V; e += NT) {
-        const float xv = __uint_as_float(KO::value_bits(KO::key(x, e)));
-        lsum += ex2(fmaf(xv, c2, nm));
+      const bool vec = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+      for (int v0 = tid * 8; v0 < V; v0 += NT * 8) {
+        uint32_t kk[8];
+        load8(x, v0, V, vec, kk);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (v0 + j < V) lsum += ex2(fmaf(KO::value(kk[j]), c2, nm));
       }
     }
     double v = warp_sum_d((double)lsum);
@@ -395,7 +417,138 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
   }
   __syncthreads();
   if (!s_wide) return;
-  // ---- nucleus larger than 32 tokens: the threshold form directly.  Mass-weighted radix select
+  // ---- nucleus larger than 32 tokens (threshold form).  Fast path: a conservative lower bound L
+  // of the cut key from digit histograms of counts and 2^-31 fixed-point masses (native 32-bit
+  // shared atomics; truncation only lowers a bin's mass, so "measured mass of keys >= L reaches
+  // top_p + 1e-5" guarantees the nucleus lies inside {key >= L}); refined digit by digit until at
+  // most kCandCap keys are >= L.  Those candidates are gathered, sorted by (key desc, index asc),
+  // and the cut is taken exactly as the oracle does: p_j = exp(y_j - y0) / tot in fp64 and the
+  // sequential cumulative >= top_p.  Deterministic (the result does not depend on L).
+  {
+    __shared__ unsigned s_msum[256];
+    __shared__ unsigned long long s_am;
+    __shared__ unsigned s_ac;
+    __shared__ int s_state;  // 0 refine, 1 gather with L = s_prefix, 2 fall back
+    __shared__ double s_pm[kCandCap];
+    const double y0 = s_y0, tot = s_lfull;
+    const float c2 = (float)(1.4426950408889634 / tau), nm = -KO::value(c_key[0]) * c2;
+    const float scale31 = (float)(2147483648.0 / tot);
+    const unsigned long long target = (unsigned long long)(((double)a.top_p + 1e-5) * 2147483648.0);
+    const bool vec = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    if (tid == 0) {
+      s_prefix = 0;
+      s_mask = 0;
+      s_am = 0ull;
+      s_ac = 0u;
+      s_state = 0;
+      s_ncand = 0;
+    }
+    for (int shift = KO::kBits - 8; shift >= 0; shift -= 8) {
+      for (int j = tid; j < 256; j += NT) {
+        hist[j] = 0u;
+        s_msum[j] = 0u;
+      }
+      __syncthreads();
+      const K prefix = s_prefix, mask = s_mask;
+      for (int v0 = tid * 8; v0 < V; v0 += NT * 8) {
+        uint32_t kk[8];
+        load8(x, v0, V, vec, kk);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (v0 + j < V && (kk[j] & mask) == prefix) {
+            const unsigned d = (kk[j] >> shift) & 255u;
+            atomicAdd(&hist[d], 1u);
+            const unsigned mf = __float2uint_rz(ex2(fmaf(KO::value(kk[j]), c2, nm)) * scale31);
+            if (mf) atomicAdd(&s_msum[d], mf);
+          }
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        unsigned long long cm = s_am;
+        unsigned cc = s_ac;
+        int d = 255;
+        for (; d >= 0; --d) {
+          cm += s_msum[d];
+          cc += hist[d];
+          if (cm >= target) break;
+        }
+        if (d < 0) s_state = 2;  // top_p + margin not reached (top_p ~ 1): fall back
+        else if (cc <= (unsigned)kCandCap) {
+          s_state = 1;
+          s_prefix = prefix | ((K)d << shift);  // L: the lowest key of digit d under the prefix
+        } else if (shift == 0) s_state = 2;  // more than kCandCap keys in the nucleus
+        else {
+          s_am = cm - s_msum[d];
+          s_ac = cc - hist[d];
+          s_prefix = prefix | ((K)d << shift);
+          s_mask = mask | ((K)255u << shift);
+        }
+      }
+      __syncthreads();
+      if (s_state) break;
+    }
+    if (s_state == 1) {
+      const K L = s_prefix;
+      for (int v0 = tid * 8; v0 < V; v0 += NT * 8) {
+        uint32_t kk[8];
+        load8(x, v0, V, vec, kk);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (v0 + j < V && kk[j] >= L) {
+            const int slot = atomicAdd(&s_ncand, 1);
+            s_cand[slot] = ((unsigned long long)kk[j] << 32) | (0xFFFFFFFFu - (uint32_t)(v0 + j));
+          }
+      }
+      __syncthreads();
+      const int nc = s_ncand;
+      int np2 = 1;
+      while (np2 < nc) np2 <<= 1;
+      for (int j = nc + tid; j < np2; j += NT) s_cand[j] = 0ull;
+      __syncthreads();
+      for (int size = 2; size <= np2; size <<= 1) {  // bitonic sort, descending composite
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+          for (int j = tid; j < np2; j += NT) {
+            const int o = j ^ stride;
+            if (o > j) {
+              const bool down = (j & size) == 0;
+              const unsigned long long u = s_cand[j], v = s_cand[o];
+              if ((u < v) == down) {
+                s_cand[j] = v;
+                s_cand[o] = u;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      }
+      for (int j = tid; j < nc; j += NT) {
+        double pj = exp((double)KO::value((K)(s_cand[j] >> 32)) / tau - y0);
+        s_pm[j] = pj / tot;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double c = 0.0;
+        int n = -1;
+        for (int j = 0; j < nc; ++j) {
+          c += s_pm[j];
+          if (c >= (double)a.top_p) {
+            n = j;
+            break;
+          }
+        }
+        if (n < 0) s_state = 2;  // rounding: the bound was not conservative enough
+        else {
+          out->th_key = (uint32_t)(s_cand[n] >> 32);
+          out->th_idx = (int)(0xFFFFFFFFu - (uint32_t)s_cand[n]);
+          out->s = c;
+        }
+      }
+      __syncthreads();
+      if (s_state == 1) return;
+    }
+  }
+  // ---- fallback (nuclei of more than kCandCap tokens, top_p ~ 1): mass-weighted radix select
   // of the cut key theta on the order-preserving key, 8 bits per pass from the top: per digit the
   // mass sum exp(y_v - y0) / tot of the keys under the current prefix, in 2^-60 fixed point
   // (integer shared atomics: order-independent, exact bin sums, deterministic), into 8
@@ -409,6 +562,10 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
     __shared__ double s_s;
     const double y0 = s_y0, tot = s_lfull;
     const unsigned long long tp_fix = (unsigned long long)((double)a.top_p * kFix);
+    // per-element mass with the normaliser's own fp32 terms: 2^{(x - x_max) log2e / tau} / tot
+    const float c2 = (float)(1.4426950408889634 / tau), nm = -KO::value(c_key[0]) * c2;
+    const float scale = (float)(kFix / tot);
+    const bool vec = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
     if (tid == 0) {
       s_prefix = 0;
       s_mask = 0;
@@ -421,11 +578,15 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
       __syncthreads();
       const K prefix = s_prefix, mask = s_mask;
       unsigned long long *mine = wm + (wid & 7) * 256;
-      for (int e = tid; e < V; e += NT) {
-        const K kk = KO::key(x, e);
-        if ((kk & mask) == prefix) {
-          const double m = exp((double)KO::value(kk) / tau - y0) / tot;
-          atomicAdd(mine + ((kk >> shift) & 255u), (unsigned long long)(m * kFix));
+      for (int v0 = tid * 8; v0 < V; v0 += NT * 8) {
+        uint32_t kk[8];
+        load8(x, v0, V, vec, kk);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (v0 + j < V && (kk[j] & mask) == prefix) {
+            const unsigned long long mf = __float2ull_rz(ex2(fmaf(KO::value(kk[j]), c2, nm)) * scale);
+            if (mf) atomicAdd(mine + ((kk[j] >> shift) & 255u), mf);
+          }
         }
       }
       __syncthreads();
@@ -532,13 +693,16 @@ __device__ __forceinline__ Thr load_thr(const FList *L) { return Thr{L->th_key, 
 // p'(v) of a row in threshold form: the kept set and the same fp64 operations as the list entries
 // (exp(y - y0), / tot, / s), so list values are reproduced bit for bit
 template <typename T>
-__device__ __forceinline__ double thr_p(const T *x, int v, const Thr &L) {
+__device__ __forceinline__ double thr_pk(uint32_t kk, int v, const Thr &L) {
   using KO = KeyOf<T>;
-  const uint32_t kk = KO::key(x, v);
   if (kk < L.key || (kk == L.key && v > L.idx)) return 0.0;
   double p = exp((double)KO::value(kk) / L.tau - L.y0);
   p = p / L.tot;
   return p / L.s;
+}
+template <typename T>
+__device__ __forceinline__ double thr_p(const T *x, int v, const Thr &L) {
+  return thr_pk<T>(KeyOf<T>::key(x, v), v, L);
 }
 
 __device__ __forceinline__ double block_sum_d(double v, double *red) {  // fixed order: warps, then 0..nw-1
@@ -632,13 +796,20 @@ __global__ void __launch_bounds__(512) sv_fwide_score_kernel(const __grid_consta
   const int t = a.tok[r];
   if (t < 0 || t >= a.V) st |= 4;
   double S = 0.0, KL = 0.0;
+  const bool vec = ((reinterpret_cast<uintptr_t>(xd) | reinterpret_cast<uintptr_t>(xc)) & 15) == 0;
   if (!st)
-    for (int v = threadIdx.x; v < a.V; v += blockDim.x) {
-      const double pd = thr_p(xd, v, ld);
-      if (pd > 0.0) {
-        const double pc = thr_p(xc, v, lc);
-        S += fmin(pd, pc);
-        KL += pc > 0.0 ? pd * log(pd / pc) : INFINITY;
+    for (int v0 = threadIdx.x * 8; v0 < a.V; v0 += blockDim.x * 8) {
+      uint32_t kd[8], kc[8];
+      load8(xd, v0, a.V, vec, kd);
+      load8(xc, v0, a.V, vec, kc);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double pd = v0 + j < a.V ? thr_pk<T>(kd[j], v0 + j, ld) : 0.0;
+        if (pd > 0.0) {
+          const double pc = thr_pk<T>(kc[j], v0 + j, lc);
+          S += fmin(pd, pc);
+          KL += pc > 0.0 ? pd * log(pd / pc) : INFINITY;
+        }
       }
     }
   S = block_sum_d(S, red);
@@ -798,22 +969,31 @@ __global__ void __launch_bounds__(512) sv_fwide_sample_kernel(const __grid_const
     s_dp[rank] = LdN->p[tid];
   }
   __syncthreads();
-  const int chunk = (V + NT - 1) / NT, v0 = min(V, tid * chunk), v1 = min(V, v0 + chunk);
+  // contiguous chunks of a multiple of 8 elements (vector loads of 8 keys)
+  const int chunk = (((V + NT - 1) / NT) + 7) & ~7, v0 = min(V, tid * chunk), v1 = min(V, v0 + chunk);
+  const bool vec = ((reinterpret_cast<uintptr_t>(xt) | reinterpret_cast<uintptr_t>(xd)) & 15) == 0;
   int q = 0;  // first draft entry with index >= v (list-mode draft rows; v ascends within a pass)
-  auto rv = [&](int v) {
-    const double pt = thr_p(xt, v, lt);
+  auto rv = [&](int v, uint32_t kt, uint32_t kd) {
+    const double pt = thr_pk<T>(kt, v, lt);
     if (!resid || !(pt > 0.0)) return pt;
-    if (dwide) return fmax(0.0, pt - thr_p(xd, v, ld));
+    if (dwide) return fmax(0.0, pt - thr_pk<T>(kd, v, ld));
     while (q < nd && s_di[q] < v) ++q;
     return fmax(0.0, pt - ((q < nd && s_di[q] == v) ? s_dp[q] : 0.0));
   };
   double sum = 0.0;
   int lastp = -1;
-  for (int v = v0; v < v1; ++v) {
-    const double r = rv(v);
-    if (r > 0.0) {
-      sum += r;
-      lastp = v;
+  for (int w0 = v0; w0 < v1; w0 += 8) {
+    uint32_t kt[8], kd[8];
+    load8(xt, w0, V, vec, kt);
+    if (dwide) load8(xd, w0, V, vec, kd);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (w0 + j >= v1) break;
+      const double r = rv(w0 + j, kt[j], dwide ? kd[j] : 0u);
+      if (r > 0.0) {
+        sum += r;
+        lastp = w0 + j;
+      }
     }
   }
   s_sum[tid] = sum;
@@ -855,13 +1035,20 @@ __global__ void __launch_bounds__(512) sv_fwide_sample_kernel(const __grid_const
   double cum = s_pre[jc];
   int tok = s_last[jc];
   q = 0;
-  for (int v = v0; v < v1; ++v) {
-    const double r = rv(v);
-    if (!(r > 0.0)) continue;
-    cum += r;
-    if (cum > th) {
-      tok = v;
-      break;
+  bool found = false;
+  for (int w0 = v0; w0 < v1 && !found; w0 += 8) {
+    uint32_t kt[8], kd[8];
+    load8(xt, w0, V, vec, kt);
+    if (dwide) load8(xd, w0, V, vec, kd);
+    for (int j = 0; j < 8 && w0 + j < v1; ++j) {
+      const double r = rv(w0 + j, kt[j], dwide ? kd[j] : 0u);
+      if (!(r > 0.0)) continue;
+      cum += r;
+      if (cum > th) {
+        tok = w0 + j;
+        found = true;
+        break;
+      }
     }
   }
   a.out_tok[b] = tok;

@@ -210,13 +210,15 @@ def test_nucleus_only_verify(sv):
     assert H.close(gv["resid_mass"][~tie], rv["resid_mass"][~tie]).all()
 
 
-def test_nucleus_wide_closed_form(sv):
+@pytest.mark.parametrize("r,V,tp", [(0.995, 5000, 0.9),      # 460 tokens: candidate sort
+                                    (0.9995, 20000, 0.9),    # 4604 tokens: radix fallback
+                                    (0.99, 3000, 0.99999)])  # top_p + margin > 1: radix fallback
+def test_nucleus_wide_closed_form(sv, r, V, tp):
     """Geometric rows p_j ∝ r^j on a shuffled vocabulary (fp32 logits): nucleus size
     ceil(log(1 - top_p (1 - r^V)) / log r) > 32, so the GPU holds them in threshold form; with
     draft = companion, S = 1, A = 1, KL = 0 and p'_d(t) = r^j (1 - r) / (1 - r^n) for the token of
-    rank j; a token just outside the nucleus is DRAFT_ZERO."""
+    rank j; a token outside the nucleus is DRAFT_ZERO."""
     import math
-    r, V, tp = 0.995, 5000, 0.9
     n = math.ceil(math.log(1 - tp * (1 - r ** V)) / math.log(r))
     rng = np.random.default_rng(3)
     B, k = 2, 3
@@ -224,7 +226,7 @@ def test_nucleus_wide_closed_form(sv):
     x = np.empty((B, k, V), dtype=np.float32)
     for j in range(B * k):
         x[j // k, j % k, perm[j]] = (np.arange(V) * math.log(r)).astype(np.float32)
-    ranks = np.array([[3, n - 1, 0], [n, 17, n - 2]])
+    ranks = np.array([[3, n - 5, 0], [n + 5, 17, n - 6]])  # clear of the cut (fp32 logits move it by ~1e-7)
     tok = np.array([[perm[b * k + i][ranks[b, i]] for i in range(k)] for b in range(B)], dtype=np.int32)
     D = torch.from_numpy(x).cuda()
     gs = sv.sv_score_filtered(D, D, torch.from_numpy(tok).cuda(), 0, tp, 1.0, 1.0)
