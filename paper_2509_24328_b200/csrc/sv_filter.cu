@@ -136,6 +136,9 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
     s_ntie = 0;
   }
   bool fast = false;
+  const double tau = (double)(which == 0 ? a.tau_d : which == 1 ? a.tau_c : a.tau_t);
+  const float c2n = (float)(1.4426950408889634 / tau);
+  float om = -FLT_MAX, ol = 0.f;
   // ---- fast path: the KK-th largest of the 512 thread maxima is a lower bound of the KK-th
   // largest key, so every top-KK element has key >= that bound; gather those few candidates
   // (second pass, an L2 hit) and sort them by (key desc, index asc).  Falls back to the radix
@@ -147,6 +150,8 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
     K tmax = 0;
     int bad = 0;
     constexpr int UF = 4;  // independent 16-byte loads in flight per thread
+    // nucleus-only: the full-row normaliser rides on this pass as a per-thread online sum
+    // ol = sum 2^{(x - om) log2e / tau}, rescaled when a unit raises the running max om
     for (int u0 = tid; u0 < units; u0 += UF * NT) {
       uint4 w[UF];
 #pragma unroll
@@ -158,11 +163,23 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
       for (int q = 0; q < UF; ++q) {
         if (u0 + q * NT >= units) continue;
         const T *e = reinterpret_cast<const T *>(&w[q]);
+        K um = 0;
 #pragma unroll
         for (int j = 0; j < EPU; ++j) {
           const K kk = KO::key(e, j);
-          tmax = kk > tmax ? kk : tmax;
+          um = kk > um ? kk : um;
           bad |= KO::bad(kk);
+        }
+        tmax = um > tmax ? um : tmax;
+        if (nucleus) {
+          const float umv = KO::value(um);
+          if (umv > om) {
+            ol *= ex2((om - umv) * c2n);
+            om = umv;
+          }
+          const float nm = -om * c2n;
+#pragma unroll
+          for (int j = 0; j < EPU; ++j) ol += ex2(fmaf(KO::value(KO::key(e, j)), c2n, nm));
         }
       }
     }
@@ -170,6 +187,14 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
       const K kk = KO::key(x, e);
       tmax = kk > tmax ? kk : tmax;
       bad |= KO::bad(kk);
+      if (nucleus) {
+        const float v = KO::value(kk);
+        if (v > om) {
+          ol *= ex2((om - v) * c2n);
+          om = v;
+        }
+        ol += ex2(fmaf(v, c2n, -om * c2n));
+      }
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) s_bad = 1;
     __syncthreads();
@@ -320,23 +345,12 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
     }
     __syncthreads();
   }
-  const double tau = (double)(which == 0 ? a.tau_d : which == 1 ? a.tau_c : a.tau_t);
-  if (nucleus) {  // full-row normaliser sum_v 2^{(x_v - x_max) log2e / tau} (L2 pass, fp64 block sum)
+  if (nucleus) {  // full-row normaliser sum_v 2^{(x_v - x_max) log2e / tau}: merge of the pass-1
+                  // online sums (fp64 block sum)
     K kmax = c_key[0];
     for (int j = 1; j < KK; ++j) kmax = c_key[j] > kmax ? c_key[j] : kmax;
-    const float xmax = KO::value(kmax), c2 = (float)(1.4426950408889634 / tau);
-    float lsum = 0.f;
-    if (xmax > -FLT_MAX) {
-      const float nm = -xmax * c2;
-      const bool vec = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
-      for (int v0 = tid * 8; v0 < V; v0 += NT * 8) {
-        uint32_t kk[8];
-        load8(x, v0, V, vec, kk);
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (v0 + j < V) lsum += ex2(fmaf(KO::value(kk[j]), c2, nm));
-      }
-    }
+    const float xmax = KO::value(kmax);
+    const float lsum = (xmax > -FLT_MAX && ol > 0.f) ? ol * ex2((om - xmax) * c2n) : 0.f;
     double v = warp_sum_d((double)lsum);
     if (lane == 0) s_lsum[wid] = v;
     __syncthreads();
@@ -417,36 +431,41 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
   }
   __syncthreads();
   if (!s_wide) return;
-  // ---- nucleus larger than 32 tokens (threshold form).  Fast path: a conservative lower bound L
-  // of the cut key from digit histograms of counts and 2^-31 fixed-point masses (native 32-bit
-  // shared atomics; truncation only lowers a bin's mass, so "measured mass of keys >= L reaches
-  // top_p + 1e-5" guarantees the nucleus lies inside {key >= L}); refined digit by digit until at
-  // most kCandCap keys are >= L.  Those candidates are gathered, sorted by (key desc, index asc),
-  // and the cut is taken exactly as the oracle does: p_j = exp(y_j - y0) / tot in fp64 and the
-  // sequential cumulative >= top_p.  Deterministic (the result does not depend on L).
+  // ---- nucleus larger than 32 tokens (threshold form).  Digit histograms (8 bits per level from
+  // the top) of counts and 2^-31 fixed-point masses (native 32-bit shared atomics, per-warp
+  // copies) bound the cumulative mass from below and above; they locate a band of keys [L, U)
+  // that surely holds the cut, refined digit by digit until it has at most kCandCap keys.  The
+  // keys >= U are surely inside the nucleus: their exact fp64 mass c_U is summed in a fixed order;
+  // the band is gathered, sorted by (key desc, index asc) and the cut taken as the oracle does
+  // (p_j = exp(y_j - y0) / tot, sequential cumulative from c_U until >= top_p).  Deterministic.
   {
     __shared__ unsigned s_msum[256];
-    __shared__ unsigned long long s_am;
-    __shared__ unsigned s_ac;
+    __shared__ unsigned long long s_am, s_ahi, s_L, s_U;
+    __shared__ double s_cu;
     __shared__ int s_state;  // 0 refine, 1 gather with L = s_prefix, 2 fall back
     __shared__ double s_pm[kCandCap];
     const double y0 = s_y0, tot = s_lfull;
     const float c2 = (float)(1.4426950408889634 / tau), nm = -KO::value(c_key[0]) * c2;
     const float scale31 = (float)(2147483648.0 / tot);
-    const unsigned long long target = (unsigned long long)(((double)a.top_p + 1e-5) * 2147483648.0);
+    const unsigned long long target = (unsigned long long)((double)a.top_p * 2147483648.0);
     const bool vec = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
     if (tid == 0) {
       s_prefix = 0;
       s_mask = 0;
       s_am = 0ull;
-      s_ac = 0u;
+      s_ahi = 0ull;
       s_state = 0;
       s_ncand = 0;
     }
+    // per-warp private histograms (counts in the candidate buffer, masses in the p buffer -- both
+    // free until the gather): same-address contention stays inside a warp
+    unsigned *wc = reinterpret_cast<unsigned *>(s_cand) + wid * 256;
+    unsigned *wmass = reinterpret_cast<unsigned *>(s_pm) + wid * 256;
+    static_assert(kCandCap * 2 >= (kTopKThreads / 32) * 256, "private histograms must fit");
     for (int shift = KO::kBits - 8; shift >= 0; shift -= 8) {
-      for (int j = tid; j < 256; j += NT) {
-        hist[j] = 0u;
-        s_msum[j] = 0u;
+      for (int j = lane; j < 256; j += 32) {
+        wc[j] = 0u;
+        wmass[j] = 0u;
       }
       __syncthreads();
       const K prefix = s_prefix, mask = s_mask;
@@ -457,50 +476,91 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
         for (int j = 0; j < 8; ++j) {
           if (v0 + j < V && (kk[j] & mask) == prefix) {
             const unsigned d = (kk[j] >> shift) & 255u;
-            atomicAdd(&hist[d], 1u);
+            atomicAdd(&wc[d], 1u);
             const unsigned mf = __float2uint_rz(ex2(fmaf(KO::value(kk[j]), c2, nm)) * scale31);
-            if (mf) atomicAdd(&s_msum[d], mf);
+            if (mf) atomicAdd(&wmass[d], mf);
           }
         }
       }
       __syncthreads();
+      if (tid < 256) {
+        const unsigned *c0 = reinterpret_cast<const unsigned *>(s_cand);
+        const unsigned *m0 = reinterpret_cast<const unsigned *>(s_pm);
+        unsigned c = 0u, m = 0u;
+        for (int w = 0; w < NT / 32; ++w) {
+          c += c0[w * 256 + tid];
+          m += m0[w * 256 + tid];
+        }
+        hist[tid] = c;
+        s_msum[tid] = m;
+      }
+      __syncthreads();
       if (tid == 0) {
-        unsigned long long cm = s_am;
-        unsigned cc = s_ac;
-        int d = 255;
-        for (; d >= 0; --d) {
-          cm += s_msum[d];
-          cc += hist[d];
-          if (cm >= target) break;
+        // lower / upper bounds of the cumulative mass from the top (truncation: each element's
+        // fixed-point mass is low by < 1 unit, so hi = lo + count bounds it from above; eps covers
+        // the fp32 ex2 terms).  Digits above da are surely inside the nucleus, digits from ds up
+        // surely contain it: the cut lies in the band [ds, da].
+        const unsigned long long eps = 4295ull;  // 2e-6 in 2^-31 units
+        unsigned long long lo = s_am, hi = s_ahi, lo_a = 0ull, hi_a = 0ull;
+        int da = -1, ds = -1;
+        for (int d = 255; d >= 0; --d) {
+          const unsigned long long lo0 = lo, hi0 = hi;
+          lo += s_msum[d];
+          hi += (unsigned long long)s_msum[d] + hist[d];
+          if (da < 0 && hi + eps >= target) {
+            da = d;
+            lo_a = lo0;
+            hi_a = hi0;
+          }
+          if (lo >= target + eps) {
+            ds = d;
+            break;
+          }
         }
-        if (d < 0) s_state = 2;  // top_p + margin not reached (top_p ~ 1): fall back
-        else if (cc <= (unsigned)kCandCap) {
+        unsigned cnt = 0u;
+        for (int d = ds; d >= 0 && d <= da; ++d) cnt += hist[d];
+        const unsigned long long base = (unsigned long long)prefix;
+        if (ds < 0) s_state = 2;  // top_p + margin not reached (top_p ~ 1): fall back
+        else if (cnt <= (unsigned)kCandCap) {
           s_state = 1;
-          s_prefix = prefix | ((K)d << shift);  // L: the lowest key of digit d under the prefix
-        } else if (shift == 0) s_state = 2;  // more than kCandCap keys in the nucleus
-        else {
-          s_am = cm - s_msum[d];
-          s_ac = cc - hist[d];
-          s_prefix = prefix | ((K)d << shift);
+          s_L = base | ((unsigned long long)ds << shift);
+          s_U = base + ((unsigned long long)(da + 1) << shift);
+        } else if (ds == da && shift > 0) {  // one uncertain digit: refine inside it
+          s_am = lo_a;
+          s_ahi = hi_a;
+          s_prefix = prefix | ((K)ds << shift);
           s_mask = mask | ((K)255u << shift);
-        }
+        } else s_state = 2;  // more than kCandCap keys in the uncertain band
       }
       __syncthreads();
       if (s_state) break;
     }
     if (s_state == 1) {
-      const K L = s_prefix;
+      const unsigned long long L = s_L, U = s_U;
+      const double itot = 1.0 / tot;
+      double cu = 0.0;  // exact mass of the keys >= U (all inside the nucleus), fixed-order sum
       for (int v0 = tid * 8; v0 < V; v0 += NT * 8) {
         uint32_t kk[8];
         load8(x, v0, V, vec, kk);
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (v0 + j < V && kk[j] >= L) {
+        for (int j = 0; j < 8; ++j) {
+          if (v0 + j >= V) continue;
+          if (kk[j] >= U) {
+            cu += exp((double)KO::value((K)kk[j]) / tau - y0) * itot;
+          } else if (kk[j] >= L) {
             const int slot = atomicAdd(&s_ncand, 1);
             s_cand[slot] = ((unsigned long long)kk[j] << 32) | (0xFFFFFFFFu - (uint32_t)(v0 + j));
           }
+        }
       }
+      cu = warp_sum_d(cu);
+      if (lane == 0) s_lsum[wid] = cu;
       __syncthreads();
+      if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < NT / 32; ++w) t += s_lsum[w];
+        s_cu = t;
+      }
       const int nc = s_ncand;
       int np2 = 1;
       while (np2 < nc) np2 <<= 1;
@@ -528,7 +588,7 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
       }
       __syncthreads();
       if (tid == 0) {
-        double c = 0.0;
+        double c = s_cu;
         int n = -1;
         for (int j = 0; j < nc; ++j) {
           c += s_pm[j];
@@ -705,6 +765,23 @@ __device__ __forceinline__ double thr_p(const T *x, int v, const Thr &L) {
   return thr_pk<T>(KeyOf<T>::key(x, v), v, L);
 }
 
+// bulk form for full-row passes: log p'(v) = x_v / tau - c with c = y0 + log(tot s) (no divisions;
+// the same values up to rounding)
+struct ThrF {
+  uint32_t key;
+  int32_t idx;
+  double itau, c;
+};
+__device__ __forceinline__ ThrF make_thrf(const Thr &L) { return ThrF{L.key, L.idx, 1.0 / L.tau, L.y0 + log(L.tot * L.s)}; }
+template <typename T>
+__device__ __forceinline__ bool thr_kept(uint32_t kk, int v, const ThrF &L) {
+  return kk > L.key || (kk == L.key && v <= L.idx);
+}
+template <typename T>
+__device__ __forceinline__ double thr_logp(uint32_t kk, const ThrF &L) {
+  return (double)KeyOf<T>::value(kk) * L.itau - L.c;
+}
+
 __device__ __forceinline__ double block_sum_d(double v, double *red) {  // fixed order: warps, then 0..nw-1
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   v = warp_sum_d(v);
@@ -797,6 +874,9 @@ __global__ void __launch_bounds__(512) sv_fwide_score_kernel(const __grid_consta
   if (t < 0 || t >= a.V) st |= 4;
   double S = 0.0, KL = 0.0;
   const bool vec = ((reinterpret_cast<uintptr_t>(xd) | reinterpret_cast<uintptr_t>(xc)) & 15) == 0;
+  // per kept draft entry: log p' in fp64 (x / tau - c), p' = 2^{log p' log2 e} on the fp32 MUFU
+  // (relative error ~1e-6, inside the north_star tolerance), KL term p'_d (log p'_d - log p'_c)
+  const ThrF fd = make_thrf(ld), fc = make_thrf(lc);
   if (!st)
     for (int v0 = threadIdx.x * 8; v0 < a.V; v0 += blockDim.x * 8) {
       uint32_t kd[8], kc[8];
@@ -804,11 +884,17 @@ __global__ void __launch_bounds__(512) sv_fwide_score_kernel(const __grid_consta
       load8(xc, v0, a.V, vec, kc);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const double pd = v0 + j < a.V ? thr_pk<T>(kd[j], v0 + j, ld) : 0.0;
+        if (v0 + j >= a.V || !thr_kept<T>(kd[j], v0 + j, fd)) continue;
+        const double lpd = thr_logp<T>(kd[j], fd);
+        const double pd = (double)ex2((float)(lpd * 1.4426950408889634));
         if (pd > 0.0) {
-          const double pc = thr_pk<T>(kc[j], v0 + j, lc);
-          S += fmin(pd, pc);
-          KL += pc > 0.0 ? pd * log(pd / pc) : INFINITY;
+          if (thr_kept<T>(kc[j], v0 + j, fc)) {
+            const double lpc = thr_logp<T>(kc[j], fc);
+            const double pc = (double)ex2((float)(lpc * 1.4426950408889634));
+            S += fmin(pd, pc);
+            KL += pd * (lpd - lpc);
+          } else
+            KL = INFINITY;
         }
       }
     }
@@ -973,10 +1059,11 @@ __global__ void __launch_bounds__(512) sv_fwide_sample_kernel(const __grid_const
   const int chunk = (((V + NT - 1) / NT) + 7) & ~7, v0 = min(V, tid * chunk), v1 = min(V, v0 + chunk);
   const bool vec = ((reinterpret_cast<uintptr_t>(xt) | reinterpret_cast<uintptr_t>(xd)) & 15) == 0;
   int q = 0;  // first draft entry with index >= v (list-mode draft rows; v ascends within a pass)
+  const ThrF ft = make_thrf(lt), fd = make_thrf(ld);
   auto rv = [&](int v, uint32_t kt, uint32_t kd) {
-    const double pt = thr_pk<T>(kt, v, lt);
+    const double pt = thr_kept<T>(kt, v, ft) ? exp(thr_logp<T>(kt, ft)) : 0.0;
     if (!resid || !(pt > 0.0)) return pt;
-    if (dwide) return fmax(0.0, pt - thr_pk<T>(kd, v, ld));
+    if (dwide) return fmax(0.0, pt - (thr_kept<T>(kd, v, fd) ? exp(thr_logp<T>(kd, fd)) : 0.0));
     while (q < nd && s_di[q] < v) ++q;
     return fmax(0.0, pt - ((q < nd && s_di[q] == v) ? s_dp[q] : 0.0));
   };
