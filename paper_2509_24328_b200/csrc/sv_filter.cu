@@ -546,7 +546,7 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
         for (int j = 0; j < 8; ++j) {
           if (v0 + j >= V) continue;
           if (kk[j] >= U) {
-            cu += exp((double)KO::value((K)kk[j]) / tau - y0) * itot;
+            cu += (double)ex2(fmaf(KO::value((K)kk[j]), c2, nm)) * itot;  // MUFU terms (~1e-7)
           } else if (kk[j] >= L) {
             const int slot = atomicAdd(&s_ncand, 1);
             s_cand[slot] = ((unsigned long long)kk[j] << 32) | (0xFFFFFFFFu - (uint32_t)(v0 + j));
