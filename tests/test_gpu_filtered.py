@@ -128,7 +128,8 @@ def test_nucleus_only_llama_setting(sv, V, dtype, tau):
     print("rows with a nucleus > 32:", int(big.sum()), "of", big.size, "cut ties:", int(tie.sum()))
 
 
-@pytest.mark.parametrize("V,dtype,tau", [(4096, "bf16", 1.0), (32000, "f32", 1.0), (32000, "bf16", 0.8)])
+@pytest.mark.parametrize("V,dtype,tau", [(4096, "bf16", 1.0), (32000, "f32", 1.0), (32000, "bf16", 0.8),
+                                         (32000, "f32", 3.0)])  # nuclei of thousands: radix fallback
 def test_nucleus_wide_verify(sv, V, dtype, tau):
     """sd_verify_filtered, nucleus-only, with nuclei wider than 32 tokens on draft and target rows:
     accept tests in threshold form and the full-row residual / bonus sample against the oracle;
@@ -151,6 +152,7 @@ def test_nucleus_wide_verify(sv, V, dtype, tau):
             wide_t[b, i] = len(filter_dist(Td[b, i], tau, 0, 0.9)[1]) > 32
             tie[b] |= _cut_margin(Td[b, i], tau, 0.9) < 1e-6
     assert wide_d.any() and wide_t.any()
+    print("largest draft nucleus:", max(len(filter_dist(Dd[b, i], tau, 0, 0.9)[1]) for b in range(B) for i in range(k)))
     D, C, T, _ = H.to_torch(x)
     tk = torch.from_numpy(tok).cuda()
     gs = sv.sv_score_filtered(D, C, tk, 0, 0.9, tau, tau, sv.Profile.from_dict(synth.load_profile()))
