@@ -246,3 +246,22 @@ def test_nucleus_wide_closed_form(sv, r, V, tp):
             j = ranks[b, i]
             want = math.exp(xs[b, i, perm[b * k + i][j]]) * (1 - r) / (1 - r ** n)
             assert abs(g["draft_ptok"][b, i] - want) <= 1e-5 * want
+
+
+def test_nucleus_wide_deterministic(sv):
+    """The wide-nucleus path is bitwise reproducible (integer fixed-point histograms, sorted
+    candidate bands, fixed-order sums): two runs of score + verify give identical outputs."""
+    B, k, V, tau = 6, 4, 32000, 1.5
+    x = synth.make_inputs(B, k, V, "bf16", seed=2024)
+    D, C, T, tok = H.to_torch(x)
+    gam = torch.full((B,), k, dtype=torch.int32, device="cuda")
+    outs = []
+    for _ in range(2):
+        gs = sv.sv_score_filtered(D, C, tok, 0, 0.9, tau, tau)
+        gv = sv.sd_verify_filtered(T, tok, gam, gs["fworkspace"], 0, 0.9, tau, seed=3, offset=7, D=D)
+        torch.cuda.synchronize()
+        outs.append({**{n: gs[n].cpu().numpy() for n in ("S", "A", "KL", "draft_ptok", "status")},
+                     **{n: v.cpu().numpy() for n, v in gv.items()}})
+    for n in outs[0]:
+        assert np.array_equal(outs[0][n], outs[1][n], equal_nan=True) if outs[0][n].dtype.kind == "f" \
+            else np.array_equal(outs[0][n], outs[1][n]), n
