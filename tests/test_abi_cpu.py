@@ -94,6 +94,15 @@ def test_host_validation_of_the_widened_abi(lib):
                                    None, None, None, None, None, None, P, 1 << 20, None)
         assert st == want, (top_k, top_p, st)
     assert lib.sv_filter_workspace_bytes(80, 8) > 0 and lib.sv_filter_workspace_bytes(80, 17) == 0
+    # filtered verify: the optional draft logits must match the target's dtype; gamma is required
+    f = _lib.SvFilter(0, 0.9)
+    Lf = _lib.SvLogits(16, _lib.SV_F32, 0, 0, 0)
+    st = lib.sd_verify_filtered(ctypes.byref(L), ctypes.byref(Lf), P, P, 2, 2, 100, 1.0, ctypes.byref(f), 0, 0, 0,
+                                P, P, None, None, None, P, 1 << 20, None)
+    assert st == _lib.SV_ERR_INVALID_ARG
+    st = lib.sd_verify_filtered(ctypes.byref(L), None, P, None, 2, 2, 100, 1.0, ctypes.byref(f), 0, 0, 0,
+                                P, P, None, None, None, P, 1 << 20, None)
+    assert st == _lib.SV_ERR_INVALID_ARG
     # ragged verify: missing row pointers / short row stride
     st = lib.sd_verify_ragged(ctypes.byref(L), P, 99, P, P, P, P, P, P, 2, 2, 100, 1.0, 1.0, 0, 0, None, 0,
                               P, P, None, None, None, P, 1 << 30, None)
