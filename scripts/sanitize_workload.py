@@ -28,5 +28,14 @@ for (B, k, V, dt) in [(3, 4, 3001, "bf16"), (2, 3, 1001, "f32")]:
     run_vocab_sharded_lockstep(pipes, [sl(D, r) for r in range(G)], [sl(C, r) for r in range(G)], [sl(T, r) for r in range(G)], tok, 1, 0)
     Lg = torch.tensor(synth.latency_table(B * (k + 1) + 1), dtype=torch.float64, device="cuda")
     sv.sv_schedule(pipe.score_out["p_hat"], Lg, sv.SV_SCHED_BATCH_GREEDY)
+# wide nucleus of ~4600 tokens (geometric row): the radix fallback of the cut search
+import math
+r, V = 0.9995, 20000
+xg = torch.tensor([[[j * math.log(r) for j in range(V)]] * 2] * 2, dtype=torch.float32, device="cuda")
+tg = torch.zeros((2, 2), dtype=torch.int32, device="cuda")
+gsw = sv.sv_score_filtered(xg, xg, tg, 0, 0.9, 1.0, 1.0)
+T3 = torch.cat([xg, xg[:, :1]], dim=1).contiguous()
+sv.sd_verify_filtered(T3, tg, torch.tensor([2, 1], dtype=torch.int32, device="cuda"), gsw["fworkspace"], 0, 0.9, 1.0,
+                      1, 0, D=xg)
 torch.cuda.synchronize()
 print("sanitizer workload done")
