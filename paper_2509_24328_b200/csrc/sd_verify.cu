@@ -415,6 +415,10 @@ __global__ void __launch_bounds__(256) sv_find_kernel(const __grid_constant__ Ve
   // Slices go in chunks of 32 (one warp scan each, running total across chunks); the loads of
   // kFindChunks chunks are issued together.
   double Z = 0.0;
+  // one chunk group covers every slice (V <= 32 kFindChunks slices): the crossing scan below
+  // reuses these registers instead of loading the masses again
+  double mc[kFindChunks];
+  int mc_half = -1;
   for (int pass = 0; pass < 2; ++pass) {
     const int half = mode ? 0 : 1;
     double run = 0.0;
@@ -424,6 +428,11 @@ __global__ void __launch_bounds__(256) sv_find_kernel(const __grid_constant__ Ve
       for (int j = 0; j < kFindChunks; ++j) {
         const int q = c0 + 32 * j + lane;
         m[j] = q < nq ? __ldcg(sm + midx(half, q)) : 0.0;
+      }
+      if (nq <= 32 * kFindChunks) {
+#pragma unroll
+        for (int j = 0; j < kFindChunks; ++j) mc[j] = m[j];
+        mc_half = half;
       }
 #pragma unroll
       for (int j = 0; j < kFindChunks; ++j) {
@@ -450,7 +459,7 @@ __global__ void __launch_bounds__(256) sv_find_kernel(const __grid_constant__ Ve
 #pragma unroll
     for (int j = 0; j < kFindChunks; ++j) {
       const int q = c0 + 32 * j + lane;
-      mm[j] = q < nq ? __ldcg(sm + midx(half, q)) : 0.0;
+      mm[j] = mc_half == half ? mc[j] : (q < nq ? __ldcg(sm + midx(half, q)) : 0.0);
     }
 #pragma unroll
     for (int j = 0; j < kFindChunks; ++j) {
