@@ -94,7 +94,8 @@ def _cut_margin(x, tau, top_p):
 
 
 @pytest.mark.parametrize("V,dtype,tau", [(32000, "f32", 0.6), (32000, "bf16", 0.6), (4096, "bf16", 1.0),
-                                         (32000, "f32", 1.0), (152064, "bf16", 1.0)])
+                                         (32000, "f32", 1.0), (152064, "bf16", 1.0),
+                                         (1001, "f32", 2.0), (4099, "bf16", 1.5)])  # unaligned rows
 def test_nucleus_only_llama_setting(sv, V, dtype, tau):
     """top_k = 0, top_p = 0.9 (P L739-740, Llama) over the FULL distribution, any nucleus size:
     <= 32 tokens as lists, larger nuclei in threshold form (mass-weighted radix select, full-row
@@ -129,7 +130,8 @@ def test_nucleus_only_llama_setting(sv, V, dtype, tau):
 
 
 @pytest.mark.parametrize("V,dtype,tau", [(4096, "bf16", 1.0), (32000, "f32", 1.0), (32000, "bf16", 0.8),
-                                         (32000, "f32", 3.0)])  # nuclei of thousands: radix fallback
+                                         (32000, "f32", 3.0),   # nuclei of thousands: radix fallback
+                                         (1001, "f32", 2.0)])   # unaligned rows
 def test_nucleus_wide_verify(sv, V, dtype, tau):
     """sd_verify_filtered, nucleus-only, with nuclei wider than 32 tokens on draft and target rows:
     accept tests in threshold form and the full-row residual / bonus sample against the oracle;
