@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(32 * (SV_MAX_K_DEV + 1)) sv_decide_kernel(cons
 
 // Persistent warp-granular K4 over the items (b, i <= gamma_b, split), in sequence order.
 template <typename T>
-__global__ void __launch_bounds__(kRowsThreads, 3) sv_rows_kernel(const __grid_constant__ VerifyArgs a) {
+__global__ void __launch_bounds__(kRowsThreads, 4) sv_rows_kernel(const __grid_constant__ VerifyArgs a) {
   constexpr int NT = kRowsThreads, NW = NT / 32;
   __shared__ int s_pref[NT + 1];
   __shared__ int s_wtot[NW];
