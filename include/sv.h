@@ -15,7 +15,7 @@
  *    unsupported dtype, workspace too small, n_lat too short, grid limits exceeded)
  *    return a status != SV_OK and launch nothing.
  *  - Data errors found on the device (NaN / +inf logit, all -inf row, token outside
- *    [0, V), p_d(t) = 0, non-finite p_hat, L[n] <= 0, gamma outside [0, k]) never trap:
+ *    [0, V), p_d(t) = 0, p_hat outside [0, 1], L[n] <= 0, gamma outside [0, k]) never trap:
  *    they set per-row SV_ROW_* bits in `row_status` (when non-NULL) and write the
  *    deterministic sentinels documented per call.
  *  - Logit tensors are row-major with the vocabulary dimension contiguous; element
@@ -59,7 +59,7 @@ typedef enum { SV_F32 = 0, SV_BF16 = 1 } sv_dtype;
 #define SV_ROW_ALL_NEG_INF 2   /* every logit of a row is -inf (or < -1e30)         */
 #define SV_ROW_BAD_TOKEN   4   /* draft token outside [0, V)                         */
 #define SV_ROW_DRAFT_ZERO  8   /* p_d(t) = 0 (draft logit of t is -inf)              */
-#define SV_ROW_PHAT_BAD    16  /* non-finite p_hat fed to the scheduler (used as 0)  */
+#define SV_ROW_PHAT_BAD    16  /* p_hat outside [0, 1] (or NaN) fed to the scheduler: used as 0 */
 #define SV_ROW_RESID_ZERO  32  /* rejected but residual mass Z = 0: sampled p_t (R10) */
 #define SV_ROW_BAD_GAMMA   64  /* gamma outside [0, k]                               */
 #define SV_ROW_BAD_LATENCY 128 /* a latency entry used by the schedule is <= 0 / NaN */
@@ -98,10 +98,6 @@ SV_API size_t sv_workspace_bytes(int32_t B, int32_t k, int32_t V, int32_t dtype)
 
 /* Human-readable text of a status code (static storage). */
 SV_API const char *sv_status_string(int32_t status);
-
-/* Vestigial (earlier on-chip designs): the CTA-cluster size that would hold a (D, C) row pair
- * of this (V, dtype) in <= 80 KB per CTA; 0 if none <= 16.  No current kernel uses clusters. */
-SV_API int32_t sv_cluster_size(int32_t V, int32_t dtype);
 
 /*
  * sv_score -- steps a1-a3: softmax normalisers of the draft and companion rows,

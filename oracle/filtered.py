@@ -99,6 +99,7 @@ def verify_filtered(D, T, tok, gamma, tau_d, tau_t, top_k, top_p, seed, offset, 
     Z = np.zeros(B)
     ratio = np.full((B, k), np.nan)
     margin = np.full(B, np.inf)
+    resid_zero = np.zeros(B, dtype=bool)
     for b in range(B):
         g = int(gamma[b])
         N = g
@@ -115,28 +116,40 @@ def verify_filtered(D, T, tok, gamma, tau_d, tau_t, top_k, top_p, seed, offset, 
                 break
         n_acc[b] = N
         pt, _ = filter_dist(T[b, N], tau_t, top_k, top_p)
-        if N < g:
-            pd, _ = filter_dist(D[b, N], tau_d, top_k, top_p)
-            r = np.maximum(0.0, pt - pd)
-        else:
-            r = pt
+        pd = filter_dist(D[b, N], tau_d, top_k, top_p)[0] if N < g else None
+        _, us = uniforms(seed, offset, seq_base + b, N)
+        tokn, z, mg, rz = sample_filtered(pt, pd, us)
+        Z[b] = z
+        margin[b] = min(margin[b], mg)
+        resid_zero[b] = rz
+        out[b] = tokn
+    return {"n_accept": n_acc, "out_tok": out, "resid_mass": Z, "accept_ratio": ratio, "margin": margin,
+            "resid_zero": resid_zero}
+
+
+def sample_filtered(pt, pd, us):
+    """The correction / bonus draw over full-length filtered distributions (S L151, L157-165):
+    r = max(0, p_t - p_d) (residual, pd given) or p_t (bonus, pd None); Z = sum r in vocabulary
+    order; token = smallest j with cumulative > u_s Z (R11), fallback the last positive entry.
+    A zero residual mass (reachable through rounding only) samples p_t instead and is flagged
+    (R10, S L152).  Returns (token, Z, margin to the crossing, resid_zero)."""
+    r = pt if pd is None else np.maximum(0.0, pt - pd)
+    z = 0.0
+    for v in r:
+        z += v
+    resid_zero = False
+    if pd is not None and not z > 0.0:
+        resid_zero = True
+        r = pt
         z = 0.0
         for v in r:
             z += v
-        Z[b] = z
-        _, us = uniforms(seed, offset, seq_base + b, N)
-        th = us * z
-        cum = 0.0
-        tokn = -1
-        for j in range(V):
-            if r[j] <= 0.0:
-                continue
-            cum += r[j]
-            if cum > th:
-                tokn = j
-                margin[b] = min(margin[b], abs(cum - th))
-                break
-        if tokn < 0:
-            tokn = int(np.nonzero(r > 0)[0][-1])
-        out[b] = tokn
-    return {"n_accept": n_acc, "out_tok": out, "resid_mass": Z, "accept_ratio": ratio, "margin": margin}
+    th = us * z
+    cum = 0.0
+    for j in range(r.size):
+        if r[j] <= 0.0:
+            continue
+        cum += r[j]
+        if cum > th:
+            return j, z, abs(cum - th), resid_zero
+    return int(np.nonzero(r > 0)[0][-1]), z, np.inf, resid_zero

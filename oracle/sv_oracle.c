@@ -258,7 +258,7 @@ void oracle_goodputs(const double *p, int32_t k, const double *L, int32_t plus_o
 }
 
 /* Exhaustive argmax over gamma in [0, k], smallest gamma on ties (S L396,
- * DESIGN R4).  Non-finite p_hat entries are treated as 0 and flagged. */
+ * DESIGN R4).  p_hat entries outside [0, 1] are treated as 0 and flagged (R22). */
 void oracle_schedule(const double *p_hat, int32_t B, int32_t k, const double *L, int32_t n_lat,
                      int32_t plus_one, int32_t *gamma, double *exp_accept, double *goodput, int32_t *status)
 {
@@ -268,7 +268,9 @@ void oracle_schedule(const double *p_hat, int32_t B, int32_t k, const double *L,
         int st = 0;
         for (int i = 0; i < k; ++i) {
             double v = p_hat[(int64_t)b * k + i];
-            if (!isfinite(v)) { v = 0.0; st |= O_ROW_PHAT_BAD; }
+            /* p_hat is an acceptance probability (P L176); outside [0, 1] it is not one:
+             * used as 0 and flagged (DESIGN R22) */
+            if (!(v >= 0.0 && v <= 1.0)) { v = 0.0; st |= O_ROW_PHAT_BAD; }
             p[i] = v;
         }
         int bad_lat = 0;
@@ -331,6 +333,11 @@ double oracle_batch_greedy(const double *p_hat, int32_t B, int32_t k, const doub
         n += 1;
     }
     if (n >= n_lat) { free(P); return NAN; }
+    /* every latency the walk can reach, L[B .. min(B + B k, n_lat - 1)], must be a positive
+     * finite time (as in the per-row mode); otherwise gamma = 0 everywhere, goodput NaN */
+    for (int64_t j = n; j <= n + (int64_t)B * k && j < n_lat; ++j) {
+        if (!(L[j] > 0.0) || !isfinite(L[j])) { free(P); return NAN; }
+    }
     double G = num / L[n];
     for (;;) {
         int bq = -1;
@@ -338,7 +345,7 @@ double oracle_batch_greedy(const double *p_hat, int32_t B, int32_t k, const doub
         for (int q = 0; q < B; ++q) {
             if (gamma[q] >= k) continue;
             double v = p_hat[(int64_t)q * k + gamma[q]];
-            if (!isfinite(v)) v = 0.0;
+            if (!(v >= 0.0 && v <= 1.0)) v = 0.0; /* DESIGN R22 */
             double gain = P[q] * v;
             if (gain > bgain) { bgain = gain; bq = q; }
         }

@@ -11,7 +11,6 @@ streams only.  No CPU fallback exists: the compute calls raise without libsv.so 
 from __future__ import annotations
 
 import ctypes
-import os
 
 import torch
 
@@ -19,7 +18,7 @@ from . import _lib
 from ._lib import (ROW_ALL_NEG_INF, ROW_BAD_GAMMA, ROW_BAD_LATENCY, ROW_BAD_TOKEN, ROW_DRAFT_ZERO,  # noqa: F401
                    ROW_NAN, ROW_PHAT_BAD, ROW_RESID_ZERO, SV_SCHED_BATCH_GREEDY, SV_SCHED_PER_ROW, SvError)
 
-__all__ = ["sv_score", "sv_score_schedule", "sv_schedule", "sd_verify", "sd_verify_ragged", "workspace_bytes", "cluster_size", "Profile",
+__all__ = ["sv_score", "sv_score_schedule", "sv_schedule", "sd_verify", "sd_verify_ragged", "workspace_bytes", "Profile",
            "Pipeline", "GraphPipeline", "sv_profile_build", "sv_score_filtered", "sd_verify_filtered", "load_library"]
 
 
@@ -53,6 +52,34 @@ def _ptr(t) -> int | None:
     return t.data_ptr()
 
 
+def _req(t, name: str, dtype: torch.dtype, shape: tuple, device=None):
+    """Argument contract of the C ABI that the C side cannot see (element type and extent)."""
+    if t is None:
+        raise SvError(f"{name} is required")
+    if t.dtype != dtype:
+        raise SvError(f"{name} must be {dtype}, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise SvError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    if device is not None and t.device != device:
+        raise SvError(f"{name} must live on {device}, got {t.device}")
+    return t
+
+
+def _out(o: dict, name: str, shape, dtype, dev):
+    if name in o and o[name] is not None:
+        return _req(o[name], f"out[{name!r}]", dtype, shape, dev)
+    return torch.empty(shape, dtype=dtype, device=dev)
+
+
+def _same_logits(ref, t, name: str, shape):
+    if t.dtype != ref.dtype:
+        raise SvError(f"{name} must have the draft's dtype {ref.dtype}, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise SvError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    if t.device != ref.device:
+        raise SvError(f"{name} must live on {ref.device}")
+
+
 def _stream(stream) -> int:
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream
@@ -61,11 +88,6 @@ def _stream(stream) -> int:
 def workspace_bytes(B: int, k: int, V: int, dtype: torch.dtype) -> int:
     code = _lib.SV_BF16 if dtype == torch.bfloat16 else _lib.SV_F32
     return int(_lib.load().sv_workspace_bytes(B, k, V, code))
-
-
-def cluster_size(V: int, dtype: torch.dtype) -> int:
-    code = _lib.SV_BF16 if dtype == torch.bfloat16 else _lib.SV_F32
-    return int(_lib.load().sv_cluster_size(V, code))
 
 
 class Profile:
@@ -96,13 +118,15 @@ def sv_score(D, C, tok, tau_d=1.0, tau_c=1.0, profile: Profile | None = None, wo
              stream=None) -> dict:
     """Steps a1-a3 (P L159, L164, L176) through the C ABI `sv_score`."""
     B, k, V = D.shape
+    dev = D.device
+    _same_logits(D, C, "C", (B, k, V))
+    _req(tok, "tok", torch.int32, (B, k), dev)
     if workspace is None:
         workspace = new_workspace(B, k, V, D.dtype, D.device)
-    dev = D.device
     o = out or {}
-    f = lambda name: o.get(name) if name in o else torch.empty((B, k), dtype=torch.float32, device=dev)  # noqa: E731
-    res = {n: f(n) for n in ("S", "A", "KL", "p_hat", "draft_m", "draft_l", "draft_ptok")}
-    res["status"] = o.get("status") if "status" in o else torch.empty((B, k), dtype=torch.int32, device=dev)
+    res = {n: _out(o, n, (B, k), torch.float32, dev) for n in ("S", "A", "KL", "p_hat", "draft_m", "draft_l",
+                                                                 "draft_ptok")}
+    res["status"] = _out(o, "status", (B, k), torch.int32, dev)
     if profile is None:
         res["p_hat"] = None
     st = _lib.load().sv_score(
@@ -123,20 +147,20 @@ def sv_score_schedule(D, C, tok, latency, tau_d=1.0, tau_c=1.0, profile: Profile
     dev = D.device
     if profile is None:
         raise SvError("sv_score_schedule needs a profile (p_hat drives the schedule)")
-    if latency.dtype != torch.float64:
-        raise SvError("latency table must be float64")
+    _same_logits(D, C, "C", (B, k, V))
+    _req(tok, "tok", torch.int32, (B, k), dev)
+    _req(latency, "latency", torch.float64, (latency.numel(),), dev)
     if workspace is None:
         workspace = new_workspace(B, k, V, D.dtype, dev)
     o = out or {}
-    f = lambda name: o.get(name) if name in o else torch.empty((B, k), dtype=torch.float32, device=dev)  # noqa: E731
-    res = {n: f(n) for n in ("S", "A", "KL", "p_hat", "draft_m", "draft_l", "draft_ptok")}
-    res["status"] = o.get("status") if "status" in o else torch.empty((B, k), dtype=torch.int32, device=dev)
+    res = {n: _out(o, n, (B, k), torch.float32, dev) for n in ("S", "A", "KL", "p_hat", "draft_m", "draft_l",
+                                                                 "draft_ptok")}
+    res["status"] = _out(o, "status", (B, k), torch.int32, dev)
     so = sched_out or {}
-    sch = {"gamma": so.get("gamma") if "gamma" in so else torch.empty(B, dtype=torch.int32, device=dev),
-           "exp_accept": so.get("exp_accept") if "exp_accept" in so else torch.empty(B, dtype=torch.float32,
-                                                                                      device=dev),
-           "goodput": so.get("goodput") if "goodput" in so else torch.empty(B, dtype=torch.float32, device=dev),
-           "status": so.get("status") if "status" in so else torch.empty(B, dtype=torch.int32, device=dev)}
+    sch = {"gamma": _out(so, "gamma", (B,), torch.int32, dev),
+           "exp_accept": _out(so, "exp_accept", (B,), torch.float32, dev),
+           "goodput": _out(so, "goodput", (B,), torch.float32, dev),
+           "status": _out(so, "status", (B,), torch.int32, dev)}
     st = _lib.load().sv_score_schedule(
         ctypes.byref(_logits(D)), ctypes.byref(_logits(C)), _ptr(tok), B, k, V, float(tau_d), float(tau_c),
         ctypes.byref(profile.c), _ptr(res["S"]), _ptr(res["A"]), _ptr(res["KL"]), _ptr(res["p_hat"]),
@@ -151,15 +175,13 @@ def sv_schedule(p_hat, latency, mode=SV_SCHED_PER_ROW, plus_one=1, out=None, str
     """Step a4 (P L207-252) through the C ABI `sv_schedule`; latency is a CUDA fp64 tensor."""
     B, k = p_hat.shape
     dev = p_hat.device
+    _req(p_hat, "p_hat", torch.float32, (B, k))
+    _req(latency, "latency", torch.float64, (latency.numel(),), dev)
     o = out or {}
-    res = {
-        "gamma": o.get("gamma", None) if "gamma" in o else torch.empty(B, dtype=torch.int32, device=dev),
-        "exp_accept": o.get("exp_accept") if "exp_accept" in o else torch.empty(B, dtype=torch.float32, device=dev),
-        "goodput": o.get("goodput") if "goodput" in o else torch.empty(B, dtype=torch.float32, device=dev),
-        "status": o.get("status") if "status" in o else torch.empty(B, dtype=torch.int32, device=dev),
-    }
-    if latency.dtype != torch.float64:
-        raise SvError("latency table must be float64")
+    res = {"gamma": _out(o, "gamma", (B,), torch.int32, dev),
+           "exp_accept": _out(o, "exp_accept", (B,), torch.float32, dev),
+           "goodput": _out(o, "goodput", (B,), torch.float32, dev),
+           "status": _out(o, "status", (B,), torch.int32, dev)}
     st = _lib.load().sv_schedule(_ptr(p_hat), B, k, _ptr(latency), latency.numel(), mode, plus_one,
                                  _ptr(res["gamma"]), _ptr(res["exp_accept"]), _ptr(res["goodput"]),
                                  _ptr(res["status"]), None, 0, _stream(stream))
@@ -167,20 +189,29 @@ def sv_schedule(p_hat, latency, mode=SV_SCHED_PER_ROW, plus_one=1, out=None, str
     return res
 
 
+def _verify_args(B, k, dev, tok, gamma, draft_m, draft_l, draft_ptok):
+    _req(tok, "tok", torch.int32, (B, k), dev)
+    _req(gamma, "gamma", torch.int32, (B,), dev)
+    for n, t in (("draft_m", draft_m), ("draft_l", draft_l), ("draft_ptok", draft_ptok)):
+        _req(t, n, torch.float32, (B, k), dev)
+
+
+def _verify_out(o: dict, B, k, dev) -> dict:
+    return {"n_accept": _out(o, "n_accept", (B,), torch.int32, dev),
+            "out_tok": _out(o, "out_tok", (B,), torch.int32, dev),
+            "accept_ratio": _out(o, "accept_ratio", (B, k), torch.float32, dev),
+            "resid_mass": _out(o, "resid_mass", (B,), torch.float32, dev),
+            "status": _out(o, "status", (B,), torch.int32, dev)}
+
+
 def sd_verify(D, T, tok, gamma, draft_m, draft_l, draft_ptok, tau_d=1.0, tau_t=1.0, seed=0, offset=0,
               seq_base=0, workspace=None, out=None, stream=None) -> dict:
     """Steps a5-a6 (P L29; S L148-165) through the C ABI `sd_verify`."""
     B, k, V = D.shape
     dev = D.device
-    o = out or {}
-    res = {
-        "n_accept": o.get("n_accept") if "n_accept" in o else torch.empty(B, dtype=torch.int32, device=dev),
-        "out_tok": o.get("out_tok") if "out_tok" in o else torch.empty(B, dtype=torch.int32, device=dev),
-        "accept_ratio": o.get("accept_ratio") if "accept_ratio" in o else torch.empty((B, k), dtype=torch.float32,
-                                                                                       device=dev),
-        "resid_mass": o.get("resid_mass") if "resid_mass" in o else torch.empty(B, dtype=torch.float32, device=dev),
-        "status": o.get("status") if "status" in o else torch.empty(B, dtype=torch.int32, device=dev),
-    }
+    _same_logits(D, T, "T", (B, k + 1, V))
+    _verify_args(B, k, dev, tok, gamma, draft_m, draft_l, draft_ptok)
+    res = _verify_out(out or {}, B, k, dev)
     if workspace is None:
         workspace = new_workspace(B, k, V, D.dtype, dev)
     st = _lib.load().sd_verify(
@@ -199,17 +230,15 @@ def sd_verify_ragged(D, T_rows, t_rowptr, tok, gamma, draft_m, draft_l, draft_pt
     uint64/int64 scalar tensor) makes the Philox offset a device value (CUDA-graph replays)."""
     B, k, V = D.shape
     dev = D.device
-    if T_rows.dim() != 2 or T_rows.stride(1) != 1 or T_rows.dtype != D.dtype:
+    if T_rows.dim() != 2 or T_rows.stride(1) != 1 or T_rows.dtype != D.dtype or T_rows.shape[1] != V:
         raise SvError("ragged target must be [rows, V] with the vocabulary contiguous and the draft's dtype")
-    o = out or {}
-    res = {
-        "n_accept": o.get("n_accept") if "n_accept" in o else torch.empty(B, dtype=torch.int32, device=dev),
-        "out_tok": o.get("out_tok") if "out_tok" in o else torch.empty(B, dtype=torch.int32, device=dev),
-        "accept_ratio": o.get("accept_ratio") if "accept_ratio" in o else torch.empty((B, k), dtype=torch.float32,
-                                                                                       device=dev),
-        "resid_mass": o.get("resid_mass") if "resid_mass" in o else torch.empty(B, dtype=torch.float32, device=dev),
-        "status": o.get("status") if "status" in o else torch.empty(B, dtype=torch.int32, device=dev),
-    }
+    _req(t_rowptr, "t_rowptr", torch.int64, (B,), dev)
+    if offset_dev is not None and (offset_dev.dtype not in (torch.int64, torch.uint64) or offset_dev.numel() != 1):
+        raise SvError("offset_dev must be a one-element int64 / uint64 CUDA tensor")
+    _verify_args(B, k, dev, tok, gamma, draft_m, draft_l, draft_ptok)
+    if not T_rows.is_cuda or T_rows.device != dev:
+        raise SvError(f"ragged target must be a CUDA tensor on {dev}")
+    res = _verify_out(out or {}, B, k, dev)
     if workspace is None:
         workspace = new_workspace(B, k, V, D.dtype, dev)
     st = _lib.load().sd_verify_ragged(
@@ -232,6 +261,8 @@ def sv_score_filtered(D, C, tok, top_k=20, top_p=0.8, tau_d=1.0, tau_c=1.0, prof
     `sv_score_filtered`.  Keep `fworkspace` for `sd_verify_filtered` (it holds the draft lists)."""
     B, k, V = D.shape
     dev = D.device
+    _same_logits(D, C, "C", (B, k, V))
+    _req(tok, "tok", torch.int32, (B, k), dev)
     fworkspace = fworkspace if fworkspace is not None else new_filter_workspace(B, k, dev)
     res = {n: torch.empty((B, k), dtype=torch.float32, device=dev) for n in ("S", "A", "KL", "p_hat", "draft_ptok")}
     res["status"] = torch.empty((B, k), dtype=torch.int32, device=dev)
@@ -256,6 +287,10 @@ def sd_verify_filtered(T, tok, gamma, fworkspace, top_k=20, top_p=0.8, tau_t=1.0
     B, k1, V = T.shape
     k = k1 - 1
     dev = T.device
+    _req(tok, "tok", torch.int32, (B, k), dev)
+    _req(gamma, "gamma", torch.int32, (B,), dev)
+    if D is not None:
+        _same_logits(T, D, "D", (B, k, V))
     res = {"n_accept": torch.empty(B, dtype=torch.int32, device=dev),
            "out_tok": torch.empty(B, dtype=torch.int32, device=dev),
            "accept_ratio": torch.empty((B, k), dtype=torch.float32, device=dev),
@@ -355,7 +390,7 @@ class Pipeline:
     the fixed-bytes roofline variant of SURVEY §8(d))."""
 
     def __init__(self, B, k, V, dtype, profile: Profile, latency: torch.Tensor, tau=(1.0, 1.0, 1.0),
-                 mode=SV_SCHED_PER_ROW, device="cuda"):
+                 mode=SV_SCHED_PER_ROW, device="cuda", fused=False):
         self.B, self.k, self.V, self.dtype = B, k, V, dtype
         self.profile, self.latency, self.mode = profile, latency, mode
         self.tau_d, self.tau_c, self.tau_t = tau
@@ -373,8 +408,8 @@ class Pipeline:
         self.forced_gamma = torch.empty(B, **i32)
         self._forced = None
         # sv_score_schedule (K3 folded into K1's last row epilogue) measured ~1.5 us SLOWER per step
-        # than sv_score + a PDL-overlapped sv_schedule at every config; SV_FUSED_SCHED=1 opts in
-        self.fused = os.environ.get("SV_FUSED_SCHED", "0") == "1"
+        # than sv_score + a PDL-overlapped sv_schedule at every config; fused=True opts in
+        self.fused = bool(fused)
 
     def run(self, D, C, T, tok, seed=0, offset=0, seq_base=0, force_gamma=None, stream=None):
         if force_gamma is None and self.mode == SV_SCHED_PER_ROW and self.fused:

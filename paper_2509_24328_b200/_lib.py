@@ -16,7 +16,7 @@ ROW_NAN, ROW_ALL_NEG_INF, ROW_BAD_TOKEN, ROW_DRAFT_ZERO = 1, 2, 4, 8
 ROW_PHAT_BAD, ROW_RESID_ZERO, ROW_BAD_GAMMA, ROW_BAD_LATENCY = 16, 32, 64, 128
 ROW_FILTER_UNSUPPORTED = 256
 
-EXPORTS = ("sv_workspace_bytes", "sv_status_string", "sv_cluster_size", "sv_score", "sv_schedule", "sd_verify",
+EXPORTS = ("sv_workspace_bytes", "sv_status_string", "sv_score", "sv_schedule", "sd_verify",
            "sv_shard_xch_bytes", "sv_shard_score_p1", "sv_shard_score_p2", "sv_shard_score_finish",
            "sv_shard_verify_p1", "sv_shard_verify_p2", "sv_shard_verify_finish", "sd_verify_ragged",
            "sv_profile_workspace_bytes", "sv_profile_build", "sv_filter_workspace_bytes", "sv_score_filtered",
@@ -58,8 +58,6 @@ def load(path: str = LIB_PATH):
     lib.sv_workspace_bytes.restype = sz
     lib.sv_status_string.argtypes = [i32]
     lib.sv_status_string.restype = ctypes.c_char_p
-    lib.sv_cluster_size.argtypes = [i32, i32]
-    lib.sv_cluster_size.restype = i32
     LP = ctypes.POINTER(SvLogits)
     lib.sv_score.argtypes = [LP, LP, P, i32, i32, i32, f32, f32, ctypes.POINTER(SvProfile),
                              P, P, P, P, P, P, P, P, P, sz, P]

@@ -1,23 +1,25 @@
 // sd_verify.cu -- K4 + K5: steps a5-a6 (standard SD verification and the correction /
 // bonus sample; P L29 citing Leviathan et al.; S L148-165, L82-90; DESIGN R1, R10-R13).
 //
-// K4 sv_rows_kernel: a persistent grid over the COMPACTED list of (sequence b, target row
-//   i <= gamma_b, vocabulary split) items -- rows past gamma_b are never read and cost no CTA.
-//   Items are WARP-granular (no block barrier on the path): a warp streams 32 lanes x 8
-//   16-byte units of one target row (8 independent loads per lane in flight), reduces the raw
-//   max m and l = sum 2^{(x - m) log2e / tau_t} (fp32 per unit, fp64 per lane and butterfly)
-//   and writes one (m, l) partial.  acq_rel completion counters elect the warp that finishes a
-//   row (it merges the row's partials in a fixed order) and then the warp that finishes a
-//   sequence: it computes p_t(t_i), ratio_i = p_t(t_i) / p_d(t_i), the Philox u_i, N_b = first
-//   rejection and u_s (word 1 of position N_b), and writes the sequence's Decision
-//   (+ n_accept, accept_ratio).
-// K5 sv_resid_kernel: persistent, one warp per (sequence, slice of 32 lanes x 4 contiguous
-//   16-byte units).  r_v = max(0, p_t - p_d) on row N_b (or p_t for the bonus), every lane
-//   summing its contiguous elements in vocabulary order in fp64, a fixed-order warp scan gives
-//   the slice mass.  The warp that completes a sequence walks the slice masses in vocabulary
-//   order (Z, theta = u_s Z, owning slice), recomputes the owning slice -- identical bits, an
-//   L2 hit -- and locates the smallest j with cum_j > theta (R11) by warp scan + in-lane
-//   sequential scan.  Every reduction order is a function of V and the dtype only.
+// Four kernels, each launched with programmatic dependent launch (PDL): a kernel enters
+// griddepcontrol.wait before it reads anything its predecessor wrote, so the stream order is the
+// only synchronisation -- there are no completion counters or spin waits in sd_verify.
+//   K4  sv_rows_kernel   (persistent, warp-granular) over the COMPACTED list of (sequence b,
+//       target row i <= gamma_b, vocabulary split) items -- rows past gamma_b are never read.
+//       A warp streams 32 lanes x 8 16-byte units of one row and writes one (max, sum-exp)
+//       partial (fp32 per unit, fp64 per lane and butterfly).
+//   K4b sv_decide_kernel (one CTA of k+1 warps per sequence): warp i merges row i's partials in
+//       a fixed order; warp 0 computes p_t(t_i), ratio_i = p_t(t_i) / p_d(t_i), the Philox u_i,
+//       N_b = first rejection and u_s (word 1 of position N_b), and writes the sequence's
+//       Decision (+ n_accept, accept_ratio).
+//   K5  sv_resid_kernel  (persistent, one warp per (sequence, slice of 32 lanes x 4 contiguous
+//       16-byte units)): r_v = max(0, p_t - p_d) on row N_b (or p_t for the bonus), every lane
+//       summing its contiguous elements in vocabulary order in fp64; a fixed-order warp scan
+//       gives the slice's residual mass and its target mass (the R10 fallback).
+//   K5b sv_find_kernel   (one warp per sequence): Z and theta = u_s Z over the slice masses in
+//       vocabulary order, the owning slice, its recomputation (identical bits, an L2 hit) and
+//       the smallest j with cum_j > theta (R11) by warp scan + in-lane sequential scan.
+// Every reduction order is a function of V and the dtype only.
 #include <float.h>
 
 #include "sv_device.cuh"
@@ -585,10 +587,7 @@ cudaError_t launch_verify_stage(int stage, const VerifyArgs &a, cudaStream_t st)
 }
 
 cudaError_t launch_verify(const VerifyArgs &a, cudaStream_t st) {
-  // SV_VERIFY_MASK (timing experiments only: outputs are garbage unless all 4 bits are set)
-  static const int mask = tune_knob("SV_VERIFY_MASK", 15);
   for (int stage = 0; stage < 4; ++stage) {
-    if (!(mask >> stage & 1)) continue;
     const cudaError_t e = launch_verify_stage(stage, a, st);
     if (e != cudaSuccess) return e;
   }

@@ -2,7 +2,6 @@
 // workspace carving.  Every entry point only enqueues work on the caller's stream.
 #include <stdio.h>
 #include <stdint.h>
-#include <stdlib.h>
 
 #include <map>
 #include <mutex>
@@ -13,33 +12,11 @@
 
 namespace sv {
 
-// Tuning knobs, read once from the environment (benchmark experiments only; the defaults are
-// the shipped configuration).  Both are functions of nothing but the process environment, so
-// results stay independent of B and of the GPU count.
-int tune_knob(const char *name, int dflt) {
-  const char *v = getenv(name);
-  return (v && *v) ? atoi(v) : dflt;
-}
-
-bool pdl_enabled() {
-  static const bool on = tune_knob("SV_PDL", 1) != 0;
-  return on;
-}
-
-int cluster_size_for(int64_t V, int elem_bytes) {
-  static const int budget = tune_knob("SV_CHUNK_PAIR_KB", kChunkPairBudget / 1024) * 1024;
-  for (int cs = 1; cs <= kMaxCluster; cs <<= 1) {
-    const int64_t chunk = chunk_elems_for(V, cs);
-    if (2 * chunk * elem_bytes <= budget) return cs;
-  }
-  return 0;
-}
-
+// Chunking of a row is a function of V only (never of B, the SM count or any process state),
+// so every reduction order -- and every output bit -- is independent of how B is split.
 int score_splits_for(int64_t V) {
-  static const int target = tune_knob("SV_SCORE_CHUNK", kScoreChunk);
-  static const int min_cs = tune_knob("SV_SCORE_MIN_CS", kScoreMinSplits);
-  int64_t s = (V + target - 1) / target;
-  if (s < min_cs) s = min_cs;  // short rows: several chunk tasks per row (latency at small B)
+  int64_t s = (V + kScoreChunk - 1) / kScoreChunk;
+  if (s < kScoreMinSplits) s = kScoreMinSplits;  // short rows: several chunk tasks per row (latency at small B)
   return (int)(s < 1 ? 1 : (s > kScoreMaxSplits ? kScoreMaxSplits : s));
 }
 
@@ -234,11 +211,6 @@ const char *sv_status_string(int32_t s) {
   }
 }
 
-int32_t sv_cluster_size(int32_t V, int32_t dtype) {
-  if (!dtype_ok(dtype) || V < 2) return 0;
-  return cluster_size_for(V, elem_bytes(dtype));
-}
-
 static int32_t score_impl(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok, int32_t B,
                           int32_t k, int32_t V, float tau_d, float tau_c, const sv_profile *prof, float *S, float *A,
                           float *KL, float *p_hat, float *draft_m, float *draft_l, float *draft_ptok,
@@ -260,8 +232,7 @@ static int32_t score_impl(const sv_logits *draft, const sv_logits *comp, const i
                                 draft_ptok, row_status, draft->dtype, V);
   const int64_t rows = (int64_t)B * k;
   if (2 * rows * a.cs > INT32_MAX) return SV_ERR_UNSUPPORTED;  // one CTA per chunk task
-  static const int lag = tune_knob("SV_SCORE_LAG", kScoreLag);
-  a.lead = (rows < lag ? rows : (int64_t)lag) * a.cs;
+  a.lead = (rows < kScoreLag ? rows : (int64_t)kScoreLag) * a.cs;
   uint8_t *ws = reinterpret_cast<uint8_t *>(workspace);
   a.part = reinterpret_cast<double *>(ws);
   a.spart = reinterpret_cast<float *>(ws + ws_round(rows * a.cs * 5 * 8));

@@ -990,18 +990,26 @@ __global__ void __launch_bounds__(256) sv_fverify_kernel(const __grid_constant__
   // entries in vocabulary order (rank by index), then sequential Z and inverse CDF (R11)
   int rank = 0;
   for (int l = 0; l < nt; ++l) rank += __shfl_sync(0xffffffffu, vi, l) < vi;
-  __shared__ double s_r[8][32];
+  __shared__ double s_r[8][32], s_pt[8][32];
   __shared__ int s_v[8][32];
   const int w8 = threadIdx.x >> 5;
   if (lane < nt) {
     s_r[w8][rank] = r;
+    s_pt[w8][rank] = Lt->p[lane];
     s_v[w8][rank] = vi;
   }
   __syncwarp();
   if (lane == 0) {
     double Z = 0.0;
     for (int l = 0; l < nt; ++l) Z += s_r[w8][l];
-    if (!(Z > 0.0)) st |= 32; /*SV_ROW_RESID_ZERO*/
+    if (LdN && !(Z > 0.0)) {  // R10: a zero residual (rounding only) samples p_t of row N instead
+      st |= 32;               /*SV_ROW_RESID_ZERO*/
+      Z = 0.0;
+      for (int l = 0; l < nt; ++l) {
+        s_r[w8][l] = s_pt[w8][l];
+        Z += s_r[w8][l];
+      }
+    }
     const double us = u24(sv_philox(a.seed, off, a.seq_base + b, N).y);
     const double th = us * Z;
     double cum = 0.0;
@@ -1042,7 +1050,7 @@ __global__ void __launch_bounds__(512) sv_fwide_sample_kernel(const __grid_const
   const int N = a.n_accept[b], g = a.gamma[b];
   const Thr lt = load_thr(a.tl + b * (k + 1) + N);
   const T *xt = reinterpret_cast<const T *>(a.t) + b * a.t_sb + (int64_t)N * a.t_si;
-  const bool resid = N < g;
+  bool resid = N < g;
   const FList *LdN = a.dl + b * k + N;
   const bool dwide = resid && LdN->wide;  // else the <= 32 draft entries, walked in index order
   const Thr ld = dwide ? load_thr(LdN) : lt;
@@ -1070,8 +1078,13 @@ __global__ void __launch_bounds__(512) sv_fwide_sample_kernel(const __grid_const
     while (q < nd && s_di[q] < v) ++q;
     return fmax(0.0, pt - ((q < nd && s_di[q] == v) ? s_dp[q] : 0.0));
   };
-  double sum = 0.0;
-  int lastp = -1;
+  __shared__ int s_retry;
+  double sum;
+  int lastp;
+pass_again:  // R10: when the residual mass is 0 (rounding only), the pass is redone over p_t
+  sum = 0.0;
+  lastp = -1;
+  q = 0;
   for (int w0 = v0; w0 < v1; w0 += 8) {
     uint32_t kt[8], kd[8];
     load8(xt, w0, V, vec, kt);
@@ -1095,6 +1108,7 @@ __global__ void __launch_bounds__(512) sv_fwide_sample_kernel(const __grid_const
       s_pre[j] = c;
       c += s_sum[j];
     }
+    s_retry = resid && !(c > 0.0);
     const double us = u24(sv_philox(a.seed, a.offset, a.seq_base + b, N).y);
     const double th = us * c;
     int jc = -1;
@@ -1108,6 +1122,12 @@ __global__ void __launch_bounds__(512) sv_fwide_sample_kernel(const __grid_const
     s_th = th;
   }
   __syncthreads();
+  if (s_retry) {
+    resid = false;
+    if (tid == 0 && a.status) a.status[b] |= 32;  // SV_ROW_RESID_ZERO
+    __syncthreads();
+    goto pass_again;
+  }
   const int jc = s_j;
   if (jc < 0) {  // rounding left no crossing (or Z = 0): the last positive entry (R11 fallback)
     if (tid == 0) {

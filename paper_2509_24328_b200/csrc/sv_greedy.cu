@@ -38,16 +38,35 @@ __global__ void __launch_bounds__(kGreedyThreads) sv_greedy_kernel(const Schedul
   const int B = a.B, k = a.k, N = B * k, tid = threadIdx.x;
 
   // (0) stage p_hat and the latencies the walk can reach (coalesced, all threads)
-  for (int x = tid; x < N; x += blockDim.x) ph[x] = a.p_hat[x];
-  for (int x = tid; x <= N + 1; x += blockDim.x) Ls[x] = (int64_t)B + x < a.n_lat ? a.L[B + x] : 1.0;
+  // the latencies the walk can reach, L[B .. B + mmax], must be positive and finite (as in the
+  // per-row mode); otherwise every sequence gets the sentinel gamma = 0 and SV_ROW_BAD_LATENCY
+  __shared__ int s_badlat;
+  if (tid == 0) s_badlat = 0;
   __syncthreads();
+  const int mmax = (int)min((int64_t)N, (int64_t)a.n_lat - 1 - B);  // n + 1 < n_lat
+  for (int x = tid; x < N; x += blockDim.x) ph[x] = a.p_hat[x];
+  for (int x = tid; x <= N + 1; x += blockDim.x) {
+    const double v = (int64_t)B + x < a.n_lat ? a.L[B + x] : 1.0;
+    Ls[x] = v;
+    if (x <= max(mmax, 0) && !(v > 0.0 && v <= DBL_MAX)) s_badlat = 1;
+  }
+  __syncthreads();
+  if (s_badlat) {
+    for (int q = tid; q < B; q += blockDim.x) {
+      a.gamma[q] = 0;
+      if (a.exp_accept) a.exp_accept[q] = 0.f;
+      if (a.goodput) a.goodput[q] = __int_as_float(0x7fc00000);
+      if (a.status) a.status[q] = 128;  // SV_ROW_BAD_LATENCY
+    }
+    return;
+  }
   // (1) gains: per-sequence prefix products (thread per sequence, sequential fp64)
   for (int q = tid; q < B; q += blockDim.x) {
     double P = 1.0;
     int st = 0;
     for (int j = 0; j < k; ++j) {
       float v = ph[q * k + j];
-      if (!(fabsf(v) <= FLT_MAX)) {
+      if (!(v >= 0.f && v <= 1.f)) {  // not a probability: used as 0 (SV_ROW_PHAT_BAD, DESIGN R22)
         v = 0.f;
         st |= 16;
       }
@@ -102,7 +121,6 @@ __global__ void __launch_bounds__(kGreedyThreads) sv_greedy_kernel(const Schedul
     s_stop = N;  // default: every candidate taken (or the latency table ends first)
   }
   __syncthreads();
-  const int mmax = (int)min((int64_t)N, (int64_t)a.n_lat - 1 - B);  // n + 1 < n_lat
   for (int m = tid; m < mmax; m += blockDim.x) {
     const double G = __ddiv_rn(g[m], Ls[m]), G2 = __ddiv_rn(g[m + 1], Ls[m + 1]);
     if (!(G2 > G)) atomicMin(&s_stop, m);
@@ -123,7 +141,7 @@ __global__ void __launch_bounds__(kGreedyThreads) sv_greedy_kernel(const Schedul
     double E = 0.0, P = 1.0;
     for (int j = 0; j < gam; ++j) {
       float v = ph[q * k + j];
-      if (!(fabsf(v) <= FLT_MAX)) v = 0.f;
+      if (!(v >= 0.f && v <= 1.f)) v = 0.f;
       P = __dmul_rn(P, (double)v);
       E = __dadd_rn(E, P);
     }

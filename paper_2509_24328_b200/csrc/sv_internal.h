@@ -20,26 +20,18 @@ constexpr int kScoreMaxSplits = 32;
 constexpr int kScoreMinSplits = 4;  // chunk tasks per row at least (a function of V only)
 constexpr int kRowsThreads = 256;
 constexpr int kSampleThreads = 256;
-// On-chip budget for the (D, C) [or (T, D)] chunk pair one CTA holds: the cluster size is
-// the smallest power of two that fits a row pair in this budget (a function of V and the
-// dtype only, so reductions are identical for any B and any GPU count).
-constexpr int kChunkPairBudget = 80 * 1024;
-constexpr int kMaxCluster = 16;
 // sd_verify K4: 8 x 16-byte loads in flight per thread per (row, split) item.
 constexpr int kRowUnitsPerThread = 8;
 // sd_verify K5: every lane owns 4 contiguous 16-byte units of a warp slice.
 constexpr int kSampleUnitsPerThread = 4;
 
-int cluster_size_for(int64_t V, int elem_bytes);     // 0 = unsupported
 int score_splits_for(int64_t V);                     // sv_score chunks per row
-int tune_knob(const char *name, int dflt);           // integer from the environment (tuning)
 int64_t chunk_elems_for(int64_t V, int cs);          // per-CTA elements (multiple of 16)
 int64_t rows_splits_for(int64_t V, int elem_bytes);  // sd_verify phase-1 CTAs per row
 // co-resident CTAs of a persistent kernel on this device (cached)
 int resident_grid(const void *fn, int threads, int smem);
 
-// Launch with programmatic stream serialization (PDL, see sv_device.cuh); SV_PDL=0 disables it.
-bool pdl_enabled();
+// Launch with programmatic stream serialization (PDL, see sv_device.cuh).
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -51,7 +43,7 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 

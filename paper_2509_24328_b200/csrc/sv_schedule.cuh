@@ -16,8 +16,10 @@ namespace sv {
 
 constexpr int kSchedMaxK = 16;  // SV_MAX_K
 
+// p_hat is an acceptance probability (P L176): outside [0, 1] (NaN, inf, negative, > 1) it is
+// used as 0 and flagged SV_ROW_PHAT_BAD (DESIGN R22)
 __device__ __forceinline__ double phat_val(float v, int &st) {
-  if (!(fabsf(v) <= FLT_MAX)) {  // NaN / inf -> 0 (SV_ROW_PHAT_BAD)
+  if (!(v >= 0.f && v <= 1.f)) {
     st |= 16;
     return 0.0;
   }

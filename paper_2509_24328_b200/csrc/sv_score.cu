@@ -174,51 +174,20 @@ __device__ __forceinline__ void p1_group(P1State &t, const uint4 (&rd)[g], const
 
 // Pass 1 of the thread's share of a chunk: full groups of G units per tensor (all loads of a
 // group in flight together, no per-unit guards), then single units, then the element tail.
-template <typename T, bool kGuard, int NT, int G, bool PF>
+template <typename T, bool kGuard, int NT, int G>
 __device__ __forceinline__ P1State pass1_thread(const Chunk<T> &ch, float cd, float cc, uint64_t pol) {
   constexpr int EPU = Elem<T>::kPerUnit;
   const int tid = threadIdx.x;
   P1State t{kMFloor, kMFloor, kMFloor, kMFloor, 0.f, 0.f, 0.f};
   int u0 = tid;
-  if constexpr (PF) {  // software pipelined: the next group's loads are in flight during this one
+  for (; u0 + (G - 1) * NT < ch.units; u0 += G * NT) {
     uint4 rd[G], rc[G];
-    if (u0 + (G - 1) * NT < ch.units) {
 #pragma unroll
-      for (int q = 0; q < G; ++q) {
-        rd[q] = ldg_hint(ch.d + (size_t)(u0 + q * NT) * EPU, pol);
-        rc[q] = ldg_hint(ch.c + (size_t)(u0 + q * NT) * EPU, pol);
-      }
-      while (true) {
-        const int un = u0 + G * NT;
-        const bool more = un + (G - 1) * NT < ch.units;
-        uint4 nd[G], nc[G];
-        if (more) {
-#pragma unroll
-          for (int q = 0; q < G; ++q) {
-            nd[q] = ldg_hint(ch.d + (size_t)(un + q * NT) * EPU, pol);
-            nc[q] = ldg_hint(ch.c + (size_t)(un + q * NT) * EPU, pol);
-          }
-        }
-        p1_group<T, kGuard, G>(t, rd, rc, cd, cc);
-        u0 = un;
-        if (!more) break;
-#pragma unroll
-        for (int q = 0; q < G; ++q) {
-          rd[q] = nd[q];
-          rc[q] = nc[q];
-        }
-      }
+    for (int q = 0; q < G; ++q) {
+      rd[q] = ldg_hint(ch.d + (size_t)(u0 + q * NT) * EPU, pol);
+      rc[q] = ldg_hint(ch.c + (size_t)(u0 + q * NT) * EPU, pol);
     }
-  } else {
-    for (; u0 + (G - 1) * NT < ch.units; u0 += G * NT) {
-      uint4 rd[G], rc[G];
-#pragma unroll
-      for (int q = 0; q < G; ++q) {
-        rd[q] = ldg_hint(ch.d + (size_t)(u0 + q * NT) * EPU, pol);
-        rc[q] = ldg_hint(ch.c + (size_t)(u0 + q * NT) * EPU, pol);
-      }
-      p1_group<T, kGuard, G>(t, rd, rc, cd, cc);
-    }
+    p1_group<T, kGuard, G>(t, rd, rc, cd, cc);
   }
   for (; u0 < ch.units; u0 += NT) {
     uint4 rd[1] = {ldg_hint(ch.d + (size_t)u0 * EPU, pol)}, rc[1] = {ldg_hint(ch.c + (size_t)u0 * EPU, pol)};
@@ -650,7 +619,7 @@ __device__ __forceinline__ void p2_finish(const ScoreArgs &a, const Task &k, flo
 }
 
 // LDG variant: every thread loads its own units (kScoreGroup 16-byte loads per tensor in flight).
-template <typename T, int NT, int MINB, int G, bool PF, int PFA = 0>
+template <typename T, int NT, int MINB, int G, int PFA = 0>
 __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constant__ ScoreArgs a) {
   constexpr int NW = NT / 32;
   __shared__ Smem<NW> sm;
@@ -664,12 +633,12 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constan
     P1State t;
     if constexpr (PFA > 0) {
       t = ch.units <= PFA * NT ? pass1_thread_all<T, false, NT, G, PFA>(ch, cd, cc, pol_keep)
-                               : pass1_thread<T, false, NT, G, PF>(ch, cd, cc, pol_keep);
+                               : pass1_thread<T, false, NT, G>(ch, cd, cc, pol_keep);
     } else {
-      t = pass1_thread<T, false, NT, G, PF>(ch, cd, cc, pol_keep);
+      t = pass1_thread<T, false, NT, G>(ch, cd, cc, pol_keep);
     }
     if (t.w != t.w && t.ld == t.ld && t.lc == t.lc)  // 0 * (-inf) from masked logits: guarded redo
-      t = pass1_thread<T, true, NT, G, false>(ch, cd, cc, pol_keep);
+      t = pass1_thread<T, true, NT, G>(ch, cd, cc, pol_keep);
     p1_publish<NW>(a, k, t, sm);
     return;
   }
@@ -688,198 +657,20 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constan
   p2_finish<T, NW>(a, k, s_loc, sm);
 }
 
-__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
-                                              uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
-      "%4;" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-      : "memory");
-}
-
-// Bulk-copy (TMA engine) variant: NC consumer threads + one producer warp.  The producer's lane 0
-// streams the chunk pair through a ring of NS shared-memory stages (SU units per consumer thread
-// per tensor per stage) with cp.async.bulk + mbarrier complete_tx, so the bytes in flight do not
-// depend on registers; consumers take unit tid + q NC of each stage -- the same units, per
-// thread, as the LDG variant's stride-NC walk.
-template <typename T, int SU, int NS, int MINB>
-__global__ void __launch_bounds__(kScoreThreads + 32, MINB) sv_score_tma_kernel(const __grid_constant__ ScoreArgs a) {
-  constexpr int NC = kScoreThreads, NW = NC / 32 + 1, EPU = Elem<T>::kPerUnit, SUN = SU * NC;
-  __shared__ Smem<NW> sm;
-  __shared__ uint64_t full[NS], empty[NS];
-  extern __shared__ __align__(128) uint4 stage_buf[];  // [NS][2][SUN]
-  pdl_wait();
-  pdl_trigger();
-  const Task k = task_of(a);
-  const float cd = a.cd, cc = a.cc;
-  const Chunk<T> ch = chunk_of<T>(a, k.bb, k.ii, k.rank);
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const bool producer = wid == NW - 1;
-  const int nst = (ch.units + SUN - 1) / SUN;
-  if (tid == 0) {
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NC / 32);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  const uint64_t pol = k.p2 ? l2_policy_evict_first() : l2_policy_evict_last();
-  auto issue = [&](int st) {  // producer lane 0 only
-    const int slot = st % NS;
-    if (st >= NS) mbar_wait(&empty[slot], ((st / NS) - 1) & 1);
-    const int u0 = st * SUN, nu = min(SUN, ch.units - u0);
-    uint4 *dst = stage_buf + (size_t)slot * 2 * SUN;
-    mbar_arrive_expect_tx(&full[slot], (uint32_t)(2 * nu * 16));
-    bulk_g2s_hint(dst, ch.d + (size_t)u0 * EPU, (uint32_t)(nu * 16), &full[slot], pol);
-    bulk_g2s_hint(dst + SUN, ch.c + (size_t)u0 * EPU, (uint32_t)(nu * 16), &full[slot], pol);
-  };
-
-  if (!k.p2) {
-    P1State t{kMFloor, kMFloor, kMFloor, kMFloor, 0.f, 0.f, 0.f};
-    if (producer) {
-      if (lane == 0)
-        for (int st = 0; st < nst; ++st) issue(st);
-    } else {
-      for (int st = 0; st < nst; ++st) {
-        const int slot = st % NS;
-        mbar_wait(&full[slot], (st / NS) & 1);
-        const uint4 *sd = stage_buf + (size_t)slot * 2 * SUN, *sc = sd + SUN;
-        const int nu = min(SUN, ch.units - st * SUN);
-        if (nu == SUN) {
-          uint4 rd[SU], rc[SU];
-#pragma unroll
-          for (int q = 0; q < SU; ++q) {
-            rd[q] = sd[tid + q * NC];
-            rc[q] = sc[tid + q * NC];
-          }
-          p1_group<T, false, SU>(t, rd, rc, cd, cc);
-        } else {
-          for (int u = tid; u < nu; u += NC) {
-            const uint4 rd[1] = {sd[u]}, rc[1] = {sc[u]};
-            p1_group<T, false, 1>(t, rd, rc, cd, cc);
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
-      }
-      // element tail (and the unaligned-chunk case, units == 0) from global
-      const int e0 = ch.units * EPU;
-      for (int e = e0 + tid; e < ch.n; e += NC) {
-        t.md = fmaxf(t.md, Elem<T>::load(ch.d + e));
-        t.mc = fmaxf(t.mc, Elem<T>::load(ch.c + e));
-      }
-      p1_rescale(t, cd, cc);
-      const float nmd = -t.rd * cd, nmc = -t.rc * cc;
-      for (int e = e0 + tid; e < ch.n; e += NC) {
-        const float ad = fmaf(Elem<T>::load(ch.d + e), cd, nmd), ac = fmaf(Elem<T>::load(ch.c + e), cc, nmc);
-        const float ed = ex2(ad);
-        t.ld += ed;
-        t.lc += ex2(ac);
-        t.w += ed > 0.f ? ed * (ad - ac) : 0.f;
-      }
-      if (t.w != t.w && t.ld == t.ld && t.lc == t.lc)  // 0 * (-inf) from masked logits: guarded redo
-        t = pass1_thread<T, true, NC, 1, false>(ch, cd, cc, pol);
-    }
-    p1_publish<NW>(a, k, t, sm);
-    return;
-  }
-
-  // P2: the first NS stages are requested before the partials are even merged
-  if (producer) {
-    if (lane == 0)
-      for (int st = 0; st < min(NS, nst); ++st) issue(st);
-    __syncwarp();
-    p2_merge<NW>(a, k, sm);
-  }
-  __syncthreads();
-  const float lamd = sm.lam[0], lamc = sm.lam[1];
-  const bool good = lamd == lamd && lamc == lamc;
-  float s_loc = 0.f;
-  if (producer) {
-    if (lane == 0)
-      for (int st = NS; st < nst; ++st) issue(st);
-  } else {
-    const f2 cdd{cd, cd}, ccc{cc, cc}, ld2{-lamd, -lamd}, lc2{-lamc, -lamc};
-    f2 acc{0.f, 0.f};
-    for (int st = 0; st < nst; ++st) {
-      const int slot = st % NS;
-      mbar_wait(&full[slot], (st / NS) & 1);
-      const uint4 *sd = stage_buf + (size_t)slot * 2 * SUN, *sc = sd + SUN;
-      const int nu = min(SUN, ch.units - st * SUN);
-      if (good) {
-        if (nu == SUN) {
-          uint4 rd[SU], rc[SU];
-#pragma unroll
-          for (int q = 0; q < SU; ++q) {
-            rd[q] = sd[tid + q * NC];
-            rc[q] = sc[tid + q * NC];
-          }
-          p2_group<T, SU>(acc, rd, rc, cdd, ccc, ld2, lc2);
-        } else {
-          for (int u = tid; u < nu; u += NC) {
-            const uint4 rd[1] = {sd[u]}, rc[1] = {sc[u]};
-            p2_group<T, 1>(acc, rd, rc, cdd, ccc, ld2, lc2);
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
-    }
-    if (good)
-      for (int e = ch.units * EPU + tid; e < ch.n; e += NC)
-        acc.x += ex2(fminf(fmaf(Elem<T>::load(ch.d + e), cd, -lamd), fmaf(Elem<T>::load(ch.c + e), cc, -lamc)));
-    s_loc = acc.x + acc.y;
-  }
-  p2_finish<T, NW>(a, k, s_loc, sm);
-}
-
-template <typename T, int NT, int MINB, int G, bool PF = false, int PFA = 0>
+template <typename T, int NT, int MINB, int G, int PFA = 0>
 cudaError_t launch_score_t(const ScoreArgs &a, cudaStream_t st) {
   const int64_t tasks = 2 * (int64_t)a.B * a.k * a.cs;
   if (tasks == 0) return cudaSuccess;
-  return launch_k(sv_score_kernel<T, NT, MINB, G, PF, PFA>, dim3((unsigned)tasks), dim3(NT), 0, st, a);
-}
-
-template <typename T, int SU, int NS, int MINB>
-cudaError_t launch_score_tma(const ScoreArgs &a, cudaStream_t st) {
-  const int64_t tasks = 2 * (int64_t)a.B * a.k * a.cs;
-  if (tasks == 0) return cudaSuccess;
-  const int smem = NS * 2 * SU * kScoreThreads * 16;
-  auto fn = sv_score_tma_kernel<T, SU, NS, MINB>;
-  static bool attr_done[64] = {};  // per instantiation and device
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64 || !attr_done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    if (dev >= 0 && dev < 64) attr_done[dev] = true;
-  }
-  return launch_k(fn, dim3((unsigned)tasks), dim3(kScoreThreads + 32), smem, st, a);
+  return launch_k(sv_score_kernel<T, NT, MINB, G, PFA>, dim3((unsigned)tasks), dim3(NT), 0, st, a);
 }
 
 template <typename T>
 cudaError_t launch_score_cfg(const ScoreArgs &a, cudaStream_t st) {
-  // threads x CTAs per SM (register budget) x loads in flight per thread; SV_SCORE_CFG overrides
-  static const int cfg = tune_knob("SV_SCORE_CFG", 0);
-  switch (cfg) {
-    case 1: return launch_score_t<T, 256, 4, 2, true>(a, st);
-    case 3: return launch_score_t<T, 256, 4, 3>(a, st);
-    case 5: return launch_score_tma<T, 2, 3, 4>(a, st);
-    case 6: return launch_score_tma<T, 1, 4, 5>(a, st);
-    case 7: return launch_score_tma<T, 2, 2, 5>(a, st);
-    case 8: return launch_score_tma<T, 1, 6, 4>(a, st);
-    default: {
-      // small grids (every task resident at once): the all-loads-up-front variant -- one memory
-      // round trip per pass instead of one per group; identical arithmetic, so identical bits
-      static const int small = tune_knob("SV_SCORE_SMALL", 1);
-      const int64_t tasks = 2 * (int64_t)a.B * a.k * a.cs;
-      if (small && tasks <= kScoreSmallGrid)
-        return launch_score_t<T, kScoreThreads, 2, kScoreGroup, false, kScoreSmallUnits>(a, st);
-      return launch_score_t<T, kScoreThreads, kScoreMinBlocks, kScoreGroup>(a, st);
-    }
-  }
+  // small grids (every task resident at once): the all-loads-up-front variant -- one memory
+  // round trip per pass instead of one per group; identical arithmetic, so identical bits
+  const int64_t tasks = 2 * (int64_t)a.B * a.k * a.cs;
+  if (tasks <= kScoreSmallGrid) return launch_score_t<T, kScoreThreads, 2, kScoreGroup, kScoreSmallUnits>(a, st);
+  return launch_score_t<T, kScoreThreads, kScoreMinBlocks, kScoreGroup>(a, st);
 }
 
 // ---------------------------------------------------------------- vocab-sharded staging
@@ -910,8 +701,8 @@ __global__ void __launch_bounds__(NT) sv_shard_p1_kernel(const __grid_constant__
   const Task k = shard_task(a);
   const Chunk<T> ch = chunk_of<T>(a, k.bb, k.ii, k.rank);
   const uint64_t pol = l2_policy_evict_last();
-  P1State t = pass1_thread<T, false, NT, kScoreGroup, false>(ch, a.cd, a.cc, pol);
-  if (t.w != t.w && t.ld == t.ld && t.lc == t.lc) t = pass1_thread<T, true, NT, 1, false>(ch, a.cd, a.cc, pol);
+  P1State t = pass1_thread<T, false, NT, kScoreGroup>(ch, a.cd, a.cc, pol);
+  if (t.w != t.w && t.ld == t.ld && t.lc == t.lc) t = pass1_thread<T, true, NT, 1>(ch, a.cd, a.cc, pol);
   p1_publish<NW>(a, k, t, sm);
   if (k.rank == 0 && threadIdx.x == 0) {
     const int64_t loc = (int64_t)a.tok[k.row] - v_begin;

@@ -47,10 +47,6 @@ def test_sm100a_cubin_embedded():
 def test_host_validation_without_gpu(lib):
     from paper_2509_24328_b200 import _lib
     assert lib.sv_status_string(0) == b"ok"
-    # bf16 V=152064 -> cluster of 8 CTAs, 76 KB of (D, C) per CTA
-    assert lib.sv_cluster_size(152064, _lib.SV_BF16) == 8
-    assert lib.sv_cluster_size(32000, _lib.SV_F32) == 4
-    assert lib.sv_cluster_size(10_000_000, _lib.SV_F32) == 0
     assert lib.sv_workspace_bytes(80, 8, 152064, _lib.SV_BF16) > 0
     assert lib.sv_workspace_bytes(80, 17, 152064, _lib.SV_BF16) == 0
     L = _lib.SvLogits(0, _lib.SV_BF16, 0, 0, 0)
@@ -66,6 +62,17 @@ def test_host_validation_without_gpu(lib):
     assert st == _lib.SV_ERR_INVALID_ARG
 
 
+def test_library_configured_by_arguments_only():
+    # SURVEY §5 / include/sv.h determinism promise: no environment variables, no tuning globals
+    csrc = os.path.join(ROOT, "paper_2509_24328_b200", "csrc")
+    for f in os.listdir(csrc):
+        with open(os.path.join(csrc, f)) as fh:
+            src = fh.read()
+        assert "getenv" not in src and "environ" not in src, f
+    with open(os.path.join(ROOT, "paper_2509_24328_b200", "__init__.py")) as fh:
+        assert "os.environ" not in fh.read()
+
+
 def test_product_has_no_cpu_fallback():
     # the package never imports the oracle, and compute calls refuse CPU tensors
     import torch
@@ -77,6 +84,38 @@ def test_product_has_no_cpu_fallback():
             assert "oracle" not in open(os.path.join(pkg, fn)).read().replace("fp64 oracle", "")
     with pytest.raises(sv.SvError):
         sv.sv_score(torch.zeros(1, 1, 8), torch.zeros(1, 1, 8), torch.zeros(1, 1, dtype=torch.int32))
+
+
+def test_wrappers_enforce_element_types_and_extents():
+    """The C ABI takes untyped pointers, so the binding checks what the kernels assume:
+    int32 tokens / gamma, T with k + 1 rows, C shaped like D, fp32 normalisers, int64 row pointers.
+    These checks run before any CUDA call (no GPU needed)."""
+    import torch
+
+    import paper_2509_24328_b200 as sv
+    D = torch.zeros(2, 3, 16)
+    ok_tok = torch.zeros(2, 3, dtype=torch.int32)
+    with pytest.raises(sv.SvError, match="int32"):
+        sv.sv_score(D, D, torch.zeros(2, 3, dtype=torch.int64))
+    with pytest.raises(sv.SvError, match="shape"):
+        sv.sv_score(D, torch.zeros(2, 3, 15), ok_tok)
+    with pytest.raises(sv.SvError, match="dtype"):
+        sv.sv_score(D, D.double(), ok_tok)
+    f32 = torch.zeros(2, 3)
+    g = torch.zeros(2, dtype=torch.int32)
+    with pytest.raises(sv.SvError, match="shape"):  # T with k rows instead of k + 1
+        sv.sd_verify(D, torch.zeros(2, 3, 16), ok_tok, g, f32, f32, f32)
+    T = torch.zeros(2, 4, 16)
+    with pytest.raises(sv.SvError, match="int32"):
+        sv.sd_verify(D, T, ok_tok, g.long(), f32, f32, f32)
+    with pytest.raises(sv.SvError, match="float32"):
+        sv.sd_verify(D, T, ok_tok, g, f32.double(), f32, f32)
+    with pytest.raises(sv.SvError, match="int64"):
+        sv.sd_verify_ragged(D, torch.zeros(8, 16), torch.zeros(2, dtype=torch.int32), ok_tok, g, f32, f32, f32)
+    with pytest.raises(sv.SvError, match="float32"):
+        sv.sv_schedule(torch.zeros(2, 3, dtype=torch.float64), torch.zeros(5, dtype=torch.float64))
+    with pytest.raises(sv.SvError, match="out"):  # a caller-provided output of the wrong type
+        sv.sv_score(D, D, ok_tok, out={"S": torch.zeros(2, 3, dtype=torch.float64)})
 
 
 def test_host_validation_of_the_widened_abi(lib):

@@ -445,6 +445,23 @@ def test_filter_spec_examples():
     assert np.allclose(p, [0.5, 0.3, 0.2], rtol=0, atol=1e-15)
 
 
+def test_filter_sample_zero_residual_falls_back_to_target():
+    """R10 (S L152 asserts the zero residual unreachable; it is reachable through rounding only):
+    a zero residual mass samples p_t of the same row and is flagged; otherwise the residual is
+    max(0, p_t - p_d) (S L157-165) and the bonus samples p_t."""
+    from oracle.filtered import sample_filtered
+    pt = np.array([0.0, 0.25, 0.0, 0.75])
+    # p_d = p_t -> r = 0 everywhere: the draw is inverse-CDF over p_t (cum .25, 1.0)
+    assert sample_filtered(pt, pt.copy(), 0.2)[::3] == (1, True)
+    tok, z, _, rz = sample_filtered(pt, pt.copy(), 0.5)
+    assert (tok, z, rz) == (3, 1.0, True)
+    # ordinary residual: p_d = one-hot at 1 -> r = [0, 0, 0, .75], Z = .75
+    tok, z, _, rz = sample_filtered(pt, np.array([0.0, 1.0, 0.0, 0.0]), 0.99)
+    assert (tok, z, rz) == (3, 0.75, False)
+    # bonus (no draft): plain p_t
+    assert sample_filtered(pt, None, 0.1)[0] == 1
+
+
 def test_filter_identity_idempotence_support():
     """Identity config = plain softmax (S L78) and idempotent; every config shrinks the support
     (S L196-197: "idempotent for identity config and monotone-support-shrinking otherwise");
