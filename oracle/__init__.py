@@ -79,7 +79,7 @@ def lib():
         _lib.oracle_batch_greedy.argtypes = [P, i32, i32, P, i32, P, P]
         _lib.oracle_batch_greedy.restype = d
         _lib.oracle_verify.argtypes = [P, P, P, P, i32, i32, i64, d, d, u64, u64, i64,
-                                       P, P, P, P, P, P, P, i32]
+                                       P, P, P, P, P, P, P, i32, P, P, P]
     return _lib
 
 
@@ -233,25 +233,38 @@ def batch_greedy(p_hat, L) -> dict:
 
 
 # --------------------------------------------------------------------- a5 + a6
-def verify(D, T, tok, gamma, tau_d=1.0, tau_t=1.0, seed=0, offset=0, seq_base=0, nthreads=None) -> dict:
+def verify(D, T, tok, gamma, tau_d=1.0, tau_t=1.0, seed=0, offset=0, seq_base=0, nthreads=None,
+           n_force=None) -> dict:
     """Standard SD verification + residual / bonus inverse-CDF sample
-    (P L29; S L148-165, L82-90; R1, R10-R13)."""
+    (P L29; S L148-165, L82-90; R1, R10-R13).
+
+    Tie reporting (north_star: decisions within 1e-6 of their threshold are logged):
+    ``accept_margins[b, i]`` = |u_i - ratio_i| of every test performed; ``sample_margin_hi`` =
+    |cum_{j*} - u_s Z| and ``sample_margin_lo`` = |cum_{j*-1} - u_s Z| with ``tok_next`` /
+    ``tok_prev`` the positive-residual neighbours a perturbed sampler would pick instead.
+    ``n_force[b] >= 0`` replaces the first rejection by a given N (stage-wise comparison of the
+    sampling step after a logged accept tie); ratios and margins are still those of the tests."""
     D, T = _f64(D), _f64(T)
     B, k, V = D.shape
     assert T.shape == (B, k + 1, V)
     tok = _i32(tok).reshape(B, k)
     gamma = _i32(gamma).reshape(B)
+    nf = None if n_force is None else _i32(n_force).reshape(B)
     n_acc = np.empty(B, dtype=np.int32)
     out_tok = np.empty(B, dtype=np.int32)
     ratio = np.empty((B, k))
     Z = np.empty(B)
     st = np.empty(B, dtype=np.int32)
-    margins = np.empty((B, 2))
+    margins = np.empty((B, 3))
     ea = np.empty((B, k))
+    am = np.empty((B, k))
+    nbr = np.empty((B, 2), dtype=np.int32)
     lib().oracle_verify(_p(D), _p(T), _p(tok), _p(gamma), B, k, V, tau_d, tau_t,
                         ctypes.c_uint64(seed), ctypes.c_uint64(offset), seq_base,
                         _p(n_acc), _p(out_tok), _p(ratio), _p(Z), _p(st), _p(margins), _p(ea),
-                        nthreads or default_threads())
+                        nthreads or default_threads(), _p(nf) if nf is not None else None, _p(am), _p(nbr))
     return {"n_accept": n_acc, "out_tok": out_tok, "accept_ratio": ratio, "resid_mass": Z,
-            "status": st, "accept_margin": margins[:, 0], "sample_margin": margins[:, 1],
-            "exp_accept_true": ea}
+            "status": st, "accept_margin": margins[:, 2], "accept_margins": am,
+            "sample_margin": np.minimum(margins[:, 0], margins[:, 1]),
+            "sample_margin_hi": margins[:, 0], "sample_margin_lo": margins[:, 1],
+            "tok_prev": nbr[:, 0], "tok_next": nbr[:, 1], "exp_accept_true": ea}

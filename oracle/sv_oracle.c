@@ -376,14 +376,24 @@ double oracle_batch_greedy(const double *p_hat, int32_t B, int32_t k, const doub
 /* min(1, P_t/P_d) for every i < gamma (the paper's X, P L150), NaN otherwise. */
 /* Any data error in a verified row (or the resampled row): status, N = 0,    */
 /* token = -1, Z = NaN.                                                       */
-/* margins (optional, [B, 2]): min |u_i - ratio_i| over the tests performed,  */
-/* and min(|cum_{j*} - theta|, |cum_{j*-1} - theta|) for the sampled token.   */
+/* Reporting for tie handling (north_star: "ties within 1e-6 of the threshold   */
+/* logged"); none of it changes a decision:                                   */
+/*   margins [B, 3] (optional): |cum_{j*} - theta| (theta just below the       */
+/*     crossing: a perturbed sampler may pick the next positive entry),        */
+/*     |cum_{j*-1} - theta| (theta just above the previous cumulative: it may  */
+/*     pick the previous positive entry), and min |u_i - ratio_i|;             */
+/*   acc_margins [B, k] (optional): |u_i - ratio_i| for every test performed;  */
+/*   nbr [B, 2] (optional): the previous / next index with r > 0 around j*.    */
+/* n_force [B] (optional, -1 = off): take N = n_force[b] instead of the first  */
+/* rejection (the ratios are still reported) -- used to compare the sampling  */
+/* stage on the GPU's own N after a logged accept tie.                        */
 /* ------------------------------------------------------------------------ */
 void oracle_verify(const double *D, const double *T, const int32_t *tok, const int32_t *gamma_in,
                    int32_t B, int32_t k, int64_t V, double tau_d, double tau_t,
                    uint64_t seed, uint64_t offset, int64_t seq_base,
                    int32_t *n_accept, int32_t *out_tok, double *accept_ratio, double *resid_mass,
-                   int32_t *status, double *margins, double *exp_accept_true, int32_t nthreads)
+                   int32_t *status, double *margins, double *exp_accept_true, int32_t nthreads,
+                   const int32_t *n_force, double *acc_margins, int32_t *nbr)
 {
 #pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads > 0 ? nthreads : 1)
     for (int32_t b = 0; b < B; ++b) {
@@ -396,7 +406,9 @@ void oracle_verify(const double *D, const double *T, const int32_t *tok, const i
         for (int i = 0; i < k; ++i) {
             accept_ratio[(int64_t)b * k + i] = NAN;
             if (exp_accept_true) exp_accept_true[(int64_t)b * k + i] = NAN;
+            if (acc_margins) acc_margins[(int64_t)b * k + i] = NAN;
         }
+        if (nbr) { nbr[2 * b] = -1; nbr[2 * b + 1] = -1; }
         if (gamma < 0 || gamma > k) st |= O_ROW_BAD_GAMMA;
         /* Every verified row i < gamma is scored (its X = min(1, ratio) is reported,
          * DESIGN R13); the accept chain stops at the first rejection. */
@@ -418,16 +430,18 @@ void oracle_verify(const double *D, const double *T, const int32_t *tok, const i
                 oracle_uniforms(seed, offset, seq_base + b, i, &u, NULL);
                 double mg = fabs(u - ratio);
                 if (mg < m_acc) m_acc = mg;
+                if (acc_margins) acc_margins[(int64_t)b * k + i] = mg;
                 if (!(u < ratio)) N = i;
             }
         }
+        if (!st && n_force && n_force[b] >= 0 && n_force[b] <= gamma) N = n_force[b];
         if (st) {
             n_accept[b] = 0;
             out_tok[b] = -1;
             resid_mass[b] = NAN;
             status[b] = st;
             for (int i = 0; i < k; ++i) accept_ratio[(int64_t)b * k + i] = NAN;
-            if (margins) { margins[2 * b] = NAN; margins[2 * b + 1] = NAN; }
+            if (margins) { margins[3 * b] = NAN; margins[3 * b + 1] = NAN; margins[3 * b + 2] = NAN; }
             free(pd); free(pt); free(r);
             continue;
         }
@@ -451,7 +465,7 @@ void oracle_verify(const double *D, const double *T, const int32_t *tok, const i
             out_tok[b] = -1;
             resid_mass[b] = NAN;
             status[b] = st;
-            if (margins) { margins[2 * b] = NAN; margins[2 * b + 1] = NAN; }
+            if (margins) { margins[3 * b] = NAN; margins[3 * b + 1] = NAN; margins[3 * b + 2] = NAN; }
             free(pd); free(pt); free(r);
             continue;
         }
@@ -461,24 +475,30 @@ void oracle_verify(const double *D, const double *T, const int32_t *tok, const i
         }
         double theta = u_s * Z;
         double cum = 0.0, prev = 0.0;
-        int64_t j_star = -1, last_pos = -1;
+        int64_t j_star = -1, last_pos = -1, j_prev = -1, j_next = -1;
+        double m_hi = INFINITY, m_lo = INFINITY;
         for (int64_t v = 0; v < V; ++v) {
             prev = cum;
             cum += r[v];
-            if (r[v] > 0.0) last_pos = v;
             if (cum > theta) { j_star = v; break; }
+            if (r[v] > 0.0) last_pos = v;
         }
         if (j_star < 0) {
             j_star = last_pos;
         } else {
-            double a1 = fabs(cum - theta), a0 = fabs(prev - theta);
-            m_smp = a1 < a0 ? a1 : a0;
+            m_hi = fabs(cum - theta);
+            m_lo = fabs(prev - theta);
+            j_prev = last_pos; /* the positive entry before j* (r[j*] > 0 since cum grew) */
+            for (int64_t v = j_star + 1; v < V; ++v)
+                if (r[v] > 0.0) { j_next = v; break; }
         }
         n_accept[b] = N;
         out_tok[b] = (int32_t)j_star;
         resid_mass[b] = Z;
         status[b] = st;
-        if (margins) { margins[2 * b] = m_acc; margins[2 * b + 1] = m_smp; }
+        (void)m_smp;
+        if (margins) { margins[3 * b] = m_hi; margins[3 * b + 1] = m_lo; margins[3 * b + 2] = m_acc; }
+        if (nbr) { nbr[2 * b] = (int32_t)j_prev; nbr[2 * b + 1] = (int32_t)j_next; }
         free(pd); free(pt); free(r);
     }
 }

@@ -65,6 +65,7 @@ def test_filtered_parity(sv, B, k, V, dtype, top_k, top_p, tau):
     assert np.array_equal(gv["n_accept"][~tie], rv["n_accept"][~tie])
     assert np.array_equal(gv["out_tok"][~tie], rv["out_tok"][~tie])
     assert H.close(gv["resid_mass"][~tie], rv["resid_mass"][~tie]).all()
+    assert np.array_equal((gv["status"][~tie] & 32) != 0, rv["resid_zero"][~tie])  # R10 flag
     r_ok = ~np.isnan(rv["accept_ratio"])
     assert np.array_equal(np.isnan(gv["accept_ratio"]), ~r_ok)
     assert H.close(gv["accept_ratio"][r_ok], rv["accept_ratio"][r_ok]).all()
@@ -212,6 +213,7 @@ def test_nucleus_only_verify(sv):
     assert np.array_equal(gv["n_accept"][~tie], rv["n_accept"][~tie])
     assert np.array_equal(gv["out_tok"][~tie], rv["out_tok"][~tie])
     assert H.close(gv["resid_mass"][~tie], rv["resid_mass"][~tie]).all()
+    assert np.array_equal((gv["status"][~tie] & 32) != 0, rv["resid_zero"][~tie])  # R10 flag
 
 
 @pytest.mark.parametrize("r,V,tp", [(0.995, 5000, 0.9),      # 460 tokens: candidate sort

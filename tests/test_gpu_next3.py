@@ -5,6 +5,7 @@ Philox offset offset0 + j (P L266 for the compaction; DESIGN R12 for the offset 
 import numpy as np
 import pytest
 
+import oracle
 import synth
 import sv_helpers as H
 
@@ -43,6 +44,13 @@ def test_ragged_target_matches_dense(sv, B, k, V, dtype):
                               11, 3)
     for n in dense:
         assert _eq(dense[n], rag[n]), n
+    # and the ragged call itself against the oracle (P L266 compaction changes no arithmetic)
+    torch.cuda.synchronize()
+    Dd, _, Td = H.oracle_inputs(x)
+    rv = oracle.verify(Dd, Td, x["tok"], g, 1.0, 1.0, 11, 3, 0)
+    rep = H.ParityReport()
+    H.compare_verify(H.gpu_np(rag), rv, rep, H.oracle_rerun(Dd, Td, x["tok"], g, 1.0, 1.0, 11, 3, 0))
+    print("ties:", rep.ties)
 
 
 def test_graph_replay_matches_eager(sv):
@@ -95,23 +103,60 @@ def test_score_schedule_fused_matches_separate(sv, B, k, V, dtype):
         assert _eq(sh[n], fh[n]), n
 
 
-def test_graph_replay_headline_size(sv):
-    """The bench's headline launch configuration (GraphPipeline: sv_score, sv_schedule,
-    sd_verify_ragged in one graph) at B=80, k=8, V=152064 bf16 equals the eager pipeline
-    bitwise (which test_gpu_parity checks against the oracle at this size)."""
-    B, k, V = 80, 8, 152064
-    x = synth.make_inputs(B, k, V, "bf16", seed=0x5EED)
+def _graph_vs_oracle(sv, B, k, V, dtype, seed_in, offset0, replays, seq_base=0):
+    """The bench's timed path -- GraphPipeline (sv_score, sv_schedule, sd_verify_ragged with a
+    device-side Philox offset, offset += 1, one CUDA graph) -- replayed `replays` times and every
+    replay compared with the oracle on ALL sequences: score and schedule stage-wise, verify at
+    offset0 + j (R12: replay j draws the uniforms of offset0 + j)."""
+    x = synth.make_inputs(B, k, V, dtype, seed=seed_in, seq_ids=np.arange(seq_base, seq_base + B))
     D, C, T, tok = H.to_torch(x)
-    prof = sv.Profile.from_dict(synth.load_profile())
-    L = torch.tensor(synth.latency_table(k + 2), dtype=torch.float64, device="cuda")
-    gp = sv.GraphPipeline(B, k, V, torch.bfloat16, prof, L, seed=0xC0FFEE, offset0=4)
+    prof_dict = synth.load_profile()
+    prof = sv.Profile.from_dict(prof_dict)
+    Lh = synth.latency_table(k + 2)
+    L = torch.tensor(Lh, dtype=torch.float64, device="cuda")
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    gp = sv.GraphPipeline(B, k, V, tdt, prof, L, seed=0xC0FFEE, offset0=offset0, seq_base=seq_base)
     gp.D.copy_(D)
     gp.C.copy_(C)
     gp.T.copy_(T)
     gp.tok.copy_(tok)
     gp.capture()
-    out = {n: v.clone() for n, v in gp.replay().items()}
-    ref = sv.Pipeline(B, k, V, torch.bfloat16, prof, L).run(D, C, T, tok, seed=0xC0FFEE, offset=4)
+    outs = []
+    for _ in range(replays):
+        gv = {n: v.clone() for n, v in gp.replay().items()}
+        gs = {n: v.clone() for n, v in gp.pipe.score_out.items()}
+        gh = {n: v.clone() for n, v in gp.pipe.sched_out.items()}
+        outs.append((gs, gh, gv))
     torch.cuda.synchronize()
-    for n in ref:
-        assert _eq(out[n], ref[n]), n
+    assert int(gp.offset.item()) == offset0 + replays
+    del gp, D, C, T
+    Dd, Cd, Td = H.oracle_inputs(x)
+    rs = oracle.score(Dd, Cd, x["tok"], 1.0, 1.0, prof_dict)
+    rep = H.ParityReport()
+    for j, (gs, gh, gv) in enumerate(outs):
+        gs, gh, gv = H.gpu_np(gs), H.gpu_np(gh), H.gpu_np(gv)
+        H.compare_score(gs, rs, prof_dict, rep)
+        rh = oracle.schedule(gs["p_hat"].astype(np.float64), Lh)
+        assert np.array_equal(gh["gamma"], rh["gamma"])
+        assert np.array_equal(gh["exp_accept"], rh["exp_accept"].astype(np.float32))
+        gam = gh["gamma"]
+        off = offset0 + j
+        rv = oracle.verify(Dd, Td, x["tok"], gam, 1.0, 1.0, 0xC0FFEE, off, seq_base)
+        H.compare_verify(gv, rv, rep, H.oracle_rerun(Dd, Td, x["tok"], gam, 1.0, 1.0, 0xC0FFEE, off, seq_base))
+    return rep
+
+
+def test_graph_replay_headline_size_vs_oracle(sv):
+    """BASELINE config 3 at full size (B=80, k=8, V=152064 bf16), the exact launch configuration
+    bench.py times, three consecutive replays, all 80 sequences against the oracle."""
+    rep = _graph_vs_oracle(sv, 80, 8, 152064, "bf16", 0x5EED, offset0=4, replays=3)
+    print("ties:", rep.ties)
+
+
+@pytest.mark.parametrize("B,k,V,dtype,seq_base", [(4, 4, 32000, "f32", 0), (32, 8, 32000, "bf16", 0),
+                                                  (40, 8, 152064, "bf16", 40)])
+def test_graph_replay_configs_vs_oracle(sv, B, k, V, dtype, seq_base):
+    """Configs 1 and 2 and one rank's half of config 3 at world size 2 (seq_base = 40) through
+    the graph path, three replays each, against the oracle."""
+    rep = _graph_vs_oracle(sv, B, k, V, dtype, 0x5EED + V + B, offset0=7, replays=3, seq_base=seq_base)
+    print("ties:", rep.ties)

@@ -54,7 +54,7 @@ def run_case(sv, prof_dict, x, tau=(1.0, 1.0, 1.0), seed=0xC0FFEE, offset=3, seq
     else:
         gam_np = np.asarray(gamma, dtype=np.int32)
     rv = oracle.verify(Dd, Td, x["tok"], gam_np, tau[0], tau[2], seed, offset, seq_base)
-    H.compare_verify(gv, rv, rep)
+    H.compare_verify(gv, rv, rep, H.oracle_rerun(Dd, Td, x["tok"], gam_np, tau[0], tau[2], seed, offset, seq_base))
     return gs, gv, gam_np, rep
 
 
@@ -215,7 +215,8 @@ def test_headline_full_size_sampled(sv, prof_dict):
         rs = oracle.score(Dd, Cd, sub["tok"], 1.0, 1.0, prof_dict)
         H.compare_score({kk: v[b:b + 1] for kk, v in gs.items()}, rs, prof_dict, rep)
         rv = oracle.verify(Dd, Td, sub["tok"], gam[b:b + 1], 1.0, 1.0, 0xC0FFEE, 1, b)
-        H.compare_verify({kk: v[b:b + 1] for kk, v in gv.items()}, rv, rep)
+        H.compare_verify({kk: v[b:b + 1] for kk, v in gv.items()}, rv, rep,
+                         H.oracle_rerun(Dd, Td, sub["tok"], gam[b:b + 1], 1.0, 1.0, 0xC0FFEE, 1, b))
     print("ties:", rep.ties)
 
 
@@ -237,3 +238,71 @@ def test_extreme_shapes(sv, prof_dict, B, k, V, dtype):
     x = synth.make_inputs(B, k, V, dtype, seed=31337 + V)
     *_, rep = run_case(sv, prof_dict, x)
     print("ties:", rep.ties)
+
+
+def test_golden_convention_vector_gpu(sv):
+    """SURVEY §8(c)'s golden convention vector (tests/golden/convention_vector.json) through the
+    CUDA path: every printed value within its 6-decimal rounding, integer decisions exact."""
+    g, x, Lh = H.load_golden()
+    e, st = g["expected"], g["setup"]
+    D, C, T, tok = H.to_torch(x)
+    prof = sv.Profile.from_dict(st["profile"])
+    L = torch.tensor(Lh, dtype=torch.float64, device="cuda")
+    gs = sv.sv_score(D, C, tok, 1.0, 1.0, prof)
+    gh = sv.sv_schedule(gs["p_hat"], L)
+    gv = sv.sd_verify(D, T, tok, gh["gamma"], gs["draft_m"], gs["draft_l"], gs["draft_ptok"], 1.0, 1.0,
+                      st["seed"], st["offset"], st["seq_base"])
+    torch.cuda.synchronize()
+    gs, gh, gv = H.gpu_np(gs), H.gpu_np(gh), H.gpu_np(gv)
+    tol = 6e-7
+    for n in ("S", "A", "KL"):
+        assert np.allclose(gs[n], e[n], rtol=0, atol=tol), (n, gs[n])
+    assert np.array_equal(gs["p_hat"], np.array(e["p_hat"], dtype=np.float32))
+    assert gh["gamma"].tolist() == e["gamma"]
+    want_ratio = np.array([[np.nan if v is None else v for v in row] for row in e["accept_ratio"]])
+    assert np.allclose(gv["accept_ratio"], want_ratio, rtol=0, atol=tol, equal_nan=True)
+    assert gv["n_accept"].tolist() == e["n_accept"] and gv["out_tok"].tolist() == e["out_tok"]
+    assert np.allclose(gv["resid_mass"], e["resid_mass"], rtol=0, atol=tol)
+
+
+def test_schedule_literal_goodput_plus_one_0(sv):
+    """R2's literal reading g_j = E_j / L[j] (plus_one = 0) on the GPU: bit-exact with the oracle,
+    including the S L392 chain where it moves gamma from 2 to 3."""
+    rng = np.random.default_rng(19)
+    ph = np.concatenate([np.array([[0.9, 0.9, 0.2, 0.2, 0.2, 0.0, 0.0, 0.0]], dtype=np.float32),
+                         (rng.random((300, 8)) ** rng.uniform(0.2, 3, (300, 1))).astype(np.float32)])
+    for Lh in (np.array([10.0 + n for n in range(10)]), synth.latency_table(10),
+               np.cumsum(rng.random(10) + 0.05)):
+        g = sv.sv_schedule(torch.as_tensor(ph, device="cuda"), torch.as_tensor(Lh, device="cuda"), plus_one=0)
+        torch.cuda.synchronize()
+        r = oracle.schedule(ph.astype(np.float64), Lh, plus_one=0)
+        assert np.array_equal(g["gamma"].cpu().numpy(), r["gamma"])
+        assert np.array_equal(g["exp_accept"].cpu().numpy(), r["exp_accept"].astype(np.float32))
+        assert np.array_equal(g["goodput"].cpu().numpy(), r["goodput"].astype(np.float32))
+    g = sv.sv_schedule(torch.as_tensor(ph[:1], device="cuda"),
+                       torch.as_tensor(np.array([10.0 + n for n in range(10)]), device="cuda"), plus_one=0)
+    assert int(g["gamma"][0]) == 3
+
+
+def test_schedule_phat_out_of_range_and_bad_latency(sv):
+    """R22: p_hat outside [0, 1] is used as 0 and flagged PHAT_BAD, in both schedule modes; the
+    batch-greedy mode flags every sequence BAD_LATENCY when a reachable latency is not positive."""
+    ph = np.array([[0.9, 1.5, 0.9], [0.5, -0.25, 0.5], [0.0, 1.0, 0.7], [np.nan, 0.5, 0.5]], dtype=np.float32)
+    Lh = synth.latency_table(5)
+    g = sv.sv_schedule(torch.as_tensor(ph, device="cuda"), torch.as_tensor(Lh, device="cuda"))
+    r = oracle.schedule(ph.astype(np.float64), Lh)
+    assert np.array_equal(g["gamma"].cpu().numpy(), r["gamma"])
+    assert np.array_equal(g["status"].cpu().numpy(), r["status"])
+    assert (g["status"].cpu().numpy() & oracle.ROW_PHAT_BAD).tolist() == [16, 16, 0, 16]
+    Lg = synth.latency_table(4 * 4 + 1, base=4.0, knee=8, slope=0.5)
+    g = sv.sv_schedule(torch.as_tensor(ph, device="cuda"), torch.as_tensor(Lg, device="cuda"),
+                       mode=sv.SV_SCHED_BATCH_GREEDY)
+    rg = oracle.batch_greedy(ph.astype(np.float64), Lg)
+    assert np.array_equal(g["gamma"].cpu().numpy(), rg["gamma"])
+    assert (g["status"].cpu().numpy() & oracle.ROW_PHAT_BAD).tolist() == [16, 16, 0, 16]
+    Lg[6] = -1.0
+    g = sv.sv_schedule(torch.as_tensor(ph, device="cuda"), torch.as_tensor(Lg, device="cuda"),
+                       mode=sv.SV_SCHED_BATCH_GREEDY)
+    rg = oracle.batch_greedy(ph.astype(np.float64), Lg)
+    assert np.array_equal(g["gamma"].cpu().numpy(), rg["gamma"]) and rg["gamma"].tolist() == [0, 0, 0, 0]
+    assert np.all(g["status"].cpu().numpy() == oracle.ROW_BAD_LATENCY)

@@ -65,7 +65,8 @@ def test_vocab_sharded_matches_oracle(sv, B, k, V, dtype, G):
     rh = oracle.schedule(s0["p_hat"].astype(np.float64), synth.latency_table(k + 2))
     assert np.array_equal(gam, rh["gamma"])
     gv = H.gpu_np(outs[0])
-    H.compare_verify(gv, oracle.verify(Dd, Td, x["tok"], gam, 1.0, 1.0, 0xC0FFEE, 5, 0), rep)
+    H.compare_verify(gv, oracle.verify(Dd, Td, x["tok"], gam, 1.0, 1.0, 0xC0FFEE, 5, 0), rep,
+                     H.oracle_rerun(Dd, Td, x["tok"], gam, 1.0, 1.0, 0xC0FFEE, 5, 0))
     print("ties:", rep.ties)
 
 
@@ -82,4 +83,5 @@ def test_vocab_sharded_forced_gamma_and_bonus(sv):
     assert np.array_equal(gv["n_accept"], gam)  # identical rows: every verified token accepted
     Dd, Cd, Td = H.oracle_inputs(x)
     rep = H.ParityReport()
-    H.compare_verify(gv, oracle.verify(Dd, Td, x["tok"], gam, 1.0, 1.0, 0xC0FFEE, 5, 0), rep)
+    H.compare_verify(gv, oracle.verify(Dd, Td, x["tok"], gam, 1.0, 1.0, 0xC0FFEE, 5, 0), rep,
+                     H.oracle_rerun(Dd, Td, x["tok"], gam, 1.0, 1.0, 0xC0FFEE, 5, 0))

@@ -126,6 +126,22 @@ def test_a_is_one_when_companion_dominates():
     assert abs(r["A"] - 0.5) < 1e-12
 
 
+def test_kl_two_point_closed_form():
+    """KL between two-point distributions (north_star KL, direction R6: expectation under the
+    draft).  Bernoulli closed form: KL(Ber(1/2) || Ber(1/4)) = 1/2 ln(1/2 / 1/4) + 1/2 ln(1/2 /
+    3/4) = 1/2 ln(4/3); the reverse direction KL(Ber(1/4) || Ber(1/2)) = 3/4 ln 3 - ln 2.  Both
+    through oracle.score on logits (softmax included): draft [0, 0], companion [0, ln 3]."""
+    D = np.array([[[0.0, 0.0]]])
+    C = np.array([[[0.0, math.log(3.0)]]])
+    r = oracle.score(D, C, [[0]])
+    assert abs(r["KL"][0, 0] - 0.5 * math.log(4.0 / 3.0)) < 1e-15
+    r = oracle.score(C, D, [[0]])  # swapped roles: the other direction
+    assert abs(r["KL"][0, 0] - (0.75 * math.log(3.0) - math.log(2.0))) < 1e-15
+    # p_c = 0 where p_d > 0 -> +inf
+    r = oracle.score(D, np.array([[[0.0, -np.inf]]]), [[0]])
+    assert np.isinf(r["KL"][0, 0]) and r["KL"][0, 0] > 0
+
+
 def test_kl_against_scipy_gibbs_pinsker():
     rng = np.random.default_rng(4)
     for _ in range(50):
@@ -299,9 +315,47 @@ def test_first_decline_equals_argmax_under_convex_latency():
         assert oracle.first_decline(chain, L) == oracle.schedule(chain[None], L)["gamma"][0]
 
 
+def test_goodput_literal_reading_plus_one_0():
+    """R2's literal reading of P L211 ("expected number of accepted tokens divided by
+    verification latency"): g_j = E_j / L[j].  Hand enumeration of the S L392 chain
+    p=[.9,.9,.2,.2,.2] with L[n] = 10 + n: E = 0, .9, 1.71, 1.872, 1.9044, 1.91088, so
+    g = 0/10, .9/11, 1.71/12, 1.872/13, 1.9044/14, 1.91088/15 and the maximum moves from
+    gamma = 2 (plus_one = 1, S L392) to gamma = 3."""
+    L = _lat(10, 0, 1, 8)
+    chain = [0.9, 0.9, 0.2, 0.2, 0.2]
+    g = oracle.goodputs(chain, L, plus_one=0)
+    by_hand = [0 / 10, 0.9 / 11, 1.71 / 12, 1.872 / 13, 1.9044 / 14, 1.91088 / 15]
+    assert np.allclose(g, by_hand, rtol=0, atol=1e-12)
+    r = oracle.schedule(np.array([chain]), L, plus_one=0)
+    assert r["gamma"][0] == 3 and abs(r["exp_accept"][0] - 1.872) < 1e-12
+    assert abs(r["goodput"][0] - 1.872 / 13) < 1e-12
+    # gamma = 0 scores 0 under the literal reading: an all-zero chain ties everywhere -> 0 (S L396)
+    assert oracle.schedule(np.zeros((1, 4)), L, plus_one=0)["gamma"][0] == 0
+    # constant acceptance alpha, flat latency: E_j = alpha (1 - alpha^j) / (1 - alpha) (Leviathan's
+    # closed form minus the bonus token) is increasing, so gamma* = k
+    r = oracle.schedule(np.full((1, 7), 0.5), np.full(9, 2.0), plus_one=0)
+    assert r["gamma"][0] == 7 and abs(r["exp_accept"][0] - 0.5 * (1 - 0.5 ** 7) / 0.5) < 1e-15
+    # exhaustive argmax with brute-force E (2^gamma enumeration, S L383) under the literal reading
+    rng = np.random.default_rng(17)
+    for _ in range(200):
+        k = int(rng.integers(1, 9))
+        chain = rng.random(k)
+        Lr = np.cumsum(rng.random(k + 3) + 0.05)
+        g_bf = [_brute_force_E(chain, j) / Lr[j] for j in range(k + 1)]
+        gam = oracle.schedule(chain[None], Lr, plus_one=0)["gamma"][0]
+        assert g_bf[gam] >= max(g_bf) - 1e-12
+
+
 def test_schedule_bad_inputs():
     r = oracle.schedule(np.array([[np.nan, 0.5]]), _lat(4, 2, 1, 4))
     assert r["status"][0] & oracle.ROW_PHAT_BAD
+    # R22: p_hat is an acceptance probability (P L176); outside [0, 1] it is used as 0 and flagged
+    for bad in (1.5, -0.25, np.inf):
+        r = oracle.schedule(np.array([[0.9, bad, 0.9]]), np.full(6, 2.0))
+        assert r["status"][0] & oracle.ROW_PHAT_BAD
+        assert r["gamma"][0] == 1 and r["exp_accept"][0] == 0.9  # the chain stops at the bad entry
+    r = oracle.schedule(np.array([[0.0, 1.0]]), np.full(4, 2.0))
+    assert r["status"][0] == 0  # the end points are probabilities
     r = oracle.schedule(np.array([[0.5, 0.5]]), np.array([0.0, 1.0, -1.0, 1.0]))
     assert r["status"][0] & oracle.ROW_BAD_LATENCY and r["gamma"][0] == 0
 
@@ -313,6 +367,17 @@ def test_batch_greedy_spec_trace():
     r = oracle.batch_greedy(np.array([[0.9, 0.9], [0.8, 0.8]]), _lat(4, 2, 1, 10))
     assert list(r["gamma"]) == [2, 1]
     assert abs(r["goodput"] - 4.51 / 7) < 1e-12
+
+
+def test_batch_greedy_bad_inputs():
+    # a non-positive / non-finite reachable latency: gamma = 0 everywhere, goodput NaN
+    L = _lat(4, 2, 1, 10)
+    L[5] = 0.0
+    r = oracle.batch_greedy(np.array([[0.9, 0.9], [0.8, 0.8]]), L)
+    assert list(r["gamma"]) == [0, 0] and np.isnan(r["goodput"])
+    # R22: p_hat outside [0, 1] counts as 0 -> that query never gains a token
+    r = oracle.batch_greedy(np.array([[1.5, 0.9], [0.8, 0.8]]), _lat(4, 2, 1, 10))
+    assert r["gamma"][0] == 0
 
 
 def test_batch_greedy_consistency_properties():
@@ -383,6 +448,73 @@ def test_gamma_zero_is_target_sampling():
     assert np.all(r["n_accept"] == 0)
     freq = np.bincount(r["out_tok"], minlength=4) / r["out_tok"].size
     assert np.abs(freq - pt).sum() / 2 < 0.005
+
+
+def test_survey_golden_convention_vector():
+    """SURVEY §8(c) golden convention vector (tests/golden/convention_vector.json; values from an
+    independent scratch implementation of the conventions, printed to 6 decimals) through the
+    whole oracle pipeline: score -> schedule -> verify, and the Philox words it draws."""
+    import sv_helpers as H
+    g, x, L = H.load_golden()
+    e, st = g["expected"], g["setup"]
+    prof = st["profile"]
+    D, C, T = (x[n].astype(np.float64) for n in ("D", "C", "T"))
+    rs = oracle.score(D, C, x["tok"], 1.0, 1.0, prof)
+    tol = 6e-7
+    for n in ("S", "A", "KL"):
+        assert np.allclose(rs[n], e[n], rtol=0, atol=tol), (n, rs[n])
+    assert np.array_equal(rs["p_hat"], np.array(e["p_hat"]))
+    for b in range(3):
+        assert np.allclose(oracle.goodputs(rs["p_hat"][b], L), e["goodputs"][b], rtol=0, atol=tol)
+    rh = oracle.schedule(rs["p_hat"], L)
+    assert list(rh["gamma"]) == e["gamma"]
+    for b in range(3):
+        for i, u in enumerate(e["u_w0"][b]):
+            assert abs(oracle.uniforms(0, 0, b, i)[0] - u) < tol
+    rv = oracle.verify(D, T, x["tok"], rh["gamma"], 1.0, 1.0, st["seed"], st["offset"], st["seq_base"])
+    want_ratio = np.array([[np.nan if v is None else v for v in row] for row in e["accept_ratio"]])
+    assert np.allclose(rv["accept_ratio"], want_ratio, rtol=0, atol=tol, equal_nan=True)
+    assert list(rv["n_accept"]) == e["n_accept"] and list(rv["out_tok"]) == e["out_tok"]
+    assert np.allclose(rv["resid_mass"], e["resid_mass"], rtol=0, atol=tol)
+    for b in range(3):
+        assert abs(oracle.uniforms(0, 0, b, int(rv["n_accept"][b]))[1] - e["u_s"][b]) < tol
+
+
+def test_verify_forced_n_and_crossing_neighbours():
+    """The tie-reporting outputs of oracle.verify: n_force = the oracle's own N reproduces the run;
+    the crossing neighbours are the positive-residual entries around the token (S L82-90, R11)."""
+    rng = np.random.default_rng(23)
+    B, k, V = 6, 4, 50
+    D = rng.normal(0, 1, (B, k, V))
+    T = rng.normal(0, 1.5, (B, k + 1, V))
+    T[:, :k] += D
+    tok = rng.integers(0, V, (B, k))
+    gam = np.full(B, k)
+    r0 = oracle.verify(D, T, tok, gam, seed=3, offset=9)
+    r1 = oracle.verify(D, T, tok, gam, seed=3, offset=9, n_force=r0["n_accept"])
+    for n in ("n_accept", "out_tok", "resid_mass"):
+        assert np.array_equal(r0[n], r1[n])
+    for b in range(B):
+        N, t = int(r0["n_accept"][b]), int(r0["out_tok"][b])
+        pt, _ = oracle.softmax(T[b, N])
+        r = np.maximum(0.0, pt - oracle.softmax(D[b, N])[0]) if N < k else pt
+        pos = np.nonzero(r > 0)[0]
+        j = int(np.searchsorted(pos, t))
+        assert pos[j] == t
+        assert r0["tok_prev"][b] == (pos[j - 1] if j > 0 else -1)
+        assert r0["tok_next"][b] == (pos[j + 1] if j + 1 < pos.size else -1)
+        # margins: distances of u_s Z to the cumulative sums at the token and just before it
+        _, us = oracle.uniforms(3, 9, b, N)
+        cum = np.cumsum(r)
+        assert abs(r0["sample_margin_hi"][b] - abs(cum[t] - us * cum[-1])) < 1e-12
+        # forcing N = 0 samples the residual of row 0 (gamma = k > 0)
+        rf = oracle.verify(D[b:b + 1], T[b:b + 1], tok[b:b + 1], gam[b:b + 1], seed=3, offset=9, seq_base=b,
+                           n_force=[0])
+        assert rf["n_accept"][0] == 0
+        pt0, _ = oracle.softmax(T[b, 0])
+        r_0 = np.maximum(0.0, pt0 - oracle.softmax(D[b, 0])[0])
+        assert abs(rf["resid_mass"][0] - r_0.sum()) < 1e-12
+        assert np.isfinite(r0["accept_margins"][b, : max(1, min(N + 1, k))]).all()
 
 
 def test_hand_derived_convention_vector():
