@@ -5,20 +5,26 @@ Metric (BASELINE.json): scored (b, i) positions / s at B=80, k=8, V=152064 (bf16
 GB/s against the measured B200 peak.  One step = one pass of the whole hot path over one
 batch (B sequences x k draft positions) of synthetic logits already resident in HBM.
 
-    python bench.py [--gpus N --steps K --warmup W]              # our CUDA path
-    python bench.py --impl reference ...                          # the fp64 oracle on host cores
-    torchrun --nproc-per-node N bench.py --gpus N ...             # batch-sharded, weak scaling
+    python bench.py [--gpus N --steps K --warmup W]   # our CUDA path; N > 1 self-launches N ranks
+    python bench.py --impl reference ...               # the fp64 oracle on host cores
+    torchrun --nproc-per-node N bench.py --gpus N ...  # what the driver runs for N > 1
 
-Multi-GPU: every rank scores its own B sequences (global ids rank*B + b enter Philox via
-seq_base); no data-path collective exists.  Time = max over ranks of the
-CUDA-event time of exactly K steps bracketed by barrier + synchronize.
+Multi-GPU (BASELINE config 3, "B=80 ... batch-sharded across 1/2/4/8 GPUs"; P L266, L305):
+STRONG scaling of the global batch of 80 sequences -- rank r owns sequences
+[floor(80 r / N), floor(80 (r+1) / N)) with seq_base = its first id, so every output is
+bit-identical to the single-GPU run (checked on the hardware: `split_check`).  No data-path
+collective exists; NCCL carries only the barrier, the max-over-ranks timing and the
+post-run gather.  Weak scaling (80 sequences per rank) is reported as the labelled extra `weak`.
+Time = max over ranks of the CUDA-event time of exactly K steps bracketed by barrier + sync.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -33,7 +39,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "scored (b,i) positions/sec at B=80,k=8,V=152064; HBM GB/s vs B200 peak"
 CONFIGS = {
-    # name: (B per GPU, k, V, dtype, BASELINE config label)
+    # name: (global B, k, V, dtype, BASELINE config label)
     "headline": (80, 8, 152064, "bf16", "config 3: B=80,k=8,V=152064 bf16, batch-sharded"),
     "c1": (4, 4, 32000, "f32", "config 1: B=4,k=4,V=32000 fp32"),
     "c2": (32, 8, 32000, "bf16", "config 2: B=32,k=8,V=32000 bf16"),
@@ -42,10 +48,62 @@ CONFIGS = {
     "vocab": (80, 8, 152064, "bf16", "config 4: B=80,k=8,V=152064 bf16, vocab-sharded over the ranks "
                                      "(NCCL all-gather of the stage partials, all-reduce MAX of the token)"),
 }
+SWEEP_B = (4, 8, 16, 32, 48, 64, 80)
+SWEEP_K = (2, 4, 8)
 
 
+# --------------------------------------------------------------------------- rank plumbing
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def rank_plan(B_global: int, world: int, rank: int, scaling: str = "strong") -> tuple[int, int]:
+    """This rank's global sequences [b0, b1): strong = a contiguous balanced split of the global
+    batch (the default multi-GPU line), weak = B_global sequences per rank.  seq_base = b0."""
+    from paper_2509_24328_b200.shard import shard_range, weak_range
+    if scaling == "strong":
+        return shard_range(B_global, world, rank)
+    if scaling == "weak":
+        return weak_range(B_global, rank)
+    raise ValueError(scaling)
+
+
+def init_dist(backend: str, device=None):
+    """Process group from the torchrun environment (nothing to do at world size 1)."""
+    import torch.distributed as dist
+    rank, world, _ = dist_env()
+    if world > 1 and not dist.is_initialized():
+        kw = {"device_id": device} if backend == "nccl" else {}
+        dist.init_process_group(backend, **kw)
+    return rank, world
+
+
+def max_over_ranks(v: float, device=None) -> float:
+    """The slowest rank's time (every multi-GPU number is a max over ranks)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return v
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def gather_outputs(outs: dict, B_global: int) -> dict | None:
+    """Rank blocks of per-sequence outputs gathered to rank 0 in global sequence order."""
+    import torch.distributed as dist
+
+    from paper_2509_24328_b200.shard import gather_rows
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return {n: v.clone() for n, v in outs.items()}
+    got = {n: gather_rows(v.contiguous(), B_global) for n, v in sorted(outs.items())}
+    return got if dist.get_rank() == 0 else None
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
 def measured_peaks():
@@ -143,7 +201,7 @@ def run_reference(args, rank, world):
     value = args.steps * k / dt_s
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "positions/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt_s / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (synth.make_inputs, seeded)",
             "config": {"workload": label, "B": B, "k": k, "V": V, "input_dtype": dt,
                        "reference_step": "oracle score+schedule+verify on 1 sequence (k positions)"},
@@ -205,23 +263,15 @@ class _SelfComm:
         pass
 
 
-def run_vocab(args, rank, world, local_rank):
-    """BASELINE config 4: one global batch, vocabulary split over the N ranks (strong scaling)."""
+def vocab_step_ms(sv, x, world, rank, dev, steps, warmup, comm):
+    """Mean ms per vocab-sharded step of this rank (columns [r V/N, (r+1) V/N)), two rotating
+    resident input sets; returns (ms, pipe, host tensors)."""
     import torch
-    import torch.distributed as dist
 
-    import paper_2509_24328_b200 as sv
     import synth
-    from paper_2509_24328_b200.shard import TorchComm, VocabShardedPipeline
-
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    B, k, V, dt, label = CONFIGS[args.config]
-    elem = 2
+    from paper_2509_24328_b200.shard import VocabShardedPipeline
+    B, k, V = x["B"], x["k"], x["V"]
     VL = V // world
-    x = synth.make_inputs(B, k, V, dt, seed=0x5EED)
     cols = slice(rank * VL, (rank + 1) * VL)
 
     def host(a):
@@ -233,42 +283,59 @@ def run_vocab(args, rank, world, local_rank):
     prof = sv.Profile.from_dict(synth.load_profile(), device=dev)
     L = torch.tensor(synth.latency_table(k + 2), dtype=torch.float64, device=dev)
     pipe = VocabShardedPipeline(B, k, V, world, rank, torch.bfloat16, prof, L, device=dev)
-    comm = TorchComm() if world > 1 else _SelfComm()
     stream = torch.cuda.current_stream()
 
     def step(j):
         D, C, T, tok = sets[j & 1]
         return pipe.run(comm, D, C, T, tok, seed=0xC0FFEE, offset=j)
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    def max_ms(ms):
-        if world > 1:
-            tt = torch.tensor([ms], device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ms = float(tt.item())
-        return ms
-
-    for j in range(args.warmup):
+    for j in range(warmup):
         step(j)
-    barrier()
+    _barrier(dev)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for j in range(steps):
+        step(warmup + j)
+    t1.record(stream)
+    _barrier(dev)
+    return max_over_ranks(t0.elapsed_time(t1), dev) / steps, pipe, (hD, hC, hT, htok), sets
+
+
+def _barrier(dev=None):
+    import torch
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def run_vocab(args, local_rank):
+    """BASELINE config 4: one global batch, vocabulary split over the N ranks (strong scaling)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2509_24328_b200 as sv
+    import synth
+    from paper_2509_24328_b200.shard import TorchComm
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    rank, world = init_dist("nccl", dev)
+    B, k, V, dt, label = CONFIGS[args.config]
+    elem = 2
+    VL = V // world
+    x = synth.make_inputs(B, k, V, dt, seed=0x5EED)
+    comm = TorchComm() if world > 1 else _SelfComm()
     with ClockSampler(local_rank) as clk:
-        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0.record(stream)
-        for j in range(args.steps):
-            step(args.warmup + j)
-        t1.record(stream)
-        barrier()
-    ms_step = max_ms(t0.elapsed_time(t1)) / args.steps
+        ms_step, pipe, (hD, hC, hT, htok), sets = vocab_step_ms(sv, x, world, rank, dev, args.steps, args.warmup,
+                                                                comm)
     gam = pipe.sched_out["gamma"].cpu().numpy()
     n_acc = pipe.ver_out["n_accept"].cpu().numpy()
     R = int((n_acc < gam).sum())
     rank_bytes = (2 * B * k + int((gam + 1).sum()) + R) * VL * elem  # this rank's algorithmic bytes
     peak, peak_src = measured_peaks()
     rank_gbs = rank_bytes / (ms_step * 1e-3) / 1e9
+    stream = torch.cuda.current_stream()
 
     # e2e: this rank's column slices from pinned host memory every step, tokens back
     hout = torch.empty((2, B), dtype=torch.int32).pin_memory()
@@ -286,14 +353,14 @@ def run_vocab(args, rank, world, local_rank):
     e2e_steps = min(args.steps, 20)
     for j in range(2):
         e2e_step(j)
-    barrier()
+    _barrier(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for j in range(e2e_steps):
         e2e_step(j)
     e1.record(stream)
-    barrier()
-    e2e_ms = max_ms(e0.elapsed_time(e1)) / e2e_steps
+    _barrier(dev)
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), dev) / e2e_steps
     if rank == 0:
         line = {
             "metric": METRIC, "value": B * k / (ms_step * 1e-3), "unit": "positions/s", "n_gpus": world,
@@ -324,7 +391,95 @@ def run_vocab(args, rank, world, local_rank):
 
 
 # --------------------------------------------------------------------------- our arm
-def run_ours(args, rank, world, local_rank):
+def step_bytes(B, k, V, elem, gam, n_acc):
+    """(2 B k + sum_b (gamma_b + 1) + R) V s with R = #{b : N_b < gamma_b}."""
+    R = int((n_acc < gam).sum())
+    return (2 * B * k + int((gam + 1).sum()) + R) * V * elem
+
+
+def graph_point(sv, torch, dev, D, C, T, tok, B, k, V, tdtype, elem, prof, steps, warmup, flush, peak):
+    """One (B, k, V) point through the graph path with an L2 flush (a 256 MB write, outside the
+    events) before every timed replay: per-replay CUDA events, summed.  Inputs are copied once
+    into the GraphPipeline's own buffers."""
+    import synth
+    L = torch.tensor(synth.latency_table(k + 2), dtype=torch.float64, device=dev)
+    gp = sv.GraphPipeline(B, k, V, tdtype, prof, L, device=dev, seed=0xC0FFEE, offset0=0)
+    gp.D.copy_(D)
+    gp.C.copy_(C)
+    gp.T.copy_(T)
+    gp.tok.copy_(tok)
+    gp.capture()
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        gp.replay()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for j in range(steps):
+        flush.add_(1)
+        ev[j][0].record(stream)
+        gp.replay()
+        ev[j][1].record(stream)
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in ev) / steps
+    gam = gp.pipe.sched_out["gamma"].cpu().numpy()
+    n_acc = gp.pipe.ver_out["n_accept"].cpu().numpy()
+    by = step_bytes(B, k, V, elem, gam, n_acc)
+    gbs = by / (ms * 1e-3) / 1e9
+    del gp
+    return {"ms_per_step": ms, "value": B * k / (ms * 1e-3), "hbm_gbs": gbs, "frac": gbs / peak,
+            "bytes": by, "mean_gamma": float(gam.mean())}
+
+
+def config_extras(sv, torch, dev, prof, peak, steps, warmup):
+    """BASELINE configs 1, 2, the config-5 grid (V = 128256, B x k, acceptance swept) and config 4
+    at N = 1, each through the graph path (per-replay events, L2 flushed before every replay)."""
+    import synth
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MB > L2
+    out = {}
+
+    def dev_inputs(x):
+        conv = (lambda a: torch.from_numpy(np.ascontiguousarray(a)).view(torch.bfloat16).to(dev)) \
+            if x["dtype"] == "bf16" else (lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev))
+        return conv(x["D"]), conv(x["C"]), conv(x["T"]), torch.from_numpy(x["tok"]).to(dev)
+
+    for name in ("c1", "c2"):
+        B, k, V, dt, label = CONFIGS[name]
+        x = synth.make_inputs(B, k, V, dt, seed=0x5EED)
+        D, C, T, tok = dev_inputs(x)
+        tdt, elem = (torch.bfloat16, 2) if dt == "bf16" else (torch.float32, 4)
+        r = graph_point(sv, torch, dev, D, C, T, tok, B, k, V, tdt, elem, prof, steps, warmup, flush, peak)
+        r["workload"] = label
+        out[name] = r
+        del D, C, T, tok
+    # config 5: one draw at the largest point (alignment swept: per-sequence acceptance ~0.1..0.9),
+    # every (B, k) point a leading slice of it
+    Bm, km, V = max(SWEEP_B), max(SWEEP_K), 128256
+    x = synth.make_inputs(Bm, km, V, "bf16", seed=0x5EED + 5 * 97, alignment="sweep")
+    D, C, T, tok = dev_inputs(x)
+    grid = {}
+    for k in SWEEP_K:
+        for B in SWEEP_B:
+            r = graph_point(sv, torch, dev, D[:B, :k].contiguous(), C[:B, :k].contiguous(),
+                            T[:B, :k + 1].contiguous(), tok[:B, :k].contiguous(), B, k, V, torch.bfloat16, 2, prof,
+                            steps, warmup, flush, peak)
+            grid[f"B{B}_k{k}"] = {n: r[n] for n in ("ms_per_step", "value", "hbm_gbs", "frac", "mean_gamma")}
+    del D, C, T, tok
+    out["c5_grid"] = {"workload": "config 5: V=128256 bf16, B in " + str(list(SWEEP_B)) + ", k in "
+                      + str(list(SWEEP_K)) + ", acceptance swept ~0.1..0.9", "points": grid}
+    # config 4 at N = 1 (the vocab-sharded staging on one rank: P1 / P2 / finish without K1's interleave)
+    B, k, V, dt, label = CONFIGS["vocab"]
+    xv = synth.make_inputs(B, k, V, dt, seed=0x5EED)
+    ms, pipe, _, _ = vocab_step_ms(sv, xv, 1, 0, dev, steps, warmup, _SelfComm())
+    gam = pipe.sched_out["gamma"].cpu().numpy()
+    by = step_bytes(B, k, V, 2, gam, pipe.ver_out["n_accept"].cpu().numpy())
+    out["vocab_n1"] = {"workload": label + " -- at N = 1", "ms_per_step": ms, "value": B * k / (ms * 1e-3),
+                       "hbm_gbs": by / (ms * 1e-3) / 1e9, "frac": by / (ms * 1e-3) / 1e9 / peak,
+                       "timing": "2 rotating resident input sets (608 MB each > L2), eager launches"}
+    out["method"] = ("graph path (GraphPipeline), per-replay CUDA events summed, 256 MB L2 flush before every "
+                     "replay (outside the events)")
+    return out
+
+
+def run_ours(args, local_rank):
     import torch
     import torch.distributed as dist
 
@@ -333,12 +488,13 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    B, k, V, dt, label = CONFIGS[args.config]
+    rank, world = init_dist("nccl", dev)
+    B_glob, k, V, dt, label = CONFIGS[args.config]
+    b0, b1 = rank_plan(B_glob, world, rank, "strong")
+    B = b1 - b0
     tdtype = torch.bfloat16 if dt == "bf16" else torch.float32
     elem = 2 if dt == "bf16" else 4
-    x = synth.make_inputs(B, k, V, dt, seed=0x5EED, seq_ids=np.arange(rank * B, (rank + 1) * B))
+    x = synth.make_inputs(B, k, V, dt, seed=0x5EED, seq_ids=np.arange(b0, b1))
 
     def host(a):
         t = torch.from_numpy(np.ascontiguousarray(a))
@@ -346,26 +502,21 @@ def run_ours(args, rank, world, local_rank):
 
     hD, hC, hT, htok = host(x["D"]).pin_memory(), host(x["C"]).pin_memory(), host(x["T"]).pin_memory(), \
         torch.from_numpy(x["tok"]).pin_memory()
-    # two resident input sets at different addresses, alternated every step: each step's
-    # bytes (608 MB at the headline) exceed the 126 MB L2 and are never L2-warm from the
-    # previous step
-    sets = []
-    for _ in range(2):
-        sets.append((hD.to(dev), hC.to(dev), hT.to(dev), htok.to(dev)))
+    set_mb = (hD.numel() + hC.numel() + hT.numel()) * elem / 1e6
+    # resident input sets at different addresses, rotated every step: together they exceed the
+    # 126 MB L2, so a step never finds its inputs L2-warm from its previous use
+    n_sets = max(2, int(np.ceil(2 * 126.0 / max(set_mb, 1e-3))))
+    sets = [(hD.to(dev), hC.to(dev), hT.to(dev), htok.to(dev)) for _ in range(n_sets)]
     prof = sv.Profile.from_dict(synth.load_profile(), device=dev)
     L = torch.tensor(synth.latency_table(k + 2), dtype=torch.float64, device=dev)
     pipe = sv.Pipeline(B, k, V, tdtype, prof, L, device=dev)
-    seq_base = rank * B
+    seq_base = b0
     stream = torch.cuda.current_stream()
+    peak, peak_src = measured_peaks()
 
     def step(j, force=None):
-        D, C, T, tok = sets[j & 1]
+        D, C, T, tok = sets[j % n_sets]
         return pipe.run(D, C, T, tok, seed=0xC0FFEE, offset=j, seq_base=seq_base, force_gamma=force)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
 
     def timed(force, steps, warmup, k1_events=False):
         if force is not None:
@@ -375,11 +526,11 @@ def run_ours(args, rank, world, local_rank):
             step(j, force)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)] \
             if k1_events else None
-        barrier()
+        _barrier(dev)
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         for j in range(steps):
-            D, C, T, tok = sets[j & 1]
+            D, C, T, tok = sets[j % n_sets]
             if ev:
                 ev[j][0].record(stream)
                 sc = sv.sv_score(D, C, tok, pipe.tau_d, pipe.tau_c, prof, workspace=pipe.workspace,
@@ -395,145 +546,109 @@ def run_ours(args, rank, world, local_rank):
             else:
                 step(warmup + j, force)
         t1.record(stream)
-        barrier()
-        ms = t0.elapsed_time(t1)
+        _barrier(dev)
         k1_ms = sum(a.elapsed_time(b) for a, b in ev) / steps if ev else None
-        if world > 1:
-            tt = torch.tensor([ms], device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ms = float(tt.item())
-        return ms, k1_ms
+        return max_over_ranks(t0.elapsed_time(t1), dev), k1_ms
 
-    # ---------------- headline: SV as scheduled
+    # ---------------- eager: SV as scheduled, call by call (carries the K1 events of `roofline`)
     with ClockSampler(local_rank) as clk:
         ms, k1_ms = timed(None, args.steps, args.warmup, k1_events=True)
     gam = pipe.sched_out["gamma"].cpu().numpy()
     n_acc = pipe.ver_out["n_accept"].cpu().numpy()
-    R = int((n_acc < gam).sum())
-    step_bytes = (2 * B * k + int((gam + 1).sum()) + R) * V * elem
-    k1_bytes = 2 * B * k * V * elem
     ms_step = ms / args.steps
-    value = world * B * k / (ms_step * 1e-3)
-    peak, peak_src = measured_peaks()
+    k1_bytes = 2 * B * k * V * elem
     k1_gbs = k1_bytes / (k1_ms * 1e-3) / 1e9
-    step_gbs = step_bytes / (ms_step * 1e-3) / 1e9
+    eager_bytes = step_bytes(B, k, V, elem, gam, n_acc)
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "sv_score_traffic.json")
-    if os.path.exists(tfile) and args.config == "headline":
+    if os.path.exists(tfile) and args.config == "headline" and world == 1:
         with open(tfile) as f:
             traffic = json.load(f).get("traffic_bytes_per_launch")
 
     # ---------------- variant: gamma forced to k (full SD verify, fixed bytes)
-    ms_full, _ = timed(k, max(10, args.steps // 2), args.warmup)
-    ms_full_step = ms_full / max(10, args.steps // 2)
-    n_acc_f = pipe.ver_out["n_accept"].cpu().numpy()
-    full_bytes = (2 * B * k + B * (k + 1) + int((n_acc_f < k).sum())) * V * elem
+    n_full = max(10, args.steps // 2)
+    ms_full, _ = timed(k, n_full, args.warmup)
+    ms_full_step = ms_full / n_full
+    full_bytes = step_bytes(B, k, V, elem, np.full(B, k), pipe.ver_out["n_accept"].cpu().numpy())
 
     # ---------------- the headline number: the whole step captured in CUDA graphs (NEXT-3), one
-    # graph per resident input set, replays alternating between them (each replay reads 608 MB
-    # > L2 that the previous replay did not touch) -- how a serving loop runs the step
-    gps = []
-    for si in range(2):
-        gp = sv.GraphPipeline(B, k, V, tdtype, prof, L, device=dev, seed=0xC0FFEE, offset0=si, seq_base=seq_base)
-        gp.D.copy_(sets[si][0])
-        gp.C.copy_(sets[si][1])
-        gp.T.copy_(sets[si][2])
-        gp.tok.copy_(sets[si][3])
-        gps.append(gp.capture())
-    for j in range(args.warmup):
-        gps[j & 1].replay()
-    barrier()
-    with ClockSampler(local_rank) as gclk:
-        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        g0.record(stream)
-        for j in range(args.steps):
-            gps[j & 1].replay()
-        g1.record(stream)
-        barrier()
-    g_ms = g0.elapsed_time(g1)
+    # graph per resident input set, replays rotating between them -- how a serving loop runs it
+    def graph_run(sets_, Bn, sb, steps, warmup):
+        gps = []
+        for si, (D, C, T, tok) in enumerate(sets_):
+            gp = sv.GraphPipeline(Bn, k, V, tdtype, prof, L, device=dev, seed=0xC0FFEE, offset0=si, seq_base=sb)
+            gp.D.copy_(D)
+            gp.C.copy_(C)
+            gp.T.copy_(T)
+            gp.tok.copy_(tok)
+            gps.append(gp.capture())
+        for j in range(warmup):
+            gps[j % len(gps)].replay()
+        _barrier(dev)
+        with ClockSampler(local_rank) as gclk:
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            for j in range(steps):
+                gps[j % len(gps)].replay()
+            g1.record(stream)
+            _barrier(dev)
+        g_ms = max_over_ranks(g0.elapsed_time(g1), dev) / steps
+        last = gps[(steps - 1) % len(gps)]
+        g = last.pipe.sched_out["gamma"].cpu().numpy()
+        na = last.pipe.ver_out["n_accept"].cpu().numpy()
+        return g_ms, gclk.summary(), gps, g, na
+
+    g_ms_step, gclocks, gps, g_gam, g_nacc = graph_run(sets, B, seq_base, args.steps, args.warmup)
+    g_bytes = step_bytes(B, k, V, elem, g_gam, g_nacc)
+    rank_gbs = g_bytes / (g_ms_step * 1e-3) / 1e9
+
+    # ---------------- multi-GPU: the split contract on the hardware.  Every rank replays its graph
+    # once more at a fixed Philox offset; the gathered outputs must equal one rank running the
+    # whole global batch at that offset, bit for bit (seq_base enters the Philox counter, R12)
+    split_check = None
     if world > 1:
-        tt = torch.tensor([g_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        g_ms = float(tt.item())
-    g_ms_step = g_ms / args.steps
+        CHECK_OFF = 1 << 20
+        gps[0].offset.fill_(CHECK_OFF)
+        mine = {n: v.clone() for n, v in gps[0].replay().items()}
+        _barrier(dev)
+        gathered = gather_outputs(mine, B_glob)
+        if rank == 0:
+            xg = synth.make_inputs(B_glob, k, V, dt, seed=0x5EED)
+            gp = sv.GraphPipeline(B_glob, k, V, tdtype, prof, L, device=dev, seed=0xC0FFEE, offset0=CHECK_OFF,
+                                  seq_base=0)
+            gp.D.copy_(host(xg["D"]).to(dev))
+            gp.C.copy_(host(xg["C"]).to(dev))
+            gp.T.copy_(host(xg["T"]).to(dev))
+            gp.tok.copy_(torch.from_numpy(xg["tok"]).to(dev))
+            gp.capture()
+            ref = {n: v.clone() for n, v in gp.replay().items()}
+            torch.cuda.synchronize()
+            eq = {n: bool(torch.equal(torch.nan_to_num(gathered[n].cpu(), nan=7.0),
+                                      torch.nan_to_num(ref[n].cpu(), nan=7.0))) for n in gathered}
+            split_check = {"bitwise_equal": all(eq.values()), "fields": eq,
+                           "what": f"gathered {world}-rank outputs vs one rank over all {B_glob} sequences "
+                                   f"(graph replay at Philox offset {CHECK_OFF})"}
+            del gp
+        _barrier(dev)
     del gps
 
-    # ---------------- NEXT-2: the step under the paper's Qwen sampling filters (Table 5: top_k 20,
-    # top_p 0.8, tau 0.7) on the same inputs
-    fws = sv.new_filter_workspace(B, k, dev)
-    fgam = torch.empty(B, dtype=torch.int32, device=dev)
+    # ---------------- weak scaling extra (N > 1): 80 sequences per rank
+    weak = None
+    if world > 1:
+        w0, w1 = rank_plan(B_glob, world, rank, "weak")
+        xw = synth.make_inputs(w1 - w0, k, V, dt, seed=0x5EED, seq_ids=np.arange(w0, w1))
+        wsets = [(host(xw["D"]).to(dev), host(xw["C"]).to(dev), host(xw["T"]).to(dev),
+                  torch.from_numpy(xw["tok"]).to(dev)) for _ in range(2)]
+        w_ms, _, wgps, _, _ = graph_run(wsets, w1 - w0, w0, args.steps, args.warmup)
+        del wgps
+        weak = {"value": world * (w1 - w0) * k / (w_ms * 1e-3), "unit": "positions/s", "ms_per_step": w_ms,
+                "B_per_gpu": w1 - w0, "scaling": "weak", "note": "80 sequences per rank (global ids rank*80+b)"}
+        del wsets
 
-    def fstep(j):
-        D, C, T, tok = sets[j & 1]
-        fs = sv.sv_score_filtered(D, C, tok, 20, 0.8, 0.7, 0.7, prof, fworkspace=fws, stream=stream)
-        g = sv.sv_schedule(fs["p_hat"], L, out={"gamma": fgam}, stream=stream)["gamma"]
-        return sv.sd_verify_filtered(T, tok, g, fws, 20, 0.8, 0.7, 0xC0FFEE, j, seq_base, stream=stream)
-
-    for j in range(args.warmup):
-        fstep(j)
-    barrier()
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f_steps = max(10, args.steps // 4)
-    f0.record(stream)
-    for j in range(f_steps):
-        fstep(args.warmup + j)
-    f1.record(stream)
-    barrier()
-    f_ms_step = f0.elapsed_time(f1) / f_steps
-
-    # the Llama setting (Table 5: nucleus only, top_p 0.9, tau 0.6; any nucleus size -- lists up to
-    # 32 tokens, threshold form beyond)
-    def nstep(j):
-        D, C, T, tok = sets[j & 1]
-        fs = sv.sv_score_filtered(D, C, tok, 0, 0.9, 0.6, 0.6, prof, fworkspace=fws, stream=stream)
-        g = sv.sv_schedule(fs["p_hat"], L, out={"gamma": fgam}, stream=stream)["gamma"]
-        return sv.sd_verify_filtered(T, tok, g, fws, 0, 0.9, 0.6, 0xC0FFEE, j, seq_base, stream=stream, D=D)
-
-    for j in range(args.warmup):
-        nstep(j)
-    barrier()
-    f0.record(stream)
-    for j in range(f_steps):
-        nstep(args.warmup + j)
-    f1.record(stream)
-    barrier()
-    n_ms_step = f0.elapsed_time(f1) / f_steps
-
-    # ---------------- NEXT-1: the paper's batch greedy schedule (one CTA: gains, bitonic sort,
-    # greedy walk) on this step's p_hat, latency L[n] over the batch's total target positions
-    Lg = torch.tensor(synth.latency_table(B * (k + 1) + 1, base=4.0, knee=2 * B, slope=4.0 / B),
-                      dtype=torch.float64, device=dev)
-    gout = {"gamma": torch.empty(B, dtype=torch.int32, device=dev), "exp_accept": torch.empty(B, device=dev),
-            "goodput": torch.empty(B, device=dev), "status": torch.empty(B, dtype=torch.int32, device=dev)}
-    for _ in range(args.warmup):
-        sv.sv_schedule(pipe.score_out["p_hat"], Lg, sv.SV_SCHED_BATCH_GREEDY, 1, out=gout, stream=stream)
-    barrier()
-    q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    q0.record(stream)
-    for _ in range(50):
-        sv.sv_schedule(pipe.score_out["p_hat"], Lg, sv.SV_SCHED_BATCH_GREEDY, 1, out=gout, stream=stream)
-    q1.record(stream)
-    barrier()
-    greedy_us = q0.elapsed_time(q1) / 50 * 1e3
-    greedy_mean_gamma = float(gout["gamma"].float().mean().item())
-
-    # ---------------- NEXT-4: GPU profile builder on a 65,536-record profiling run (P L176,
-    # S L331's run size): records = this step's (S, A, accept_ratio) with gamma = k, tiled
-    ver_full = pipe.ver_out
-    recs = [t.reshape(-1) for t in (pipe.score_out["S"], pipe.score_out["A"], ver_full["accept_ratio"])]
-    n_rec = 65536
-    rep = (n_rec + recs[0].numel() - 1) // recs[0].numel()
-    S_r, A_r, X_r = (torch.nan_to_num(t, nan=0.0).repeat(rep)[:n_rec].contiguous() for t in recs)
-    sv.sv_profile_build(S_r, A_r, X_r)
-    barrier()
-    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    p0.record(stream)
-    n_pb = 5
-    for _ in range(n_pb):
-        sv.sv_profile_build(S_r, A_r, X_r)
-    p1.record(stream)
-    barrier()
-    prof_ms = p0.elapsed_time(p1) / n_pb
+    # ---------------- single-GPU extras (N = 1 only)
+    extras = {}
+    if world == 1 and not args.no_extras:
+        extras = n1_extras(args, sv, torch, dev, sets, pipe, prof, L, B, k, V, seq_base, stream, peak)
 
     # ---------------- e2e: host buffers, H2D + pipeline + D2H every step.  As in the paper's
     # serving loop (P L266, NEXT-3) the target side only ships the gamma_b + 1 verified rows of
@@ -576,39 +691,36 @@ def run_ours(args, rank, world, local_rank):
 
     for j in range(2):
         e2e_step(j)
-    barrier()
+    _barrier(dev)
     h2d_acc[0] = 0
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for j in range(e2e_steps):
         e2e_step(j)
     e1.record(stream)
-    barrier()
-    e2e_ms = e0.elapsed_time(e1)
-    if world > 1:
-        tt = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
+    _barrier(dev)
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), dev)
     h2d = h2d_acc[0] // e2e_steps
     d2h = hout.numel() * 4 + gam_h.numel() * 4
 
     cpu = cpu_baseline_sample(args.config) if (rank == 0 and world == 1 and not args.no_cpu_baseline) else None
     if rank == 0:
+        B_total = B_glob
         line = {
-            "metric": METRIC, "value": world * B * k / (g_ms_step * 1e-3), "unit": "positions/s", "n_gpus": world,
+            "metric": METRIC, "value": B_total * k / (g_ms_step * 1e-3), "unit": "positions/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": g_ms_step, "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16" if dt == "bf16" else "f32",
             "data": "synthetic (synth.make_inputs: LLM-like head+tail logits, seeded; no model weights)",
-            "config": {"workload": label, "B_per_gpu": B, "k": k, "V": V, "schedule": "per_row (SV)",
-                       "parallelism": f"batch-sharded x{world}, no collective",
-                       "l2": "inputs larger than L2: 2 rotating resident input sets "
-                             f"({(hD.numel() + hC.numel() + hT.numel()) * elem / 1e6:.0f} MB each)",
-                       "mean_gamma": float(gam.mean()), "rejected_seqs_last_step": R},
-            "hbm_gbs": step_bytes / (g_ms_step * 1e-3) / 1e9, "hbm_frac": step_bytes / (g_ms_step * 1e-3) / 1e9 / peak,
-            "eager": {"value": value, "ms_per_step": ms_step, "hbm_gbs": step_gbs,
-                      "clocks": clk.summary(),
-                      "note": "same step launched call by call from Python (alternating input sets); "
+            "config": {"workload": label, "B": B_total, "B_per_gpu": B, "k": k, "V": V, "schedule": "per_row (SV)",
+                       "parallelism": f"batch-sharded x{world} (strong scaling of the global batch), no collective",
+                       "l2": f"inputs larger than L2: {n_sets} rotating resident input sets ({set_mb:.0f} MB each "
+                             "per rank)",
+                       "mean_gamma": float(g_gam.mean()), "rejected_seqs_last_step": int((g_nacc < g_gam).sum())},
+            "hbm_gbs": rank_gbs * world, "hbm_frac": rank_gbs / peak,
+            "eager": {"value": B_total * k / (ms_step * 1e-3), "ms_per_step": ms_step,
+                      "hbm_gbs": eager_bytes / (ms_step * 1e-3) / 1e9 * world, "clocks": clk.summary(),
+                      "note": "same step launched call by call from Python (rotating input sets); "
                               "the roofline / K1 events below are measured in this loop"},
             "roofline": {"bound": "hbm", "kernel": "sv_score (K1)", "achieved": k1_gbs, "peak": peak,
                          "unit": "GB/s", "frac": k1_gbs / peak, "traffic": traffic,
@@ -623,35 +735,27 @@ def run_ours(args, rank, world, local_rank):
                                   "peak_per_s": 15.9 * 148 * (clk.summary()["sm_mhz"] or 1965) * 1e6,
                                   "frac": 1.5 * B * k * V * 2 / (k1_ms * 1e-3)
                                           / (15.9 * 148 * (clk.summary()["sm_mhz"] or 1965) * 1e6)}},
-            "sd_full_verify": {"value": world * B * k / (ms_full_step * 1e-3), "unit": "positions/s",
+            "step_roofline": {"bound": "hbm", "kernel": "whole graph step (K1 + K3 + K4..K5b)",
+                              "achieved": rank_gbs, "peak": peak, "unit": "GB/s", "frac": rank_gbs / peak,
+                              "algorithmic_bytes_per_step": g_bytes,
+                              "bytes_formula": "(2 B k + sum_b (gamma_b + 1) + R) V s, SURVEY §8(d)"},
+            "sd_full_verify": {"value": B_total * k / (ms_full_step * 1e-3), "unit": "positions/s",
                                "ms_per_step": ms_full_step,
-                               "hbm_gbs": full_bytes / (ms_full_step * 1e-3) / 1e9,
+                               "hbm_gbs": full_bytes / (ms_full_step * 1e-3) / 1e9 * world,
                                "hbm_frac": full_bytes / (ms_full_step * 1e-3) / 1e9 / peak},
             "cuda_graph": {"note": "value / ms_per_step: the whole step (sv_score, sv_schedule, sd_verify_ragged, "
-                                   "offset += 1) captured once per resident input set and replayed alternately "
+                                   "offset += 1) captured once per resident input set and replayed in rotation "
                                    "(GraphPipeline)"},
-            "filtered": {"value": world * B * k / (f_ms_step * 1e-3), "unit": "positions/s", "ms_per_step": f_ms_step,
-                         "filters": "top_k 20, top_p 0.8, tau 0.7 on draft / companion / target (P L731-743)",
-                         "note": "NEXT-2: radix-select top-k per row + list arithmetic; output allocations per "
-                                 "call included"},
-            "filtered_nucleus": {"value": world * B * k / (n_ms_step * 1e-3), "unit": "positions/s",
-                                 "ms_per_step": n_ms_step,
-                                 "filters": "top_k 0, top_p 0.9, tau 0.6 (the Llama setting, P L739-740)",
-                                 "note": "NEXT-2 nucleus-only: lists up to 32 tokens, threshold form (mass-"
-                                         "weighted radix select, full-row passes) beyond"},
-            "batch_greedy": {"us_per_call": greedy_us, "mean_gamma": greedy_mean_gamma,
-                             "latency": f"L[n] = 4 + (4/B) max(0, n - 2B) over the batch's target positions",
-                             "note": "NEXT-1 sv_schedule mode BATCH_GREEDY on the step's p_hat (B*k candidates)"},
-            "profile_build": {"records": n_rec, "ms": prof_ms, "bins": "20 x 15, X in 10 bins",
-                              "note": "NEXT-4 offline builder (sv_profile_build), incl. its host sync for the "
-                                      "kept-bin counts"},
-            "e2e": {"value": world * B * k / (e2e_ms / e2e_steps * 1e-3), "unit": "positions/s",
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+            "split_check": split_check,
+            "weak": weak,
+            **extras,
+            "e2e": {"value": B_total * k / (e2e_ms / e2e_steps * 1e-3), "unit": "positions/s",
+                    "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world, "steps": e2e_steps,
                     "path": "pinned host -> D, C, tokens -> sv_score, sv_schedule -> gamma to host -> only the "
                             "gamma_b + 1 verified target rows -> sd_verify_ragged -> n_accept, tokens to host "
                             "(C ABI)"},
             "gpu_launches": KERNELS_PER_STEP * args.steps,  # per timed step: 6 libsv kernels (+ 1 torch add)
-            "clocks": gclk.summary(),
+            "clocks": gclocks,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
@@ -659,23 +763,114 @@ def run_ours(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
+def n1_extras(args, sv, torch, dev, sets, pipe, prof, L, B, k, V, seq_base, stream, peak):
+    """NEXT rows and the other BASELINE configs, measured by the driver's own run at N = 1."""
+    import synth
+    out = {}
+    if args.config == "headline":
+        out["configs"] = config_extras(sv, torch, dev, prof, peak, max(20, min(args.steps, 60)), args.warmup)
+    n_sets = len(sets)
+
+    # NEXT-2: the step under the paper's Qwen sampling filters (Table 5: top_k 20, top_p 0.8, tau 0.7)
+    fws = sv.new_filter_workspace(B, k, dev)
+    fgam = torch.empty(B, dtype=torch.int32, device=dev)
+
+    def fstep(j):
+        D, C, T, tok = sets[j % n_sets]
+        fs = sv.sv_score_filtered(D, C, tok, 20, 0.8, 0.7, 0.7, prof, fworkspace=fws, stream=stream)
+        g = sv.sv_schedule(fs["p_hat"], L, out={"gamma": fgam}, stream=stream)["gamma"]
+        return sv.sd_verify_filtered(T, tok, g, fws, 20, 0.8, 0.7, 0xC0FFEE, j, seq_base, stream=stream)
+
+    def nstep(j):  # the Llama setting (Table 5: nucleus only, top_p 0.9, tau 0.6; any nucleus size)
+        D, C, T, tok = sets[j % n_sets]
+        fs = sv.sv_score_filtered(D, C, tok, 0, 0.9, 0.6, 0.6, prof, fworkspace=fws, stream=stream)
+        g = sv.sv_schedule(fs["p_hat"], L, out={"gamma": fgam}, stream=stream)["gamma"]
+        return sv.sd_verify_filtered(T, tok, g, fws, 0, 0.9, 0.6, 0xC0FFEE, j, seq_base, stream=stream, D=D)
+
+    f_steps = max(10, args.steps // 4)
+    for name, fn, filt, note in (
+            ("filtered", fstep, "top_k 20, top_p 0.8, tau 0.7 on draft / companion / target (P L731-743)",
+             "NEXT-2: radix-select top-k per row + list arithmetic; output allocations per call included"),
+            ("filtered_nucleus", nstep, "top_k 0, top_p 0.9, tau 0.6 (the Llama setting, P L739-740)",
+             "NEXT-2 nucleus-only: lists up to 32 tokens, threshold form beyond")):
+        for j in range(args.warmup):
+            fn(j)
+        _barrier(dev)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for j in range(f_steps):
+            fn(args.warmup + j)
+        f1.record(stream)
+        _barrier(dev)
+        ms = f0.elapsed_time(f1) / f_steps
+        out[name] = {"value": B * k / (ms * 1e-3), "unit": "positions/s", "ms_per_step": ms, "filters": filt,
+                     "note": note}
+
+    # NEXT-1: the paper's batch greedy schedule on this step's p_hat, latency over the batch's positions
+    Lg = torch.tensor(synth.latency_table(B * (k + 1) + 1, base=4.0, knee=2 * B, slope=4.0 / B),
+                      dtype=torch.float64, device=dev)
+    gout = {"gamma": torch.empty(B, dtype=torch.int32, device=dev), "exp_accept": torch.empty(B, device=dev),
+            "goodput": torch.empty(B, device=dev), "status": torch.empty(B, dtype=torch.int32, device=dev)}
+    for _ in range(args.warmup):
+        sv.sv_schedule(pipe.score_out["p_hat"], Lg, sv.SV_SCHED_BATCH_GREEDY, 1, out=gout, stream=stream)
+    _barrier(dev)
+    q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    q0.record(stream)
+    for _ in range(50):
+        sv.sv_schedule(pipe.score_out["p_hat"], Lg, sv.SV_SCHED_BATCH_GREEDY, 1, out=gout, stream=stream)
+    q1.record(stream)
+    _barrier(dev)
+    out["batch_greedy"] = {"us_per_call": q0.elapsed_time(q1) / 50 * 1e3,
+                           "mean_gamma": float(gout["gamma"].float().mean().item()),
+                           "latency": "L[n] = 4 + (4/B) max(0, n - 2B) over the batch's target positions",
+                           "note": "NEXT-1 sv_schedule mode BATCH_GREEDY on the step's p_hat (B*k candidates)"}
+
+    # NEXT-4: GPU profile builder on a 65,536-record profiling run (P L176, S L331's run size)
+    recs = [t.reshape(-1) for t in (pipe.score_out["S"], pipe.score_out["A"], pipe.ver_out["accept_ratio"])]
+    n_rec = 65536
+    rep = (n_rec + recs[0].numel() - 1) // recs[0].numel()
+    S_r, A_r, X_r = (torch.nan_to_num(t, nan=0.0).repeat(rep)[:n_rec].contiguous() for t in recs)
+    sv.sv_profile_build(S_r, A_r, X_r)
+    _barrier(dev)
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for _ in range(5):
+        sv.sv_profile_build(S_r, A_r, X_r)
+    p1.record(stream)
+    _barrier(dev)
+    out["profile_build"] = {"records": n_rec, "ms": p0.elapsed_time(p1) / 5, "bins": "20 x 15, X in 10 bins",
+                            "note": "NEXT-4 offline builder (sv_profile_build), incl. its host sync for the "
+                                    "kept-bin counts"}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="headline", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the N = 1 extra configs / NEXT-row timings")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch this script under torch.distributed.run (loopback rendezvous)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+               *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     rank, world, local_rank = dist_env()
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE {world}; using the launched world size",
+              file=sys.stderr)
     if args.impl == "reference":
         run_reference(args, rank, world)
     elif args.config == "vocab":
-        run_vocab(args, rank, world, local_rank)
+        run_vocab(args, local_rank)
     else:
-        run_ours(args, rank, world, local_rank)
+        run_ours(args, local_rank)
 
 
 if __name__ == "__main__":
