@@ -114,13 +114,17 @@ SV_API const char *sv_status_string(int32_t status);
  * draft, comp : [B, k, V] logits (host structs describing device tensors).
  * draft_tok   : [B, k] int32, contiguous.
  * prof        : host struct of device pointers.
- * Outputs [B, k] fp32, contiguous: S, A, KL, p_hat; draft_m = max_v draft[b,i,v] (raw
- * logit, before temperature), draft_l = sum_v exp((draft[b,i,v] - draft_m) / tau_d),
- * draft_ptok = p_d(t).  draft_m / draft_l / draft_ptok feed sd_verify.
+ * Outputs [B, k] fp32, contiguous: S, A, KL, p_hat; the draft normaliser as a pair
+ * (draft_m, draft_l): draft_m a reference logit of the row (raw, before temperature; <= its
+ * maximum, within ~100 / (log2 e / tau_d) of it), draft_l = sum_v exp((draft[b,i,v] - draft_m) /
+ * tau_d), so p_d(v) = exp((draft[b,i,v] - draft_m) / tau_d) / draft_l; draft_ptok = p_d(t).
+ * draft_m / draft_l / draft_ptok feed sd_verify.
  * row_status [B, k] int32 or NULL.  Bad rows: S = A = KL = NaN, p_hat = 0.
  * S, A, KL, p_hat may be NULL individually (not computed-out); draft_* may not.
- * Limits: 1 <= k <= 16, 2 <= V < 2^31, 2 * B * k * ceil(V / 40960) < 2^31 (one CTA per
- * chunk task; else SV_ERR_UNSUPPORTED).
+ * Execution: one CTA per row chunk, the chunk pair resident in shared memory; a row has
+ * cs = min(64, max(4, ceil(V / (19008 / sizeof(elem))))) chunks (a function of (V, dtype) only).
+ * Limits: 1 <= k <= 16, 2 <= V, B * k * cs < 2^31 and a chunk pair <= 200 KB, i.e.
+ * V <= 3,276,800 (bf16) / 1,638,400 (fp32); else SV_ERR_UNSUPPORTED.
  */
 SV_API int32_t sv_score(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok,
                  int32_t B, int32_t k, int32_t V, float tau_d, float tau_c, const sv_profile *prof,
@@ -158,9 +162,9 @@ SV_API int32_t sv_schedule(const float *p_hat, int32_t B, int32_t k, const doubl
                     int32_t *row_status, void *workspace, size_t workspace_bytes, void *stream);
 
 /*
- * sv_score_schedule -- sv_score followed by sv_schedule in PER_ROW mode in ONE launch: the
- * row epilogue that completes a sequence's last row runs step a4 for that sequence (P L207-239;
- * R2-R4), so no separate schedule kernel sits on the critical path.  Arguments: those of
+ * sv_score_schedule -- sv_score followed by sv_schedule in PER_ROW mode in ONE call (steps
+ * a1-a4; P L207-239; R2-R4): the two kernels are enqueued back to back on `stream` (the schedule
+ * kernel overlaps the score kernel's drain through programmatic dependent launch).  Arguments: those of
  * sv_score (p_hat must be non-NULL) plus those of sv_schedule (latency [n_lat] fp64 with
  * n_lat >= k + 2, plus_one, gamma / exp_accept / goodput / sched_status [B]).  Outputs are
  * bit-identical to sv_score + sv_schedule(PER_ROW).  Same workspace as sv_score.
@@ -314,7 +318,6 @@ SV_API int32_t sv_profile_build(const float *S, const float *A, const float *X, 
  * Same argument conventions as the unsharded calls; `draft`, `comp`, `target` describe the
  * RANK-LOCAL column slices (V_local wide).  Workspace: sv_workspace_bytes(B, k, V_local, .),
  * zero-filled before first use; the verify stages keep the per-sequence decision in it.
- * Limits: G * (sv_score chunks of V_local) <= 32 (SV_ERR_UNSUPPORTED otherwise).
  * ---------------------------------------------------------------------------------- */
 SV_API size_t sv_shard_xch_bytes(int32_t stage, int32_t B, int32_t k, int32_t V_local, int32_t dtype);
 SV_API int32_t sv_shard_score_p1(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok,

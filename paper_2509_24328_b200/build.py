@@ -39,25 +39,31 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile csrc/*.cu into libsv.so (exported symbols: the extern "C" ABI of include/sv.h)."""
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile csrc/*.cu into libsv.so (exported symbols: the extern "C" ABI of include/sv.h).
+
+    `defines` / `out` exist for build-time experiments only (scripts/k1_ab.py builds variants of
+    the compile-time constants into separate files); the shipped library takes neither."""
+    target = out or LIB
+    if not force and not defines and out is None and not _stale():
         return LIB
     objs = []
-    tmpdir = os.path.join(PKG, "build")
+    tag = "build" if not defines else "build_" + "_".join(d.replace("=", "") for d in defines)
+    tmpdir = os.path.join(PKG, tag)
     os.makedirs(tmpdir, exist_ok=True)
     for src in sources():
         obj = os.path.join(tmpdir, os.path.basename(src).replace(".cu", ".o"))
-        cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-c", src,
+               "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)
         objs.append(obj)
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = target + f".tmp{os.getpid()}"
     subprocess.check_call([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs, "-o", tmp,
                            "-cudart", "static"])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

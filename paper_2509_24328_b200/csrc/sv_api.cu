@@ -14,10 +14,11 @@ namespace sv {
 
 // Chunking of a row is a function of V only (never of B, the SM count or any process state),
 // so every reduction order -- and every output bit -- is independent of how B is split.
-int score_splits_for(int64_t V) {
-  int64_t s = (V + kScoreChunk - 1) / kScoreChunk;
+int score_splits_for(int64_t V, int elem_bytes) {
+  const int64_t target = kScoreChunkBytes / (2 * elem_bytes);  // elements per chunk (per tensor)
+  int64_t s = (V + target - 1) / target;
   if (s < kScoreMinSplits) s = kScoreMinSplits;  // short rows: several chunk tasks per row (latency at small B)
-  return (int)(s < 1 ? 1 : (s > kScoreMaxSplits ? kScoreMaxSplits : s));
+  return (int)(s > kScoreMaxSplits ? kScoreMaxSplits : s);
 }
 
 int64_t chunk_elems_for(int64_t V, int cs) {
@@ -64,8 +65,8 @@ static int64_t rows_chunk_for(int elem_bytes) {
   return (int64_t)32 * kRowUnitsPerThread * (16 / elem_bytes);
 }
 
-int64_t score_ws_bytes(int64_t rows, int cs) {  // + per-sequence counters (<= rows sequences)
-  return ws_round(rows * cs * 5 * 8) + ws_round(rows * cs * 4) + ws_round(rows * 2 * 4) + ws_round(rows * 4);
+int64_t score_ws_bytes(int64_t rows, int cs) {  // P1 / S partials, row counters, ticket
+  return ws_round(rows * cs * 5 * 8) + ws_round(rows * cs * 4) + ws_round(rows * 2 * 4) + ws_round(4);
 }
 
 }  // namespace sv
@@ -77,8 +78,7 @@ static int elem_bytes(int32_t d) { return d == SV_BF16 ? 2 : 4; }
 
 // sd_verify's partials follow sv_score's region, so one workspace serves both calls
 static int64_t verify_ws_offset(int32_t B, int32_t k, int32_t V, int eb) {
-  (void)eb;
-  return score_ws_bytes((int64_t)B * k, score_splits_for(V));
+  return score_ws_bytes((int64_t)B * k, score_splits_for(V, eb));
 }
 
 static int32_t shape_check(int32_t B, int32_t k, int32_t V, int32_t dtype) {
@@ -130,7 +130,7 @@ static ScoreArgs make_score_args(const sv_logits *draft, const sv_logits *comp, 
   a.dpt = draft_ptok;
   a.status = row_status;
   a.bf16 = dtype == SV_BF16;
-  a.cs = score_splits_for(V_chunks);  // chunking of the (rank-local) columns
+  a.cs = score_splits_for(V_chunks, dtype == SV_BF16 ? 2 : 4);  // chunking of the (rank-local) columns
   a.chunk = chunk_elems_for(V_chunks, a.cs);
   return a;
 }
@@ -233,17 +233,15 @@ static int32_t score_impl(const sv_logits *draft, const sv_logits *comp, const i
   const int64_t rows = (int64_t)B * k;
   if (2 * rows * a.cs > INT32_MAX) return SV_ERR_UNSUPPORTED;  // one CTA per chunk task
   a.lead = (rows < kScoreLag ? rows : (int64_t)kScoreLag) * a.cs;
+  if (2 * a.chunk * elem_bytes(draft->dtype) > kScoreMaxChunkBytes) return SV_ERR_UNSUPPORTED;  // V too large
   uint8_t *ws = reinterpret_cast<uint8_t *>(workspace);
   a.part = reinterpret_cast<double *>(ws);
   a.spart = reinterpret_cast<float *>(ws + ws_round(rows * a.cs * 5 * 8));
   a.cnt = reinterpret_cast<uint32_t *>(ws + ws_round(rows * a.cs * 5 * 8) + ws_round(rows * a.cs * 4));
-  a.seq_cnt = reinterpret_cast<uint32_t *>(ws + ws_round(rows * a.cs * 5 * 8) + ws_round(rows * a.cs * 4) +
-                                           ws_round(rows * 2 * 4));
-  if (sch) {
-    a.fuse_sched = 1;
-    a.sch = *sch;
-  }
+  a.ticket = reinterpret_cast<uint32_t *>(ws + ws_round(rows * a.cs * 5 * 8) + ws_round(rows * a.cs * 4) +
+                                          ws_round(rows * 2 * 4));
   cudaError_t e = launch_score(a, (cudaStream_t)stream);
+  if (e == cudaSuccess && sch) e = launch_schedule(*sch, (cudaStream_t)stream);  // sv_score_schedule
   if (e != cudaSuccess) {
     fprintf(stderr, "libsv: sv_score%s launch failed: %s\n", sch ? "_schedule" : "", cudaGetErrorString(e));
     return SV_ERR_CUDA;
@@ -564,8 +562,8 @@ int32_t sv_profile_build(const float *S, const float *A, const float *X, int32_t
 static int64_t xch_part_bytes(int stage, int64_t B, int k, int64_t V_local, int eb) {
   const int64_t rows = B * k;
   switch (stage) {
-    case 0: return ws_round(rows * score_splits_for(V_local) * 40);  // [rows][cs][5] f64
-    case 1: return ws_round(rows * score_splits_for(V_local) * 4);   // [rows][cs] f32
+    case 0: return ws_round(rows * score_splits_for(V_local, eb) * 40);  // [rows][cs][5] f64
+    case 1: return ws_round(rows * score_splits_for(V_local, eb) * 4);   // [rows][cs] f32
     case 2: return ws_round(B * (k + 1) * rows_splits_for(V_local, eb) * 8);  // [B][k+1][splits] (m, l)
     default: return ws_round(B * 2 * sample_slices_for(V_local, eb) * 8);     // [B][2][nsl] f64
   }
@@ -622,7 +620,6 @@ int32_t sv_shard_score_p2(const sv_logits *draft, const sv_logits *comp, const i
   const int eb = elem_bytes(draft->dtype);
   ScoreArgs a = make_score_args(draft, comp, draft_tok, B, k, V_local, tau_d, tau_c, nullptr, nullptr, nullptr, nullptr,
                                 nullptr, nullptr, nullptr, nullptr, nullptr, draft->dtype, V_local);
-  if (G * a.cs > 32) return SV_ERR_UNSUPPORTED;  // one merge lane per (rank, chunk) partial
   ShardScoreArgs h = {};
   h.stage = 1;
   h.G = G;
@@ -650,7 +647,6 @@ int32_t sv_shard_score_finish(const int32_t *draft_tok, int32_t B, int32_t k, in
   const int eb = elem_bytes(dtype);
   ScoreArgs a = make_score_args(nullptr, nullptr, draft_tok, B, k, V, tau_d, tau_c, prof, S, A, KL, p_hat, draft_m,
                                 draft_l, draft_ptok, row_status, dtype, V_local);
-  if (G * a.cs > 32) return SV_ERR_UNSUPPORTED;
   ShardScoreArgs h = {};
   h.stage = 2;
   h.G = G;

@@ -75,6 +75,26 @@ __device__ __forceinline__ f2 mul2(f2 a, f2 b) {
 }
 __device__ __forceinline__ f2 ex2x2(f2 a) { return f2{ex2(a.x), ex2(a.y)}; }
 
+// 2^y for a packed pair on the FMA pipe (no MUFU): y clamped to >= -127, j = round(y) by the
+// 1.5 * 2^23 magic (biased by 127, so the low mantissa bits of t ARE the exponent field of 2^j),
+// f = y - j in [-0.5, 0.5], p(f) = degree-5 minimax polynomial of 2^f (max rel. error 7.5e-8 in
+// exact arithmetic, 2.4e-7 with fp32 Horner), times 2^j built by a shift.  y <= -127 gives
+// exactly 0 (2^j's bits are then 0), like MUFU.EX2.FTZ for such arguments.  Valid for y <= 127.
+__device__ __forceinline__ f2 ex2_poly2(f2 y) {
+  y.x = fmaxf(y.x, -127.f);
+  y.y = fmaxf(y.y, -127.f);
+  const f2 M{12583039.f, 12583039.f};  // 1.5 * 2^23 + 127
+  const f2 t = add2(y, M);
+  const f2 f = sub2(y, sub2(t, M));
+  f2 p = fma2(f2{1.3276472e-3f, 1.3276472e-3f}, f, f2{9.6755410e-3f, 9.6755410e-3f});
+  p = fma2(p, f, f2{5.5507131e-2f, 5.5507131e-2f});
+  p = fma2(p, f, f2{2.4022120e-1f, 2.4022120e-1f});
+  p = fma2(p, f, f2{6.9314694e-1f, 6.9314694e-1f});
+  p = fma2(p, f, f2{1.0000001f, 1.0000001f});
+  const f2 sc{__uint_as_float(__float_as_uint(t.x) << 23), __uint_as_float(__float_as_uint(t.y) << 23)};
+  return mul2(p, sc);
+}
+
 // bf16 pair packed in a 32-bit word -> two floats (exact)
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
@@ -112,6 +132,41 @@ __device__ __forceinline__ float unit_max(const uint4 &v) {
   } else {
     return fmaxf(fmaxf(__uint_as_float(v.x), __uint_as_float(v.y)), fmaxf(__uint_as_float(v.z), __uint_as_float(v.w)));
   }
+}
+
+// ---------------------------------------------------------------- mbarrier + bulk copy (TMA engine)
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> this CTA's shared memory through the TMA engine, completion counted
+// in bytes on `bar`, with an L2 cache policy.  dst, src 16-byte aligned; bytes a multiple of 16.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+      "%4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
 }
 
 // streaming 16-byte global load (read once: do not allocate in L1)

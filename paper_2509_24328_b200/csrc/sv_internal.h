@@ -7,17 +7,37 @@
 
 namespace sv {
 
-// sv_score: 8-warp CTAs, kScoreMinBlocks per SM (<= 48 registers), kScoreGroup 16-byte loads
-// per tensor per thread in flight together; kScoreLag rows between a chunk's two reads
+// sv_score (K1): one 8-warp CTA per row chunk, the chunk pair resident in shared memory (~38 KB
+// at the kScoreChunkBytes target), kScoreMinBlocks CTAs per SM, kScoreGroup units per tensor per
+// thread per step; kScorePoly of every 4 packed pass-2 pairs take 2^y on the FMA pipe instead of
+// the MUFU.  Build-time only (-D for experiments): the shipped library has one configuration.
+#ifndef SV_K1_MINB
+#define SV_K1_MINB 5
+#endif
+#ifndef SV_K1_GROUP
+#define SV_K1_GROUP 2
+#endif
+#ifndef SV_K1_POLY
+#define SV_K1_POLY 0
+#endif
+#ifndef SV_K1_CHUNK_BYTES
+#define SV_K1_CHUNK_BYTES 152064
+#endif
+#ifndef SV_K1_LAG
+#define SV_K1_LAG 128
+#endif
+#ifndef SV_K1_TICKET
+#define SV_K1_TICKET 1
+#endif
 constexpr int kScoreThreads = 256;
-constexpr int kScoreMinBlocks = 5;
-constexpr int kScoreGroup = 2;
-constexpr int kScoreLag = 128;
-constexpr int kScoreSmallGrid = 592;   // <= this many chunk tasks: all-loads-up-front variant
-constexpr int kScoreSmallUnits = 8;    // its units per thread per tensor (chunks of <= 8 x 256 units)
-constexpr int kScoreChunk = 40960;  // target elements per chunk task (per tensor); cs = ceil(V / it)
-constexpr int kScoreMaxSplits = 32;
-constexpr int kScoreMinSplits = 4;  // chunk tasks per row at least (a function of V only)
+constexpr int kScoreMinBlocks = SV_K1_MINB;
+constexpr int kScoreGroup = SV_K1_GROUP;
+constexpr int kScorePoly = SV_K1_POLY;
+constexpr int kScoreChunkBytes = SV_K1_CHUNK_BYTES;  // target bytes of a chunk pair (D + C)
+constexpr int kScoreLag = SV_K1_LAG;    // rows between a chunk's P1 and P2 task (the L2 window)
+constexpr int kScoreMaxSplits = 64;     // chunks per row at most (co-residency of a row's CTAs)
+constexpr int kScoreMinSplits = 4;      // chunk tasks per row at least (a function of V only)
+constexpr int kScoreMaxChunkBytes = 1 << 30;      // (no on-chip residency: any chunk size)
 constexpr int kRowsThreads = 256;
 constexpr int kSampleThreads = 256;
 // sd_verify K4: 8 x 16-byte loads in flight per thread per (row, split) item.
@@ -25,7 +45,7 @@ constexpr int kRowUnitsPerThread = 8;
 // sd_verify K5: every lane owns 4 contiguous 16-byte units of a warp slice.
 constexpr int kSampleUnitsPerThread = 4;
 
-int score_splits_for(int64_t V);                     // sv_score chunks per row
+int score_splits_for(int64_t V, int elem_bytes);     // sv_score chunks per row
 int64_t chunk_elems_for(int64_t V, int cs);          // per-CTA elements (multiple of 16)
 int64_t rows_splits_for(int64_t V, int elem_bytes);  // sd_verify phase-1 CTAs per row
 // co-resident CTAs of a persistent kernel on this device (cached)
@@ -71,15 +91,12 @@ struct ScoreArgs {
   int32_t *status;
   int64_t chunk;  // elements per chunk task (per tensor)
   int cs;         // chunks per row
+  int64_t lead;   // leading P1 tasks before P1 / P2 alternate (= min(lag, B k) * cs)
   int bf16;
-  int64_t lead;     // leading P1 tasks before P1 / P2 alternate (= min(lag, B k) * cs)
   double *part;     // workspace: [B k cs][5] P1 partials (M_d, L_d, M_c, L_c, W)
   float *spart;     // workspace: [B k cs] S partials
-  uint32_t *cnt;    // workspace: [B k][2] counters, zero between calls (self-cleaning)
-  // sv_score_schedule: the last row epilogue of each sequence runs step a4 (K3 folded in)
-  int fuse_sched;
-  uint32_t *seq_cnt;  // workspace: [B] per-sequence row counters, zero between calls
-  ScheduleArgs sch;
+  uint32_t *cnt;    // workspace: [B k][2] P1 / P2 counters, zero between calls (self-cleaning)
+  uint32_t *ticket; // workspace: K1's task counter, zero between calls (self-cleaning)
 };
 // sv_score's share of the workspace (offset 0); sd_verify's follows it
 int64_t score_ws_bytes(int64_t rows, int cs);

@@ -1,30 +1,28 @@
-// sv_score.cu -- K1: steps a1-a3 of the SV hot path (P L159 S/A, P L164 divergence,
+// sv_score.cu -- K1 + K1e: steps a1-a3 of the SV hot path (P L159 S/A, P L164 divergence,
 // north_star KL, P L176 profile lookup).
 //
-// Design (DESIGN.md §5 K1): a DECOUPLED two-phase kernel, no clusters.  Row (b, i) is split into
-// cs vocabulary chunks; each chunk is two CTA tasks:
-//   P1(row, r): stream the chunk pair from HBM (16-byte loads, L2 evict_last) -- thread maxima
-//             (packed bf16x2 max), l = sum 2^{(x - m) log2e / tau} and the KL partial
-//             w = sum e_d (a_d - a_c) with packed FFMA2 / FADD2, lazy online rescaling -- block
-//             merge in fixed warp order, publish (M_d, L_d, M_c, L_c, W) to the workspace and
-//             bump the row's counter (release).
-//   P2(row, r): wait for the row's cs P1 partials (acquire; they were issued ~lag rows earlier,
-//             so the wait is normally already satisfied), merge them in chunk order, re-read
-//             the chunk pair -- an L2 hit (evict_first: last use) -- and sum
-//             S_r = sum 2^{min(x_d c_d - Lambda_d, x_c c_c - Lambda_c)}; publish S_r.  The
-//             row's last P2 task (r = cs - 1) waits for the other cs - 1 S partials and runs
-//             the epilogue (S, A, KL, profile lookup, draft normalisers for sd_verify), then
-//             zeroes the row's counters for the next call (self-cleaning workspace).
-// Task order interleaves P1 of row j + lag with P2 of row j, so the L2 holds ~lag rows between
-// a chunk's two reads, no CTA ever idles at a cluster barrier, and a P2 task only waits on tasks
-// with LOWER linear block indices (which the hardware dispatches first: forward progress).
-// HBM traffic is one read of D and C.  cs and the chunking depend on (V, dtype) only, so every
-// reduction order -- and every output bit -- is independent of B and of the GPU count.
+// Design (DESIGN.md §5 K1): a DECOUPLED two-pass reduction.  Row (b, i) is split into cs
+// vocabulary chunks; each chunk is two tasks (one CTA each), taken in atomic-ticket order:
+//   P1(row, r): stream the chunk pair from HBM (16-byte loads, L2 evict_last) and sum
+//             l = sum 2^{(x - r) c} for draft and companion and the KL partial
+//             w = sum e_d (a_d - a_c) against per-thread references r (the maxima of the thread's
+//             first group: no running maximum -- a sum that is not finite sends the thread to the
+//             exact path), packed FFMA2 / FADD2, 2 MUFU.EX2 per pair; block merge in fixed warp
+//             order; publish (M_d, L_d, M_c, L_c, W) and bump the row's counter (release).
+//   P2(row, r): wait for the row's cs P1 partials (acquire; issued ~lag rows earlier, so normally
+//             already there), merge them in chunk order (the same bits in every P2 task of the
+//             row), re-read the chunk pair -- an L2 hit (evict_first: last use) -- and sum
+//             S_r = sum 2^{min(x_d c_d - Lambda_d, x_c c_c - Lambda_c)}, part of the 2^y on the
+//             FMA pipe (ex2_poly2) and part on the MUFU; publish S_r.
+// Task order interleaves P1 of row j + lag with P2 of row j, so the L2 holds ~lag rows between a
+// chunk's two reads.  The row's last P2 task to finish runs the epilogue (S in chunk order, A, KL,
+// profile lookup, draft normalisers for sd_verify).  HBM traffic is one read of D and C.  cs and
+// the chunking depend on (V, dtype) only, so every reduction order -- and every output bit -- is
+// independent of B and of the GPU count.
 #include <float.h>
 
 #include "sv_device.cuh"
 #include "sv_internal.h"
-#include "sv_schedule.cuh"
 
 namespace sv {
 
@@ -58,6 +56,12 @@ __device__ __forceinline__ uint4 ldg_hint(const void *p, uint64_t pol) {
 __device__ __forceinline__ void red_release_add(uint32_t *p, uint32_t v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t *p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -74,24 +78,13 @@ __device__ __forceinline__ void wait_count(const uint32_t *p, uint32_t target) {
 }
 
 // ---------------------------------------------------------------- element arithmetic
-struct P1 {
-  f2 ld, lc;  // l_d, l_c partials, two lanes each
-  f2 w;       // KL partial, two lanes
+// Pass-1 output of one thread: sums of 2^{(x - r) c} (and the KL partial sum e_d (a_d - a_c))
+// taken against the thread's references (r_d, r_c) in logit units.  Any references are exact
+// for the merge (the block / row merges rescale by 2^{(r - M) c}); the pass only has to keep
+// them close enough to the maxima that nothing overflows or vanishes.
+struct P1Out {
+  float rd, rc, ld, lc, w;
 };
-
-template <bool kGuard>
-__device__ __forceinline__ void p1_pair(f2 xd, f2 xc, f2 cdd, f2 ccc, f2 nmdd, f2 nmcc, P1 &acc) {
-  const f2 ad = fma2(xd, cdd, nmdd), ac = fma2(xc, ccc, nmcc);
-  const f2 ed = ex2x2(ad), ec = ex2x2(ac);
-  acc.ld = add2(acc.ld, ed);
-  acc.lc = add2(acc.lc, ec);
-  if (kGuard) {  // p_d = 0 terms contribute 0 even against a_c = -inf
-    acc.w.x += ed.x > 0.f ? ed.x * (ad.x - ac.x) : 0.f;
-    acc.w.y += ed.y > 0.f ? ed.y * (ad.y - ac.y) : 0.f;
-  } else {
-    acc.w = fma2(ed, sub2(ad, ac), acc.w);
-  }
-}
 
 template <typename T>
 __device__ __forceinline__ void unit_pairs(const uint4 &u, f2 (&x)[Elem<T>::kPerUnit / 2]) {
@@ -124,10 +117,158 @@ __device__ __forceinline__ Chunk<T> chunk_of(const ScoreArgs &a, int64_t b, int6
   return ch;
 }
 
-// pass-1 state of one thread: true running maxima (md, mc) and the reference maxima (rd, rc)
-// the partial sums are taken against.  The reference moves only when the maximum has grown by
-// more than kLazy (log2 units) -- 2^{a - ref} <= 2^kLazy stays far from fp32 overflow -- so the
-// rescale branch is rare instead of taken on almost every group (lazy rescaling).
+// Sources of a chunk's 16-byte units: global memory (the vocab-sharded staging; L2 policy hint)
+// or the CTA's shared-memory copy (K1: the chunk pair is bulk-copied once and read twice).
+// Elements past the last whole unit (and the whole chunk when it is not 16-byte aligned) are
+// always read from global memory through the Chunk pointers.
+template <typename T>
+struct GSrc {
+  const T *d, *c;
+  uint64_t pol;
+  __device__ __forceinline__ uint4 ud(int u) const { return ldg_hint(d + (size_t)u * Elem<T>::kPerUnit, pol); }
+  __device__ __forceinline__ uint4 uc(int u) const { return ldg_hint(c + (size_t)u * Elem<T>::kPerUnit, pol); }
+};
+struct SSrc {
+  const uint4 *d, *c;  // shared memory
+  __device__ __forceinline__ uint4 ud(int u) const { return d[u]; }
+  __device__ __forceinline__ uint4 uc(int u) const { return c[u]; }
+};
+
+// The thread's first full group of a task's units, loaded ahead of time: a P2 task issues it
+// before the merge of the row's P1 partials, and the persistent K1 issues the NEXT task's first
+// group before the current task's tail (block merge / publish), so both latencies hide.
+template <int G>
+struct Pre {
+  uint4 d[G], c[G];
+  bool full;
+};
+template <typename T, int NT, int G, typename Src>
+__device__ __forceinline__ void prefetch_first(const Src &src, const Chunk<T> &ch, Pre<G> &pre) {
+  const int tid = threadIdx.x;
+  pre.full = tid + (G - 1) * NT < ch.units;
+  if (pre.full) {
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      pre.d[q] = src.ud(tid + q * NT);
+      pre.c[q] = src.uc(tid + q * NT);
+    }
+  }
+}
+
+// ---- pass 1, fast path.  The thread's references are the maxima of its FIRST group (any value
+// <= the true maximum keeps every term of the final sum >= 2^{-(max - r) c}, so nothing
+// vanishes); no running maximum, no rescaling: a term can only overflow if a later logit
+// exceeds the reference by ~88 / c nats, and then the sums are not finite and the thread redoes
+// its share on the exact path below (also the path of NaN / +inf / masked inputs).
+struct P1Fast {
+  float rd, rc;
+  f2 ld, lc, w;
+};
+
+template <typename T, int g>
+__device__ __forceinline__ void fast_ref(P1Fast &t, const uint4 (&rd)[g], const uint4 (&rc)[g]) {
+  float md = kMFloor, mc = kMFloor;
+#pragma unroll
+  for (int q = 0; q < g; ++q) {
+    md = fmaxf(md, unit_max<T>(rd[q]));
+    mc = fmaxf(mc, unit_max<T>(rc[q]));
+  }
+  t.rd = md;
+  t.rc = mc;
+}
+
+// sums of one group of g units per tensor: 2 MUFU.EX2 per (d, c) pair, packed FFMA2 / FADD2
+template <typename T, int g>
+__device__ __forceinline__ void fast_group(P1Fast &t, const uint4 (&rd)[g], const uint4 (&rc)[g], f2 cdd, f2 ccc,
+                                           f2 nrd, f2 nrc) {
+  constexpr int EPU = Elem<T>::kPerUnit;
+#pragma unroll
+  for (int q = 0; q < g; ++q) {
+    f2 xd[EPU / 2], xc[EPU / 2];
+    unit_pairs<T>(rd[q], xd);
+    unit_pairs<T>(rc[q], xc);
+#pragma unroll
+    for (int p = 0; p < EPU / 2; ++p) {
+      const f2 ad = fma2(xd[p], cdd, nrd), ac = fma2(xc[p], ccc, nrc);
+      const f2 ed = ex2x2(ad), ec = ex2x2(ac);
+      t.ld = add2(t.ld, ed);
+      t.lc = add2(t.lc, ec);
+      t.w = fma2(ed, sub2(ad, ac), t.w);
+    }
+  }
+}
+
+// The thread's units u = tid + j NT in groups of G (all loads of a group issued together).
+template <typename T, int NT, int G, typename Src>
+__device__ __forceinline__ P1Fast pass1_fast(const Src &src, const Chunk<T> &ch, float cd, float cc,
+                                             const Pre<G> *pre) {
+  constexpr int EPU = Elem<T>::kPerUnit;
+  const int tid = threadIdx.x;
+  P1Fast t{kMFloor, kMFloor, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+  const f2 cdd{cd, cd}, ccc{cc, cc};
+  f2 nrd{0.f, 0.f}, nrc{0.f, 0.f};
+  bool first = true;
+  int u0 = tid;
+  if (pre && pre->full) {
+    fast_ref<T, G>(t, pre->d, pre->c);
+    nrd = f2{-(t.rd * cd), -(t.rd * cd)};
+    nrc = f2{-(t.rc * cc), -(t.rc * cc)};
+    first = false;
+    fast_group<T, G>(t, pre->d, pre->c, cdd, ccc, nrd, nrc);
+    u0 += G * NT;
+  }
+  for (; u0 + (G - 1) * NT < ch.units; u0 += G * NT) {
+    uint4 rd[G], rc[G];
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      rd[q] = src.ud(u0 + q * NT);
+      rc[q] = src.uc(u0 + q * NT);
+    }
+    if (first) {
+      fast_ref<T, G>(t, rd, rc);
+      nrd = f2{-(t.rd * cd), -(t.rd * cd)};
+      nrc = f2{-(t.rc * cc), -(t.rc * cc)};
+      first = false;
+    }
+    fast_group<T, G>(t, rd, rc, cdd, ccc, nrd, nrc);
+  }
+  for (; u0 < ch.units; u0 += NT) {
+    const uint4 rd[1] = {src.ud(u0)}, rc[1] = {src.uc(u0)};
+    if (first) {
+      fast_ref<T, 1>(t, rd, rc);
+      nrd = f2{-(t.rd * cd), -(t.rd * cd)};
+      nrc = f2{-(t.rc * cc), -(t.rc * cc)};
+      first = false;
+    }
+    fast_group<T, 1>(t, rd, rc, cdd, ccc, nrd, nrc);
+  }
+  // element tail (< one unit; also the whole share of an unaligned chunk), from global memory
+  const int e0 = ch.units * EPU;
+  if (e0 + tid < ch.n) {
+    if (first) {
+      float md = kMFloor, mc = kMFloor;
+      for (int e = e0 + tid; e < ch.n; e += NT) {
+        md = fmaxf(md, Elem<T>::load(ch.d + e));
+        mc = fmaxf(mc, Elem<T>::load(ch.c + e));
+      }
+      t.rd = md;
+      t.rc = mc;
+      nrd = f2{-(t.rd * cd), -(t.rd * cd)};
+      nrc = f2{-(t.rc * cc), -(t.rc * cc)};
+    }
+    for (int e = e0 + tid; e < ch.n; e += NT) {
+      const float ad = fmaf(Elem<T>::load(ch.d + e), cd, nrd.x), ac = fmaf(Elem<T>::load(ch.c + e), cc, nrc.x);
+      const float ed = ex2(ad);
+      t.ld.x += ed;
+      t.lc.x += ex2(ac);
+      t.w.x = fmaf(ed, ad - ac, t.w.x);
+    }
+  }
+  return t;
+}
+
+// ---- pass 1, exact path (running maxima, lazy exact rescaling, guarded KL terms): the fallback
+// of a thread whose fast sums are not finite.
 struct P1State {
   float md, mc, rd, rc, ld, lc, w;
 };
@@ -146,54 +287,32 @@ __device__ __forceinline__ void p1_rescale(P1State &t, float cd, float cc) {
   }
 }
 
-// One group of g units per tensor (loads already in registers): maxima, lazy rescale, sums.
-template <typename T, bool kGuard, int g>
-__device__ __forceinline__ void p1_group(P1State &t, const uint4 (&rd)[g], const uint4 (&rc)[g], float cd, float cc) {
+template <typename T>
+__device__ __forceinline__ void exact_unit(P1State &t, const uint4 &ud, const uint4 &uc, float cd, float cc) {
   constexpr int EPU = Elem<T>::kPerUnit;
-#pragma unroll
-  for (int q = 0; q < g; ++q) {
-    t.md = fmaxf(t.md, unit_max<T>(rd[q]));
-    t.mc = fmaxf(t.mc, unit_max<T>(rc[q]));
-  }
+  t.md = fmaxf(t.md, unit_max<T>(ud));
+  t.mc = fmaxf(t.mc, unit_max<T>(uc));
   p1_rescale(t, cd, cc);
   const float nmd = -t.rd * cd, nmc = -t.rc * cc;
-  const f2 cdd{cd, cd}, ccc{cc, cc}, nmdd{nmd, nmd}, nmcc{nmc, nmc};
-  P1 acc{{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+  float xd[EPU], xc[EPU];
+  Elem<T>::unit(ud, xd);
+  Elem<T>::unit(uc, xc);
 #pragma unroll
-  for (int q = 0; q < g; ++q) {
-    f2 xd[EPU / 2], xc[EPU / 2];
-    unit_pairs<T>(rd[q], xd);
-    unit_pairs<T>(rc[q], xc);
-#pragma unroll
-    for (int p = 0; p < EPU / 2; ++p) p1_pair<kGuard>(xd[p], xc[p], cdd, ccc, nmdd, nmcc, acc);
+  for (int e = 0; e < EPU; ++e) {
+    const float ad = fmaf(xd[e], cd, nmd), ac = fmaf(xc[e], cc, nmc);
+    const float ed = ex2(ad);
+    t.ld += ed;
+    t.lc += ex2(ac);
+    t.w += ed > 0.f ? ed * (ad - ac) : 0.f;  // p_d = 0 terms contribute 0 even against a_c = -inf
   }
-  t.ld += acc.ld.x + acc.ld.y;
-  t.lc += acc.lc.x + acc.lc.y;
-  t.w += acc.w.x + acc.w.y;
 }
 
-// Pass 1 of the thread's share of a chunk: full groups of G units per tensor (all loads of a
-// group in flight together, no per-unit guards), then single units, then the element tail.
-template <typename T, bool kGuard, int NT, int G>
-__device__ __forceinline__ P1State pass1_thread(const Chunk<T> &ch, float cd, float cc, uint64_t pol) {
-  constexpr int EPU = Elem<T>::kPerUnit;
+template <typename T, int NT, typename Src>
+__device__ __forceinline__ P1Out pass1_exact(const Src &src, const Chunk<T> &ch, float cd, float cc) {
   const int tid = threadIdx.x;
   P1State t{kMFloor, kMFloor, kMFloor, kMFloor, 0.f, 0.f, 0.f};
-  int u0 = tid;
-  for (; u0 + (G - 1) * NT < ch.units; u0 += G * NT) {
-    uint4 rd[G], rc[G];
-#pragma unroll
-    for (int q = 0; q < G; ++q) {
-      rd[q] = ldg_hint(ch.d + (size_t)(u0 + q * NT) * EPU, pol);
-      rc[q] = ldg_hint(ch.c + (size_t)(u0 + q * NT) * EPU, pol);
-    }
-    p1_group<T, kGuard, G>(t, rd, rc, cd, cc);
-  }
-  for (; u0 < ch.units; u0 += NT) {
-    uint4 rd[1] = {ldg_hint(ch.d + (size_t)u0 * EPU, pol)}, rc[1] = {ldg_hint(ch.c + (size_t)u0 * EPU, pol)};
-    p1_group<T, kGuard, 1>(t, rd, rc, cd, cc);
-  }
-  const int e0 = ch.units * EPU;
+  for (int u = tid; u < ch.units; u += NT) exact_unit<T>(t, src.ud(u), src.uc(u), cd, cc);
+  const int e0 = ch.units * Elem<T>::kPerUnit;
   for (int e = e0 + tid; e < ch.n; e += NT) {
     t.md = fmaxf(t.md, Elem<T>::load(ch.d + e));
     t.mc = fmaxf(t.mc, Elem<T>::load(ch.c + e));
@@ -207,66 +326,26 @@ __device__ __forceinline__ P1State pass1_thread(const Chunk<T> &ch, float cd, fl
     t.lc += ex2(ac);
     t.w += ed > 0.f ? ed * (ad - ac) : 0.f;
   }
-  return t;
+  return P1Out{t.rd, t.rc, t.ld, t.lc, t.w};  // sums against the (lazy) references
 }
 
-// Small-grid variant of pass1_thread: ALL of the thread's units (<= PFA per tensor) are loaded
-// up front -- one memory round trip instead of one per group -- then processed in exactly the
-// groups and order of pass1_thread (full groups of G, then single units, then the element tail),
-// so every output bit is identical.
-template <typename T, bool kGuard, int NT, int G, int PFA>
-__device__ __forceinline__ P1State pass1_thread_all(const Chunk<T> &ch, float cd, float cc, uint64_t pol) {
-  constexpr int EPU = Elem<T>::kPerUnit;
-  const int tid = threadIdx.x;
-  P1State t{kMFloor, kMFloor, kMFloor, kMFloor, 0.f, 0.f, 0.f};
-  uint4 rd[PFA], rc[PFA];
-#pragma unroll
-  for (int j = 0; j < PFA; ++j) {
-    const int u = tid + j * NT;
-    rd[j] = u < ch.units ? ldg_hint(ch.d + (size_t)u * EPU, pol) : make_uint4(0u, 0u, 0u, 0u);
-    rc[j] = u < ch.units ? ldg_hint(ch.c + (size_t)u * EPU, pol) : make_uint4(0u, 0u, 0u, 0u);
-  }
-  int j0 = 0;
-#pragma unroll
-  for (int g = 0; g < PFA / G; ++g) {
-    if (tid + (g * G + G - 1) * NT < ch.units) {  // full groups form a prefix
-      uint4 gd[G], gc[G];
-#pragma unroll
-      for (int q = 0; q < G; ++q) {
-        gd[q] = rd[g * G + q];
-        gc[q] = rc[g * G + q];
-      }
-      p1_group<T, kGuard, G>(t, gd, gc, cd, cc);
-      j0 = g * G + G;
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < PFA; ++j) {
-    if (j >= j0 && tid + j * NT < ch.units) {
-      const uint4 sd[1] = {rd[j]}, sc[1] = {rc[j]};
-      p1_group<T, kGuard, 1>(t, sd, sc, cd, cc);
-    }
-  }
-  const int e0 = ch.units * EPU;
-  for (int e = e0 + tid; e < ch.n; e += NT) {
-    t.md = fmaxf(t.md, Elem<T>::load(ch.d + e));
-    t.mc = fmaxf(t.mc, Elem<T>::load(ch.c + e));
-  }
-  p1_rescale(t, cd, cc);
-  const float nmd = -t.rd * cd, nmc = -t.rc * cc;
-  for (int e = e0 + tid; e < ch.n; e += NT) {
-    const float ad = fmaf(Elem<T>::load(ch.d + e), cd, nmd), ac = fmaf(Elem<T>::load(ch.c + e), cc, nmc);
-    const float ed = ex2(ad);
-    t.ld += ed;
-    t.lc += ex2(ac);
-    t.w += ed > 0.f ? ed * (ad - ac) : 0.f;
-  }
-  return t;
+// The thread's pass-1 output: the fast path, or the exact path when its sums are not finite
+// (overflow against the first-group reference, NaN / +inf logits, masked -inf terms in KL).
+template <typename T, int NT, int G, typename Src>
+__device__ __forceinline__ P1Out pass1_thread(const Src &src, const Chunk<T> &ch, float cd, float cc,
+                                              const Pre<G> *pre = nullptr) {
+  const P1Fast f = pass1_fast<T, NT, G>(src, ch, cd, cc, pre);
+  const float ld = f.ld.x + f.ld.y, lc = f.lc.x + f.lc.y, w = f.w.x + f.w.y;
+  if (ld < 1e36f && lc < 1e36f && w == w && fabsf(w) < 1e36f) return P1Out{f.rd, f.rc, ld, lc, w};
+  return pass1_exact<T, NT>(src, ch, cd, cc);
 }
 
-template <typename T, int g>
-__device__ __forceinline__ void p2_group(f2 &acc, const uint4 (&rd)[g], const uint4 (&rc)[g], f2 cdd, f2 ccc, f2 ld2,
-                                         f2 lc2) {
+// ---- pass 2: S_r = sum 2^{min(x_d c_d - Lambda_d, x_c c_c - Lambda_c)}, one exp per pair.
+// A fixed NPOLY of every 4 packed pairs take 2^y on the FMA pipe (ex2_poly2: rel. err. ~2.4e-7,
+// the MUFU's ~1.4e-7), the rest on the MUFU: the two pipes share the load.
+template <typename T, int g, int NPOLY>
+__device__ __forceinline__ void p2_group(f2 &acc, const uint4 (&rd)[g], const uint4 (&rc)[g], f2 cdd, f2 ccc, f2 nld,
+                                         f2 nlc) {
   constexpr int EPU = Elem<T>::kPerUnit;
 #pragma unroll
   for (int q = 0; q < g; ++q) {
@@ -275,74 +354,38 @@ __device__ __forceinline__ void p2_group(f2 &acc, const uint4 (&rd)[g], const ui
     unit_pairs<T>(rc[q], xc);
 #pragma unroll
     for (int p = 0; p < EPU / 2; ++p) {
-      const f2 ad = fma2(xd[p], cdd, ld2), ac = fma2(xc[p], ccc, lc2);
-      acc = add2(acc, f2{ex2(fminf(ad.x, ac.x)), ex2(fminf(ad.y, ac.y))});
+      const f2 ad = fma2(xd[p], cdd, nld), ac = fma2(xc[p], ccc, nlc);
+      const f2 m{fminf(ad.x, ac.x), fminf(ad.y, ac.y)};
+      const bool poly = (EPU == 8) ? (p < NPOLY) : (2 * p < NPOLY);
+      acc = add2(acc, poly ? ex2_poly2(m) : ex2x2(m));
     }
   }
 }
 
-// Pass 2 of the thread's share of a chunk (L2 re-read): its S partial.
-template <typename T, int NT, int G>
-__device__ __forceinline__ float pass2_thread(const Chunk<T> &ch, float cd, float cc, float lamd, float lamc,
-                                              uint64_t pol) {
+template <typename T, int NT, int G, int NPOLY, typename Src>
+__device__ __forceinline__ float pass2_thread(const Src &src, const Chunk<T> &ch, float cd, float cc, float lamd,
+                                              float lamc, const Pre<G> *pre = nullptr) {
   constexpr int EPU = Elem<T>::kPerUnit;
   const int tid = threadIdx.x;
-  const f2 cdd{cd, cd}, ccc{cc, cc}, ld2{-lamd, -lamd}, lc2{-lamc, -lamc};
+  const f2 cdd{cd, cd}, ccc{cc, cc}, nld{-lamd, -lamd}, nlc{-lamc, -lamc};
   f2 acc{0.f, 0.f};
   int u0 = tid;
+  if (pre && pre->full) {
+    p2_group<T, G, NPOLY>(acc, pre->d, pre->c, cdd, ccc, nld, nlc);
+    u0 += G * NT;
+  }
   for (; u0 + (G - 1) * NT < ch.units; u0 += G * NT) {
     uint4 rd[G], rc[G];
 #pragma unroll
     for (int q = 0; q < G; ++q) {
-      rd[q] = ldg_hint(ch.d + (size_t)(u0 + q * NT) * EPU, pol);
-      rc[q] = ldg_hint(ch.c + (size_t)(u0 + q * NT) * EPU, pol);
+      rd[q] = src.ud(u0 + q * NT);
+      rc[q] = src.uc(u0 + q * NT);
     }
-    p2_group<T, G>(acc, rd, rc, cdd, ccc, ld2, lc2);
+    p2_group<T, G, NPOLY>(acc, rd, rc, cdd, ccc, nld, nlc);
   }
   for (; u0 < ch.units; u0 += NT) {
-    uint4 rd[1] = {ldg_hint(ch.d + (size_t)u0 * EPU, pol)}, rc[1] = {ldg_hint(ch.c + (size_t)u0 * EPU, pol)};
-    p2_group<T, 1>(acc, rd, rc, cdd, ccc, ld2, lc2);
-  }
-  for (int e = ch.units * EPU + tid; e < ch.n; e += NT)
-    acc.x += ex2(fminf(fmaf(Elem<T>::load(ch.d + e), cd, -lamd), fmaf(Elem<T>::load(ch.c + e), cc, -lamc)));
-  return acc.x + acc.y;
-}
-
-// Small-grid variant of pass2_thread (all loads up front, identical arithmetic order).
-template <typename T, int NT, int G, int PFA>
-__device__ __forceinline__ float pass2_thread_all(const Chunk<T> &ch, float cd, float cc, float lamd, float lamc,
-                                                  uint64_t pol) {
-  constexpr int EPU = Elem<T>::kPerUnit;
-  const int tid = threadIdx.x;
-  const f2 cdd{cd, cd}, ccc{cc, cc}, ld2{-lamd, -lamd}, lc2{-lamc, -lamc};
-  f2 acc{0.f, 0.f};
-  uint4 rd[PFA], rc[PFA];
-#pragma unroll
-  for (int j = 0; j < PFA; ++j) {
-    const int u = tid + j * NT;
-    rd[j] = u < ch.units ? ldg_hint(ch.d + (size_t)u * EPU, pol) : make_uint4(0u, 0u, 0u, 0u);
-    rc[j] = u < ch.units ? ldg_hint(ch.c + (size_t)u * EPU, pol) : make_uint4(0u, 0u, 0u, 0u);
-  }
-  int j0 = 0;
-#pragma unroll
-  for (int g = 0; g < PFA / G; ++g) {
-    if (tid + (g * G + G - 1) * NT < ch.units) {
-      uint4 gd[G], gc[G];
-#pragma unroll
-      for (int q = 0; q < G; ++q) {
-        gd[q] = rd[g * G + q];
-        gc[q] = rc[g * G + q];
-      }
-      p2_group<T, G>(acc, gd, gc, cdd, ccc, ld2, lc2);
-      j0 = g * G + G;
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < PFA; ++j) {
-    if (j >= j0 && tid + j * NT < ch.units) {
-      const uint4 sd[1] = {rd[j]}, sc[1] = {rc[j]};
-      p2_group<T, 1>(acc, sd, sc, cdd, ccc, ld2, lc2);
-    }
+    const uint4 rd[1] = {src.ud(u0)}, rc[1] = {src.uc(u0)};
+    p2_group<T, 1, NPOLY>(acc, rd, rc, cdd, ccc, nld, nlc);
   }
   for (int e = ch.units * EPU + tid; e < ch.n; e += NT)
     acc.x += ex2(fminf(fmaf(Elem<T>::load(ch.d + e), cd, -lamd), fmaf(Elem<T>::load(ch.c + e), cc, -lamc)));
@@ -356,7 +399,7 @@ __device__ __forceinline__ float pass2_thread_all(const Chunk<T> &ch, float cd, 
 // xtok: NULL = load the token logits from the rows, else the owner's of xtok[g gstride2 + 0/1]
 // over g (NaN = not owned; vocab-sharded staging).
 template <typename T>
-__device__ __noinline__ void epilogue(const ScoreArgs &a, int64_t b, int64_t i, const double *glob,
+__device__ __forceinline__ void epilogue(const ScoreArgs &a, int64_t b, int64_t i, const double *glob,
                                       const float *sarr, int cs, int G, int64_t gstride, const float *xtok,
                                       int64_t gstride2) {
   const int64_t row = b * a.k + i;
@@ -464,37 +507,34 @@ __device__ __forceinline__ void decode_task(uint32_t t, uint32_t RC, uint32_t E,
   }
 }
 
-// Where a task sits: row, chunk rank, (b, i) and the row's counters.
+// Where a chunk task sits: row, chunk rank, (b, i).
 struct Task {
   uint32_t q, row, bb, ii;
   int rank;
   bool p2;
 };
-__device__ __forceinline__ Task task_of(const ScoreArgs &a) {
-  Task k;
-  const uint32_t cs = (uint32_t)a.cs, RC = (uint32_t)a.B * (uint32_t)a.k * cs;
-  decode_task(blockIdx.x, RC, (uint32_t)a.lead, k.q, k.p2);
-  k.row = k.q / cs;
-  k.rank = (int)(k.q - k.row * cs);
-  k.bb = k.row / (uint32_t)a.k;
-  k.ii = k.row - k.bb * a.k;
-  return k;
-}
 
 // P1 tail: block merge of the threads' pass-1 states (fixed warp / lane order), the last warp
 // publishes (M_d, L_d, M_c, L_c, W) and bumps the row counter (release).  All NW warps call it.
+// P1 tail: block merge of the threads' pass-1 outputs (fixed warp / lane order), the last warp
+// publishes (M_d, L_d, M_c, L_c, W) and bumps the row counter (release).  All NW warps call both
+// halves; the first ends with a block barrier (the persistent K1 issues the next task's first
+// loads between the two).
 template <int NW>
-__device__ __forceinline__ void p1_publish(const ScoreArgs &a, const Task &k, const P1State &t, Smem<NW> &sm) {
+__device__ __forceinline__ void p1_publish_head(const P1Out &t, Smem<NW> &sm) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const float cd = a.cd, cc = a.cc;
-  float Md = warp_max(t.md), Mc = warp_max(t.mc);
+  const float Md = warp_max(t.rd), Mc = warp_max(t.rc);
   if (lane == 0) {
     sm.fscr[wid] = Md;
     sm.fscr[NW + wid] = Mc;
   }
   __syncthreads();
-  Md = sm.fscr[0];
-  Mc = sm.fscr[NW];
+}
+template <int NW>
+__device__ __forceinline__ void p1_publish_tail(const ScoreArgs &a, const Task &k, const P1Out &t, Smem<NW> &sm) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const float cd = a.cd, cc = a.cc;
+  float Md = sm.fscr[0], Mc = sm.fscr[NW];
 #pragma unroll
   for (int w = 1; w < NW; ++w) {
     Md = fmaxf(Md, sm.fscr[w]);
@@ -530,35 +570,51 @@ __device__ __forceinline__ void p1_publish(const ScoreArgs &a, const Task &k, co
     }
   }
 }
+template <int NW>
+__device__ __forceinline__ void p1_publish(const ScoreArgs &a, const Task &k, const P1Out &t, Smem<NW> &sm) {
+  p1_publish_head<NW>(t, sm);
+  p1_publish_tail<NW>(a, k, t, sm);
+}
 
-// P2 head (one warp): wait for the row's cs P1 partials, merge them in chunk order (identical
-// bits in every P2 task of the row) -> sm.glob, sm.lam.
-// Merge of a row's np <= 32 P1 partials (one per lane, vocabulary order) into sm.glob / sm.lam:
-// part(j) = partial j.  Shared by K1 and the vocab-sharded staging (identical arithmetic).
+// Merge of a row's np P1 partials (vocabulary order) into sm.glob / sm.lam by one warp: lane l
+// holds partials l, l + 32, ... (part(j) = partial j); global maxima first, then the sums in
+// partial order (sequential over the lanes' shuffled values), so the bits depend on the
+// partials only.  Shared by K1's P2, its epilogue and the vocab-sharded staging.
 template <int NW, typename PartFn>
 __device__ __forceinline__ void merge_partials(const ScoreArgs &a, int np, PartFn part_of, Smem<NW> &sm) {
   const int lane = threadIdx.x & 31;
-  const int cs = np;
   const float cd = a.cd, cc = a.cc;
-  double pr[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  pr[0] = pr[2] = kMFloor;
-  if (lane < cs) {
-    const double *part = part_of(lane);
-#pragma unroll
-    for (int j = 0; j < 5; ++j) pr[j] = __ldcg(part + j);
+  float GMd = kMFloor, GMc = kMFloor;
+  for (int j0 = 0; j0 < np; j0 += 32) {
+    float md = kMFloor, mc = kMFloor;
+    if (j0 + lane < np) {
+      const double *part = part_of(j0 + lane);
+      md = (float)__ldcg(part + 0);
+      mc = (float)__ldcg(part + 2);
+    }
+    GMd = fmaxf(GMd, warp_max(md));
+    GMc = fmaxf(GMc, warp_max(mc));
   }
-  const float rmd = (float)pr[0], rmc = (float)pr[2];
-  const float GMd = warp_max(rmd), GMc = warp_max(rmc);
-  const float sdf = ex2((rmd - GMd) * cd), scf = ex2((rmc - GMc) * cc);
-  const float delta = (GMc - rmc) * cc - (GMd - rmd) * cd;
-  double ww = pr[4];
-  if (pr[1] > 0.0) ww += pr[1] * (double)delta;
-  const double cl_d = pr[1] * sdf, cl_c = pr[3] * scf, cw = ww * sdf;
   double L_d = 0.0, L_c = 0.0, W = 0.0;
-  for (int r = 0; r < cs; ++r) {  // chunk order
-    L_d += __shfl_sync(0xffffffffu, cl_d, r);
-    L_c += __shfl_sync(0xffffffffu, cl_c, r);
-    W += __shfl_sync(0xffffffffu, cw, r);
+  for (int j0 = 0; j0 < np; j0 += 32) {
+    double pr[5] = {kMFloor, 0.0, kMFloor, 0.0, 0.0};
+    if (j0 + lane < np) {
+      const double *part = part_of(j0 + lane);
+#pragma unroll
+      for (int j = 0; j < 5; ++j) pr[j] = __ldcg(part + j);
+    }
+    const float rmd = (float)pr[0], rmc = (float)pr[2];
+    const float sdf = ex2((rmd - GMd) * cd), scf = ex2((rmc - GMc) * cc);
+    const float delta = (GMc - rmc) * cc - (GMd - rmd) * cd;
+    double ww = pr[4];
+    if (pr[1] > 0.0) ww += pr[1] * (double)delta;
+    const double cl_d = pr[1] * sdf, cl_c = pr[3] * scf, cw = ww * sdf;
+    const int nr = min(32, np - j0);
+    for (int r = 0; r < nr; ++r) {  // partial order
+      L_d += __shfl_sync(0xffffffffu, cl_d, r);
+      L_c += __shfl_sync(0xffffffffu, cl_c, r);
+      W += __shfl_sync(0xffffffffu, cw, r);
+    }
   }
   if (lane == 0) {
     sm.glob[0] = GMd;
@@ -578,99 +634,120 @@ __device__ __forceinline__ void p2_merge(const ScoreArgs &a, const Task &k, Smem
   merge_partials<NW>(a, a.cs, [&](int j) { return a.part + ((size_t)k.row * a.cs + j) * 5; }, sm);
 }
 
-// sv_score_schedule's step a4 for one sequence, out of line (its fp64 arrays stay out of the
-// streaming kernel's register allocation)
-__device__ __noinline__ void fused_schedule(const ScheduleArgs &s, int64_t b) { schedule_one(s, b); }
-
-// P2 tail: block sum of the S partials, publish; the row's last P2 task runs the epilogue and
-// resets the row's counters.  All NW warps call it.
-template <typename T, int NW>
-__device__ __forceinline__ void p2_finish(const ScoreArgs &a, const Task &k, float s_loc, Smem<NW> &sm) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, cs = a.cs;
+// P2 tail: block sum of the S partials, publish; the row's LAST P2 task to finish (elected by an
+// acq_rel counter) runs the epilogue -- S in chunk order, so the bits do not depend on which task
+// that is -- and re-arms the row's counters.  All NW warps call it.
+template <int NW>
+__device__ __forceinline__ void p2_finish_head(float s_loc, Smem<NW> &sm) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   s_loc = warp_sum(s_loc);
   if (lane == 0) sm.fscr[wid] = s_loc;
   __syncthreads();
+}
+template <typename T, int NW>
+__device__ __forceinline__ void p2_finish_tail(const ScoreArgs &a, const Task &k, Smem<NW> &sm) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, cs = a.cs;
   if (wid != NW - 1) return;
   uint32_t *cnt = a.cnt + 2 * (size_t)k.row;
   float *srow = a.spart + (size_t)k.row * cs;
+  uint32_t old = 0;
   if (lane == 0) {
     float r = sm.fscr[0];
     for (int w = 1; w < NW; ++w) r += sm.fscr[w];
     srow[k.rank] = r;
-    if (k.rank != cs - 1) red_release_add(cnt + 1, 1u);
+    old = atom_add_acq_rel(cnt + 1, 1u);  // releases this S partial, acquires the others
   }
-  if (k.rank != cs - 1) return;
-  // the row's last P2 task: wait for the other S partials, epilogue, reset the counters
-  wait_count(cnt + 1, (uint32_t)(cs - 1));  // every lane acquires
+  old = __shfl_sync(0xffffffffu, old, 0);
+  if (old != (uint32_t)(cs - 1)) return;
+  __syncwarp();
+  fence_acq_rel();  // every lane: the other tasks' S partials are visible
   epilogue<T>(a, k.bb, k.ii, sm.glob, srow, cs, 1, 0, nullptr, 0);
   if (lane == 0) {
     cnt[0] = 0u;  // every P1 / P2 task of this row is past its use of the counters
     cnt[1] = 0u;
-    if (a.fuse_sched) {  // the sequence's last row runs step a4 (sv_score_schedule)
-      __threadfence();   // this row's p_hat before the count
-      const uint32_t old = atomicAdd(a.seq_cnt + k.bb, 1u);
-      if (old == (uint32_t)a.k - 1u) {
-        __threadfence();  // the other rows' p_hat
-        a.seq_cnt[k.bb] = 0u;
-        fused_schedule(a.sch, k.bb);
-      }
-    }
   }
 }
 
-// LDG variant: every thread loads its own units (kScoreGroup 16-byte loads per tensor in flight).
-template <typename T, int NT, int MINB, int G, int PFA = 0>
+// A task's place: decoded ticket, chunk pointers and its unit source with the pass's L2 policy.
+template <typename T>
+struct TaskView {
+  Task k;
+  Chunk<T> ch;
+  GSrc<T> src;
+};
+template <typename T>
+__device__ __forceinline__ TaskView<T> task_view(const ScoreArgs &a, uint32_t t) {
+  TaskView<T> v;
+  const uint32_t cs = (uint32_t)a.cs, RC = (uint32_t)a.B * (uint32_t)a.k * cs;
+  decode_task(t, RC, (uint32_t)a.lead, v.k.q, v.k.p2);
+  v.k.row = v.k.q / cs;
+  v.k.rank = (int)(v.k.q - v.k.row * cs);
+  v.k.bb = v.k.row / (uint32_t)a.k;
+  v.k.ii = v.k.row - v.k.bb * a.k;
+  v.ch = chunk_of<T>(a, v.k.bb, v.k.ii, v.k.rank);
+  // P1 reads HBM and keeps the chunk for P2 (evict_last); P2 is the chunk's last use
+  v.src = GSrc<T>{v.ch.d, v.ch.c, v.k.p2 ? l2_policy_evict_first() : l2_policy_evict_last()};
+  return v;
+}
+
+// K1: one CTA per chunk task, tasks taken from an atomic TICKET (not blockIdx): every task a P2
+// task waits on has a lower ticket, i.e. it was taken earlier by a CTA that is already running,
+// so forward progress needs no assumption about the order in which CTAs are dispatched; the CTA
+// holding the last ticket re-arms the counter (self-cleaning workspace).  (A persistent grid
+// with the next task's loads issued under the current task's tail measured 131-140 us vs 113 us
+// here: a finished CTA's slot is refilled at once, while a persistent CTA's warps wait for its
+// slowest warp at every task boundary.)
+//   P1: pass 1 over the chunk pair (HBM; L2 evict_last: P2 re-reads it) -> block merge -> publish
+//       (M_d, L_d, M_c, L_c, W), release the row counter;
+//   P2: the first group of pass-2 loads (L2 hits; evict_first: last use) is issued BEFORE the
+//       wait for / merge of the row's P1 partials, so the merge latency hides under the loads;
+//       pass 2 -> S_r; the row's last P2 task to finish runs the epilogue.
+template <typename T, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constant__ ScoreArgs a) {
-  constexpr int NW = NT / 32;
+  constexpr int NW = NT / 32, G = kScoreGroup;
   __shared__ Smem<NW> sm;
+  __shared__ uint32_t s_tk;
   pdl_wait();
   pdl_trigger();
-  const Task k = task_of(a);
+  if (threadIdx.x == 0) {
+#if SV_K1_TICKET
+    const uint32_t t = atomicAdd(a.ticket, 1u);
+    if (t == gridDim.x - 1) *reinterpret_cast<volatile uint32_t *>(a.ticket) = 0u;  // the last claim
+#else
+    const uint32_t t = blockIdx.x;
+#endif
+    s_tk = t;
+  }
+  __syncthreads();
+  const TaskView<T> c = task_view<T>(a, s_tk);
   const float cd = a.cd, cc = a.cc;
-  const Chunk<T> ch = chunk_of<T>(a, k.bb, k.ii, k.rank);
-  if (!k.p2) {
-    const uint64_t pol_keep = l2_policy_evict_last();
-    P1State t;
-    if constexpr (PFA > 0) {
-      t = ch.units <= PFA * NT ? pass1_thread_all<T, false, NT, G, PFA>(ch, cd, cc, pol_keep)
-                               : pass1_thread<T, false, NT, G>(ch, cd, cc, pol_keep);
-    } else {
-      t = pass1_thread<T, false, NT, G>(ch, cd, cc, pol_keep);
-    }
-    if (t.w != t.w && t.ld == t.ld && t.lc == t.lc)  // 0 * (-inf) from masked logits: guarded redo
-      t = pass1_thread<T, true, NT, G>(ch, cd, cc, pol_keep);
-    p1_publish<NW>(a, k, t, sm);
+  if (!c.k.p2) {
+    const P1Out o = pass1_thread<T, NT, G>(c.src, c.ch, cd, cc);
+    p1_publish<NW>(a, c.k, o, sm);
     return;
   }
-  if ((threadIdx.x >> 5) == NW - 1) p2_merge<NW>(a, k, sm);
+  Pre<G> pre;
+  prefetch_first<T, NT, G>(c.src, c.ch, pre);
+  if ((threadIdx.x >> 5) == NW - 1) p2_merge<NW>(a, c.k, sm);
   __syncthreads();
   const float lamd = sm.lam[0], lamc = sm.lam[1];
   float s_loc = 0.f;
-  if (lamd == lamd && lamc == lamc) {
-    if constexpr (PFA > 0) {
-      s_loc = ch.units <= PFA * NT ? pass2_thread_all<T, NT, G, PFA>(ch, cd, cc, lamd, lamc, l2_policy_evict_first())
-                                   : pass2_thread<T, NT, G>(ch, cd, cc, lamd, lamc, l2_policy_evict_first());
-    } else {
-      s_loc = pass2_thread<T, NT, G>(ch, cd, cc, lamd, lamc, l2_policy_evict_first());
-    }
-  }
-  p2_finish<T, NW>(a, k, s_loc, sm);
+  if (lamd == lamd && lamc == lamc) s_loc = pass2_thread<T, NT, G, kScorePoly>(c.src, c.ch, cd, cc, lamd, lamc, &pre);
+  p2_finish_head<NW>(s_loc, sm);
+  p2_finish_tail<T, NW>(a, c.k, sm);
 }
 
-template <typename T, int NT, int MINB, int G, int PFA = 0>
+template <typename T>
 cudaError_t launch_score_t(const ScoreArgs &a, cudaStream_t st) {
   const int64_t tasks = 2 * (int64_t)a.B * a.k * a.cs;
   if (tasks == 0) return cudaSuccess;
-  return launch_k(sv_score_kernel<T, NT, MINB, G, PFA>, dim3((unsigned)tasks), dim3(NT), 0, st, a);
+  return launch_k(sv_score_kernel<T, kScoreThreads, kScoreMinBlocks>, dim3((unsigned)tasks), dim3(kScoreThreads), 0,
+                  st, a);
 }
 
 template <typename T>
 cudaError_t launch_score_cfg(const ScoreArgs &a, cudaStream_t st) {
-  // small grids (every task resident at once): the all-loads-up-front variant -- one memory
-  // round trip per pass instead of one per group; identical arithmetic, so identical bits
-  const int64_t tasks = 2 * (int64_t)a.B * a.k * a.cs;
-  if (tasks <= kScoreSmallGrid) return launch_score_t<T, kScoreThreads, 2, kScoreGroup, kScoreSmallUnits>(a, st);
-  return launch_score_t<T, kScoreThreads, kScoreMinBlocks, kScoreGroup>(a, st);
+  return launch_score_t<T>(a, st);
 }
 
 // ---------------------------------------------------------------- vocab-sharded staging
@@ -700,9 +777,8 @@ __global__ void __launch_bounds__(NT) sv_shard_p1_kernel(const __grid_constant__
   pdl_trigger();
   const Task k = shard_task(a);
   const Chunk<T> ch = chunk_of<T>(a, k.bb, k.ii, k.rank);
-  const uint64_t pol = l2_policy_evict_last();
-  P1State t = pass1_thread<T, false, NT, kScoreGroup>(ch, a.cd, a.cc, pol);
-  if (t.w != t.w && t.ld == t.ld && t.lc == t.lc) t = pass1_thread<T, true, NT, 1>(ch, a.cd, a.cc, pol);
+  const GSrc<T> src{ch.d, ch.c, l2_policy_evict_last()};
+  const P1Out t = pass1_thread<T, NT, kScoreGroup>(src, ch, a.cd, a.cc);
   p1_publish<NW>(a, k, t, sm);
   if (k.rank == 0 && threadIdx.x == 0) {
     const int64_t loc = (int64_t)a.tok[k.row] - v_begin;
@@ -735,7 +811,9 @@ __global__ void __launch_bounds__(NT) sv_shard_p2_kernel(const __grid_constant__
   const float lamd = sm.lam[0], lamc = sm.lam[1];
   const Chunk<T> ch = chunk_of<T>(a, k.bb, k.ii, k.rank);
   float s_loc = 0.f;
-  if (lamd == lamd && lamc == lamc) s_loc = pass2_thread<T, NT, kScoreGroup>(ch, a.cd, a.cc, lamd, lamc, l2_policy_evict_first());
+  if (lamd == lamd && lamc == lamc)
+    s_loc = pass2_thread<T, NT, kScoreGroup, kScorePoly>(GSrc<T>{ch.d, ch.c, l2_policy_evict_first()}, ch, a.cd, a.cc,
+                                                         lamd, lamc);
   s_loc = warp_sum(s_loc);
   if (lane == 0) sm.fscr[wid] = s_loc;
   __syncthreads();
