@@ -29,6 +29,9 @@ namespace sv {
 #ifndef SV_K1_TICKET
 #define SV_K1_TICKET 1
 #endif
+#ifndef SV_K1_SAMECTA
+#define SV_K1_SAMECTA 0
+#endif
 constexpr int kScoreThreads = 256;
 constexpr int kScoreMinBlocks = SV_K1_MINB;
 constexpr int kScoreGroup = SV_K1_GROUP;

@@ -33,7 +33,9 @@ struct Smem {
   double glob[5];  // merged (M_d, L_d, M_c, L_c, W)
   float lam[2];    // Lambda_d, Lambda_c
   float fscr[2 * NW];
-  double dscr[3 * NW];
+  double dscr[5 * NW];  // per-warp pass-1 partials (ref_d, l_d, ref_c, l_c, w)
+  double wglob[NW][5];  // P2: every warp merges the row's partials itself (no block barrier)
+  float wlam[NW][2];
 };
 
 __device__ __forceinline__ uint64_t l2_policy_evict_last() {
@@ -514,74 +516,14 @@ struct Task {
   bool p2;
 };
 
-// P1 tail: block merge of the threads' pass-1 states (fixed warp / lane order), the last warp
-// publishes (M_d, L_d, M_c, L_c, W) and bumps the row counter (release).  All NW warps call it.
-// P1 tail: block merge of the threads' pass-1 outputs (fixed warp / lane order), the last warp
-// publishes (M_d, L_d, M_c, L_c, W) and bumps the row counter (release).  All NW warps call both
-// halves; the first ends with a block barrier (the persistent K1 issues the next task's first
-// loads between the two).
-template <int NW>
-__device__ __forceinline__ void p1_publish_head(const P1Out &t, Smem<NW> &sm) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const float Md = warp_max(t.rd), Mc = warp_max(t.rc);
-  if (lane == 0) {
-    sm.fscr[wid] = Md;
-    sm.fscr[NW + wid] = Mc;
-  }
-  __syncthreads();
-}
-template <int NW>
-__device__ __forceinline__ void p1_publish_tail(const ScoreArgs &a, const Task &k, const P1Out &t, Smem<NW> &sm) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const float cd = a.cd, cc = a.cc;
-  float Md = sm.fscr[0], Mc = sm.fscr[NW];
-#pragma unroll
-  for (int w = 1; w < NW; ++w) {
-    Md = fmaxf(Md, sm.fscr[w]);
-    Mc = fmaxf(Mc, sm.fscr[NW + w]);
-  }
-  {
-    const float sdf = ex2((t.rd - Md) * cd), scf = ex2((t.rc - Mc) * cc);
-    const float delta = (Mc - t.rc) * cc - (Md - t.rd) * cd;
-    double ww = t.w;
-    if (t.ld > 0.f) ww += (double)t.ld * (double)delta;
-    double v[3] = {(double)t.ld * sdf, (double)t.lc * scf, ww * sdf};
-#pragma unroll
-    for (int j = 0; j < 3; ++j) v[j] = warp_sum_d(v[j]);
-    if (lane == 0)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) sm.dscr[j * NW + wid] = v[j];
-  }
-  __syncthreads();
-  if (wid == NW - 1) {  // lanes 0..2 sum the 3 quantities over warps (warp order); lane 0 publishes
-    double r = 0.0;
-    if (lane < 3)
-      for (int w = 0; w < NW; ++w) r += sm.dscr[lane * NW + w];
-    const double r0 = __shfl_sync(0xffffffffu, r, 0), r1 = __shfl_sync(0xffffffffu, r, 1),
-                 r2 = __shfl_sync(0xffffffffu, r, 2);
-    if (lane == 0) {
-      double *part = a.part + (size_t)k.q * 5;
-      part[0] = (double)Md;
-      part[1] = r0;
-      part[2] = (double)Mc;
-      part[3] = r1;
-      part[4] = r2;
-      if (a.cnt) red_release_add(a.cnt + 2 * (size_t)k.row, 1u);
-    }
-  }
-}
-template <int NW>
-__device__ __forceinline__ void p1_publish(const ScoreArgs &a, const Task &k, const P1Out &t, Smem<NW> &sm) {
-  p1_publish_head<NW>(t, sm);
-  p1_publish_tail<NW>(a, k, t, sm);
-}
-
 // Merge of a row's np P1 partials (vocabulary order) into sm.glob / sm.lam by one warp: lane l
 // holds partials l, l + 32, ... (part(j) = partial j); global maxima first, then the sums in
 // partial order (sequential over the lanes' shuffled values), so the bits depend on the
 // partials only.  Shared by K1's P2, its epilogue and the vocab-sharded staging.
-template <int NW, typename PartFn>
-__device__ __forceinline__ void merge_partials(const ScoreArgs &a, int np, PartFn part_of, Smem<NW> &sm) {
+template <typename PartFn, bool kGlobal = true>
+__device__ __forceinline__ void merge_partials_to(const ScoreArgs &a, int np, PartFn part_of, double (&glob)[5],
+                                                  float (&lam)[2]) {
+  auto ld = [](const double *p) { return kGlobal ? __ldcg(p) : *p; };  // global: through L2 (other CTAs')
   const int lane = threadIdx.x & 31;
   const float cd = a.cd, cc = a.cc;
   float GMd = kMFloor, GMc = kMFloor;
@@ -589,8 +531,8 @@ __device__ __forceinline__ void merge_partials(const ScoreArgs &a, int np, PartF
     float md = kMFloor, mc = kMFloor;
     if (j0 + lane < np) {
       const double *part = part_of(j0 + lane);
-      md = (float)__ldcg(part + 0);
-      mc = (float)__ldcg(part + 2);
+      md = (float)ld(part + 0);
+      mc = (float)ld(part + 2);
     }
     GMd = fmaxf(GMd, warp_max(md));
     GMc = fmaxf(GMc, warp_max(mc));
@@ -601,7 +543,7 @@ __device__ __forceinline__ void merge_partials(const ScoreArgs &a, int np, PartF
     if (j0 + lane < np) {
       const double *part = part_of(j0 + lane);
 #pragma unroll
-      for (int j = 0; j < 5; ++j) pr[j] = __ldcg(part + j);
+      for (int j = 0; j < 5; ++j) pr[j] = ld(part + j);
     }
     const float rmd = (float)pr[0], rmc = (float)pr[2];
     const float sdf = ex2((rmd - GMd) * cd), scf = ex2((rmc - GMc) * cc);
@@ -617,21 +559,84 @@ __device__ __forceinline__ void merge_partials(const ScoreArgs &a, int np, PartF
     }
   }
   if (lane == 0) {
-    sm.glob[0] = GMd;
-    sm.glob[1] = L_d;
-    sm.glob[2] = GMc;
-    sm.glob[3] = L_c;
-    sm.glob[4] = W;
+    glob[0] = GMd;
+    glob[1] = L_d;
+    glob[2] = GMc;
+    glob[3] = L_c;
+    glob[4] = W;
     const bool ok = L_d > 0.0 && L_c > 0.0 && L_d < 1e300 && L_c < 1e300 && GMd < FLT_MAX && GMc < FLT_MAX;
-    sm.lam[0] = ok ? (float)((double)GMd * cd + log2_acc(L_d)) : __int_as_float(0x7fc00000);
-    sm.lam[1] = ok ? (float)((double)GMc * cc + log2_acc(L_c)) : __int_as_float(0x7fc00000);
+    lam[0] = ok ? (float)((double)GMd * cd + log2_acc(L_d)) : __int_as_float(0x7fc00000);
+    lam[1] = ok ? (float)((double)GMc * cc + log2_acc(L_c)) : __int_as_float(0x7fc00000);
   }
+}
+template <int NW, typename PartFn>
+__device__ __forceinline__ void merge_partials(const ScoreArgs &a, int np, PartFn part_of, Smem<NW> &sm) {
+  merge_partials_to(a, np, part_of, sm.glob, sm.lam);
+}
+
+// P1 tail: block merge of the threads' pass-1 states (fixed warp / lane order), the last warp
+// publishes (M_d, L_d, M_c, L_c, W) and bumps the row counter (release).  All NW warps call it.
+// P1 tail: block merge of the threads' pass-1 outputs (fixed warp / lane order), the last warp
+// publishes (M_d, L_d, M_c, L_c, W) and bumps the row counter (release).  All NW warps call both
+// halves; the first ends with a block barrier (the persistent K1 issues the next task's first
+// loads between the two).
+template <int NW>
+__device__ __forceinline__ void p1_publish_head(const P1Out &t, Smem<NW> &sm, float cd, float cc) {
+  // warp partial against the warp's maxima of the references (fp64 butterfly sums), one barrier
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const float Mw = warp_max(t.rd), Mcw = warp_max(t.rc);
+  const float sdf = ex2((t.rd - Mw) * cd), scf = ex2((t.rc - Mcw) * cc);
+  const float delta = (Mcw - t.rc) * cc - (Mw - t.rd) * cd;
+  double ww = t.w;
+  if (t.ld > 0.f) ww += (double)t.ld * (double)delta;
+  const double v0 = warp_sum_d((double)t.ld * sdf), v1 = warp_sum_d((double)t.lc * scf), v2 = warp_sum_d(ww * sdf);
+  if (lane == 0) {
+    double *d = sm.dscr + 5 * wid;
+    d[0] = Mw;
+    d[1] = v0;
+    d[2] = Mcw;
+    d[3] = v1;
+    d[4] = v2;
+  }
+  __syncthreads();
+}
+template <int NW>
+__device__ __forceinline__ void p1_publish_tail(const ScoreArgs &a, const Task &k, Smem<NW> &sm) {
+  // the last warp merges the NW warp partials in warp order (the row merge's arithmetic) and
+  // publishes the chunk's (M_d, L_d, M_c, L_c, W)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (wid != NW - 1) return;
+  auto warp_part = [&](int j) { return (const double *)(sm.dscr + 5 * j); };
+  merge_partials_to<decltype(warp_part), false>(a, NW, warp_part, sm.glob, sm.lam);
+  __syncwarp();
+  if (lane == 0) {
+    double *part = a.part + (size_t)k.q * 5;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) part[j] = sm.glob[j];
+    if (a.cnt) red_release_add(a.cnt + 2 * (size_t)k.row, 1u);
+  }
+}
+template <int NW>
+__device__ __forceinline__ void p1_publish(const ScoreArgs &a, const Task &k, const P1Out &t, Smem<NW> &sm) {
+  p1_publish_head<NW>(t, sm, a.cd, a.cc);
+  p1_publish_tail<NW>(a, k, sm);
 }
 
 template <int NW>
 __device__ __forceinline__ void p2_merge(const ScoreArgs &a, const Task &k, Smem<NW> &sm) {
   wait_count(a.cnt + 2 * (size_t)k.row, (uint32_t)a.cs);  // every lane acquires
   merge_partials<NW>(a, a.cs, [&](int j) { return a.part + ((size_t)k.row * a.cs + j) * 5; }, sm);
+}
+// Every warp of a P2 task merges the row's P1 partials itself (identical bits: the same loads and
+// operations), so no warp waits at a block barrier for another warp's merge; returns Lambda.
+template <int NW>
+__device__ __forceinline__ float2 p2_merge_warp(const ScoreArgs &a, const Task &k, Smem<NW> &sm) {
+  const int wid = threadIdx.x >> 5;
+  wait_count(a.cnt + 2 * (size_t)k.row, (uint32_t)a.cs);  // every lane acquires
+  merge_partials_to(a, a.cs, [&](int j) { return a.part + ((size_t)k.row * a.cs + j) * 5; }, sm.wglob[wid],
+                    sm.wlam[wid]);
+  __syncwarp();
+  return make_float2(sm.wlam[wid][0], sm.wlam[wid][1]);
 }
 
 // P2 tail: block sum of the S partials, publish; the row's LAST P2 task to finish (elected by an
@@ -661,7 +666,7 @@ __device__ __forceinline__ void p2_finish_tail(const ScoreArgs &a, const Task &k
   if (old != (uint32_t)(cs - 1)) return;
   __syncwarp();
   fence_acq_rel();  // every lane: the other tasks' S partials are visible
-  epilogue<T>(a, k.bb, k.ii, sm.glob, srow, cs, 1, 0, nullptr, 0);
+  epilogue<T>(a, k.bb, k.ii, sm.wglob[NW - 1], srow, cs, 1, 0, nullptr, 0);
   if (lane == 0) {
     cnt[0] = 0u;  // every P1 / P2 task of this row is past its use of the counters
     cnt[1] = 0u;
@@ -719,8 +724,34 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constan
     s_tk = t;
   }
   __syncthreads();
-  const TaskView<T> c = task_view<T>(a, s_tk);
   const float cd = a.cd, cc = a.cc;
+#if SV_K1_SAMECTA
+  {  // one task = one chunk, both passes: P1 -> publish -> (P2 loads issued) wait for the row's
+     // other chunks -> merge -> P2 from the L2 lines this SM just read
+    Task k;
+    const uint32_t cs = (uint32_t)a.cs;
+    k.q = s_tk;
+    k.row = k.q / cs;
+    k.rank = (int)(k.q - k.row * cs);
+    k.bb = k.row / (uint32_t)a.k;
+    k.ii = k.row - k.bb * a.k;
+    k.p2 = true;
+    const Chunk<T> ch = chunk_of<T>(a, k.bb, k.ii, k.rank);
+    const P1Out o = pass1_thread<T, NT, G>(GSrc<T>{ch.d, ch.c, l2_policy_evict_last()}, ch, cd, cc);
+    p1_publish<NW>(a, k, o, sm);
+    const GSrc<T> src{ch.d, ch.c, l2_policy_evict_first()};
+    Pre<G> pre;
+    prefetch_first<T, NT, G>(src, ch, pre);
+    const float2 lam = p2_merge_warp<NW>(a, k, sm);
+    const float lamd = lam.x, lamc = lam.y;
+    float s_loc = 0.f;
+    if (lamd == lamd && lamc == lamc) s_loc = pass2_thread<T, NT, G, kScorePoly>(src, ch, cd, cc, lamd, lamc, &pre);
+    p2_finish_head<NW>(s_loc, sm);
+    p2_finish_tail<T, NW>(a, k, sm);
+    return;
+  }
+#endif
+  const TaskView<T> c = task_view<T>(a, s_tk);
   if (!c.k.p2) {
     const P1Out o = pass1_thread<T, NT, G>(c.src, c.ch, cd, cc);
     p1_publish<NW>(a, c.k, o, sm);
@@ -728,9 +759,8 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constan
   }
   Pre<G> pre;
   prefetch_first<T, NT, G>(c.src, c.ch, pre);
-  if ((threadIdx.x >> 5) == NW - 1) p2_merge<NW>(a, c.k, sm);
-  __syncthreads();
-  const float lamd = sm.lam[0], lamc = sm.lam[1];
+  const float2 lam = p2_merge_warp<NW>(a, c.k, sm);
+  const float lamd = lam.x, lamc = lam.y;
   float s_loc = 0.f;
   if (lamd == lamd && lamc == lamc) s_loc = pass2_thread<T, NT, G, kScorePoly>(c.src, c.ch, cd, cc, lamd, lamc, &pre);
   p2_finish_head<NW>(s_loc, sm);
@@ -739,7 +769,7 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constan
 
 template <typename T>
 cudaError_t launch_score_t(const ScoreArgs &a, cudaStream_t st) {
-  const int64_t tasks = 2 * (int64_t)a.B * a.k * a.cs;
+  const int64_t tasks = (SV_K1_SAMECTA ? 1 : 2) * (int64_t)a.B * a.k * a.cs;
   if (tasks == 0) return cudaSuccess;
   return launch_k(sv_score_kernel<T, kScoreThreads, kScoreMinBlocks>, dim3((unsigned)tasks), dim3(kScoreThreads), 0,
                   st, a);
