@@ -43,6 +43,11 @@ __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t l2_policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -580,10 +585,10 @@ __device__ __forceinline__ void merge_partials(const ScoreArgs &a, int np, PartF
 // publishes (M_d, L_d, M_c, L_c, W) and bumps the row counter (release).  All NW warps call both
 // halves; the first ends with a block barrier (the persistent K1 issues the next task's first
 // loads between the two).
-template <int NW>
-__device__ __forceinline__ void p1_publish_head(const P1Out &t, Smem<NW> &sm, float cd, float cc) {
-  // warp partial against the warp's maxima of the references (fp64 butterfly sums), one barrier
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+// The warp's pass-1 partial (M_d, L_d, M_c, L_c, W) against the warp's maxima of the lanes'
+// references (fp64 butterfly sums); lane 0 writes it to dst.
+__device__ __forceinline__ void warp_p1_partial(const P1Out &t, float cd, float cc, double *dst) {
+  const int lane = threadIdx.x & 31;
   const float Mw = warp_max(t.rd), Mcw = warp_max(t.rc);
   const float sdf = ex2((t.rd - Mw) * cd), scf = ex2((t.rc - Mcw) * cc);
   const float delta = (Mcw - t.rc) * cc - (Mw - t.rd) * cd;
@@ -591,13 +596,17 @@ __device__ __forceinline__ void p1_publish_head(const P1Out &t, Smem<NW> &sm, fl
   if (t.ld > 0.f) ww += (double)t.ld * (double)delta;
   const double v0 = warp_sum_d((double)t.ld * sdf), v1 = warp_sum_d((double)t.lc * scf), v2 = warp_sum_d(ww * sdf);
   if (lane == 0) {
-    double *d = sm.dscr + 5 * wid;
-    d[0] = Mw;
-    d[1] = v0;
-    d[2] = Mcw;
-    d[3] = v1;
-    d[4] = v2;
+    dst[0] = Mw;
+    dst[1] = v0;
+    dst[2] = Mcw;
+    dst[3] = v1;
+    dst[4] = v2;
   }
+}
+template <int NW>
+__device__ __forceinline__ void p1_publish_head(const P1Out &t, Smem<NW> &sm, float cd, float cc) {
+  // warp partial against the warp's maxima of the references (fp64 butterfly sums), one barrier
+  warp_p1_partial(t, cd, cc, sm.dscr + 5 * (threadIdx.x >> 5));
   __syncthreads();
 }
 template <int NW>
@@ -767,8 +776,461 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constan
   p2_finish_tail<T, NW>(a, c.k, sm);
 }
 
+// ---------------------------------------------------------------- K1r: warp-specialised rings
+// Rows are split into cs chunks (as K1).  A GROUP of cs persistent CTAs (one per SM) owns rows
+// g, g + NG, g + 2 NG, ... (NG groups); member m always takes chunk m.  Each CTA runs two
+// INDEPENDENT pipelines over its chunk sequence (DESIGN §5 K1r):
+//   pass 1: warp 0 streams the chunk pair of each of the CTA's rows from HBM into a ring of
+//     shared-memory stages with 1-D bulk copies (TMA engine, L2 evict_last); kRingP1 consumer
+//     warps sum l_d, l_c and the KL partial (2 MUFU.EX2 per pair); warp 2 merges their warp
+//     partials in warp order and publishes the chunk's (M_d, L_d, M_c, L_c, W).  The row's LAST
+//     chunk to be published (acq_rel counter) merges the row once (count cs + 1).  Pass 1 waits on
+//     nothing but its own pass 2 (back-pressure, <= kRingWin rows ahead).
+//   pass 2: warp 1 waits for the row's merge (the group's cs CTAs work on the same row at the same
+//     pace, so the wait is short), hands Lambda to the slot and streams the chunk pair again -- an
+//     L2 hit (evict_first: last use); kRingP2 consumer warps sum S = sum 2^{min(a_d, a_c)}
+//     (1 exp per pair); warp 3 publishes the S partial and the row's last one runs the epilogue.
+// L2 holds about NG x (1 + kRingWin) rows between a chunk's two reads.  Lane l of consumer w owns
+// units w*32U + u*32 + l (u < U) of every stage of its pipeline; chunks and stages depend on
+// (V, dtype) only, so every output bit is independent of B, of the grid and of the GPU count.
+struct RingHdr {
+  uint32_t n;     // CTA-local task number: slot n % kRingSlots
+  int32_t sit;    // stage index within the task
+  int32_t nu;     // units per tensor in this stage; < 0: no more tasks
+  int32_t last;   // last stage of the task
+};
+template <int SU>
+struct RingStages {
+  uint4 buf[kRingStages][2][SU];
+  RingHdr hdr[kRingStages];
+  uint64_t full[kRingStages], empty[kRingStages];
+};
+struct P1Slot {
+  uint32_t row, end;
+  double wpart[kRingP1][5];
+};
+struct P2Slot {
+  uint32_t row, end;
+  float lam[2];
+  double glob[5];  // the row's merged pass-1 partials (the epilogue's input)
+  float wsum[kRingP2];
+};
+struct RingSmem {
+  RingStages<kRingSU1> r1;
+  RingStages<kRingSU2> r2;
+  P1Slot s1[kRingSlots];
+  P2Slot s2[kRingSlots];
+  double pglob[5];
+  float plam[2];
+  uint32_t p2_rows;  // rows pass 2 has started (pass 1's back-pressure)
+  uint64_t task1[kRingSlots], parts1[kRingSlots], free1[kRingSlots];
+  uint64_t task2[kRingSlots], parts2[kRingSlots], free2[kRingSlots];
+};
+
+// this CTA's group, member and the group count; row of the CTA's n-th task
+struct RingPlace {
+  uint32_t g, m, ng, rows;
+  __device__ __forceinline__ uint32_t row(uint32_t n) const { return g + n * ng; }
+};
+__device__ __forceinline__ RingPlace ring_place(const ScoreArgs &a) {
+  RingPlace p;
+  p.m = blockIdx.x % (uint32_t)a.cs;
+  p.g = blockIdx.x / (uint32_t)a.cs;
+  p.ng = gridDim.x / (uint32_t)a.cs;
+  p.rows = (uint32_t)a.B * (uint32_t)a.k;
+  return p;
+}
+
+template <typename T>
+__device__ __forceinline__ Chunk<T> ring_chunk(const ScoreArgs &a, uint32_t row, int rank) {
+  const int64_t b = row / (uint32_t)a.k, i = row - b * a.k, v0 = (int64_t)rank * a.chunk;
+  Chunk<T> ch;
+  ch.d = reinterpret_cast<const T *>(a.d) + b * a.d_sb + i * a.d_si + v0;
+  ch.c = reinterpret_cast<const T *>(a.c) + b * a.c_sb + i * a.c_si + v0;
+  ch.n = (int)max((int64_t)0, min(a.chunk, (int64_t)a.V - v0));
+  ch.units = ch.n / Elem<T>::kPerUnit;  // K1r rows: whole 16-byte units, aligned
+  return ch;
+}
+
+// Streams a chunk pair into a ring as stages of SU units per tensor (producer lane).
+template <typename T, int SU>
+__device__ __forceinline__ void ring_stream(RingStages<SU> &r, uint32_t &it, uint32_t n, const Chunk<T> &ch,
+                                            uint64_t pol) {
+  constexpr int EPU = Elem<T>::kPerUnit;
+  const int nst = max(1, (ch.units + SU - 1) / SU);  // an empty chunk is one empty stage
+  for (int sit = 0; sit < nst; ++sit, ++it) {
+    const int s = it % kRingStages;
+    mbar_wait_bounded(&r.empty[s], ((it / kRingStages) & 1) ^ 1);
+    const int nu = min(SU, ch.units - sit * SU);
+    r.hdr[s] = RingHdr{n, sit, nu, sit == nst - 1};
+    mbar_arrive_expect_tx(&r.full[s], 2u * (uint32_t)nu * 16u);
+    if (nu > 0) {
+      bulk_g2s(r.buf[s][0], ch.d + (size_t)sit * SU * EPU, (uint32_t)nu * 16u, &r.full[s], pol);
+      bulk_g2s(r.buf[s][1], ch.c + (size_t)sit * SU * EPU, (uint32_t)nu * 16u, &r.full[s], pol);
+    }
+  }
+}
+template <int SU>
+__device__ __forceinline__ void ring_end(RingStages<SU> &r, uint32_t it, uint32_t n) {
+  const int s = it % kRingStages;
+  mbar_wait_bounded(&r.empty[s], ((it / kRingStages) & 1) ^ 1);
+  r.hdr[s] = RingHdr{n, 0, -1, 0};
+  mbar_arrive(&r.full[s]);
+}
+
+template <typename T>
+__device__ void ring_producer1(const ScoreArgs &a, RingSmem &sm) {
+  if ((threadIdx.x & 31) != 0) return;
+  const RingPlace pl = ring_place(a);
+  const uint64_t pol = SV_K1R_NOPOL ? l2_policy_evict_normal() : l2_policy_evict_last();  // pass 2 re-reads it
+  uint32_t it = 0;
+  for (uint32_t n = 0;; ++n) {
+    const uint32_t row = pl.row(n);
+    const int slot = n % kRingSlots;
+    mbar_wait_bounded(&sm.free1[slot], ((n / kRingSlots) & 1) ^ 1);
+    sm.s1[slot].row = row;
+    sm.s1[slot].end = row >= pl.rows;
+    mbar_arrive(&sm.task1[slot]);
+    if (row >= pl.rows) return ring_end(sm.r1, it, n);
+    // back-pressure: at most kRingWin rows ahead of this CTA's pass 2 (which only ever waits on
+    // rows pass 1 has streamed: no cycle)
+    for (uint32_t k = 0; !SV_K1R_DBG && n > (uint32_t)kRingWin &&
+                         *reinterpret_cast<volatile uint32_t *>(&sm.p2_rows) + kRingWin < n;
+         ++k) {
+      if (k > (1u << 26)) __trap();
+      __nanosleep(64);
+    }
+    ring_stream<T>(sm.r1, it, n, ring_chunk<T>(a, row, (int)pl.m), pol);
+  }
+}
+
+template <typename T>
+__device__ void ring_producer2(const ScoreArgs &a, RingSmem &sm) {
+  if ((threadIdx.x & 31) != 0) return;
+  const RingPlace pl = ring_place(a);
+  if (SV_K1R_DBG == 2) {  // timing experiment: no pass 2 at all
+    sm.s2[0].end = 1;
+    mbar_arrive(&sm.task2[0]);
+    return ring_end(sm.r2, 0, 0);
+  }
+  const uint64_t pol = l2_policy_evict_first();  // the chunk's last use
+  uint32_t it = 0;
+  for (uint32_t n = 0;; ++n) {
+    const uint32_t row = pl.row(n);
+    const int slot = n % kRingSlots;
+    mbar_wait_bounded(&sm.free2[slot], ((n / kRingSlots) & 1) ^ 1);
+    P2Slot &sl = sm.s2[slot];
+    sl.row = row;
+    sl.end = row >= pl.rows;
+    if (row >= pl.rows) {
+      mbar_arrive(&sm.task2[slot]);
+      return ring_end(sm.r2, it, n);
+    }
+    if (SV_K1R_DBG == 0) wait_count(a.cnt + 2 * (size_t)row, (uint32_t)a.cs + 1u);  // the row's merge is published
+    const double *ri = a.rowinfo + (size_t)row * 8;
+    double v[7];
+#pragma unroll
+    for (int j = 0; j < 7; ++j) v[j] = __ldcg(ri + j);
+#pragma unroll
+    for (int j = 0; j < 5; ++j) sl.glob[j] = v[j];
+    sl.lam[0] = (float)v[5];
+    sl.lam[1] = (float)v[6];
+    mbar_arrive(&sm.task2[slot]);
+    *reinterpret_cast<volatile uint32_t *>(&sm.p2_rows) = n + 1;
+    ring_stream<T>(sm.r2, it, n, ring_chunk<T>(a, row, (int)pl.m), pol);  // full releases lam / glob
+  }
+}
+
+template <typename T>
+__device__ void ring_publish1(const ScoreArgs &a, RingSmem &sm) {
+  const int lane = threadIdx.x & 31, cs = a.cs;
+  const RingPlace pl = ring_place(a);
+  for (uint32_t n = 0;; ++n) {
+    const int slot = n % kRingSlots;
+    const uint32_t par = (n / kRingSlots) & 1;
+    mbar_wait_bounded(&sm.task1[slot], par);
+    P1Slot &sl = sm.s1[slot];
+    if (sl.end) return;
+    const uint32_t row = sl.row;
+    mbar_wait_bounded(&sm.parts1[slot], par);
+    auto warp_part = [&](int j) { return (const double *)sl.wpart[j]; };
+    merge_partials_to<decltype(warp_part), false>(a, kRingP1, warp_part, sm.pglob, sm.plam);
+    __syncwarp();
+    uint32_t *cnt = a.cnt + 2 * (size_t)row;
+    uint32_t old = 0;
+    if (lane == 0) {
+      double *part = a.part + ((size_t)row * cs + pl.m) * 5;
+#pragma unroll
+      for (int j = 0; j < 5; ++j) part[j] = sm.pglob[j];
+      old = atom_add_acq_rel(cnt, 1u);  // releases this partial, acquires the others
+    }
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if (old == (uint32_t)(cs - 1)) {  // the row's last chunk: merge the row once
+      __syncwarp();
+      fence_acq_rel();
+      merge_partials_to(a, cs, [&](int j) { return a.part + ((size_t)row * cs + j) * 5; }, sm.pglob, sm.plam);
+      __syncwarp();
+      if (lane == 0) {
+        double *ri = a.rowinfo + (size_t)row * 8;
+#pragma unroll
+        for (int j = 0; j < 5; ++j) ri[j] = sm.pglob[j];
+        ri[5] = sm.plam[0];
+        ri[6] = sm.plam[1];
+        red_release_add(cnt, 1u);  // count cs + 1: the row merge is visible
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.free1[slot]);
+  }
+}
+
+template <typename T>
+__device__ void ring_publish2(const ScoreArgs &a, RingSmem &sm) {
+  const int lane = threadIdx.x & 31, cs = a.cs;
+  const RingPlace pl = ring_place(a);
+  for (uint32_t n = 0;; ++n) {
+    const int slot = n % kRingSlots;
+    const uint32_t par = (n / kRingSlots) & 1;
+    mbar_wait_bounded(&sm.task2[slot], par);
+    P2Slot &sl = sm.s2[slot];
+    if (sl.end) return;
+    const uint32_t row = sl.row;
+    mbar_wait_bounded(&sm.parts2[slot], par);
+    uint32_t *cnt = a.cnt + 2 * (size_t)row;
+    float *srow = a.spart + (size_t)row * cs;
+    uint32_t old = 0;
+    if (lane == 0) {
+      float r = sl.wsum[0];
+      for (int w = 1; w < kRingP2; ++w) r += sl.wsum[w];
+      srow[pl.m] = r;
+      old = atom_add_acq_rel(cnt + 1, 1u);  // releases this S partial, acquires the others
+    }
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if (old == (uint32_t)(cs - 1)) {  // the row's last S partial: epilogue, re-arm the counters
+      __syncwarp();
+      fence_acq_rel();
+      const int64_t b = row / (uint32_t)a.k, i = row - b * a.k;
+      epilogue<T>(a, b, i, sl.glob, srow, cs, 1, 0, nullptr, 0);
+      if (lane == 0) {
+        cnt[0] = 0u;
+        cnt[1] = 0u;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.free2[slot]);
+  }
+}
+
+// Exact pass 1 over one consumer lane's units of a chunk (global memory; the fallback of a lane
+// whose fast sums are not finite -- its shared-memory stages are gone by then).
+template <typename T>
+__device__ __noinline__ P1Out ring_exact(const ScoreArgs &a, uint32_t row, int rank, int ubase) {
+  constexpr int EPU = Elem<T>::kPerUnit;
+  const Chunk<T> ch = ring_chunk<T>(a, row, rank);
+  P1State s{kMFloor, kMFloor, kMFloor, kMFloor, 0.f, 0.f, 0.f};
+  for (int s0 = 0; s0 < ch.units; s0 += kRingSU1)
+    for (int u = 0; u < kRingU; ++u) {
+      const int idx = s0 + ubase + u * 32;
+      if (idx < min(ch.units, s0 + kRingSU1))
+        exact_unit<T>(s, ldg_stream(ch.d + (size_t)idx * EPU), ldg_stream(ch.c + (size_t)idx * EPU), a.cd, a.cc);
+    }
+  return P1Out{s.rd, s.rc, s.ld, s.lc, s.w};
+}
+
+// Loads the lane's units of stage s (ok[u]: inside a partial stage), then releases the stage.
+template <int SU>
+__device__ __forceinline__ void ring_take(RingStages<SU> &r, int s, int ubase, int nu, uint4 (&rd)[kRingU],
+                                          uint4 (&rc)[kRingU], bool (&ok)[kRingU]) {
+  const uint4 *bd = r.buf[s][0], *bc = r.buf[s][1];
+#pragma unroll
+  for (int u = 0; u < kRingU; ++u) {
+    ok[u] = ubase + u * 32 < nu;
+    if (ok[u]) {
+      rd[u] = bd[ubase + u * 32];
+      rc[u] = bc[ubase + u * 32];
+    }
+  }
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(&r.empty[s]);  // the stage's data is in registers
+}
+
+template <typename T>
+__device__ void ring_consumer1(const ScoreArgs &a, RingSmem &sm, int cw) {
+  constexpr int U = kRingU, SU = kRingSU1;
+  const int lane = threadIdx.x & 31, ubase = cw * 32 * U + lane;
+  const float cd = a.cd, cc = a.cc;
+  const f2 cdd{cd, cd}, ccc{cc, cc};
+  P1Fast t{kMFloor, kMFloor, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+  f2 nrd{0.f, 0.f}, nrc{0.f, 0.f};
+  bool first = true;
+  for (uint32_t it = 0;; ++it) {
+    const int s = it % kRingStages;
+    mbar_wait_bounded(&sm.r1.full[s], (it / kRingStages) & 1);
+    const RingHdr h = sm.r1.hdr[s];
+    if (h.nu < 0) return;
+    if (h.sit == 0) {
+      t = P1Fast{kMFloor, kMFloor, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+      nrd = nrc = f2{0.f, 0.f};
+      first = true;
+    }
+    uint4 rd[U], rc[U];
+    bool ok[U];
+    ring_take(sm.r1, s, ubase, h.nu, rd, rc, ok);
+    if (h.nu == SU) {  // a whole stage
+      if (first) {
+        fast_ref<T, U>(t, rd, rc);
+        nrd = f2{-(t.rd * cd), -(t.rd * cd)};
+        nrc = f2{-(t.rc * cc), -(t.rc * cc)};
+        first = false;
+      }
+      fast_group<T, U>(t, rd, rc, cdd, ccc, nrd, nrc);
+    } else {  // the row's last (partial) stage
+      if (first && ok[0]) {
+        float md = kMFloor, mc = kMFloor;
+#pragma unroll
+        for (int v = 0; v < U; ++v)
+          if (ok[v]) {
+            md = fmaxf(md, unit_max<T>(rd[v]));
+            mc = fmaxf(mc, unit_max<T>(rc[v]));
+          }
+        t.rd = md;
+        t.rc = mc;
+        nrd = f2{-(t.rd * cd), -(t.rd * cd)};
+        nrc = f2{-(t.rc * cc), -(t.rc * cc)};
+        first = false;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (ok[u]) {
+          const uint4 d1[1] = {rd[u]}, c1[1] = {rc[u]};
+          fast_group<T, 1>(t, d1, c1, cdd, ccc, nrd, nrc);
+        }
+    }
+    if (h.last) {  // the chunk's last stage: the warp's partial -> slot
+      const int slot = h.n % kRingSlots;
+      P1Slot &sl = sm.s1[slot];
+      const float ld = t.ld.x + t.ld.y, lc = t.lc.x + t.lc.y, w = t.w.x + t.w.y;
+      P1Out o{t.rd, t.rc, ld, lc, w};
+      if (!(ld < 1e36f && lc < 1e36f && w == w && fabsf(w) < 1e36f))
+        o = ring_exact<T>(a, sl.row, (int)(blockIdx.x % (uint32_t)a.cs), ubase);
+      warp_p1_partial(o, cd, cc, sl.wpart[cw]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.parts1[slot]);
+    }
+  }
+}
+
+template <typename T>
+__device__ void ring_consumer2(const ScoreArgs &a, RingSmem &sm, int cw) {
+  constexpr int U = kRingU, SU = kRingSU2;
+  const int lane = threadIdx.x & 31, ubase = cw * 32 * U + lane;
+  const float cd = a.cd, cc = a.cc;
+  const f2 cdd{cd, cd}, ccc{cc, cc};
+  f2 acc{0.f, 0.f}, nld{0.f, 0.f}, nlc{0.f, 0.f};
+  bool skip = false;
+  for (uint32_t it = 0;; ++it) {
+    const int s = it % kRingStages;
+    mbar_wait_bounded(&sm.r2.full[s], (it / kRingStages) & 1);
+    const RingHdr h = sm.r2.hdr[s];
+    if (h.nu < 0) return;
+    const int slot = h.n % kRingSlots;
+    if (h.sit == 0) {  // Lambda was written before the stage was released
+      const float lamd = sm.s2[slot].lam[0], lamc = sm.s2[slot].lam[1];
+      skip = !(lamd == lamd && lamc == lamc);
+      nld = f2{-lamd, -lamd};
+      nlc = f2{-lamc, -lamc};
+      acc = f2{0.f, 0.f};
+    }
+    uint4 rd[U], rc[U];
+    bool ok[U];
+    ring_take(sm.r2, s, ubase, h.nu, rd, rc, ok);
+    if (!skip) {
+      if (h.nu == SU) {
+        p2_group<T, U, kRingPoly>(acc, rd, rc, cdd, ccc, nld, nlc);
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (ok[u]) {
+            const uint4 d1[1] = {rd[u]}, c1[1] = {rc[u]};
+            p2_group<T, 1, kRingPoly>(acc, d1, c1, cdd, ccc, nld, nlc);
+          }
+      }
+    }
+    if (h.last) {
+      const float sw = warp_sum(acc.x + acc.y);
+      if (lane == 0) sm.s2[slot].wsum[cw] = sw;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.parts2[slot]);
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRingThreads, 1) sv_score_ring_kernel(const __grid_constant__ ScoreArgs a) {
+  extern __shared__ __align__(128) uint8_t ring_raw[];
+  RingSmem &sm = *reinterpret_cast<RingSmem *>(ring_raw);
+  const int wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRingStages; ++s) {
+      mbar_init(&sm.r1.full[s], 1);
+      mbar_init(&sm.r1.empty[s], kRingP1);
+      mbar_init(&sm.r2.full[s], 1);
+      mbar_init(&sm.r2.empty[s], kRingP2);
+    }
+    for (int s = 0; s < kRingSlots; ++s) {
+      mbar_init(&sm.task1[s], 1);
+      mbar_init(&sm.parts1[s], kRingP1);
+      mbar_init(&sm.free1[s], 1);
+      mbar_init(&sm.task2[s], 1);
+      mbar_init(&sm.parts2[s], kRingP2);
+      mbar_init(&sm.free2[s], 1);
+    }
+    sm.p2_rows = 0;
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  if (wid == 0)
+    ring_producer1<T>(a, sm);
+  else if (wid == 1)
+    ring_producer2<T>(a, sm);
+  else if (wid == 2)
+    ring_publish1<T>(a, sm);
+  else if (wid == 3)
+    ring_publish2<T>(a, sm);
+  else if (wid < 4 + kRingP1)
+    ring_consumer1<T>(a, sm, wid - 4);
+  else
+    ring_consumer2<T>(a, sm, wid - 4 - kRingP1);
+}
+
+// Grid: whole groups of cs CTAs, at most one per SM (resident_grid), at most one group per row.
+// Returns 0 when not even one group fits (the caller then uses K1).
+template <typename T>
+int score_ring_grid(const ScoreArgs &a) {
+  const int smem = (int)sizeof(RingSmem);
+  if (cudaFuncSetAttribute(sv_score_ring_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  const int64_t rows = (int64_t)a.B * a.k;
+  int64_t groups = resident_grid((const void *)sv_score_ring_kernel<T>, kRingThreads, smem) / a.cs;
+  if (groups > rows) groups = rows;
+  return (int)(groups * a.cs);
+}
+template <typename T>
+cudaError_t launch_score_ring(const ScoreArgs &a, int grid, cudaStream_t st) {
+  return launch_k(sv_score_ring_kernel<T>, dim3((unsigned)grid), dim3(kRingThreads), sizeof(RingSmem), st, a);
+}
+
 template <typename T>
 cudaError_t launch_score_t(const ScoreArgs &a, cudaStream_t st) {
+  if ((int64_t)a.B * a.k == 0) return cudaSuccess;
+  if (a.ring) {
+    const int grid = score_ring_grid<T>(a);
+    if (grid > 0) return launch_score_ring<T>(a, grid, st);
+  }
   const int64_t tasks = (SV_K1_SAMECTA ? 1 : 2) * (int64_t)a.B * a.k * a.cs;
   if (tasks == 0) return cudaSuccess;
   return launch_k(sv_score_kernel<T, kScoreThreads, kScoreMinBlocks>, dim3((unsigned)tasks), dim3(kScoreThreads), 0,

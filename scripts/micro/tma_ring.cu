@@ -1,0 +1,140 @@
+// Microbenchmark: streaming two tensors (D, C: 2 x 194.6 MB bf16) through a shared-memory ring
+// filled by 1-D bulk copies (cp.async.bulk, TMA engine) -- the K1r data path -- with a single
+// producer lane per CTA and NC consumer warps.  MATH 0: consumers only take the stage (LDS +
+// arrive); MATH 1: K1's pass-1 math (2 ex2 per pair + KL term); MATH 2: + pass-2's ex2 (3 per pair).
+// Reports GB/s of the algorithmic bytes for each (stage bytes, stages, CTAs per SM).
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+__device__ __forceinline__ float ex2(float x) { float y; asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+__device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t c) { asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c)); }
+__device__ __forceinline__ void arrive(uint64_t *b) { asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory"); }
+__device__ __forceinline__ void arrive_tx(uint64_t *b, uint32_t n) { asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory"); }
+__device__ __forceinline__ void wait(uint64_t *b, uint32_t par) {
+  asm volatile("{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(su32(b)), "r"(par) : "memory");
+}
+__device__ __forceinline__ void bulk(void *dst, const void *src, uint32_t n, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(dst)), "l"(src), "r"(n), "r"(su32(bar)) : "memory");
+}
+template <int NC, int NS, int SB, int MATH, int PAT = 0>
+__global__ void __launch_bounds__((NC + 1) * 32) k(const uint8_t *d, const uint8_t *c, size_t bytes, float *out) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  uint8_t *buf = sm;  // [NS][2][SB]
+  uint64_t *full = reinterpret_cast<uint64_t *>(sm + (size_t)NS * 2 * SB), *empty = full + NS;
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) { for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NC); } asm volatile("fence.mbarrier_init.release.cluster;"); }
+  __syncthreads();
+  // PAT 0: SB-byte blocks round robin over CTAs; PAT 1: K1r's layout -- CTA (g, m) of 37 groups
+  // of 4 streams chunk m (76032 B) of rows g, g + 37, ... (640 rows of 304128 B)
+  const size_t RB = 304128, CB = 76032;
+  const uint32_t g = blockIdx.x / 4, m = blockIdx.x % 4, ng = gridDim.x / 4;
+  const size_t nrow = (g < 640 % ng) ? 640 / ng + 1 : 640 / ng;
+  const size_t spc = (CB + SB - 1) / SB;  // stages per chunk
+  const size_t nst = PAT == 0 ? (bytes / SB + gridDim.x - 1 - blockIdx.x) / gridDim.x : (PAT == 2 ? 2 : 1) * nrow * spc;
+  // PAT 2 order: P1(0), P1(1), P2(0), P1(2), P2(1), ..., P2(last)
+  auto seq = [&](size_t j, size_t &ch, size_t &st) -> bool {  // returns true for a pass-2 stage
+    if (PAT != 2) { ch = j / spc; st = j % spc; return false; }
+    const size_t blk = j / spc; st = j % spc;
+    if (blk == 0) { ch = 0; return false; }
+    const size_t q = blk - 1;  // blocks after the first alternate P1(q/2+1), P2(q/2)
+    if (q / 2 + 1 < nrow) { ch = (q & 1) ? q / 2 : q / 2 + 1; return (q & 1) != 0; }
+    ch = nrow - 1; return true;  // the last P2
+  };
+  auto off = [&](size_t j, uint32_t &n) -> size_t {
+    if (PAT == 0) { n = SB; return (blockIdx.x + j * gridDim.x) * (size_t)SB; }
+    size_t ch, st; seq(j, ch, st);
+    const size_t r = g + ch * ng, o = st * SB;
+    n = (uint32_t)((o + SB <= CB) ? SB : CB - o);
+    return r * RB + m * CB + o;
+  };
+  if (wid == 0) {
+    if (lane) return;
+    uint32_t it = 0;
+    for (size_t j = 0; j < nst; ++j, ++it) {
+      const int s = it % NS;
+      wait(&empty[s], ((it / NS) & 1) ^ 1);
+      uint32_t n;
+      const size_t o = off(j, n);
+      arrive_tx(&full[s], 2 * n);
+      bulk(buf + (size_t)s * 2 * SB, d + o, n, &full[s]);
+      bulk(buf + (size_t)s * 2 * SB + SB, c + o, n, &full[s]);
+    }
+    return;
+  }
+  const int cw = wid - 1;
+  constexpr int UPS = SB / 16, UPW = UPS / NC;  // units per stage, per consumer warp
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+  uint32_t it = 0;
+  for (size_t j = 0; j < nst; ++j, ++it) {
+    const int s = it % NS;
+    wait(&full[s], (it / NS) & 1);
+    size_t ch_, st_;
+    const bool p2 = seq(j, ch_, st_);
+    const uint4 *bd = reinterpret_cast<const uint4 *>(buf + (size_t)s * 2 * SB), *bc = bd + UPS;
+    uint4 rd[UPW / 32], rc[UPW / 32];
+#pragma unroll
+    for (int u = 0; u < UPW / 32; ++u) { rd[u] = bd[cw * UPW + u * 32 + lane]; rc[u] = bc[cw * UPW + u * 32 + lane]; }
+    __syncwarp();
+    if (lane == 0) arrive(&empty[s]);
+    if (MATH == 3 && p2) {
+#pragma unroll
+      for (int u = 0; u < UPW / 32; ++u) {
+        const uint32_t wa[4] = {rd[u].x, rd[u].y, rd[u].z, rd[u].w}, wb[4] = {rc[u].x, rc[u].y, rc[u].z, rc[u].w};
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          float x0 = __uint_as_float(wa[p] << 16), x1 = __uint_as_float(wa[p] & 0xffff0000u);
+          float y0 = __uint_as_float(wb[p] << 16), y1 = __uint_as_float(wb[p] & 0xffff0000u);
+          a2 += ex2(fminf(fmaf(x0, 1.44f, -5.f), fmaf(y0, 1.44f, -5.f))) + ex2(fminf(fmaf(x1, 1.44f, -5.f), fmaf(y1, 1.44f, -5.f)));
+        }
+      }
+      continue;
+    }
+#pragma unroll
+    for (int u = 0; u < UPW / 32; ++u) {
+      const uint32_t wa[4] = {rd[u].x, rd[u].y, rd[u].z, rd[u].w}, wb[4] = {rc[u].x, rc[u].y, rc[u].z, rc[u].w};
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        float x0 = __uint_as_float(wa[p] << 16), x1 = __uint_as_float(wa[p] & 0xffff0000u);
+        float y0 = __uint_as_float(wb[p] << 16), y1 = __uint_as_float(wb[p] & 0xffff0000u);
+        if (MATH == 0) { a0 += x0 + x1; a1 += y0 + y1; }
+        if (MATH >= 1) {
+          float e0 = ex2(fmaf(x0, 1.44f, -3.f)), e1 = ex2(fmaf(x1, 1.44f, -3.f)), f0 = ex2(fmaf(y0, 1.44f, -3.f)), f1 = ex2(fmaf(y1, 1.44f, -3.f));
+          a0 += e0 + e1; a1 += f0 + f1; a2 = fmaf(e0, x0 - y0, fmaf(e1, x1 - y1, a2));
+        }
+        if (MATH == 2) a2 += ex2(fminf(fmaf(x0, 1.44f, -5.f), fmaf(y0, 1.44f, -5.f))) + ex2(fminf(fmaf(x1, 1.44f, -5.f), fmaf(y1, 1.44f, -5.f)));
+      }
+    }
+  }
+  if (a0 + a1 + a2 == 1234.5f) out[0] = a0;
+}
+template <int NC, int NS, int SB, int MATH, int PAT = 0>
+void run(const uint8_t *d, const uint8_t *c, size_t bytes, float *out, int cps) {
+  const int smem = NS * 2 * SB + 2 * NS * 8;
+  cudaFuncSetAttribute(k<NC, NS, SB, MATH, PAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int per = 0; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k<NC, NS, SB, MATH, PAT>, (NC + 1) * 32, smem);
+  if (per < cps) { printf("PAT=%d NC=%d NS=%d SB=%d MATH=%d cps=%d: not resident (%d)\n", PAT, NC, NS, SB, MATH, cps, per); return; }
+  const int grid = 148 * cps;
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  for (int w = 0; w < 3; ++w) k<NC, NS, SB, MATH, PAT><<<grid, (NC + 1) * 32, smem>>>(d, c, bytes, out);
+  cudaEventRecord(e0);
+  const int R = 10;
+  for (int r = 0; r < R; ++r) k<NC, NS, SB, MATH, PAT><<<grid, (NC + 1) * 32, smem>>>(d, c, bytes, out);
+  cudaEventRecord(e1); cudaEventSynchronize(e1);
+  float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= R;
+  printf("PAT=%d NC=%2d NS=%2d SB=%6d MATH=%d cps=%d smem=%6d: %7.1f us  %6.0f GB/s (%s)\n", PAT, NC, NS, SB, MATH, cps, smem, ms * 1e3,
+         2.0 * bytes / (ms * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+}
+int main() {
+  const size_t bytes = (size_t)80 * 8 * 152064 * 2;  // one tensor
+  uint8_t *d, *c; float *out;
+  cudaMalloc(&d, bytes); cudaMalloc(&c, bytes); cudaMalloc(&out, 4);
+  cudaMemset(d, 0x3c, bytes); cudaMemset(c, 0x3d, bytes);
+  run<16, 6, 16384, 1, 1>(d, c, bytes, out, 1);
+  run<16, 6, 16384, 2, 1>(d, c, bytes, out, 1);
+  run<16, 6, 16384, 0, 2>(d, c, bytes, out, 1);
+  run<16, 6, 16384, 3, 2>(d, c, bytes, out, 1);
+  run<16, 12, 8192, 3, 2>(d, c, bytes, out, 1);
+  run<8, 6, 8192, 3, 2>(d, c, bytes, out, 2);
+  return 0;
+}
