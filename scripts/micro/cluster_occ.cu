@@ -1,15 +1,18 @@
 // How many thread-block clusters of each size fit on this GPU at one CTA per SM (K1 design input).
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 __global__ void kern(int *p) { if (p) p[0] = 1; }
-int main() {
-  const int smem = 200 * 1024;
+int main(int argc, char **argv) {
+  const int smem = (argc > 1 ? atoi(argv[1]) : 200) * 1024;
+  const int threads = argc > 2 ? atoi(argv[2]) : 640;
+  printf("smem %d KB, %d threads\n", smem / 1024, threads);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   for (int cs : {1, 2, 4, 8, 16}) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs * 64);
-    cfg.blockDim = dim3(640);
+    cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;

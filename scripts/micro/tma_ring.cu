@@ -23,7 +23,7 @@ __global__ void __launch_bounds__((NC + 1) * 32) k(const uint8_t *d, const uint8
   uint8_t *buf = sm;  // [NS][2][SB]
   uint64_t *full = reinterpret_cast<uint64_t *>(sm + (size_t)NS * 2 * SB), *empty = full + NS;
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) { for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NC); } asm volatile("fence.mbarrier_init.release.cluster;"); }
+  if (threadIdx.x == 0) { for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], MATH == 5 ? 1 : NC); } asm volatile("fence.mbarrier_init.release.cluster;"); }
   __syncthreads();
   // PAT 0: SB-byte blocks round robin over CTAs; PAT 1: K1r's layout -- CTA (g, m) of 37 groups
   // of 4 streams chunk m (76032 B) of rows g, g + 37, ... (640 rows of 304128 B)
@@ -31,9 +31,18 @@ __global__ void __launch_bounds__((NC + 1) * 32) k(const uint8_t *d, const uint8
   const uint32_t g = blockIdx.x / 4, m = blockIdx.x % 4, ng = gridDim.x / 4;
   const size_t nrow = (g < 640 % ng) ? 640 / ng + 1 : 640 / ng;
   const size_t spc = (CB + SB - 1) / SB;  // stages per chunk
-  const size_t nst = PAT == 0 ? (bytes / SB + gridDim.x - 1 - blockIdx.x) / gridDim.x : (PAT == 2 ? 2 : 1) * nrow * spc;
+  const size_t nst = PAT == 0 ? (bytes / SB + gridDim.x - 1 - blockIdx.x) / gridDim.x : (PAT >= 2 ? 2 : 1) * nrow * spc;
   // PAT 2 order: P1(0), P1(1), P2(0), P1(2), P2(1), ..., P2(last)
   auto seq = [&](size_t j, size_t &ch, size_t &st) -> bool {  // returns true for a pass-2 stage
+    if (PAT == 3) {  // j = 2 (c spc + s) + {0: P1 of chunk c, 1: P2 of chunk c - 1}; the last spc P2 at the end
+      const size_t q = j / 2, half = j & 1;
+      if (q < nrow * spc) {
+        ch = q / spc; st = q % spc;
+        if (half == 0) return false;
+        if (ch == 0) { ch = nrow - 1; st = q % spc; return true; }  // (reorder: chunk 0 slots do the last P2)
+        ch -= 1; return true;
+      }
+    }
     if (PAT != 2) { ch = j / spc; st = j % spc; return false; }
     const size_t blk = j / spc; st = j % spc;
     if (blk == 0) { ch = 0; return false; }
@@ -63,6 +72,24 @@ __global__ void __launch_bounds__((NC + 1) * 32) k(const uint8_t *d, const uint8
     return;
   }
   const int cw = wid - 1;
+  if (MATH == 5) {  // warp-owned stages
+    constexpr int UPL = SB / 16 / 32;
+    float acc = 0.f;
+    for (size_t j = cw; j < nst; j += NC) {
+      const int s = j % NS;
+      wait(&full[s], (j / NS) & 1);
+      const uint4 *bd = reinterpret_cast<const uint4 *>(buf + (size_t)s * 2 * SB), *bc = bd + SB / 16;
+      uint4 rd[UPL], rc[UPL];
+#pragma unroll
+      for (int u = 0; u < UPL; ++u) { rd[u] = bd[u * 32 + lane]; rc[u] = bc[u * 32 + lane]; }
+      __syncwarp();
+      if (lane == 0) arrive(&empty[s]);
+#pragma unroll
+      for (int u = 0; u < UPL; ++u) acc += __uint_as_float(rd[u].x) + __uint_as_float(rc[u].y);
+    }
+    if (acc == 1234.5f) out[0] = acc;
+    return;
+  }
   constexpr int UPS = SB / 16, UPW = UPS / NC;  // units per stage, per consumer warp
   float a0 = 0.f, a1 = 0.f, a2 = 0.f;
   uint32_t it = 0;
@@ -72,7 +99,7 @@ __global__ void __launch_bounds__((NC + 1) * 32) k(const uint8_t *d, const uint8
     size_t ch_, st_;
     const bool p2 = seq(j, ch_, st_);
     const uint4 *bd = reinterpret_cast<const uint4 *>(buf + (size_t)s * 2 * SB), *bc = bd + UPS;
-    uint4 rd[UPW / 32], rc[UPW / 32];
+    uint4 rd[UPW / 32 > 0 ? UPW / 32 : 1], rc[UPW / 32 > 0 ? UPW / 32 : 1];
 #pragma unroll
     for (int u = 0; u < UPW / 32; ++u) { rd[u] = bd[cw * UPW + u * 32 + lane]; rc[u] = bc[cw * UPW + u * 32 + lane]; }
     __syncwarp();
@@ -109,12 +136,12 @@ __global__ void __launch_bounds__((NC + 1) * 32) k(const uint8_t *d, const uint8
   if (a0 + a1 + a2 == 1234.5f) out[0] = a0;
 }
 template <int NC, int NS, int SB, int MATH, int PAT = 0>
-void run(const uint8_t *d, const uint8_t *c, size_t bytes, float *out, int cps) {
+void run(const uint8_t *d, const uint8_t *c, size_t bytes, float *out, int cps, int ctas = 148) {
   const int smem = NS * 2 * SB + 2 * NS * 8;
   cudaFuncSetAttribute(k<NC, NS, SB, MATH, PAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int per = 0; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k<NC, NS, SB, MATH, PAT>, (NC + 1) * 32, smem);
   if (per < cps) { printf("PAT=%d NC=%d NS=%d SB=%d MATH=%d cps=%d: not resident (%d)\n", PAT, NC, NS, SB, MATH, cps, per); return; }
-  const int grid = 148 * cps;
+  const int grid = ctas * cps;
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   for (int w = 0; w < 3; ++w) k<NC, NS, SB, MATH, PAT><<<grid, (NC + 1) * 32, smem>>>(d, c, bytes, out);
   cudaEventRecord(e0);
@@ -122,7 +149,7 @@ void run(const uint8_t *d, const uint8_t *c, size_t bytes, float *out, int cps) 
   for (int r = 0; r < R; ++r) k<NC, NS, SB, MATH, PAT><<<grid, (NC + 1) * 32, smem>>>(d, c, bytes, out);
   cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= R;
-  printf("PAT=%d NC=%2d NS=%2d SB=%6d MATH=%d cps=%d smem=%6d: %7.1f us  %6.0f GB/s (%s)\n", PAT, NC, NS, SB, MATH, cps, smem, ms * 1e3,
+  printf("grid=%3d PAT=%d NC=%2d NS=%2d SB=%6d MATH=%d cps=%d smem=%6d: %7.1f us  %6.0f GB/s (%s)\n", grid, PAT, NC, NS, SB, MATH, cps, smem, ms * 1e3,
          2.0 * bytes / (ms * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
 }
 int main() {
@@ -130,11 +157,9 @@ int main() {
   uint8_t *d, *c; float *out;
   cudaMalloc(&d, bytes); cudaMalloc(&c, bytes); cudaMalloc(&out, 4);
   cudaMemset(d, 0x3c, bytes); cudaMemset(c, 0x3d, bytes);
-  run<16, 6, 16384, 1, 1>(d, c, bytes, out, 1);
-  run<16, 6, 16384, 2, 1>(d, c, bytes, out, 1);
-  run<16, 6, 16384, 0, 2>(d, c, bytes, out, 1);
-  run<16, 6, 16384, 3, 2>(d, c, bytes, out, 1);
-  run<16, 12, 8192, 3, 2>(d, c, bytes, out, 1);
-  run<8, 6, 8192, 3, 2>(d, c, bytes, out, 2);
+  run<4, 32, 2048, 0, 0>(d, c, bytes, out, 1);
+  run<16, 32, 2048, 5, 0>(d, c, bytes, out, 1);
+  run<16, 16, 4096, 5, 0>(d, c, bytes, out, 1);
+  run<8, 16, 4096, 5, 0>(d, c, bytes, out, 1);
   return 0;
 }
