@@ -316,116 +316,6 @@ __global__ void __launch_bounds__(kRowsThreads, 4) sv_rows_kernel(const __grid_c
   }
 }
 
-// ------------------------------------------------------------------ K4r
-// K4 with the loads moved to the TMA engine (rows 16-byte aligned, V a whole number of 16-byte
-// units, unsharded, B <= kRowsRingMaxB): one persistent CTA per SM of kRowsRingWarps warps; every
-// warp is its own producer -- item it of the compacted list belongs to warp it % (grid NW) --
-// and keeps kRowsRingDepth items in flight in its private shared-memory stages (1-D bulk copies,
-// completion on the stage's mbarrier; the warp refills a stage as soon as it has the stage's units
-// in registers).  The lane -> unit mapping and the arithmetic are K4's (rows_units_core), so the
-// partials are bit-identical to K4's.
-#ifndef SV_K4R
-#define SV_K4R 0  // measured slower than K4 (32.8 vs 25.6 us at the headline): experiment only
-#endif
-constexpr int kRowsRingWarps = 16;
-constexpr int kRowsRingDepth = 3;
-constexpr int kRowsItemUnits = 32 * kRowUnitsPerThread;
-constexpr int kRowsRingMaxB = 2048;
-constexpr int kRowsRingThreads = kRowsRingWarps * 32;
-struct RowsRingSmem {
-  uint4 buf[kRowsRingWarps][kRowsRingDepth][kRowsItemUnits];
-  uint64_t full[kRowsRingWarps][kRowsRingDepth];
-  int32_t pref[kRowsRingMaxB + 1];
-  int64_t rowptr[kRowsRingMaxB];  // ragged target: first row of each sequence (staged once)
-};
-
-// Item `it` of the compacted list -> (b, rem) by walking the prefix forward from b (increasing it).
-__device__ __forceinline__ int rows_item_seq(const RowsRingSmem &sm, int64_t it, int b) {
-  while (sm.pref[b + 1] <= it) ++b;
-  return b;
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kRowsRingThreads, 1) sv_rows_ring_kernel(const __grid_constant__ VerifyArgs a) {
-  constexpr int EPU = Elem<T>::kPerUnit, D = kRowsRingDepth;
-  extern __shared__ __align__(128) uint8_t rr_raw[];
-  RowsRingSmem &sm = *reinterpret_cast<RowsRingSmem *>(rr_raw);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (lane == 0) {
-    for (int q = 0; q < D; ++q) mbar_init(&sm.full[wid][q], 1);
-    fence_mbar_init();
-  }
-  pdl_wait();
-  pdl_trigger();
-  const int splits = (int)a.splits;
-  if (wid == 0) {  // item prefix over the sequences: items of b = (gamma_b + 1) splits (0 if bad)
-    int run = 0;
-    for (int b0 = 0; b0 < a.B; b0 += 32) {
-      int cnt = 0;
-      if (b0 + lane < a.B) {
-        const int g = a.gamma[b0 + lane];
-        cnt = (g >= 0 && g <= a.k) ? (g + 1) * splits : 0;
-      }
-      int incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      if (b0 + lane < a.B) {
-        sm.pref[b0 + lane + 1] = run + incl;
-        if (a.t_rowptr) sm.rowptr[b0 + lane] = a.t_rowptr[b0 + lane];
-      }
-      run += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    if (lane == 0) sm.pref[0] = 0;
-  }
-  __syncthreads();
-  const int64_t total = sm.pref[a.B], stride = (int64_t)gridDim.x * kRowsRingWarps;
-  const int64_t first = (int64_t)blockIdx.x * kRowsRingWarps + wid;
-  // lane 0 issues the copy of item `it` into stage q (its first unit, the units, the row)
-  int bi = 0;  // lane 0's walk over the sequences (issue side)
-  auto issue = [&](int64_t it, int q) {
-    bi = rows_item_seq(sm, it, bi);
-    const int rem = (int)(it - sm.pref[bi]), i = rem / splits, split = rem - i * splits;
-    const int64_t v0 = (int64_t)split * a.rows_chunk;
-    const int units = (int)(min(a.rows_chunk, (int64_t)a.V - v0) / EPU);
-    const T *row = reinterpret_cast<const T *>(a.t) +
-                   (a.t_rowptr ? (sm.rowptr[bi] + i) * a.t_si : (int64_t)bi * a.t_sb + (int64_t)i * a.t_si);
-    mbar_arrive_expect_tx(&sm.full[wid][q], (uint32_t)units * 16u);
-    bulk_g2s_plain(sm.buf[wid][q], row + v0, (uint32_t)units * 16u, &sm.full[wid][q]);
-  };
-  if (lane == 0)
-    for (int q = 0; q < D; ++q)
-      if (first + q * stride < total) issue(first + q * stride, q);
-  const float c = a.ct;
-  int bc = 0;  // the consumer side's walk
-  for (int64_t n = 0;; ++n) {
-    const int64_t it = first + n * stride;
-    if (it >= total) return;
-    const int q = (int)(n % D);
-    mbar_wait_bounded(&sm.full[wid][q], (uint32_t)(n / D) & 1);
-    bc = rows_item_seq(sm, it, bc);
-    const int rem = (int)(it - sm.pref[bc]), i = rem / splits, split = rem - i * splits;
-    const int units = (int)(min(a.rows_chunk, (int64_t)a.V - (int64_t)split * a.rows_chunk) / EPU);
-    uint4 r[kRowUnitsPerThread];
-#pragma unroll
-    for (int j = 0; j < kRowUnitsPerThread; ++j)
-      if (lane + 32 * j < units) r[j] = sm.buf[wid][q][lane + 32 * j];
-    float m = kMFloor;
-    double l = 0.0;
-    rows_units_core<T>(r, units, kMFloor, c, m, l);
-    __syncwarp();  // every lane has consumed the stage: refill it with item it + D stride
-    if (lane == 0 && it + D * stride < total) {
-      fence_proxy_async_smem();  // generic-proxy reads before the async-proxy (TMA) writes
-      issue(it + D * stride, q);
-    }
-    const float M = warp_max(m);
-    const double v = warp_sum_d(l * ex2((m - M) * c));
-    if (lane == 0) a.partials[((int64_t)bc * (a.k + 1) + i) * a.splits + split] = make_float2(M, (float)v);
-  }
-}
-
 // ------------------------------------------------------------------ K5
 template <typename T>
 struct SampleRow {
@@ -676,16 +566,6 @@ __global__ void __launch_bounds__(kSampleThreads, 3) sv_resid_kernel(const __gri
 
 }  // namespace
 
-// K4r: unsharded, B <= kRowsRingMaxB, target rows 16-byte aligned and a whole number of units
-static bool rows_ring_ok(const VerifyArgs &a) {
-  if (!SV_K4R) return false;
-  const int eb = a.bf16 ? 2 : 4;
-  if (a.xtok_out || a.B > kRowsRingMaxB || ((int64_t)a.V * eb) % 16 != 0) return false;
-  if ((reinterpret_cast<uintptr_t>(a.t) & 15) != 0 || (a.t_si * eb) % 16 != 0) return false;
-  if (!a.t_rowptr && (a.t_sb * eb) % 16 != 0) return false;
-  return a.rows_chunk % 8 == 0;
-}
-
 int64_t verify_ws_bytes(int64_t B, int k, int64_t splits, int nsl) {
   return ws_round(B * (k + 1) * splits * 8) + ws_round(B * (int64_t)sizeof(Decision)) + ws_round(B * nsl * 16);
 }
@@ -694,16 +574,6 @@ int64_t verify_ws_bytes(int64_t B, int k, int64_t splits, int nsl) {
 cudaError_t launch_verify_stage(int stage, const VerifyArgs &a, cudaStream_t st) {
   switch (stage) {
     case 0: {  // K4: persistent over the compacted (sequence, row <= gamma, split) items
-      if (rows_ring_ok(a)) {
-        const int smem = (int)sizeof(RowsRingSmem);
-        const void *fr = a.bf16 ? (const void *)sv_rows_ring_kernel<__nv_bfloat16> : (const void *)sv_rows_ring_kernel<float>;
-        cudaFuncSetAttribute(fr, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        const int grid = resident_grid(fr, kRowsRingThreads, smem);
-        return a.bf16 ? launch_k(sv_rows_ring_kernel<__nv_bfloat16>, dim3((unsigned)grid), dim3(kRowsRingThreads),
-                                 (size_t)smem, st, a)
-                      : launch_k(sv_rows_ring_kernel<float>, dim3((unsigned)grid), dim3(kRowsRingThreads), (size_t)smem,
-                                 st, a);
-      }
       const void *fn = a.bf16 ? (const void *)sv_rows_kernel<__nv_bfloat16> : (const void *)sv_rows_kernel<float>;
       const int64_t need = ((int64_t)a.B * (a.k + 1) * a.splits + kRowsThreads / 32 - 1) / (kRowsThreads / 32);
       const int64_t grid = need < resident_grid(fn, kRowsThreads, 0) ? need : resident_grid(fn, kRowsThreads, 0);

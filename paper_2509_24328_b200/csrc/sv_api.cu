@@ -26,27 +26,6 @@ int64_t chunk_elems_for(int64_t V, int cs) {
   return (c + 15) / 16 * 16;
 }
 
-// K1s: rows whose 16-byte units are aligned (base pointers, strides and V * elem_bytes).
-bool score_res_ok(const void *d, const void *c, int64_t d_sb, int64_t d_si, int64_t c_sb, int64_t c_si, int64_t V,
-                  int elem_bytes) {
-  if (!SV_K1S) return false;
-  if ((V * elem_bytes) % 16 != 0) return false;
-  if (((reinterpret_cast<uintptr_t>(d) | reinterpret_cast<uintptr_t>(c)) & 15) != 0) return false;
-  for (int64_t s : {d_sb, d_si, c_sb, c_si})
-    if ((s * elem_bytes) % 16 != 0) return false;
-  return score_res_cs(V, elem_bytes) <= 32;  // (one lane per chunk partial in the merges)
-}
-
-int score_res_cs(int64_t V, int elem_bytes) {  // chunks of <= kResBufUnits units (a function of V only)
-  const int64_t units = V * elem_bytes / 16;
-  return (int)((units + kResBufUnits - 1) / kResBufUnits);
-}
-
-int score_ws_cs(int64_t V, int elem_bytes) {
-  const int a = score_splits_for(V, elem_bytes), b = score_res_cs(V, elem_bytes);
-  return a > b ? a : b;
-}
-
 int64_t rows_splits_for(int64_t V, int elem_bytes) {
   const int64_t per = (int64_t)32 * kRowUnitsPerThread * (16 / elem_bytes);
   return (V + per - 1) / per;
@@ -99,7 +78,7 @@ static int elem_bytes(int32_t d) { return d == SV_BF16 ? 2 : 4; }
 
 // sd_verify's partials follow sv_score's region, so one workspace serves both calls
 static int64_t verify_ws_offset(int32_t B, int32_t k, int32_t V, int eb) {
-  return score_ws_bytes((int64_t)B * k, score_ws_cs(V, eb));
+  return score_ws_bytes((int64_t)B * k, score_splits_for(V, eb));
 }
 
 static int32_t shape_check(int32_t B, int32_t k, int32_t V, int32_t dtype) {
@@ -254,22 +233,12 @@ static int32_t score_impl(const sv_logits *draft, const sv_logits *comp, const i
   const int64_t rows = (int64_t)B * k;
   if (2 * rows * a.cs > INT32_MAX) return SV_ERR_UNSUPPORTED;  // one CTA per chunk task
   a.lead = (rows < kScoreLag ? rows : (int64_t)kScoreLag) * a.cs;
-  if (score_res_ok(a.d, a.c, a.d_sb, a.d_si, a.c_sb, a.c_si, V, elem_bytes(draft->dtype))) {
-    a.res = 1;  // K1s chunks: whole 16-byte units, at most kResBufUnits per tensor
-    a.cs = score_res_cs(V, elem_bytes(draft->dtype));
-    const int64_t units = (int64_t)V * elem_bytes(draft->dtype) / 16;
-    a.chunk = (units + a.cs - 1) / a.cs * (16 / elem_bytes(draft->dtype));
-    a.lead = (rows < kScoreLag ? rows : (int64_t)kScoreLag) * a.cs;  // (K1 fallback)
-  }
   if (2 * a.chunk * elem_bytes(draft->dtype) > kScoreMaxChunkBytes) return SV_ERR_UNSUPPORTED;  // V too large
   uint8_t *ws = reinterpret_cast<uint8_t *>(workspace);
-  {  // layout of score_ws_bytes(rows, score_ws_cs(V)) (>= the cs in use)
-    const int cs0 = score_ws_cs(V, elem_bytes(draft->dtype));
-    a.part = reinterpret_cast<double *>(ws);
-    a.spart = reinterpret_cast<float *>(ws + ws_round(rows * cs0 * 5 * 8));
-    a.cnt = reinterpret_cast<uint32_t *>(ws + ws_round(rows * cs0 * 5 * 8) + ws_round(rows * cs0 * 4));
-    a.ticket = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(a.cnt) + ws_round(rows * 2 * 4));
-  }
+  a.part = reinterpret_cast<double *>(ws);  // the layout of score_ws_bytes(rows, cs)
+  a.spart = reinterpret_cast<float *>(ws + ws_round(rows * a.cs * 5 * 8));
+  a.cnt = reinterpret_cast<uint32_t *>(ws + ws_round(rows * a.cs * 5 * 8) + ws_round(rows * a.cs * 4));
+  a.ticket = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(a.cnt) + ws_round(rows * 2 * 4));
   cudaError_t e = launch_score(a, (cudaStream_t)stream);
   if (e == cudaSuccess && sch) e = launch_schedule(*sch, (cudaStream_t)stream);  // sv_score_schedule
   if (e != cudaSuccess) {

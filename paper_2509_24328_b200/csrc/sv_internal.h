@@ -32,40 +32,6 @@ namespace sv {
 #ifndef SV_K1_SAMECTA
 #define SV_K1_SAMECTA 0
 #endif
-// K1s (the resident-chunk path of sv_score, rows with 16-byte aligned units): a row is split
-// into cs chunks of at most kResBufUnits 16-byte units per tensor; a group of cs persistent CTAs
-// (one per SM) takes the group's rows, member m chunk m; each CTA keeps kResBufs chunk pairs in
-// shared memory, so both passes read a chunk from HBM once.  kResConsumers consumer warps; a
-// stage is one 16-byte unit per consumer lane per tensor.
-#ifndef SV_K1S
-#define SV_K1S 0
-#endif
-#ifndef SV_K1S_POLY
-#define SV_K1S_POLY 0
-#endif
-#ifndef SV_K1S_DBG
-#define SV_K1S_DBG 0  // timing experiments only
-#endif
-#ifndef SV_K1S_TRACE
-#define SV_K1S_TRACE 0  // timing experiments only
-#endif
-#ifndef SV_K1S_BUFS
-#define SV_K1S_BUFS 4
-#endif
-#ifndef SV_K1S_UNITS
-#define SV_K1S_UNITS 1536
-#endif
-#ifndef SV_K1S_LAG
-#define SV_K1S_LAG 2
-#endif
-constexpr int kResConsumers = 16;
-constexpr int kResBufs = SV_K1S_BUFS;
-constexpr int kResStageUnits = kResConsumers * 32;  // 512
-constexpr int kResBufUnits = SV_K1S_UNITS;          // 4 buffers x (D + C) x 24576 B = 196608 B
-constexpr int kResLag = SV_K1S_LAG;  // pass 2 of chunk n runs after pass 1 of chunk n + kResLag (<= kResBufs - 2)
-constexpr int kResMaxStages = (kResBufUnits + kResStageUnits - 1) / kResStageUnits;
-constexpr int kResThreads = (kResConsumers + 4) * 32;  // + producer, Lambda, P1-publish, S-publish warps
-constexpr int kResPoly = SV_K1S_POLY;  // of every 4 packed pass-2 pairs, this many take 2^y on the FMA pipe
 constexpr int kScoreThreads = 256;
 constexpr int kScoreMinBlocks = SV_K1_MINB;
 constexpr int kScoreGroup = SV_K1_GROUP;
@@ -134,14 +100,7 @@ struct ScoreArgs {
   float *spart;     // workspace: [B k cs] S partials
   uint32_t *cnt;    // workspace: [B k][2] P1 / P2 counters, zero between calls (self-cleaning)
   uint32_t *ticket; // workspace: K1's task counter, zero between calls (self-cleaning)
-  int res;          // 1: K1s (cs / chunk are then score_res_cs / its chunk)
 };
-// K1s eligibility (a function of V, dtype and the row alignment only) and its chunks per row
-bool score_res_ok(const void *d, const void *c, int64_t d_sb, int64_t d_si, int64_t c_sb, int64_t c_si, int64_t V,
-                  int elem_bytes);
-int score_res_cs(int64_t V, int elem_bytes);
-// chunks per row the sv_score workspace is sized for (K1 and K1s)
-int score_ws_cs(int64_t V, int elem_bytes);
 // sv_score's share of the workspace (offset 0); sd_verify's follows it
 int64_t score_ws_bytes(int64_t rows, int cs);
 cudaError_t launch_score(const ScoreArgs &a, cudaStream_t st);

@@ -48,18 +48,10 @@ __device__ __forceinline__ uint4 ldg_hint(const void *p, uint64_t pol) {
 __device__ __forceinline__ void red_release_add(uint32_t *p, uint32_t v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ void red_relaxed_add(uint32_t *p, uint32_t v) {
-  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 __device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t *p, uint32_t v) {
   uint32_t old;
   asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
   return old;
-}
-__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
 }
 __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
@@ -779,366 +771,9 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constan
   p2_finish_tail<T, NW>(a, c.k, sm);
 }
 
-// Merge of np <= 32 partials (M_d, L_d, M_c, L_c, W) with lane j holding partial j, by a fixed
-// xor butterfly (every lane ends with the same bits; one load round trip); lane 0 writes glob / lam.
-template <typename PartFn, bool kGlobal = true>
-__device__ __forceinline__ void merge_partials_bfly(const ScoreArgs &a, int np, PartFn part_of, double (&glob)[5],
-                                                    float (&lam)[2]) {
-  auto ld = [](const double *p) { return kGlobal ? __ldcg(p) : *p; };
-  const int lane = threadIdx.x & 31;
-  const float cd = a.cd, cc = a.cc;
-  double pr[5] = {kMFloor, 0.0, kMFloor, 0.0, 0.0};
-  if (lane < np) {
-    const double *part = part_of(lane);
-#pragma unroll
-    for (int j = 0; j < 5; ++j) pr[j] = ld(part + j);
-  }
-  const float rmd = (float)pr[0], rmc = (float)pr[2];
-  const float GMd = warp_max(rmd), GMc = warp_max(rmc);
-  const float sdf = ex2((rmd - GMd) * cd), scf = ex2((rmc - GMc) * cc);
-  const float delta = (GMc - rmc) * cc - (GMd - rmd) * cd;
-  double ww = pr[4];
-  if (pr[1] > 0.0) ww += pr[1] * (double)delta;
-  const double L_d = warp_sum_d(pr[1] * sdf), L_c = warp_sum_d(pr[3] * scf), W = warp_sum_d(ww * sdf);
-  if (lane == 0) {
-    glob[0] = GMd;
-    glob[1] = L_d;
-    glob[2] = GMc;
-    glob[3] = L_c;
-    glob[4] = W;
-    const bool ok = L_d > 0.0 && L_c > 0.0 && L_d < 1e300 && L_c < 1e300 && GMd < FLT_MAX && GMc < FLT_MAX;
-    lam[0] = ok ? (float)((double)GMd * cd + log2_acc(L_d)) : __int_as_float(0x7fc00000);
-    lam[1] = ok ? (float)((double)GMc * cc + log2_acc(L_c)) : __int_as_float(0x7fc00000);
-  }
-}
-
-// ---------------------------------------------------------------- K1s: resident chunks
-// A row is split into cs chunks (score_res_cs: <= kResBufUnits 16-byte units per tensor).  A GROUP
-// of cs persistent CTAs (one per SM, groups of consecutive blockIdx) owns rows g, g + NG, ...;
-// member m always takes chunk m, and each CTA keeps kResBufs chunk pairs in shared memory, so a
-// chunk is read from HBM ONCE and both passes run on the resident copy (DESIGN §5 K1s):
-//   warp 0 (producer): 1-D bulk copies (TMA engine) of chunk n into buffer n % kResBufs, one
-//     full-barrier per stage (L2 evict_first: no second read), as soon as chunk n - kResBufs has
-//     left the buffer;
-//   consumers (kResConsumers warps): pass 1 of chunk n as its stages land (l_d, l_c, KL partial:
-//     2 MUFU.EX2 per pair), warp partials -> slot; then pass 2 of chunk n - kResLag from shared memory
-//     (S = sum 2^{min(a_d, a_c)}) with the group's Lambda, release the buffer, warp S -> slot;
-//   warp 2 (P1 publish): merges the warp partials in warp order, publishes the chunk's
-//     (M_d, L_d, M_c, L_c, W) and bumps the row counter (release);
-//   warp 1 (Lambda): waits for the row's cs partials and merges them (the same bits in every
-//     member) one chunk ahead of the consumers' pass 2;
-//   warp 3 (S publish): sums the warp S in warp order, publishes the S partial; the row's last one
-//     (acq_rel counter) runs the epilogue and re-arms the row's counters.
-// Lane l of consumer w owns unit s * 512 + w * 32 + l of stage s of every chunk; chunks, stages and
-// merge orders depend on (V, dtype) only, so every output bit is independent of B, the grid and the
-// GPU count.
-#if SV_K1S_TRACE
-// timing experiment only: per CTA, per chunk n < 32, event e: 0 load issued, 1 P1 done (consumer 0),
-// 2 P1 published, 3 Lambda ready, 4 P2 done (consumer 0), 5 S published
-__device__ unsigned long long g_res_trace[160][32][8];
-__device__ __forceinline__ void res_trace(uint32_t n, int e) {
-  if (n < 32 && blockIdx.x < 160) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_res_trace[blockIdx.x][n][e] = t;
-  }
-}
-#else
-__device__ __forceinline__ void res_trace(uint32_t, int) {}
-#endif
-static_assert(kResLag >= 1 && kResLag <= kResBufs - 2, "K1s: chunks n - kResLag .. n resident, n + 1 in flight");
-struct ResSmem {
-  uint4 buf[kResBufs][2][kResBufUnits];
-  double wpart[2][kResConsumers][5];  // pass-1 warp partials of chunk n (slot n % 2)
-  double glob[kResBufs][5];           // the row's merged pass-1 partials (Lambda warp -> epilogue)
-  float lam[kResBufs][2];
-  float wsum[kResBufs][kResConsumers];
-  double pglob[5];
-  float plam[2];
-  uint64_t full[kResBufs][kResMaxStages], empty[kResBufs];
-  uint64_t lamb[kResBufs], parts2[kResBufs], gfree[kResBufs];
-  uint64_t parts1[2], pfree1[2];
-};
-
-// This CTA's place: group g of ng, member m; its n-th chunk is chunk m of row g + n ng.
-struct ResPlace {
-  uint32_t g, m, ng, rows, nchunks;
-  __device__ __forceinline__ uint32_t row(uint32_t n) const { return g + n * ng; }
-};
-__device__ __forceinline__ ResPlace res_place(const ScoreArgs &a) {
-  ResPlace p;
-  p.m = blockIdx.x % (uint32_t)a.cs;
-  p.g = blockIdx.x / (uint32_t)a.cs;
-  p.ng = gridDim.x / (uint32_t)a.cs;
-  p.rows = (uint32_t)a.B * (uint32_t)a.k;
-  p.nchunks = p.g < p.rows ? (p.rows - p.g + p.ng - 1) / p.ng : 0;
-  return p;
-}
-template <typename T>
-__device__ __forceinline__ Chunk<T> res_chunk(const ScoreArgs &a, uint32_t row, uint32_t m) {
-  const int64_t b = row / (uint32_t)a.k, i = row - b * a.k, v0 = (int64_t)m * a.chunk;
-  Chunk<T> ch;
-  ch.d = reinterpret_cast<const T *>(a.d) + b * a.d_sb + i * a.d_si + v0;
-  ch.c = reinterpret_cast<const T *>(a.c) + b * a.c_sb + i * a.c_si + v0;
-  ch.n = (int)max((int64_t)0, min(a.chunk, (int64_t)a.V - v0));
-  ch.units = ch.n / Elem<T>::kPerUnit;  // K1s rows: whole 16-byte units, aligned
-  return ch;
-}
-__device__ __forceinline__ int res_stages(int units) {
-  return max(1, (units + kResStageUnits - 1) / kResStageUnits);  // an empty chunk is one empty stage
-}
-
-template <typename T>
-__device__ void res_producer(const ScoreArgs &a, ResSmem &sm) {
-  constexpr int EPU = Elem<T>::kPerUnit;
-  if ((threadIdx.x & 31) != 0) return;
-  const ResPlace pl = res_place(a);
-  const uint64_t pol = l2_policy_evict_first();  // read once
-  for (uint32_t n = 0; n < pl.nchunks; ++n) {
-    const int b = n % kResBufs;
-    mbar_wait_bounded(&sm.empty[b], ((n / kResBufs) & 1) ^ 1);  // chunk n - kResBufs has left the buffer
-    const Chunk<T> ch = res_chunk<T>(a, pl.row(n), pl.m);
-    const int nst = res_stages(ch.units);
-    res_trace(n, 0);
-    for (int s = 0; s < nst; ++s) {
-      const int u0 = s * kResStageUnits, nu = max(0, min(kResStageUnits, ch.units - u0));
-      mbar_arrive_expect_tx(&sm.full[b][s], 2u * (uint32_t)nu * 16u);
-      if (nu > 0) {
-        bulk_g2s(&sm.buf[b][0][u0], ch.d + (size_t)u0 * EPU, (uint32_t)nu * 16u, &sm.full[b][s], pol);
-        bulk_g2s(&sm.buf[b][1][u0], ch.c + (size_t)u0 * EPU, (uint32_t)nu * 16u, &sm.full[b][s], pol);
-      }
-    }
-  }
-}
-
-template <typename T>
-__device__ void res_lambda(const ScoreArgs &a, ResSmem &sm) {
-  const int lane = threadIdx.x & 31, cs = a.cs;
-  const ResPlace pl = res_place(a);
-  for (uint32_t n = 0; n < pl.nchunks; ++n) {
-    const int b = n % kResBufs;
-    const uint32_t row = pl.row(n);
-    mbar_wait_bounded(&sm.gfree[b], ((n / kResBufs) & 1) ^ 1);  // chunk n - kResBufs's epilogue is done
-    const uint32_t *cnt = a.cnt + 2 * (size_t)row;
-    for (uint32_t k = 0; SV_K1S_DBG != 3 && ld_relaxed(cnt) < (uint32_t)cs; ++k)
-      if (k > (1u << 28)) __trap();
-    if (SV_K1S_DBG != 1) fence_acq_rel();  // every lane: the cs partials are visible
-    merge_partials_bfly(a, cs, [&](int j) { return a.part + ((size_t)row * cs + j) * 5; }, sm.glob[b], sm.lam[b]);
-    __syncwarp();
-    if (lane == 0) {
-      res_trace(n, 3);
-      mbar_arrive(&sm.lamb[b]);
-    }
-  }
-}
-
-template <typename T>
-__device__ void res_publish1(const ScoreArgs &a, ResSmem &sm) {
-  const int lane = threadIdx.x & 31, cs = a.cs;
-  const ResPlace pl = res_place(a);
-  for (uint32_t n = 0; n < pl.nchunks; ++n) {
-    const int p = n & 1;
-    const uint32_t row = pl.row(n);
-    mbar_wait_bounded(&sm.parts1[p], (n >> 1) & 1);
-    auto warp_part = [&](int j) { return (const double *)sm.wpart[p][j]; };
-    merge_partials_bfly<decltype(warp_part), false>(a, kResConsumers, warp_part, sm.pglob, sm.plam);
-    __syncwarp();
-    if (lane == 0) {
-      double *part = a.part + ((size_t)row * cs + pl.m) * 5;
-#pragma unroll
-      for (int j = 0; j < 5; ++j) part[j] = sm.pglob[j];
-      if (SV_K1S_DBG == 1)
-        red_relaxed_add(a.cnt + 2 * (size_t)row, 1u);  // timing experiment only (no ordering)
-      else
-        red_release_add(a.cnt + 2 * (size_t)row, 1u);
-      res_trace(n, 2);
-      mbar_arrive(&sm.pfree1[p]);
-    }
-  }
-}
-
-template <typename T>
-__device__ void res_publish2(const ScoreArgs &a, ResSmem &sm) {
-  const int lane = threadIdx.x & 31, cs = a.cs;
-  const ResPlace pl = res_place(a);
-  for (uint32_t n = 0; n < pl.nchunks; ++n) {
-    const int b = n % kResBufs;
-    const uint32_t row = pl.row(n);
-    mbar_wait_bounded(&sm.parts2[b], (n / kResBufs) & 1);
-    uint32_t *cnt = a.cnt + 2 * (size_t)row;
-    float *srow = a.spart + (size_t)row * cs;
-    uint32_t old = 0;
-    if (lane == 0) {
-      float r = sm.wsum[b][0];
-      for (int w = 1; w < kResConsumers; ++w) r += sm.wsum[b][w];
-      srow[pl.m] = r;
-      old = atom_add_acq_rel(cnt + 1, 1u);  // releases this S partial, acquires the others
-    }
-    old = __shfl_sync(0xffffffffu, old, 0);
-    if (old == (uint32_t)(cs - 1)) {  // the row's last S partial: epilogue, re-arm the counters
-      __syncwarp();
-      fence_acq_rel();
-      const int64_t bb = row / (uint32_t)a.k, ii = row - bb * a.k;
-      epilogue<T>(a, bb, ii, sm.glob[b], srow, cs, 1, 0, nullptr, 0);
-      if (lane == 0) {
-        cnt[0] = 0u;  // every member's Lambda warp has read it (its pass 2 is done)
-        cnt[1] = 0u;
-      }
-    }
-    __syncwarp();
-    if (lane == 0) {
-      res_trace(n, 5);
-      mbar_arrive(&sm.gfree[b]);
-    }
-  }
-}
-
-// Exact pass 1 over one consumer lane's units of a chunk (global memory; the fallback of a lane
-// whose fast sums are not finite).
-template <typename T>
-__device__ __noinline__ P1Out res_exact(const ScoreArgs &a, uint32_t row, uint32_t m, int ubase) {
-  constexpr int EPU = Elem<T>::kPerUnit;
-  const Chunk<T> ch = res_chunk<T>(a, row, m);
-  P1State s{kMFloor, kMFloor, kMFloor, kMFloor, 0.f, 0.f, 0.f};
-  for (int u = ubase; u < ch.units; u += kResStageUnits)
-    exact_unit<T>(s, ldg_stream(ch.d + (size_t)u * EPU), ldg_stream(ch.c + (size_t)u * EPU), a.cd, a.cc);
-  return P1Out{s.rd, s.rc, s.ld, s.lc, s.w};
-}
-
-template <typename T>
-__device__ __forceinline__ void res_pass2(const ScoreArgs &a, ResSmem &sm, const ResPlace &pl, uint32_t n, int cw,
-                                          int ubase, f2 cdd, f2 ccc) {
-  const int b = n % kResBufs, lane = threadIdx.x & 31;
-  const Chunk<T> ch = res_chunk<T>(a, pl.row(n), pl.m);
-  if (SV_K1S_DBG != 2) mbar_wait_bounded(&sm.lamb[b], (n / kResBufs) & 1);
-  const float lamd = sm.lam[b][0], lamc = sm.lam[b][1];
-  f2 acc{0.f, 0.f};
-  if (lamd == lamd && lamc == lamc) {
-    const f2 nld{-lamd, -lamd}, nlc{-lamc, -lamc};
-    for (int u = ubase; u < ch.units; u += kResStageUnits) {
-      const uint4 d1[1] = {sm.buf[b][0][u]}, c1[1] = {sm.buf[b][1][u]};
-      p2_group<T, 1, kResPoly>(acc, d1, c1, cdd, ccc, nld, nlc);
-    }
-  }
-  __syncwarp();
-  if (lane == 0) mbar_arrive(&sm.empty[b]);  // the chunk leaves the buffer
-  if (cw == 0 && lane == 0) res_trace(n, 4);
-  const float sw = warp_sum(acc.x + acc.y);
-  if (lane == 0) {
-    sm.wsum[b][cw] = sw;
-    mbar_arrive(&sm.parts2[b]);
-  }
-}
-
-template <typename T>
-__device__ void res_consumer(const ScoreArgs &a, ResSmem &sm, int cw) {
-  const int lane = threadIdx.x & 31, ubase = cw * 32 + lane;
-  const ResPlace pl = res_place(a);
-  const float cd = a.cd, cc = a.cc;
-  const f2 cdd{cd, cd}, ccc{cc, cc};
-  for (uint32_t n = 0; n < pl.nchunks; ++n) {
-    const int b = n % kResBufs;
-    const uint32_t par = (n / kResBufs) & 1;
-    const Chunk<T> ch = res_chunk<T>(a, pl.row(n), pl.m);
-    const int nst = res_stages(ch.units);
-    // pass 1 of chunk n, one unit per lane per stage as the stages land
-    P1Fast t{kMFloor, kMFloor, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
-    f2 nrd{0.f, 0.f}, nrc{0.f, 0.f};
-    bool first = true;
-    for (int s = 0; s < nst; ++s) {
-      mbar_wait_bounded(&sm.full[b][s], par);
-      const int u = s * kResStageUnits + ubase;
-      if (u < ch.units) {
-        const uint4 d1[1] = {sm.buf[b][0][u]}, c1[1] = {sm.buf[b][1][u]};
-        if (first) {
-          fast_ref<T, 1>(t, d1, c1);
-          nrd = f2{-(t.rd * cd), -(t.rd * cd)};
-          nrc = f2{-(t.rc * cc), -(t.rc * cc)};
-          first = false;
-        }
-        fast_group<T, 1>(t, d1, c1, cdd, ccc, nrd, nrc);
-      }
-    }
-    {
-      const float ld = t.ld.x + t.ld.y, lc = t.lc.x + t.lc.y, w = t.w.x + t.w.y;
-      P1Out o{t.rd, t.rc, ld, lc, w};
-      if (!(ld < 1e36f && lc < 1e36f && w == w && fabsf(w) < 1e36f)) o = res_exact<T>(a, pl.row(n), pl.m, ubase);
-      const int p = n & 1;
-      mbar_wait_bounded(&sm.pfree1[p], ((n >> 1) & 1) ^ 1);  // the publisher is done with chunk n - 2
-      warp_p1_partial(o, cd, cc, sm.wpart[p][cw]);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.parts1[p]);
-      if (cw == 0 && lane == 0) res_trace(n, 1);
-    }
-    // pass 2 of chunk n - kResLag (its Lambda has had kResLag chunks' time to arrive)
-    if (n >= (uint32_t)kResLag) res_pass2<T>(a, sm, pl, n - kResLag, cw, ubase, cdd, ccc);
-  }
-  for (uint32_t n = pl.nchunks > (uint32_t)kResLag ? pl.nchunks - kResLag : 0; n < pl.nchunks; ++n)
-    res_pass2<T>(a, sm, pl, n, cw, ubase, cdd, ccc);
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kResThreads, 1) sv_score_res_kernel(const __grid_constant__ ScoreArgs a) {
-  extern __shared__ __align__(128) uint8_t res_raw[];
-  ResSmem &sm = *reinterpret_cast<ResSmem *>(res_raw);
-  const int wid = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-    for (int b = 0; b < kResBufs; ++b) {
-      for (int s = 0; s < kResMaxStages; ++s) mbar_init(&sm.full[b][s], 1);
-      mbar_init(&sm.empty[b], kResConsumers);
-      mbar_init(&sm.lamb[b], 1);
-      mbar_init(&sm.parts2[b], kResConsumers);
-      mbar_init(&sm.gfree[b], 1);
-    }
-    for (int p = 0; p < 2; ++p) {
-      mbar_init(&sm.parts1[p], kResConsumers);
-      mbar_init(&sm.pfree1[p], 1);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  pdl_wait();
-  pdl_trigger();
-  // control warps take the highest warp ids: the warp arbiter picks the highest eligible id
-  // first, so the 16 consumers never starve the producer / merge / publish warps
-  if (wid < kResConsumers)
-    res_consumer<T>(a, sm, wid);
-  else if (wid == kResConsumers)
-    res_producer<T>(a, sm);
-  else if (wid == kResConsumers + 1)
-    res_lambda<T>(a, sm);
-  else if (wid == kResConsumers + 2)
-    res_publish1<T>(a, sm);
-  else
-    res_publish2<T>(a, sm);
-}
-
-// Grid: whole groups of cs CTAs, one CTA per SM (co-resident: members wait on each other), at
-// most one group per row.  0 when not even one group fits (the caller then uses K1).
-template <typename T>
-int score_res_grid(const ScoreArgs &a) {
-  const int smem = (int)sizeof(ResSmem);
-  if (cudaFuncSetAttribute(sv_score_res_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
-    cudaGetLastError();
-    return 0;
-  }
-  const int64_t rows = (int64_t)a.B * a.k;
-  int64_t groups = resident_grid((const void *)sv_score_res_kernel<T>, kResThreads, smem) / a.cs;
-  if (groups > rows) groups = rows;
-  return (int)(groups * a.cs);
-}
-template <typename T>
-cudaError_t launch_score_res(const ScoreArgs &a, int grid, cudaStream_t st) {
-  return launch_k(sv_score_res_kernel<T>, dim3((unsigned)grid), dim3(kResThreads), sizeof(ResSmem), st, a);
-}
-
 template <typename T>
 cudaError_t launch_score_t(const ScoreArgs &a, cudaStream_t st) {
   if ((int64_t)a.B * a.k == 0) return cudaSuccess;
-  if (a.res) {
-    const int grid = score_res_grid<T>(a);
-    if (grid > 0) return launch_score_res<T>(a, grid, st);
-  }
   const int64_t tasks = (SV_K1_SAMECTA ? 1 : 2) * (int64_t)a.B * a.k * a.cs;
   if (tasks == 0) return cudaSuccess;
   return launch_k(sv_score_kernel<T, kScoreThreads, kScoreMinBlocks>, dim3((unsigned)tasks), dim3(kScoreThreads), 0,
@@ -1260,11 +895,6 @@ cudaError_t shard_score_stage_t(const ShardScoreArgs &h, const ScoreArgs &a, cud
 
 }  // namespace
 
-#if SV_K1S_TRACE
-extern "C" __attribute__((visibility("default"))) int sv_debug_res_trace(void *host) {
-  return (int)cudaMemcpyFromSymbol(host, g_res_trace, sizeof(g_res_trace));
-}
-#endif
 cudaError_t launch_score(const ScoreArgs &a, cudaStream_t st) {
   return a.bf16 ? launch_score_cfg<__nv_bfloat16>(a, st) : launch_score_cfg<float>(a, st);
 }
