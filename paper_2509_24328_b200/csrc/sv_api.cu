@@ -26,17 +26,6 @@ int64_t chunk_elems_for(int64_t V, int cs) {
   return (c + 15) / 16 * 16;
 }
 
-// K1g: rows whose 16-byte units are aligned (base pointers, strides and V * elem_bytes), cs <= 32.
-bool score_grp_ok(const void *d, const void *c, int64_t d_sb, int64_t d_si, int64_t c_sb, int64_t c_si, int64_t V,
-                  int elem_bytes, int cs) {
-  if (!SV_K1G || cs > 32) return false;
-  if ((V * elem_bytes) % 16 != 0) return false;
-  if (((reinterpret_cast<uintptr_t>(d) | reinterpret_cast<uintptr_t>(c)) & 15) != 0) return false;
-  for (int64_t s : {d_sb, d_si, c_sb, c_si})
-    if ((s * elem_bytes) % 16 != 0) return false;
-  return true;
-}
-
 int64_t rows_splits_for(int64_t V, int elem_bytes) {
   const int64_t per = (int64_t)32 * kRowUnitsPerThread * (16 / elem_bytes);
   return (V + per - 1) / per;
@@ -245,7 +234,6 @@ static int32_t score_impl(const sv_logits *draft, const sv_logits *comp, const i
   if (2 * rows * a.cs > INT32_MAX) return SV_ERR_UNSUPPORTED;  // one CTA per chunk task
   a.lead = (rows < kScoreLag ? rows : (int64_t)kScoreLag) * a.cs;
   if (2 * a.chunk * elem_bytes(draft->dtype) > kScoreMaxChunkBytes) return SV_ERR_UNSUPPORTED;  // V too large
-  a.grp = score_grp_ok(a.d, a.c, a.d_sb, a.d_si, a.c_sb, a.c_si, V, elem_bytes(draft->dtype), a.cs) ? 1 : 0;
   uint8_t *ws = reinterpret_cast<uint8_t *>(workspace);
   a.part = reinterpret_cast<double *>(ws);  // the layout of score_ws_bytes(rows, cs)
   a.spart = reinterpret_cast<float *>(ws + ws_round(rows * a.cs * 5 * 8));

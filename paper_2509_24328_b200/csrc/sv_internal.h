@@ -32,29 +32,6 @@ namespace sv {
 #ifndef SV_K1_SAMECTA
 #define SV_K1_SAMECTA 0
 #endif
-// K1g (grouped, interleaved sv_score path for rows with 16-byte aligned units; DESIGN §5 K1g):
-// kGrpConsumers consumer warps, one 16-byte unit per consumer lane per tensor per stage, a ring of
-// kGrpStages stages, pass 2 of a row kGrpLag steps after its pass 1.
-#ifndef SV_K1G
-#define SV_K1G 0
-#endif
-#ifndef SV_K1G_STAGES
-#define SV_K1G_STAGES 12
-#endif
-#ifndef SV_K1G_LAG
-#define SV_K1G_LAG 1
-#endif
-#ifndef SV_K1G_POLY
-#define SV_K1G_POLY 0
-#endif
-constexpr int kGrpConsumers = 16;
-constexpr int kGrpSU = kGrpConsumers * 32;  // 16-byte units per tensor per stage
-constexpr int kGrpStages = SV_K1G_STAGES;
-constexpr int kGrpLag = SV_K1G_LAG;
-constexpr int kGrpSlots = 4;
-constexpr int kGrpPoly = SV_K1G_POLY;
-constexpr int kGrpThreads = (kGrpConsumers + 4) * 32;
-static_assert(kGrpSlots >= kGrpLag + 2, "K1g: a slot lives from a row's pass 1 to its epilogue");
 constexpr int kScoreThreads = 256;
 constexpr int kScoreMinBlocks = SV_K1_MINB;
 constexpr int kScoreGroup = SV_K1_GROUP;
@@ -123,10 +100,7 @@ struct ScoreArgs {
   float *spart;     // workspace: [B k cs] S partials
   uint32_t *cnt;    // workspace: [B k][2] P1 / P2 counters, zero between calls (self-cleaning)
   uint32_t *ticket; // workspace: K1's task counter, zero between calls (self-cleaning)
-  int grp;          // 1: K1g (rows 16-byte aligned, cs <= 32)
 };
-bool score_grp_ok(const void *d, const void *c, int64_t d_sb, int64_t d_si, int64_t c_sb, int64_t c_si, int64_t V,
-                  int elem_bytes, int cs);
 // sv_score's share of the workspace (offset 0); sd_verify's follows it
 int64_t score_ws_bytes(int64_t rows, int cs);
 cudaError_t launch_score(const ScoreArgs &a, cudaStream_t st);

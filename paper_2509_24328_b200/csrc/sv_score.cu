@@ -771,336 +771,8 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constan
   p2_finish_tail<T, NW>(a, c.k, sm);
 }
 
-// ---------------------------------------------------------------- K1g: grouped, interleaved
-// Rows keep K1's chunks (cs per row, score_splits_for).  A GROUP of cs persistent CTAs (one per
-// SM) owns rows g, g + NG, g + 2 NG, ...; member m always takes chunk m.  Step n of a CTA streams
-// pass 1 of its chunk of row(n) (HBM) and pass 2 of its chunk of row(n - kGrpLag) (the L2 re-read
-// of data it read kGrpLag steps earlier) INTERLEAVED stage by stage through one shared-memory
-// ring (1-D bulk copies), so every stage mixes the HBM stream with the L2 stream and the MUFU
-// load stays even (DESIGN §5 K1g).  Roles (control warps on the highest warp ids: the warp
-// arbiter picks the highest eligible id first, so consumers never starve them):
-//   warps 0..15 (consumers): lane l of warp w owns unit w*32 + l of every stage: pass 1 (2 MUFU.EX2
-//     per pair) or pass 2 (1 exp per pair, with the row's Lambda); warp partials -> slot;
-//   warp 16 (producer): the ring;
-//   warp 17 (Lambda): waits for the row's cs chunk partials, merges them (the same bits in every
-//     member), kGrpLag steps ahead of the pass-2 stages;
-//   warp 18 (P1 publish): merges the 16 warp partials, publishes the chunk's partial (release);
-//   warp 19 (S publish): sums the warp S, publishes; the row's last S partial runs the epilogue.
-// The lane -> unit mapping depends on (V, dtype) only: every output bit is independent of B, the
-// grid and the GPU count (but differs from K1's, which maps units to threads differently).
-struct GrpHdr {
-  int32_t n, sit, nu, flags;  // step, stage in chunk, units (< 0: end), 1 = pass 2, 2 = last stage
-};
-struct GrpSmem {
-  uint4 buf[kGrpStages][2][kGrpSU];
-  GrpHdr hdr[kGrpStages];
-  double wpart[kGrpSlots][kGrpConsumers][5];
-  float wsum[kGrpSlots][kGrpConsumers];
-  double glob[kGrpSlots][5];
-  float lam[kGrpSlots][2];
-  double pglob[5];
-  float plam[2];
-  uint64_t full[kGrpStages], empty[kGrpStages];
-  uint64_t parts1[kGrpSlots], pfree1[kGrpSlots], lamb[kGrpSlots], parts2[kGrpSlots], gfree[kGrpSlots];
-};
-
-struct GrpPlace {
-  uint32_t g, m, ng, rows, nrows;  // group, member, groups, rows, this CTA's rows
-  __device__ __forceinline__ uint32_t row(uint32_t j) const { return g + j * ng; }
-};
-__device__ __forceinline__ GrpPlace grp_place(const ScoreArgs &a) {
-  GrpPlace p;
-  p.m = blockIdx.x % (uint32_t)a.cs;
-  p.g = blockIdx.x / (uint32_t)a.cs;
-  p.ng = gridDim.x / (uint32_t)a.cs;
-  p.rows = (uint32_t)a.B * (uint32_t)a.k;
-  p.nrows = p.g < p.rows ? (p.rows - p.g + p.ng - 1) / p.ng : 0;
-  return p;
-}
-template <typename T>
-__device__ __forceinline__ Chunk<T> grp_chunk(const ScoreArgs &a, uint32_t row, uint32_t m) {
-  const uint32_t b = row / (uint32_t)a.k, i = row - b * (uint32_t)a.k;
-  return chunk_of<T>(a, b, i, (int)m);  // K1g rows: 16-byte aligned, whole units
-}
-__device__ __forceinline__ int grp_stages(int units) { return max(1, (units + kGrpSU - 1) / kGrpSU); }
-
-// Merge of np <= 32 partials by a fixed xor butterfly (every lane gets the same bits; one load
-// round trip); lane 0 writes glob / lam.
-template <typename PartFn, bool kGlobal>
-__device__ __forceinline__ void merge_bfly(const ScoreArgs &a, int np, PartFn part_of, double (&glob)[5],
-                                           float (&lam)[2]) {
-  auto ld = [](const double *p) { return kGlobal ? __ldcg(p) : *p; };
-  const int lane = threadIdx.x & 31;
-  const float cd = a.cd, cc = a.cc;
-  double pr[5] = {kMFloor, 0.0, kMFloor, 0.0, 0.0};
-  if (lane < np) {
-    const double *part = part_of(lane);
-#pragma unroll
-    for (int j = 0; j < 5; ++j) pr[j] = ld(part + j);
-  }
-  const float rmd = (float)pr[0], rmc = (float)pr[2];
-  const float GMd = warp_max(rmd), GMc = warp_max(rmc);
-  const float sdf = ex2((rmd - GMd) * cd), scf = ex2((rmc - GMc) * cc);
-  const float delta = (GMc - rmc) * cc - (GMd - rmd) * cd;
-  double ww = pr[4];
-  if (pr[1] > 0.0) ww += pr[1] * (double)delta;
-  const double L_d = warp_sum_d(pr[1] * sdf), L_c = warp_sum_d(pr[3] * scf), W = warp_sum_d(ww * sdf);
-  if (lane == 0) {
-    glob[0] = GMd;
-    glob[1] = L_d;
-    glob[2] = GMc;
-    glob[3] = L_c;
-    glob[4] = W;
-    const bool ok = L_d > 0.0 && L_c > 0.0 && L_d < 1e300 && L_c < 1e300 && GMd < FLT_MAX && GMc < FLT_MAX;
-    lam[0] = ok ? (float)((double)GMd * cd + log2_acc(L_d)) : __int_as_float(0x7fc00000);
-    lam[1] = ok ? (float)((double)GMc * cc + log2_acc(L_c)) : __int_as_float(0x7fc00000);
-  }
-}
-
-template <typename T>
-__device__ void grp_producer(const ScoreArgs &a, GrpSmem &sm) {
-  constexpr int EPU = Elem<T>::kPerUnit;
-  if ((threadIdx.x & 31) != 0) return;
-  const GrpPlace pl = grp_place(a);
-  const uint64_t pol1 = l2_policy_evict_last(), pol2 = l2_policy_evict_first();
-  uint32_t it = 0;
-  auto push = [&](uint32_t n, int sit, int nst, const Chunk<T> &ch, bool p2) {
-    const int q = it % kGrpStages;
-    mbar_wait_bounded(&sm.empty[q], ((it / kGrpStages) & 1) ^ 1);
-    const int u0 = sit * kGrpSU, nu = max(0, min(kGrpSU, ch.units - u0));
-    sm.hdr[q] = GrpHdr{(int32_t)n, sit, nu, (p2 ? 1 : 0) | (sit == nst - 1 ? 2 : 0)};
-    mbar_arrive_expect_tx(&sm.full[q], 2u * (uint32_t)nu * 16u);
-    if (nu > 0) {
-      bulk_g2s(sm.buf[q][0], ch.d + (size_t)u0 * EPU, (uint32_t)nu * 16u, &sm.full[q], p2 ? pol2 : pol1);
-      bulk_g2s(sm.buf[q][1], ch.c + (size_t)u0 * EPU, (uint32_t)nu * 16u, &sm.full[q], p2 ? pol2 : pol1);
-    }
-    ++it;
-  };
-  for (uint32_t n = 0; n < pl.nrows + kGrpLag; ++n) {
-    const bool h1 = n < pl.nrows, h2 = n >= (uint32_t)kGrpLag;
-    const Chunk<T> c1 = grp_chunk<T>(a, pl.row(h1 ? n : 0), pl.m);
-    const Chunk<T> c2 = grp_chunk<T>(a, pl.row(h2 ? n - kGrpLag : 0), pl.m);
-    const int nst = grp_stages((h1 ? c1 : c2).units);  // every chunk of this member: the same stages
-    for (int s = 0; s < nst; ++s) {
-      if (h1) push(n, s, nst, c1, false);
-      if (h2) push(n - kGrpLag, s, nst, c2, true);
-    }
-  }
-  {  // end marker (every consumer reads every stage)
-    const int q = it % kGrpStages;
-    mbar_wait_bounded(&sm.empty[q], ((it / kGrpStages) & 1) ^ 1);
-    sm.hdr[q] = GrpHdr{0, 0, -1, 0};
-    mbar_arrive(&sm.full[q]);
-  }
-}
-
-template <typename T>
-__device__ void grp_lambda(const ScoreArgs &a, GrpSmem &sm) {
-  const int lane = threadIdx.x & 31, cs = a.cs;
-  const GrpPlace pl = grp_place(a);
-  for (uint32_t j = 0; j < pl.nrows; ++j) {
-    const int q = j % kGrpSlots;
-    const uint32_t row = pl.row(j);
-    mbar_wait_bounded(&sm.gfree[q], ((j / kGrpSlots) & 1) ^ 1);  // row j - slots's epilogue is done
-    wait_count(a.cnt + 2 * (size_t)row, (uint32_t)cs);               // every lane acquires
-    auto pf = [&](int jj) { return (const double *)(a.part + ((size_t)row * cs + jj) * 5); };
-    merge_bfly<decltype(pf), true>(a, cs, pf, sm.glob[q], sm.lam[q]);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.lamb[q]);
-  }
-}
-
-template <typename T>
-__device__ void grp_publish1(const ScoreArgs &a, GrpSmem &sm) {
-  const int lane = threadIdx.x & 31, cs = a.cs;
-  const GrpPlace pl = grp_place(a);
-  for (uint32_t j = 0; j < pl.nrows; ++j) {
-    const int q = j % kGrpSlots;
-    const uint32_t row = pl.row(j);
-    mbar_wait_bounded(&sm.parts1[q], (j / kGrpSlots) & 1);
-    auto wp = [&](int w) { return (const double *)sm.wpart[q][w]; };
-    merge_bfly<decltype(wp), false>(a, kGrpConsumers, wp, sm.pglob, sm.plam);
-    __syncwarp();
-    if (lane == 0) {
-      double *part = a.part + ((size_t)row * cs + pl.m) * 5;
-#pragma unroll
-      for (int jj = 0; jj < 5; ++jj) part[jj] = sm.pglob[jj];
-      red_release_add(a.cnt + 2 * (size_t)row, 1u);
-      mbar_arrive(&sm.pfree1[q]);
-    }
-  }
-}
-
-template <typename T>
-__device__ void grp_publish2(const ScoreArgs &a, GrpSmem &sm) {
-  const int lane = threadIdx.x & 31, cs = a.cs;
-  const GrpPlace pl = grp_place(a);
-  for (uint32_t j = 0; j < pl.nrows; ++j) {
-    const int q = j % kGrpSlots;
-    const uint32_t row = pl.row(j);
-    mbar_wait_bounded(&sm.parts2[q], (j / kGrpSlots) & 1);
-    uint32_t *cnt = a.cnt + 2 * (size_t)row;
-    float *srow = a.spart + (size_t)row * cs;
-    uint32_t old = 0;
-    if (lane == 0) {
-      float r = sm.wsum[q][0];
-      for (int w = 1; w < kGrpConsumers; ++w) r += sm.wsum[q][w];
-      srow[pl.m] = r;
-      old = atom_add_acq_rel(cnt + 1, 1u);  // releases this S partial, acquires the others
-    }
-    old = __shfl_sync(0xffffffffu, old, 0);
-    if (old == (uint32_t)(cs - 1)) {  // the row's last S partial: epilogue, re-arm the counters
-      __syncwarp();
-      fence_acq_rel();
-      const uint32_t b = row / (uint32_t)a.k, i = row - b * (uint32_t)a.k;
-      epilogue<T>(a, b, i, sm.glob[q], srow, cs, 1, 0, nullptr, 0);
-      if (lane == 0) {
-        cnt[0] = 0u;  // every member's Lambda warp has read it (its pass 2 is done)
-        cnt[1] = 0u;
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.gfree[q]);
-  }
-}
-
-// Exact pass 1 over one consumer lane's units of a chunk (global memory; the fallback of a lane
-// whose fast sums are not finite).
-template <typename T>
-__device__ __noinline__ P1Out grp_exact(const ScoreArgs &a, uint32_t row, uint32_t m, int ubase) {
-  constexpr int EPU = Elem<T>::kPerUnit;
-  const Chunk<T> ch = grp_chunk<T>(a, row, m);
-  P1State s{kMFloor, kMFloor, kMFloor, kMFloor, 0.f, 0.f, 0.f};
-  for (int u = ubase; u < ch.units; u += kGrpSU)
-    exact_unit<T>(s, ldg_stream(ch.d + (size_t)u * EPU), ldg_stream(ch.c + (size_t)u * EPU), a.cd, a.cc);
-  return P1Out{s.rd, s.rc, s.ld, s.lc, s.w};
-}
-
-template <typename T>
-__device__ void grp_consumer(const ScoreArgs &a, GrpSmem &sm, int cw) {
-  const int lane = threadIdx.x & 31, ubase = cw * 32 + lane;
-  const GrpPlace pl = grp_place(a);
-  const float cd = a.cd, cc = a.cc;
-  const f2 cdd{cd, cd}, ccc{cc, cc};
-  P1Fast t{kMFloor, kMFloor, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
-  f2 nrd{0.f, 0.f}, nrc{0.f, 0.f}, acc{0.f, 0.f}, nld{0.f, 0.f}, nlc{0.f, 0.f};
-  bool first = true, skip = false;
-  for (uint32_t it = 0;; ++it) {
-    const int q = it % kGrpStages;
-    mbar_wait_bounded(&sm.full[q], (it / kGrpStages) & 1);
-    const GrpHdr h = sm.hdr[q];
-    if (h.nu < 0) return;
-    const bool p2 = h.flags & 1;
-    const bool ok = ubase < h.nu;
-    uint4 d1[1], c1[1];
-    if (ok) {
-      d1[0] = sm.buf[q][0][ubase];
-      c1[0] = sm.buf[q][1][ubase];
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[q]);  // the stage's data is in registers
-    const int slot = h.n % kGrpSlots;
-    if (!p2) {
-      if (h.sit == 0) {
-        t = P1Fast{kMFloor, kMFloor, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
-        first = true;
-      }
-      if (ok) {
-        if (first) {
-          fast_ref<T, 1>(t, d1, c1);
-          nrd = f2{-(t.rd * cd), -(t.rd * cd)};
-          nrc = f2{-(t.rc * cc), -(t.rc * cc)};
-          first = false;
-        }
-        fast_group<T, 1>(t, d1, c1, cdd, ccc, nrd, nrc);
-      }
-      if (h.flags & 2) {  // the chunk's last stage: the warp's pass-1 partial -> slot
-        const float ld = t.ld.x + t.ld.y, lc = t.lc.x + t.lc.y, w = t.w.x + t.w.y;
-        P1Out o{t.rd, t.rc, ld, lc, w};
-        if (!(ld < 1e36f && lc < 1e36f && w == w && fabsf(w) < 1e36f)) o = grp_exact<T>(a, pl.row(h.n), pl.m, ubase);
-        mbar_wait_bounded(&sm.pfree1[slot], ((h.n / kGrpSlots) & 1) ^ 1);
-        warp_p1_partial(o, cd, cc, sm.wpart[slot][cw]);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.parts1[slot]);
-      }
-    } else {
-      if (h.sit == 0) {
-        mbar_wait_bounded(&sm.lamb[slot], (h.n / kGrpSlots) & 1);
-        const float lamd = sm.lam[slot][0], lamc = sm.lam[slot][1];
-        skip = !(lamd == lamd && lamc == lamc);
-        nld = f2{-lamd, -lamd};
-        nlc = f2{-lamc, -lamc};
-        acc = f2{0.f, 0.f};
-      }
-      if (ok && !skip) p2_group<T, 1, kGrpPoly>(acc, d1, c1, cdd, ccc, nld, nlc);
-      if (h.flags & 2) {
-        const float sw = warp_sum(acc.x + acc.y);
-        if (lane == 0) {
-          sm.wsum[slot][cw] = sw;
-          mbar_arrive(&sm.parts2[slot]);
-        }
-      }
-    }
-  }
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kGrpThreads, 1) sv_score_grp_kernel(const __grid_constant__ ScoreArgs a) {
-  extern __shared__ __align__(128) uint8_t grp_raw[];
-  GrpSmem &sm = *reinterpret_cast<GrpSmem *>(grp_raw);
-  const int wid = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-    for (int q = 0; q < kGrpStages; ++q) {
-      mbar_init(&sm.full[q], 1);
-      mbar_init(&sm.empty[q], kGrpConsumers);
-    }
-    for (int q = 0; q < kGrpSlots; ++q) {
-      mbar_init(&sm.parts1[q], kGrpConsumers);
-      mbar_init(&sm.pfree1[q], 1);
-      mbar_init(&sm.lamb[q], 1);
-      mbar_init(&sm.parts2[q], kGrpConsumers);
-      mbar_init(&sm.gfree[q], 1);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  pdl_wait();
-  pdl_trigger();
-  if (wid < kGrpConsumers)
-    grp_consumer<T>(a, sm, wid);
-  else if (wid == kGrpConsumers)
-    grp_producer<T>(a, sm);
-  else if (wid == kGrpConsumers + 1)
-    grp_lambda<T>(a, sm);
-  else if (wid == kGrpConsumers + 2)
-    grp_publish1<T>(a, sm);
-  else
-    grp_publish2<T>(a, sm);
-}
-
-// Grid: whole groups of cs CTAs, one CTA per SM (members wait on each other: co-resident), at
-// most one group per row.  0 when not even one group fits (the caller then uses K1).
-template <typename T>
-int score_grp_grid(const ScoreArgs &a) {
-  const int smem = (int)sizeof(GrpSmem);
-  if (cudaFuncSetAttribute(sv_score_grp_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
-    cudaGetLastError();
-    return 0;
-  }
-  const int64_t rows = (int64_t)a.B * a.k;
-  int64_t groups = resident_grid((const void *)sv_score_grp_kernel<T>, kGrpThreads, smem) / a.cs;
-  if (groups > rows) groups = rows;
-  return (int)(groups * a.cs);
-}
-
 template <typename T>
 cudaError_t launch_score_t(const ScoreArgs &a, cudaStream_t st) {
-  if ((int64_t)a.B * a.k == 0) return cudaSuccess;
-  if (a.grp) {
-    const int grid = score_grp_grid<T>(a);
-    if (grid > 0)
-      return launch_k(sv_score_grp_kernel<T>, dim3((unsigned)grid), dim3(kGrpThreads), sizeof(GrpSmem), st, a);
-  }
   if ((int64_t)a.B * a.k == 0) return cudaSuccess;
   const int64_t tasks = (SV_K1_SAMECTA ? 1 : 2) * (int64_t)a.B * a.k * a.cs;
   if (tasks == 0) return cudaSuccess;
