@@ -153,13 +153,26 @@ void run(const uint8_t *d, const uint8_t *c, size_t bytes, float *out, int cps, 
          2.0 * bytes / (ms * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
 }
 int main() {
-  const size_t bytes = (size_t)80 * 8 * 152064 * 2;  // one tensor
+  // PAT 0: blocks round robin over CTAs; 1: K1's layout (37 groups x 4 CTAs, chunk m of each row);
+  // 2: two passes in chunk blocks (P1 chunk j, then P2 chunk j - 1 re-read from L2);
+  // 3: two passes interleaved stage by stage.  MATH 0: LDS only; 1: pass-1 math (2 ex2 per
+  // pair + KL); 2: one pass with all 3 ex2 per pair; 3: pass-1 math on P1 stages, pass-2 math
+  // on P2 stages; 5: warp-owned stages (LDS only).  grid = CTAs (1 per SM).
+  const size_t bytes = (size_t)80 * 8 * 152064 * 2;  // one tensor (D or C) at the headline
   uint8_t *d, *c; float *out;
   cudaMalloc(&d, bytes); cudaMalloc(&c, bytes); cudaMalloc(&out, 4);
   cudaMemset(d, 0x3c, bytes); cudaMemset(c, 0x3d, bytes);
-  run<4, 32, 2048, 0, 0>(d, c, bytes, out, 1);
-  run<16, 32, 2048, 5, 0>(d, c, bytes, out, 1);
-  run<16, 16, 4096, 5, 0>(d, c, bytes, out, 1);
-  run<8, 16, 4096, 5, 0>(d, c, bytes, out, 1);
+  run<8, 6, 8192, 0, 0>(d, c, bytes, out, 1);      // bulk-copy stream of D + C
+  run<16, 6, 16384, 0, 0>(d, c, bytes, out, 1);
+  run<8, 6, 8192, 0, 1>(d, c, bytes, out, 1);
+  run<8, 12, 8192, 0, 0>(d, c, bytes, out, 1, 80);  // 80 SMs
+  run<8, 12, 8192, 0, 0>(d, c, bytes, out, 1, 40);  // 40 SMs
+  run<16, 6, 16384, 1, 1>(d, c, bytes, out, 1);     // + pass-1 math
+  run<10, 6, 10240, 1, 1>(d, c, bytes, out, 1);
+  run<16, 6, 16384, 2, 1>(d, c, bytes, out, 1);     // one pass, 3 ex2 per pair
+  run<16, 6, 16384, 0, 3>(d, c, bytes, out, 1);     // two passes (HBM + L2), no math
+  run<16, 6, 16384, 3, 2>(d, c, bytes, out, 1);     // two passes in chunk blocks
+  run<16, 6, 16384, 3, 3>(d, c, bytes, out, 1);     // two passes interleaved by stage
+  run<16, 16, 4096, 5, 0>(d, c, bytes, out, 1);     // warp-owned stages
   return 0;
 }
