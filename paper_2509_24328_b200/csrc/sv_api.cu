@@ -211,11 +211,12 @@ const char *sv_status_string(int32_t s) {
   }
 }
 
-static int32_t score_impl(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok, int32_t B,
-                          int32_t k, int32_t V, float tau_d, float tau_c, const sv_profile *prof, float *S, float *A,
-                          float *KL, float *p_hat, float *draft_m, float *draft_l, float *draft_ptok,
-                          int32_t *row_status, void *workspace, size_t workspace_bytes, void *stream,
-                          const ScheduleArgs *sch) {
+// sv_score's validation and launch geometry (SV_OK with a.B == 0: nothing to do)
+static int32_t score_setup(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok, int32_t B,
+                           int32_t k, int32_t V, float tau_d, float tau_c, const sv_profile *prof, float *S, float *A,
+                           float *KL, float *p_hat, float *draft_m, float *draft_l, float *draft_ptok,
+                           int32_t *row_status, void *workspace, size_t workspace_bytes, ScoreArgs &a) {
+  a = ScoreArgs{};
   if (!draft) return SV_ERR_INVALID_ARG;
   int32_t r = shape_check(B, k, V, draft->dtype);
   if (r != SV_OK) return r;
@@ -228,7 +229,7 @@ static int32_t score_impl(const sv_logits *draft, const sv_logits *comp, const i
   if (B == 0) return SV_OK;
   if (!workspace || workspace_bytes < sv_workspace_bytes(B, k, V, draft->dtype)) return SV_ERR_WORKSPACE;
   if ((reinterpret_cast<uintptr_t>(workspace) & 15) != 0) return SV_ERR_INVALID_ARG;
-  ScoreArgs a = make_score_args(draft, comp, draft_tok, B, k, V, tau_d, tau_c, prof, S, A, KL, p_hat, draft_m, draft_l,
+  a = make_score_args(draft, comp, draft_tok, B, k, V, tau_d, tau_c, prof, S, A, KL, p_hat, draft_m, draft_l,
                                 draft_ptok, row_status, draft->dtype, V);
   const int64_t rows = (int64_t)B * k;
   if (2 * rows * a.cs > INT32_MAX) return SV_ERR_UNSUPPORTED;  // one CTA per chunk task
@@ -239,6 +240,18 @@ static int32_t score_impl(const sv_logits *draft, const sv_logits *comp, const i
   a.spart = reinterpret_cast<float *>(ws + ws_round(rows * a.cs * 5 * 8));
   a.cnt = reinterpret_cast<uint32_t *>(ws + ws_round(rows * a.cs * 5 * 8) + ws_round(rows * a.cs * 4));
   a.ticket = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(a.cnt) + ws_round(rows * 2 * 4));
+  return SV_OK;
+}
+
+static int32_t score_impl(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok, int32_t B,
+                          int32_t k, int32_t V, float tau_d, float tau_c, const sv_profile *prof, float *S, float *A,
+                          float *KL, float *p_hat, float *draft_m, float *draft_l, float *draft_ptok,
+                          int32_t *row_status, void *workspace, size_t workspace_bytes, void *stream,
+                          const ScheduleArgs *sch) {
+  ScoreArgs a;
+  const int32_t r = score_setup(draft, comp, draft_tok, B, k, V, tau_d, tau_c, prof, S, A, KL, p_hat, draft_m, draft_l,
+                                draft_ptok, row_status, workspace, workspace_bytes, a);
+  if (r != SV_OK || B == 0) return r;
   cudaError_t e = launch_score(a, (cudaStream_t)stream);
   if (e == cudaSuccess && sch) e = launch_schedule(*sch, (cudaStream_t)stream);  // sv_score_schedule
   if (e != cudaSuccess) {
@@ -367,6 +380,48 @@ int32_t sd_verify_ragged(const sv_logits *draft, const void *target, int64_t tar
   const cudaError_t e = launch_verify(a, (cudaStream_t)stream);
   if (e != cudaSuccess) {
     fprintf(stderr, "libsv: sd_verify_ragged launch failed: %s\n", cudaGetErrorString(e));
+    return SV_ERR_CUDA;
+  }
+  return SV_OK;
+}
+
+int32_t sv_step(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok, const void *target,
+                int64_t target_row_stride, const int64_t *target_rowptr, int32_t B, int32_t k, int32_t V, float tau_d,
+                float tau_c, float tau_t, const sv_profile *prof, const double *latency, int32_t n_lat,
+                int32_t plus_one, uint64_t seed, uint64_t offset, const uint64_t *offset_dev, int64_t seq_base,
+                float *S, float *A, float *KL, float *p_hat, float *draft_m, float *draft_l, float *draft_ptok,
+                int32_t *row_status, int32_t *gamma, float *exp_accept, float *goodput, int32_t *sched_status,
+                int32_t *n_accept, int32_t *out_tok, float *accept_ratio, float *resid_mass, int32_t *seq_status,
+                void *workspace, size_t workspace_bytes, void *stream) {
+  if (!p_hat || !latency || !gamma || n_lat < k + 2 || k < 1 || k > SV_MAX_K) return SV_ERR_INVALID_ARG;
+  if (!draft || !target || !target_rowptr || target_row_stride < V || !n_accept || !out_tok) return SV_ERR_INVALID_ARG;
+  if (!(tau_t > 0.f) || seq_base < 0) return SV_ERR_INVALID_ARG;
+  if (k > kStepMaxK || (int64_t)B * k > kStepMaxRows) return SV_ERR_UNSUPPORTED;
+  ScoreArgs sa;
+  int32_t r = score_setup(draft, comp, draft_tok, B, k, V, tau_d, tau_c, prof, S, A, KL, p_hat, draft_m, draft_l,
+                          draft_ptok, row_status, workspace, workspace_bytes, sa);
+  if (r != SV_OK || B == 0) return r;
+  ScheduleArgs ha = {};
+  ha.p_hat = p_hat;
+  ha.B = B;
+  ha.k = k;
+  ha.L = latency;
+  ha.n_lat = n_lat;
+  ha.mode = SV_SCHED_PER_ROW;
+  ha.plus_one = plus_one ? 1 : 0;
+  ha.gamma = gamma;
+  ha.exp_accept = exp_accept;
+  ha.goodput = goodput;
+  ha.status = sched_status;
+  const sv_logits tl = {target, draft->dtype, 0, 0, target_row_stride};
+  VerifyArgs va = make_verify_args(draft, &tl, draft_tok, gamma, draft_m, draft_l, draft_ptok, B, k, V, tau_d, tau_t,
+                                   seed, offset, seq_base, n_accept, out_tok, accept_ratio, resid_mass, seq_status,
+                                   workspace, V);
+  va.t_rowptr = target_rowptr;
+  va.offset_dev = offset_dev;
+  const cudaError_t e = launch_step(sa, ha, va, (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "libsv: sv_step launch failed: %s\n", cudaGetErrorString(e));
     return SV_ERR_CUDA;
   }
   return SV_OK;
