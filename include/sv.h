@@ -231,29 +231,6 @@ SV_API int32_t sd_verify_ragged(const sv_logits *draft, const void *target, int6
                                 size_t workspace_bytes, void *stream);
 
 /*
- * sv_step -- the whole step (sv_score -> sv_schedule PER_ROW -> sd_verify_ragged; steps a1-a6,
- * P L159-266, S L148-165, L384-401) in ONE launch: one thread-block cluster of k CTAs per
- * sequence, the phases separated by cluster barriers (DESIGN §5 "fused small-batch step").
- * Arguments: those of sv_score (p_hat non-NULL), of sv_schedule (latency [n_lat] fp64,
- * n_lat >= k + 2, plus_one, gamma / exp_accept / goodput / sched_status [B]) and of
- * sd_verify_ragged (target rows at target + (target_rowptr[b] + i) * target_row_stride for
- * i <= gamma_b, tau_t, seed / offset / offset_dev, seq_base, n_accept / out_tok / accept_ratio /
- * resid_mass / seq_status [B]).  Every output is bit-identical to the three calls on the same
- * inputs (the same device code runs each phase).  Same workspace as sv_score / sd_verify.
- * Supported: 1 <= k <= 16 and B * k <= 512 (a latency path for small and mid batches; larger
- * batches keep the separate kernels) -- SV_ERR_UNSUPPORTED otherwise, with nothing launched.
- */
-SV_API int32_t sv_step(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok, const void *target,
-                       int64_t target_row_stride, const int64_t *target_rowptr, int32_t B, int32_t k, int32_t V,
-                       float tau_d, float tau_c, float tau_t, const sv_profile *prof, const double *latency,
-                       int32_t n_lat, int32_t plus_one, uint64_t seed, uint64_t offset, const uint64_t *offset_dev,
-                       int64_t seq_base, float *S, float *A, float *KL, float *p_hat, float *draft_m, float *draft_l,
-                       float *draft_ptok, int32_t *row_status, int32_t *gamma, float *exp_accept, float *goodput,
-                       int32_t *sched_status, int32_t *n_accept, int32_t *out_tok, float *accept_ratio,
-                       float *resid_mass, int32_t *seq_status, void *workspace, size_t workspace_bytes,
-                       void *stream);
-
-/*
  * Sampling filters (NEXT-2): temperature -> top_k -> top_p -> renormalise, applied to the
  * draft, companion AND target distributions before S / A and the accept test (S L73-81, L183,
  * L238; P L731-743 Table 5: Qwen top_k 20, top_p 0.8, tau 0.7).  Readings (DESIGN R21): top_k

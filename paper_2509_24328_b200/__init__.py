@@ -18,7 +18,7 @@ from . import _lib
 from ._lib import (ROW_ALL_NEG_INF, ROW_BAD_GAMMA, ROW_BAD_LATENCY, ROW_BAD_TOKEN, ROW_DRAFT_ZERO,  # noqa: F401
                    ROW_NAN, ROW_PHAT_BAD, ROW_RESID_ZERO, SV_SCHED_BATCH_GREEDY, SV_SCHED_PER_ROW, SvError)
 
-__all__ = ["sv_score", "sv_score_schedule", "sv_schedule", "sd_verify", "sd_verify_ragged", "sv_step", "workspace_bytes", "Profile",
+__all__ = ["sv_score", "sv_score_schedule", "sv_schedule", "sd_verify", "sd_verify_ragged", "workspace_bytes", "Profile",
            "Pipeline", "GraphPipeline", "sv_profile_build", "sv_score_filtered", "sd_verify_filtered", "load_library"]
 
 
@@ -251,50 +251,6 @@ def sd_verify_ragged(D, T_rows, t_rowptr, tok, gamma, draft_m, draft_l, draft_pt
     return res
 
 
-def sv_step(D, C, T_rows, t_rowptr, tok, latency, profile: Profile, tau=(1.0, 1.0, 1.0), plus_one=1, seed=0,
-            offset=0, offset_dev=None, seq_base=0, workspace=None, score_out=None, sched_out=None, out=None,
-            stream=None):
-    """The whole step in one launch (C ABI `sv_step`: one thread-block cluster per sequence):
-    sv_score -> sv_schedule(PER_ROW) -> sd_verify_ragged, bit-identical to the three calls.
-    Returns (score, schedule, verify) dicts, or None when the library declines the shape
-    (k > 16 or B k > 512; nothing is launched) -- then use the three calls."""
-    B, k, V = D.shape
-    dev = D.device
-    _same_logits(D, C, "C", (B, k, V))
-    _req(tok, "tok", torch.int32, (B, k), dev)
-    _req(latency, "latency", torch.float64, (latency.numel(),), dev)
-    if T_rows.dim() != 2 or T_rows.stride(1) != 1 or T_rows.dtype != D.dtype or T_rows.shape[1] != V:
-        raise SvError("ragged target must be [rows, V] with the vocabulary contiguous and the draft's dtype")
-    _req(t_rowptr, "t_rowptr", torch.int64, (B,), dev)
-    if offset_dev is not None and (offset_dev.dtype not in (torch.int64, torch.uint64) or offset_dev.numel() != 1):
-        raise SvError("offset_dev must be a one-element int64 / uint64 CUDA tensor")
-    if workspace is None:
-        workspace = new_workspace(B, k, V, D.dtype, dev)
-    o = score_out or {}
-    sc = {n: _out(o, n, (B, k), torch.float32, dev) for n in ("S", "A", "KL", "p_hat", "draft_m", "draft_l",
-                                                                "draft_ptok")}
-    sc["status"] = _out(o, "status", (B, k), torch.int32, dev)
-    so = sched_out or {}
-    sh = {"gamma": _out(so, "gamma", (B,), torch.int32, dev),
-          "exp_accept": _out(so, "exp_accept", (B,), torch.float32, dev),
-          "goodput": _out(so, "goodput", (B,), torch.float32, dev),
-          "status": _out(so, "status", (B,), torch.int32, dev)}
-    ver = _verify_out(out or {}, B, k, dev)
-    st = _lib.load().sv_step(
-        ctypes.byref(_logits(D)), ctypes.byref(_logits(C)), _ptr(tok), T_rows.data_ptr(), T_rows.stride(0),
-        _ptr(t_rowptr), B, k, V, float(tau[0]), float(tau[1]), float(tau[2]), ctypes.byref(profile.c),
-        _ptr(latency), latency.numel(), int(plus_one), ctypes.c_uint64(seed), ctypes.c_uint64(offset),
-        _ptr(offset_dev), int(seq_base), _ptr(sc["S"]), _ptr(sc["A"]), _ptr(sc["KL"]), _ptr(sc["p_hat"]),
-        _ptr(sc["draft_m"]), _ptr(sc["draft_l"]), _ptr(sc["draft_ptok"]), _ptr(sc["status"]), _ptr(sh["gamma"]),
-        _ptr(sh["exp_accept"]), _ptr(sh["goodput"]), _ptr(sh["status"]), _ptr(ver["n_accept"]), _ptr(ver["out_tok"]),
-        _ptr(ver["accept_ratio"]), _ptr(ver["resid_mass"]), _ptr(ver["status"]), workspace.data_ptr(),
-        workspace.numel(), _stream(stream))
-    if st == _lib.SV_ERR_UNSUPPORTED:
-        return None
-    _lib.check(st, "sv_step")
-    return sc, sh, ver
-
-
 def new_filter_workspace(B: int, k: int, device="cuda") -> torch.Tensor:
     return torch.empty(max(16, int(_lib.load().sv_filter_workspace_bytes(B, k))), dtype=torch.uint8, device=device)
 
@@ -381,11 +337,8 @@ class GraphPipeline:
     eager step with offset = offset0 + j."""
 
     def __init__(self, B, k, V, dtype, profile: Profile, latency: torch.Tensor, tau=(1.0, 1.0, 1.0),
-                 mode=SV_SCHED_PER_ROW, device="cuda", seed=0, offset0=0, seq_base=0, use_step=False):
+                 mode=SV_SCHED_PER_ROW, device="cuda", seed=0, offset0=0, seq_base=0):
         self.pipe = Pipeline(B, k, V, dtype, profile, latency, tau, mode, device)
-        # sv_step (one cluster launch per step) where the library takes the shape (B k <= 512,
-        # k <= 16); bit-identical to the three calls, which stay the path for larger batches
-        self.use_step = bool(use_step)
         self.B, self.k, self.V = B, k, V
         self.D = torch.empty((B, k, V), dtype=dtype, device=device)
         self.C = torch.empty((B, k, V), dtype=dtype, device=device)
@@ -398,14 +351,6 @@ class GraphPipeline:
 
     def _step(self, stream):
         p = self.pipe
-        if p.mode == SV_SCHED_PER_ROW and self.use_step:  # small / mid batches: one launch (sv_step)
-            r = sv_step(self.D, self.C, self.T.view(-1, self.V), self.rowptr, self.tok, p.latency, p.profile,
-                        (p.tau_d, p.tau_c, p.tau_t), 1, self.seed, 0, self.offset, self.seq_base,
-                        workspace=p.workspace, score_out=p.score_out, sched_out=p.sched_out, out=p.ver_out,
-                        stream=stream)
-            if r is not None:
-                self.offset.add_(1)
-                return r[2]
         if p.mode == SV_SCHED_PER_ROW and p.fused:
             sc, sh = sv_score_schedule(self.D, self.C, self.tok, p.latency, p.tau_d, p.tau_c, p.profile,
                                        workspace=p.workspace, out=p.score_out, sched_out=p.sched_out, stream=stream)

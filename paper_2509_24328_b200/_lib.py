@@ -73,9 +73,6 @@ def load(path: str = LIB_PATH):
     lib.sd_verify_ragged.argtypes = [LP, P, i64, P, P, P, P, P, P, i32, i32, i32, f32, f32, u64, u64, P, i64,
                                      P, P, P, P, P, P, sz, P]
     lib.sd_verify_ragged.restype = i32
-    lib.sv_step.argtypes = [LP, LP, P, P, i64, P, i32, i32, i32, f32, f32, f32, ctypes.POINTER(SvProfile), P, i32,
-                            i32, u64, u64, P, i64, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, sz, P]
-    lib.sv_step.restype = i32
     FP = ctypes.POINTER(SvFilter)
     lib.sv_filter_workspace_bytes.argtypes = [i32, i32]
     lib.sv_filter_workspace_bytes.restype = sz

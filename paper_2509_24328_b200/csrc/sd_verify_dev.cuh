@@ -1,7 +1,6 @@
 // sd_verify_dev.cuh -- the device code of K4..K5b (steps a5-a6): target-row partials, the row
-// merges and accept tests, residual slice masses, the token search.  Included by sd_verify.cu
-// (the verify kernels) and sv_step.cu (the fused small-batch step): the same operations in the
-// same order.
+// merges and accept tests, residual slice masses, the token search, as per-warp / per-sequence
+// device functions (included by sd_verify.cu, the verify kernels).
 #pragma once
 #include <float.h>
 

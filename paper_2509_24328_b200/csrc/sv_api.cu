@@ -385,48 +385,6 @@ int32_t sd_verify_ragged(const sv_logits *draft, const void *target, int64_t tar
   return SV_OK;
 }
 
-int32_t sv_step(const sv_logits *draft, const sv_logits *comp, const int32_t *draft_tok, const void *target,
-                int64_t target_row_stride, const int64_t *target_rowptr, int32_t B, int32_t k, int32_t V, float tau_d,
-                float tau_c, float tau_t, const sv_profile *prof, const double *latency, int32_t n_lat,
-                int32_t plus_one, uint64_t seed, uint64_t offset, const uint64_t *offset_dev, int64_t seq_base,
-                float *S, float *A, float *KL, float *p_hat, float *draft_m, float *draft_l, float *draft_ptok,
-                int32_t *row_status, int32_t *gamma, float *exp_accept, float *goodput, int32_t *sched_status,
-                int32_t *n_accept, int32_t *out_tok, float *accept_ratio, float *resid_mass, int32_t *seq_status,
-                void *workspace, size_t workspace_bytes, void *stream) {
-  if (!p_hat || !latency || !gamma || n_lat < k + 2 || k < 1 || k > SV_MAX_K) return SV_ERR_INVALID_ARG;
-  if (!draft || !target || !target_rowptr || target_row_stride < V || !n_accept || !out_tok) return SV_ERR_INVALID_ARG;
-  if (!(tau_t > 0.f) || seq_base < 0) return SV_ERR_INVALID_ARG;
-  if (k > kStepMaxK || (int64_t)B * k > kStepMaxRows) return SV_ERR_UNSUPPORTED;
-  ScoreArgs sa;
-  int32_t r = score_setup(draft, comp, draft_tok, B, k, V, tau_d, tau_c, prof, S, A, KL, p_hat, draft_m, draft_l,
-                          draft_ptok, row_status, workspace, workspace_bytes, sa);
-  if (r != SV_OK || B == 0) return r;
-  ScheduleArgs ha = {};
-  ha.p_hat = p_hat;
-  ha.B = B;
-  ha.k = k;
-  ha.L = latency;
-  ha.n_lat = n_lat;
-  ha.mode = SV_SCHED_PER_ROW;
-  ha.plus_one = plus_one ? 1 : 0;
-  ha.gamma = gamma;
-  ha.exp_accept = exp_accept;
-  ha.goodput = goodput;
-  ha.status = sched_status;
-  const sv_logits tl = {target, draft->dtype, 0, 0, target_row_stride};
-  VerifyArgs va = make_verify_args(draft, &tl, draft_tok, gamma, draft_m, draft_l, draft_ptok, B, k, V, tau_d, tau_t,
-                                   seed, offset, seq_base, n_accept, out_tok, accept_ratio, resid_mass, seq_status,
-                                   workspace, V);
-  va.t_rowptr = target_rowptr;
-  va.offset_dev = offset_dev;
-  const cudaError_t e = launch_step(sa, ha, va, (cudaStream_t)stream);
-  if (e != cudaSuccess) {
-    fprintf(stderr, "libsv: sv_step launch failed: %s\n", cudaGetErrorString(e));
-    return SV_ERR_CUDA;
-  }
-  return SV_OK;
-}
-
 // ------------------------------------------------------------------ NEXT-2 sampling filters
 size_t sv_filter_workspace_bytes(int32_t B, int32_t k) {
   if (B < 0 || k < 1 || k > SV_MAX_K) return 0;

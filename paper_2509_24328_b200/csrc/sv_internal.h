@@ -215,10 +215,6 @@ struct ProfileArgs {
 };
 cudaError_t launch_profile(const ProfileArgs &a, cudaStream_t st);
 cudaError_t launch_verify_stage(int stage, const VerifyArgs &a, cudaStream_t st);
-// the fused small-batch step (sv_step.cu): one cluster of k CTAs per sequence
-constexpr int kStepMaxK = 16;
-constexpr int kStepMaxCluster = 16;  // CTAs per cluster (non-portable above 8)
-constexpr int kStepMaxRows = 512;
-cudaError_t launch_step(const ScoreArgs &sa, const ScheduleArgs &ha, const VerifyArgs &va, cudaStream_t st);
+
 
 }  // namespace sv

@@ -1,6 +1,5 @@
 // sv_score_dev.cuh -- the device code of K1 (steps a1-a3): element arithmetic of both passes,
-// block / row merges, the row epilogue.  Included by sv_score.cu (the K1 kernels) and sv_step.cu
-// (the fused small-batch step), which therefore run the same operations in the same order.
+// block / row merges, the row epilogue (included by sv_score.cu, the K1 kernels).
 #pragma once
 #include <float.h>
 
