@@ -39,7 +39,10 @@ constexpr int kScorePoly = SV_K1_POLY;
 constexpr int kScoreChunkBytes = SV_K1_CHUNK_BYTES;  // target bytes of a chunk pair (D + C)
 constexpr int kScoreLag = SV_K1_LAG;    // rows between a chunk's P1 and P2 task (the L2 window)
 constexpr int kScoreMaxSplits = 64;     // chunks per row at most (co-residency of a row's CTAs)
-constexpr int kScoreMinSplits = 4;      // chunk tasks per row at least (a function of V only)
+#ifndef SV_K1_MINSPLITS
+#define SV_K1_MINSPLITS 4
+#endif
+constexpr int kScoreMinSplits = SV_K1_MINSPLITS;  // chunk tasks per row at least (a function of V only)
 constexpr int kScoreMaxChunkBytes = 1 << 30;      // (no on-chip residency: any chunk size)
 constexpr int kRowsThreads = 256;
 constexpr int kSampleThreads = 256;
