@@ -246,11 +246,26 @@ __device__ __forceinline__ SampleRow<T> sample_row(const VerifyArgs &a, const De
   return r;
 }
 
-// This lane's EPT contiguous elements of warp slice s: r_v (residual when kMode = 1, else p_t)
-// and, in vocabulary order, their fp64 sum (and the fp64 sum of p_t, the R10 fallback mass).
+// Sum of one 16-byte unit's values in a fixed fp32 tree (packed pairs, then the two halves).
+template <int EPU>
+__device__ __forceinline__ float unit_tree(const f2 (&v)[EPU / 2]) {
+  if constexpr (EPU == 8) {
+    const f2 s = add2(add2(v[0], v[1]), add2(v[2], v[3]));
+    return s.x + s.y;
+  } else {
+    const f2 s = add2(v[0], v[1]);
+    return s.x + s.y;
+  }
+}
+
+// This lane's EPT contiguous elements of warp slice s: r_v (residual when kMode = 1, else p_t),
+// one fp32 tree sum per 16-byte unit (u[q]; packed FFMA2 / FMUL2 / FADD2 arithmetic), and in
+// vocabulary order the fp64 sum of the unit sums (and the same for p_t, the R10 fallback mass).
+// K5 and K5b's recomputation of the owning slice call this with the same arguments, so the
+// unit sums are bit-identical in both.
 template <typename T, int kMode, bool kKeep>
-__device__ __forceinline__ void slice_lane(const VerifyArgs &a, const SampleRow<T> &sr, int64_t s, float *r,
-                                           double &sum, double &sum_t) {
+__device__ __forceinline__ bool slice_lane(const VerifyArgs &a, const SampleRow<T> &sr, int64_t s, float *r,
+                                           float *u, double &sum, double &sum_t) {
   constexpr int EPU = Elem<T>::kPerUnit, UPT = kSampleUnitsPerThread, EPT = UPT * EPU;
   const int lane = threadIdx.x & 31;
   const int64_t v0 = s * a.slice + (int64_t)lane * EPT;
@@ -268,21 +283,33 @@ __device__ __forceinline__ void slice_lane(const VerifyArgs &a, const SampleRow<
 #pragma unroll
       for (int q = 0; q < UPT; ++q) ud[q] = *reinterpret_cast<const uint4 *>(dp + q * EPU);
     }
+    const f2 ct{sr.ct, sr.ct}, nmt{sr.nmt, sr.nmt}, ilt{sr.ilt, sr.ilt};
+    const f2 cd{sr.cd, sr.cd}, nmd{sr.nmd, sr.nmd}, ild{sr.ild, sr.ild};
 #pragma unroll
     for (int q = 0; q < UPT; ++q) {
-      float xt[EPU], xd[EPU];
-      Elem<T>::unit(ut[q], xt);
-      if (kMode) Elem<T>::unit(ud[q], xd);
+      f2 xt[EPU / 2], xd[EPU / 2], pt[EPU / 2], v[EPU / 2];
+      unit_pairs<T>(ut[q], xt);
+      if (kMode) unit_pairs<T>(ud[q], xd);
 #pragma unroll
-      for (int e = 0; e < EPU; ++e) {
-        const float pt = ex2(fmaf(xt[e], sr.ct, sr.nmt)) * sr.ilt;
-        const float v = kMode ? fmaxf(0.f, pt - ex2(fmaf(xd[e], sr.cd, sr.nmd)) * sr.ild) : pt;
-        if (kKeep) r[q * EPU + e] = v;
-        sum += (double)v;
-        if (kMode) sum_t += (double)pt;
+      for (int p = 0; p < EPU / 2; ++p) {
+        pt[p] = mul2(ex2x2(fma2(xt[p], ct, nmt)), ilt);
+        if (kMode) {
+          const f2 dd = sub2(pt[p], mul2(ex2x2(fma2(xd[p], cd, nmd)), ild));
+          v[p] = f2{fmaxf(0.f, dd.x), fmaxf(0.f, dd.y)};
+        } else {
+          v[p] = pt[p];
+        }
+        if (kKeep) {
+          r[q * EPU + 2 * p] = v[p].x;
+          r[q * EPU + 2 * p + 1] = v[p].y;
+        }
       }
+      const float uq = unit_tree<EPU>(v);
+      if (kKeep) u[q] = uq;
+      sum += (double)uq;
+      if (kMode) sum_t += (double)unit_tree<EPU>(pt);
     }
-  } else {
+  } else {  // ragged tail / unaligned rows: one element per "unit"
     for (int e = 0; e < EPT; ++e) {
       float v = 0.f, pt = 0.f;
       if (e < n) {
@@ -295,6 +322,7 @@ __device__ __forceinline__ void slice_lane(const VerifyArgs &a, const SampleRow<
     }
   }
   if (!kMode) sum_t = sum;
+  return vec;
 }
 
 // Exclusive / inclusive warp prefix (fixed Kogge-Stone order).
@@ -409,10 +437,11 @@ __device__ __forceinline__ void find_seq(const VerifyArgs &a, int64_t b) {
   const int own_rank = own >= 0 ? own / nsl : -1;
   own = own >= 0 ? own % nsl : -1;
   if (own >= 0 && own_rank == a.rank) {
-    float r[EPT];
+    constexpr int EPU = Elem<T>::kPerUnit, UPT = kSampleUnitsPerThread;
+    float r[EPT], uu[UPT];
     double mine, mine_t;
-    if (mode) slice_lane<T, 1, true>(a, sr, own, r, mine, mine_t);
-    else slice_lane<T, 0, true>(a, sr, own, r, mine, mine_t);
+    const bool vec = mode ? slice_lane<T, 1, true>(a, sr, own, r, uu, mine, mine_t)
+                          : slice_lane<T, 0, true>(a, sr, own, r, uu, mine, mine_t);
     double incl, excl;
     warp_scan_d(mine, incl, excl);
     // crossing lane (exact), else the last lane with mass (fallback)
@@ -420,13 +449,37 @@ __device__ __forceinline__ void find_seq(const VerifyArgs &a, int64_t b) {
     if (sel) {
       const int ls = exact ? __ffs(sel) - 1 : 31 - __clz(sel);
       if (lane == ls) {
+        // the lane's sum is the fp64 sum of its unit sums (vec) or of its elements: find the
+        // crossing unit in that order, then the element inside it by a sequential fp64 scan
         double cum = Pc + excl;
         int lastp = -1;
+        if (vec) {
 #pragma unroll
-        for (int e = 0; e < EPT; ++e) {
-          if (r[e] > 0.f) lastp = e;
-          cum += (double)r[e];
-          if (exact && tok < 0 && cum > theta) tok = e;
+          for (int q = 0; q < UPT; ++q) {
+            const double next = cum + (double)uu[q];
+            if (exact && tok < 0 && next > theta) {
+              double c2 = cum;
+              int lq = -1;
+#pragma unroll
+              for (int e = 0; e < EPU; ++e) {
+                if (r[q * EPU + e] > 0.f) lq = q * EPU + e;
+                c2 += (double)r[q * EPU + e];
+                if (tok < 0 && c2 > theta) tok = q * EPU + e;
+              }
+              if (tok < 0) tok = lq;  // rounding inside the unit: its last positive element
+            }
+#pragma unroll
+            for (int e = 0; e < EPU; ++e)
+              if (r[q * EPU + e] > 0.f) lastp = q * EPU + e;
+            cum = next;
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < EPT; ++e) {
+            if (r[e] > 0.f) lastp = e;
+            cum += (double)r[e];
+            if (exact && tok < 0 && cum > theta) tok = e;
+          }
         }
         if (tok < 0) tok = lastp;  // rounding left no crossing: the last positive element
         if (tok >= 0) tok = (int)(a.v_begin + (int64_t)own * a.slice + (int64_t)ls * EPT + tok);
@@ -448,8 +501,8 @@ __device__ __forceinline__ void resid_item(const VerifyArgs &a, const Decision &
   const int lane = threadIdx.x & 31;
   const SampleRow<T> sr = sample_row<T>(a, dc, b);
   double mine, mine_t;
-  if (dc.mode) slice_lane<T, 1, false>(a, sr, s, nullptr, mine, mine_t);
-  else slice_lane<T, 0, false>(a, sr, s, nullptr, mine, mine_t);
+  if (dc.mode) slice_lane<T, 1, false>(a, sr, s, nullptr, nullptr, mine, mine_t);
+  else slice_lane<T, 0, false>(a, sr, s, nullptr, nullptr, mine, mine_t);
   double incl, excl, incl_t, excl_t;
   warp_scan_d(mine, incl, excl);
   warp_scan_d(mine_t, incl_t, excl_t);

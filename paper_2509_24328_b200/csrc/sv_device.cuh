@@ -119,6 +119,19 @@ template <> struct Elem<__nv_bfloat16> {
   }
 };
 
+// one 16-byte unit -> packed element pairs (exact)
+template <typename T>
+__device__ __forceinline__ void unit_pairs(const uint4 &u, f2 (&x)[Elem<T>::kPerUnit / 2]) {
+  if constexpr (sizeof(T) == 2) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int p = 0; p < 4; ++p) x[p] = f2{bf_lo(w[p]), bf_hi(w[p])};
+  } else {
+    x[0] = f2{__uint_as_float(u.x), __uint_as_float(u.y)};
+    x[1] = f2{__uint_as_float(u.z), __uint_as_float(u.w)};
+  }
+}
+
 // max of one 16-byte unit straight from the packed bits (bf16x2 HMNMX2 is exact)
 __device__ __forceinline__ float unit_max_bf16(const uint4 &v) {
   const __nv_bfloat162 *p = reinterpret_cast<const __nv_bfloat162 *>(&v);

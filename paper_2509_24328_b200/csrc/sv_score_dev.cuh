@@ -60,18 +60,6 @@ struct P1Out {
   float rd, rc, ld, lc, w;
 };
 
-template <typename T>
-__device__ __forceinline__ void unit_pairs(const uint4 &u, f2 (&x)[Elem<T>::kPerUnit / 2]) {
-  if constexpr (sizeof(T) == 2) {
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-    for (int p = 0; p < 4; ++p) x[p] = f2{bf_lo(w[p]), bf_hi(w[p])};
-  } else {
-    x[0] = f2{__uint_as_float(u.x), __uint_as_float(u.y)};
-    x[1] = f2{__uint_as_float(u.z), __uint_as_float(u.w)};
-  }
-}
-
 // Where this CTA's chunk of a row lives.
 template <typename T>
 struct Chunk {

@@ -64,6 +64,17 @@ def run(names, steps=60, B=80, k=8, V=152064):
         e1.record(st)
         torch.cuda.synchronize()
         eager = e0.elapsed_time(e1) / steps
+        # sd_verify alone (K4..K5b) on the last step's gamma, rotating input sets
+        sc, gam = pipe.score_out, pipe.sched_out["gamma"]
+        e0.record(st)
+        for j in range(steps):
+            D, C, T, tok = sets[j & 1]
+            sv.sd_verify(D, T, tok, gam, sc["draft_m"], sc["draft_l"], sc["draft_ptok"], 1.0, 1.0, 1, j,
+                         workspace=pipe.workspace, out=pipe.ver_out)
+        e1.record(st)
+        torch.cuda.synchronize()
+        verify = e0.elapsed_time(e1) / steps
+        vout = (pipe.ver_out["n_accept"].clone(), pipe.ver_out["out_tok"].clone())
         gps = []
         for si in range(2):
             gp = sv.GraphPipeline(B, k, V, torch.bfloat16, prof, L, seed=1, offset0=si)
@@ -84,12 +95,14 @@ def run(names, steps=60, B=80, k=8, V=152064):
         if ref is not None:
             diff = {n: float((out[n] - ref[n]).abs().nan_to_num(0).max()) for n in ("S", "A", "KL", "draft_l")}
             diff["p_hat_eq"] = bool(torch.equal(out["p_hat"], ref["p_hat"]))
+            diff["n_accept_eq"] = bool(torch.equal(vout[0], vref[0]))
+            diff["out_tok_mismatch"] = int((vout[1] != vref[1]).sum())
         else:
-            ref = out
+            ref, vref = out, vout
         k1_mean = sum(k1) / len(k1)
         print(json.dumps({"variant": name, "k1_us_mean": k1_mean * 1e3, "k1_us_median": k1[len(k1) // 2] * 1e3,
                           "k1_frac": 2 * B * k * V * 2 / (k1_mean * 1e-3) / 1e9 / 6545.0,
-                          "eager_us": eager * 1e3, "graph_us": graph * 1e3, "diff_vs_product": diff}), flush=True)
+                          "eager_us": eager * 1e3, "verify_us": verify * 1e3, "graph_us": graph * 1e3, "diff_vs_product": diff}), flush=True)
         del gps, pipe
 
 
