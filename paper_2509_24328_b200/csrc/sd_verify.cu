@@ -172,8 +172,13 @@ cudaError_t launch_verify_stage(int stage, const VerifyArgs &a, cudaStream_t st)
   }
 }
 
+// SV_EXP_VERIFY_STAGES: build-time experiment knob (scripts/k1_ab.py variants time the chain
+// stage by stage); the product always launches all four stages.
+#ifndef SV_EXP_VERIFY_STAGES
+#define SV_EXP_VERIFY_STAGES 4
+#endif
 cudaError_t launch_verify(const VerifyArgs &a, cudaStream_t st) {
-  for (int stage = 0; stage < 4; ++stage) {
+  for (int stage = 0; stage < SV_EXP_VERIFY_STAGES; ++stage) {
     const cudaError_t e = launch_verify_stage(stage, a, st);
     if (e != cudaSuccess) return e;
   }

@@ -162,7 +162,12 @@ class VocabShardedPipeline:
             P(vo["status"]), self.workspace.data_ptr(), self.workspace.numel(), S(stream)), "sv_shard_verify_finish")
 
     def run(self, comm, Dl, Cl, Tl, tok, seed=0, offset=0, seq_base=0, stream=None):
-        """The whole step on this rank: 4 all-gathers of the stage blocks + 1 all-reduce(MAX)."""
+        """The whole step on this rank: 4 all-gathers of the stage blocks + 1 all-reduce(MAX).
+        Kernels and collectives go to ONE stream: `stream` is made current for the step, so the
+        process group's collectives are ordered after the kernels that produce their inputs."""
+        if stream is not None:
+            with torch.cuda.stream(stream):
+                return self.run(comm, Dl, Cl, Tl, tok, seed, offset, seq_base, None)
         self.score_p1(Dl, Cl, tok, stream)
         comm.all_gather(self.xch_all[0], self.xch[0])
         self.score_p2(Dl, Cl, tok, stream)
