@@ -32,6 +32,13 @@ namespace sv {
 #ifndef SV_K1_SAMECTA
 #define SV_K1_SAMECTA 0
 #endif
+#ifndef SV_K1_VARIANT
+#define SV_K1_VARIANT -1  // experiment: force a K1 variant (0 ticket, 1 K1c, 2 K1c resident); -1 = by shape
+#endif
+// K1c (one cluster of cs CTAs per row) for D + C up to this many bytes; its resident form when
+// every chunk pair fits in shared memory and the whole grid in one wave
+constexpr int64_t kScoreClusterMaxBytes = 64ll << 20;
+constexpr int64_t kScoreResMaxPairBytes = 200 << 10;
 constexpr int kScoreThreads = 256;
 constexpr int kScoreMinBlocks = SV_K1_MINB;
 constexpr int kScoreGroup = SV_K1_GROUP;

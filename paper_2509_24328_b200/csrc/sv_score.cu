@@ -97,9 +97,134 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constan
   p2_finish_tail<T, NW>(a, c.k, sm);
 }
 
+// K1c: one cluster of cs CTAs per row (CTA rank r = chunk r), both passes in one CTA: pass 1
+// (HBM, L2 evict_last) -> block merge into shared memory -> cluster barrier -> every warp merges
+// the cs chunk partials from the peers' shared memory (DSMEM) in chunk order -> pass 2 (the same
+// chunk again, an L2 hit: it was read microseconds earlier) -> S partial -> cluster barrier ->
+// rank 0 runs the row epilogue.  No ticket, no counters, no polling: a row's exchange is two
+// cluster barriers, and clusters are independent of each other.  Every arithmetic step is the
+// ticket kernel's (same chunking, per-thread units, warp / block / row merge orders, epilogue),
+// so the outputs are bit-identical to it.
+template <typename T, int NT, int MINB, bool kRes>
+__global__ void __launch_bounds__(NT, MINB) sv_score_cluster_kernel(const __grid_constant__ ScoreArgs a) {
+  constexpr int NW = NT / 32, G = kScoreGroup;
+  __shared__ Smem<NW> sm;
+  __shared__ uint64_t s_bar;
+  extern __shared__ __align__(128) uint8_t s_chunk[];  // kRes: the chunk pair (D at 0, C at chunk bytes)
+  pdl_wait();
+  pdl_trigger();
+  cg::cluster_group cl = cg::this_cluster();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const float cd = a.cd, cc = a.cc;
+  Task k;
+  k.q = blockIdx.x;
+  k.row = k.q / (uint32_t)a.cs;
+  k.rank = (int)(k.q - k.row * (uint32_t)a.cs);
+  k.bb = k.row / (uint32_t)a.k;
+  k.ii = k.row - k.bb * a.k;
+  k.p2 = false;
+  const Chunk<T> ch = chunk_of<T>(a, k.bb, k.ii, k.rank);
+  float s_loc = 0.f;
+  auto both_passes = [&](const auto &src1, const auto &src2, auto *pre) {
+    const P1Out o = pass1_thread<T, NT, G>(src1, ch, cd, cc);
+    p1_publish_head<NW>(o, sm, cd, cc);  // warp partials, block barrier
+    if (wid == NW - 1) {                 // the chunk's (M_d, L_d, M_c, L_c, W): the NW warp partials merged
+      auto warp_part = [&](int j) { return (const double *)(sm.dscr + 5 * j); };
+      merge_partials_to<decltype(warp_part), false>(a, NW, warp_part, sm.glob, sm.lam);
+    }
+    if (pre) prefetch_first<T, NT, G>(src2, ch, *pre);
+    cl.sync();  // every CTA's chunk partial is in its shared memory
+    auto peer_part = [&](int j) { return (const double *)cl.map_shared_rank(&sm.glob[0], (unsigned)j); };
+    merge_partials_to<decltype(peer_part), false>(a, a.cs, peer_part, sm.wglob[wid], sm.wlam[wid]);
+    __syncwarp();
+    const float lamd = sm.wlam[wid][0], lamc = sm.wlam[wid][1];
+    if (lamd == lamd && lamc == lamc) s_loc = pass2_thread<T, NT, G, kScorePoly>(src2, ch, cd, cc, lamd, lamc, pre);
+  };
+  if constexpr (kRes) {  // one bulk copy per tensor from HBM; both passes read shared memory
+    const uint32_t nb = (uint32_t)ch.units * 16u;
+    if (threadIdx.x == 0) {
+      mbar_init(&s_bar, 1);
+      fence_mbar_init();
+      if (nb) {
+        const uint64_t pol = l2_policy_evict_first();
+        mbar_arrive_expect_tx(&s_bar, 2 * nb);
+        bulk_g2s(s_chunk, ch.d, nb, &s_bar, pol);
+        bulk_g2s(s_chunk + a.chunk * sizeof(T), ch.c, nb, &s_bar, pol);
+      }
+    }
+    __syncthreads();
+    if (nb) mbar_wait_bounded(&s_bar, 0);
+    const SSrc src{reinterpret_cast<const uint4 *>(s_chunk),
+                   reinterpret_cast<const uint4 *>(s_chunk + a.chunk * sizeof(T))};
+    both_passes(src, src, (Pre<G> *)nullptr);
+  } else {
+    Pre<G> pre;
+    both_passes(GSrc<T>{ch.d, ch.c, l2_policy_evict_last()}, GSrc<T>{ch.d, ch.c, l2_policy_evict_first()}, &pre);
+  }
+  p2_finish_head<NW>(s_loc, sm);  // warp sums, block barrier
+  float *srow = a.spart + (size_t)k.row * a.cs;
+  if (wid == NW - 1 && lane == 0) {
+    float r = sm.fscr[0];
+    for (int w = 1; w < NW; ++w) r += sm.fscr[w];
+    srow[k.rank] = r;
+  }
+  cl.sync();  // S partials written (and no CTA leaves while a peer may still read its glob)
+  if (k.rank == 0 && wid == NW - 1) epilogue<T>(a, k.bb, k.ii, sm.wglob[NW - 1], srow, a.cs, 1, 0, nullptr, 0);
+}
+
+template <typename T, bool kRes>
+cudaError_t launch_score_cluster(const ScoreArgs &a, cudaStream_t st) {
+  auto kern = sv_score_cluster_kernel<T, kScoreThreads, kScoreMinBlocks, kRes>;
+  const size_t smem = kRes ? 2 * (size_t)a.chunk * sizeof(T) : 0;
+  if (kRes) {
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((int64_t)a.B * a.k * a.cs));
+  cfg.blockDim = dim3(kScoreThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = (unsigned)a.cs;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+// Which K1 runs for a launch shape (all three give identical bits): the ticket kernel (0) for
+// large inputs; K1c (1) when D + C is at most kScoreClusterMaxBytes -- a row's exchange is two
+// cluster barriers instead of global counters, which pays while the grid is a few waves; its
+// resident form (2) when the chunk pairs fit in shared memory and the grid is one wave.  cs <= 8
+// (portable cluster size).  Measured per BASELINE config in DESIGN.md §5.
+template <typename T>
+int score_variant(const ScoreArgs &a) {
+  if (SV_K1_VARIANT >= 0) return SV_K1_VARIANT;
+  if (a.cs > 8) return 0;
+  const int64_t rows = (int64_t)a.B * a.k, pair = 2 * a.chunk * (int64_t)sizeof(T);
+  if (pair <= kScoreResMaxPairBytes) {
+    auto kern = sv_score_cluster_kernel<T, kScoreThreads, kScoreMinBlocks, true>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pair) == cudaSuccess &&
+        rows * a.cs <= resident_grid((const void *)kern, kScoreThreads, (int)pair))
+      return 2;
+    cudaGetLastError();
+  }
+  return rows * a.cs * pair <= kScoreClusterMaxBytes ? 1 : 0;
+}
+
 template <typename T>
 cudaError_t launch_score_t(const ScoreArgs &a, cudaStream_t st) {
   if ((int64_t)a.B * a.k == 0) return cudaSuccess;
+  switch (score_variant<T>(a)) {
+    case 2: return launch_score_cluster<T, true>(a, st);
+    case 1: return launch_score_cluster<T, false>(a, st);
+    default: break;
+  }
   const int64_t tasks = (SV_K1_SAMECTA ? 1 : 2) * (int64_t)a.B * a.k * a.cs;
   if (tasks == 0) return cudaSuccess;
   return launch_k(sv_score_kernel<T, kScoreThreads, kScoreMinBlocks>, dim3((unsigned)tasks), dim3(kScoreThreads), 0,
