@@ -25,7 +25,7 @@ def inputs(B, k, V, dt, seed, alignment="mix"):
     return conv(x["D"]), conv(x["C"]), conv(x["T"]), torch.from_numpy(x["tok"]).to(dev)
 
 
-points = [("c1", 4, 4, 32000, "f32"), ("c2", 32, 8, 32000, "bf16"), ("B4k8", 4, 8, 128256, "bf16"),
+points = [("tiny", 1, 1, 64, "f32"), ("c1", 4, 4, 32000, "f32"), ("c2", 32, 8, 32000, "bf16"), ("B4k8", 4, 8, 128256, "bf16"),
           ("B16k8", 16, 8, 128256, "bf16"), ("B32k8", 32, 8, 128256, "bf16"), ("B80k8", 80, 8, 128256, "bf16"),
           ("head", 80, 8, 152064, "bf16")]
 for name in sys.argv[1:]:
