@@ -34,10 +34,12 @@ template <typename T>
 __global__ void __launch_bounds__(32 * (SV_MAX_K_DEV + 1)) sv_decide_kernel(const __grid_constant__ VerifyArgs a) {
   __shared__ float s_M[SV_MAX_K_DEV + 1];
   __shared__ double s_L[SV_MAX_K_DEV + 1];
-  pdl_wait();
-  pdl_trigger();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t b = blockIdx.x;
+  DecidePre pre{};
+  if (wid == 0) pre = decide_prefetch<T>(a, b);  // inputs written >= 2 launches earlier (see there)
+  pdl_wait();
+  pdl_trigger();
   const int g = a.gamma[b];
   if (g >= 0 && g <= a.k && wid <= g) {
     float M;
@@ -51,7 +53,7 @@ __global__ void __launch_bounds__(32 * (SV_MAX_K_DEV + 1)) sv_decide_kernel(cons
   __syncthreads();
   if (wid != 0) return;
   const bool in = g >= 0 && g <= a.k && lane <= g;
-  decide_warp<T>(a, b, g, in ? s_M[lane] : kMFloor, in ? s_L[lane] : 0.0);
+  decide_warp<T>(a, b, g, in ? s_M[lane] : kMFloor, in ? s_L[lane] : 0.0, pre);
 }
 
 // Persistent warp-granular K4 over the items (b, i <= gamma_b, split), in sequence order.

@@ -131,37 +131,63 @@ __device__ __forceinline__ void merge_row_warp(const VerifyArgs &a, int64_t b, i
   L = warp_sum_d(l);
 }
 
+// Per-lane inputs of the accept tests that K4 does not produce (lane i < k: draft token t_i, the
+// draft normalisers and p_d(t_i) from sv_score, the target logit x_t(t_i); lane i <= k: the
+// Philox block of position i).  K4b loads them BEFORE its griddepcontrol.wait: they were written
+// two or more launches earlier, and every libsv kernel triggers its dependants only after its own
+// wait, so K4b's launch already implies their completion (the vocab-sharded token logits come
+// from a collective and are read after the wait).
+struct DecidePre {
+  int t;
+  float dl, dpt, dmv, xt;
+  uint4 w;
+};
+template <typename T>
+__device__ __forceinline__ DecidePre decide_prefetch(const VerifyArgs &a, int64_t b) {
+  const int lane = threadIdx.x & 31, k = a.k;
+  DecidePre p{-1, 0.f, 0.f, 0.f, 0.f, make_uint4(0u, 0u, 0u, 0u)};
+  if (lane <= k) {
+    const uint64_t off = a.offset_dev ? *a.offset_dev : a.offset;  // device offset: graph replays
+    if (lane < k) {
+      const int64_t ri = b * k + lane;
+      p.t = a.tok[ri];
+      p.dl = a.dl[ri];
+      p.dpt = a.dpt[ri];
+      p.dmv = a.dm[ri];
+      if (!a.xtok_all && p.t >= 0 && p.t < a.Vg) p.xt = Elem<T>::load(trow<T>(a, b, lane) + p.t);
+    }
+    p.w = sv_philox(a.seed, off, a.seq_base + b, lane);
+  }
+  return p;
+}
+
 // The accept tests of sequence b by one warp, lane i <= g holding row i's merged (Mi, Li):
 // p_t(t_i), ratio_i = p_t(t_i) / p_d(t_i), u_i, N_b = first rejection, u_s; writes the Decision
 // for K5 (+ n_accept, accept_ratio and, for a bad sequence, its sentinels).
 template <typename T>
-__device__ __forceinline__ void decide_warp(const VerifyArgs &a, int64_t b, int g, float Mi, double Li) {
+__device__ __forceinline__ void decide_warp(const VerifyArgs &a, int64_t b, int g, float Mi, double Li,
+                                            const DecidePre &pre) {
   const int lane = threadIdx.x & 31, k = a.k;
   const bool gok = g >= 0 && g <= k;
   int t = -1;
   float dl = 0.f, dpt = 0.f, dmv = 0.f, xt = 0.f;
   uint4 w = make_uint4(0u, 0u, 0u, 0u);
   if (gok && lane <= g) {
-    const uint64_t off = a.offset_dev ? *a.offset_dev : a.offset;  // device offset: graph replays
     if (lane < g) {
-      const int64_t ri = b * k + lane;
-      t = a.tok[ri];
-      dl = a.dl[ri];
-      dpt = a.dpt[ri];
-      dmv = a.dm[ri];
-      if (t >= 0 && t < a.Vg) {
-        if (a.xtok_all) {  // vocab-sharded: the owner rank's logit (NaN elsewhere)
-          xt = __int_as_float(0x7fc00000);
-          for (int q = 0; q < a.G; ++q) {
-            const float v = a.xtok_all[(int64_t)q * a.gs_tok + b * k + lane];
-            if (xt != xt) xt = v;
-          }
-        } else {
-          xt = Elem<T>::load(trow<T>(a, b, lane) + t);
+      t = pre.t;
+      dl = pre.dl;
+      dpt = pre.dpt;
+      dmv = pre.dmv;
+      xt = pre.xt;
+      if (a.xtok_all && t >= 0 && t < a.Vg) {  // vocab-sharded: the owner rank's logit (NaN elsewhere)
+        xt = __int_as_float(0x7fc00000);
+        for (int q = 0; q < a.G; ++q) {
+          const float v = a.xtok_all[(int64_t)q * a.gs_tok + b * k + lane];
+          if (xt != xt) xt = v;
         }
       }
     }
-    w = sv_philox(a.seed, off, a.seq_base + b, lane);
+    w = pre.w;
   }
   int st = gok ? 0 : 64 /*BAD_GAMMA*/;
   const int gg = st ? -1 : g;
@@ -359,37 +385,32 @@ __device__ __forceinline__ void find_seq(const VerifyArgs &a, int64_t b) {
   auto midx = [&](int half, int q) { return (int64_t)(q / nsl) * a.gs_mass + (b * 2 + half) * nsl + q % nsl; };
   const double *sm = a.smass;
   // Z: first the residual masses; R10 (Z = 0) falls back to the target masses (same row).
-  // Slices go in chunks of 32 (one warp scan each, running total across chunks); the loads of
-  // kFindChunks chunks are issued together.
-  double Z = 0.0;
-  // one chunk group covers every slice (V <= 32 kFindChunks slices): the crossing scan below
-  // reuses these registers instead of loading the masses again
-  double mc[kFindChunks];
-  int mc_half = -1;
-  for (int pass = 0; pass < 2; ++pass) {
-    const int half = mode ? 0 : 1;
-    double run = 0.0;
-    for (int c0 = 0; c0 < nq; c0 += 32 * kFindChunks) {
-      double m[kFindChunks];
+  // Lane l owns the contiguous entries [q0, q1) (vocabulary order): a sequential fp64 sum per
+  // lane, one fixed-order warp scan over the lanes; the crossing lane then walks its own entries
+  // from its exclusive prefix.  Up to kFindChunks entries per lane stay in registers.
+  const int per = (nq + 31) / 32;
+  const int q0 = min(nq, lane * per), q1 = min(nq, q0 + per);
+  const bool cached = per <= kFindChunks;
+  double mreg[kFindChunks];
+  auto mass = [&](int half, int q) { return __ldcg(sm + midx(half, q)); };
+  auto lane_sum = [&](int half) {
+    double s = 0.0;
+    if (cached) {
 #pragma unroll
-      for (int j = 0; j < kFindChunks; ++j) {
-        const int q = c0 + 32 * j + lane;
-        m[j] = q < nq ? __ldcg(sm + midx(half, q)) : 0.0;
-      }
-      if (nq <= 32 * kFindChunks) {
+      for (int j = 0; j < kFindChunks; ++j) mreg[j] = q0 + j < q1 ? mass(half, q0 + j) : 0.0;
 #pragma unroll
-        for (int j = 0; j < kFindChunks; ++j) mc[j] = m[j];
-        mc_half = half;
-      }
-#pragma unroll
-      for (int j = 0; j < kFindChunks; ++j) {
-        if (c0 + 32 * j >= nq) break;
-        double incl, excl;
-        warp_scan_d(m[j], incl, excl);
-        run += __shfl_sync(0xffffffffu, incl, 31);
-      }
+      for (int j = 0; j < kFindChunks; ++j)
+        if (q0 + j < q1) s += mreg[j];
+    } else {
+      for (int q = q0; q < q1; ++q) s += mass(half, q);
     }
-    Z = run;
+    return s;
+  };
+  double Z = 0.0, lsum = 0.0, incl = 0.0, excl = 0.0;
+  for (int pass = 0; pass < 2; ++pass) {
+    lsum = lane_sum(mode ? 0 : 1);
+    warp_scan_d(lsum, incl, excl);
+    Z = __shfl_sync(0xffffffffu, incl, 31);
     if (mode == 1 && !(Z > 0.0)) {
       mode = 0;
       st = 32;  // SV_ROW_RESID_ZERO
@@ -399,37 +420,34 @@ __device__ __forceinline__ void find_seq(const VerifyArgs &a, int64_t b) {
   }
   const double theta = dc.us * Z;
   const int half = mode ? 0 : 1;
-  double run = 0.0, Pc = 0.0;
-  int own = -1, last_pos = -1;
-  for (int c0 = 0; c0 < nq; c0 += 32 * kFindChunks) {
-    double mm[kFindChunks];
-#pragma unroll
-    for (int j = 0; j < kFindChunks; ++j) {
-      const int q = c0 + 32 * j + lane;
-      mm[j] = mc_half == half ? mc[j] : (q < nq ? __ldcg(sm + midx(half, q)) : 0.0);
-    }
-#pragma unroll
-    for (int j = 0; j < kFindChunks; ++j) {
-      const int cj = c0 + 32 * j;
-      if (cj >= nq) break;
-      const bool valid = cj + lane < nq;
-      const double m = mm[j];
-      double incl, excl;
-      warp_scan_d(m, incl, excl);
-      const double P = run + excl;
-      const unsigned pos = __ballot_sync(0xffffffffu, valid && m > 0.0);
-      if (pos) last_pos = cj + 31 - __clz(pos);
-      if (own < 0) {
-        const unsigned cross = __ballot_sync(0xffffffffu, valid && P + m > theta);
-        if (cross) {
-          const int l = __ffs(cross) - 1;
-          own = cj + l;
-          Pc = __shfl_sync(0xffffffffu, P, l);
-        }
+  // the owning entry: the first q with P_q + m_q > theta; if rounding leaves none (or inside the
+  // crossing lane), the last entry with mass (then the token is its last positive element)
+  int own = -1, pos_q = -1;
+  double Pc = 0.0;
+  const unsigned cross = __ballot_sync(0xffffffffu, q1 > q0 && incl > theta);
+  const unsigned posl = __ballot_sync(0xffffffffu, lsum > 0.0);
+  const int wl = cross ? __ffs(cross) - 1 : (posl ? 31 - __clz(posl) : -1);
+  if (lane == wl) {
+    double P = excl;
+    auto step = [&](int q, double m) {
+      if (m > 0.0) pos_q = q;
+      if (cross && own < 0 && P + m > theta) {
+        own = q;
+        Pc = P;
       }
-      run += __shfl_sync(0xffffffffu, incl, 31);
+      P += m;
+    };
+    if (cached) {
+#pragma unroll
+      for (int j = 0; j < kFindChunks; ++j)
+        if (q0 + j < q1) step(q0 + j, mreg[j]);
+    } else {
+      for (int q = q0; q < q1; ++q) step(q, mass(half, q));
     }
   }
+  own = __shfl_sync(0xffffffffu, wl >= 0 ? own : -1, wl >= 0 ? wl : 0);
+  Pc = __shfl_sync(0xffffffffu, Pc, wl >= 0 ? wl : 0);
+  const int last_pos = __shfl_sync(0xffffffffu, wl >= 0 ? pos_q : -1, wl >= 0 ? wl : 0);
   const bool exact = own >= 0;
   if (!exact) own = last_pos;
   int tok = -1;
