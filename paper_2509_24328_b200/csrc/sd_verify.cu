@@ -22,6 +22,10 @@
 // Every reduction order is a function of V and the dtype only.
 #include "sd_verify_dev.cuh"
 
+#ifndef SV_K5_MINB
+#define SV_K5_MINB 5  // K5 CTAs per SM (48 registers, no spills; 3 and 4 measured slower)
+#endif
+
 namespace sv {
 
 namespace {
@@ -127,7 +131,7 @@ __global__ void __launch_bounds__(256) sv_find_kernel(const __grid_constant__ Ve
 // Persistent warp-granular K5 over the B x nsl warp slices: per slice the residual mass and
 // the target mass (the R10 fallback), each the lane-31 value of a fixed-order warp scan.
 template <typename T>
-__global__ void __launch_bounds__(kSampleThreads, 3) sv_resid_kernel(const __grid_constant__ VerifyArgs a) {
+__global__ void __launch_bounds__(kSampleThreads, SV_K5_MINB) sv_resid_kernel(const __grid_constant__ VerifyArgs a) {
   const int wid = threadIdx.x >> 5;
   pdl_wait();
   pdl_trigger();
