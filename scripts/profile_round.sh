@@ -15,6 +15,6 @@ timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
   --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 4 --warmup 3 --no-cpu-baseline \
   > gpurun_out/ncu_launch_$TAG.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
-  -k regex:"sv_score_kernel|sv_schedule_row_kernel|sv_rows_kernel|sv_decide_kernel|sv_resid_kernel|sv_find_kernel" -s 12 -c 6 \
+  -k regex:"sv_score_kernel|sv_score_cluster_kernel|sv_schedule_row_kernel|sv_rows_kernel|sv_decide_kernel|sv_resid_kernel|sv_find_kernel" -s 12 -c 6 \
   -o gpurun_out/prof_all_$TAG -f python scripts/prof_step.py --steps 4 > gpurun_out/ncu_full_$TAG.log 2>&1
 echo "profile rc=$?" >> gpurun_out/ncu_full_$TAG.log

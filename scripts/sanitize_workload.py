@@ -37,5 +37,12 @@ gsw = sv.sv_score_filtered(xg, xg, tg, 0, 0.9, 1.0, 1.0)
 T3 = torch.cat([xg, xg[:, :1]], dim=1).contiguous()
 sv.sd_verify_filtered(T3, tg, torch.tensor([2, 1], dtype=torch.int32, device="cuda"), gsw["fworkspace"], 0, 0.9, 1.0,
                       1, 0, D=xg)
+# the three K1 variants (chosen by launch shape): K1c resident (the small cases above),
+# K1c with global re-reads (D + C 41 MB, more than one wave) and the ticket kernel (D + C 82 MB)
+for (B, k, V) in [(40, 8, 32000), (80, 8, 32000)]:
+    x = synth.make_inputs(B, k, V, "bf16", seed=2)
+    D, C, T, tok = H.to_torch(x)
+    L = torch.tensor(synth.latency_table(k + 2), dtype=torch.float64, device="cuda")
+    sv.Pipeline(B, k, V, D.dtype, prof, L).run(D, C, T, tok, seed=1, offset=0)
 torch.cuda.synchronize()
 print("sanitizer workload done")

@@ -18,7 +18,7 @@ import sys
 from collections import OrderedDict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-OURS = ("sv_score_kernel", "sv_schedule_row_kernel", "sv_greedy", "sv_rows_kernel", "sv_decide_kernel",
+OURS = ("sv_score_kernel", "sv_score_cluster_kernel", "sv_schedule_row_kernel", "sv_greedy", "sv_rows_kernel", "sv_decide_kernel",
         "sv_resid_kernel", "sv_find_kernel", "sv_shard_p1_kernel", "sv_shard_p2_kernel", "sv_shard_finish_kernel")
 METRICS = [
     "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
