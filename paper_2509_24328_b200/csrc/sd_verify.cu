@@ -22,6 +22,9 @@
 // Every reduction order is a function of V and the dtype only.
 #include "sd_verify_dev.cuh"
 
+#ifndef SV_K4_MINB
+#define SV_K4_MINB 4  // K4 CTAs per SM (64 registers)
+#endif
 #ifndef SV_K5_MINB
 #define SV_K5_MINB 5  // K5 CTAs per SM (48 registers, no spills; 3 and 4 measured slower)
 #endif
@@ -62,7 +65,7 @@ __global__ void __launch_bounds__(32 * (SV_MAX_K_DEV + 1)) sv_decide_kernel(cons
 
 // Persistent warp-granular K4 over the items (b, i <= gamma_b, split), in sequence order.
 template <typename T>
-__global__ void __launch_bounds__(kRowsThreads, 4) sv_rows_kernel(const __grid_constant__ VerifyArgs a) {
+__global__ void __launch_bounds__(kRowsThreads, SV_K4_MINB) sv_rows_kernel(const __grid_constant__ VerifyArgs a) {
   constexpr int NT = kRowsThreads, NW = NT / 32;
   __shared__ int s_pref[NT + 1];
   __shared__ int s_wtot[NW];

@@ -156,6 +156,30 @@ def test_determinism_and_batch_split(sv, prof_dict):
         assert np.array_equal(a[1][k_][4:], c[1][k_], equal_nan=True)
 
 
+def test_k1_variants_bit_identical(sv, prof_dict):
+    """sv_score picks its K1 kernel by launch shape: at V = 32000 bf16 the whole batch
+    B = 80 (D + C 82 MB) runs the ticket kernel, B = 40 (41 MB, more than one wave) K1c with
+    cluster-exchanged partials, B = 2 K1c with shared-memory resident chunks.  All three share
+    the chunking and every reduction order, so the rows of a sub-batch must match the full batch
+    bit for bit (the batch-sharded multi-GPU layout relies on it)."""
+    x = synth.make_inputs(80, 8, 32000, "bf16", seed=33)
+    D, C, T, tok = H.to_torch(x)
+    prof = sv.Profile.from_dict(prof_dict)
+    keys = ("S", "A", "KL", "p_hat", "draft_m", "draft_l", "draft_ptok", "status")
+    full = H.gpu_np(sv.sv_score(D, C, tok, 1.0, 1.0, prof))
+    for lo, hi in ((0, 40), (40, 42), (77, 80)):
+        part = H.gpu_np(sv.sv_score(D[lo:hi].contiguous(), C[lo:hi].contiguous(), tok[lo:hi].contiguous(), 1.0, 1.0,
+                                    prof))
+        for k_ in keys:
+            assert np.array_equal(full[k_][lo:hi], part[k_], equal_nan=True), (lo, hi, k_)
+    # and the full batch against the oracle on sampled sequences
+    rep = H.ParityReport()
+    idx = np.array([0, 39, 40, 79])
+    Dd, Cd, _ = H.oracle_inputs({**x, "D": x["D"][idx], "C": x["C"][idx], "T": x["T"][idx]})
+    rs = oracle.score(Dd, Cd, x["tok"][idx], 1.0, 1.0, prof_dict)
+    H.compare_score({k_: full[k_][idx] for k_ in full}, rs, prof_dict, rep)
+
+
 def test_broadcast_losslessness(sv):
     # S L156, L521: the emitted first token follows P_t (chi^2 / TV < 0.005 over 10^6 trials),
     # and P(accept) = sum min(p_d, p_t); stride_b = 0 broadcast rows, fresh t ~ p_d per trial
