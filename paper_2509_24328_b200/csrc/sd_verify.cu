@@ -31,6 +31,8 @@
 
 namespace sv {
 
+SV_TRACE_DECL
+
 namespace {
 
 // K4b sv_decide_kernel: one CTA of k+1 warps per sequence.  Warp i <= gamma_b merges row i's
@@ -47,6 +49,7 @@ __global__ void __launch_bounds__(32 * (SV_MAX_K_DEV + 1)) sv_decide_kernel(cons
   if (wid == 0) pre = decide_prefetch<T>(a, b);  // inputs written >= 2 launches earlier (see there)
   pdl_wait();
   pdl_trigger();
+  SV_TRACE_START(3);
   const int g = a.gamma[b];
   if (g >= 0 && g <= a.k && wid <= g) {
     float M;
@@ -61,6 +64,7 @@ __global__ void __launch_bounds__(32 * (SV_MAX_K_DEV + 1)) sv_decide_kernel(cons
   if (wid != 0) return;
   const bool in = g >= 0 && g <= a.k && lane <= g;
   decide_warp<T>(a, b, g, in ? s_M[lane] : kMFloor, in ? s_L[lane] : 0.0, pre);
+  SV_TRACE_END(3);
 }
 
 // Persistent warp-granular K4 over the items (b, i <= gamma_b, split), in sequence order.
@@ -72,6 +76,7 @@ __global__ void __launch_bounds__(kRowsThreads, SV_K4_MINB) sv_rows_kernel(const
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   pdl_wait();
   pdl_trigger();
+  SV_TRACE_START(2);
   const int splits = (int)a.splits;
   const int64_t nwarps = (int64_t)gridDim.x * NW;
   int64_t base = 0, my = (int64_t)blockIdx.x * NW + wid;
@@ -121,14 +126,17 @@ __global__ void __launch_bounds__(kRowsThreads, SV_K4_MINB) sv_rows_kernel(const
     }
     base += total;
   }
+  SV_TRACE_END(2);
 }
 
 template <typename T>
 __global__ void __launch_bounds__(256) sv_find_kernel(const __grid_constant__ VerifyArgs a) {
   pdl_wait();
   pdl_trigger();
+  SV_TRACE_START(5);
   const int64_t b = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (b < a.B) find_seq<T>(a, b);
+  SV_TRACE_END(5);
 }
 
 // Persistent warp-granular K5 over the B x nsl warp slices: per slice the residual mass and
@@ -138,6 +146,7 @@ __global__ void __launch_bounds__(kSampleThreads, SV_K5_MINB) sv_resid_kernel(co
   const int wid = threadIdx.x >> 5;
   pdl_wait();
   pdl_trigger();
+  SV_TRACE_START(4);
   const int64_t nwarps = (int64_t)gridDim.x * (kSampleThreads / 32);
   const int64_t items = (int64_t)a.B * a.nsl;
   for (int64_t it = (int64_t)blockIdx.x * (kSampleThreads / 32) + wid; it < items; it += nwarps) {
@@ -145,6 +154,7 @@ __global__ void __launch_bounds__(kSampleThreads, SV_K5_MINB) sv_resid_kernel(co
     const Decision dc = a.dec[b];
     if (!dc.st) resid_item<T>(a, dc, b, it - b * a.nsl);  // (bad sequences: K4b wrote the sentinels)
   }
+  SV_TRACE_END(4);
 }
 
 }  // namespace
@@ -195,3 +205,5 @@ cudaError_t launch_verify(const VerifyArgs &a, cudaStream_t st) {
 }
 
 }  // namespace sv
+
+SV_TRACE_READER(verify)

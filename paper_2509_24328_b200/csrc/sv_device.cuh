@@ -250,6 +250,46 @@ __device__ __forceinline__ uint4 ldg_stream(const void *p) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// ---------------------------------------------------------------- experiment-only kernel trace
+// SV_EXP_TRACE builds (scripts/trace_step.py) record, per kernel slot k, the earliest start and
+// the latest warp exit (%globaltimer, ns) in a per-translation-unit device array read back by
+// sv_debug_trace_<tu>(); the product build compiles none of it.
+#ifndef SV_EXP_TRACE
+#define SV_EXP_TRACE 0
+#endif
+#if SV_EXP_TRACE
+__device__ __forceinline__ unsigned long long sv_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SV_TRACE_DECL static __device__ unsigned long long g_sv_trace[32];
+#define SV_TRACE_START(k) \
+  do {                    \
+    if (threadIdx.x == 0) atomicMin(&g_sv_trace[2 * (k)], sv_gtimer()); \
+  } while (0)
+#define SV_TRACE_END(k) \
+  do {                  \
+    if ((threadIdx.x & 31) == 0) atomicMax(&g_sv_trace[2 * (k) + 1], sv_gtimer()); \
+  } while (0)
+#define SV_TRACE_READER(name)                                                              \
+  extern "C" __attribute__((visibility("default"))) int sv_debug_trace_##name(unsigned long long *out) { \
+    unsigned long long init[32];                                                           \
+    for (int i = 0; i < 32; ++i) init[i] = (i & 1) ? 0ull : ~0ull;                         \
+    if (out && cudaMemcpyFromSymbol(out, sv::g_sv_trace, sizeof(init)) != cudaSuccess) return 1; \
+    return cudaMemcpyToSymbol(sv::g_sv_trace, init, sizeof(init)) != cudaSuccess;          \
+  }
+#else
+#define SV_TRACE_DECL
+#define SV_TRACE_START(k) \
+  do {                    \
+  } while (0)
+#define SV_TRACE_END(k) \
+  do {                  \
+  } while (0)
+#define SV_TRACE_READER(name)
+#endif
+
 // ---------------------------------------------------------------- reductions
 // Fixed butterfly order: the result depends only on the lane -> value mapping.
 __device__ __forceinline__ float warp_max(float v) {

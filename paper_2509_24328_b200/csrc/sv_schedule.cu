@@ -18,14 +18,17 @@
 
 namespace sv {
 
+SV_TRACE_DECL
+
 namespace {
 
 __global__ void __launch_bounds__(128) sv_schedule_row_kernel(const __grid_constant__ ScheduleArgs a) {
   pdl_wait();
   pdl_trigger();
+  SV_TRACE_START(1);
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= a.B) return;
-  schedule_one(a, b);
+  if (b < a.B) schedule_one(a, b);
+  SV_TRACE_END(1);
 }
 
 }  // namespace
@@ -39,3 +42,5 @@ cudaError_t launch_schedule(const ScheduleArgs &a, cudaStream_t st) {
 }
 
 }  // namespace sv
+
+SV_TRACE_READER(sched)

@@ -23,6 +23,8 @@
 
 namespace sv {
 
+SV_TRACE_DECL
+
 namespace {
 
 // K1: one CTA per chunk task, tasks taken from an atomic TICKET (not blockIdx): every task a P2
@@ -44,6 +46,7 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constan
   __shared__ uint32_t s_tk;
   pdl_wait();
   pdl_trigger();
+  SV_TRACE_START(0);
   if (threadIdx.x == 0) {
 #if SV_K1_TICKET
     const uint32_t t = atomicAdd(a.ticket, 1u);
@@ -85,6 +88,7 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constan
   if (!c.k.p2) {
     const P1Out o = pass1_thread<T, NT, G>(c.src, c.ch, cd, cc);
     p1_publish<NW>(a, c.k, o, sm);
+    SV_TRACE_END(0);
     return;
   }
   Pre<G> pre;
@@ -95,6 +99,7 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constan
   if (lamd == lamd && lamc == lamc) s_loc = pass2_thread<T, NT, G, kScorePoly>(c.src, c.ch, cd, cc, lamd, lamc, &pre);
   p2_finish_head<NW>(s_loc, sm);
   p2_finish_tail<T, NW>(a, c.k, sm);
+  SV_TRACE_END(0);
 }
 
 // K1c: one cluster of cs CTAs per row (CTA rank r = chunk r), both passes in one CTA: pass 1
@@ -112,7 +117,10 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_cluster_kernel(const __grid
   __shared__ uint64_t s_bar;
   extern __shared__ __align__(128) uint8_t s_chunk[];  // kRes: the chunk pair (D at 0, C at chunk bytes)
   pdl_wait();
-  pdl_trigger();
+  // No griddepcontrol.launch_dependents here: a PDL dependant launched early next to this
+  // cluster grid ran ~5.5 us slower after its wait (traced: K3 1.8 -> 7.6 us at config 1); the
+  // implicit trigger at grid completion costs ~0.7 us of launch latency instead.
+  SV_TRACE_START(6);
   cg::cluster_group cl = cg::this_cluster();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const float cd = a.cd, cc = a.cc;
@@ -170,6 +178,7 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_cluster_kernel(const __grid
   }
   cl.sync();  // S partials written (and no CTA leaves while a peer may still read its glob)
   if (k.rank == 0 && wid == NW - 1) epilogue<T>(a, k.bb, k.ii, sm.wglob[NW - 1], srow, a.cs, 1, 0, nullptr, 0);
+  SV_TRACE_END(6);
 }
 
 template <typename T, bool kRes>
@@ -355,3 +364,5 @@ cudaError_t launch_shard_score(const ShardScoreArgs &h, const ScoreArgs &a, cuda
 }
 
 }  // namespace sv
+
+SV_TRACE_READER(score)
