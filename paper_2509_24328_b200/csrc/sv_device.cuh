@@ -272,6 +272,14 @@ __device__ __forceinline__ unsigned long long sv_gtimer() {
   do {                  \
     if ((threadIdx.x & 31) == 0) atomicMax(&g_sv_trace[2 * (k) + 1], sv_gtimer()); \
   } while (0)
+#define SV_TRACE_POINT(k) \
+  do {                    \
+    if (threadIdx.x == 0 && blockIdx.x == 0) g_sv_trace[2 * (k)] = g_sv_trace[2 * (k) + 1] = sv_gtimer(); \
+  } while (0)
+#define SV_TRACE_POINT_ANY(k) \
+  do {                        \
+    g_sv_trace[2 * (k)] = g_sv_trace[2 * (k) + 1] = sv_gtimer(); \
+  } while (0)
 #define SV_TRACE_READER(name)                                                              \
   extern "C" __attribute__((visibility("default"))) int sv_debug_trace_##name(unsigned long long *out) { \
     unsigned long long init[32];                                                           \
@@ -286,6 +294,12 @@ __device__ __forceinline__ unsigned long long sv_gtimer() {
   } while (0)
 #define SV_TRACE_END(k) \
   do {                  \
+  } while (0)
+#define SV_TRACE_POINT(k) \
+  do {                    \
+  } while (0)
+#define SV_TRACE_POINT_ANY(k) \
+  do {                        \
   } while (0)
 #define SV_TRACE_READER(name)
 #endif

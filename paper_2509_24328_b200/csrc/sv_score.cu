@@ -131,6 +131,9 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_cluster_kernel(const __grid
   k.bb = k.row / (uint32_t)a.k;
   k.ii = k.row - k.bb * a.k;
   k.p2 = false;
+  __shared__ EpiPre s_epi;
+  // the epilogue's inputs (token, its logits, profile edges) now, off the row's critical path
+  if (k.rank == 0 && wid == NW - 1) epilogue_prefetch<T>(a, k.bb, k.ii, s_epi);
   const Chunk<T> ch = chunk_of<T>(a, k.bb, k.ii, k.rank);
   float s_loc = 0.f;
   auto both_passes = [&](const auto &src1, const auto &src2, auto *pre) {
@@ -141,7 +144,9 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_cluster_kernel(const __grid
       merge_partials_to<decltype(warp_part), false>(a, NW, warp_part, sm.glob, sm.lam);
     }
     if (pre) prefetch_first<T, NT, G>(src2, ch, *pre);
+    SV_TRACE_POINT(8);
     cl.sync();  // every CTA's chunk partial is in its shared memory
+    SV_TRACE_POINT(9);
     auto peer_part = [&](int j) { return (const double *)cl.map_shared_rank(&sm.glob[0], (unsigned)j); };
     merge_partials_to<decltype(peer_part), false>(a, a.cs, peer_part, sm.wglob[wid], sm.wlam[wid]);
     __syncwarp();
@@ -162,6 +167,7 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_cluster_kernel(const __grid
     }
     __syncthreads();
     if (nb) mbar_wait_bounded(&s_bar, 0);
+    SV_TRACE_POINT(7);
     const SSrc src{reinterpret_cast<const uint4 *>(s_chunk),
                    reinterpret_cast<const uint4 *>(s_chunk + a.chunk * sizeof(T))};
     both_passes(src, src, (Pre<G> *)nullptr);
@@ -169,6 +175,7 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_cluster_kernel(const __grid
     Pre<G> pre;
     both_passes(GSrc<T>{ch.d, ch.c, l2_policy_evict_last()}, GSrc<T>{ch.d, ch.c, l2_policy_evict_first()}, &pre);
   }
+  SV_TRACE_POINT(10);
   p2_finish_head<NW>(s_loc, sm);  // warp sums, block barrier
   float *srow = a.spart + (size_t)k.row * a.cs;
   if (wid == NW - 1 && lane == 0) {
@@ -177,7 +184,12 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_cluster_kernel(const __grid
     srow[k.rank] = r;
   }
   cl.sync();  // S partials written (and no CTA leaves while a peer may still read its glob)
-  if (k.rank == 0 && wid == NW - 1) epilogue<T>(a, k.bb, k.ii, sm.wglob[NW - 1], srow, a.cs, 1, 0, nullptr, 0);
+  SV_TRACE_POINT(11);
+  if (k.rank == 0 && wid == NW - 1) {
+    __syncwarp();
+    epilogue<T>(a, k.bb, k.ii, sm.wglob[NW - 1], srow, a.cs, 1, 0, nullptr, 0, &s_epi);
+    if ((threadIdx.x & 31) == 0 && blockIdx.x == 0) SV_TRACE_POINT_ANY(12);
+  }
   SV_TRACE_END(6);
 }
 

@@ -360,10 +360,38 @@ __device__ __forceinline__ float pass2_thread(const Src &src, const Chunk<T> &ch
 // S partials: entry j < G cs of this row is sarr[(j / cs) gstride + j % cs] (vocabulary order);
 // xtok: NULL = load the token logits from the rows, else the owner's of xtok[g gstride2 + 0/1]
 // over g (NaN = not owned; vocab-sharded staging).
+// Inputs of a row's epilogue that do not depend on the passes (token, its logits, profile edges),
+// loaded ahead by K1c's epilogue warp into shared memory (lane l's edges at [l]).
+struct EpiPre {
+  int32_t t;
+  float x[2];
+  float se[2][32], ae[2][32];
+};
+template <typename T>
+__device__ __forceinline__ void epilogue_prefetch(const ScoreArgs &a, int64_t b, int64_t i, EpiPre &p) {
+  const int lane = threadIdx.x & 31;
+  const int32_t t = a.tok[b * a.k + i];
+  const float inf = __int_as_float(0x7f800000);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int j = lane + 1 + 32 * h;
+    p.se[h][lane] = (a.p_hat && j < a.n_s) ? a.s_edges[j] : inf;
+    p.ae[h][lane] = (a.p_hat && j < a.n_a) ? a.a_edges[j] : inf;
+  }
+  if (lane < 2) {
+    float x = 0.f;
+    if (t >= 0 && t < a.V)
+      x = lane == 0 ? Elem<T>::load(reinterpret_cast<const T *>(a.d) + b * a.d_sb + i * a.d_si + t)
+                    : Elem<T>::load(reinterpret_cast<const T *>(a.c) + b * a.c_sb + i * a.c_si + t);
+    p.x[lane] = x;
+  }
+  if (lane == 0) p.t = t;
+}
+
 template <typename T>
 __device__ __forceinline__ void epilogue(const ScoreArgs &a, int64_t b, int64_t i, const double *glob,
                                       const float *sarr, int cs, int G, int64_t gstride, const float *xtok,
-                                      int64_t gstride2) {
+                                      int64_t gstride2, const EpiPre *pre = nullptr) {
   const int64_t row = b * a.k + i;
   const int lane = threadIdx.x & 31;
   const float cd = a.cd, cc = a.cc;
@@ -374,7 +402,7 @@ __device__ __forceinline__ void epilogue(const ScoreArgs &a, int64_t b, int64_t 
     return (L > 0.0) ? 0 : 2;                                  /*SV_ROW_ALL_NEG_INF*/
   };
   const int d_st = row_bits(L_d, GMd), c_st = row_bits(L_c, GMc);
-  const int32_t t = a.tok[row];
+  const int32_t t = pre ? pre->t : a.tok[row];
   const bool tok_ok = t >= 0 && t < a.V;
   int st = d_st | c_st | (tok_ok ? 0 : 4 /*SV_ROW_BAD_TOKEN*/);
   // profile edges j = lane + 1, lane + 33 (+inf past the end) -- loads issued early
@@ -383,12 +411,18 @@ __device__ __forceinline__ void epilogue(const ScoreArgs &a, int64_t b, int64_t 
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int j = lane + 1 + 32 * h;
-    se[h] = (a.p_hat && j < a.n_s) ? a.s_edges[j] : inf;
-    ae[h] = (a.p_hat && j < a.n_a) ? a.a_edges[j] : inf;
+    if (pre) {
+      se[h] = pre->se[h][lane];
+      ae[h] = pre->ae[h][lane];
+    } else {
+      se[h] = (a.p_hat && j < a.n_s) ? a.s_edges[j] : inf;
+      ae[h] = (a.p_hat && j < a.n_a) ? a.a_edges[j] : inf;
+    }
   }
   // lane 0: log2 p_d(t); lane 1: log2 p_c(t); lane 2: log2 L_d - log2 L_c; lane 3: S (rank order)
   double piece = 0.0;
   auto tok_logit = [&](int which) {  // 0 = draft, 1 = companion
+    if (pre) return pre->x[which];
     if (!xtok) {
       return which == 0 ? Elem<T>::load(reinterpret_cast<const T *>(a.d) + b * a.d_sb + i * a.d_si + t)
                         : Elem<T>::load(reinterpret_cast<const T *>(a.c) + b * a.c_sb + i * a.c_si + t);

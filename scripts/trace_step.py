@@ -20,7 +20,8 @@ _lib._lib = None
 lib = _lib.load(path)
 raw = ctypes.CDLL(path)
 readers = [getattr(raw, f"sv_debug_trace_{n}") for n in ("score", "sched", "verify") if hasattr(raw, f"sv_debug_trace_{n}")]
-names = {0: "K1 ticket", 6: "K1c", 1: "K3", 2: "K4", 3: "K4b", 4: "K5", 5: "K5b"}
+names = {0: "K1 ticket", 6: "K1c", 1: "K3", 2: "K4", 3: "K4b", 4: "K5", 5: "K5b", 7: " c0 bulk in", 8: " c0 pass 1",
+         9: " c0 sync 1", 10: " c0 pass 2", 11: " c0 sync 2", 12: " c0 epilogue"}
 dev = torch.device("cuda")
 x = synth.make_inputs(B, k, V, dt, seed=0x5EED)
 tdt = torch.bfloat16 if dt == "bf16" else torch.float32
