@@ -177,17 +177,17 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_cluster_kernel(const __grid
   }
   SV_TRACE_POINT(10);
   p2_finish_head<NW>(s_loc, sm);  // warp sums, block barrier
-  float *srow = a.spart + (size_t)k.row * a.cs;
+  __shared__ float s_spart[8];    // rank 0: the row's S partials in chunk order (pushed over DSMEM)
   if (wid == NW - 1 && lane == 0) {
     float r = sm.fscr[0];
     for (int w = 1; w < NW; ++w) r += sm.fscr[w];
-    srow[k.rank] = r;
+    *cl.map_shared_rank(&s_spart[k.rank], 0u) = r;
   }
-  cl.sync();  // S partials written (and no CTA leaves while a peer may still read its glob)
+  cl.sync();  // S partials in rank 0 (and no CTA leaves while a peer may still read its glob)
   SV_TRACE_POINT(11);
   if (k.rank == 0 && wid == NW - 1) {
     __syncwarp();
-    epilogue<T>(a, k.bb, k.ii, sm.wglob[NW - 1], srow, a.cs, 1, 0, nullptr, 0, &s_epi);
+    epilogue<T>(a, k.bb, k.ii, sm.wglob[NW - 1], s_spart, a.cs, 1, 0, nullptr, 0, &s_epi, true);
     if ((threadIdx.x & 31) == 0 && blockIdx.x == 0) SV_TRACE_POINT_ANY(12);
   }
   SV_TRACE_END(6);

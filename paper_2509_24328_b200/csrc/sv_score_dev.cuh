@@ -391,7 +391,7 @@ __device__ __forceinline__ void epilogue_prefetch(const ScoreArgs &a, int64_t b,
 template <typename T>
 __device__ __forceinline__ void epilogue(const ScoreArgs &a, int64_t b, int64_t i, const double *glob,
                                       const float *sarr, int cs, int G, int64_t gstride, const float *xtok,
-                                      int64_t gstride2, const EpiPre *pre = nullptr) {
+                                      int64_t gstride2, const EpiPre *pre = nullptr, bool sarr_local = false) {
   const int64_t row = b * a.k + i;
   const int lane = threadIdx.x & 31;
   const float cd = a.cd, cc = a.cc;
@@ -447,7 +447,8 @@ __device__ __forceinline__ void epilogue(const ScoreArgs &a, int64_t b, int64_t 
     const int ns = G * cs;
     for (int j0 = 0; j0 < ns; j0 += 32) {
       const int j = j0 + lane;
-      const float v = j < ns ? __ldcg(sarr + (j / cs) * gstride + j % cs) : 0.f;
+      const float *sp = sarr + (j / cs) * gstride + j % cs;
+      const float v = j < ns ? (sarr_local ? *sp : __ldcg(sp)) : 0.f;  // local: shared memory (K1c)
       const int nr = min(32, ns - j0);
       for (int r = 0; r < nr; ++r) {
         const float x = __shfl_sync(0xffffffffu, v, r);
