@@ -43,7 +43,8 @@ template <> struct KeyOf<__nv_bfloat16> {
     const uint32_t b = *reinterpret_cast<const uint16_t *>(p + e);
     return (b & 0x8000u) ? (~b & 0xFFFFu) : (b | 0x8000u);
   }
-  __device__ static bool bad(K k) { return k >= 0xFF80u; }  // +inf or NaN (R18)
+  // +inf or NaN of either sign (R18): +inf / +NaN map to keys >= 0xFF80, -NaN to keys <= 0x007E
+  __device__ static bool bad(K k) { return k >= 0xFF80u || k < 0x007Fu; }
   __device__ static float value(K k) { return __uint_as_float(value_bits(k)); }
   __device__ static uint32_t value_bits(K k) {  // fp32 bits of the logit of key k
     const uint32_t b = (k & 0x8000u) ? (k & 0x7FFFu) : (~k & 0xFFFFu);
@@ -57,7 +58,7 @@ template <> struct KeyOf<float> {
     const uint32_t b = __float_as_uint(p[e]);
     return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
   }
-  __device__ static bool bad(K k) { return k >= 0xFF800000u; }
+  __device__ static bool bad(K k) { return k >= 0xFF800000u || k < 0x007FFFFFu; }  // (as above)
   __device__ static float value(K k) { return __uint_as_float(value_bits(k)); }
   __device__ static uint32_t value_bits(K k) { return (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k; }
 };
@@ -165,11 +166,33 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
         if (u0 + q * NT >= units) continue;
         const T *e = reinterpret_cast<const T *>(&w[q]);
         K um = 0;
+        auto keys_max = [&]() {
 #pragma unroll
-        for (int j = 0; j < EPU; ++j) {
-          const K kk = KO::key(e, j);
-          um = kk > um ? kk : um;
-          bad |= KO::bad(kk);
+          for (int j = 0; j < EPU; ++j) {
+            const K kk = KO::key(e, j);
+            um = kk > um ? kk : um;
+            bad |= KO::bad(kk);
+          }
+        };
+        if constexpr (sizeof(T) == 2) {
+          if (!nucleus) {
+            // bf16: NaN-propagating packed maxima of the 8 values, then the keys of the 2
+            // survivors (for non-NaN values the float order is the key order except +-0, whose
+            // keys differ by one: either survivor is an element of the unit, so the group bound
+            // stays valid; a NaN of either sign or +inf survives and flags the row)
+            const __nv_bfloat162 *h2 = reinterpret_cast<const __nv_bfloat162 *>(&w[q]);
+            const __nv_bfloat162 m2 = __hmax2_nan(__hmax2_nan(h2[0], h2[1]), __hmax2_nan(h2[2], h2[3]));
+            const uint32_t mb = *reinterpret_cast<const uint32_t *>(&m2);
+            const __nv_bfloat16 lo = __ushort_as_bfloat16((unsigned short)(mb & 0xFFFFu));
+            const __nv_bfloat16 hi = __ushort_as_bfloat16((unsigned short)(mb >> 16));
+            const K k0 = KO::key(&lo, 0), k1 = KO::key(&hi, 0);
+            um = k0 > k1 ? k0 : k1;
+            bad |= KO::bad(k0) | KO::bad(k1);
+          } else {
+            keys_max();
+          }
+        } else {
+          keys_max();
         }
         tmax = um > tmax ? um : tmax;
         if (nucleus) {

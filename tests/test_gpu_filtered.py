@@ -72,6 +72,33 @@ def test_filtered_parity(sv, B, k, V, dtype, top_k, top_p, tau):
     print("ties:", int(tie.sum()))
 
 
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_filtered_nan_rows(sv, dtype):
+    """R18 in the filtered path: a NaN of either sign or +inf in a draft or companion row flags
+    SV_ROW_NAN (1) for that position; -inf is a legal mask; clean rows stay clean."""
+    V = 1000
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((1, 4, V)).astype(np.float32)
+    c = x + 0.1 * rng.standard_normal((1, 4, V)).astype(np.float32)
+    bits = x.view(np.uint32)
+    bits[0, 0, 17] = 0xFFC00000  # -NaN in draft row 0
+    cb = c.view(np.uint32)
+    cb[0, 1, 400] = 0x7F800000   # +inf in companion row 1
+    bits[0, 2, 999] = 0x7FC00000  # +NaN in draft row 2
+    x[0, 3, 5] = -np.inf          # a masked logit in row 3 (legal)
+    tok = np.argmax(np.where(np.isfinite(x), x, -np.inf), axis=-1).astype(np.int32)
+    if dtype == "bf16":
+        D = torch.from_numpy(synth.f32_to_bf16_bits(x).astype(np.int16)).view(torch.bfloat16).cuda()
+        C = torch.from_numpy(synth.f32_to_bf16_bits(c).astype(np.int16)).view(torch.bfloat16).cuda()
+    else:
+        D, C = torch.from_numpy(x).cuda(), torch.from_numpy(c).cuda()
+    g = sv.sv_score_filtered(D, C, torch.from_numpy(tok).cuda(), 20, 0.8, 0.7, 0.7,
+                             sv.Profile.from_dict(synth.load_profile()))
+    st = g["status"].cpu().numpy()[0]
+    assert (st[0] & 1) and (st[1] & 1) and (st[2] & 1), st
+    assert st[3] == 0, st
+
+
 def test_filtered_bad_configs(sv):
     B, k, V = 2, 2, 64
     x = synth.make_inputs(B, k, V, "f32", seed=1)
