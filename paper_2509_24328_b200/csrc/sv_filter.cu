@@ -251,6 +251,15 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
         const int u = u0 + q * NT;
         if (u >= units) continue;
         const T *e = reinterpret_cast<const T *>(&w[q]);
+        if constexpr (sizeof(T) == 2) {  // skip units whose packed maximum is below the bound
+          const __nv_bfloat162 *h2 = reinterpret_cast<const __nv_bfloat162 *>(&w[q]);
+          const __nv_bfloat162 m2 = __hmax2_nan(__hmax2_nan(h2[0], h2[1]), __hmax2_nan(h2[2], h2[3]));
+          const uint32_t mb = *reinterpret_cast<const uint32_t *>(&m2);
+          const __nv_bfloat16 lo = __ushort_as_bfloat16((unsigned short)(mb & 0xFFFFu));
+          const __nv_bfloat16 hi = __ushort_as_bfloat16((unsigned short)(mb >> 16));
+          const K k0 = KO::key(&lo, 0), k1 = KO::key(&hi, 0);
+          if ((k0 > k1 ? k0 : k1) + 1u < lb) continue;  // (+1: -0 and +0 are one key apart)
+        }
 #pragma unroll
         for (int j = 0; j < EPU; ++j) {
           const K kk = KO::key(e, j);
