@@ -101,7 +101,9 @@ __device__ __forceinline__ bool row_of(const FilterArgs &a, int64_t r, int which
   return true;
 }
 
-template <typename T>
+// kNuc: nucleus-only (top_k = 0) -- a separate instantiation so the top-k path's registers and
+// schedule do not carry the normaliser's code
+template <typename T, bool kNuc>
 __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_constant__ FilterArgs a, int which0) {
   const int which = which0 + (int)blockIdx.y;  // score: y = 0 draft rows, y = 1 companion rows
   using KO = KeyOf<T>;
@@ -127,7 +129,7 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   // top_k = 0: nucleus-only (top_p over the FULL distribution), supported when the nucleus has
   // at most 32 tokens -- the 32 largest are selected and the full-row normaliser is added below
-  const bool nucleus = a.top_k == 0;
+  constexpr bool nucleus = kNuc;  // the launch picks kNuc = (a.top_k == 0)
   const int V = a.V, KK = min(nucleus ? 32 : a.top_k, V);
   if (tid == 0) {
     s_prefix = 0;
@@ -175,22 +177,18 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
           }
         };
         if constexpr (sizeof(T) == 2) {
-          if (!nucleus) {
-            // bf16: NaN-propagating packed maxima of the 8 values, then the keys of the 2
-            // survivors (for non-NaN values the float order is the key order except +-0, whose
-            // keys differ by one: either survivor is an element of the unit, so the group bound
-            // stays valid; a NaN of either sign or +inf survives and flags the row)
-            const __nv_bfloat162 *h2 = reinterpret_cast<const __nv_bfloat162 *>(&w[q]);
-            const __nv_bfloat162 m2 = __hmax2_nan(__hmax2_nan(h2[0], h2[1]), __hmax2_nan(h2[2], h2[3]));
-            const uint32_t mb = *reinterpret_cast<const uint32_t *>(&m2);
-            const __nv_bfloat16 lo = __ushort_as_bfloat16((unsigned short)(mb & 0xFFFFu));
-            const __nv_bfloat16 hi = __ushort_as_bfloat16((unsigned short)(mb >> 16));
-            const K k0 = KO::key(&lo, 0), k1 = KO::key(&hi, 0);
-            um = k0 > k1 ? k0 : k1;
-            bad |= KO::bad(k0) | KO::bad(k1);
-          } else {
-            keys_max();
-          }
+          // bf16: NaN-propagating packed maxima of the 8 values, then the keys of the 2 survivors
+          // (for non-NaN values the float order is the key order except +-0, whose keys differ
+          // by one: either survivor is an element of the unit, so the group bound stays valid; a
+          // NaN of either sign or +inf survives and flags the row)
+          const __nv_bfloat162 *h2 = reinterpret_cast<const __nv_bfloat162 *>(&w[q]);
+          const __nv_bfloat162 m2 = __hmax2_nan(__hmax2_nan(h2[0], h2[1]), __hmax2_nan(h2[2], h2[3]));
+          const uint32_t mb = *reinterpret_cast<const uint32_t *>(&m2);
+          const __nv_bfloat16 lo = __ushort_as_bfloat16((unsigned short)(mb & 0xFFFFu));
+          const __nv_bfloat16 hi = __ushort_as_bfloat16((unsigned short)(mb >> 16));
+          const K k0 = KO::key(&lo, 0), k1 = KO::key(&hi, 0);
+          um = k0 > k1 ? k0 : k1;
+          bad |= KO::bad(k0) | KO::bad(k1);
         } else {
           keys_max();
         }
@@ -202,8 +200,19 @@ __global__ void __launch_bounds__(kTopKThreads) sv_topk_kernel(const __grid_cons
             om = umv;
           }
           const float nm = -om * c2n;
+          if constexpr (sizeof(T) == 2) {  // packed FFMA2 arguments, fixed FADD2 tree per unit
+            f2 xv[EPU / 2];
+            unit_pairs<T>(w[q], xv);
+            const f2 cc{c2n, c2n}, nm2{nm, nm};
+            f2 ev[EPU / 2];
 #pragma unroll
-          for (int j = 0; j < EPU; ++j) ol += ex2(fmaf(KO::value(KO::key(e, j)), c2n, nm));
+            for (int p2 = 0; p2 < EPU / 2; ++p2) ev[p2] = ex2x2(fma2(xv[p2], cc, nm2));
+            const f2 t = add2(add2(ev[0], ev[1]), add2(ev[2], ev[3]));
+            ol += t.x + t.y;
+          } else {
+#pragma unroll
+            for (int j = 0; j < EPU; ++j) ol += ex2(fmaf(KO::value(KO::key(e, j)), c2n, nm));
+          }
         }
       }
     }
@@ -1197,12 +1206,20 @@ pass_again:  // R10: when the residual mass is 0 (rounding only), the pass is re
   if (a.resid) a.resid[b] = (float)s_Z;
 }
 
+cudaError_t launch_topk(const FilterArgs &a, dim3 grid, int which0, cudaStream_t st) {
+  const dim3 blk(kTopKThreads);
+  if (a.top_k == 0)
+    return a.bf16 ? launch_k(sv_topk_kernel<__nv_bfloat16, true>, grid, blk, 0, st, a, which0)
+                  : launch_k(sv_topk_kernel<float, true>, grid, blk, 0, st, a, which0);
+  return a.bf16 ? launch_k(sv_topk_kernel<__nv_bfloat16, false>, grid, blk, 0, st, a, which0)
+                : launch_k(sv_topk_kernel<float, false>, grid, blk, 0, st, a, which0);
+}
+
 }  // namespace
 
 cudaError_t launch_filter_score(const FilterArgs &a, cudaStream_t st) {
   const unsigned rows = (unsigned)((int64_t)a.B * a.k);
-  cudaError_t e = a.bf16 ? launch_k(sv_topk_kernel<__nv_bfloat16>, dim3(rows, 2), dim3(kTopKThreads), 0, st, a, 0)
-                         : launch_k(sv_topk_kernel<float>, dim3(rows, 2), dim3(kTopKThreads), 0, st, a, 0);
+  cudaError_t e = launch_topk(a, dim3(rows, 2), 0, st);
   if (e != cudaSuccess) return e;
   e = launch_k(sv_fscore_kernel, dim3((rows + 7) / 8), dim3(256), 0, st, a);
   if (e != cudaSuccess || a.top_k != 0) return e;  // wide rows exist only without top_k
@@ -1212,8 +1229,7 @@ cudaError_t launch_filter_score(const FilterArgs &a, cudaStream_t st) {
 
 cudaError_t launch_filter_verify(const FilterArgs &a, cudaStream_t st) {
   const unsigned rows = (unsigned)((int64_t)a.B * (a.k + 1));
-  cudaError_t e = a.bf16 ? launch_k(sv_topk_kernel<__nv_bfloat16>, dim3(rows), dim3(kTopKThreads), 0, st, a, 2)
-                         : launch_k(sv_topk_kernel<float>, dim3(rows), dim3(kTopKThreads), 0, st, a, 2);
+  cudaError_t e = launch_topk(a, dim3(rows), 2, st);
   if (e != cudaSuccess) return e;
   const dim3 gv((unsigned)((a.B + 7) / 8));
   e = a.bf16 ? launch_k(sv_fverify_kernel<__nv_bfloat16>, gv, dim3(256), 0, st, a)
