@@ -899,16 +899,21 @@ __global__ void __launch_bounds__(256) sv_fscore_kernel(const __grid_constant__ 
   if (lane == 0) write_fscore(a, r, st, S, A, KL, pdt);
 }
 
-// KF2w: rows where the draft or the companion nucleus exceeds 32 tokens -- one CTA per (b, i),
-// full-row pass over both rows in threshold form (S = sum min(p'_d, p'_c), KL over p'_d > 0)
+// KF2w: rows where the draft or the companion nucleus exceeds 32 tokens -- one cluster of
+// kWideSplit CTAs per (b, i), CTA y streams the vocabulary slice y of both rows in threshold form
+// (S = sum min(p'_d, p'_c), KL over p'_d > 0); the slices' sums meet in rank 0 over DSMEM and are
+// added in slice order.  (One CTA per row took ~67 us for the few wide rows of a launch.)
+constexpr int kWideSplit = 8;
 template <typename T>
-__global__ void __launch_bounds__(512) sv_fwide_score_kernel(const __grid_constant__ FilterArgs a) {
-  pdl_wait();
-  pdl_trigger();
+__global__ void __launch_bounds__(256) sv_fwide_score_kernel(const __grid_constant__ FilterArgs a) {
+  pdl_wait();  // (no early launch_dependents: a cluster grid, see K1c in sv_score.cu)
   __shared__ double red[16];
-  const int64_t r = blockIdx.x;
+  __shared__ double part[2];
+  cg::cluster_group cl = cg::this_cluster();
+  const int64_t r = blockIdx.x / kWideSplit;
+  const int y = (int)(blockIdx.x % kWideSplit);
   const FList *Ld = a.dl + r, *Lc = a.cl + r;
-  if (!Ld->wide && !Lc->wide) return;
+  if (!Ld->wide && !Lc->wide) return;  // the whole cluster (same row) leaves
   const int64_t b = r / a.k, i = r % a.k;
   const T *xd = reinterpret_cast<const T *>(a.d) + b * a.d_sb + i * a.d_si;
   const T *xc = reinterpret_cast<const T *>(a.c) + b * a.c_sb + i * a.c_si;
@@ -918,17 +923,20 @@ __global__ void __launch_bounds__(512) sv_fwide_score_kernel(const __grid_consta
   if (t < 0 || t >= a.V) st |= 4;
   double S = 0.0, KL = 0.0;
   const bool vec = ((reinterpret_cast<uintptr_t>(xd) | reinterpret_cast<uintptr_t>(xc)) & 15) == 0;
+  // slice y: [vb, ve), boundaries multiples of 8
+  const int vb = (int)(((int64_t)a.V * y / kWideSplit) & ~7ll);
+  const int ve = y + 1 == kWideSplit ? a.V : (int)(((int64_t)a.V * (y + 1) / kWideSplit) & ~7ll);
   // per kept draft entry: log p' in fp64 (x / tau - c), p' = 2^{log p' log2 e} on the fp32 MUFU
   // (relative error ~1e-6, inside the north_star tolerance), KL term p'_d (log p'_d - log p'_c)
   const ThrF fd = make_thrf(ld), fc = make_thrf(lc);
   if (!st)
-    for (int v0 = threadIdx.x * 8; v0 < a.V; v0 += blockDim.x * 8) {
+    for (int v0 = vb + threadIdx.x * 8; v0 < ve; v0 += blockDim.x * 8) {
       uint32_t kd[8], kc[8];
       load8(xd, v0, a.V, vec, kd);
       load8(xc, v0, a.V, vec, kc);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        if (v0 + j >= a.V || !thr_kept<T>(kd[j], v0 + j, fd)) continue;
+        if (v0 + j >= ve || !thr_kept<T>(kd[j], v0 + j, fd)) continue;
         const double lpd = thr_logp<T>(kd[j], fd);
         const double pd = (double)ex2((float)(lpd * 1.4426950408889634));
         if (pd > 0.0) {
@@ -944,11 +952,44 @@ __global__ void __launch_bounds__(512) sv_fwide_score_kernel(const __grid_consta
     }
   S = block_sum_d(S, red);
   KL = block_sum_d(KL, red);
-  if (threadIdx.x != 0) return;
+  if (threadIdx.x == 0) {
+    part[0] = S;
+    part[1] = KL;
+  }
+  cl.sync();  // every slice's sums are in its shared memory
+  if (y == 0 && threadIdx.x == 0) {
+    S = 0.0;
+    KL = 0.0;
+    for (int q = 0; q < kWideSplit; ++q) {  // slice order
+      const double *pq = cl.map_shared_rank(part, (unsigned)q);
+      S += pq[0];
+      KL += pq[1];
+    }
+  }
+  cl.sync();  // (no CTA leaves while rank 0 reads its shared memory)
+  if (y != 0 || threadIdx.x != 0) return;
   const double pdt = (st & 4) ? 0.0 : thr_p(xd, t, ld), pct = (st & 4) ? 0.0 : thr_p(xc, t, lc);
   if (!st && pdt == 0.0) st |= 8;
   const double A = st ? 0.0 : fmin(1.0, pct / pdt);
   write_fscore(a, r, st, S, A, KL, pdt);
+}
+
+template <typename T>
+cudaError_t launch_fwide_score(const FilterArgs &a, unsigned rows, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(rows * kWideSplit);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = kWideSplit;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, sv_fwide_score_kernel<T>, a);
 }
 
 constexpr int kPendingWide = -2;  // out_tok marker: the residual / bonus sample needs a full-row pass
@@ -1223,8 +1264,7 @@ cudaError_t launch_filter_score(const FilterArgs &a, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   e = launch_k(sv_fscore_kernel, dim3((rows + 7) / 8), dim3(256), 0, st, a);
   if (e != cudaSuccess || a.top_k != 0) return e;  // wide rows exist only without top_k
-  return a.bf16 ? launch_k(sv_fwide_score_kernel<__nv_bfloat16>, dim3(rows), dim3(512), 0, st, a)
-                : launch_k(sv_fwide_score_kernel<float>, dim3(rows), dim3(512), 0, st, a);
+  return a.bf16 ? launch_fwide_score<__nv_bfloat16>(a, rows, st) : launch_fwide_score<float>(a, rows, st);
 }
 
 cudaError_t launch_filter_verify(const FilterArgs &a, cudaStream_t st) {
