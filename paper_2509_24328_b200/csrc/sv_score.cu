@@ -89,8 +89,10 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constan
     const P1Out o = pass1_thread<T, NT, G>(c.src, c.ch, cd, cc);
     p1_publish<NW>(a, c.k, o, sm);
     SV_TRACE_END(0);
+    SV_TRACE_END(13);  // P1 tasks: last exit
     return;
   }
+  SV_TRACE_START(14);  // P2 tasks: first start
   Pre<G> pre;
   prefetch_first<T, NT, G>(c.src, c.ch, pre);
   const float2 lam = p2_merge_warp<NW>(a, c.k, sm);

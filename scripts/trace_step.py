@@ -21,7 +21,8 @@ lib = _lib.load(path)
 raw = ctypes.CDLL(path)
 readers = [getattr(raw, f"sv_debug_trace_{n}") for n in ("score", "sched", "verify") if hasattr(raw, f"sv_debug_trace_{n}")]
 names = {0: "K1 ticket", 6: "K1c", 1: "K3", 2: "K4", 3: "K4b", 4: "K5", 5: "K5b", 7: " c0 bulk in", 8: " c0 pass 1",
-         9: " c0 sync 1", 10: " c0 pass 2", 11: " c0 sync 2", 12: " c0 epilogue"}
+         9: " c0 sync 1", 10: " c0 pass 2", 11: " c0 sync 2", 12: " c0 epilogue", 13: " K1 P1 tasks (end)",
+         14: " K1 P2 tasks (start)"}
 dev = torch.device("cuda")
 x = synth.make_inputs(B, k, V, dt, seed=0x5EED)
 tdt = torch.bfloat16 if dt == "bf16" else torch.float32
@@ -52,6 +53,10 @@ for it in range(R + 3):
             s0, s1 = buf[2 * slot], buf[2 * slot + 1]
             if s1 and s0 != 2 ** 64 - 1:
                 ev[slot] = (s0, s1)
+            elif s1:  # end-only marker
+                ev[slot] = (s1, s1)
+            elif s0 != 2 ** 64 - 1:  # start-only marker
+                ev[slot] = (s0, s0)
     t0 = min(v[0] for v in ev.values())
     if it >= 3:
         for slot, (a, b) in ev.items():
