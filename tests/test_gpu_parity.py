@@ -156,25 +156,30 @@ def test_determinism_and_batch_split(sv, prof_dict):
         assert np.array_equal(a[1][k_][4:], c[1][k_], equal_nan=True)
 
 
-def test_k1_variants_bit_identical(sv, prof_dict):
+@pytest.mark.parametrize("B,k,V,parts", [
+    (80, 8, 32000, ((0, 40), (40, 42), (77, 80))),
+    (8, 8, 300000, ((0, 1), (3, 6))),   # cs = 8: the widest K1c cluster (8 CTAs) vs the ticket kernel
+])
+def test_k1_variants_bit_identical(sv, prof_dict, B, k, V, parts):
     """sv_score picks its K1 kernel by launch shape: at V = 32000 bf16 the whole batch
     B = 80 (D + C 82 MB) runs the ticket kernel, B = 40 (41 MB, more than one wave) K1c with
-    cluster-exchanged partials, B = 2 K1c with shared-memory resident chunks.  All three share
-    the chunking and every reduction order, so the rows of a sub-batch must match the full batch
-    bit for bit (the batch-sharded multi-GPU layout relies on it)."""
-    x = synth.make_inputs(80, 8, 32000, "bf16", seed=33)
+    cluster-exchanged partials, B = 2 K1c with shared-memory resident chunks; at V = 300000 (cs =
+    8 chunks per row) B = 8 runs the ticket kernel and its sub-batches K1c.  All share the chunking
+    and every reduction order, so the rows of a sub-batch must match the full batch bit for bit
+    (the batch-sharded multi-GPU layout relies on it)."""
+    x = synth.make_inputs(B, k, V, "bf16", seed=33)
     D, C, T, tok = H.to_torch(x)
     prof = sv.Profile.from_dict(prof_dict)
     keys = ("S", "A", "KL", "p_hat", "draft_m", "draft_l", "draft_ptok", "status")
     full = H.gpu_np(sv.sv_score(D, C, tok, 1.0, 1.0, prof))
-    for lo, hi in ((0, 40), (40, 42), (77, 80)):
+    for lo, hi in parts:
         part = H.gpu_np(sv.sv_score(D[lo:hi].contiguous(), C[lo:hi].contiguous(), tok[lo:hi].contiguous(), 1.0, 1.0,
                                     prof))
         for k_ in keys:
             assert np.array_equal(full[k_][lo:hi], part[k_], equal_nan=True), (lo, hi, k_)
     # and the full batch against the oracle on sampled sequences
     rep = H.ParityReport()
-    idx = np.array([0, 39, 40, 79])
+    idx = np.array(sorted({0, B // 2 - 1, B // 2, B - 1}))
     Dd, Cd, _ = H.oracle_inputs({**x, "D": x["D"][idx], "C": x["C"][idx], "T": x["T"][idx]})
     rs = oracle.score(Dd, Cd, x["tok"][idx], 1.0, 1.0, prof_dict)
     H.compare_score({k_: full[k_][idx] for k_ in full}, rs, prof_dict, rep)
