@@ -995,20 +995,22 @@ cudaError_t launch_fwide_score(const FilterArgs &a, unsigned rows, cudaStream_t 
 constexpr int kPendingWide = -2;  // out_tok marker: the residual / bonus sample needs a full-row pass
 
 template <typename T>
-__global__ void __launch_bounds__(256) sv_fverify_kernel(const __grid_constant__ FilterArgs a) {
+__global__ void __launch_bounds__(32 * 16) sv_fverify_kernel(const __grid_constant__ FilterArgs a) {
   pdl_wait();
   pdl_trigger();
-  const int lane = threadIdx.x & 31, k = a.k;
-  const int64_t b = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (b >= a.B) return;
+  // one CTA of k warps per sequence: warp i evaluates draft position i's accept test (its list
+  // lookups are warp-cooperative), warp 0 then takes the first rejection / error in position order
+  // -- the same decisions as a sequential walk -- and draws the token
+  __shared__ double s_ratio[16];
+  __shared__ int s_rst[16], s_rej[16];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, k = a.k;
+  const int64_t b = blockIdx.x;
   const int g = a.gamma[b];
   int st = (g < 0 || g > k) ? 64 /*BAD_GAMMA*/ : 0;
   const int gg = st ? -1 : g;
   const uint64_t off = a.offset;
-  // accept tests: one draft position per iteration (all lanes), ratios kept in lane i
-  double ratio_mine = 0.0;
-  int N = st ? 0 : gg;
-  for (int i = 0; i < gg; ++i) {
+  if (wid < gg) {
+    const int i = wid;
     const int64_t rd = b * k + i, rt = b * (k + 1) + i;
     const FList *Ldr = a.dl + rd, *Ltr = a.tl + rt;
     const int t = a.tok[rd];
@@ -1023,14 +1025,26 @@ __global__ void __launch_bounds__(256) sv_fverify_kernel(const __grid_constant__
                       : list_p(Ltr, Ltr->n, t);
     }
     if (!rst && pdt == 0.0) rst |= 8;
-    if (rst) {
-      st |= rst;
+    const double ratio = rst ? 0.0 : ptt / pdt;
+    const uint4 w = sv_philox(a.seed, off, a.seq_base + b, i);
+    if (lane == 0) {
+      s_rst[i] = rst;
+      s_ratio[i] = ratio;
+      s_rej[i] = !rst && !(u24(w.x) < ratio);
+    }
+  }
+  __syncthreads();
+  if (wid != 0) return;
+  // the walk in position order: an error stops it (its bits), else the first rejection sets N
+  double ratio_mine = 0.0;
+  int N = st ? 0 : gg;
+  for (int i = 0; i < gg; ++i) {
+    if (s_rst[i]) {
+      st |= s_rst[i];
       break;
     }
-    const double ratio = ptt / pdt;
-    if (lane == i) ratio_mine = ratio;
-    const uint4 w = sv_philox(a.seed, off, a.seq_base + b, i);
-    if (!(u24(w.x) < ratio)) {
+    if (lane == i) ratio_mine = s_ratio[i];
+    if (s_rej[i]) {
       N = i;
       break;
     }
@@ -1074,7 +1088,7 @@ __global__ void __launch_bounds__(256) sv_fverify_kernel(const __grid_constant__
   for (int l = 0; l < nt; ++l) rank += __shfl_sync(0xffffffffu, vi, l) < vi;
   __shared__ double s_r[8][32], s_pt[8][32];
   __shared__ int s_v[8][32];
-  const int w8 = threadIdx.x >> 5;
+  const int w8 = 0;  // warp 0 of the sequence's CTA
   if (lane < nt) {
     s_r[w8][rank] = r;
     s_pt[w8][rank] = Lt->p[lane];
@@ -1272,8 +1286,9 @@ cudaError_t launch_filter_verify(const FilterArgs &a, cudaStream_t st) {
   cudaError_t e = launch_topk(a, dim3(rows), 2, st);
   if (e != cudaSuccess) return e;
   const dim3 gv((unsigned)((a.B + 7) / 8));
-  e = a.bf16 ? launch_k(sv_fverify_kernel<__nv_bfloat16>, gv, dim3(256), 0, st, a)
-             : launch_k(sv_fverify_kernel<float>, gv, dim3(256), 0, st, a);
+  const dim3 gq((unsigned)a.B), bq(32 * (a.k > 0 ? a.k : 1));  // one CTA of k warps per sequence
+  e = a.bf16 ? launch_k(sv_fverify_kernel<__nv_bfloat16>, gq, bq, 0, st, a)
+             : launch_k(sv_fverify_kernel<float>, gq, bq, 0, st, a);
   if (e != cudaSuccess || a.top_k != 0) return e;
   return a.bf16 ? launch_k(sv_fwide_sample_kernel<__nv_bfloat16>, dim3((unsigned)a.B), dim3(512), 0, st, a)
                 : launch_k(sv_fwide_sample_kernel<float>, dim3((unsigned)a.B), dim3(512), 0, st, a);
