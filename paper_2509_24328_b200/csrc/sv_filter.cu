@@ -1142,7 +1142,7 @@ __global__ void __launch_bounds__(512) sv_fwide_sample_kernel(const __grid_const
   __shared__ double s_Z, s_th;
   const int64_t b = blockIdx.x;
   if (a.out_tok[b] != kPendingWide) return;
-  const int tid = threadIdx.x, k = a.k, V = a.V;
+  const int tid = threadIdx.x, lane = tid & 31, k = a.k, V = a.V;
   const int N = a.n_accept[b], g = a.gamma[b];
   const Thr lt = load_thr(a.tl + b * (k + 1) + N);
   const T *xt = reinterpret_cast<const T *>(a.t) + b * a.t_sb + (int64_t)N * a.t_si;
@@ -1198,24 +1198,38 @@ pass_again:  // R10: when the residual mass is 0 (rounding only), the pass is re
   s_sum[tid] = sum;
   s_last[tid] = lastp;
   __syncthreads();
-  if (tid == 0) {
-    double c = 0.0;
-    for (int j = 0; j < NT; ++j) {
-      s_pre[j] = c;
-      c += s_sum[j];
+  if (tid < 32) {  // warp 0: prefix over the chunks (lane l: chunks 16 l .. 16 l + 15 in order)
+    constexpr int PER = NT / 32;
+    double ls = 0.0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) ls += s_sum[lane * PER + j];
+    const double incl = warp_incl_scan_d(ls, lane);
+    double p = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) p = 0.0;
+    const double c = __shfl_sync(0xffffffffu, incl, 31);
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      s_pre[lane * PER + j] = p;
+      p += s_sum[lane * PER + j];
     }
-    s_retry = resid && !(c > 0.0);
     const double us = u24(sv_philox(a.seed, a.offset, a.seq_base + b, N).y);
     const double th = us * c;
-    int jc = -1;
-    for (int j = 0; j < NT; ++j)
-      if (s_sum[j] > 0.0 && s_pre[j] + s_sum[j] > th) {
-        jc = j;
+    int myj = -1;
+    for (int j = 0; j < PER; ++j) {
+      const int idx = lane * PER + j;
+      if (s_sum[idx] > 0.0 && s_pre[idx] + s_sum[idx] > th) {
+        myj = idx;
         break;
       }
-    s_j = jc;
-    s_Z = c;
-    s_th = th;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, myj >= 0);
+    const int jc = m ? __shfl_sync(0xffffffffu, myj, __ffs(m) - 1) : -1;
+    if (lane == 0) {
+      s_retry = resid && !(c > 0.0);
+      s_j = jc;
+      s_Z = c;
+      s_th = th;
+    }
   }
   __syncthreads();
   if (s_retry) {
@@ -1236,27 +1250,61 @@ pass_again:  // R10: when the residual mass is 0 (rounding only), the pass is re
     }
     return;
   }
-  if (tid != jc) return;
+  if (tid >= 32) return;
+  // warp 0 rescans chunk jc: lane l takes a contiguous sub-range (multiple of 8 elements), sums
+  // it sequentially in fp64; a fixed-order warp scan finds the crossing lane, which walks its
+  // sub-range from its prefix (R11); if rounding leaves no crossing, the last positive element
   const double th = s_th;
-  double cum = s_pre[jc];
-  int tok = s_last[jc];
+  const int c0 = min(V, jc * chunk), c1 = min(V, c0 + chunk);
+  const int per = ((((c1 - c0) + 31) / 32) + 7) & ~7;
+  const int l0 = min(c1, c0 + lane * per), l1 = min(c1, l0 + per);
+  double ls = 0.0;
+  int llast = -1;
   q = 0;
-  bool found = false;
-  for (int w0 = v0; w0 < v1 && !found; w0 += 8) {
+  for (int w0 = l0; w0 < l1; w0 += 8) {
     uint32_t kt[8], kd[8];
     load8(xt, w0, V, vec, kt);
     if (dwide) load8(xd, w0, V, vec, kd);
-    for (int j = 0; j < 8 && w0 + j < v1; ++j) {
+    for (int j = 0; j < 8 && w0 + j < l1; ++j) {
       const double r = rv(w0 + j, kt[j], dwide ? kd[j] : 0u);
-      if (!(r > 0.0)) continue;
-      cum += r;
-      if (cum > th) {
-        tok = w0 + j;
-        found = true;
-        break;
+      if (r > 0.0) {
+        ls += r;
+        llast = w0 + j;
       }
     }
   }
+  const double incl = warp_incl_scan_d(ls, lane);
+  double excl = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) excl = 0.0;
+  const double base = s_pre[jc];
+  const unsigned cross = __ballot_sync(0xffffffffu, ls > 0.0 && base + incl > th);
+  int tok = s_last[jc];
+  if (cross) {
+    const int lc = __ffs(cross) - 1;
+    if (lane == lc) {
+      double cum = base + excl;
+      bool found = false;
+      q = 0;
+      for (int w0 = l0; w0 < l1 && !found; w0 += 8) {
+        uint32_t kt[8], kd[8];
+        load8(xt, w0, V, vec, kt);
+        if (dwide) load8(xd, w0, V, vec, kd);
+        for (int j = 0; j < 8 && w0 + j < l1; ++j) {
+          const double r = rv(w0 + j, kt[j], dwide ? kd[j] : 0u);
+          if (!(r > 0.0)) continue;
+          cum += r;
+          if (cum > th) {
+            tok = w0 + j;
+            found = true;
+            break;
+          }
+        }
+      }
+      if (!found) tok = llast;
+    }
+    tok = __shfl_sync(0xffffffffu, tok, lc);
+  }
+  if (lane != 0) return;
   a.out_tok[b] = tok;
   if (a.resid) a.resid[b] = (float)s_Z;
 }
