@@ -26,12 +26,6 @@ namespace sv {
 #ifndef SV_K1_LAG
 #define SV_K1_LAG 128
 #endif
-#ifndef SV_K1_TICKET
-#define SV_K1_TICKET 1
-#endif
-#ifndef SV_K1_SAMECTA
-#define SV_K1_SAMECTA 0
-#endif
 #ifndef SV_K1_VARIANT
 #define SV_K1_VARIANT -1  // experiment: force a K1 variant (0 ticket, 1 K1c, 2 K1c resident); -1 = by shape
 #endif

@@ -48,42 +48,12 @@ __global__ void __launch_bounds__(NT, MINB) sv_score_kernel(const __grid_constan
   pdl_trigger();
   SV_TRACE_START(0);
   if (threadIdx.x == 0) {
-#if SV_K1_TICKET
     const uint32_t t = atomicAdd(a.ticket, 1u);
     if (t == gridDim.x - 1) *reinterpret_cast<volatile uint32_t *>(a.ticket) = 0u;  // the last claim
-#else
-    const uint32_t t = blockIdx.x;
-#endif
     s_tk = t;
   }
   __syncthreads();
   const float cd = a.cd, cc = a.cc;
-#if SV_K1_SAMECTA
-  {  // one task = one chunk, both passes: P1 -> publish -> (P2 loads issued) wait for the row's
-     // other chunks -> merge -> P2 from the L2 lines this SM just read
-    Task k;
-    const uint32_t cs = (uint32_t)a.cs;
-    k.q = s_tk;
-    k.row = k.q / cs;
-    k.rank = (int)(k.q - k.row * cs);
-    k.bb = k.row / (uint32_t)a.k;
-    k.ii = k.row - k.bb * a.k;
-    k.p2 = true;
-    const Chunk<T> ch = chunk_of<T>(a, k.bb, k.ii, k.rank);
-    const P1Out o = pass1_thread<T, NT, G>(GSrc<T>{ch.d, ch.c, l2_policy_evict_last()}, ch, cd, cc);
-    p1_publish<NW>(a, k, o, sm);
-    const GSrc<T> src{ch.d, ch.c, l2_policy_evict_first()};
-    Pre<G> pre;
-    prefetch_first<T, NT, G>(src, ch, pre);
-    const float2 lam = p2_merge_warp<NW>(a, k, sm);
-    const float lamd = lam.x, lamc = lam.y;
-    float s_loc = 0.f;
-    if (lamd == lamd && lamc == lamc) s_loc = pass2_thread<T, NT, G, kScorePoly>(src, ch, cd, cc, lamd, lamc, &pre);
-    p2_finish_head<NW>(s_loc, sm);
-    p2_finish_tail<T, NW>(a, k, sm);
-    return;
-  }
-#endif
   const TaskView<T> c = task_view<T>(a, s_tk);
   if (!c.k.p2) {
     const P1Out o = pass1_thread<T, NT, G>(c.src, c.ch, cd, cc);
@@ -248,7 +218,7 @@ cudaError_t launch_score_t(const ScoreArgs &a, cudaStream_t st) {
     case 1: return launch_score_cluster<T, false>(a, st);
     default: break;
   }
-  const int64_t tasks = (SV_K1_SAMECTA ? 1 : 2) * (int64_t)a.B * a.k * a.cs;
+  const int64_t tasks = 2 * (int64_t)a.B * a.k * a.cs;
   if (tasks == 0) return cudaSuccess;
   return launch_k(sv_score_kernel<T, kScoreThreads, kScoreMinBlocks>, dim3((unsigned)tasks), dim3(kScoreThreads), 0,
                   st, a);
